@@ -1,0 +1,182 @@
+"""fp64 CPU oracle for the Domain Transform Solver (arXiv 1805.04590).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  The product package ``paper_1805_04590_b200`` never imports it, and
+it shares no code with the CUDA path: the arithmetic lives in ``dts_oracle.c``
+(plain loops, double precision); this module only marshals numpy arrays.
+
+Functions (each cites the passage its C routine follows; see dts_oracle.c):
+  distances(guide, sigma_s, sigma_r)            O1  P:231-240 (Eqs. 8-9)
+  sigmas(sigma_s, N)                            O2  pass schedule (reading R5)
+  rf1d(x, A)                                    O3  recursive filter, causal + anticausal (R4)
+  dtf(X, dx, dy, sigma_s, N)                    O4  X then Y passes
+  support(dx, dy, sigma_s, mode)                O5  S = sum_j W_ij
+  solve(guide, target, conf, ...)               O6  Eq. (3) gradient descent
+
+Parity status: O1, O3, O4, O5 and O6 are pinned by tests/test_oracle_pins.py
+(worked examples, dense triangular matrices, closed forms, brute force,
+reductions); the whole solve is NOT pinned against the paper's own outputs,
+which it never prints ("parity unpinned vs the paper").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dts_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "libdts_oracle.so")
+_lib = None
+
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+_c_float_p = ctypes.POINTER(ctypes.c_float)
+
+
+def build(force: bool = False) -> str:
+    """Compile dts_oracle.c into oracle/libdts_oracle.so (gcc, OpenMP, no fast-math)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
+               "-shared", "-fPIC", "-o", _LIB_PATH, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    build()
+    lib = ctypes.CDLL(_LIB_PATH)
+    i64, i32, dbl = ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    lib.dts_oracle_distances.argtypes = [_c_float_p, i64, i64, i32, dbl, dbl, _c_double_p, _c_double_p]
+    lib.dts_oracle_distances.restype = ctypes.c_int
+    lib.dts_oracle_sigmas.argtypes = [dbl, i32, _c_double_p]
+    lib.dts_oracle_sigmas.restype = None
+    lib.dts_oracle_rf1d.argtypes = [_c_double_p, _c_double_p, i64, i64]
+    lib.dts_oracle_rf1d.restype = None
+    lib.dts_oracle_dtf.argtypes = [_c_double_p, i64, i64, i32, _c_double_p, _c_double_p, dbl, i32]
+    lib.dts_oracle_dtf.restype = ctypes.c_int
+    lib.dts_oracle_support.argtypes = [_c_double_p, _c_double_p, i64, i64, dbl, i32, _c_double_p]
+    lib.dts_oracle_support.restype = ctypes.c_int
+    lib.dts_oracle_solve.argtypes = [_c_float_p, i64, i64, i32, dbl, dbl, i32,
+                                     _c_float_p, i32, _c_float_p, dbl, dbl, i32, i32,
+                                     _c_double_p, _c_double_p]
+    lib.dts_oracle_solve.restype = ctypes.c_int
+    lib.dts_oracle_num_threads.argtypes = []
+    lib.dts_oracle_num_threads.restype = ctypes.c_int
+    lib.dts_oracle_set_threads.argtypes = [ctypes.c_int]
+    lib.dts_oracle_set_threads.restype = None
+    _lib = lib
+    return lib
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def num_threads() -> int:
+    return _load().dts_oracle_num_threads()
+
+
+def set_threads(n: int) -> None:
+    _load().dts_oracle_set_threads(int(n))
+
+
+def distances(guide, sigma_s: float, sigma_r: float):
+    """O1: (d_x, d_y), each H x W float64; +inf on the first column / row."""
+    g = _f32(guide)
+    if g.ndim == 2:
+        g = g[:, :, None]
+    H, W, C = g.shape
+    dx = np.empty((H, W), np.float64)
+    dy = np.empty((H, W), np.float64)
+    st = _load().dts_oracle_distances(_p(g, _c_float_p), H, W, C, sigma_s, sigma_r,
+                                      _p(dx, _c_double_p), _p(dy, _c_double_p))
+    if st:
+        raise ValueError(f"dts_oracle_distances failed ({st})")
+    return dx, dy
+
+
+def sigmas(sigma_s: float, N: int):
+    """O2: per-pass sigma_i, i = 1..N."""
+    out = np.empty(N, np.float64)
+    _load().dts_oracle_sigmas(sigma_s, N, _p(out, _c_double_p))
+    return out
+
+
+def rf1d(x, A):
+    """O3: one causal + anticausal recursive-filter pass of a 1-D signal."""
+    z = _f64(x).copy()
+    a = _f64(A)
+    assert a.shape == z.shape and z.ndim == 1
+    _load().dts_oracle_rf1d(_p(z, _c_double_p), _p(a, _c_double_p), z.shape[0], 1)
+    return z
+
+
+def dtf(X, dx, dy, sigma_s: float, N: int):
+    """O4: DTF of an H x W (or Ct x H x W planar) array; returns a new array."""
+    Z = _f64(X).copy()
+    squeeze = Z.ndim == 2
+    if squeeze:
+        Z = Z[None]
+    Ct, H, W = Z.shape
+    dxa, dya = _f64(dx), _f64(dy)
+    st = _load().dts_oracle_dtf(_p(Z, _c_double_p), H, W, Ct, _p(dxa, _c_double_p),
+                                _p(dya, _c_double_p), sigma_s, N)
+    if st:
+        raise ValueError(f"dts_oracle_dtf failed ({st})")
+    return Z[0] if squeeze else Z
+
+
+def support(dx, dy, sigma_s: float, mode: int = 0):
+    """O5: S = s_x * s_y (mode 0) or S = 1 (mode 1)."""
+    dxa, dya = _f64(dx), _f64(dy)
+    H, W = dxa.shape
+    S = np.empty((H, W), np.float64)
+    st = _load().dts_oracle_support(_p(dxa, _c_double_p), _p(dya, _c_double_p), H, W,
+                                    sigma_s, mode, _p(S, _c_double_p))
+    if st:
+        raise ValueError(f"dts_oracle_support failed ({st})")
+    return S
+
+
+def solve(guide, target, confidence, sigma_s: float, sigma_r: float, N: int,
+          lam: float, iters: int, step: float = 0.99, support_mode: int = 0,
+          diagnostics: bool = False):
+    """O6: the DTS gradient-descent solve.  Returns out (H x W x Ct float64; H x W if the
+    target was 2-D) and, if diagnostics, an iters x 4 array [|g|_inf, |g|_2, Fhat, Eq]."""
+    g = _f32(guide)
+    if g.ndim == 2:
+        g = g[:, :, None]
+    t = _f32(target)
+    squeeze = t.ndim == 2
+    if squeeze:
+        t = t[:, :, None]
+    c = _f32(confidence)
+    H, W, Cg = g.shape
+    assert t.shape[:2] == (H, W) and c.shape == (H, W)
+    Ct = t.shape[2]
+    out = np.empty((H, W, Ct), np.float64)
+    diag = np.zeros((max(iters, 1), 4), np.float64)
+    st = _load().dts_oracle_solve(_p(g, _c_float_p), H, W, Cg, sigma_s, sigma_r, N,
+                                  _p(t, _c_float_p), Ct, _p(c, _c_float_p), lam, step,
+                                  iters, support_mode, _p(out, _c_double_p),
+                                  _p(diag, _c_double_p) if diagnostics else None)
+    if st:
+        raise ValueError(f"dts_oracle_solve failed ({st})")
+    res = out[:, :, 0] if squeeze else out
+    if diagnostics:
+        return res, diag[:iters]
+    return res

@@ -1,0 +1,341 @@
+/*
+ * dts_oracle.c -- plain, slow, fp64 CPU oracle for the Domain Transform Solver
+ * (Bapat & Frahm, "The Domain Transform Solver", arXiv 1805.04590).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.  The
+ * product path (paper_1805_04590_b200/) never links, imports or calls it, and
+ * this file shares no code, header, table or constant with the CUDA path.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
+ * "Qk" = the reading numbered k in SURVEY.md 8(c), restated in DESIGN.md.
+ *
+ * Every routine below is the definition written out with plain loops in double
+ * precision, in the paper's order and notation:
+ *   O1 dts_oracle_distances   P:231-240 (Eqs. 8-9, square restored, Q1/Q2)
+ *   O2 dts_oracle_sigmas      recursive-filter pass schedule (Q5)
+ *   O3 dts_oracle_rf1d        recursive filter, causal then anticausal (Q4)
+ *   O4 dts_oracle_dtf         2-D edge-aware mean: rows then columns, per pass (Q6)
+ *   O5 dts_oracle_support     S = sum_j W_ij by unnormalised two-sided sums (Q7)
+ *   O6 dts_oracle_solve       gradient descent on Eq. (2) with the Eq. (3) gradient
+ * Parallelism: OpenMP "parallel for" over independent rows / column ranges only;
+ * each output element is produced by exactly one thread with the same
+ * arithmetic, so results do not depend on the thread count.  Reductions for
+ * diagnostics are serial.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_OK 0
+#define ORACLE_E_ARG 1
+#define ORACLE_E_OOM 7
+
+int dts_oracle_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+void dts_oracle_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
+/* ------------------------------------------------------------------------ */
+/* O1: domain-transform increments between adjacent pixels.
+ * (DT(x+h) - DT(x))^2 = h^2 + sum_k (I(x+h)-I(x))^2 (the L2 isometry,
+ * P:231); with the spatial/range scales of the experiments
+ * folded in as in S:125 (reading Q2):
+ *     d_x[r][c] = sqrt(1 + (sigma_s/sigma_r)^2 * sum_k (I[r][c][k] - I[r][c-1][k])^2),  c >= 1
+ *     d_x[r][0] = +inf   (no left neighbour: the recursion restarts, reading Q4)
+ * and d_y the same along columns (d_y[0][c] = +inf).
+ * guide: H x W x C fp32, HWC interleaved.  dx, dy: H x W doubles, row-major.  */
+int dts_oracle_distances(const float* guide, int64_t H, int64_t W, int32_t C,
+                         double sigma_s, double sigma_r, double* dx, double* dy) {
+    if (!guide || !dx || !dy || H < 1 || W < 1 || C < 1) return ORACLE_E_ARG;
+    if (!(sigma_s > 0.0) || !(sigma_r > 0.0)) return ORACLE_E_ARG;
+    const double ratio = sigma_s / sigma_r;
+    const double ratio2 = ratio * ratio;
+    int64_t r;
+#pragma omp parallel for schedule(static)
+    for (r = 0; r < H; ++r) {
+        for (int64_t c = 0; c < W; ++c) {
+            /* horizontal neighbour (r, c-1) */
+            if (c == 0) {
+                dx[r * W + c] = INFINITY;
+            } else {
+                double sum = 0.0;
+                for (int32_t k = 0; k < C; ++k) {
+                    double diff = (double)guide[(r * W + c) * C + k] - (double)guide[(r * W + c - 1) * C + k];
+                    sum += diff * diff;
+                }
+                dx[r * W + c] = sqrt(1.0 + ratio2 * sum);
+            }
+            /* vertical neighbour (r-1, c) */
+            if (r == 0) {
+                dy[r * W + c] = INFINITY;
+            } else {
+                double sum = 0.0;
+                for (int32_t k = 0; k < C; ++k) {
+                    double diff = (double)guide[(r * W + c) * C + k] - (double)guide[((r - 1) * W + c) * C + k];
+                    sum += diff * diff;
+                }
+                dy[r * W + c] = sqrt(1.0 + ratio2 * sum);
+            }
+        }
+    }
+    return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O2: per-pass standard deviations of the N-pass recursive filter (reading Q5):
+ *     sigma_i = sigma_s * sqrt(3) * 2^(N-i) / sqrt(4^N - 1),  i = 1..N
+ * so that sum_i sigma_i^2 = sigma_s^2; the pass-i feedback is a_i = exp(-sqrt(2)/sigma_i)
+ * and the per-pixel coefficient is a_i^d = exp(-sqrt(2) d / sigma_i). */
+void dts_oracle_sigmas(double sigma_s, int32_t N, double* sigma_i) {
+    const double denom = sqrt(pow(4.0, (double)N) - 1.0);
+    for (int32_t i = 1; i <= N; ++i)
+        sigma_i[i - 1] = sigma_s * sqrt(3.0) * pow(2.0, (double)(N - i)) / denom;
+}
+
+/* coefficient a^d for pass sigma: exp(-sqrt(2) * d / sigma); exp(-inf) = 0 */
+static double rf_coef(double d, double sigma) {
+    return exp(-sqrt(2.0) * d / sigma);
+}
+
+/* ------------------------------------------------------------------------ */
+/* O3: one recursive-filter pass over a 1-D signal of n samples, spaced `stride`
+ * elements apart (reading Q4; the recurrence is the one BASELINE.json's
+ * north star restates, J[n] = (1 - a^d) I[n] + a^d J[n-1]):
+ *     causal:      y[0] = x[0];        y[k] = (1 - A[k]) x[k] + A[k] y[k-1]
+ *     anticausal:  z[n-1] = y[n-1];    z[k] = (1 - A[k+1]) y[k] + A[k+1] z[k+1]
+ * A[0] is not used (the +inf sentinel makes it 0).  In place: x <- z. */
+void dts_oracle_rf1d(double* x, const double* A, int64_t n, int64_t stride) {
+    if (n <= 0) return;
+    /* causal */
+    for (int64_t k = 1; k < n; ++k) {
+        double a = A[k * stride];
+        x[k * stride] = (1.0 - a) * x[k * stride] + a * x[(k - 1) * stride];
+    }
+    /* anticausal */
+    for (int64_t k = n - 2; k >= 0; --k) {
+        double a = A[(k + 1) * stride];
+        x[k * stride] = (1.0 - a) * x[k * stride] + a * x[(k + 1) * stride];
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O4: the 2-D edge-aware mean  zbar = DTF(z)  ("two passes, once in the
+ * X direction and once in Y"; P:249 alternating X then Y; N passes with the O2
+ * schedule, reading Q5/Q6).  For i = 1..N: every row is filtered with
+ * A_i^x = exp(-sqrt2 d_x / sigma_i), then every column with A_i^y.
+ * X: Ct planes of H x W doubles, filtered in place; channels are independent
+ * (reading Q14).  Ax, Ay: per-pass coefficient arrays, N x H x W each.       */
+static void dtf_with_coefs(double* X, int64_t H, int64_t W, int32_t Ct, int32_t N,
+                           const double* Ax, const double* Ay) {
+    for (int32_t i = 0; i < N; ++i) {
+        const double* ax = Ax + (int64_t)i * H * W;
+        const double* ay = Ay + (int64_t)i * H * W;
+        for (int32_t ch = 0; ch < Ct; ++ch) {
+            double* P = X + (int64_t)ch * H * W;
+            /* rows: each row is one 1-D signal */
+            int64_t r;
+#pragma omp parallel for schedule(static)
+            for (r = 0; r < H; ++r) dts_oracle_rf1d(P + r * W, ax + r * W, W, 1);
+            /* columns, row-streaming: the same recurrence as dts_oracle_rf1d
+             * along each column, evaluated for all columns of a range at once
+             * so that memory is walked row by row. */
+            const int64_t block = 256;
+            const int64_t nblk = (W + block - 1) / block;
+            int64_t b;
+#pragma omp parallel for schedule(static)
+            for (b = 0; b < nblk; ++b) {
+                const int64_t c0 = b * block;
+                const int64_t c1 = (c0 + block < W) ? c0 + block : W;
+                for (int64_t k = 1; k < H; ++k)          /* causal, top -> bottom */
+                    for (int64_t c = c0; c < c1; ++c) {
+                        double a = ay[k * W + c];
+                        P[k * W + c] = (1.0 - a) * P[k * W + c] + a * P[(k - 1) * W + c];
+                    }
+                for (int64_t k = H - 2; k >= 0; --k)     /* anticausal, bottom -> top */
+                    for (int64_t c = c0; c < c1; ++c) {
+                        double a = ay[(k + 1) * W + c];
+                        P[k * W + c] = (1.0 - a) * P[k * W + c] + a * P[(k + 1) * W + c];
+                    }
+            }
+        }
+    }
+}
+
+static int make_coefs(const double* dx, const double* dy, int64_t H, int64_t W,
+                      double sigma_s, int32_t N, double** Ax_out, double** Ay_out) {
+    double sig[64];
+    if (N < 1 || N > 64) return ORACLE_E_ARG;
+    dts_oracle_sigmas(sigma_s, N, sig);
+    double* Ax = (double*)malloc(sizeof(double) * (size_t)N * (size_t)H * (size_t)W);
+    double* Ay = (double*)malloc(sizeof(double) * (size_t)N * (size_t)H * (size_t)W);
+    if (!Ax || !Ay) { free(Ax); free(Ay); return ORACLE_E_OOM; }
+    for (int32_t i = 0; i < N; ++i) {
+        int64_t p;
+#pragma omp parallel for schedule(static)
+        for (p = 0; p < H * W; ++p) {
+            Ax[(int64_t)i * H * W + p] = rf_coef(dx[p], sig[i]);
+            Ay[(int64_t)i * H * W + p] = rf_coef(dy[p], sig[i]);
+        }
+    }
+    *Ax_out = Ax;
+    *Ay_out = Ay;
+    return ORACLE_OK;
+}
+
+/* DTF of Ct planar channels given the O1 distances.  X (Ct x H x W) in place. */
+int dts_oracle_dtf(double* X, int64_t H, int64_t W, int32_t Ct,
+                   const double* dx, const double* dy, double sigma_s, int32_t N) {
+    if (!X || !dx || !dy || H < 1 || W < 1 || Ct < 1 || N < 1) return ORACLE_E_ARG;
+    double *Ax = NULL, *Ay = NULL;
+    int st = make_coefs(dx, dy, H, W, sigma_s, N, &Ax, &Ay);
+    if (st) return st;
+    dtf_with_coefs(X, H, W, Ct, N, Ax, Ay);
+    free(Ax);
+    free(Ay);
+    return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O5: support S_i = sum_j W_ij ("weigh the confidence c_i ... by
+ * sum_j W_ij"), for the recursive-filter kernel (reading Q7): separable
+ * unnormalised two-sided exponential sums with a = exp(-sqrt2 / sigma_s),
+ *     P[k] = 1 + a^{d[k]} P[k-1],  P[0] = 1
+ *     Q[k] = 1 + a^{d[k+1]} Q[k+1], Q[n-1] = 1
+ *     s = P + Q - 1     (each pixel counts itself once: W_ii = 1)
+ * along rows (s_x, with d_x) and along columns (s_y, with d_y); S = s_x * s_y.
+ * support_mode 1 gives S = 1 (the unweighted A/B option of Q7).             */
+int dts_oracle_support(const double* dx, const double* dy, int64_t H, int64_t W,
+                       double sigma_s, int32_t support_mode, double* S) {
+    if (!dx || !dy || !S || H < 1 || W < 1 || !(sigma_s > 0.0)) return ORACLE_E_ARG;
+    if (support_mode == 1) {
+        for (int64_t p = 0; p < H * W; ++p) S[p] = 1.0;
+        return ORACLE_OK;
+    }
+    double* sx = (double*)malloc(sizeof(double) * (size_t)H * (size_t)W);
+    double* P = (double*)malloc(sizeof(double) * (size_t)(H > W ? H : W));
+    double* Q = (double*)malloc(sizeof(double) * (size_t)(H > W ? H : W));
+    if (!sx || !P || !Q) { free(sx); free(P); free(Q); return ORACLE_E_OOM; }
+    /* rows (serial: create-time, plain) */
+    for (int64_t r = 0; r < H; ++r) {
+        const double* d = dx + r * W;
+        P[0] = 1.0;
+        for (int64_t k = 1; k < W; ++k) P[k] = 1.0 + rf_coef(d[k], sigma_s) * P[k - 1];
+        Q[W - 1] = 1.0;
+        for (int64_t k = W - 2; k >= 0; --k) Q[k] = 1.0 + rf_coef(d[k + 1], sigma_s) * Q[k + 1];
+        for (int64_t k = 0; k < W; ++k) sx[r * W + k] = P[k] + Q[k] - 1.0;
+    }
+    /* columns */
+    for (int64_t c = 0; c < W; ++c) {
+        P[0] = 1.0;
+        for (int64_t k = 1; k < H; ++k) P[k] = 1.0 + rf_coef(dy[k * W + c], sigma_s) * P[k - 1];
+        Q[H - 1] = 1.0;
+        for (int64_t k = H - 2; k >= 0; --k) Q[k] = 1.0 + rf_coef(dy[(k + 1) * W + c], sigma_s) * Q[k + 1];
+        for (int64_t k = 0; k < H; ++k) S[k * W + c] = sx[k * W + c] * (P[k] + Q[k] - 1.0);
+    }
+    free(sx);
+    free(P);
+    free(Q);
+    return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O6: the DTS iteration (Eqs. 3-4; step 0.99):
+ *     chat = c / S                                        (reading Q7)
+ *     Z^0 = T                                             (reading Q11)
+ *     for k = 0..iters-1:
+ *         zbar = DTF(Z^k)                                  (recomputed every iteration, Q12)
+ *         g    = lambda (Z^k - zbar) + chat (Z^k - T)      (Eq. 3 as printed, Q8)
+ *         Z^{k+1} = Z^k - step * g
+ * guide: H x W x Cg fp32 HWC; target: H x W x Ct fp32 HWC; confidence: H x W fp32
+ * (one channel broadcast over Ct, Q14).  out: H x W x Ct doubles HWC.
+ * diag (optional, iters x 4 doubles): per iteration k, computed at Z^k:
+ *     [0] ||g||_inf   [1] ||g||_2
+ *     [2] Fhat = lambda/2 ||Z - zbar||^2 + 1/2 sum chat (Z - T)^2
+ *     [3] Eq  = lambda/2 Z.(Z - zbar) + 1/2 sum chat (Z - T)^2
+ * (reading Q13: the residual norms are asserted monotone, the objectives only
+ * reported).                                                                  */
+int dts_oracle_solve(const float* guide, int64_t H, int64_t W, int32_t Cg,
+                     double sigma_s, double sigma_r, int32_t N,
+                     const float* target, int32_t Ct, const float* confidence,
+                     double lambda, double step, int32_t iters, int32_t support_mode,
+                     double* out, double* diag) {
+    if (!guide || !target || !confidence || !out) return ORACLE_E_ARG;
+    if (H < 1 || W < 1 || Cg < 1 || Ct < 1 || N < 1 || iters < 0) return ORACLE_E_ARG;
+    const int64_t HW = H * W;
+    double* dx = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* dy = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* S = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* chat = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* Z = (double*)malloc(sizeof(double) * (size_t)HW * (size_t)Ct);
+    double* T = (double*)malloc(sizeof(double) * (size_t)HW * (size_t)Ct);
+    double* Zbar = (double*)malloc(sizeof(double) * (size_t)HW * (size_t)Ct);
+    double *Ax = NULL, *Ay = NULL;
+    int st = ORACLE_OK;
+    if (!dx || !dy || !S || !chat || !Z || !T || !Zbar) { st = ORACLE_E_OOM; goto done; }
+
+    st = dts_oracle_distances(guide, H, W, Cg, sigma_s, sigma_r, dx, dy);        /* O1 */
+    if (st) goto done;
+    st = dts_oracle_support(dx, dy, H, W, sigma_s, support_mode, S);            /* O5 */
+    if (st) goto done;
+    st = make_coefs(dx, dy, H, W, sigma_s, N, &Ax, &Ay);                        /* O2 */
+    if (st) goto done;
+
+    for (int64_t p = 0; p < HW; ++p) chat[p] = (double)confidence[p] / S[p];
+    /* planar copies of the target: channel ch of pixel p at [ch*HW + p] */
+    for (int32_t ch = 0; ch < Ct; ++ch)
+        for (int64_t p = 0; p < HW; ++p) {
+            T[ch * HW + p] = (double)target[p * Ct + ch];
+            Z[ch * HW + p] = T[ch * HW + p];
+        }
+
+    for (int32_t k = 0; k < iters; ++k) {
+        memcpy(Zbar, Z, sizeof(double) * (size_t)HW * (size_t)Ct);
+        dtf_with_coefs(Zbar, H, W, Ct, N, Ax, Ay);                              /* O4 */
+        if (diag) {
+            double ginf = 0.0, g2 = 0.0, fhat = 0.0, eq = 0.0;
+            for (int32_t ch = 0; ch < Ct; ++ch)
+                for (int64_t p = 0; p < HW; ++p) {
+                    double z = Z[ch * HW + p], zb = Zbar[ch * HW + p], t = T[ch * HW + p];
+                    double g = lambda * (z - zb) + chat[p] * (z - t);
+                    if (fabs(g) > ginf) ginf = fabs(g);
+                    g2 += g * g;
+                    fhat += 0.5 * lambda * (z - zb) * (z - zb) + 0.5 * chat[p] * (z - t) * (z - t);
+                    eq += 0.5 * lambda * z * (z - zb) + 0.5 * chat[p] * (z - t) * (z - t);
+                }
+            diag[4 * k + 0] = ginf;
+            diag[4 * k + 1] = sqrt(g2);
+            diag[4 * k + 2] = fhat;
+            diag[4 * k + 3] = eq;
+        }
+        int64_t q;
+#pragma omp parallel for schedule(static)
+        for (q = 0; q < HW * Ct; ++q) {
+            int64_t p = q % HW;
+            double g = lambda * (Z[q] - Zbar[q]) + chat[p] * (Z[q] - T[q]);        /* Eq. (3) */
+            Z[q] = Z[q] - step * g;
+        }
+    }
+    for (int32_t ch = 0; ch < Ct; ++ch)
+        for (int64_t p = 0; p < HW; ++p) out[p * Ct + ch] = Z[ch * HW + p];
+
+done:
+    free(dx); free(dy); free(S); free(chat); free(Z); free(T); free(Zbar);
+    free(Ax); free(Ay);
+    return st;
+}

@@ -1,0 +1,347 @@
+"""Pins for the fp64 oracle (CPU only).  Each test checks the oracle against
+something other than itself: values hand-derived in tests/golden (cited there),
+closed forms, dense triangular matrices built from their product formulas
+(tests/dense.py), brute-force sums, invariants and the paper's stated
+reductions.  Chosen so that a dropped term, wrong sign, wrong index (A[k] vs
+A[k+1]), transposed operand or wrong pass order fails at least one test."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from tests import dense
+from synth import make_inputs, random_problem
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+SS = GOLD["sigma_s"]  # a = 1/2
+
+
+def const_guide(H, W, C=3, v=0.3):
+    return np.full((H, W, C), v, np.float32)
+
+
+# ------------------------------------------------------------------ O1
+def test_distances_spec_examples():
+    dx, dy = oracle.distances(const_guide(1, 5), 8.0, 0.2)
+    np.testing.assert_array_equal(dx[0], GOLD["distances_spec"]["constant_row_dx"])
+    assert np.all(np.isinf(dy))
+    g = np.array([[[0.0], [1.0]]], np.float32)
+    dx, _ = oracle.distances(g, 0.5, 0.5)
+    np.testing.assert_allclose(dx[0], GOLD["distances_spec"]["ramp_dx"], rtol=1e-15)
+
+
+def test_distances_hand_2x2():
+    e = GOLD["distances_2x2"]
+    g = np.array(e["guide"], np.float32)[:, :, None]
+    dx, dy = oracle.distances(g, e["sigma_s"], e["sigma_r"])
+    np.testing.assert_allclose(dx, np.array(e["dx"]), rtol=1e-6)
+    np.testing.assert_allclose(dy, np.array(e["dy"]), rtol=1e-6)
+
+
+def test_distances_invariants():
+    rng = np.random.default_rng(1)
+    g1 = rng.uniform(0, 1, (7, 9, 2)).astype(np.float32)
+    g2 = rng.uniform(0, 1, (7, 9, 3)).astype(np.float32)
+    ss, sr = 5.0, 0.3
+    dx1, dy1 = oracle.distances(g1, ss, sr)
+    dx2, dy2 = oracle.distances(g2, ss, sr)
+    dx12, dy12 = oracle.distances(np.concatenate([g1, g2], 2), ss, sr)
+    fin = np.isfinite(dx12)
+    # squared increments add over channels (L2 isometry)
+    np.testing.assert_allclose((dx12 ** 2 - 1)[fin], ((dx1 ** 2 - 1) + (dx2 ** 2 - 1))[fin], rtol=1e-12)
+    fin = np.isfinite(dy12)
+    np.testing.assert_allclose((dy12 ** 2 - 1)[fin], ((dy1 ** 2 - 1) + (dy2 ** 2 - 1))[fin], rtol=1e-12)
+    # vertical distances are horizontal distances of the transposed guide
+    dxt, dyt = oracle.distances(np.ascontiguousarray(g1.transpose(1, 0, 2)), ss, sr)
+    np.testing.assert_array_equal(dy1, dxt.T)
+    np.testing.assert_array_equal(dx1, dyt.T)
+    # monotone DT: every finite increment >= 1; sentinels exactly on first column / row
+    assert np.all(dx1[:, 1:] >= 1) and np.all(np.isinf(dx1[:, 0]))
+    assert np.all(dy1[1:] >= 1) and np.all(np.isinf(dy1[0]))
+    # sigma scaling enters only through sigma_s / sigma_r
+    dxs, _ = oracle.distances(g1, 2 * ss, 2 * sr)
+    np.testing.assert_allclose(dxs, dx1, rtol=1e-14)
+
+
+# ------------------------------------------------------------------ O2
+@pytest.mark.parametrize("N", [1, 2, 3, 5])
+def test_sigma_schedule(N):
+    s = oracle.sigmas(16.0, N)
+    assert math.isclose(float(np.sum(s ** 2)), 256.0, rel_tol=1e-12)  # variances add to sigma_s^2
+    np.testing.assert_allclose(s[:-1] / s[1:], 2.0, rtol=1e-12)       # halving per pass
+    if N == 1:
+        assert math.isclose(s[0], 16.0, rel_tol=1e-14)
+
+
+# ------------------------------------------------------------------ O3
+def test_rf1d_worked_example():
+    e = GOLD["impulse_1x5"]
+    A = np.array([0, .5, .5, .5, .5])
+    np.testing.assert_allclose(oracle.rf1d(e["x"], A), e["dtf"], rtol=0, atol=1e-16)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 8, 13])
+def test_rf1d_equals_dense_triangular(n):
+    rng = np.random.default_rng(n)
+    A = rng.uniform(0, 0.95, n)
+    A[0] = 0.0
+    x = rng.normal(size=n)
+    np.testing.assert_allclose(oracle.rf1d(x, A), dense.pass1d(A) @ x, rtol=1e-13, atol=1e-14)
+
+
+def test_rf1d_row_stochastic_and_edge_free_kernel():
+    rng = np.random.default_rng(3)
+    A = rng.uniform(0, 0.99, 50)
+    A[0] = 0
+    np.testing.assert_allclose(oracle.rf1d(np.full(50, 2.5), A), 2.5, rtol=1e-14)
+    a, n = 0.8, 801
+    A = np.full(n, a)
+    A[0] = 0
+    x = np.zeros(n)
+    x[n // 2] = 1.0
+    z = oracle.rf1d(x, A)
+    half = 200
+    np.testing.assert_allclose(z[n // 2 - half:n // 2 + half + 1], dense.edge_free_kernel(a, half),
+                               rtol=1e-12, atol=1e-18)
+
+
+# ------------------------------------------------------------------ O4
+def test_dtf_worked_examples():
+    g = const_guide(1, 5)
+    dx, dy = oracle.distances(g, SS, 0.1)
+    np.testing.assert_allclose(oracle.dtf(np.array([[0, 0, 1, 0, 0.]]), dx, dy, SS, 1)[0],
+                               GOLD["impulse_1x5"]["dtf"], atol=1e-15)
+    g = const_guide(2, 2)
+    dx, dy = oracle.distances(g, SS, 0.1)
+    np.testing.assert_allclose(oracle.dtf(np.array(GOLD["dtf_2x2"]["t"], float), dx, dy, SS, 1),
+                               GOLD["dtf_2x2"]["dtf"], atol=1e-15)
+    g = const_guide(1, 2)
+    dx, dy = oracle.distances(g, SS, 0.1)
+    K = np.stack([oracle.dtf(np.array([[1., 0]]), dx, dy, SS, 1)[0],
+                  oracle.dtf(np.array([[0., 1]]), dx, dy, SS, 1)[0]], 1)
+    np.testing.assert_allclose(K, GOLD["pair_1x2"]["K"], atol=1e-15)
+
+
+@pytest.mark.parametrize("H,W,N", [(1, 6, 2), (5, 1, 1), (4, 5, 3), (6, 7, 3), (3, 3, 4)])
+def test_dtf_equals_dense_operator(H, W, N):
+    rng = np.random.default_rng(H * 100 + W)
+    dx = rng.uniform(1, 4, (H, W))
+    dy = rng.uniform(1, 4, (H, W))
+    dx[:, 0] = np.inf
+    dy[0, :] = np.inf
+    ss = 3.0
+    K = dense.dtf_operator(dx, dy, oracle.sigmas(ss, N))
+    assert np.all(K >= -1e-15)
+    np.testing.assert_allclose(K.sum(1), 1.0, rtol=1e-13)              # row-stochastic
+    X = rng.normal(size=(2, H, W))
+    Y = oracle.dtf(X, dx, dy, ss, N)
+    for ch in range(2):
+        np.testing.assert_allclose(Y[ch].ravel(), K @ X[ch].ravel(), rtol=1e-12, atol=1e-13)
+
+
+def test_dtf_order_rows_then_columns_matters():
+    """Pass order is part of the definition (reading R6): columns-first differs."""
+    rng = np.random.default_rng(5)
+    dx = rng.uniform(1, 5, (4, 4)); dx[:, 0] = np.inf
+    dy = rng.uniform(1, 5, (4, 4)); dy[0] = np.inf
+    s = oracle.sigmas(3.0, 1)
+    Kr = dense.dtf_operator(dx, dy, s)
+    Ax = np.exp(-np.sqrt(2) * dx / s[0]); Ay = np.exp(-np.sqrt(2) * dy / s[0])
+    Kc = dense.row_operator(Ax) @ dense.col_operator(Ay)
+    X = rng.normal(size=(4, 4))
+    Y = oracle.dtf(X, dx, dy, 3.0, 1).ravel()
+    np.testing.assert_allclose(Y, Kr @ X.ravel(), rtol=1e-12)
+    assert np.max(np.abs(Y - Kc @ X.ravel())) > 1e-6
+
+
+def test_dtf_edge_free_cascade_closed_form():
+    """Edge-free guide: the N-pass cascade is the convolution of the per-pass kernels
+    (1-a_i)/(1+a_i) a_i^|k|; its variance is sum 2 a_i/(1-a_i)^2 ~= sigma_s^2 (R5)."""
+    ss, N, n = 16.0, 3, 2001
+    sig = oracle.sigmas(ss, N)
+    a = np.exp(-np.sqrt(2) / sig)
+    dx = np.ones((1, n)); dx[0, 0] = np.inf
+    dy = np.full((1, n), np.inf)
+    x = np.zeros((1, n)); x[0, n // 2] = 1
+    z = oracle.dtf(x, dx, dy, ss, N)[0]
+    half = 700
+    h = np.array([1.0])
+    for ai in a:
+        h = np.convolve(h, dense.edge_free_kernel(ai, half))
+    c = len(h) // 2
+    h = h[c - 300:c + 301]
+    np.testing.assert_allclose(z[n // 2 - 300:n // 2 + 301], h, rtol=1e-9, atol=1e-17)
+    k = np.arange(-(n // 2), n // 2 + 1)
+    var = float(np.sum(z * k ** 2))
+    assert math.isclose(var, float(np.sum(2 * a / (1 - a) ** 2)), rel_tol=1e-9)
+    assert abs(var - ss ** 2) / ss ** 2 < 0.01   # 255.50 vs 256 at sigma_s = 16
+    # 2-D edge-free: impulse response is the outer product of the 1-D cascades
+    m = 81
+    g = const_guide(m, m)
+    dx2, dy2 = oracle.distances(g, 3.0, 0.1)
+    X = np.zeros((m, m)); X[m // 2, m // 2] = 1
+    Z = oracle.dtf(X, dx2, dy2, 3.0, 2)
+    X1 = np.zeros((1, m)); X1[0, m // 2] = 1
+    z1 = oracle.dtf(X1, dx2[:1], np.full((1, m), np.inf), 3.0, 2)[0]
+    np.testing.assert_allclose(Z, np.outer(z1, z1), rtol=1e-9, atol=1e-16)
+
+
+def test_dtf_decoupling_exact():
+    """Tiny sigma_r: a^d across a strong edge underflows to exactly 0 (BASELINE north star),
+    so the left region's result is bit-identical whatever is on the right."""
+    H, W = 10, 16
+    g = np.zeros((H, W, 3), np.float32); g[:, W // 2:] = 1.0
+    dx, dy = oracle.distances(g, 8.0, 1e-3)
+    rng = np.random.default_rng(0)
+    X1 = rng.normal(size=(H, W)); X2 = X1.copy(); X2[:, W // 2:] = rng.normal(size=(H, W // 2)) * 100
+    Y1 = oracle.dtf(X1, dx, dy, 8.0, 3)
+    Y2 = oracle.dtf(X2, dx, dy, 8.0, 3)
+    np.testing.assert_array_equal(Y1[:, :W // 2], Y2[:, :W // 2])
+    Yc = oracle.dtf(np.ascontiguousarray(X1[:, :W // 2]), dx[:, :W // 2], dy[:, :W // 2], 8.0, 3)
+    np.testing.assert_allclose(Y1[:, :W // 2], Yc, rtol=1e-14, atol=1e-15)
+
+
+# ------------------------------------------------------------------ O5
+def brute_support(dx, dy, ss):
+    H, W = dx.shape
+    sx = np.zeros((H, W)); sy = np.zeros((H, W))
+    for r in range(H):
+        ct = np.concatenate([[0.0], np.cumsum(dx[r, 1:])])
+        sx[r] = np.exp(-np.sqrt(2) * np.abs(ct[:, None] - ct[None, :]) / ss).sum(1)
+    for c in range(W):
+        ct = np.concatenate([[0.0], np.cumsum(dy[1:, c])])
+        sy[:, c] = np.exp(-np.sqrt(2) * np.abs(ct[:, None] - ct[None, :]) / ss).sum(1)
+    return sx * sy
+
+
+def test_support_worked_and_closed_form():
+    dx, dy = oracle.distances(const_guide(1, 2), SS, 0.1)
+    np.testing.assert_allclose(oracle.support(dx, dy, SS)[0], GOLD["pair_1x2"]["S"], atol=1e-15)
+    dx, dy = oracle.distances(const_guide(2, 2), SS, 0.1)
+    np.testing.assert_allclose(oracle.support(dx, dy, SS), GOLD["dtf_2x2"]["S"], atol=1e-15)
+    W, ss = 40, 6.0
+    a = math.exp(-math.sqrt(2) / ss)
+    dx, dy = oracle.distances(const_guide(1, W), ss, 0.1)
+    n = np.arange(W)
+    closed = (1 + a - a ** (n + 1) - a ** (W - n)) / (1 - a)
+    np.testing.assert_allclose(oracle.support(dx, dy, ss)[0], closed, rtol=1e-13)
+
+
+def test_support_brute_force_and_mode():
+    g, _, _ = random_problem(9, 11, 3, 1, seed=4)
+    dx, dy = oracle.distances(g, 4.0, 0.2)
+    S = oracle.support(dx, dy, 4.0)
+    np.testing.assert_allclose(S, brute_support(dx, dy, 4.0), rtol=1e-12)
+    assert np.all(S >= 1.0)
+    np.testing.assert_array_equal(oracle.support(dx, dy, 4.0, mode=1), 1.0)
+
+
+# ------------------------------------------------------------------ O6
+def test_solve_worked_1x2():
+    e = GOLD["solve_1x2"]
+    g = const_guide(1, 2)
+    t = np.array([e["t"]], np.float32); c = np.array([e["c"]], np.float32)
+    z1, diag = oracle.solve(g, t, c, SS, 0.1, 1, e["lambda"], 1, step=e["step"], diagnostics=True)
+    np.testing.assert_allclose(z1[0], e["z_iter1"], atol=1e-15)
+    assert math.isclose(diag[0, 0], max(abs(v) for v in e["g_iter1"]), rel_tol=1e-14)
+    zc = oracle.solve(g, t, c, SS, 0.1, 1, e["lambda"], 3000, step=e["step"])
+    np.testing.assert_allclose(zc[0], e["z_converged"], atol=1e-13)
+
+
+def test_solve_zero_iterations_is_target():
+    g, t, c = random_problem(5, 7, 3, 2, seed=1)
+    np.testing.assert_array_equal(oracle.solve(g, t, c, 4.0, 0.2, 3, 0.99, 0), t.astype(np.float64))
+
+
+def test_solve_constant_target_stays_constant():
+    g, _, c = random_problem(12, 9, 3, 1, seed=2)
+    t = np.full((12, 9), 3.25, np.float32)
+    z = oracle.solve(g, t, c, 4.0, 0.2, 3, 0.99, 50)
+    np.testing.assert_allclose(z, 3.25, rtol=1e-13)
+
+
+def test_solve_c0_is_filter():
+    """c = 0 reduces DTS to DT filtering; with step = 1/lambda one step gives DTF(t)."""
+    g, t, _ = random_problem(8, 10, 3, 1, seed=3)
+    c = np.zeros((8, 10), np.float32)
+    lam = 1 / 0.99
+    z = oracle.solve(g, t, c, 5.0, 0.2, 3, lam, 1, step=0.99)
+    dx, dy = oracle.distances(g, 5.0, 0.2)
+    K = dense.dtf_operator(dx, dy, oracle.sigmas(5.0, 3))
+    np.testing.assert_allclose(z.ravel(), K @ t.astype(np.float64).ravel(), rtol=1e-12, atol=1e-13)
+
+
+def test_solve_two_steps_dense():
+    """Two iterations of Eq. (3) written with the dense operator and brute-force support:
+    pins the sign of both terms, chat = c/S, the step and z-bar recomputation."""
+    g, t, c = random_problem(5, 6, 3, 1, seed=6, conf_lo=0.2)
+    ss, sr, lam, step = 3.0, 0.3, 0.9, 0.99
+    dx, dy = oracle.distances(g, ss, sr)
+    K = dense.dtf_operator(dx, dy, oracle.sigmas(ss, 3))
+    chat = (c.astype(np.float64) / brute_support(dx, dy, ss)).ravel()
+    tt = t.astype(np.float64).ravel()
+    z = tt.copy()
+    for _ in range(2):
+        z = z - step * (lam * (z - K @ z) + chat * (z - tt))
+    np.testing.assert_allclose(oracle.solve(g, t, c, ss, sr, 3, lam, 2, step=step).ravel(), z,
+                               rtol=1e-12, atol=1e-13)
+
+
+def test_solve_fixed_point_eq4():
+    """Eq. (4): the limit solves (lambda (I - K) + diag(chat)) z = chat t."""
+    g, t, c = random_problem(6, 8, 3, 1, seed=7, conf_lo=0.5)
+    ss, sr, lam = 2.0, 0.3, 0.99
+    dx, dy = oracle.distances(g, ss, sr)
+    K = dense.dtf_operator(dx, dy, oracle.sigmas(ss, 3))
+    chat = (c.astype(np.float64) / brute_support(dx, dy, ss)).ravel()
+    M = lam * (np.eye(48) - K) + np.diag(chat)
+    zstar = np.linalg.solve(M, chat * t.astype(np.float64).ravel())
+    z, diag = oracle.solve(g, t, c, ss, sr, 3, lam, 4000, diagnostics=True)
+    np.testing.assert_allclose(z.ravel(), zstar, rtol=1e-9, atol=1e-10)
+    assert diag[-1, 0] <= 1e-3 * (lam + 1)   # S:249 residual bound
+
+
+def test_solve_residual_norms_monotone():
+    """Reading R13: ||g||_inf and ||g||_2 never increase (asserted); Eq. (2) objectives
+    are only reported."""
+    g, t, c = make_inputs("C0")
+    _, diag = oracle.solve(g, t, c, 8.0, 0.2, 3, 1.0, 60, diagnostics=True)
+    ginf, g2 = diag[:, 0], diag[:, 1]
+    assert np.all(np.diff(ginf) <= 1e-12 * ginf[0])
+    assert np.all(np.diff(g2) <= 1e-12 * g2[0])
+    assert ginf[-1] < 0.5 * ginf[0]
+
+
+def test_solve_channels_independent():
+    g, t, c = random_problem(7, 9, 3, 3, seed=8)
+    z = oracle.solve(g, t, c, 4.0, 0.2, 3, 0.99, 5)
+    for ch in range(3):
+        z1 = oracle.solve(g, np.ascontiguousarray(t[..., ch]), c, 4.0, 0.2, 3, 0.99, 5)
+        np.testing.assert_array_equal(z[..., ch], z1)
+
+
+def test_solve_decoupled_regions():
+    H, W = 10, 14
+    g = np.zeros((H, W, 3), np.float32); g[:, W // 2:] = 1
+    rng = np.random.default_rng(9)
+    t = rng.uniform(0, 1, (H, W)).astype(np.float32)
+    t2 = t.copy(); t2[:, W // 2:] = 50
+    c = rng.uniform(0.1, 1, (H, W)).astype(np.float32)
+    z1 = oracle.solve(g, t, c, 8.0, 1e-3, 3, 0.99, 20)
+    z2 = oracle.solve(g, t2, c, 8.0, 1e-3, 3, 0.99, 20)
+    np.testing.assert_array_equal(z1[:, :W // 2], z2[:, :W // 2])
+
+
+def test_solve_thread_count_invariant():
+    g, t, c = make_inputs("C0")
+    n0 = oracle.num_threads()
+    z8 = oracle.solve(g, t, c, 8.0, 0.2, 3, 1.0, 5)
+    oracle.set_threads(1)
+    try:
+        z1 = oracle.solve(g, t, c, 8.0, 0.2, 3, 1.0, 5)
+    finally:
+        oracle.set_threads(n0)
+    np.testing.assert_array_equal(z8, z1)
