@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""DTS benchmark (driver contract).  One JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+Workload: BASELINE.json config C4 -- the 100-MP, 16-band
+satellite-scale guide, 1-channel target, sigma_s = 64, sigma_r = 0.2, N = 3 passes,
+lambda = 0.99, 20 iterations.  One STEP is the whole hot path over one input:
+dts_create (guide derivative K1 + support K5) + dts_solve (prologue K6 + 20 x
+[3 row passes K2, 2 column passes K3, 1 column pass fused with the update K4]) +
+dts_destroy.  Metric: Mpix*iterations per second (pixels x iterations / step time).
+
+`value` times the step with inputs resident in HBM (CUDA events on the launch
+stream, barrier + synchronize on both sides, max over ranks).  `e2e` times the
+same step through the C ABI with page-locked HOST buffers: H2D of the guide,
+target and confidence and D2H of the output happen inside the timed region.
+--impl reference times the fp64 CPU oracle (oracle/) on a bounded row-band sample
+of the same workload; that is the only other place this script executes oracle/.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import CONFIGS, make_inputs  # noqa: E402
+
+METRIC = "DTS Mpix·iter/s at 1/2/4/8 B200; achieved HBM GB/s vs peak"
+UNIT = "Mpix·iter/s"
+CPU_SAMPLE_ROWS = {"C0": 48, "C1": 1000, "C2": 1024, "C3": 256, "C4": 384}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload_desc(cfg):
+    return (f"{cfg.name}: {cfg.batch}x {cfg.W}x{cfg.H} guide with {cfg.Cg} channels, {cfg.Ct}-channel target, "
+            f"sigma_s={cfg.sigma_s:g}, sigma_r={cfg.sigma_r:g}, N={cfg.N} passes, lambda={cfg.lam:g}, "
+            f"{cfg.iters} iterations")
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def cpu_oracle_sample(cfg, steps=1, warmup=0):
+    """The oracle, as it stands, on a bounded sample: the first CPU_SAMPLE_ROWS rows
+    (full width, all channels) of the workload's image 0, all iterations."""
+    import oracle
+    rows = min(CPU_SAMPLE_ROWS.get(cfg.name, 256), cfg.H)
+    g, t, c = make_inputs(cfg.name, rows=(0, rows))
+    mpix_iter = rows * cfg.W * cfg.iters / 1e6
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        oracle.solve(g, t, c, cfg.sigma_s, cfg.sigma_r, cfg.N, cfg.lam, cfg.iters)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    return {"value": mpix_iter / statistics.median(times), "unit": UNIT, "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"rows [0,{rows}) x {cfg.W} cols of {cfg.name} image 0 ({cfg.Cg}-channel guide), "
+                      f"{cfg.iters} iterations = {mpix_iter:.1f} Mpix*iter per run; fp64 C oracle, OpenMP, "
+                      f"includes distances + support + solve",
+            "seconds_per_run": statistics.median(times)}
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    cb = cpu_oracle_sample(cfg, steps=max(args.steps, 1), warmup=args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * cb["seconds_per_run"],
+            "higher_is_better": True, "scaling": "strong" if cfg.batch == 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "sample": cb["sample"]},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1].split()[0]))
+                mx.append(float(parts[2].split()[0]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import paper_1805_04590_b200 as dts
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    # units of this rank: images (batched configs) or a row band (single-image configs)
+    if cfg.batch > 1:
+        per = cfg.batch // world
+        images = list(range(rank * per, (rank + 1) * per))
+        inputs = [make_inputs(cfg.name, image=i) for i in images]
+        scaling = "weak" if False else "strong"
+    else:
+        if world > 1:
+            raise SystemExit("row-band multi-GPU mode for single-image configs is not built yet")
+        inputs = [make_inputs(cfg.name)]
+        scaling = "strong"
+    pixels_rank = sum(g.shape[0] * g.shape[1] for g, _, _ in inputs)
+
+    stream = torch.cuda.Stream(device=dev)
+    dev_in = [tuple(torch.from_numpy(a).to(dev) for a in x) for x in inputs]
+    outs = [torch.empty_like(t) for _, t, _ in dev_in]
+
+    def step_device():
+        for (g, t, c), o in zip(dev_in, outs):
+            ctx = dts.dts_create(g, cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
+            dts.dts_solve(ctx, t, c, cfg.lam, cfg.iters, o, stream=stream.cuda_stream)
+            dts.dts_destroy(ctx)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.barrier()
+
+    def timed(fn, steps):
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            import torch.distributed as tdist
+            tt = torch.tensor([ms], device=dev)
+            tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs), per-kernel events + clock sampling ----
+    dts.dts_profile_enable(0, True)
+    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    # the library counts its own launches per context; count them for one step
+    ms = timed(step_device, args.steps)
+    clk = clocks.stop() if clocks else None
+    kstats = dts.dts_profile_read(0)
+    dts.dts_profile_enable(0, False)
+    launches = sum(v["launches"] for v in kstats.values())
+
+    ms_step = ms / args.steps
+    mpix_iter_total = pixels_rank * world * cfg.iters / 1e6
+    value = mpix_iter_total / (ms_step / 1e3)
+
+    # ---- e2e: the same step through the C ABI with pinned HOST buffers ----
+    e2e = None
+    if not args.no_e2e:
+        host_in = [tuple(torch.from_numpy(a).pin_memory() for a in x) for x in inputs]
+        host_out = [torch.empty(t.shape, dtype=torch.float32, pin_memory=True) for _, t, _ in host_in]
+        h2d = sum(g.numel() * 4 + t.numel() * 4 + c.numel() * 4 for g, t, c in host_in)
+        d2h = sum(o.numel() * 4 for o in host_out)
+
+        def step_host():
+            for (g, t, c), o in zip(host_in, host_out):
+                ctx = dts.dts_create(g, cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
+                dts.dts_solve(ctx, t, c, cfg.lam, cfg.iters, o, stream=stream.cuda_stream)
+                dts.dts_destroy(ctx)
+
+        step_host()  # warm the staging buffers
+        e_ms = timed(step_host, max(1, min(args.steps, 3)))
+        e_steps = max(1, min(args.steps, 3))
+        e2e = {"value": mpix_iter_total / (e_ms / e_steps / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / e_steps,
+               "check_max_abs_vs_device": float((host_out[0].to(dev) - outs[0]).abs().max().item())}
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel ----
+    peak, peak_src = measured_peaks()
+    fams = {k: v for k, v in kstats.items() if v["launches"] > 0}
+    for v in fams.values():
+        v["gbs"] = v["bytes_per_launch"] / (v["avg_ms"] / 1e3) / 1e9 if v["avg_ms"] > 0 else 0.0
+        v["share_of_step"] = v["total_ms"] / ms if ms > 0 else 0.0
+    dom_name = max(fams, key=lambda k: fams[k]["total_ms"])
+    dom = fams[dom_name]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        ent = tj.get(cfg.name, {}).get(dom_name)
+        if ent:
+            traffic = ent.get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": dom_name, "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
+                "frac": dom["gbs"] / peak, "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_launch": dom["bytes_per_launch"], "avg_launch_ms": dom["avg_ms"],
+                "step_gbs_algorithmic": None}
+    # whole-step algorithmic bytes / step time
+    step_bytes = sum(v["bytes_per_launch"] * v["launches"] for v in fams.values()) / args.steps
+    roofline["step_gbs_algorithmic"] = step_bytes / (ms_step / 1e3) / 1e9 * world
+
+    cpu = None
+    if not args.no_cpu and world == 1:
+        cb = cpu_oracle_sample(cfg)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "pixels": cfg.pixels, "iterations": cfg.iters,
+                       "step": "dts_create + dts_solve + dts_destroy (guide derivative, support, prologue, "
+                               f"{cfg.iters} x 6 pass kernels)",
+                       "l2": "inputs larger than L2 (6.4 GB guide, 0.4 GB per state plane): no flush needed"
+                             if cfg.name == "C4" else "L2 not flushed between steps",
+                       "parallelism": f"{'image split' if cfg.batch > 1 else 'single image'} x{world}"},
+            "roofline": roofline,
+            "kernels": {k: {kk: v[kk] for kk in ("launches", "avg_ms", "bytes_per_launch", "gbs", "share_of_step")}
+                        for k, v in fams.items()},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,146 @@
+/*
+ * dts.h -- C ABI of the B200-native Domain Transform Solver hot path.
+ *
+ * The method: Bapat & Frahm, "The Domain Transform Solver" (arXiv 1805.04590).
+ * Citations: P:n = /root/reference/PAPER.md line n; "R<k>" = reading k in
+ * DESIGN.md "Readings of the paper".
+ *
+ * The library solves, for a guide image I and a target t with confidence c,
+ *     min_z  lambda/2 sum_i (z_i - zbar_i)^2 + sum_i c_i (z_i - t_i)^2        (Eq. 2)
+ * by the gradient descent of P:481 / P:567:
+ *     z <- z - step * [ lambda (z - zbar) + (c / S) (z - t) ]                  (Eq. 3)
+ * where zbar = DTF(z) is the edge-aware mean computed with the domain
+ * transform as N passes of Gastal & Oliveira's recursive filter
+ * along rows then columns (R3-R6), and S = sum_j W_ij is the filter's support
+ * (R7).
+ *
+ * Conventions shared by every entry point:
+ *  - Images are fp32, C-contiguous, row-major, channel-interleaved (HWC):
+ *    element (r, c, k) of an H x W x C image is at [(r * W + c) * C + k].
+ *  - Array arguments may be CUDA DEVICE pointers or HOST pointers (pageable or
+ *    page-locked); the library tells them apart with cudaPointerGetAttributes.
+ *    Host arrays are copied to/from device staging buffers owned by the context
+ *    on `stream`; when any argument of a call is host memory the call returns
+ *    only after its results are in host memory (it synchronises `stream`).
+ *    With device pointers every call is asynchronous and stream-ordered.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *  - Ownership: the caller owns every array it passes; the library never frees
+ *    or retains a caller pointer after the call returns.  A dts_ctx owns its
+ *    derived buffers (domain distances, support, solver state) until
+ *    dts_destroy.  One context must not be used from two streams at once;
+ *    distinct contexts are independent.
+ *  - Errors: every entry point validates its scalar arguments on the host
+ *    before any launch and returns a dts_status; on error nothing is launched
+ *    and the outputs are untouched.  DTS_E_CUDA reports a CUDA launch/runtime
+ *    error (dts_last_error_string gives the CUDA message).  There is NO CPU
+ *    fallback: if the CUDA runtime or an sm_100a device is missing, calls fail.
+ *  - Results are deterministic: identical inputs on the same device give
+ *    bit-identical outputs (no atomics on the data path).
+ */
+#ifndef DTS_B200_H
+#define DTS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dts_ctx dts_ctx; /* opaque; owned by the library */
+
+typedef enum {
+    DTS_OK = 0,
+    DTS_E_ARG = 1,       /* invalid scalar argument or NULL / overlapping pointer      */
+    DTS_E_SHAPE = 2,     /* sizes outside what this build supports (see dts_create)   */
+    DTS_E_NONFINITE = 3, /* non-finite input detected (opt-in checks)                  */
+    DTS_E_RANGE = 4,     /* confidence outside [0, 1] (opt-in checks)                  */
+    DTS_E_CUDA = 5,      /* CUDA runtime / launch error, or no sm_100 device           */
+    DTS_E_NCCL = 6,      /* collective error (row-band mode)                           */
+    DTS_E_OOM = 7        /* device or host allocation failed                           */
+} dts_status;
+
+/* dts_create -- domain-transform setup for one guide image.
+ *   guide          H x W x C fp32, HWC; read once.  Colours are used as given (no
+ *                  clamping, R16); only differences of adjacent pixels matter.
+ *   H, W, C        >= 1.  This build supports W <= 18432 and H <= 12800 (C_t = 1;
+ *                  H <= 6400 for C_t = 3) in one context; larger -> DTS_E_SHAPE.
+ *   sigma_s        spatial std-dev in pixels (sigma_x = sigma_y), > 0, finite.
+ *   sigma_r        range std-dev in colour units, > 0, finite.
+ *   filter_passes  N >= 1 recursive-filter passes per edge-aware mean (R5); N <= 16.
+ * Computes the horizontal / vertical domain distances
+ *     d = sqrt(1 + (sigma_s/sigma_r)^2 * sum_k (I_k(p) - I_k(p'))^2)      (Eqs. 8-9, R1, R2)
+ * with +inf at the first column / row, and the support S = s_x * s_y (R7).
+ * On success *out_ctx receives a new context (release with dts_destroy).    */
+dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C,
+                      float sigma_s, float sigma_r, int32_t filter_passes,
+                      void* stream, dts_ctx** out_ctx);
+
+/* dts_solve -- `iterations` gradient-descent steps of Eq. (3) with
+ * step 0.99, starting from z^0 = t (R11).
+ *   target            H x W x target_channels fp32, HWC.  Channels are solved
+ *                     independently with the same filter (R14).
+ *   target_channels   C_t >= 1 (this build: 1 <= C_t <= 4).
+ *   confidence        H x W fp32, one channel shared by all target channels, c >= 0
+ *                     (values are not range-checked unless dts_solve_ex asks).
+ *   lambda            smoothness weight, finite, >= 0, and step*(lambda + 1) < 2
+ *                     (descent stability); the paper uses 0.99.
+ *   iterations        >= 0; 0 copies target to out exactly.
+ *   out               H x W x C_t fp32, HWC; must not overlap target or confidence.
+ * Each iteration recomputes zbar = DTF(z) (R12) and applies
+ *     z <- z - 0.99 * [ lambda (z - zbar) + (c / S) (z - t) ].                  */
+dts_status dts_solve(dts_ctx* ctx, const float* target, int32_t target_channels,
+                     const float* confidence, float lambda, int32_t iterations,
+                     float* out, void* stream);
+
+/* dts_destroy -- releases the context and its device buffers.  NULL-safe.  */
+void dts_destroy(dts_ctx* ctx);
+
+/* Human-readable name of a status code (static storage). */
+const char* dts_status_string(dts_status s);
+
+/* Message of the last CUDA error seen by this thread (static storage, "" if none). */
+const char* dts_last_error_string(void);
+
+/* ---- extensions used by the tests and the benchmark -------------------- */
+
+typedef struct {
+    float step;          /* gradient step; <= 0 selects the paper's 0.99        */
+    int32_t support_mode;/* 0: S = s_x * s_y (R7, default); 1: S = 1 (unweighted c)     */
+    int32_t check_inputs;/* 1: verify finite target/confidence and c in [0,1] (syncs)   */
+} dts_solve_opts;
+
+/* dts_solve with options; opts == NULL is exactly dts_solve. */
+dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t target_channels,
+                        const float* confidence, float lambda, int32_t iterations,
+                        float* out, void* stream, const dts_solve_opts* opts);
+
+/* Buffers a test can read back (row-major H x W, fp32; stream-ordered then synchronised). */
+typedef enum { DTS_BUF_DX = 0, DTS_BUF_DY = 1, DTS_BUF_SUPPORT = 2 } dts_buffer;
+/* Copies the H x W buffer `which` into host memory `host_out` (H*W floats). */
+dts_status dts_debug_read(dts_ctx* ctx, dts_buffer which, float* host_out);
+
+/* Per-kernel timing with CUDA events recorded on the launch stream around every
+ * launch of the library's kernels (off by default; costs one event pair per launch).
+ * The profiler is PROCESS-WIDE (statistics survive dts_destroy, so a timed step may
+ * create and destroy contexts); `ctx` is ignored and may be NULL.  Both calls
+ * synchronise the device.  Enabling (or re-enabling) resets the statistics. */
+typedef struct {
+    char name[32];          /* kernel family: deriv, row_pass, col_pass, col_update, ...  */
+    int64_t launches;       /* launches timed since dts_profile_enable                    */
+    double total_ms;        /* sum of event-measured durations                            */
+    double bytes_per_launch;/* algorithmic HBM bytes of one launch            */
+} dts_kernel_stat;
+dts_status dts_profile_enable(dts_ctx* ctx, int32_t on);
+/* Fills up to `max` records; *count receives the number of kernel families. */
+dts_status dts_profile_read(dts_ctx* ctx, dts_kernel_stat* out, int32_t max, int32_t* count);
+
+/* Number of kernel launches issued by the library since context creation (all streams). */
+int64_t dts_launch_count(const dts_ctx* ctx);
+
+/* Library version string. */
+const char* dts_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DTS_B200_H */

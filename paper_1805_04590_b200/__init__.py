@@ -1,0 +1,240 @@
+"""Python binding of the B200-native Domain Transform Solver (include/dts.h).
+
+Argument marshalling only: every step of the path runs in the sm_100a kernels of
+``libdts_b200.so`` (built in-tree by ``_build.build()`` / ``__graft_entry__.build()``).
+There is no CPU fallback: if the library is missing, or there is no sm_100 GPU,
+calls raise ``DTSError``.  PyTorch supplies device memory and streams only.
+
+Names follow the C ABI: ``dts_create``, ``dts_solve``, ``dts_solve_ex``,
+``dts_destroy`` (+ the test/bench extensions).  Arrays may be torch tensors
+(CUDA or CPU) or numpy arrays; they must be float32 and C-contiguous.  Host
+arrays are staged by the library itself (include/dts.h).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["DTSError", "dts_create", "dts_solve", "dts_solve_ex", "dts_destroy", "dts_status_string",
+           "dts_debug_read", "dts_profile_enable", "dts_profile_read", "dts_launch_count", "dts_version",
+           "Solver", "lib_path", "load_library", "DTS_BUF_DX", "DTS_BUF_DY", "DTS_BUF_SUPPORT",
+           "ABI_FUNCTIONS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libdts_b200.so")
+_lib = None
+
+DTS_BUF_DX, DTS_BUF_DY, DTS_BUF_SUPPORT = 0, 1, 2
+
+# every symbol declared in include/dts.h
+ABI_FUNCTIONS = ["dts_create", "dts_solve", "dts_destroy", "dts_status_string", "dts_last_error_string",
+                 "dts_solve_ex", "dts_debug_read", "dts_profile_enable", "dts_profile_read",
+                 "dts_launch_count", "dts_version"]
+
+
+class DTSError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        self.status = status
+        msg = f"{where}: {dts_status_string(status)}"
+        if detail:
+            msg += f" ({detail})"
+        super().__init__(msg)
+
+
+class SolveOpts(ctypes.Structure):
+    _fields_ = [("step", ctypes.c_float), ("support_mode", ctypes.c_int32), ("check_inputs", ctypes.c_int32)]
+
+
+class KernelStat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_int64), ("total_ms", ctypes.c_double),
+                ("bytes_per_launch", ctypes.c_double)]
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libdts_b200.so (raises DTSError-like RuntimeError if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise RuntimeError(f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                           f"g.build()'` (there is no CPU fallback)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
+    lib.dts_create.argtypes = [vp, i64, i64, i32, f32, f32, i32, vp, ctypes.POINTER(vp)]
+    lib.dts_create.restype = ctypes.c_int
+    lib.dts_solve.argtypes = [vp, vp, i32, vp, f32, i32, vp, vp]
+    lib.dts_solve.restype = ctypes.c_int
+    lib.dts_solve_ex.argtypes = [vp, vp, i32, vp, f32, i32, vp, vp, ctypes.POINTER(SolveOpts)]
+    lib.dts_solve_ex.restype = ctypes.c_int
+    lib.dts_destroy.argtypes = [vp]
+    lib.dts_destroy.restype = None
+    lib.dts_status_string.argtypes = [ctypes.c_int]
+    lib.dts_status_string.restype = ctypes.c_char_p
+    lib.dts_last_error_string.argtypes = []
+    lib.dts_last_error_string.restype = ctypes.c_char_p
+    lib.dts_debug_read.argtypes = [vp, ctypes.c_int, vp]
+    lib.dts_debug_read.restype = ctypes.c_int
+    lib.dts_profile_enable.argtypes = [vp, i32]
+    lib.dts_profile_enable.restype = ctypes.c_int
+    lib.dts_profile_read.argtypes = [vp, ctypes.POINTER(KernelStat), i32, ctypes.POINTER(i32)]
+    lib.dts_profile_read.restype = ctypes.c_int
+    lib.dts_launch_count.argtypes = [vp]
+    lib.dts_launch_count.restype = i64
+    lib.dts_version.argtypes = []
+    lib.dts_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def dts_status_string(status: int) -> str:
+    return load_library().dts_status_string(int(status)).decode()
+
+
+def dts_version() -> str:
+    return load_library().dts_version().decode()
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise DTSError(st, where, load_library().dts_last_error_string().decode())
+
+
+def _ptr(a, name: str):
+    """Device or host address of a float32 C-contiguous torch tensor / numpy array."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]:
+            raise TypeError(f"{name} must be a C-contiguous float32 array")
+        return a.ctypes.data
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(a, torch.Tensor):
+        if a.dtype != torch.float32 or not a.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous float32 tensor")
+        return a.data_ptr()
+    raise TypeError(f"{name}: unsupported array type {type(a)}")
+
+
+def _stream(stream, *arrays):
+    if stream is not None:
+        return int(stream) if not hasattr(stream, "cuda_stream") else int(stream.cuda_stream)
+    try:
+        import torch
+        if torch.cuda.is_available() and any(getattr(a, "is_cuda", False) for a in arrays):
+            return int(torch.cuda.current_stream().cuda_stream)
+    except ImportError:  # pragma: no cover
+        pass
+    return 0
+
+
+def dts_create(guide, sigma_s: float, sigma_r: float, filter_passes: int = 3, stream=None) -> int:
+    """guide: H x W x C float32 (HWC).  Returns an opaque context handle (int)."""
+    if len(guide.shape) == 2:
+        H, W = guide.shape
+        C = 1
+    else:
+        H, W, C = guide.shape
+    ctx = ctypes.c_void_p()
+    st = load_library().dts_create(_ptr(guide, "guide"), H, W, C, sigma_s, sigma_r, filter_passes,
+                                   _stream(stream, guide), ctypes.byref(ctx))
+    _check(st, "dts_create")
+    return ctx.value
+
+
+def dts_solve_ex(ctx: int, target, confidence, lam: float, iterations: int, out, stream=None,
+                 step: float = 0.0, support_mode: int = 0, check_inputs: bool = False):
+    Ct = 1 if len(target.shape) == 2 else int(target.shape[2])
+    opts = SolveOpts(step, support_mode, 1 if check_inputs else 0)
+    st = load_library().dts_solve_ex(ctx, _ptr(target, "target"), Ct, _ptr(confidence, "confidence"), lam,
+                                     iterations, _ptr(out, "out"), _stream(stream, target, confidence, out),
+                                     ctypes.byref(opts))
+    _check(st, "dts_solve_ex")
+    return out
+
+
+def dts_solve(ctx: int, target, confidence, lam: float, iterations: int, out, stream=None):
+    """target: H x W (x Ct) float32 HWC; confidence: H x W; out like target (written)."""
+    Ct = 1 if len(target.shape) == 2 else int(target.shape[2])
+    st = load_library().dts_solve(ctx, _ptr(target, "target"), Ct, _ptr(confidence, "confidence"), lam,
+                                  iterations, _ptr(out, "out"), _stream(stream, target, confidence, out))
+    _check(st, "dts_solve")
+    return out
+
+
+def dts_destroy(ctx: int) -> None:
+    if ctx:
+        load_library().dts_destroy(ctx)
+
+
+def dts_debug_read(ctx: int, which: int, H: int, W: int) -> np.ndarray:
+    out = np.empty((H, W), np.float32)
+    _check(load_library().dts_debug_read(ctx, which, out.ctypes.data), "dts_debug_read")
+    return out
+
+
+def dts_profile_enable(ctx: int, on: bool = True) -> None:
+    _check(load_library().dts_profile_enable(ctx, 1 if on else 0), "dts_profile_enable")
+
+
+def dts_profile_read(ctx: int):
+    """{family: {"launches", "total_ms", "bytes_per_launch", "avg_ms"}}"""
+    arr = (KernelStat * 16)()
+    n = ctypes.c_int32(0)
+    _check(load_library().dts_profile_read(ctx, arr, 16, ctypes.byref(n)), "dts_profile_read")
+    res = {}
+    for i in range(min(n.value, 16)):
+        k = arr[i]
+        res[k.name.decode()] = {"launches": int(k.launches), "total_ms": float(k.total_ms),
+                                "bytes_per_launch": float(k.bytes_per_launch),
+                                "avg_ms": float(k.total_ms) / k.launches if k.launches else 0.0}
+    return res
+
+
+def dts_launch_count(ctx: int) -> int:
+    return int(load_library().dts_launch_count(ctx))
+
+
+class Solver:
+    """Thin RAII wrapper: ``Solver(guide, sigma_s, sigma_r, N).solve(t, c, lam, iters)``."""
+
+    def __init__(self, guide, sigma_s: float, sigma_r: float, filter_passes: int = 3, stream=None):
+        self.H, self.W = int(guide.shape[0]), int(guide.shape[1])
+        self.ctx = dts_create(guide, sigma_s, sigma_r, filter_passes, stream)
+
+    def solve(self, target, confidence, lam: float, iterations: int, out=None, stream=None, **opts):
+        if out is None:
+            if isinstance(target, np.ndarray):
+                out = np.empty_like(target)
+            else:
+                import torch
+                out = torch.empty_like(target)
+        if opts:
+            return dts_solve_ex(self.ctx, target, confidence, lam, iterations, out, stream, **opts)
+        return dts_solve(self.ctx, target, confidence, lam, iterations, out, stream)
+
+    def read(self, which: int) -> np.ndarray:
+        return dts_debug_read(self.ctx, which, self.H, self.W)
+
+    def close(self):
+        if self.ctx:
+            dts_destroy(self.ctx)
+            self.ctx = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,511 @@
+// dts_capi.cu -- the C ABI declared in include/dts.h: context lifetime, argument
+// validation, host/device staging and the per-iteration launch sequence.
+//
+// Solve loop, for k = 0 .. iterations-1 and passes i = 1..N:
+//     K2 row pass i      X <- RF_rows(i == 1 ? Z : X, a_i^{d_x})
+//     K3 col pass i      X <- RF_cols(X, a_i^{d_y})                       (i < N)
+//     K4 col pass N      Z <- Z - step [lambda (Z - RF_cols(X)) + chat (Z - T)]   (-> out on the last k)
+// (readings R4-R12.)
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dts.h"
+#include "dts_launch.h"
+
+using namespace dts;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct ProfFamily {
+    std::string name;
+    double bytes_per_launch = 0;
+    int64_t launches = 0;
+    double total_ms = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+};
+
+dts_status cuda_fail(cudaError_t e) {
+    g_last_error = cudaGetErrorString(e);
+    if (e == cudaErrorMemoryAllocation) return DTS_E_OOM;
+    return DTS_E_CUDA;
+}
+
+bool finite_pos(float v) { return std::isfinite(v) && v > 0.f; }
+
+enum PtrKind { PTR_DEVICE, PTR_HOST, PTR_BAD };
+
+PtrKind classify(const void* p, int device) {
+    if (!p) return PTR_BAD;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return PTR_HOST;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+        if (a.type == cudaMemoryTypeDevice && a.device != device) return PTR_BAD;
+        return PTR_DEVICE;
+    }
+    return PTR_HOST;
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+    const char* pa = static_cast<const char*>(a);
+    const char* pb = static_cast<const char*>(b);
+    return pa < pb + nb && pb < pa + na;
+}
+
+std::once_flag g_pool_once;
+
+}  // namespace
+
+struct dts_ctx {
+    int device = 0;
+    int num_sms = 148;
+    Geometry g{};
+    int C = 0;
+    float sigma_s = 0, sigma_r = 0;
+    int N = 0;
+    std::vector<float> kc;  // per pass: sqrt(2) * log2(e) / sigma_i
+    float ks = 0;           // support: sqrt(2) * log2(e) / sigma_s
+    float* dx = nullptr;
+    float* dy = nullptr;
+    float* S = nullptr;
+    // solver state (allocated for ct_cap target channels)
+    int ct_cap = 0;
+    float* Z = nullptr;
+    float* T = nullptr;
+    float* X = nullptr;
+    float* chat = nullptr;
+    // host staging (device buffers holding host inputs / outputs)
+    float* st_t = nullptr;
+    float* st_c = nullptr;
+    float* st_o = nullptr;
+    size_t st_bytes = 0;
+    unsigned int* counters = nullptr;
+    cudaStream_t last_stream = nullptr;
+    int64_t launches = 0;
+};
+
+namespace {
+
+enum Family { F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_COUNT };
+const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update",
+                                     "support_row", "support_col", "prologue"};
+
+// Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
+// and go inside a timed step, the statistics outlive them.
+struct Profiler {
+    std::mutex mu;
+    bool on = false;
+    std::vector<ProfFamily> fam;
+    std::vector<cudaEvent_t> pool;
+    Profiler() {
+        fam.resize(F_COUNT);
+        for (int i = 0; i < F_COUNT; ++i) fam[i].name = kFamilyNames[i];
+    }
+    cudaEvent_t take() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+    // resolve pending event pairs (caller synchronised the device)
+    void resolve() {
+        for (auto& f : fam) {
+            for (auto& pr : f.pending) {
+                float ms = 0.f;
+                if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) {
+                    f.total_ms += ms;
+                    ++f.launches;
+                }
+                pool.push_back(pr.first);
+                pool.push_back(pr.second);
+            }
+            f.pending.clear();
+        }
+    }
+};
+Profiler& profiler() {
+    static Profiler* p = new Profiler();  // never destroyed: events may outlive contexts
+    return *p;
+}
+
+// Every kernel launch goes through here: counts it and, when profiling, brackets it
+// with events on the launch stream.
+template <typename F>
+dts_status run_launch(dts_ctx* ctx, int fam, double bytes, cudaStream_t s, F&& launch) {
+    Profiler& P = profiler();
+    const bool prof = P.on;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (prof) {
+        std::lock_guard<std::mutex> lk(P.mu);
+        e0 = P.take();
+        e1 = P.take();
+        cudaEventRecord(e0, s);
+    }
+    cudaError_t e = launch();
+    if (e != cudaSuccess) return cuda_fail(e);
+    ++ctx->launches;
+    if (prof) {
+        std::lock_guard<std::mutex> lk(P.mu);
+        cudaEventRecord(e1, s);
+        ProfFamily& f = P.fam[fam];
+        f.bytes_per_launch = bytes;
+        f.pending.emplace_back(e0, e1);
+    }
+    return DTS_OK;
+}
+
+void free_solver_state(dts_ctx* ctx, cudaStream_t s) {
+    for (float** p : {&ctx->Z, &ctx->T, &ctx->X, &ctx->chat}) {
+        if (*p) cudaFreeAsync(*p, s);
+        *p = nullptr;
+    }
+    ctx->ct_cap = 0;
+}
+
+dts_status ensure_solver_state(dts_ctx* ctx, int Ct, cudaStream_t s) {
+    if (ctx->ct_cap >= Ct && ctx->chat) return DTS_OK;
+    free_solver_state(ctx, s);
+    const size_t plane = (size_t)ctx->g.plane * sizeof(float);
+    cudaError_t e;
+    if ((e = cudaMallocAsync((void**)&ctx->Z, plane * Ct, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMallocAsync((void**)&ctx->T, plane * Ct, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMallocAsync((void**)&ctx->X, plane * Ct, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMallocAsync((void**)&ctx->chat, plane, s)) != cudaSuccess) return cuda_fail(e);
+    ctx->ct_cap = Ct;
+    return DTS_OK;
+}
+
+dts_status ensure_staging(dts_ctx* ctx, size_t bytes_per_image, cudaStream_t s) {
+    if (ctx->st_bytes >= bytes_per_image) return DTS_OK;
+    for (float** p : {&ctx->st_t, &ctx->st_c, &ctx->st_o}) {
+        if (*p) cudaFreeAsync(*p, s);
+        *p = nullptr;
+    }
+    cudaError_t e;
+    if ((e = cudaMallocAsync((void**)&ctx->st_t, bytes_per_image, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMallocAsync((void**)&ctx->st_c, bytes_per_image, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMallocAsync((void**)&ctx->st_o, bytes_per_image, s)) != cudaSuccess) return cuda_fail(e);
+    ctx->st_bytes = bytes_per_image;
+    return DTS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dts_version(void) { return "dts-b200 0.1 (sm_100a)"; }
+
+const char* dts_status_string(dts_status s) {
+    switch (s) {
+        case DTS_OK: return "DTS_OK";
+        case DTS_E_ARG: return "DTS_E_ARG: invalid argument";
+        case DTS_E_SHAPE: return "DTS_E_SHAPE: unsupported size";
+        case DTS_E_NONFINITE: return "DTS_E_NONFINITE: non-finite input";
+        case DTS_E_RANGE: return "DTS_E_RANGE: confidence outside [0, 1]";
+        case DTS_E_CUDA: return "DTS_E_CUDA: CUDA error";
+        case DTS_E_NCCL: return "DTS_E_NCCL: collective error";
+        case DTS_E_OOM: return "DTS_E_OOM: out of memory";
+    }
+    return "unknown dts_status";
+}
+
+const char* dts_last_error_string(void) { return g_last_error.c_str(); }
+
+dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float sigma_s, float sigma_r,
+                      int32_t filter_passes, void* stream, dts_ctx** out_ctx) {
+    if (!out_ctx || !guide) return DTS_E_ARG;
+    *out_ctx = nullptr;
+    if (H < 1 || W < 1 || C < 1) return DTS_E_ARG;
+    if (!finite_pos(sigma_s) || !finite_pos(sigma_r)) return DTS_E_ARG;
+    if (filter_passes < 1 || filter_passes > 16) return DTS_E_ARG;
+    if (W > 18432 || H > (int64_t)1 << 30 || C > 4096) return DTS_E_SHAPE;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+    int device = 0;
+    cudaError_t e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return cuda_fail(e);
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    if (major < 10) {
+        g_last_error = "device is not sm_100-class";
+        return DTS_E_CUDA;
+    }
+    std::call_once(g_pool_once, [device]() {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;  // keep freed blocks cached: create/destroy cycles do not hit the driver
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+
+    dts_ctx* ctx = new dts_ctx();
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->g.H = H;
+    ctx->g.W = W;
+    ctx->g.pitch = (W + 31) / 32 * 32;
+    ctx->g.plane = H * ctx->g.pitch;
+    ctx->C = C;
+    ctx->sigma_s = sigma_s;
+    ctx->sigma_r = sigma_r;
+    ctx->N = filter_passes;
+    // R5: sigma_i = sigma_s sqrt(3) 2^(N-i) / sqrt(4^N - 1); coefficient a_i^d = 2^(-kc_i d)
+    const double log2e = 1.4426950408889634, sqrt2 = 1.4142135623730951;
+    const double denom = std::sqrt(std::pow(4.0, filter_passes) - 1.0);
+    for (int i = 1; i <= filter_passes; ++i) {
+        const double sig = sigma_s * std::sqrt(3.0) * std::pow(2.0, filter_passes - i) / denom;
+        ctx->kc.push_back((float)(sqrt2 * log2e / sig));
+    }
+    ctx->ks = (float)(sqrt2 * log2e / sigma_s);
+
+    // plans (validate that this build supports the shape before allocating)
+    RowPlan rp;
+    ColPlan cp;
+    if (plan_row_pass(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &rp) != cudaSuccess ||
+        plan_col_pass(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &cp) != cudaSuccess) {
+        delete ctx;
+        return DTS_E_SHAPE;
+    }
+
+    const size_t plane = (size_t)ctx->g.plane * sizeof(float);
+    dts_status st = DTS_OK;
+    const float* gdev = guide;
+    float* gstage = nullptr;
+    PtrKind gk = classify(guide, device);
+    if (gk == PTR_BAD) {
+        delete ctx;
+        return DTS_E_ARG;
+    }
+    if ((e = cudaMallocAsync((void**)&ctx->dx, plane, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->dy, plane, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->S, plane, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->counters, 2 * sizeof(unsigned int), s)) != cudaSuccess) {
+        st = cuda_fail(e);
+        dts_destroy(ctx);
+        return st;
+    }
+    const size_t gbytes = (size_t)H * W * C * sizeof(float);
+    if (gk == PTR_HOST) {
+        if ((e = cudaMallocAsync((void**)&gstage, gbytes, s)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(gstage, guide, gbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
+            st = cuda_fail(e);
+            if (gstage) cudaFreeAsync(gstage, s);
+            dts_destroy(ctx);
+            return st;
+        }
+        gdev = gstage;
+    }
+    const float ratio = sigma_s / sigma_r;
+    const double px = (double)H * W;
+    st = run_launch(ctx, F_DERIV, px * (4.0 * C + 8.0), s,
+                    [&] { return launch_guide_deriv(gdev, C, ratio * ratio, ctx->g, ctx->dx, ctx->dy, s); });
+    if (st == DTS_OK)
+        st = run_launch(ctx, F_SUPPORT_ROW, px * 8.0, s, [&] {
+            return launch_row_pass(rp, ctx->g, 1, MODE_SUPPORT, nullptr, ctx->S, ctx->dx, ctx->ks, s);
+        });
+    if (st == DTS_OK)
+        st = run_launch(ctx, F_SUPPORT_COL, px * 12.0, s, [&] {
+            return launch_col_pass(cp, ctx->g, 1, MODE_SUPPORT, nullptr, ctx->dy, ctx->ks, nullptr, ctx->S, s);
+        });
+    if (gstage) {
+        cudaFreeAsync(gstage, s);
+        if (st == DTS_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess) st = cuda_fail(e);
+    }
+    if (st != DTS_OK) {
+        dts_destroy(ctx);
+        return st;
+    }
+    ctx->last_stream = s;
+    *out_ctx = ctx;
+    return DTS_OK;
+}
+
+dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const float* confidence, float lambda,
+                        int32_t iterations, float* out, void* stream, const dts_solve_opts* opts) {
+    if (!ctx || !target || !confidence || !out) return DTS_E_ARG;
+    if (Ct < 1) return DTS_E_ARG;
+    if (Ct > 4) return DTS_E_SHAPE;
+    if (iterations < 0) return DTS_E_ARG;
+    const float step = (opts && opts->step > 0.f) ? opts->step : 0.99f;
+    const int support_mode = opts ? opts->support_mode : 0;
+    if (support_mode != 0 && support_mode != 1) return DTS_E_ARG;
+    if (!std::isfinite(lambda) || lambda < 0.f || !std::isfinite(step)) return DTS_E_ARG;
+    if (step * (lambda + 1.f) >= 2.f) return DTS_E_ARG;  // descent stability
+    const Geometry& g = ctx->g;
+    const size_t img = (size_t)g.H * g.W * Ct * sizeof(float);
+    const size_t cb = (size_t)g.H * g.W * sizeof(float);
+    if (overlaps(out, img, target, img) || overlaps(out, img, confidence, cb)) return DTS_E_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->last_stream = s;
+
+    RowPlan rp;
+    ColPlan cpf, cpu;
+    if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess ||
+        plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf) != cudaSuccess ||
+        plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu) != cudaSuccess)
+        return DTS_E_SHAPE;
+
+    const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),
+                  ko = classify(out, ctx->device);
+    if (kt == PTR_BAD || kc == PTR_BAD || ko == PTR_BAD) return DTS_E_ARG;
+    const bool any_host = kt == PTR_HOST || kc == PTR_HOST || ko == PTR_HOST;
+    cudaError_t e;
+    dts_status st;
+    if (any_host && (st = ensure_staging(ctx, img, s)) != DTS_OK) return st;
+    const float* t_d = target;
+    const float* c_d = confidence;
+    float* o_d = out;
+    if (kt == PTR_HOST) {
+        if ((e = cudaMemcpyAsync(ctx->st_t, target, img, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+            return cuda_fail(e);
+        t_d = ctx->st_t;
+    }
+    if (kc == PTR_HOST) {
+        if ((e = cudaMemcpyAsync(ctx->st_c, confidence, cb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+            return cuda_fail(e);
+        c_d = ctx->st_c;
+    }
+    if (ko == PTR_HOST) o_d = ctx->st_o;
+
+    if (opts && opts->check_inputs) {
+        unsigned int h[2] = {0, 0};
+        if ((e = cudaMemsetAsync(ctx->counters, 0, sizeof(h), s)) != cudaSuccess) return cuda_fail(e);
+        if ((e = launch_check_inputs(t_d, c_d, Ct, g.H, g.W, ctx->counters, s)) != cudaSuccess) return cuda_fail(e);
+        ++ctx->launches;
+        if ((e = cudaMemcpyAsync(h, ctx->counters, sizeof(h), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(s)) != cudaSuccess)
+            return cuda_fail(e);
+        if (h[0]) return DTS_E_NONFINITE;
+        if (h[1]) return DTS_E_RANGE;
+    }
+
+    if (iterations == 0) {
+        if ((e = cudaMemcpyAsync(o_d, t_d, img, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return cuda_fail(e);
+    } else {
+        if ((st = ensure_solver_state(ctx, Ct, s)) != DTS_OK) return st;
+        const double px = (double)g.H * g.W;
+        st = run_launch(ctx, F_PROLOGUE, px * (12.0 * Ct + 12), s, [&] {
+            return launch_prologue(t_d, c_d, Ct, g, ctx->S, support_mode, ctx->Z, ctx->T, ctx->chat, s);
+        });
+        if (st != DTS_OK) return st;
+        const double row_bytes = px * (8.0 * Ct + 4);
+        const double upd_bytes = px * (16.0 * Ct + 8);  // X, d, Z, T, chat in; Z out
+        for (int k = 0; k < iterations; ++k) {
+            for (int i = 0; i < ctx->N; ++i) {
+                const float* in = (i == 0) ? ctx->Z : ctx->X;
+                st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
+                    return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
+                });
+                if (st != DTS_OK) return st;
+                if (i + 1 < ctx->N) {
+                    st = run_launch(ctx, F_COL, row_bytes, s, [&] {
+                        return launch_col_pass(cpf, g, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr,
+                                               nullptr, s);
+                    });
+                } else {
+                    UpdateArgs u;
+                    u.Z = ctx->Z;
+                    u.T = ctx->T;
+                    u.chat = ctx->chat;
+                    u.lam = lambda;
+                    u.step = step;
+                    u.out_hwc = (k + 1 == iterations) ? o_d : nullptr;
+                    st = run_launch(ctx, F_UPDATE, upd_bytes, s, [&] {
+                        return launch_col_pass(cpu, g, Ct, MODE_UPDATE, ctx->X, ctx->dy, ctx->kc[i], &u, nullptr,
+                                               s);
+                    });
+                }
+                if (st != DTS_OK) return st;
+            }
+        }
+    }
+    if (ko == PTR_HOST) {
+        if ((e = cudaMemcpyAsync(out, o_d, img, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return cuda_fail(e);
+    }
+    if (any_host) {
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e);
+    }
+    return DTS_OK;
+}
+
+dts_status dts_solve(dts_ctx* ctx, const float* target, int32_t target_channels, const float* confidence,
+                     float lambda, int32_t iterations, float* out, void* stream) {
+    return dts_solve_ex(ctx, target, target_channels, confidence, lambda, iterations, out, stream, nullptr);
+}
+
+void dts_destroy(dts_ctx* ctx) {
+    if (!ctx) return;
+    cudaStream_t s = ctx->last_stream;
+    free_solver_state(ctx, s);
+    for (float** p : {&ctx->dx, &ctx->dy, &ctx->S, &ctx->st_t, &ctx->st_c, &ctx->st_o}) {
+        if (*p) cudaFreeAsync(*p, s);
+        *p = nullptr;
+    }
+    if (ctx->counters) cudaFreeAsync(ctx->counters, s);
+    delete ctx;
+}
+
+dts_status dts_debug_read(dts_ctx* ctx, dts_buffer which, float* host_out) {
+    if (!ctx || !host_out) return DTS_E_ARG;
+    const float* src = which == DTS_BUF_DX ? ctx->dx : which == DTS_BUF_DY ? ctx->dy
+                     : which == DTS_BUF_SUPPORT ? ctx->S : nullptr;
+    if (!src) return DTS_E_ARG;
+    cudaError_t e = cudaMemcpy2DAsync(host_out, ctx->g.W * sizeof(float), src, ctx->g.pitch * sizeof(float),
+                                      ctx->g.W * sizeof(float), ctx->g.H, cudaMemcpyDeviceToHost, ctx->last_stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->last_stream);
+    return e == cudaSuccess ? DTS_OK : cuda_fail(e);
+}
+
+dts_status dts_profile_enable(dts_ctx* ctx, int32_t on) {
+    (void)ctx;  // the profiler is process-wide
+    Profiler& P = profiler();
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e);
+    std::lock_guard<std::mutex> lk(P.mu);
+    P.resolve();
+    for (auto& f : P.fam) {  // (re)starting resets the statistics
+        f.launches = 0;
+        f.total_ms = 0;
+    }
+    P.on = on != 0;
+    return DTS_OK;
+}
+
+dts_status dts_profile_read(dts_ctx* ctx, dts_kernel_stat* out, int32_t max, int32_t* count) {
+    (void)ctx;
+    Profiler& P = profiler();
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e);
+    std::lock_guard<std::mutex> lk(P.mu);
+    P.resolve();
+    int n = 0;
+    for (auto& f : P.fam) {
+        if (out && n < max) {
+            std::memset(&out[n], 0, sizeof(dts_kernel_stat));
+            std::strncpy(out[n].name, f.name.c_str(), sizeof(out[n].name) - 1);
+            out[n].launches = f.launches;
+            out[n].total_ms = f.total_ms;
+            out[n].bytes_per_launch = f.bytes_per_launch;
+        }
+        ++n;
+    }
+    if (count) *count = n;
+    return DTS_OK;
+}
+
+int64_t dts_launch_count(const dts_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

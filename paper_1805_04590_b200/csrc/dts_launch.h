@@ -1,0 +1,56 @@
+// dts_launch.h -- host-side launchers of the sm_100a kernels (internal to libdts_b200.so).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dts {
+
+enum PassMode : int { MODE_FILTER = 0, MODE_UPDATE = 1, MODE_SUPPORT = 2 };
+
+// Internal planar layout: every H x W plane has row pitch `pitch` floats (a multiple
+// of 32, so every row starts 128-B aligned); channel planes are `plane` floats apart.
+struct Geometry {
+    int64_t H, W, pitch, plane;
+};
+
+// K1: domain distances from the HWC guide (Eqs. 8-9; R1, R2).
+cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Geometry& g, float* dx, float* dy,
+                               cudaStream_t s);
+
+// K2: recursive-filter row pass (causal + anticausal, fused), FILTER or SUPPORT mode.
+struct RowPlan {
+    int L, G, R, threads, grid, nbuf;
+    size_t smem;
+    int64_t rowstride;
+};
+cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowPlan* plan);
+cudaError_t launch_row_pass(const RowPlan& plan, const Geometry& g, int Ct, int mode, const float* in, float* out,
+                            const float* d, float kc, cudaStream_t s);
+
+// K3/K4: recursive-filter column pass (cluster-resident two-level scan), FILTER,
+// UPDATE (fused solver step, Eq. 3) or SUPPORT mode.
+struct ColPlan {
+    int TW, CB, HB, S, Ls, threads;
+    dim3 grid;
+    size_t smem;
+};
+struct UpdateArgs {
+    float* Z;            // planar state (read; written unless out_hwc)
+    const float* T;      // planar target
+    const float* chat;   // c / S
+    float lam, step;
+    float* out_hwc;      // when non-null: write the result here (H x W x Ct) instead of Z
+};
+cudaError_t plan_col_pass(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
+cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
+                            float kc, const UpdateArgs* upd, float* support, cudaStream_t s);
+
+// K6: solve prologue -- planar Z = T = target, chat = c / S (or c when support_mode = 1).
+cudaError_t launch_prologue(const float* target, const float* conf, int Ct, const Geometry& g, const float* S,
+                            int support_mode, float* Z, float* T, float* chat, cudaStream_t s);
+
+// optional input checks: counts non-finite target/confidence values and confidences outside [0, 1]
+cudaError_t launch_check_inputs(const float* target, const float* conf, int Ct, int64_t H, int64_t W,
+                                unsigned int* counters, cudaStream_t s);
+
+}  // namespace dts

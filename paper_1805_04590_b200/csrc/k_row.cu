@@ -1,0 +1,367 @@
+// k_row.cu -- K2: one recursive-filter pass along every row (sm_100a).
+//
+// Computes, for each row of every channel plane, the domain-transform recursive
+// filter of BASELINE.json's north star / DESIGN.md R4:
+//     causal      y[0] = x[0],       y[k] = (1 - A[k]) x[k] + A[k] y[k-1]
+//     anticausal  z[W-1] = y[W-1],   z[k] = (1 - A[k+1]) y[k] + A[k+1] z[k+1]
+// with A[k] = a_i^{d_x[k]} = 2^(-kc d_x[k]) (R5), A = 0 at the +inf sentinel.
+// SUPPORT mode computes the unnormalised two-sided sums of R7 instead:
+//     P[k] = 1 + A[k] P[k-1],  Q[k] = 1 + A[k+1] Q[k+1],  s_x = P + Q - 1.
+//
+// Design: each row is one linear-recurrence scan.  A group of G
+// threads owns a row; thread t keeps L consecutive samples in registers, folds
+// them into an affine map, the G maps are combined by a shuffle (+ smem across
+// warps) scan, and the thread re-applies its chunk with the exact carry -- causal
+// and anticausal fused in one kernel, so a row is read once and written once.
+// Rows are staged with TMA bulk copies (cp.async.bulk) into a double buffer by a
+// persistent CTA: the next row group streams in while the current one computes,
+// and results leave through bulk shared->global stores.
+#include "dts_device.cuh"
+#include "dts_launch.h"
+
+namespace dts {
+
+struct RowParams {
+    const float* in;
+    float* out;
+    const float* d;
+    int64_t plane, pitch, rowstride;
+    int H, W, G, R, nbuf;
+    float kc;
+};
+
+// Exclusive scan of affine maps over the G threads of a row group, in thread order
+// (REV = false) or reverse thread order (REV = true).  Must be called by every
+// thread of the CTA (contains __syncthreads when G > 32).
+template <int NV, bool REV>
+__device__ __forceinline__ Aff<NV> group_exclusive_scan(Aff<NV> v, int t, int G, float* scratch) {
+    const int lane = threadIdx.x & 31;
+    const int width = G < 32 ? G : 32;
+    const int li = lane & (width - 1);
+    const int pos = REV ? (width - 1 - li) : li;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        if (off >= width) break;
+        Aff<NV> e;
+        e.P = REV ? __shfl_down_sync(FULL, v.P, off, width) : __shfl_up_sync(FULL, v.P, off, width);
+#pragma unroll
+        for (int c = 0; c < NV; ++c)
+            e.B[c] = REV ? __shfl_down_sync(FULL, v.B[c], off, width) : __shfl_up_sync(FULL, v.B[c], off, width);
+        if (pos >= off) v = aff_compose(e, v);
+    }
+    // inclusive -> exclusive within the warp segment
+    Aff<NV> ex;
+    ex.P = REV ? __shfl_down_sync(FULL, v.P, 1, width) : __shfl_up_sync(FULL, v.P, 1, width);
+#pragma unroll
+    for (int c = 0; c < NV; ++c)
+        ex.B[c] = REV ? __shfl_down_sync(FULL, v.B[c], 1, width) : __shfl_up_sync(FULL, v.B[c], 1, width);
+    if (pos == 0) ex = aff_identity<NV>();
+    if (G <= 32) return ex;
+
+    // cross-warp: warp totals through shared memory (one row group per CTA when G > 32)
+    const int nw = G >> 5;
+    const int w = t >> 5;
+    scratch += (threadIdx.x / G) * nw * (NV + 1);  // this row group's slots
+    if (pos == 31) {
+        scratch[w * (NV + 1)] = v.P;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) scratch[w * (NV + 1) + 1 + c] = v.B[c];
+    }
+    __syncthreads();
+    Aff<NV> pre = aff_identity<NV>();
+    if (!REV) {
+        for (int k = 0; k < w; ++k) {
+            Aff<NV> e;
+            e.P = scratch[k * (NV + 1)];
+#pragma unroll
+            for (int c = 0; c < NV; ++c) e.B[c] = scratch[k * (NV + 1) + 1 + c];
+            pre = aff_compose(pre, e);
+        }
+    } else {
+        for (int k = nw - 1; k > w; --k) {
+            Aff<NV> e;
+            e.P = scratch[k * (NV + 1)];
+#pragma unroll
+            for (int c = 0; c < NV; ++c) e.B[c] = scratch[k * (NV + 1) + 1 + c];
+            pre = aff_compose(pre, e);
+        }
+    }
+    __syncthreads();  // scratch is reused by the next scan
+    return aff_compose(pre, ex);
+}
+
+template <int L, int CT, int MODE>
+__global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
+    static_assert(L % 4 == 0, "L must be a multiple of 4 (float4 smem reads)");
+    constexpr int NX = (MODE == MODE_SUPPORT) ? 0 : CT;  // input planes
+    constexpr int NSLOT = 1 + (MODE == MODE_SUPPORT ? 1 : CT);
+    constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
+
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+
+    const int G = p.G, R = p.R;
+    const int rs = threadIdx.x / G;
+    const int t = threadIdx.x - rs * G;
+    const int64_t bufFloats = (int64_t)R * NSLOT * p.rowstride;
+    float* scratch = smem + p.nbuf * bufFloats;  // cross-warp scan scratch (32 * (NV+1) floats)
+    const uint32_t rowBytes = (uint32_t)(p.pitch * sizeof(float));
+    const int ngroups = (p.H + R - 1) / R;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](int grp, int b) {
+        float* buf = smem + b * bufFloats;
+        uint32_t bytes = 0;
+        for (int q = 0; q < R; ++q)
+            if (grp * R + q < p.H) bytes += rowBytes * (1 + NX);
+        mbar_arrive_expect_tx(&bar[b], bytes);
+        for (int q = 0; q < R; ++q) {
+            const int64_t r = (int64_t)grp * R + q;
+            if (r >= p.H) break;
+            bulk_g2s(buf + (q * NSLOT) * p.rowstride, p.d + r * p.pitch, rowBytes, &bar[b]);
+#pragma unroll
+            for (int c = 0; c < NX; ++c)
+                bulk_g2s(buf + (q * NSLOT + 1 + c) * p.rowstride, p.in + c * p.plane + r * p.pitch, rowBytes,
+                         &bar[b]);
+        }
+    };
+
+    int grp = blockIdx.x;
+    if (grp < ngroups && threadIdx.x == 0) issue(grp, 0);
+
+    const bool dbl = p.nbuf == 2;
+    for (int it = 0; grp < ngroups; grp += gridDim.x, ++it) {
+        const int b = dbl ? (it & 1) : 0;
+        const int nxt = grp + gridDim.x;
+        if (dbl && threadIdx.x == 0 && nxt < ngroups) {
+            bulk_wait_read0();  // stores issued from buffer b^1 have read their smem
+            issue(nxt, b ^ 1);
+        }
+        mbar_wait(&bar[b], (uint32_t)(dbl ? ((it >> 1) & 1) : (it & 1)));
+
+        float* row = smem + b * bufFloats + (int64_t)rs * NSLOT * p.rowstride;
+        const int k0 = t * L;
+
+        // ---- load chunk: coefficients A and samples x (masked beyond W) ----
+        float A[L];
+        float x[NV][L];
+#pragma unroll
+        for (int j4 = 0; j4 < L; j4 += 4) {
+            float4 dv = *reinterpret_cast<const float4*>(row + k0 + j4);
+            float dd[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = k0 + j4 + u;
+                A[j4 + u] = (k < p.W) ? coef_from_d(dd[u], p.kc) : 0.f;
+            }
+            if constexpr (MODE != MODE_SUPPORT) {
+#pragma unroll
+                for (int c = 0; c < CT; ++c) {
+                    float4 xv = *reinterpret_cast<const float4*>(row + (1 + c) * p.rowstride + k0 + j4);
+                    float xx[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) x[c][j4 + u] = (k0 + j4 + u < p.W) ? xx[u] : 0.f;
+                }
+            }
+        }
+        // coefficient linking this chunk's last sample to the next chunk's first
+        const int kn = k0 + L;
+        const float Anext = (kn < p.W) ? coef_from_d(row[kn], p.kc) : 0.f;
+
+        // ---- causal: fold, scan, apply ----
+        Aff<NV> m = aff_identity<NV>();
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            m.P *= A[j];
+#pragma unroll
+            for (int c = 0; c < NV; ++c) {
+                if constexpr (MODE == MODE_SUPPORT) m.B[c] = fmaf(A[j], m.B[c], 1.f);
+                else m.B[c] = fmaf(A[j], m.B[c] - x[c][j], x[c][j]);
+            }
+        }
+        Aff<NV> ex = group_exclusive_scan<NV, false>(m, t, G, scratch);
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            float y = ex.B[c];
+#pragma unroll
+            for (int j = 0; j < L; ++j) {
+                if constexpr (MODE == MODE_SUPPORT) y = fmaf(A[j], y, 1.f);
+                else y = fmaf(A[j], y - x[c][j], x[c][j]);
+                x[c][j] = y;  // x now holds y (SUPPORT: holds P)
+            }
+        }
+
+        // ---- anticausal: fold (right to left), reverse scan, apply ----
+        m = aff_identity<NV>();
+#pragma unroll
+        for (int j = L - 1; j >= 0; --j) {
+            const float a = (j == L - 1) ? Anext : A[j + 1];
+            m.P *= a;
+#pragma unroll
+            for (int c = 0; c < NV; ++c) {
+                if constexpr (MODE == MODE_SUPPORT) m.B[c] = fmaf(a, m.B[c], 1.f);
+                else m.B[c] = fmaf(a, m.B[c] - x[c][j], x[c][j]);
+            }
+        }
+        ex = group_exclusive_scan<NV, true>(m, t, G, scratch);
+
+        float* orow = row + p.rowstride;  // output slot(s)
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            float z = ex.B[c];
+            float o[L];
+#pragma unroll
+            for (int j = L - 1; j >= 0; --j) {
+                const float a = (j == L - 1) ? Anext : A[j + 1];
+                if constexpr (MODE == MODE_SUPPORT) {
+                    z = fmaf(a, z, 1.f);
+                    o[j] = x[c][j] + z - 1.f;  // s = P + Q - 1
+                } else {
+                    z = fmaf(a, z - x[c][j], x[c][j]);
+                    o[j] = z;
+                }
+            }
+#pragma unroll
+            for (int j4 = 0; j4 < L; j4 += 4)
+                *reinterpret_cast<float4*>(orow + c * p.rowstride + k0 + j4) =
+                    make_float4(o[j4], o[j4 + 1], o[j4 + 2], o[j4 + 3]);
+        }
+
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float* buf = smem + b * bufFloats;
+            for (int q = 0; q < R; ++q) {
+                const int64_t r = (int64_t)grp * R + q;
+                if (r >= p.H) break;
+#pragma unroll
+                for (int c = 0; c < NV; ++c)
+                    bulk_s2g(p.out + c * p.plane + r * p.pitch, buf + (q * NSLOT + 1 + c) * p.rowstride, rowBytes);
+            }
+            bulk_commit();
+            if (!dbl && nxt < ngroups) {  // single buffer: refill once the stores have read it
+                bulk_wait_read0();
+                issue(nxt, 0);
+            }
+        }
+    }
+    if (threadIdx.x == 0) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------------------
+
+static const int kLs[] = {4, 12, 20, 36};
+
+cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowPlan* plan) {
+    const int nslot = 1 + (mode == MODE_SUPPORT ? 1 : Ct);
+    int L = 0, G = 0;
+    for (int cand : kLs) {
+        int64_t need = (g.W + cand - 1) / cand;
+        if (need <= 512) {
+            L = cand;
+            G = (int)need;
+            break;
+        }
+    }
+    if (G == 0) return cudaErrorInvalidValue;  // W > 36 * 512
+    if (G <= 32) {
+        int p2 = 1;
+        while (p2 < G) p2 <<= 1;
+        G = p2;
+    } else {
+        G = (G + 31) / 32 * 32;
+    }
+    int R = G >= 256 ? 1 : 256 / G;
+    if (R > g.H) R = (int)g.H;
+    if (R < 1) R = 1;
+    plan->L = L;
+    plan->G = G;
+    plan->R = R;
+    plan->threads = G * R;
+    int64_t rs = g.pitch > (int64_t)G * L ? g.pitch : (int64_t)G * L;
+    rs = (rs + 3) / 4 * 4;
+    plan->rowstride = rs;
+    plan->nbuf = 2;
+    plan->smem = (size_t)2 * R * nslot * rs * sizeof(float) + 32 * 8 * sizeof(float);
+    if (plan->smem > 227 * 1024) {  // very wide rows: one buffer (no prefetch overlap)
+        plan->nbuf = 1;
+        plan->smem = (size_t)R * nslot * rs * sizeof(float) + 32 * 8 * sizeof(float);
+    }
+    if (plan->smem > 227 * 1024) return cudaErrorInvalidValue;
+    const int64_t ngroups = (g.H + R - 1) / R;
+    int per_sm = 1;
+    // occupancy limited by threads and smem
+    int by_threads = 2048 / plan->threads;
+    int by_smem = (int)((228 * 1024) / (plan->smem + 1024));
+    per_sm = by_threads < by_smem ? by_threads : by_smem;
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)num_sms * per_sm;
+    if (grid > ngroups) grid = ngroups;
+    plan->grid = (int)grid;
+    return cudaSuccess;
+}
+
+template <int L, int CT, int MODE>
+static cudaError_t launch_t(const RowPlan& plan, const RowParams& p, cudaStream_t s) {
+    static size_t configured = 0;  // largest dynamic smem enabled so far for this instantiation
+    if (plan.smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_row_pass<L, CT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)plan.smem);
+        if (e != cudaSuccess) return e;
+        configured = plan.smem;
+    }
+    k_row_pass<L, CT, MODE><<<plan.grid, plan.threads, plan.smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <int L, int MODE>
+static cudaError_t launch_ct(const RowPlan& plan, const RowParams& p, int Ct, cudaStream_t s) {
+    switch (Ct) {
+        case 1: return launch_t<L, 1, MODE>(plan, p, s);
+        case 2: return launch_t<L, 2, MODE>(plan, p, s);
+        case 3: return launch_t<L, 3, MODE>(plan, p, s);
+        case 4: return launch_t<L, 4, MODE>(plan, p, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_row_pass(const RowPlan& plan, const Geometry& g, int Ct, int mode, const float* in, float* out,
+                            const float* d, float kc, cudaStream_t s) {
+    RowParams p;
+    p.in = in;
+    p.out = out;
+    p.d = d;
+    p.plane = g.plane;
+    p.pitch = g.pitch;
+    p.rowstride = plan.rowstride;
+    p.H = (int)g.H;
+    p.W = (int)g.W;
+    p.G = plan.G;
+    p.R = plan.R;
+    p.nbuf = plan.nbuf;
+    p.kc = kc;
+    if (mode == MODE_SUPPORT) {
+        switch (plan.L) {
+            case 4: return launch_t<4, 1, MODE_SUPPORT>(plan, p, s);
+            case 12: return launch_t<12, 1, MODE_SUPPORT>(plan, p, s);
+            case 20: return launch_t<20, 1, MODE_SUPPORT>(plan, p, s);
+            case 36: return launch_t<36, 1, MODE_SUPPORT>(plan, p, s);
+        }
+        return cudaErrorInvalidValue;
+    }
+    switch (plan.L) {
+        case 4: return launch_ct<4, MODE_FILTER>(plan, p, Ct, s);
+        case 12: return launch_ct<12, MODE_FILTER>(plan, p, Ct, s);
+        case 20: return launch_ct<20, MODE_FILTER>(plan, p, Ct, s);
+        case 36: return launch_ct<36, MODE_FILTER>(plan, p, Ct, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace dts

@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by
+element on the same seeded fp32 inputs.  Tolerance (BASELINE.json north star):
+max |gpu - oracle| <= 1e-4 * (max(t) - min(t)) after the full solve (reading R15)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import paper_1805_04590_b200 as dts  # noqa: E402
+from synth import CONFIGS, make_inputs, random_problem, target_range  # noqa: E402
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    torch.cuda.set_device(0)
+
+
+def gpu_solve(g, t, c, ss, sr, N, lam, iters, host=False, **opts):
+    if host:
+        out = np.empty_like(t)
+        with dts.Solver(g, ss, sr, N) as s:
+            s.solve(t, c, lam, iters, out=out, **opts)
+        return out.astype(np.float64)
+    gd, td, cd = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (g, t, c))
+    out = torch.empty_like(td)
+    with dts.Solver(gd, ss, sr, N) as s:
+        s.solve(td, cd, lam, iters, out=out, **opts)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+def check(g, t, c, ss, sr, N, lam, iters, **kw):
+    ref = oracle.solve(g, t, c, ss, sr, N, lam, iters)
+    got = gpu_solve(g, t, c, ss, sr, N, lam, iters, **kw)
+    rng = max(target_range(t), 1e-30)
+    err = float(np.max(np.abs(got - ref))) if got.size else 0.0
+    assert np.all(np.isfinite(got))
+    assert err <= TOL * rng, f"max err {err:.3e} > {TOL * rng:.3e}"
+    return err / rng
+
+
+# ---------------------------------------------------------------- K1 / K5 pieces
+@pytest.mark.parametrize("H,W,C", [(1, 1, 1), (7, 5, 3), (48, 64, 3), (33, 70, 16), (20, 1000, 2)])
+def test_guide_derivative_parity(H, W, C):
+    g, _, _ = random_problem(H, W, C, 1, seed=H + W)
+    dx_r, dy_r = oracle.distances(g, 8.0, 0.2)
+    with dts.Solver(torch.from_numpy(g).cuda(), 8.0, 0.2, 3) as s:
+        dx, dy = s.read(dts.DTS_BUF_DX), s.read(dts.DTS_BUF_DY)
+    for got, ref in ((dx, dx_r), (dy, dy_r)):
+        inf = np.isinf(ref)
+        assert np.array_equal(np.isinf(got), inf)
+        np.testing.assert_allclose(got[~inf], ref[~inf], rtol=2e-6)
+
+
+@pytest.mark.parametrize("H,W", [(1, 1), (1, 9), (9, 1), (48, 64), (300, 41), (1500, 70), (13, 3000)])
+def test_support_parity(H, W):
+    g, _, _ = random_problem(H, W, 3, 1, seed=H * W)
+    dx_r, dy_r = oracle.distances(g, 6.0, 0.3)
+    S_r = oracle.support(dx_r, dy_r, 6.0)
+    with dts.Solver(torch.from_numpy(g).cuda(), 6.0, 0.3, 3) as s:
+        S = s.read(dts.DTS_BUF_SUPPORT)
+    np.testing.assert_allclose(S, S_r, rtol=2e-5)
+
+
+# ---------------------------------------------------------------- full solves
+def test_c0_parity():
+    cfg = CONFIGS["C0"]
+    g, t, c = make_inputs("C0")
+    rel = check(g, t, c, cfg.sigma_s, cfg.sigma_r, cfg.N, cfg.lam, cfg.iters)
+    assert rel < 1e-5
+
+
+SHAPES = [(1, 1), (1, 7), (7, 1), (2, 2), (31, 33), (33, 31), (32, 32), (61, 97), (5, 130), (130, 5),
+          (257, 3), (3, 1031), (17, 4099), (3, 10000), (2, 18000), (1000, 37), (2600, 35), (5000, 40),
+          (12000, 33)]
+
+
+@pytest.mark.parametrize("H,W", SHAPES)
+def test_edge_shapes_parity(H, W):
+    g, t, c = random_problem(H, W, 3, 1, seed=7 * H + W)
+    iters = 3 if H * W > 100000 else 6
+    check(g, t, c, 5.0, 0.2, 3, 0.99, iters)
+
+
+@pytest.mark.parametrize("Ct", [2, 3, 4])
+@pytest.mark.parametrize("H,W", [(9, 13), (70, 300), (1200, 64)])
+def test_multichannel_parity(Ct, H, W):
+    g, t, c = random_problem(H, W, 3, Ct, seed=Ct * 1000 + H)
+    check(g, t, c, 6.0, 0.15, 3, 0.99, 4)
+
+
+@pytest.mark.parametrize("N", [1, 2, 5])
+def test_pass_count_parity(N):
+    g, t, c = random_problem(40, 50, 3, 1, seed=N)
+    check(g, t, c, 7.0, 0.25, N, 0.99, 5)
+
+
+def test_support_mode_unweighted():
+    g, t, c = random_problem(30, 40, 3, 1, seed=11)
+    ref = oracle.solve(g, t, c, 6.0, 0.2, 3, 0.99, 5, support_mode=1)
+    got = gpu_solve(g, t, c, 6.0, 0.2, 3, 0.99, 5, support_mode=1)
+    assert np.max(np.abs(got - ref)) <= TOL * target_range(t)
+
+
+def test_step_option():
+    g, t, c = random_problem(20, 30, 3, 1, seed=12)
+    ref = oracle.solve(g, t, c, 6.0, 0.2, 3, 0.5, 4, step=0.7)
+    got = gpu_solve(g, t, c, 6.0, 0.2, 3, 0.5, 4, step=0.7)
+    assert np.max(np.abs(got - ref)) <= TOL * target_range(t)
+
+
+def test_zero_iterations_exact():
+    g, t, c = random_problem(11, 13, 3, 3, seed=2)
+    got = gpu_solve(g, t, c, 5.0, 0.2, 3, 0.99, 0)
+    assert np.array_equal(got, t.astype(np.float64))
+
+
+def test_constant_target_stays_constant():
+    g, _, c = random_problem(200, 300, 3, 1, seed=3)
+    t = np.full((200, 300), 7.5, np.float32)
+    got = gpu_solve(g, t, c, 8.0, 0.2, 3, 0.99, 20)
+    assert np.max(np.abs(got - 7.5)) <= 1e-6 * 7.5
+
+
+def test_c0_reduces_to_filter():
+    """c = 0, step = 1/lambda, one iteration -> the domain-transform filter output."""
+    g, t, _ = random_problem(60, 80, 3, 1, seed=4)
+    c = np.zeros((60, 80), np.float32)
+    dx, dy = oracle.distances(g, 6.0, 0.2)
+    ref = oracle.dtf(t.astype(np.float64), dx, dy, 6.0, 3)
+    got = gpu_solve(g, t, c, 6.0, 0.2, 3, 1 / 0.99, 1)
+    assert np.max(np.abs(got - ref)) <= 1e-6 * target_range(t)
+
+
+def test_decoupled_regions_bit_identical():
+    H, W = 64, 96
+    g = np.zeros((H, W, 3), np.float32)
+    g[:, W // 2:] = 1
+    rng = np.random.default_rng(5)
+    t = rng.uniform(0, 1, (H, W)).astype(np.float32)
+    t2 = t.copy()
+    t2[:, W // 2:] = 100
+    c = rng.uniform(0.1, 1, (H, W)).astype(np.float32)
+    a = gpu_solve(g, t, c, 8.0, 1e-3, 3, 0.99, 10)
+    b = gpu_solve(g, t2, c, 8.0, 1e-3, 3, 0.99, 10)
+    assert np.array_equal(a[:, :W // 2], b[:, :W // 2])
+
+
+def test_deterministic_and_host_pointer_path():
+    g, t, c = random_problem(100, 150, 3, 1, seed=6)
+    a = gpu_solve(g, t, c, 8.0, 0.2, 3, 0.99, 7)
+    b = gpu_solve(g, t, c, 8.0, 0.2, 3, 0.99, 7)
+    h = gpu_solve(g, t, c, 8.0, 0.2, 3, 0.99, 7, host=True)
+    assert np.array_equal(a, b)
+    assert np.array_equal(a, h)
+
+
+def test_multichannel_equals_single_channel():
+    g, t, c = random_problem(50, 70, 3, 3, seed=8)
+    z = gpu_solve(g, t, c, 6.0, 0.2, 3, 0.99, 5)
+    for ch in range(3):
+        z1 = gpu_solve(g, np.ascontiguousarray(t[..., ch]), c, 6.0, 0.2, 3, 0.99, 5)
+        np.testing.assert_allclose(z[..., ch], z1, rtol=0, atol=1e-6 * target_range(t))
+
+
+def test_residual_decreases_on_gpu():
+    """Reading R13 on the CUDA path: ||g||_inf of Eq. (3) evaluated by the oracle's
+    DTF at the GPU iterates is non-increasing (to fp32 noise)."""
+    g, t, c = make_inputs("C0")
+    cfg = CONFIGS["C0"]
+    dx, dy = oracle.distances(g, cfg.sigma_s, cfg.sigma_r)
+    chat = c / oracle.support(dx, dy, cfg.sigma_s)
+    prev = None
+    for k in [1, 2, 4, 8, 16]:
+        z = gpu_solve(g, t, c, cfg.sigma_s, cfg.sigma_r, cfg.N, cfg.lam, k)
+        zb = oracle.dtf(z, dx, dy, cfg.sigma_s, cfg.N)
+        gn = float(np.max(np.abs(cfg.lam * (z - zb) + chat * (z - t))))
+        if prev is not None:
+            assert gn <= prev * (1 + 1e-4)
+        prev = gn
+
+
+def test_invalid_arguments():
+    g, t, c = random_problem(8, 9, 3, 1, seed=9)
+    gd, td, cd = (torch.from_numpy(a).cuda() for a in (g, t, c))
+    with dts.Solver(gd, 5.0, 0.2, 3) as s:
+        out = torch.empty_like(td)
+        for lam, it in [(1.1, 3), (-0.1, 3), (float("nan"), 3), (0.99, -1)]:
+            with pytest.raises(dts.DTSError) as ei:
+                dts.dts_solve(s.ctx, td, cd, lam, it, out)
+            assert ei.value.status == 1
+        with pytest.raises(dts.DTSError) as ei:
+            dts.dts_solve(s.ctx, td, cd, 0.99, 3, td)  # out aliases target
+        assert ei.value.status == 1
+        bad = cd.clone()
+        bad[0, 0] = 2.0
+        with pytest.raises(dts.DTSError) as ei:
+            dts.dts_solve_ex(s.ctx, td, bad, 0.99, 3, out, check_inputs=True)
+        assert ei.value.status == 4
+        bad[0, 0] = float("nan")
+        with pytest.raises(dts.DTSError) as ei:
+            dts.dts_solve_ex(s.ctx, td, bad, 0.99, 3, out, check_inputs=True)
+        assert ei.value.status == 3
+
+
+def test_profile_counters():
+    g, t, c = random_problem(64, 128, 3, 1, seed=10)
+    gd, td, cd = (torch.from_numpy(a).cuda() for a in (g, t, c))
+    with dts.Solver(gd, 5.0, 0.2, 3) as s:
+        n0 = dts.dts_launch_count(s.ctx)
+        assert n0 == 3  # deriv + support row + support col
+        dts.dts_profile_enable(s.ctx, True)
+        s.solve(td, cd, 0.99, 4)
+        st = dts.dts_profile_read(s.ctx)
+        assert dts.dts_launch_count(s.ctx) == n0 + 1 + 4 * 6
+    assert st["row_pass"]["launches"] == 12 and st["col_pass"]["launches"] == 8
+    assert st["col_update"]["launches"] == 4 and st["prologue"]["launches"] == 1
+    assert st["row_pass"]["total_ms"] > 0
+
+
+# ---------------------------------------------------------------- BASELINE.json configs
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_config_parity(name):
+    cfg = CONFIGS[name]
+    g, t, c = make_inputs(name)
+    check(g, t, c, cfg.sigma_s, cfg.sigma_r, cfg.N, cfg.lam, cfg.iters)
+
+
+def test_c3_one_image_parity():
+    cfg = CONFIGS["C3"]
+    g, t, c = make_inputs("C3", image=5)
+    check(g, t, c, cfg.sigma_s, cfg.sigma_r, cfg.N, cfg.lam, cfg.iters)
+
+
+@pytest.mark.slow
+def test_c4_full_parity():
+    """The bench workload at full size (10000 x 10000, 16-band guide, 20 iterations),
+    in the launch configuration bench.py times, against the full fp64 oracle."""
+    cfg = CONFIGS["C4"]
+    g, t, c = make_inputs("C4")
+    check(g, t, c, cfg.sigma_s, cfg.sigma_r, cfg.N, cfg.lam, cfg.iters)
