@@ -8,41 +8,137 @@ namespace dts {
 // the square restored, R1; sigma scaling R2):
 //     d_x[r][c] = sqrt(1 + (sigma_s/sigma_r)^2 sum_k (I[r][c][k] - I[r][c-1][k])^2), d_x[r][0] = +inf
 //     d_y[r][c] likewise with row r-1, d_y[0][c] = +inf; columns c >= W (pitch padding) = +inf.
-// One thread per pixel; a warp reads 32 consecutive HWC pixels (one contiguous
-// 32*C-float span) of rows r and r-1; the left neighbour comes from the lane to the
-// left (shuffle) so the guide is streamed once (row r-1 is re-read from L2).
-template <int CMAX>
-__global__ void __launch_bounds__(256) k_guide_deriv(const float* __restrict__ guide, int C, float ratio2,
-                                                     Geometry g, float* __restrict__ dx, float* __restrict__ dy) {
-    const int64_t r = blockIdx.y;
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= g.pitch) return;
-    const int lane = threadIdx.x & 31;
-    float sx = 0.f, sy = 0.f;
-    const bool in = c < g.W;
-    const float* pr = guide + (r * g.W + c) * C;
-    const float* pl = pr - C;
-    const float* pu = pr - g.W * C;
-    for (int k = 0; k < C; ++k) {
-        const float v = in ? __ldg(pr + k) : 0.f;
-        // left neighbour's channel k: from lane-1, or a load for lane 0
-        float left = __shfl_up_sync(FULL, v, 1);
-        if (lane == 0 && in && c > 0) left = __ldg(pl + k);
-        const float up = (in && r > 0) ? __ldg(pu + k) : 0.f;
-        const float ex = v - left, ey = v - up;
-        sx = fmaf(ex, ex, sx);
-        sy = fmaf(ey, ey, sy);
+// A CTA owns a strip of 256 pixels (+1 on the left) and walks KROWS rows down it.
+// Each HWC row strip is one contiguous span of 257*C floats: it is loaded with
+// fully coalesced, independent loads (all in flight at once), parked in shared
+// memory with a conflict-free odd pixel stride, and the previous row stays
+// resident, so the guide is read from HBM once (plus 1/KROWS re-read of a row).
+constexpr int DERIV_STRIP = 256;
+constexpr int DERIV_ROWS = 16;
+
+template <int CT>  // CT = channel count (0: runtime C)
+__global__ void __launch_bounds__(DERIV_STRIP) k_guide_deriv(const float* __restrict__ guide, int Crt, float ratio2,
+                                                             Geometry g, float* __restrict__ dx,
+                                                             float* __restrict__ dy) {
+    const int C = CT > 0 ? CT : Crt;
+    const int CS = C | 1;  // odd pixel stride in shared memory -> conflict-free reads
+    extern __shared__ float sm[];
+    float* buf[2] = {sm, sm + (DERIV_STRIP + 1) * CS};
+    const int64_t c0 = (int64_t)blockIdx.x * DERIV_STRIP;  // first pixel of the strip
+    const int64_t rbeg = (int64_t)blockIdx.y * DERIV_ROWS;
+    const int64_t rend = min(rbeg + DERIV_ROWS, g.H);
+    const int t = threadIdx.x;
+    const int64_t cfirst = c0 > 0 ? c0 - 1 : 0;               // first pixel loaded
+    const int64_t clast = min(c0 + DERIV_STRIP, g.W);          // one past the last
+    const int64_t npx = clast > cfirst ? clast - cfirst : 0;
+    const int off = c0 > 0 ? 0 : 1;                            // smem pixel slot of `cfirst`
+    const int64_t n = npx * C;
+
+    // register-staged, software-pipelined row loads: row r+1 is in flight while row r computes
+    constexpr int NPER = CT > 0 ? (CT * (DERIV_STRIP + 1) + DERIV_STRIP - 1) / DERIV_STRIP : 1;
+    float v[NPER];
+    auto fetch = [&](int64_t r) {
+        const float* src = guide + (r * g.W + cfirst) * C;
+#pragma unroll
+        for (int u = 0; u < NPER; ++u) {
+            const int64_t e = t + (int64_t)u * DERIV_STRIP;
+            v[u] = e < n ? __ldg(src + e) : 0.f;
+        }
+    };
+    auto park = [&](float* dst) {
+#pragma unroll
+        for (int u = 0; u < NPER; ++u) {
+            const int64_t e = t + (int64_t)u * DERIV_STRIP;
+            if (e < n) {
+                const int px = (int)(e / C), k = (int)(e - (int64_t)px * C);
+                dst[(px + off) * CS + k] = v[u];
+            }
+        }
+    };
+    auto load_row_slow = [&](int64_t r, float* dst) {  // runtime C
+        const float* src = guide + (r * g.W + cfirst) * C;
+        for (int64_t e = t; e < n; e += DERIV_STRIP) {
+            const int px = (int)(e / C), k = (int)(e - (int64_t)px * C);
+            dst[(px + off) * CS + k] = __ldg(src + e);
+        }
+    };
+
+    const int64_t c = c0 + t;  // this thread's pixel; smem slot t + 1
+    int cur = 0;
+    if (rbeg > 0) {
+        if constexpr (CT > 0) {
+            fetch(rbeg - 1);
+            park(buf[1]);
+        } else {
+            load_row_slow(rbeg - 1, buf[1]);
+        }
     }
-    const int64_t o = r * g.pitch + c;
-    dx[o] = (in && c > 0) ? sqrtf(fmaf(ratio2, sx, 1.f)) : __int_as_float(0x7f800000);
-    dy[o] = (in && r > 0) ? sqrtf(fmaf(ratio2, sy, 1.f)) : __int_as_float(0x7f800000);
+    if constexpr (CT > 0) fetch(rbeg);
+    for (int64_t r = rbeg; r < rend; ++r) {
+        if constexpr (CT > 0) {
+            park(buf[cur]);
+        } else {
+            load_row_slow(r, buf[cur]);
+        }
+        __syncthreads();
+        if constexpr (CT > 0) {
+            if (r + 1 < rend) fetch(r + 1);
+        }
+        if (c < g.pitch) {
+            float ox = __int_as_float(0x7f800000), oy = __int_as_float(0x7f800000);
+            if (c < g.W) {
+                const float* pc = buf[cur] + (t + 1) * CS;
+                const float* pl = buf[cur] + t * CS;
+                const float* pu = buf[cur ^ 1] + (t + 1) * CS;
+                float sx = 0.f, sy = 0.f;
+                for (int k = 0; k < C; ++k) {
+                    const float x = pc[k];
+                    const float ex = x - pl[k], ey = x - pu[k];
+                    sx = fmaf(ex, ex, sx);
+                    sy = fmaf(ey, ey, sy);
+                }
+                if (c > 0) ox = sqrtf(fmaf(ratio2, sx, 1.f));
+                if (r > 0) oy = sqrtf(fmaf(ratio2, sy, 1.f));
+            }
+            dx[r * g.pitch + c] = ox;
+            dy[r * g.pitch + c] = oy;
+        }
+        cur ^= 1;
+        __syncthreads();
+    }
 }
 
 cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Geometry& g, float* dx, float* dy,
                                cudaStream_t s) {
-    dim3 block(256);
-    dim3 grid((unsigned)((g.pitch + 255) / 256), (unsigned)g.H);
-    k_guide_deriv<0><<<grid, block, 0, s>>>(guide, C, ratio2, g, dx, dy);
+    dim3 block(DERIV_STRIP);
+    dim3 grid((unsigned)((g.pitch + DERIV_STRIP - 1) / DERIV_STRIP), (unsigned)((g.H + DERIV_ROWS - 1) / DERIV_ROWS));
+    const size_t smem = 2 * (size_t)(DERIV_STRIP + 1) * (C | 1) * sizeof(float);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    switch (C) {
+#define DTS_DERIV_CASE(K)                                                                              \
+    case K: {                                                                                         \
+        static bool cfg = false;                                                                      \
+        if (!cfg) {                                                                                   \
+            cudaFuncSetAttribute(k_guide_deriv<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
+            cfg = true;                                                                               \
+        }                                                                                             \
+        k_guide_deriv<K><<<grid, block, smem, s>>>(guide, C, ratio2, g, dx, dy);                       \
+        break;                                                                                        \
+    }
+        DTS_DERIV_CASE(1)
+        DTS_DERIV_CASE(3)
+        DTS_DERIV_CASE(4)
+        DTS_DERIV_CASE(16)
+        default: {
+            static bool cfg = false;
+            if (!cfg) {
+                cudaFuncSetAttribute(k_guide_deriv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                cfg = true;
+            }
+            k_guide_deriv<0><<<grid, block, smem, s>>>(guide, C, ratio2, g, dx, dy);
+        }
+#undef DTS_DERIV_CASE
+    }
     return cudaGetLastError();
 }
 
