@@ -7,6 +7,7 @@
 //     K4 col pass N      Z <- Z - step [lambda (Z - RF_cols(X)) + chat (Z - T)]   (-> out on the last k)
 // (readings R4-R12.)
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -89,6 +90,11 @@ struct dts_ctx {
     float* st_o = nullptr;
     size_t st_bytes = 0;
     unsigned int* counters = nullptr;
+    // column-pass scratch: band tuples + publication flags (epoch-tagged)
+    float* tuples = nullptr;
+    unsigned int* flags = nullptr;
+    size_t tuple_cap = 0, flag_cap = 0;
+    unsigned int epoch = 0;
     cudaStream_t last_stream = nullptr;
     int64_t launches = 0;
 };
@@ -202,6 +208,53 @@ dts_status ensure_staging(dts_ctx* ctx, size_t bytes_per_image, cudaStream_t s) 
     return DTS_OK;
 }
 
+// column-pass plan: cluster fast path when it fits, else the decoupled band-tuple kernel
+cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan) {
+    if (!std::getenv("DTS_NO_CLUSTER") && plan_col_cluster(g, Ct, mode, num_sms, plan) == cudaSuccess)
+        return cudaSuccess;
+    cudaGetLastError();
+    return plan_col_pass(g, Ct, mode, num_sms, plan);
+}
+
+dts_status ensure_col_scratch(dts_ctx* ctx, const ColPlan& cp, cudaStream_t s) {
+    cudaError_t e;
+    if (cp.kind != 0) return DTS_OK;
+    if (cp.tuple_floats > ctx->tuple_cap) {
+        if (ctx->tuples) cudaFreeAsync(ctx->tuples, s);
+        ctx->tuples = nullptr;
+        if ((e = cudaMallocAsync((void**)&ctx->tuples, cp.tuple_floats * sizeof(float), s)) != cudaSuccess)
+            return cuda_fail(e);
+        ctx->tuple_cap = cp.tuple_floats;
+    }
+    if (cp.flag_count > ctx->flag_cap) {
+        if (ctx->flags) cudaFreeAsync(ctx->flags, s);
+        ctx->flags = nullptr;
+        if ((e = cudaMallocAsync((void**)&ctx->flags, cp.flag_count * sizeof(unsigned int), s)) != cudaSuccess ||
+            (e = cudaMemsetAsync(ctx->flags, 0, cp.flag_count * sizeof(unsigned int), s)) != cudaSuccess)
+            return cuda_fail(e);
+        ctx->flag_cap = cp.flag_count;
+        ctx->epoch = 0;
+    }
+    return DTS_OK;
+}
+
+ColScratch next_scratch(dts_ctx* ctx);
+
+cudaError_t col_launch(dts_ctx* ctx, const ColPlan& plan, int Ct, int mode, float* x, const float* d, float kc,
+                       const UpdateArgs* upd, float* support, cudaStream_t s) {
+    if (plan.kind == 1) return launch_col_cluster(plan, ctx->g, Ct, mode, x, d, kc, upd, support, s);
+    return launch_col_pass(plan, ctx->g, Ct, mode, x, d, kc, upd, support, next_scratch(ctx), s);
+}
+
+ColScratch next_scratch(dts_ctx* ctx) {
+    ColScratch sc;
+    sc.tuples = ctx->tuples;
+    sc.flags = ctx->flags;
+    sc.epoch = ++ctx->epoch;
+    if (sc.epoch == 0) sc.epoch = ++ctx->epoch;  // flags start at 0: never reuse 0
+    return sc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -275,7 +328,7 @@ dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float
     RowPlan rp;
     ColPlan cp;
     if (plan_row_pass(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &rp) != cudaSuccess ||
-        plan_col_pass(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &cp) != cudaSuccess) {
+        plan_col(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &cp) != cudaSuccess) {
         delete ctx;
         return DTS_E_SHAPE;
     }
@@ -316,9 +369,10 @@ dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float
         st = run_launch(ctx, F_SUPPORT_ROW, px * 8.0, s, [&] {
             return launch_row_pass(rp, ctx->g, 1, MODE_SUPPORT, nullptr, ctx->S, ctx->dx, ctx->ks, s);
         });
+    if (st == DTS_OK) st = ensure_col_scratch(ctx, cp, s);
     if (st == DTS_OK)
         st = run_launch(ctx, F_SUPPORT_COL, px * 12.0, s, [&] {
-            return launch_col_pass(cp, ctx->g, 1, MODE_SUPPORT, nullptr, ctx->dy, ctx->ks, nullptr, ctx->S, s);
+            return col_launch(ctx, cp, 1, MODE_SUPPORT, nullptr, ctx->dy, ctx->ks, nullptr, ctx->S, s);
         });
     if (gstage) {
         cudaFreeAsync(gstage, s);
@@ -354,8 +408,8 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     RowPlan rp;
     ColPlan cpf, cpu;
     if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess ||
-        plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf) != cudaSuccess ||
-        plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu) != cudaSuccess)
+        plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf) != cudaSuccess ||
+        plan_col(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu) != cudaSuccess)
         return DTS_E_SHAPE;
 
     const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),
@@ -396,6 +450,8 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         if ((e = cudaMemcpyAsync(o_d, t_d, img, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return cuda_fail(e);
     } else {
         if ((st = ensure_solver_state(ctx, Ct, s)) != DTS_OK) return st;
+        if ((st = ensure_col_scratch(ctx, cpf, s)) != DTS_OK) return st;
+        if ((st = ensure_col_scratch(ctx, cpu, s)) != DTS_OK) return st;
         const double px = (double)g.H * g.W;
         st = run_launch(ctx, F_PROLOGUE, px * (12.0 * Ct + 12), s, [&] {
             return launch_prologue(t_d, c_d, Ct, g, ctx->S, support_mode, ctx->Z, ctx->T, ctx->chat, s);
@@ -412,8 +468,8 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                 if (st != DTS_OK) return st;
                 if (i + 1 < ctx->N) {
                     st = run_launch(ctx, F_COL, row_bytes, s, [&] {
-                        return launch_col_pass(cpf, g, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr,
-                                               nullptr, s);
+                        return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
+                                          s);
                     });
                 } else {
                     UpdateArgs u;
@@ -424,8 +480,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                     u.step = step;
                     u.out_hwc = (k + 1 == iterations) ? o_d : nullptr;
                     st = run_launch(ctx, F_UPDATE, upd_bytes, s, [&] {
-                        return launch_col_pass(cpu, g, Ct, MODE_UPDATE, ctx->X, ctx->dy, ctx->kc[i], &u, nullptr,
-                                               s);
+                        return col_launch(ctx, cpu, Ct, MODE_UPDATE, ctx->X, ctx->dy, ctx->kc[i], &u, nullptr, s);
                     });
                 }
                 if (st != DTS_OK) return st;
@@ -455,6 +510,8 @@ void dts_destroy(dts_ctx* ctx) {
         *p = nullptr;
     }
     if (ctx->counters) cudaFreeAsync(ctx->counters, s);
+    if (ctx->tuples) cudaFreeAsync(ctx->tuples, s);
+    if (ctx->flags) cudaFreeAsync(ctx->flags, s);
     delete ctx;
 }
 

@@ -27,12 +27,19 @@ cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowP
 cudaError_t launch_row_pass(const RowPlan& plan, const Geometry& g, int Ct, int mode, const float* in, float* out,
                             const float* d, float kc, cudaStream_t s);
 
-// K3/K4: recursive-filter column pass (cluster-resident two-level scan), FILTER,
-// UPDATE (fused solver step, Eq. 3) or SUPPORT mode.
+// K3/K4: recursive-filter column pass (decoupled band-tuple scan, cooperative
+// persistent grid), FILTER, UPDATE (fused solver step, Eq. 3) or SUPPORT mode.
 struct ColPlan {
-    int TW, CB, HB, S, Ls, threads;
+    int kind;  // 0: decoupled band-tuple kernel (k_col.cu), 1: cluster kernel (k_colc.cu)
+    int TW, CB, HB, S, Ls, nb, ntiles, threads;
     dim3 grid;
     size_t smem;
+    size_t tuple_floats, flag_count;  // scratch the launch needs (ColScratch)
+};
+struct ColScratch {
+    float* tuples;         // >= plan.tuple_floats floats
+    unsigned int* flags;   // >= plan.flag_count, zero-initialised once
+    unsigned int epoch;    // distinct per launch (flags are compared against it)
 };
 struct UpdateArgs {
     float* Z;            // planar state (read; written unless out_hwc)
@@ -43,7 +50,14 @@ struct UpdateArgs {
 };
 cudaError_t plan_col_pass(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
 cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
-                            float kc, const UpdateArgs* upd, float* support, cudaStream_t s);
+                            float kc, const UpdateArgs* upd, float* support, const ColScratch& scr,
+                            cudaStream_t s);
+
+// K3/K4 fast path: cluster-held column tiles, register-resident segments (k_colc.cu).
+// Returns cudaErrorNotSupported when the shape does not fit (then use plan_col_pass).
+cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
+cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
+                               float kc, const UpdateArgs* upd, float* support, cudaStream_t s);
 
 // K6: solve prologue -- planar Z = T = target, chat = c / S (or c when support_mode = 1).
 cudaError_t launch_prologue(const float* target, const float* conf, int Ct, const Geometry& g, const float* S,

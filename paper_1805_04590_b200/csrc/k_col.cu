@@ -8,18 +8,25 @@
 // MODE_SUPPORT multiplies the two-sided unnormalised column sums s_y into S (R7).
 //
 // Design: one thread per column -- a warp covers 32 adjacent
-// columns, so every access of a warp is one 128-B row segment.  A column tile
-// (32 columns x H rows) is held ON CHIP by a thread-block cluster of CB CTAs (CTA b
-// holds rows [b*HB, (b+1)*HB) in shared memory), so each pixel is read from HBM
-// once and written once per pass:
-//   1. TMA (cp.async.bulk.tensor) streams the band in, one box and one mbarrier per
-//      segment of Ls rows, so warp s starts folding as soon as its rows land;
-//   2. each thread folds its Ls rows into an affine map; the S maps of a column
-//      are scanned by a warp-shuffle scan (lane = segment);
-//   3. per-band totals are exchanged between the cluster's CTAs through
-//      distributed shared memory (DSMEM): causal carries, then anticausal carries;
-//   4. the band is re-swept with exact carries in shared memory and leaves by TMA
-//      tensor stores (FILTER) or a vectorised, fully parallel update loop (UPDATE).
+// columns, so every access of a warp is one 128-B row segment.  The image is cut
+// into work items = (column tile of 32 columns) x (band of HB rows).  A
+// cooperative, persistent grid walks the items band-minor; each item is staged
+// on chip with TMA (one box + mbarrier per Ls-row segment) and read from HBM
+// exactly once:
+//   1. fold each segment into an affine map; warp-shuffle scan over segments;
+//   2. re-sweep with the band's causal carry c kept SYMBOLIC (y = y0 + y1 c) and
+//      fold the anticausal map symbolically too, giving the band's 5-tuple
+//          y_bottom = A c + B,    z_top = z0 + S c + Q e
+//      (e = anticausal carry from below) -- the same tuple the multi-GPU row-band
+//      exchange sends over NCCL;
+//   3. publish the tuple (global memory + release flag), wait for the other
+//      bands of the tile (acquire), and compose the exact carries (c, e) of this
+//      band from all tuples -- no serial carry chain between bands;
+//   4. finish in shared memory and leave by TMA tensor stores (FILTER) or a
+//      vectorised, fully parallel update / support loop.
+// Co-residency of the whole grid (required by the flag waits) is guaranteed by
+// the cooperative launch; items are walked in order, so every wait is on an
+// item already owned by a resident CTA.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -29,40 +36,52 @@
 namespace dts {
 
 constexpr int TW = 32;  // columns per tile (one warp)
+constexpr int LS = 32;  // rows per segment (one warp), held in registers
 
 struct ColParams {
     float* x;        // planar state (FILTER/UPDATE input; FILTER output through tm_x)
     const float* d;  // d_y (halo row)
     float* support;  // SUPPORT: S, multiplied in place by s_y
     UpdateArgs upd;
+    float* tuples;           // [ntiles][nb][NTUP][TW] band tuples
+    float* carries;          // [ntiles][nb][2][NV][TW] composed (c, e) per band
+    unsigned int* counters;  // [ntiles] arrivals (reset to 0 by the last arriver)
+    unsigned int* flags;     // [ntiles], == epoch when the tile's carries are released
     int64_t plane, pitch;
-    int H, W, HB, S, Ls, CB;
+    int H, W, HB, S, Ls, nb, ntiles, nitems;
+    unsigned int epoch;
     float kc;
 };
 
+// tuple components: A, B[NV], Q, Z0[NV], Sresp  (NTUP = 2 NV + 3)
+__host__ __device__ constexpr int ntup(int NV) { return 2 * NV + 3; }
+
 struct ColSmem {  // float offsets into dynamic shared memory
-    int xs, As, segC, segA, tot, rem, carry, bars;
+    int xs, As, segF, segR, totF, totR, tup, cj, carry, bars;
     size_t bytes;
 };
 
-__host__ __device__ inline ColSmem col_smem_layout(int NV, bool hasx, int HB, int S, int CB) {
+__host__ __device__ inline ColSmem col_smem_layout(int NV, int HB, int S, int nb) {
     ColSmem L;
     int o = 0;
     L.xs = o;
-    o += NV * HB * TW;  // samples / y / zbar (SUPPORT: P, then s_y)
-    (void)hasx;
+    o += NV * HB * TW;  // samples -> y0 -> y -> zbar (SUPPORT: P, then s_y)
     L.As = o;
-    o += (HB + 1) * TW;  // + halo row
-    L.segC = o;
+    o += (HB + 1) * TW;  // coefficients + halo row
+    L.segF = o;
     o += (NV + 1) * S * (TW + 1);
-    L.segA = o;
-    o += (NV + 1) * S * (TW + 1);
-    L.tot = o;  // [2][NV+1][TW]: causal, anticausal band totals (read remotely)
-    o += 2 * (NV + 1) * TW;
-    L.rem = o;  // gathered remote totals [CB][NV+1][TW]
-    o += CB * (NV + 1) * TW;
-    L.carry = o;  // [NV][TW]
-    o += NV * TW;
+    L.segR = o;
+    o += (NV + 2) * S * (TW + 1);
+    L.totF = o;
+    o += (NV + 1) * TW;
+    L.totR = o;
+    o += (NV + 2) * TW;
+    L.tup = o;  // the tile's band tuples, staged from global [nb][NTUP][TW]
+    o += nb * (2 * NV + 3) * TW;
+    L.cj = o;  // causal carries of every band of the tile [nb][NV][TW]
+    o += nb * NV * TW;
+    L.carry = o;  // c[NV][TW], e[NV][TW]
+    o += 2 * NV * TW;
     o = (o + 1) & ~1;  // 8-B alignment for the mbarriers
     L.bars = o;
     o += 2 * S;
@@ -70,294 +89,390 @@ __host__ __device__ inline ColSmem col_smem_layout(int NV, bool hasx, int HB, in
     return L;
 }
 
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Warp-shuffle scan across the S segment maps of column `cc` (lane = segment).
-// Forward: exclusive prefix (composite of segments < lane), written back in place.
-// Reverse: exclusive suffix (composite of segments > lane, applied right to left).
-// Lanes >= S act as identity.  Returns the total (valid in every lane).
-template <int NV, bool REV>
+// Components: P (comp 0) and NB offsets (comps 1..NB).  Forward: exclusive
+// prefix written back in place; reverse: exclusive suffix (segments below,
+// applied bottom-up).  Lanes >= S are identity.  The total goes to tot[comp][cc].
+template <int NB, bool REV>
 __device__ __forceinline__ void seg_scan(float* seg, int S, int cc, float* tot) {
     const int lane = threadIdx.x & 31;
-    Aff<NV> v = aff_identity<NV>();
+    Aff<NB> v = aff_identity<NB>();
     if (lane < S) {
         v.P = seg[(0 * S + lane) * (TW + 1) + cc];
 #pragma unroll
-        for (int k = 0; k < NV; ++k) v.B[k] = seg[((1 + k) * S + lane) * (TW + 1) + cc];
+        for (int k = 0; k < NB; ++k) v.B[k] = seg[((1 + k) * S + lane) * (TW + 1) + cc];
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-        Aff<NV> e;
+        Aff<NB> e;
         e.P = REV ? __shfl_down_sync(FULL, v.P, off) : __shfl_up_sync(FULL, v.P, off);
 #pragma unroll
-        for (int k = 0; k < NV; ++k) e.B[k] = REV ? __shfl_down_sync(FULL, v.B[k], off) : __shfl_up_sync(FULL, v.B[k], off);
+        for (int k = 0; k < NB; ++k) e.B[k] = REV ? __shfl_down_sync(FULL, v.B[k], off) : __shfl_up_sync(FULL, v.B[k], off);
         const bool take = REV ? (lane + off < 32) : (lane >= off);
         if (take) v = aff_compose(e, v);
     }
-    Aff<NV> ex;
+    Aff<NB> ex;
     ex.P = REV ? __shfl_down_sync(FULL, v.P, 1) : __shfl_up_sync(FULL, v.P, 1);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) ex.B[k] = REV ? __shfl_down_sync(FULL, v.B[k], 1) : __shfl_up_sync(FULL, v.B[k], 1);
-    if (REV ? lane == 31 : lane == 0) ex = aff_identity<NV>();
-    // total = inclusive value at the last position in scan order
-    const int src = REV ? 0 : 31;
-    Aff<NV> t;
-    t.P = __shfl_sync(FULL, v.P, src);
-#pragma unroll
-    for (int k = 0; k < NV; ++k) t.B[k] = __shfl_sync(FULL, v.B[k], src);
+    for (int k = 0; k < NB; ++k) ex.B[k] = REV ? __shfl_down_sync(FULL, v.B[k], 1) : __shfl_up_sync(FULL, v.B[k], 1);
+    if (REV ? lane == 31 : lane == 0) ex = aff_identity<NB>();
     if (lane < S) {
         seg[(0 * S + lane) * (TW + 1) + cc] = ex.P;
 #pragma unroll
-        for (int k = 0; k < NV; ++k) seg[((1 + k) * S + lane) * (TW + 1) + cc] = ex.B[k];
+        for (int k = 0; k < NB; ++k) seg[((1 + k) * S + lane) * (TW + 1) + cc] = ex.B[k];
     }
-    if (lane == 0) {
-        tot[0 * TW + cc] = t.P;
+    if (lane == (REV ? 0 : 31)) {
+        tot[0 * TW + cc] = v.P;
 #pragma unroll
-        for (int k = 0; k < NV; ++k) tot[(1 + k) * TW + cc] = t.B[k];
+        for (int k = 0; k < NB; ++k) tot[(1 + k) * TW + cc] = v.B[k];
     }
 }
 
 template <int CT, int MODE>
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(256)
     k_col_pass(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const ColParams p) {
     constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
     constexpr bool HASX = MODE != MODE_SUPPORT;
+    constexpr int NT = ntup(NV);
     extern __shared__ __align__(128) float smem[];
-    const int HB = p.HB, S = p.S, Ls = p.Ls, CB = p.CB;
-    const ColSmem L = col_smem_layout(NV, HASX, HB, S, CB);
-    float* xs = smem + L.xs;
-    float* As = smem + L.As;
-    float* segC = smem + L.segC;
-    float* segA = smem + L.segA;
-    float* totC = smem + L.tot;
-    float* totA = smem + L.tot + (NV + 1) * TW;
-    float* rem = smem + L.rem;
-    float* carry = smem + L.carry;
+    const int HB = p.HB, S = p.S, nb = p.nb;
+    const ColSmem L = col_smem_layout(NV, HB, S, nb);
+    float* xs = smem + L.xs;  // TMA landing zone: samples of the NEXT item
+    float* As = smem + L.As;  // TMA landing zone: d_y of the next item (+ halo coefficient)
+    float* segF = smem + L.segF;
+    float* segR = smem + L.segR;
+    float* totF = smem + L.totF;
+    float* totR = smem + L.totR;
+    float* tupS = smem + L.tup;
+    float* cj = smem + L.cj;
+    float* cc_ = smem + L.carry;  // c[NV][TW]
+    float* ec_ = cc_ + NV * TW;   // e[NV][TW]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
 
     const int c = threadIdx.x & 31;
     const int s = threadIdx.x >> 5;  // segment == warp
-    const int col0 = blockIdx.x * TW;
-    const int col = col0 + c;
-    const bool colok = col < p.W;
-    const int band = (CB > 1) ? (int)cluster_ctarank() : 0;
-    const int r0 = band * HB;
+    const int lo = s * LS;
 
-    // ---- 1. TMA: one box per segment and array, one mbarrier per segment ----
     if (threadIdx.x == 0) {
         for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
         fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
         tma_prefetch_desc(&tm_d);
         if (HASX) tma_prefetch_desc(&tm_x);
-        const uint32_t box = (uint32_t)(Ls * TW * sizeof(float));
-        for (int q = 0; q < S; ++q) {
-            const int rq = r0 + q * Ls;
-            const uint32_t bytes = rq < p.H ? box * (1 + (HASX ? NV : 0)) : 0u;
-            mbar_arrive_expect_tx(&bars[q], bytes);
-            if (bytes) {
-                tma_load_2d(As + q * Ls * TW, &tm_d, col0, rq, &bars[q]);
-                if constexpr (HASX) {
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) tma_load_3d(xs + (v * HB + q * Ls) * TW, &tm_x, col0, rq, v, &bars[q]);
-                }
-            }
-        }
-    }
-    if (s == 0) {  // halo: coefficient of the first row of the next band
-        const int rh = r0 + HB;
-        As[HB * TW + c] = (colok && rh < p.H) ? coef_from_d(p.d[(int64_t)rh * p.pitch + col], p.kc) : 0.f;
-    }
-
-    // ---- 2. causal fold (d -> A in place, invalid samples zeroed) ----
-    const int lo = s * Ls;
-    mbar_wait(&bars[s], 0);
-    Aff<NV> m = aff_identity<NV>();
-    for (int j = 0; j < Ls; ++j) {
-        const int rr = lo + j;
-        const bool ok = colok && (r0 + rr) < p.H;
-        const float a = ok ? coef_from_d(As[rr * TW + c], p.kc) : 0.f;
-        As[rr * TW + c] = a;
-        m.P *= a;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            if constexpr (HASX) {
-                float* px = xs + (v * HB + rr) * TW + c;
-                const float xv = ok ? *px : 0.f;
-                *px = xv;
-                m.B[v] = fmaf(a, m.B[v] - xv, xv);
-            } else {
-                m.B[v] = fmaf(a, m.B[v], 1.f);
-            }
-        }
-    }
-    segC[(0 * S + s) * (TW + 1) + c] = m.P;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) segC[((1 + v) * S + s) * (TW + 1) + c] = m.B[v];
-    __syncthreads();
-    for (int cc = s; cc < TW; cc += S) seg_scan<NV, false>(segC, S, cc, totC);
-    if (CB > 1) cluster_sync_all(); else __syncthreads();
-
-    // ---- 3a. causal carry into the band: compose the totals of the bands above ----
-    for (int q = s; q < band; q += S) {
-#pragma unroll
-        for (int k = 0; k < NV + 1; ++k) rem[(q * (NV + 1) + k) * TW + c] = ld_dsmem_f32(totC + k * TW + c, q);
-    }
-    __syncthreads();
-    if (s == 0) {
-        float cin[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) cin[v] = 0.f;
-        for (int q = 0; q < band; ++q) {
-            const float P = rem[(q * (NV + 1)) * TW + c];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) cin[v] = fmaf(P, cin[v], rem[(q * (NV + 1) + 1 + v) * TW + c]);
-        }
-#pragma unroll
-        for (int v = 0; v < NV; ++v) carry[v * TW + c] = cin[v];
     }
     __syncthreads();
 
-    // ---- 4. causal apply (y -> xs) + forward accumulation of the anticausal map ----
-    // z[n] = a z[n+1] + b_n, a = A[n+1], b_n = (1 - a) y[n] (filter) or 1 (support);
-    // segment map z_lo = Q z_hi + E accumulated forward: E += Q b_n; Q *= a.
-    {
-        float y[NV];
-        const float eP = segC[(0 * S + s) * (TW + 1) + c];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) y[v] = fmaf(eP, carry[v * TW + c], segC[((1 + v) * S + s) * (TW + 1) + c]);
-        Aff<NV> am = aff_identity<NV>();
-        for (int j = 0; j < Ls; ++j) {
-            const int rr = lo + j;
-            const float a = As[rr * TW + c];
-            const float an = As[(rr + 1) * TW + c];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                float* px = xs + (v * HB + rr) * TW + c;
-                if constexpr (HASX) {
-                    const float xv = *px;
-                    y[v] = fmaf(a, y[v] - xv, xv);
-                    am.B[v] = fmaf(am.P * (1.f - an), y[v], am.B[v]);
-                } else {
-                    y[v] = fmaf(a, y[v], 1.f);
-                    am.B[v] += am.P;
-                }
-                *px = y[v];
-            }
-            am.P *= an;
-        }
-        segA[(0 * S + s) * (TW + 1) + c] = am.P;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) segA[((1 + v) * S + s) * (TW + 1) + c] = am.B[v];
-    }
-    __syncthreads();
-    for (int cc = s; cc < TW; cc += S) seg_scan<NV, true>(segA, S, cc, totA);
-    if (CB > 1) cluster_sync_all(); else __syncthreads();
-
-    // ---- 5. anticausal carry from the bands below ----
-    for (int q = band + 1 + s; q < CB; q += S) {
-#pragma unroll
-        for (int k = 0; k < NV + 1; ++k) rem[(q * (NV + 1) + k) * TW + c] = ld_dsmem_f32(totA + k * TW + c, q);
-    }
-    if (CB > 1) cluster_arrive();  // this CTA's remote reads are issued and consumed above
-    __syncthreads();
-    if (s == 0) {
-        float ein[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) ein[v] = 0.f;
-        for (int q = CB - 1; q > band; --q) {
-            const float Q = rem[(q * (NV + 1)) * TW + c];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) ein[v] = fmaf(Q, ein[v], rem[(q * (NV + 1) + 1 + v) * TW + c]);
-        }
-#pragma unroll
-        for (int v = 0; v < NV; ++v) carry[v * TW + c] = ein[v];
-    }
-    __syncthreads();
-
-    // ---- 6. anticausal apply (bottom -> top), zbar (or s_y) back into xs ----
-    {
-        float z[NV];
-        const float eQ = segA[(0 * S + s) * (TW + 1) + c];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) z[v] = fmaf(eQ, carry[v * TW + c], segA[((1 + v) * S + s) * (TW + 1) + c]);
-        for (int j = Ls - 1; j >= 0; --j) {
-            const int rr = lo + j;
-            const float an = As[(rr + 1) * TW + c];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                float* px = xs + (v * HB + rr) * TW + c;
-                const float yv = *px;
-                if constexpr (HASX) {
-                    z[v] = fmaf(an, z[v] - yv, yv);
-                    *px = z[v];
-                } else {
-                    z[v] = fmaf(an, z[v], 1.f);
-                    *px = yv + z[v] - 1.f;  // s_y = P + Q - 1
-                }
-            }
-        }
-    }
-
-    // ---- 7. write-out ----
-    const int nrows = max(0, min(HB, p.H - r0));
-    if constexpr (MODE == MODE_FILTER) {
-        fence_proxy_async_smem();
-        __syncthreads();
+    // issue the TMA loads of `item` (thread 0) and its halo coefficient (warp 0)
+    auto stage_in = [&](int item) {
+        const int t = item / nb;
+        const int b = item - t * nb;
+        const int col0 = t * TW;
+        const int r0 = b * HB;
         if (threadIdx.x == 0) {
+            const uint32_t box = (uint32_t)(LS * TW * sizeof(float));
             for (int q = 0; q < S; ++q) {
-                const int rq = r0 + q * Ls;
-                if (rq >= p.H) break;
+                const int rq = r0 + q * LS;
+                const uint32_t bytes = rq < p.H ? box * (1 + (HASX ? NV : 0)) : 0u;
+                mbar_arrive_expect_tx(&bars[q], bytes);
+                if (bytes) {
+                    tma_load_2d(As + q * LS * TW, &tm_d, col0, rq, &bars[q]);
+                    if constexpr (HASX) {
 #pragma unroll
-                for (int v = 0; v < NV; ++v) tma_store_3d(&tm_x, col0, rq, v, xs + (v * HB + q * Ls) * TW);
-            }
-            bulk_commit();
-            bulk_wait_read0();
-        }
-    } else {
-        __syncthreads();
-        const int nitems = nrows * (TW / 4);
-#pragma unroll 4
-        for (int i = threadIdx.x; i < nitems; i += blockDim.x) {
-            const int rr = i >> 3;
-            const int q4 = (i & 7) * 4;
-            const int64_t r = r0 + rr;
-            const int cq = col0 + q4;
-            if constexpr (MODE == MODE_SUPPORT) {
-                const float4 sy = *reinterpret_cast<const float4*>(xs + rr * TW + q4);
-                float4* ps = reinterpret_cast<float4*>(p.support + r * p.pitch + cq);
-                float4 sv = *ps;
-                sv.x *= sy.x;
-                sv.y *= sy.y;
-                sv.z *= sy.z;
-                sv.w *= sy.w;
-                *ps = sv;
-            } else {
-                const float4 ch = __ldg(reinterpret_cast<const float4*>(p.upd.chat + r * p.pitch + cq));
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const int64_t idx = v * p.plane + r * p.pitch + cq;
-                    const float4 zb = *reinterpret_cast<const float4*>(xs + (v * HB + rr) * TW + q4);
-                    const float4 zo = *reinterpret_cast<const float4*>(p.upd.Z + idx);
-                    const float4 tv = __ldg(reinterpret_cast<const float4*>(p.upd.T + idx));
-                    float4 zn;
-                    zn.x = fmaf(-p.upd.step, fmaf(p.upd.lam, zo.x - zb.x, ch.x * (zo.x - tv.x)), zo.x);
-                    zn.y = fmaf(-p.upd.step, fmaf(p.upd.lam, zo.y - zb.y, ch.y * (zo.y - tv.y)), zo.y);
-                    zn.z = fmaf(-p.upd.step, fmaf(p.upd.lam, zo.z - zb.z, ch.z * (zo.z - tv.z)), zo.z);
-                    zn.w = fmaf(-p.upd.step, fmaf(p.upd.lam, zo.w - zb.w, ch.w * (zo.w - tv.w)), zo.w);
-                    if (p.upd.out_hwc) {
-                        const float zz[4] = {zn.x, zn.y, zn.z, zn.w};
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (cq + u < p.W) p.upd.out_hwc[(r * p.W + cq + u) * CT + v] = zz[u];
-                    } else {
-                        *reinterpret_cast<float4*>(p.upd.Z + idx) = zn;
+                        for (int v = 0; v < NV; ++v)
+                            tma_load_3d(xs + (v * HB + q * LS) * TW, &tm_x, col0, rq, v, &bars[q]);
                     }
                 }
             }
         }
+        if (s == 0) {
+            const int rh = r0 + HB;
+            const int cl = col0 + c;
+            As[HB * TW + c] = (cl < p.W && rh < p.H) ? coef_from_d(p.d[(int64_t)rh * p.pitch + cl], p.kc) : 0.f;
+        }
+    };
+
+    if (blockIdx.x < p.nitems) stage_in(blockIdx.x);
+
+    int k = 0;
+    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x, ++k) {
+        const int t = item / nb;
+        const int b = item - t * nb;
+        const int col0 = t * TW;
+        const int col = col0 + c;
+        const bool colok = col < p.W;
+        const int r0 = b * HB;
+
+        // ---- 1. this thread's LS rows -> registers (d -> A, invalid samples zeroed) ----
+        mbar_wait(&bars[s], (uint32_t)(k & 1));
+        float a[LS];
+        float xv[NV][LS];
+#pragma unroll
+        for (int j = 0; j < LS; ++j) {
+            const int rr = lo + j;
+            const bool ok = colok && (r0 + rr) < p.H;
+            a[j] = ok ? coef_from_d(As[rr * TW + c], p.kc) : 0.f;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                if constexpr (HASX) xv[v][j] = ok ? xs[(v * HB + rr) * TW + c] : 0.f;
+                else xv[v][j] = 0.f;
+            }
+        }
+        // causal fold
+        {
+            Aff<NV> m = aff_identity<NV>();
+#pragma unroll
+            for (int j = 0; j < LS; ++j) {
+                m.P *= a[j];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    if constexpr (HASX) m.B[v] = fmaf(a[j], m.B[v] - xv[v][j], xv[v][j]);
+                    else m.B[v] = fmaf(a[j], m.B[v], 1.f);
+                }
+            }
+            segF[(0 * S + s) * (TW + 1) + c] = m.P;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) segF[((1 + v) * S + s) * (TW + 1) + c] = m.B[v];
+        }
+        __syncthreads();
+        for (int cc = s; cc < TW; cc += S) seg_scan<NV, false>(segF, S, cc, totF);
+        // coefficient between this segment's last row and the next row (every box has landed:
+        // each warp waited on its own barrier before the barrier above)
+        float anext;
+        {
+            const int rn = r0 + lo + LS;
+            if (s + 1 < S) anext = (colok && rn < p.H) ? coef_from_d(As[(lo + LS) * TW + c], p.kc) : 0.f;
+            else anext = As[HB * TW + c];  // halo (already a coefficient)
+        }
+        __syncthreads();  // (the landing zone is free from here on)
+        {
+            const int nxt = item + gridDim.x;
+            if (nxt < p.nitems) stage_in(nxt);  // next item streams in under everything below
+        }
+
+        // ---- 2. symbolic causal apply (y0: carry 0, y1: response to carry 1) and
+        //         symbolic anticausal fold:  z_lo = Q z_hi + E0 + E1 c ----
+        {
+            float y0[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) y0[v] = segF[((1 + v) * S + s) * (TW + 1) + c];
+            float y1 = segF[(0 * S + s) * (TW + 1) + c];
+            float Q = 1.f, E1 = 0.f, E0[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) E0[v] = 0.f;
+#pragma unroll
+            for (int j = 0; j < LS; ++j) {
+                const float an = (j + 1 < LS) ? a[j + 1] : anext;
+                y1 *= a[j];
+                if constexpr (HASX) {
+                    const float qb = Q * (1.f - an);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        y0[v] = fmaf(a[j], y0[v] - xv[v][j], xv[v][j]);
+                        xv[v][j] = y0[v];
+                        E0[v] = fmaf(qb, y0[v], E0[v]);
+                    }
+                    E1 = fmaf(qb, y1, E1);
+                } else {
+                    y0[0] = fmaf(a[j], y0[0], 1.f);
+                    xv[0][j] = y0[0];
+                    E0[0] += Q;  // anticausal input is 1, independent of c
+                }
+                Q *= an;
+            }
+            segR[(0 * S + s) * (TW + 1) + c] = Q;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) segR[((1 + v) * S + s) * (TW + 1) + c] = E0[v];
+            segR[((1 + NV) * S + s) * (TW + 1) + c] = E1;
+        }
+        __syncthreads();
+        for (int cc = s; cc < TW; cc += S) seg_scan<NV + 1, true>(segR, S, cc, totR);
+        __syncthreads();
+
+        // ---- 3. publish this band's tuple; the LAST band of the tile to arrive composes
+        //         the exact carries (c_j, e_j) of every band of the tile and releases them ----
+        const float* tup_tile = p.tuples + (int64_t)t * nb * NT * TW;
+        float* car_tile = p.carries + (int64_t)t * nb * 2 * NV * TW;
+        if (s == 0) {
+            float* tb = p.tuples + ((int64_t)t * nb + b) * NT * TW;
+            tb[0 * TW + c] = totF[0 * TW + c];  // A
+#pragma unroll
+            for (int v = 0; v < NV; ++v) tb[(1 + v) * TW + c] = totF[(1 + v) * TW + c];  // B
+            tb[(1 + NV) * TW + c] = totR[0 * TW + c];                                    // Q
+#pragma unroll
+            for (int v = 0; v < NV; ++v) tb[(2 + NV + v) * TW + c] = totR[(1 + v) * TW + c];  // Z0
+            tb[(2 + 2 * NV) * TW + c] = totR[(1 + NV) * TW + c];                                // Sresp
+            __syncwarp();
+            unsigned int old = 0;
+            if (c == 0) {
+                __threadfence();
+                old = atomicAdd(p.counters + t, 1u);
+            }
+            old = __shfl_sync(FULL, old, 0);
+            cc_[0] = __uint_as_float(old == (unsigned)(nb - 1) ? 1u : 0u);
+        }
+        __syncthreads();
+        if (__float_as_uint(cc_[0]) == 1u) {  // last arriver (CTA-uniform)
+            __threadfence();
+            const int n = nb * NT * TW;  // stage all tuples of the tile, 16 loads in flight per thread
+            for (int i0 = threadIdx.x; i0 < n; i0 += 16 * blockDim.x) {
+                float r[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    r[u] = i < n ? __ldcg(tup_tile + i) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    if (i < n) tupS[i] = r[u];
+                }
+            }
+            __syncthreads();
+            if (s == 0) {
+                float cv[NV];  // causal carries c_j (c_0 = 0: A = 0 at the top row)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) cv[v] = 0.f;
+                for (int j = 0; j < nb; ++j) {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        cj[(j * NV + v) * TW + c] = cv[v];
+                        car_tile[((int64_t)(j * 2 + 0) * NV + v) * TW + c] = cv[v];
+                    }
+                    const float* tj = tupS + j * NT * TW;
+                    const float A = tj[c];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) cv[v] = fmaf(A, cv[v], tj[(1 + v) * TW + c]);
+                }
+                float ev[NV];  // anticausal carries: e_{j-1} = Z0_j + Sresp_j c_j + Q_j e_j, e_last = 0
+#pragma unroll
+                for (int v = 0; v < NV; ++v) ev[v] = 0.f;
+                for (int j = nb - 1; j >= 0; --j) {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) car_tile[((int64_t)(j * 2 + 1) * NV + v) * TW + c] = ev[v];
+                    const float* tj = tupS + j * NT * TW;
+                    const float Qj = tj[(1 + NV) * TW + c];
+                    const float Sj = tj[(2 + 2 * NV) * TW + c];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v)
+                        ev[v] = fmaf(Qj, ev[v], fmaf(Sj, cj[(j * NV + v) * TW + c], tj[(2 + NV + v) * TW + c]));
+                }
+                __syncwarp();
+                if (c == 0) {
+                    p.counters[t] = 0u;  // ready for the next launch
+                    __threadfence();
+                    st_release_u32(p.flags + t, p.epoch);
+                }
+            }
+        }
+        if (s == 0) {
+            if (c == 0)
+                while (ld_acquire_u32(p.flags + t) != p.epoch) __nanosleep(32);
+            __syncwarp();
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                cc_[v * TW + c] = __ldcg(car_tile + ((int64_t)(b * 2 + 0) * NV + v) * TW + c);
+                ec_[v * TW + c] = __ldcg(car_tile + ((int64_t)(b * 2 + 1) * NV + v) * TW + c);
+            }
+        }
+        __syncthreads();
+
+        // ---- 4. exact causal values y = y0 + y1 c, then anticausal apply (registers) ----
+        {
+            float cv[NV], z[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) cv[v] = cc_[v * TW + c];
+            float y1 = segF[(0 * S + s) * (TW + 1) + c];
+#pragma unroll
+            for (int j = 0; j < LS; ++j) {
+                y1 *= a[j];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) xv[v][j] = fmaf(y1, cv[v], xv[v][j]);
+            }
+            const float eQ = segR[(0 * S + s) * (TW + 1) + c];
+            const float eS = segR[((1 + NV) * S + s) * (TW + 1) + c];
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+                z[v] = fmaf(eQ, ec_[v * TW + c], fmaf(eS, cv[v], segR[((1 + v) * S + s) * (TW + 1) + c]));
+#pragma unroll
+            for (int j = LS - 1; j >= 0; --j) {
+                const float an = (j + 1 < LS) ? a[j + 1] : anext;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const float yv = xv[v][j];
+                    if constexpr (HASX) {
+                        z[v] = fmaf(an, z[v] - yv, yv);
+                        xv[v][j] = z[v];
+                    } else {
+                        z[v] = fmaf(an, z[v], 1.f);
+                        xv[v][j] = yv + z[v] - 1.f;  // s_y = P + Q - 1
+                    }
+                }
+            }
+        }
+
+        // ---- 5. write-out straight from registers (a warp stores one 128-B row segment) ----
+        {
+            const int nrow = min(LS, p.H - (r0 + lo));
+            if (colok && nrow > 0) {
+                if constexpr (MODE == MODE_FILTER) {
+#pragma unroll
+                    for (int j = 0; j < LS; ++j)
+                        if (j < nrow) {
+                            const int64_t o = (int64_t)(r0 + lo + j) * p.pitch + col;
+#pragma unroll
+                            for (int v = 0; v < NV; ++v) p.x[v * p.plane + o] = xv[v][j];
+                        }
+                } else if constexpr (MODE == MODE_SUPPORT) {
+#pragma unroll
+                    for (int j = 0; j < LS; ++j)
+                        if (j < nrow) {
+                            const int64_t o = (int64_t)(r0 + lo + j) * p.pitch + col;
+                            p.support[o] *= xv[0][j];
+                        }
+                } else {  // MODE_UPDATE: Eq. (3) with zbar = xv
+#pragma unroll
+                    for (int j0 = 0; j0 < LS; j0 += 8) {
+                        float zo[8][NV], tv[8][NV], ch[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int j = j0 + u;
+                            const int64_t o = (int64_t)(r0 + lo + (j < nrow ? j : 0)) * p.pitch + col;
+                            ch[u] = __ldg(p.upd.chat + o);
+#pragma unroll
+                            for (int v = 0; v < NV; ++v) {
+                                zo[u][v] = p.upd.Z[v * p.plane + o];
+                                tv[u][v] = __ldg(p.upd.T + v * p.plane + o);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int j = j0 + u;
+                            if (j < nrow) {
+                                const int64_t r = r0 + lo + j;
+                                const int64_t o = r * p.pitch + col;
+#pragma unroll
+                                for (int v = 0; v < NV; ++v) {
+                                    const float g = fmaf(p.upd.lam, zo[u][v] - xv[v][j], ch[u] * (zo[u][v] - tv[u][v]));
+                                    const float zn = fmaf(-p.upd.step, g, zo[u][v]);
+                                    if (p.upd.out_hwc) p.upd.out_hwc[(r * p.W + col) * CT + v] = zn;
+                                    else p.upd.Z[v * p.plane + o] = zn;
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();  // segF / segR / tuples are rewritten by the next item
     }
-    if (CB > 1) cluster_wait();  // keep shared memory alive until every CTA finished reading it
 }
 
 // ---------------------------------------------------------------------------------------
@@ -374,18 +489,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     return fn;
 }
 
-// rank-3 map over planar fp32 data [planes][H][pitch] with box {TW, rows, 1}
-static bool make_tmap(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int64_t planes, int rows) {
+// rank-3 map over planar fp32 data [planes][H][pitch], box {TW, rows, 1}
+static bool make_tmap3(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int64_t planes, int rows) {
     auto enc = tmap_encoder();
     if (!enc) return false;
     cuuint64_t dims[3] = {(cuuint64_t)pitch, (cuuint64_t)H, (cuuint64_t)planes};
     cuuint64_t strides[2] = {(cuuint64_t)(pitch * sizeof(float)), (cuuint64_t)(pitch * H * sizeof(float))};
     cuuint32_t box[3] = {(cuuint32_t)TW, (cuuint32_t)rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 static bool make_tmap2(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int rows) {
     auto enc = tmap_encoder();
@@ -394,93 +508,91 @@ static bool make_tmap2(CUtensorMap* m, const void* base, int64_t pitch, int64_t 
     cuuint64_t strides[1] = {(cuuint64_t)(pitch * sizeof(float))};
     cuuint32_t box[2] = {(cuuint32_t)TW, (cuuint32_t)rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static const size_t kSmemMax = 227 * 1024;
-
-cudaError_t plan_col_pass(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan) {
-    (void)num_sms;
-    const int NV = (mode == MODE_SUPPORT) ? 1 : Ct;
-    const bool hasx = mode != MODE_SUPPORT;
-    for (int CB = 1; CB <= 16; CB *= 2) {
-        const int64_t HBmin = (g.H + CB - 1) / CB;
-        int S = (int)((HBmin + 31) / 32);
-        S = S < 1 ? 1 : (S > 32 ? 32 : S);
-        const int Ls = (int)((HBmin + S - 1) / S);
-        if (Ls > 256) continue;  // TMA box limit
-        S = (int)((HBmin + Ls - 1) / Ls);
-        const int HB = S * Ls;
-        const ColSmem L = col_smem_layout(NV, hasx, HB, S, CB);
-        if (L.bytes > kSmemMax) continue;
-        plan->TW = TW;
-        plan->CB = CB;
-        plan->HB = HB;
-        plan->S = S;
-        plan->Ls = Ls;
-        plan->threads = TW * S;
-        plan->grid = dim3((unsigned)((g.W + TW - 1) / TW), (unsigned)CB, 1);
-        plan->smem = L.bytes;
-        return cudaSuccess;
-    }
-    return cudaErrorInvalidValue;
-}
+static const int kLs = LS;
 
 template <int CT, int MODE>
-static cudaError_t launch_t(const ColPlan& plan, const CUtensorMap& tx, const CUtensorMap& td, const ColParams& p,
-                            cudaStream_t s) {
-    static size_t configured = 0;
-    static bool nonportable = false;
-    auto fn = k_col_pass<CT, MODE>;
-    if (plan.smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
-        if (e != cudaSuccess) return e;
-        configured = plan.smem;
-    }
-    if (plan.CB > 8 && !nonportable) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        nonportable = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = plan.grid;
-    cfg.blockDim = dim3((unsigned)plan.threads, 1, 1);
-    cfg.dynamicSmemBytes = plan.smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = (unsigned)plan.CB;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fn, tx, td, p);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+static const void* kernel_ptr() {
+    return reinterpret_cast<const void*>(k_col_pass<CT, MODE>);
 }
 
-template <int MODE>
-static cudaError_t launch_ct(const ColPlan& plan, const CUtensorMap& tx, const CUtensorMap& td, const ColParams& p,
-                             int Ct, cudaStream_t s) {
-    switch (Ct) {
-        case 1: return launch_t<1, MODE>(plan, tx, td, p, s);
-        case 2: return launch_t<2, MODE>(plan, tx, td, p, s);
-        case 3: return launch_t<3, MODE>(plan, tx, td, p, s);
-        case 4: return launch_t<4, MODE>(plan, tx, td, p, s);
-        default: return cudaErrorInvalidValue;
+static const void* col_kernel(int Ct, int mode) {
+    if (mode == MODE_SUPPORT) return kernel_ptr<1, MODE_SUPPORT>();
+    switch (Ct * 4 + mode) {
+        case 4 + MODE_FILTER: return kernel_ptr<1, MODE_FILTER>();
+        case 8 + MODE_FILTER: return kernel_ptr<2, MODE_FILTER>();
+        case 12 + MODE_FILTER: return kernel_ptr<3, MODE_FILTER>();
+        case 16 + MODE_FILTER: return kernel_ptr<4, MODE_FILTER>();
+        case 4 + MODE_UPDATE: return kernel_ptr<1, MODE_UPDATE>();
+        case 8 + MODE_UPDATE: return kernel_ptr<2, MODE_UPDATE>();
+        case 12 + MODE_UPDATE: return kernel_ptr<3, MODE_UPDATE>();
+        case 16 + MODE_UPDATE: return kernel_ptr<4, MODE_UPDATE>();
     }
+    return nullptr;
+}
+
+cudaError_t plan_col_pass(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan) {
+    const int NV = (mode == MODE_SUPPORT) ? 1 : Ct;
+    const void* fn = col_kernel(Ct, mode);
+    if (!fn) return cudaErrorInvalidValue;
+    // band height: S segments of kLs rows; aim for >= 2 resident CTAs per SM
+    int S = (int)((g.H + kLs - 1) / kLs);
+    const int Smax = NV >= 3 ? 6 : 8;
+    if (S > Smax) S = Smax;
+    if (S < 1) S = 1;
+    const int HB = S * kLs;
+    const int nb = (int)((g.H + HB - 1) / HB);
+    const ColSmem L = col_smem_layout(NV, HB, S, nb);
+    if (L.bytes > kSmemMax) return cudaErrorInvalidValue;
+    static size_t configured[64] = {0};
+    const int slot = (mode * 8 + Ct) & 63;
+    if (L.bytes > configured[slot]) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+        if (e != cudaSuccess) return e;
+        configured[slot] = L.bytes;
+    }
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TW * S, L.bytes);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidValue;
+    const int ntiles = (int)((g.W + TW - 1) / TW);
+    const int64_t nitems = (int64_t)ntiles * nb;
+    if (nb > per_sm * num_sms) return cudaErrorInvalidValue;  // a tile's bands must be co-resident
+    int64_t grid = (int64_t)per_sm * num_sms;
+    if (grid > nitems) grid = nitems;
+    plan->kind = 0;
+    plan->TW = TW;
+    plan->CB = 1;
+    plan->HB = HB;
+    plan->S = S;
+    plan->Ls = kLs;
+    plan->nb = nb;
+    plan->ntiles = ntiles;
+    plan->threads = TW * S;
+    plan->grid = dim3((unsigned)grid, 1, 1);
+    plan->smem = L.bytes;
+    plan->tuple_floats = (size_t)nitems * (ntup(4) + 2 * 4) * TW;  // tuples + carries (NV <= 4)
+    plan->flag_count = (size_t)ntiles * 2;                           // flags + counters
+    return cudaSuccess;
 }
 
 cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
-                            float kc, const UpdateArgs* upd, float* support, cudaStream_t s) {
+                            float kc, const UpdateArgs* upd, float* support, const ColScratch& scr,
+                            cudaStream_t s) {
     ColParams p = {};
     p.x = x;
     p.d = d;
     p.support = support;
     if (upd) p.upd = *upd;
+    p.tuples = scr.tuples;
+    p.carries = scr.tuples + (size_t)plan.ntiles * plan.nb * ntup(4) * TW;
+    p.flags = scr.flags;
+    p.counters = scr.flags + plan.ntiles;
     p.plane = g.plane;
     p.pitch = g.pitch;
     p.H = (int)g.H;
@@ -488,21 +600,34 @@ cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int 
     p.HB = plan.HB;
     p.S = plan.S;
     p.Ls = plan.Ls;
-    p.CB = plan.CB;
+    p.nb = plan.nb;
+    p.ntiles = plan.ntiles;
+    p.nitems = plan.ntiles * plan.nb;
+    p.epoch = scr.epoch;
     p.kc = kc;
     CUtensorMap tx, td;
     if (!make_tmap2(&td, d, g.pitch, g.H, plan.Ls)) return cudaErrorInvalidValue;
     if (mode != MODE_SUPPORT) {
-        if (!make_tmap(&tx, x, g.pitch, g.H, Ct, plan.Ls)) return cudaErrorInvalidValue;
+        if (!make_tmap3(&tx, x, g.pitch, g.H, Ct, plan.Ls)) return cudaErrorInvalidValue;
     } else {
         tx = td;  // unused
     }
-    switch (mode) {
-        case MODE_FILTER: return launch_ct<MODE_FILTER>(plan, tx, td, p, Ct, s);
-        case MODE_UPDATE: return launch_ct<MODE_UPDATE>(plan, tx, td, p, Ct, s);
-        case MODE_SUPPORT: return launch_t<1, MODE_SUPPORT>(plan, tx, td, p, s);
-    }
-    return cudaErrorInvalidValue;
+    const void* fn = col_kernel(Ct, mode);
+    if (!fn) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = plan.grid;
+    cfg.blockDim = dim3((unsigned)plan.threads, 1, 1);
+    cfg.dynamicSmemBytes = plan.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the in-kernel tuple waits
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {&tx, &td, &p};
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
 }
 
 }  // namespace dts

@@ -1,0 +1,517 @@
+// k_colc.cu -- K3/K4 fast path: column pass with the column tile held by a
+// thread-block CLUSTER (sm_100a), persistent over tiles, TMA-prefetching the next tile.
+//
+// Same recurrence and modes as k_col.cu (R4-R7; UPDATE = Eq. (3),
+// P:185-189).  Layout of the work: a column tile is 32 columns x H rows; CTA
+// b of a cluster of CB CTAs owns rows [b*HB, (b+1)*HB); inside the CTA, warp s owns
+// rows [s*LS, (s+1)*LS) and lane c owns column c, holding its LS samples and
+// coefficients in REGISTERS.  Per tile:
+//   wait TMA boxes -> registers; the landing zone is immediately refilled with the
+//   NEXT tile (TMA), so HBM streams while this tile computes;
+//   causal fold -> warp-shuffle segment scan -> band totals exchanged through
+//   distributed shared memory (DSMEM) after a cluster barrier -> exact causal apply
+//   with the anticausal map folded on the fly -> second DSMEM exchange -> exact
+//   anticausal apply -> stores straight from registers (one 128-B row segment per
+//   warp instruction) or the fused Eq. (3) update.
+// Each pixel is read from HBM once and written once per pass; the carries between
+// bands never leave the chip.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "dts_device.cuh"
+#include "dts_launch.h"
+
+namespace dts {
+
+namespace colc {
+
+constexpr int TW = 32;  // columns per tile (one warp)
+constexpr int LS = 32;  // rows per warp segment (registers)
+
+struct Params {
+    float* x;        // planar state (in; FILTER: out)
+    const float* d;  // d_y
+    float* support;  // SUPPORT: S *= s_y
+    UpdateArgs upd;
+    int64_t plane, pitch;
+    int H, W, HB, S, CB, ntiles;
+    float kc;
+};
+
+struct Smem {
+    int land_x, land_d, segF, segR, totC, totA, rem, carry, bars;
+    size_t bytes;
+};
+
+__host__ __device__ inline Smem layout(int NV, int HB, int S) {
+    Smem L;
+    int o = 0;
+    L.land_x = o;
+    o += NV * HB * TW;
+    L.land_d = o;
+    o += HB * TW;
+    L.segF = o;
+    o += (NV + 1) * S * (TW + 1);
+    L.segR = o;
+    o += (NV + 1) * S * (TW + 1);
+    L.totC = o;  // band totals read by the other CTAs of the cluster (DSMEM)
+    o += (NV + 1) * TW;
+    L.totA = o;
+    o += (NV + 1) * TW;
+    L.rem = o;  // remote band totals gathered through DSMEM [16][NV+1][TW]
+    o += 16 * (NV + 1) * TW;
+    L.carry = o;
+    o += NV * TW;
+    o = (o + 1) & ~1;
+    L.bars = o;
+    o += 2 * S;
+    L.bytes = (size_t)o * sizeof(float);
+    return L;
+}
+
+// Shuffle scan of the S segment maps of column cc (lane = segment), exclusive
+// results written back, total -> tot.  Lanes >= S are identity.
+template <int NB, bool REV>
+__device__ __forceinline__ void seg_scan(float* seg, int S, int cc, float* tot) {
+    const int lane = threadIdx.x & 31;
+    Aff<NB> v = aff_identity<NB>();
+    if (lane < S) {
+        v.P = seg[(0 * S + lane) * (TW + 1) + cc];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v.B[k] = seg[((1 + k) * S + lane) * (TW + 1) + cc];
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        Aff<NB> e;
+        e.P = REV ? __shfl_down_sync(FULL, v.P, off) : __shfl_up_sync(FULL, v.P, off);
+#pragma unroll
+        for (int k = 0; k < NB; ++k) e.B[k] = REV ? __shfl_down_sync(FULL, v.B[k], off) : __shfl_up_sync(FULL, v.B[k], off);
+        if (REV ? (lane + off < 32) : (lane >= off)) v = aff_compose(e, v);
+    }
+    Aff<NB> ex;
+    ex.P = REV ? __shfl_down_sync(FULL, v.P, 1) : __shfl_up_sync(FULL, v.P, 1);
+#pragma unroll
+    for (int k = 0; k < NB; ++k) ex.B[k] = REV ? __shfl_down_sync(FULL, v.B[k], 1) : __shfl_up_sync(FULL, v.B[k], 1);
+    if (REV ? lane == 31 : lane == 0) ex = aff_identity<NB>();
+    if (lane < S) {
+        seg[(0 * S + lane) * (TW + 1) + cc] = ex.P;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) seg[((1 + k) * S + lane) * (TW + 1) + cc] = ex.B[k];
+    }
+    if (lane == (REV ? 0 : 31)) {
+        tot[0 * TW + cc] = v.P;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) tot[(1 + k) * TW + cc] = v.B[k];
+    }
+}
+
+template <int NV>
+constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
+
+template <int CT, int MODE>
+__global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>(), 1)
+    k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
+    constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
+    constexpr bool HASX = MODE != MODE_SUPPORT;
+    extern __shared__ __align__(128) float smem[];
+    const int HB = p.HB, S = p.S, CB = p.CB;
+    const Smem L = layout(NV, HB, S);
+    float* lx = smem + L.land_x;
+    float* ld = smem + L.land_d;
+    float* segF = smem + L.segF;
+    float* segR = smem + L.segR;
+    float* totC = smem + L.totC;
+    float* totA = smem + L.totA;
+    float* rem = smem + L.rem;
+    float* carry = smem + L.carry;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+
+    const int c = threadIdx.x & 31;
+    const int s = threadIdx.x >> 5;
+    const int band = (int)cluster_ctarank();
+    const int cluster = blockIdx.x / CB;
+    const int nclusters = gridDim.x / CB;
+    const int r0 = band * HB;
+    const int lo = s * LS;
+
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tm_d);
+        if (HASX) tma_prefetch_desc(&tm_x);
+    }
+    __syncthreads();
+
+    auto stage_in = [&](int tile) {  // thread 0: TMA boxes of `tile` into the landing zone
+        const int col0 = tile * TW;
+        const uint32_t box = (uint32_t)(LS * TW * sizeof(float));
+        for (int q = 0; q < S; ++q) {
+            const int rq = r0 + q * LS;
+            const uint32_t bytes = rq < p.H ? box * (1 + (HASX ? NV : 0)) : 0u;
+            mbar_arrive_expect_tx(&bars[q], bytes);
+            if (bytes) {
+                tma_load_2d(ld + q * LS * TW, &tm_d, col0, rq, &bars[q]);
+                if constexpr (HASX) {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) tma_load_3d(lx + (v * HB + q * LS) * TW, &tm_x, col0, rq, v, &bars[q]);
+                }
+            }
+        }
+    };
+    if (threadIdx.x == 0 && cluster < p.ntiles) stage_in(cluster);
+
+    int k = 0;
+    for (int tile = cluster; tile < p.ntiles; tile += nclusters, ++k) {
+        const int col0 = tile * TW;
+        const int col = col0 + c;
+        const bool colok = col < p.W;
+
+        // ---- 1. landing zone -> registers; refill with the next tile ----
+        mbar_wait(&bars[s], (uint32_t)(k & 1));
+        float a[LS];
+        float xv[NV][LS];
+#pragma unroll
+        for (int j = 0; j < LS; ++j) {
+            const int rr = lo + j;
+            const bool ok = colok && (r0 + rr) < p.H;
+            a[j] = ok ? coef_from_d(ld[rr * TW + c], p.kc) : 0.f;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                if constexpr (HASX) xv[v][j] = ok ? lx[(v * HB + rr) * TW + c] : 0.f;
+                else xv[v][j] = 0.f;
+            }
+        }
+        // coefficient linking this segment's last row to the next row: from the
+        // landing zone (next segment; it landed before the barrier below) or, for the
+        // band's last segment, straight from global (first row of the next band)
+        float anext = 0.f;
+        {
+            const int rn = r0 + lo + LS;
+            if (s + 1 == S && colok && rn < p.H) anext = coef_from_d(__ldg(p.d + (int64_t)rn * p.pitch + col), p.kc);
+        }
+        __syncthreads();
+        if (s + 1 < S) {
+            const int rn = r0 + lo + LS;
+            anext = (colok && rn < p.H) ? coef_from_d(ld[(lo + LS) * TW + c], p.kc) : 0.f;
+        }
+        __syncthreads();  // landing zone free
+        if (threadIdx.x == 0 && tile + nclusters < p.ntiles) stage_in(tile + nclusters);
+
+        // ---- 2. causal fold, segment scan, band total ----
+        {
+            Aff<NV> m = aff_identity<NV>();
+#pragma unroll
+            for (int j = 0; j < LS; ++j) {
+                m.P *= a[j];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    if constexpr (HASX) m.B[v] = fmaf(a[j], m.B[v] - xv[v][j], xv[v][j]);
+                    else m.B[v] = fmaf(a[j], m.B[v], 1.f);
+                }
+            }
+            segF[(0 * S + s) * (TW + 1) + c] = m.P;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) segF[((1 + v) * S + s) * (TW + 1) + c] = m.B[v];
+        }
+        __syncthreads();
+        for (int cc = s; cc < TW; cc += S) seg_scan<NV, false>(segF, S, cc, totC);
+        cluster_sync_all();  // band totals of the whole cluster are visible
+
+        // ---- 3. causal carry from the bands above: warp q fetches band q's totals (DSMEM,
+        //         all in flight at once), warp 0 composes ----
+        for (int q = s; q < band; q += S) {
+#pragma unroll
+            for (int k2 = 0; k2 < NV + 1; ++k2)
+                rem[(q * (NV + 1) + k2) * TW + c] = ld_dsmem_f32(totC + k2 * TW + c, (uint32_t)q);
+        }
+        __syncthreads();
+        if (s == 0) {
+            float cin[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) cin[v] = 0.f;
+            for (int q = 0; q < band; ++q) {
+                const float P = rem[(q * (NV + 1)) * TW + c];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) cin[v] = fmaf(P, cin[v], rem[(q * (NV + 1) + 1 + v) * TW + c]);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) carry[v * TW + c] = cin[v];
+        }
+        __syncthreads();
+        {
+            const float eP = segF[(0 * S + s) * (TW + 1) + c];
+            float y[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) y[v] = fmaf(eP, carry[v * TW + c], segF[((1 + v) * S + s) * (TW + 1) + c]);
+            float Q = 1.f, E[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) E[v] = 0.f;
+#pragma unroll
+            for (int j = 0; j < LS; ++j) {
+                const float an = (j + 1 < LS) ? a[j + 1] : anext;
+                if constexpr (HASX) {
+                    const float qb = Q * (1.f - an);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        y[v] = fmaf(a[j], y[v] - xv[v][j], xv[v][j]);
+                        xv[v][j] = y[v];
+                        E[v] = fmaf(qb, y[v], E[v]);
+                    }
+                } else {
+                    y[0] = fmaf(a[j], y[0], 1.f);
+                    xv[0][j] = y[0];
+                    E[0] += Q;
+                }
+                Q *= an;
+            }
+            segR[(0 * S + s) * (TW + 1) + c] = Q;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) segR[((1 + v) * S + s) * (TW + 1) + c] = E[v];
+        }
+        __syncthreads();
+        for (int cc = s; cc < TW; cc += S) seg_scan<NV, true>(segR, S, cc, totA);
+        cluster_sync_all();
+
+        // ---- 4. anticausal carry from the bands below (DSMEM, parallel gather), exact apply ----
+        for (int q = band + 1 + s; q < CB; q += S) {
+#pragma unroll
+            for (int k2 = 0; k2 < NV + 1; ++k2)
+                rem[(q * (NV + 1) + k2) * TW + c] = ld_dsmem_f32(totA + k2 * TW + c, (uint32_t)q);
+        }
+        __syncthreads();
+        if (s == 0) {
+            float ein[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) ein[v] = 0.f;
+            for (int q = CB - 1; q > band; --q) {
+                const float Qb = rem[(q * (NV + 1)) * TW + c];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) ein[v] = fmaf(Qb, ein[v], rem[(q * (NV + 1) + 1 + v) * TW + c]);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) carry[v * TW + c] = ein[v];
+        }
+        __syncthreads();
+        {
+            const float eQ = segR[(0 * S + s) * (TW + 1) + c];
+            float z[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) z[v] = fmaf(eQ, carry[v * TW + c], segR[((1 + v) * S + s) * (TW + 1) + c]);
+#pragma unroll
+            for (int j = LS - 1; j >= 0; --j) {
+                const float an = (j + 1 < LS) ? a[j + 1] : anext;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const float yv = xv[v][j];
+                    if constexpr (HASX) {
+                        z[v] = fmaf(an, z[v] - yv, yv);
+                        xv[v][j] = z[v];
+                    } else {
+                        z[v] = fmaf(an, z[v], 1.f);
+                        xv[v][j] = yv + z[v] - 1.f;  // s_y = P + Q - 1
+                    }
+                }
+            }
+        }
+
+        // ---- 5. write-out straight from registers ----
+        {
+            const int nrow = min(LS, p.H - (r0 + lo));
+            if (colok && nrow > 0) {
+                if constexpr (MODE == MODE_FILTER) {
+#pragma unroll
+                    for (int j = 0; j < LS; ++j)
+                        if (j < nrow) {
+                            const int64_t o = (int64_t)(r0 + lo + j) * p.pitch + col;
+#pragma unroll
+                            for (int v = 0; v < NV; ++v) p.x[v * p.plane + o] = xv[v][j];
+                        }
+                } else if constexpr (MODE == MODE_SUPPORT) {
+                    float sv[LS];  // all loads in flight before any store
+#pragma unroll
+                    for (int j = 0; j < LS; ++j)
+                        sv[j] = p.support[(int64_t)(r0 + lo + (j < nrow ? j : 0)) * p.pitch + col];
+#pragma unroll
+                    for (int j = 0; j < LS; ++j)
+                        if (j < nrow) p.support[(int64_t)(r0 + lo + j) * p.pitch + col] = sv[j] * xv[0][j];
+                } else {  // MODE_UPDATE, Eq. (3) with zbar = xv
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        float zo[LS];  // all Z loads in flight before any store (a[] is dead here)
+#pragma unroll
+                        for (int j = 0; j < LS; ++j)
+                            zo[j] = p.upd.Z[v * p.plane + (int64_t)(r0 + lo + (j < nrow ? j : 0)) * p.pitch + col];
+#pragma unroll
+                        for (int j = 0; j < LS; ++j) {
+                            if (j < nrow) {
+                                const int64_t r = r0 + lo + j;
+                                const int64_t o = r * p.pitch + col;
+                                const float ch = __ldg(p.upd.chat + o);
+                                const float tv = __ldg(p.upd.T + v * p.plane + o);
+                                const float g = fmaf(p.upd.lam, zo[j] - xv[v][j], ch * (zo[j] - tv));
+                                const float zn = fmaf(-p.upd.step, g, zo[j]);
+                                if (p.upd.out_hwc) p.upd.out_hwc[(r * p.W + col) * CT + v] = zn;
+                                else p.upd.Z[v * p.plane + o] = zn;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();  // segF / segR / carry reused by the next tile
+    }
+    cluster_sync_all();  // no CTA leaves while another may still read its shared memory
+}
+
+}  // namespace colc
+
+// ---------------------------------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+static bool tmap(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int64_t planes, int rank) {
+    auto enc = encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)pitch, (cuuint64_t)H, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)(pitch * sizeof(float)), (cuuint64_t)(pitch * H * sizeof(float))};
+    cuuint32_t box[3] = {(cuuint32_t)colc::TW, (cuuint32_t)colc::LS, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int CT, int MODE>
+static const void* kptr() {
+    return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE>);
+}
+static const void* colc_kernel(int Ct, int mode) {
+    if (mode == MODE_SUPPORT) return kptr<1, MODE_SUPPORT>();
+    switch (Ct * 4 + mode) {
+        case 4 + MODE_FILTER: return kptr<1, MODE_FILTER>();
+        case 8 + MODE_FILTER: return kptr<2, MODE_FILTER>();
+        case 12 + MODE_FILTER: return kptr<3, MODE_FILTER>();
+        case 4 + MODE_UPDATE: return kptr<1, MODE_UPDATE>();
+        case 8 + MODE_UPDATE: return kptr<2, MODE_UPDATE>();
+        case 12 + MODE_UPDATE: return kptr<3, MODE_UPDATE>();
+    }
+    return nullptr;
+}
+
+// Fast path if the column fits a cluster of <= 16 CTAs with register-resident segments.
+cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan) {
+    (void)num_sms;
+    const int NV = (mode == MODE_SUPPORT) ? 1 : Ct;
+    const void* fn = colc_kernel(Ct, mode);
+    if (!fn) return cudaErrorNotSupported;
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return e;
+    int Smax = fa.maxThreadsPerBlock / colc::TW;
+    if (Smax > 20) Smax = 20;
+    const int64_t rows_seg = colc::LS;
+    for (int CB = 1; CB <= 16; ++CB) {
+        const int64_t HBmin = (g.H + CB - 1) / CB;
+        const int S = (int)((HBmin + rows_seg - 1) / rows_seg);
+        if (S > Smax) continue;
+        const int HB = S * colc::LS;
+        const colc::Smem L = colc::layout(NV, HB, S);
+        if (L.bytes > 227 * 1024) continue;
+        if (CB > 8) {
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+        if (e != cudaSuccess) return e;
+        // how many clusters can be resident at once
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)CB, 1, 1);
+        cfg.blockDim = dim3((unsigned)(colc::TW * S), 1, 1);
+        cfg.dynamicSmemBytes = L.bytes;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)CB;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        e = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg);
+        if (e != cudaSuccess || nclusters < 1) {
+            cudaGetLastError();
+            continue;
+        }
+        const int ntiles = (int)((g.W + colc::TW - 1) / colc::TW);
+        if (nclusters > ntiles) nclusters = ntiles;
+        plan->kind = 1;
+        plan->TW = colc::TW;
+        plan->CB = CB;
+        plan->HB = HB;
+        plan->S = S;
+        plan->Ls = colc::LS;
+        plan->nb = CB;
+        plan->ntiles = ntiles;
+        plan->threads = colc::TW * S;
+        plan->grid = dim3((unsigned)(CB * nclusters), 1, 1);
+        plan->smem = L.bytes;
+        plan->tuple_floats = 0;
+        plan->flag_count = 0;
+        return cudaSuccess;
+    }
+    return cudaErrorNotSupported;
+}
+
+cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
+                               float kc, const UpdateArgs* upd, float* support, cudaStream_t s) {
+    colc::Params p = {};
+    p.x = x;
+    p.d = d;
+    p.support = support;
+    if (upd) p.upd = *upd;
+    p.plane = g.plane;
+    p.pitch = g.pitch;
+    p.H = (int)g.H;
+    p.W = (int)g.W;
+    p.HB = plan.HB;
+    p.S = plan.S;
+    p.CB = plan.CB;
+    p.ntiles = plan.ntiles;
+    p.kc = kc;
+    CUtensorMap tx, td;
+    if (!tmap(&td, d, g.pitch, g.H, 1, 2)) return cudaErrorInvalidValue;
+    if (mode != MODE_SUPPORT) {
+        if (!tmap(&tx, x, g.pitch, g.H, Ct, 3)) return cudaErrorInvalidValue;
+    } else {
+        tx = td;
+    }
+    const void* fn = colc_kernel(Ct, mode);
+    if (!fn) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = plan.grid;
+    cfg.blockDim = dim3((unsigned)plan.threads, 1, 1);
+    cfg.dynamicSmemBytes = plan.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)plan.CB;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {&tx, &td, &p};
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+}  // namespace dts

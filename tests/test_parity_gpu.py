@@ -245,3 +245,12 @@ def test_c4_full_parity():
     cfg = CONFIGS["C4"]
     g, t, c = make_inputs("C4")
     check(g, t, c, cfg.sigma_s, cfg.sigma_r, cfg.N, cfg.lam, cfg.iters)
+
+
+@pytest.mark.parametrize("H,W,Ct", [(48, 64, 1), (33, 31, 1), (700, 130, 1), (300, 90, 3), (61, 97, 2)])
+def test_fallback_column_kernel_parity(H, W, Ct, monkeypatch):
+    """The decoupled band-tuple column kernel (used when a column does not fit a
+    cluster) forced for ordinary shapes: DTS_NO_CLUSTER=1."""
+    monkeypatch.setenv("DTS_NO_CLUSTER", "1")
+    g, t, c = random_problem(H, W, 3, Ct, seed=H + 3 * W)
+    check(g, t, c, 6.0, 0.2, 3, 0.99, 5)
