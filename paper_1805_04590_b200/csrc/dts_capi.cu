@@ -101,9 +101,9 @@ struct dts_ctx {
 
 namespace {
 
-enum Family { F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_COUNT };
+enum Family { F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP, F_COUNT };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update",
-                                     "support_row", "support_col", "prologue"};
+                                     "support_row", "support_col", "prologue", "update"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -470,6 +470,18 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                     st = run_launch(ctx, F_COL, row_bytes, s, [&] {
                         return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
                                           s);
+                    });
+                } else if (cpu.kind == 1) {
+                    // cluster column kernel + streaming update kernel (K4b)
+                    st = run_launch(ctx, F_COL, row_bytes, s, [&] {
+                        return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
+                                          s);
+                    });
+                    if (st != DTS_OK) return st;
+                    float* ohwc = (k + 1 == iterations) ? o_d : nullptr;
+                    st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
+                        return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, ohwc,
+                                             ctx->num_sms, s);
                     });
                 } else {
                     UpdateArgs u;

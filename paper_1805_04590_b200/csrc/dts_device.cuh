@@ -133,6 +133,29 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
+// store a float into another CTA's shared memory (same offset as `local`), completing
+// 4 transaction bytes on that CTA's mbarrier at the offset of `local_bar`
+__device__ __forceinline__ void st_async_f32(const float* local, float v, const uint64_t* local_bar, uint32_t rank) {
+    uint32_t a = smem_u32(local), b = smem_u32(local_bar), ra, rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(b), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(ra),
+                 "r"(__float_as_uint(v)), "r"(rb)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAITC_%=;\n\t"
+        "}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
 // read a float from the same smem offset in another CTA of the cluster
 __device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank) {
     uint32_t a = smem_u32(local), ra;

@@ -59,6 +59,10 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
                                float kc, const UpdateArgs* upd, float* support, cudaStream_t s);
 
+// K4b: Eq. (3) update as a streaming kernel (zbar in X); writes Z, or out_hwc when non-null.
+cudaError_t launch_update(const float* X, float* Z, const float* T, const float* chat, int Ct, const Geometry& g,
+                          float lam, float step, float* out_hwc, int num_sms, cudaStream_t s);
+
 // K6: solve prologue -- planar Z = T = target, chat = c / S (or c when support_mode = 1).
 cudaError_t launch_prologue(const float* target, const float* conf, int Ct, const Geometry& g, const float* S,
                             int support_mode, float* Z, float* T, float* chat, cudaStream_t s);

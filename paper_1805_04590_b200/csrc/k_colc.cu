@@ -39,7 +39,7 @@ struct Params {
 };
 
 struct Smem {
-    int land_x, land_d, segF, segR, totC, totA, rem, carry, bars;
+    int land_x, land_d, segF, segR, totC, totA, remC, remA, carry, bars;
     size_t bytes;
 };
 
@@ -58,13 +58,15 @@ __host__ __device__ inline Smem layout(int NV, int HB, int S) {
     o += (NV + 1) * TW;
     L.totA = o;
     o += (NV + 1) * TW;
-    L.rem = o;  // remote band totals gathered through DSMEM [16][NV+1][TW]
+    L.remC = o;  // band totals pushed by the bands above (st.async) [16][NV+1][TW]
+    o += 16 * (NV + 1) * TW;
+    L.remA = o;  // band totals pushed by the bands below
     o += 16 * (NV + 1) * TW;
     L.carry = o;
     o += NV * TW;
     o = (o + 1) & ~1;
     L.bars = o;
-    o += 2 * S;
+    o += 2 * S + 4;  // S TMA barriers + 2 exchange barriers
     L.bytes = (size_t)o * sizeof(float);
     return L;
 }
@@ -122,9 +124,12 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
     float* segR = smem + L.segR;
     float* totC = smem + L.totC;
     float* totA = smem + L.totA;
-    float* rem = smem + L.rem;
+    float* remC = smem + L.remC;
+    float* remA = smem + L.remA;
     float* carry = smem + L.carry;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* xbarC = bars + S;      // causal totals from the bands above have landed
+    uint64_t* xbarA = bars + S + 1;  // anticausal totals from the bands below have landed
 
     const int c = threadIdx.x & 31;
     const int s = threadIdx.x >> 5;
@@ -134,13 +139,19 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
     const int r0 = band * HB;
     const int lo = s * LS;
 
+    const uint32_t xbytesC = (uint32_t)(band * (NV + 1) * TW * sizeof(float));
+    const uint32_t xbytesA = (uint32_t)((CB - 1 - band) * (NV + 1) * TW * sizeof(float));
     if (threadIdx.x == 0) {
         for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
+        mbar_init(xbarC, 1);
+        mbar_init(xbarA, 1);
         fence_mbar_init();
+        mbar_arrive_expect_tx(xbarC, xbytesC);  // armed for the first tile
+        mbar_arrive_expect_tx(xbarA, xbytesA);
         tma_prefetch_desc(&tm_d);
         if (HASX) tma_prefetch_desc(&tm_x);
     }
-    __syncthreads();
+    cluster_sync_all();  // every exchange barrier of the cluster is initialised and armed
 
     auto stage_in = [&](int tile) {  // thread 0: TMA boxes of `tile` into the landing zone
         const int col0 = tile * TW;
@@ -215,24 +226,26 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         }
         __syncthreads();
         for (int cc = s; cc < TW; cc += S) seg_scan<NV, false>(segF, S, cc, totC);
-        cluster_sync_all();  // band totals of the whole cluster are visible
+        __syncthreads();
 
-        // ---- 3. causal carry from the bands above: warp q fetches band q's totals (DSMEM,
-        //         all in flight at once), warp 0 composes ----
-        for (int q = s; q < band; q += S) {
+        // ---- 3. push this band's causal total to every band below it (st.async into their
+        //         shared memory, completing on their exchange barrier); warp 0 waits for the
+        //         totals of the bands above and composes the causal carry ----
+        for (int q = band + 1 + s; q < CB; q += S) {
 #pragma unroll
             for (int k2 = 0; k2 < NV + 1; ++k2)
-                rem[(q * (NV + 1) + k2) * TW + c] = ld_dsmem_f32(totC + k2 * TW + c, (uint32_t)q);
+                st_async_f32(remC + (band * (NV + 1) + k2) * TW + c, totC[k2 * TW + c], xbarC, (uint32_t)q);
         }
-        __syncthreads();
         if (s == 0) {
+            mbar_wait_cluster(xbarC, (uint32_t)(k & 1));
+            if (c == 0) mbar_arrive_expect_tx(xbarC, xbytesC);  // re-arm for the next tile
             float cin[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) cin[v] = 0.f;
             for (int q = 0; q < band; ++q) {
-                const float P = rem[(q * (NV + 1)) * TW + c];
+                const float P = remC[(q * (NV + 1)) * TW + c];
 #pragma unroll
-                for (int v = 0; v < NV; ++v) cin[v] = fmaf(P, cin[v], rem[(q * (NV + 1) + 1 + v) * TW + c]);
+                for (int v = 0; v < NV; ++v) cin[v] = fmaf(P, cin[v], remC[(q * (NV + 1) + 1 + v) * TW + c]);
             }
 #pragma unroll
             for (int v = 0; v < NV; ++v) carry[v * TW + c] = cin[v];
@@ -270,23 +283,24 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         }
         __syncthreads();
         for (int cc = s; cc < TW; cc += S) seg_scan<NV, true>(segR, S, cc, totA);
-        cluster_sync_all();
+        __syncthreads();
 
-        // ---- 4. anticausal carry from the bands below (DSMEM, parallel gather), exact apply ----
-        for (int q = band + 1 + s; q < CB; q += S) {
+        // ---- 4. anticausal totals flow upwards the same way ----
+        for (int q = band - 1 - s; q >= 0; q -= S) {
 #pragma unroll
             for (int k2 = 0; k2 < NV + 1; ++k2)
-                rem[(q * (NV + 1) + k2) * TW + c] = ld_dsmem_f32(totA + k2 * TW + c, (uint32_t)q);
+                st_async_f32(remA + (band * (NV + 1) + k2) * TW + c, totA[k2 * TW + c], xbarA, (uint32_t)q);
         }
-        __syncthreads();
         if (s == 0) {
+            mbar_wait_cluster(xbarA, (uint32_t)(k & 1));
+            if (c == 0) mbar_arrive_expect_tx(xbarA, xbytesA);
             float ein[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) ein[v] = 0.f;
             for (int q = CB - 1; q > band; --q) {
-                const float Qb = rem[(q * (NV + 1)) * TW + c];
+                const float Qb = remA[(q * (NV + 1)) * TW + c];
 #pragma unroll
-                for (int v = 0; v < NV; ++v) ein[v] = fmaf(Qb, ein[v], rem[(q * (NV + 1) + 1 + v) * TW + c]);
+                for (int v = 0; v < NV; ++v) ein[v] = fmaf(Qb, ein[v], remA[(q * (NV + 1) + 1 + v) * TW + c]);
             }
 #pragma unroll
             for (int v = 0; v < NV; ++v) carry[v * TW + c] = ein[v];

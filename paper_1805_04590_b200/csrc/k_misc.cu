@@ -169,6 +169,54 @@ cudaError_t launch_prologue(const float* target, const float* conf, int Ct, cons
     return cudaGetLastError();
 }
 
+// K4b: the Eq. (3) step as a streaming kernel, used after the
+// cluster column kernel:  Z <- Z - step [lambda (Z - zbar) + chat (Z - T)], zbar = X;
+// on the last iteration the result goes to the HWC output instead of Z.
+// One thread per 4 consecutive pixels of a row (float4 loads of every plane).
+__global__ void __launch_bounds__(256) k_update(const float* __restrict__ X, float* __restrict__ Z,
+                                                const float* __restrict__ T, const float* __restrict__ chat,
+                                                int Ct, Geometry g, float lam, float step,
+                                                float* __restrict__ out_hwc) {
+    const int64_t per_row = g.pitch / 4;
+    const int64_t n = g.H * per_row;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / per_row;
+        const int64_t c4 = (i - r * per_row) * 4;
+        if (c4 >= g.W) continue;
+        const int64_t o = r * g.pitch + c4;
+        const float4 ch = __ldg(reinterpret_cast<const float4*>(chat + o));
+        for (int v = 0; v < Ct; ++v) {
+            const int64_t ov = v * g.plane + o;
+            const float4 zb = __ldg(reinterpret_cast<const float4*>(X + ov));
+            const float4 zo = *reinterpret_cast<const float4*>(Z + ov);
+            const float4 tv = __ldg(reinterpret_cast<const float4*>(T + ov));
+            float4 zn;
+            zn.x = fmaf(-step, fmaf(lam, zo.x - zb.x, ch.x * (zo.x - tv.x)), zo.x);
+            zn.y = fmaf(-step, fmaf(lam, zo.y - zb.y, ch.y * (zo.y - tv.y)), zo.y);
+            zn.z = fmaf(-step, fmaf(lam, zo.z - zb.z, ch.z * (zo.z - tv.z)), zo.z);
+            zn.w = fmaf(-step, fmaf(lam, zo.w - zb.w, ch.w * (zo.w - tv.w)), zo.w);
+            if (out_hwc) {
+                const float zz[4] = {zn.x, zn.y, zn.z, zn.w};
+                for (int u = 0; u < 4; ++u)
+                    if (c4 + u < g.W) out_hwc[(r * g.W + c4 + u) * Ct + v] = zz[u];
+            } else {
+                *reinterpret_cast<float4*>(Z + ov) = zn;
+            }
+        }
+    }
+}
+
+cudaError_t launch_update(const float* X, float* Z, const float* T, const float* chat, int Ct, const Geometry& g,
+                          float lam, float step, float* out_hwc, int num_sms, cudaStream_t s) {
+    const int64_t n = g.H * (g.pitch / 4);
+    int64_t blocks = (n + 255) / 256;
+    const int64_t cap = (int64_t)num_sms * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    k_update<<<(unsigned)blocks, 256, 0, s>>>(X, Z, T, chat, Ct, g, lam, step, out_hwc);
+    return cudaGetLastError();
+}
+
 // opt-in input validation: counters[0] = non-finite target/confidence values,
 // counters[1] = confidences outside [0, 1]
 __global__ void k_check_inputs(const float* __restrict__ target, const float* __restrict__ conf, int Ct, int64_t n,
