@@ -43,7 +43,7 @@ CPU_SAMPLE_ROWS = {"C0": 48, "C1": 1000, "C2": 1024, "C3": 256, "C4": 384}
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -101,7 +101,7 @@ def run_reference(args, cfg):
     cb = cpu_oracle_sample(cfg, steps=max(args.steps, 1), warmup=args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * cb["seconds_per_run"],
-            "higher_is_better": True, "scaling": "strong" if cfg.batch == 1 else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "sample": cb["sample"]},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -170,26 +170,46 @@ def main():
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
 
-    # units of this rank: images (batched configs) or a row band (single-image configs)
+    # units of this rank: images (batched configs: no collective on the data path) or a
+    # row band of the single image (one all-gather of band tuples per column pass)
+    comm = None
+    band = None
+    scaling = "strong"  # the total work is fixed; N GPUs share it
     if cfg.batch > 1:
+        if cfg.batch % world:
+            raise SystemExit(f"{cfg.batch} images do not split over {world} ranks")
         per = cfg.batch // world
         images = list(range(rank * per, (rank + 1) * per))
         inputs = [make_inputs(cfg.name, image=i) for i in images]
-        scaling = "weak" if False else "strong"
+    elif world > 1:
+        r0, r1 = dts.band_rows(cfg.H, world, rank)
+        a, b = dts.band_guide_rows(cfg.H, r0, r1)
+        g, t, c = make_inputs(cfg.name, rows=(a, b))
+        inputs = [(g, np.ascontiguousarray(t[r0 - a:r1 - a]), np.ascontiguousarray(c[r0 - a:r1 - a]))]
+        band = (r0, r1)
+        import torch.distributed as tdist
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(dts.dts_comm_unique_id()), dtype=torch.uint8))
+        tdist.broadcast(uid, 0)
+        comm = dts.dts_comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
     else:
-        if world > 1:
-            raise SystemExit("row-band multi-GPU mode for single-image configs is not built yet")
         inputs = [make_inputs(cfg.name)]
-        scaling = "strong"
-    pixels_rank = sum(g.shape[0] * g.shape[1] for g, _, _ in inputs)
+    pixels_rank = sum(t.shape[0] * t.shape[1] for _, t, _ in inputs)
 
     stream = torch.cuda.Stream(device=dev)
     dev_in = [tuple(torch.from_numpy(a).to(dev) for a in x) for x in inputs]
     outs = [torch.empty_like(t) for _, t, _ in dev_in]
 
+    def make_ctx(g):
+        if band is not None:
+            return dts.dts_create_band(g, cfg.H, band[0], band[1] - band[0], cfg.sigma_s, cfg.sigma_r, cfg.N,
+                                       comm=comm, stream=stream.cuda_stream)
+        return dts.dts_create(g, cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
+
     def step_device():
         for (g, t, c), o in zip(dev_in, outs):
-            ctx = dts.dts_create(g, cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
+            ctx = make_ctx(g)
             dts.dts_solve(ctx, t, c, cfg.lam, cfg.iters, o, stream=stream.cuda_stream)
             dts.dts_destroy(ctx)
 
@@ -247,7 +267,7 @@ def main():
 
         def step_host():
             for (g, t, c), o in zip(host_in, host_out):
-                ctx = dts.dts_create(g, cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
+                ctx = make_ctx(g)
                 dts.dts_solve(ctx, t, c, cfg.lam, cfg.iters, o, stream=stream.cuda_stream)
                 dts.dts_destroy(ctx)
 
@@ -259,6 +279,8 @@ def main():
                "check_max_abs_vs_device": float((host_out[0].to(dev) - outs[0]).abs().max().item())}
 
     if rank != 0:
+        if comm:
+            dts.dts_comm_destroy(comm)
         if world > 1:
             import torch.distributed as tdist
             tdist.destroy_process_group()
@@ -301,12 +323,16 @@ def main():
                                f"{cfg.iters} x 6 pass kernels)",
                        "l2": "inputs larger than L2 (6.4 GB guide, 0.4 GB per state plane): no flush needed"
                              if cfg.name == "C4" else "L2 not flushed between steps",
-                       "parallelism": f"{'image split' if cfg.batch > 1 else 'single image'} x{world}"},
+                       "parallelism": (f"image split x{world}" if cfg.batch > 1 else
+                                       (f"row bands x{world} (NCCL all-gather of column-pass tuples)"
+                                        if world > 1 else "single GPU"))},
             "roofline": roofline,
             "kernels": {k: {kk: v[kk] for kk in ("launches", "avg_ms", "bytes_per_launch", "gbs", "share_of_step")}
                         for k, v in fams.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
     print(json.dumps(line), flush=True)
+    if comm:
+        dts.dts_comm_destroy(comm)
     if world > 1:
         import torch.distributed as tdist
         tdist.destroy_process_group()

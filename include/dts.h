@@ -137,6 +137,40 @@ dts_status dts_profile_read(dts_ctx* ctx, dts_kernel_stat* out, int32_t max, int
 /* Number of kernel launches issued by the library since context creation (all streams). */
 int64_t dts_launch_count(const dts_ctx* ctx);
 
+/* ---- row-band mode: one tall image split across processes / GPUs -------- */
+/* Rows [row0, row0 + rows) of an H_total x W image live on one rank.  Row passes stay
+ * local; every column pass exchanges one 5-tuple per column per rank (an all-gather of
+ * (2 C_t + 3) x W floats) and composes the carries into the rank's rows (DESIGN.md
+ * "Multi-GPU"; reading R20).  Results equal the single-context solve to fp32 rounding. */
+typedef struct dts_comm dts_comm; /* opaque; owned by the library */
+
+/* 128-byte NCCL unique id for dts_comm_init (call on one rank, broadcast the bytes). */
+dts_status dts_comm_unique_id(void* id128);
+/* NCCL communicator over `nranks` processes; rank r owns the r-th band in row order.
+ * The calling thread's current CUDA device is used.  NCCL is loaded at run time
+ * (libnccl.so.2 already in the process, else $DTS_NCCL_LIB); failures -> DTS_E_NCCL. */
+dts_status dts_comm_init(const void* id128, int32_t rank, int32_t nranks, dts_comm** out);
+/* `nranks` communicators for ranks that are host THREADS of this process sharing one
+ * GPU (testing the row-band algebra without several GPUs): comms[r] for r < nranks.
+ * Each thread drives its own context on its own stream; collective calls rendezvous
+ * on the host. */
+dts_status dts_comm_init_loopback(int32_t nranks, dts_comm** comms);
+void dts_comm_destroy(dts_comm* comm); /* NULL-safe; destroy after the contexts using it */
+
+/* dts_create_band -- like dts_create for rows [row0, row0 + rows) of an H_total-row image.
+ *   guide_with_halo  (rows + above + below) x W x C, HWC: the band's guide rows preceded
+ *                    by the row above (above = 1 if row0 > 0, else 0) and followed by the
+ *                    row below (below = 1 if row0 + rows < H_total) -- needed for the
+ *                    vertical domain distances at the seams (R20).
+ *   comm             communicator whose ranks own consecutive bands in rank order; NULL
+ *                    only for a single band (row0 = 0, rows = H_total).
+ * COLLECTIVE: every rank of `comm` calls dts_create_band (and later dts_solve, with the
+ * same target_channels / lambda / iterations) with its own band.  dts_solve on a band
+ * context takes and returns the band's rows (rows x W target / confidence / out). */
+dts_status dts_create_band(const float* guide_with_halo, int64_t H_total, int64_t row0, int64_t rows,
+                           int64_t W, int32_t C, float sigma_s, float sigma_r, int32_t filter_passes,
+                           dts_comm* comm, void* stream, dts_ctx** out_ctx);
+
 /* Library version string. */
 const char* dts_version(void);
 

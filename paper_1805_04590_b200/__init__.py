@@ -18,6 +18,8 @@ import os
 import numpy as np
 
 __all__ = ["DTSError", "dts_create", "dts_solve", "dts_solve_ex", "dts_destroy", "dts_status_string",
+           "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback", "dts_comm_destroy",
+           "dts_create_band", "band_rows", "band_guide_rows",
            "dts_debug_read", "dts_profile_enable", "dts_profile_read", "dts_launch_count", "dts_version",
            "Solver", "lib_path", "load_library", "DTS_BUF_DX", "DTS_BUF_DY", "DTS_BUF_SUPPORT",
            "ABI_FUNCTIONS"]
@@ -31,7 +33,8 @@ DTS_BUF_DX, DTS_BUF_DY, DTS_BUF_SUPPORT = 0, 1, 2
 # every symbol declared in include/dts.h
 ABI_FUNCTIONS = ["dts_create", "dts_solve", "dts_destroy", "dts_status_string", "dts_last_error_string",
                  "dts_solve_ex", "dts_debug_read", "dts_profile_enable", "dts_profile_read",
-                 "dts_launch_count", "dts_version"]
+                 "dts_launch_count", "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback",
+                 "dts_comm_destroy", "dts_create_band", "dts_version"]
 
 
 class DTSError(RuntimeError):
@@ -88,6 +91,16 @@ def load_library():
     lib.dts_launch_count.restype = i64
     lib.dts_version.argtypes = []
     lib.dts_version.restype = ctypes.c_char_p
+    lib.dts_comm_unique_id.argtypes = [vp]
+    lib.dts_comm_unique_id.restype = ctypes.c_int
+    lib.dts_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
+    lib.dts_comm_init.restype = ctypes.c_int
+    lib.dts_comm_init_loopback.argtypes = [i32, ctypes.POINTER(vp)]
+    lib.dts_comm_init_loopback.restype = ctypes.c_int
+    lib.dts_comm_destroy.argtypes = [vp]
+    lib.dts_comm_destroy.restype = None
+    lib.dts_create_band.argtypes = [vp, i64, i64, i64, i64, i32, f32, f32, i32, vp, vp, ctypes.POINTER(vp)]
+    lib.dts_create_band.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -199,6 +212,64 @@ def dts_profile_read(ctx: int):
 
 def dts_launch_count(ctx: int) -> int:
     return int(load_library().dts_launch_count(ctx))
+
+
+# ---- row-band mode (multi-GPU) -------------------------------------------------
+
+def band_rows(H: int, nranks: int, rank: int):
+    """Rows [row0, row1) owned by `rank` when H rows are split over `nranks` ranks:
+    row0 = floor(rank H / nranks)."""
+    if not (0 <= rank < nranks):
+        raise ValueError("rank out of range")
+    return (rank * H) // nranks, ((rank + 1) * H) // nranks
+
+
+def band_guide_rows(H: int, row0: int, row1: int):
+    """Guide rows a band context needs: its rows plus one halo row above / below where
+    a neighbouring band exists (include/dts.h dts_create_band)."""
+    return max(row0 - 1, 0), min(row1 + 1, H)
+
+
+def dts_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().dts_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)), "dts_comm_unique_id")
+    return buf.raw
+
+
+def dts_comm_init(uid: bytes, rank: int, nranks: int) -> int:
+    if len(uid) != 128:
+        raise ValueError("unique id must be 128 bytes")
+    buf = ctypes.create_string_buffer(uid, 128)
+    comm = ctypes.c_void_p()
+    _check(load_library().dts_comm_init(ctypes.cast(buf, ctypes.c_void_p), rank, nranks, ctypes.byref(comm)),
+           "dts_comm_init")
+    return comm.value
+
+
+def dts_comm_init_loopback(nranks: int):
+    arr = (ctypes.c_void_p * nranks)()
+    _check(load_library().dts_comm_init_loopback(nranks, arr), "dts_comm_init_loopback")
+    return [arr[i] for i in range(nranks)]
+
+
+def dts_comm_destroy(comm: int) -> None:
+    if comm:
+        load_library().dts_comm_destroy(comm)
+
+
+def dts_create_band(guide_with_halo, H_total: int, row0: int, rows: int, sigma_s: float, sigma_r: float,
+                    filter_passes: int = 3, comm=None, stream=None) -> int:
+    """guide_with_halo: the band's guide rows plus halo rows (see band_guide_rows)."""
+    if len(guide_with_halo.shape) == 2:
+        W, C = guide_with_halo.shape[1], 1
+    else:
+        W, C = guide_with_halo.shape[1], guide_with_halo.shape[2]
+    ctx = ctypes.c_void_p()
+    st = load_library().dts_create_band(_ptr(guide_with_halo, "guide"), H_total, row0, rows, W, C, sigma_s,
+                                        sigma_r, filter_passes, comm, _stream(stream, guide_with_halo),
+                                        ctypes.byref(ctx))
+    _check(st, "dts_create_band")
+    return ctx.value
 
 
 class Solver:

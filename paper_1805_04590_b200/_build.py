@@ -14,8 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdts_b200.so")
-SOURCES = ["k_misc.cu", "k_row.cu", "k_col.cu", "k_colc.cu", "dts_capi.cu"]
-HEADERS = ["dts_device.cuh", "dts_launch.h"]
+SOURCES = ["k_misc.cu", "k_row.cu", "k_col.cu", "k_colc.cu", "dts_comm.cu", "dts_capi.cu"]
+HEADERS = ["dts_device.cuh", "dts_launch.h", "dts_comm.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include")]
@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             subprocess.check_call(cmd)
     if force or _stale(LIB, objs):
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-               "-o", LIB, *objs]
+               "-o", LIB, *objs, "-ldl"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)

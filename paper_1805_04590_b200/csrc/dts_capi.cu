@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/dts.h"
+#include "dts_comm.h"
 #include "dts_launch.h"
 
 using namespace dts;
@@ -66,8 +67,22 @@ std::once_flag g_pool_once;
 
 }  // namespace
 
+struct dts_comm {
+    dts::Comm* c = nullptr;
+};
+
 struct dts_ctx {
     int device = 0;
+    // row-band mode (multi-GPU): this context owns rows [row0, row0 + g.H) of H_total
+    dts::Comm* comm = nullptr;
+    int64_t row0 = 0, H_total = 0;
+    int halo_above = 0, halo_below = 0;
+    float* dx_base = nullptr;  // allocations behind dx / dy (they include the halo rows)
+    float* dy_base = nullptr;
+    float* rank_tup = nullptr;  // this rank's aggregate tuples   [ntiles][2NV+3][32]
+    float* gathered = nullptr;  // all ranks' tuples               [P][ntiles][2NV+3][32]
+    float* ext = nullptr;       // carries into this rank's rows   [ntiles][2][NV][32]
+    size_t band_cap = 0;
     int num_sms = 148;
     Geometry g{};
     int C = 0;
@@ -101,9 +116,13 @@ struct dts_ctx {
 
 namespace {
 
-enum Family { F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP, F_COUNT };
-const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update",
-                                     "support_row", "support_col", "prologue", "update"};
+enum Family {
+    F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
+    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_COUNT
+};
+const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
+                                     "support_col", "prologue", "update", "col_tuple", "exchange",
+                                     "rank_compose"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -247,12 +266,75 @@ cudaError_t col_launch(dts_ctx* ctx, const ColPlan& plan, int Ct, int mode, floa
 }
 
 ColScratch next_scratch(dts_ctx* ctx) {
-    ColScratch sc;
+    ColScratch sc = {};
+    sc.phase = PHASE_FULL;
     sc.tuples = ctx->tuples;
     sc.flags = ctx->flags;
     sc.epoch = ++ctx->epoch;
     if (sc.epoch == 0) sc.epoch = ++ctx->epoch;  // flags start at 0: never reuse 0
     return sc;
+}
+
+dts_status ensure_band_buffers(dts_ctx* ctx, cudaStream_t s) {
+    const int ntiles = (int)((ctx->g.W + 31) / 32);
+    const size_t per = (size_t)ntiles * 11 * 32;  // 2NV+3 <= 11 floats per column (NV <= 4)
+    if (ctx->band_cap >= per) return DTS_OK;
+    cudaError_t e;
+    for (float** p : {&ctx->rank_tup, &ctx->gathered, &ctx->ext}) {
+        if (*p) cudaFreeAsync(*p, s);
+        *p = nullptr;
+    }
+    if ((e = cudaMallocAsync((void**)&ctx->rank_tup, per * sizeof(float), s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->gathered, per * ctx->comm->nranks * sizeof(float), s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->ext, per * sizeof(float), s)) != cudaSuccess)
+        return cuda_fail(e);
+    ctx->band_cap = per;
+    return DTS_OK;
+}
+
+// One column pass of a row-band context: every rank emits the
+// aggregate 5-tuple of its rows per column (TUPLE), the tuples are all-gathered (NVLink
+// via NCCL, or the loopback transport), each rank composes the carries into its rows,
+// and the pass is finished with those carries (APPLY).
+dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, const UpdateArgs* upd,
+                           float* support, int fam, double bytes, cudaStream_t s) {
+    const Geometry& g = ctx->g;
+    ColPlan plan;
+    if (plan_col_pass(g, Ct, mode, ctx->num_sms, &plan) != cudaSuccess) return DTS_E_SHAPE;
+    dts_status st;
+    if ((st = ensure_col_scratch(ctx, plan, s)) != DTS_OK) return st;
+    if ((st = ensure_band_buffers(ctx, s)) != DTS_OK) return st;
+    const int NV = mode == MODE_SUPPORT ? 1 : Ct;
+    const size_t count = (size_t)plan.ntiles * (2 * NV + 3) * 32;
+    const double px = (double)g.H * g.W;
+    st = run_launch(ctx, F_TUPLE, px * (4.0 * (mode == MODE_SUPPORT ? 0 : NV) + 4), s, [&] {
+        ColScratch sc = next_scratch(ctx);
+        sc.phase = PHASE_TUPLE;
+        sc.halo_below = ctx->halo_below;
+        sc.rank_tuples = ctx->rank_tup;
+        return launch_col_pass(plan, g, Ct, mode, x, ctx->dy, kc, upd, support, sc, s);
+    });
+    if (st != DTS_OK) return st;
+    std::string err;
+    st = run_launch(ctx, F_EXCHANGE, (double)count * 4 * ctx->comm->nranks, s, [&] {
+        return comm_allgather(ctx->comm, ctx->rank_tup, ctx->gathered, count, s, &err) ? cudaSuccess
+                                                                                        : cudaErrorUnknown;
+    });
+    if (st != DTS_OK) {
+        g_last_error = err;
+        return DTS_E_NCCL;
+    }
+    st = run_launch(ctx, F_COMPOSE, 0.0, s, [&] {
+        return launch_rank_compose(ctx->gathered, ctx->comm->nranks, ctx->comm->rank, plan.ntiles, NV, ctx->ext, s);
+    });
+    if (st != DTS_OK) return st;
+    return run_launch(ctx, fam, bytes, s, [&] {
+        ColScratch sc = next_scratch(ctx);
+        sc.phase = PHASE_APPLY;
+        sc.halo_below = ctx->halo_below;
+        sc.ext = ctx->ext;
+        return launch_col_pass(plan, g, Ct, mode, x, ctx->dy, kc, upd, support, sc, s);
+    });
 }
 
 }  // namespace
@@ -277,11 +359,14 @@ const char* dts_status_string(dts_status s) {
 
 const char* dts_last_error_string(void) { return g_last_error.c_str(); }
 
-dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float sigma_s, float sigma_r,
-                      int32_t filter_passes, void* stream, dts_ctx** out_ctx) {
+static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0, int64_t H, int64_t W, int32_t C,
+                              float sigma_s, float sigma_r, int32_t filter_passes, dts::Comm* comm, void* stream,
+                              dts_ctx** out_ctx) {
     if (!out_ctx || !guide) return DTS_E_ARG;
     *out_ctx = nullptr;
     if (H < 1 || W < 1 || C < 1) return DTS_E_ARG;
+    if (row0 < 0 || row0 + H > H_total) return DTS_E_ARG;
+    if (!comm && (row0 != 0 || H != H_total)) return DTS_E_ARG;
     if (!finite_pos(sigma_s) || !finite_pos(sigma_r)) return DTS_E_ARG;
     if (filter_passes < 1 || filter_passes > 16) return DTS_E_ARG;
     if (W > 18432 || H > (int64_t)1 << 30 || C > 4096) return DTS_E_SHAPE;
@@ -306,6 +391,12 @@ dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float
 
     dts_ctx* ctx = new dts_ctx();
     ctx->device = device;
+    ctx->comm = comm;
+    ctx->row0 = row0;
+    ctx->H_total = H_total;
+    ctx->halo_above = row0 > 0 ? 1 : 0;
+    ctx->halo_below = row0 + H < H_total ? 1 : 0;
+    const int64_t Hx = H + ctx->halo_above + ctx->halo_below;  // guide rows passed in
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
     ctx->g.H = H;
     ctx->g.W = W;
@@ -328,7 +419,8 @@ dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float
     RowPlan rp;
     ColPlan cp;
     if (plan_row_pass(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &rp) != cudaSuccess ||
-        plan_col(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &cp) != cudaSuccess) {
+        (comm ? plan_col_pass(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &cp)
+              : plan_col(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &cp)) != cudaSuccess) {
         delete ctx;
         return DTS_E_SHAPE;
     }
@@ -342,15 +434,18 @@ dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float
         delete ctx;
         return DTS_E_ARG;
     }
-    if ((e = cudaMallocAsync((void**)&ctx->dx, plane, s)) != cudaSuccess ||
-        (e = cudaMallocAsync((void**)&ctx->dy, plane, s)) != cudaSuccess ||
+    const size_t plane_x = (size_t)Hx * ctx->g.pitch * sizeof(float);
+    if ((e = cudaMallocAsync((void**)&ctx->dx_base, plane_x, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->dy_base, plane_x, s)) != cudaSuccess ||
         (e = cudaMallocAsync((void**)&ctx->S, plane, s)) != cudaSuccess ||
         (e = cudaMallocAsync((void**)&ctx->counters, 2 * sizeof(unsigned int), s)) != cudaSuccess) {
         st = cuda_fail(e);
         dts_destroy(ctx);
         return st;
     }
-    const size_t gbytes = (size_t)H * W * C * sizeof(float);
+    ctx->dx = ctx->dx_base + ctx->halo_above * ctx->g.pitch;
+    ctx->dy = ctx->dy_base + ctx->halo_above * ctx->g.pitch;
+    const size_t gbytes = (size_t)Hx * W * C * sizeof(float);
     if (gk == PTR_HOST) {
         if ((e = cudaMallocAsync((void**)&gstage, gbytes, s)) != cudaSuccess ||
             (e = cudaMemcpyAsync(gstage, guide, gbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
@@ -363,17 +458,26 @@ dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float
     }
     const float ratio = sigma_s / sigma_r;
     const double px = (double)H * W;
-    st = run_launch(ctx, F_DERIV, px * (4.0 * C + 8.0), s,
-                    [&] { return launch_guide_deriv(gdev, C, ratio * ratio, ctx->g, ctx->dx, ctx->dy, s); });
+    Geometry gx = ctx->g;  // the guide rows including halos
+    gx.H = Hx;
+    gx.plane = Hx * gx.pitch;
+    st = run_launch(ctx, F_DERIV, px * (4.0 * C + 8.0), s, [&] {
+        return launch_guide_deriv(gdev, C, ratio * ratio, gx, ctx->dx_base, ctx->dy_base, s);
+    });
     if (st == DTS_OK)
         st = run_launch(ctx, F_SUPPORT_ROW, px * 8.0, s, [&] {
             return launch_row_pass(rp, ctx->g, 1, MODE_SUPPORT, nullptr, ctx->S, ctx->dx, ctx->ks, s);
         });
     if (st == DTS_OK) st = ensure_col_scratch(ctx, cp, s);
-    if (st == DTS_OK)
-        st = run_launch(ctx, F_SUPPORT_COL, px * 12.0, s, [&] {
-            return col_launch(ctx, cp, 1, MODE_SUPPORT, nullptr, ctx->dy, ctx->ks, nullptr, ctx->S, s);
-        });
+    if (st == DTS_OK) {
+        if (comm)
+            st = col_pass_banded(ctx, 1, MODE_SUPPORT, nullptr, ctx->ks, nullptr, ctx->S, F_SUPPORT_COL, px * 12.0,
+                                 s);
+        else
+            st = run_launch(ctx, F_SUPPORT_COL, px * 12.0, s, [&] {
+                return col_launch(ctx, cp, 1, MODE_SUPPORT, nullptr, ctx->dy, ctx->ks, nullptr, ctx->S, s);
+            });
+    }
     if (gstage) {
         cudaFreeAsync(gstage, s);
         if (st == DTS_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess) st = cuda_fail(e);
@@ -385,6 +489,56 @@ dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float
     ctx->last_stream = s;
     *out_ctx = ctx;
     return DTS_OK;
+}
+
+dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float sigma_s, float sigma_r,
+                      int32_t filter_passes, void* stream, dts_ctx** out_ctx) {
+    return create_impl(guide, H, 0, H, W, C, sigma_s, sigma_r, filter_passes, nullptr, stream, out_ctx);
+}
+
+dts_status dts_create_band(const float* guide_with_halo, int64_t H_total, int64_t row0, int64_t rows, int64_t W,
+                           int32_t C, float sigma_s, float sigma_r, int32_t filter_passes, dts_comm* comm,
+                           void* stream, dts_ctx** out_ctx) {
+    if (!comm) return create_impl(guide_with_halo, H_total, row0, rows, W, C, sigma_s, sigma_r, filter_passes,
+                                  nullptr, stream, out_ctx);
+    return create_impl(guide_with_halo, H_total, row0, rows, W, C, sigma_s, sigma_r, filter_passes, comm->c, stream,
+                       out_ctx);
+}
+
+dts_status dts_comm_unique_id(void* id128) {
+    if (!id128) return DTS_E_ARG;
+    std::string err;
+    if (!dts::nccl_unique_id(id128, &err)) {
+        g_last_error = err;
+        return DTS_E_NCCL;
+    }
+    return DTS_OK;
+}
+
+dts_status dts_comm_init(const void* id128, int32_t rank, int32_t nranks, dts_comm** out) {
+    if (!id128 || !out || nranks < 1 || rank < 0 || rank >= nranks || nranks > 64) return DTS_E_ARG;
+    *out = nullptr;
+    std::string err;
+    dts::Comm* c = dts::comm_nccl(id128, rank, nranks, &err);
+    if (!c) {
+        g_last_error = err;
+        return DTS_E_NCCL;
+    }
+    *out = new dts_comm{c};
+    return DTS_OK;
+}
+
+dts_status dts_comm_init_loopback(int32_t nranks, dts_comm** comms) {
+    if (!comms || nranks < 1 || nranks > 64) return DTS_E_ARG;
+    std::vector<dts::Comm*> v = dts::comm_loopback(nranks);
+    for (int r = 0; r < nranks; ++r) comms[r] = new dts_comm{v[r]};
+    return DTS_OK;
+}
+
+void dts_comm_destroy(dts_comm* comm) {
+    if (!comm) return;
+    dts::comm_destroy(comm->c);
+    delete comm;
 }
 
 dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const float* confidence, float lambda,
@@ -408,8 +562,10 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     RowPlan rp;
     ColPlan cpf, cpu;
     if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess ||
-        plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf) != cudaSuccess ||
-        plan_col(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu) != cudaSuccess)
+        (ctx->comm ? plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)
+                   : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess ||
+        (ctx->comm ? plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu)
+                   : plan_col(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu)) != cudaSuccess)
         return DTS_E_SHAPE;
 
     const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),
@@ -466,7 +622,22 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                     return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
                 });
                 if (st != DTS_OK) return st;
-                if (i + 1 < ctx->N) {
+                if (ctx->comm) {  // row-band mode: TUPLE -> all-gather -> compose -> APPLY
+                    if (i + 1 < ctx->N) {
+                        st = col_pass_banded(ctx, Ct, MODE_FILTER, ctx->X, ctx->kc[i], nullptr, nullptr, F_COL,
+                                             row_bytes, s);
+                    } else {
+                        UpdateArgs u;
+                        u.Z = ctx->Z;
+                        u.T = ctx->T;
+                        u.chat = ctx->chat;
+                        u.lam = lambda;
+                        u.step = step;
+                        u.out_hwc = (k + 1 == iterations) ? o_d : nullptr;
+                        st = col_pass_banded(ctx, Ct, MODE_UPDATE, ctx->X, ctx->kc[i], &u, nullptr, F_UPDATE,
+                                             upd_bytes, s);
+                    }
+                } else if (i + 1 < ctx->N) {
                     st = run_launch(ctx, F_COL, row_bytes, s, [&] {
                         return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
                                           s);
@@ -517,7 +688,8 @@ void dts_destroy(dts_ctx* ctx) {
     if (!ctx) return;
     cudaStream_t s = ctx->last_stream;
     free_solver_state(ctx, s);
-    for (float** p : {&ctx->dx, &ctx->dy, &ctx->S, &ctx->st_t, &ctx->st_c, &ctx->st_o}) {
+    for (float** p : {&ctx->dx_base, &ctx->dy_base, &ctx->S, &ctx->st_t, &ctx->st_c, &ctx->st_o, &ctx->rank_tup,
+                      &ctx->gathered, &ctx->ext}) {
         if (*p) cudaFreeAsync(*p, s);
         *p = nullptr;
     }

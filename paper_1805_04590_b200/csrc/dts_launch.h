@@ -6,6 +6,9 @@
 namespace dts {
 
 enum PassMode : int { MODE_FILTER = 0, MODE_UPDATE = 1, MODE_SUPPORT = 2 };
+// column-pass phases (row-band mode): FULL = single band set; TUPLE = emit the aggregate
+// 5-tuple of this rank's rows; APPLY = finish with external carries (after the exchange)
+enum ColPhase : int { PHASE_FULL = 0, PHASE_TUPLE = 1, PHASE_APPLY = 2 };
 
 // Internal planar layout: every H x W plane has row pitch `pitch` floats (a multiple
 // of 32, so every row starts 128-B aligned); channel planes are `plane` floats apart.
@@ -40,6 +43,11 @@ struct ColScratch {
     float* tuples;         // >= plan.tuple_floats floats
     unsigned int* flags;   // >= plan.flag_count, zero-initialised once
     unsigned int epoch;    // distinct per launch (flags are compared against it)
+    // row-band mode
+    int phase;             // ColPhase
+    int halo_below;        // the d array has a row H (link to the rank below)
+    const float* ext;      // APPLY: [ntiles][2][NV][32] carries into the rank band
+    float* rank_tuples;    // TUPLE: [ntiles][2NV+3][32]
 };
 struct UpdateArgs {
     float* Z;            // planar state (read; written unless out_hwc)
@@ -62,6 +70,11 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
 // K4b: Eq. (3) update as a streaming kernel (zbar in X); writes Z, or out_hwc when non-null.
 cudaError_t launch_update(const float* X, float* Z, const float* T, const float* chat, int Ct, const Geometry& g,
                           float lam, float step, float* out_hwc, int num_sms, cudaStream_t s);
+
+// compose gathered rank tuples [P][ntiles][2NV+3][32] into this rank's carries
+// [ntiles][2][NV][32] (causal carry from the ranks above, anticausal from below)
+cudaError_t launch_rank_compose(const float* gathered, int P, int rank, int ntiles, int NV, float* ext,
+                                cudaStream_t s);
 
 // K6: solve prologue -- planar Z = T = target, chat = c / S (or c when support_mode = 1).
 cudaError_t launch_prologue(const float* target, const float* conf, int Ct, const Geometry& g, const float* S,

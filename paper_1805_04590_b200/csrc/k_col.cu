@@ -51,6 +51,11 @@ struct ColParams {
     int H, W, HB, S, Ls, nb, ntiles, nitems;
     unsigned int epoch;
     float kc;
+    // row-band (multi-GPU) support: this grid covers rows [0, H) of a taller image
+    int phase;                // PHASE_FULL, PHASE_TUPLE (emit the rank tuple only), PHASE_APPLY
+    int halo_below;           // d row H exists: coefficient linking row H-1 to the next rank's row 0
+    const float* ext;         // APPLY: [ntiles][2][NV][TW] causal carry in (top), anticausal carry in (bottom)
+    float* rank_tuples;       // TUPLE: [ntiles][NTUP][TW] aggregate tuple of rows [0, H)
 };
 
 // tuple components: A, B[NV], Q, Z0[NV], Sresp  (NTUP = 2 NV + 3)
@@ -78,8 +83,8 @@ __host__ __device__ inline ColSmem col_smem_layout(int NV, int HB, int S, int nb
     o += (NV + 2) * TW;
     L.tup = o;  // the tile's band tuples, staged from global [nb][NTUP][TW]
     o += nb * (2 * NV + 3) * TW;
-    L.cj = o;  // causal carries of every band of the tile [nb][NV][TW]
-    o += nb * NV * TW;
+    L.cj = o;  // causal carries of every band of the tile [nb][NV][TW] (TUPLE: [nb][NV+1][TW])
+    o += nb * (NV + 1) * TW;
     L.carry = o;  // c[NV][TW], e[NV][TW]
     o += 2 * NV * TW;
     o = (o + 1) & ~1;  // 8-B alignment for the mbarriers
@@ -170,6 +175,18 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
 
+    // Coefficient of row `row` as seen by the anticausal step of row-1 (R4, R20): the
+    // filter coefficient inside [0, H); at row H the link to the rank below (halo) or 0
+    // at the image bottom; pass-through (1) on padding rows beyond, so that a carry
+    // entering at the band bottom reaches row H-1 unchanged.  The causal step of a
+    // padding row uses 1 as well (see causal()).
+    auto coefA = [&](int row, bool colok, float dv) -> float {
+        if (!colok) return 0.f;
+        if (row < p.H) return coef_from_d(dv, p.kc);
+        if (row == p.H) return p.halo_below ? coef_from_d(dv, p.kc) : 0.f;
+        return 1.f;
+    };
+
     // issue the TMA loads of `item` (thread 0) and its halo coefficient (warp 0)
     auto stage_in = [&](int item) {
         const int t = item / nb;
@@ -195,7 +212,8 @@ __global__ void __launch_bounds__(256)
         if (s == 0) {
             const int rh = r0 + HB;
             const int cl = col0 + c;
-            As[HB * TW + c] = (cl < p.W && rh < p.H) ? coef_from_d(p.d[(int64_t)rh * p.pitch + cl], p.kc) : 0.f;
+            const bool inb = cl < p.W && (rh < p.H || (rh == p.H && p.halo_below));
+            As[HB * TW + c] = coefA(rh, cl < p.W, inb ? p.d[(int64_t)rh * p.pitch + cl] : 0.f);
         }
     };
 
@@ -218,23 +236,26 @@ __global__ void __launch_bounds__(256)
         for (int j = 0; j < LS; ++j) {
             const int rr = lo + j;
             const bool ok = colok && (r0 + rr) < p.H;
-            a[j] = ok ? coef_from_d(As[rr * TW + c], p.kc) : 0.f;
+            a[j] = coefA(r0 + rr, colok, As[rr * TW + c]);
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 if constexpr (HASX) xv[v][j] = ok ? xs[(v * HB + rr) * TW + c] : 0.f;
                 else xv[v][j] = 0.f;
             }
         }
+        // causal coefficient of local row j: padding rows beyond H pass the state through
+        auto causal = [&](int j) -> float { return (colok && r0 + lo + j >= p.H) ? 1.f : a[j]; };
         // causal fold
         {
             Aff<NV> m = aff_identity<NV>();
 #pragma unroll
             for (int j = 0; j < LS; ++j) {
-                m.P *= a[j];
+                const float aj = causal(j);
+                m.P *= aj;
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
-                    if constexpr (HASX) m.B[v] = fmaf(a[j], m.B[v] - xv[v][j], xv[v][j]);
-                    else m.B[v] = fmaf(a[j], m.B[v], 1.f);
+                    if constexpr (HASX) m.B[v] = fmaf(aj, m.B[v] - xv[v][j], xv[v][j]);
+                    else m.B[v] = fmaf(aj, m.B[v], (colok && r0 + lo + j >= p.H) ? 0.f : 1.f);
                 }
             }
             segF[(0 * S + s) * (TW + 1) + c] = m.P;
@@ -248,7 +269,7 @@ __global__ void __launch_bounds__(256)
         float anext;
         {
             const int rn = r0 + lo + LS;
-            if (s + 1 < S) anext = (colok && rn < p.H) ? coef_from_d(As[(lo + LS) * TW + c], p.kc) : 0.f;
+            if (s + 1 < S) anext = coefA(rn, colok, As[(lo + LS) * TW + c]);
             else anext = As[HB * TW + c];  // halo (already a coefficient)
         }
         __syncthreads();  // (the landing zone is free from here on)
@@ -270,20 +291,22 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int j = 0; j < LS; ++j) {
                 const float an = (j + 1 < LS) ? a[j + 1] : anext;
-                y1 *= a[j];
+                const float aj = causal(j);
+                const bool valid = !(colok && r0 + lo + j >= p.H);
+                y1 *= aj;
                 if constexpr (HASX) {
                     const float qb = Q * (1.f - an);
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
-                        y0[v] = fmaf(a[j], y0[v] - xv[v][j], xv[v][j]);
+                        y0[v] = fmaf(aj, y0[v] - xv[v][j], xv[v][j]);
                         xv[v][j] = y0[v];
                         E0[v] = fmaf(qb, y0[v], E0[v]);
                     }
                     E1 = fmaf(qb, y1, E1);
                 } else {
-                    y0[0] = fmaf(a[j], y0[0], 1.f);
+                    y0[0] = fmaf(aj, y0[0], valid ? 1.f : 0.f);
                     xv[0][j] = y0[0];
-                    E0[0] += Q;  // anticausal input is 1, independent of c
+                    if (valid) E0[0] += Q;  // anticausal input is 1 on valid rows, independent of c
                 }
                 Q *= an;
             }
@@ -336,10 +359,51 @@ __global__ void __launch_bounds__(256)
                 }
             }
             __syncthreads();
-            if (s == 0) {
-                float cv[NV];  // causal carries c_j (c_0 = 0: A = 0 at the top row)
+            if (s == 0 && p.phase == PHASE_TUPLE) {
+                // aggregate tuple of all local bands, symbolic in the carries (c, e) of the
+                // rank band:  c_j = Ac c + Bc (top-down), e_{j-1} = Ze + Se c + Qe e (bottom-up)
+                float Ac = 1.f, Bc[NV];
 #pragma unroll
-                for (int v = 0; v < NV; ++v) cv[v] = 0.f;
+                for (int v = 0; v < NV; ++v) Bc[v] = 0.f;
+                for (int j = 0; j < nb; ++j) {
+                    const float* tj = tupS + j * NT * TW;
+                    cj[(j * (NV + 1) + 0) * TW + c] = Ac;  // park (Ac_j, Bc_j)
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) cj[(j * (NV + 1) + 1 + v) * TW + c] = Bc[v];
+                    const float A = tj[c];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) Bc[v] = fmaf(A, Bc[v], tj[(1 + v) * TW + c]);
+                    Ac *= A;
+                }
+                float Ze[NV], Se = 0.f, Qe = 1.f;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) Ze[v] = 0.f;
+                for (int j = nb - 1; j >= 0; --j) {
+                    const float* tj = tupS + j * NT * TW;
+                    const float Qj = tj[(1 + NV) * TW + c];
+                    const float Sj = tj[(2 + 2 * NV) * TW + c];
+                    const float Acj = cj[(j * (NV + 1) + 0) * TW + c];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v)
+                        Ze[v] = fmaf(Qj, Ze[v], fmaf(Sj, cj[(j * (NV + 1) + 1 + v) * TW + c], tj[(2 + NV + v) * TW + c]));
+                    Se = fmaf(Qj, Se, Sj * Acj);
+                    Qe *= Qj;
+                }
+                float* rt = p.rank_tuples + (int64_t)t * NT * TW;
+                rt[0 * TW + c] = Ac;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) rt[(1 + v) * TW + c] = Bc[v];
+                rt[(1 + NV) * TW + c] = Qe;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) rt[(2 + NV + v) * TW + c] = Ze[v];
+                rt[(2 + 2 * NV) * TW + c] = Se;
+                __syncwarp();
+                if (c == 0) p.counters[t] = 0u;  // ready for the next launch
+            } else if (s == 0) {
+                const float* ext = p.phase == PHASE_APPLY ? p.ext + (int64_t)t * 2 * NV * TW : nullptr;
+                float cv[NV];  // causal carries c_j (c_0 = carry into the rank band, 0 on a single GPU)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) cv[v] = ext ? ext[v * TW + c] : 0.f;
                 for (int j = 0; j < nb; ++j) {
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
@@ -351,9 +415,9 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
                     for (int v = 0; v < NV; ++v) cv[v] = fmaf(A, cv[v], tj[(1 + v) * TW + c]);
                 }
-                float ev[NV];  // anticausal carries: e_{j-1} = Z0_j + Sresp_j c_j + Q_j e_j, e_last = 0
+                float ev[NV];  // anticausal carries: e_{j-1} = Z0_j + Sresp_j c_j + Q_j e_j, e_last = carry in
 #pragma unroll
-                for (int v = 0; v < NV; ++v) ev[v] = 0.f;
+                for (int v = 0; v < NV; ++v) ev[v] = ext ? ext[(NV + v) * TW + c] : 0.f;
                 for (int j = nb - 1; j >= 0; --j) {
 #pragma unroll
                     for (int v = 0; v < NV; ++v) car_tile[((int64_t)(j * 2 + 1) * NV + v) * TW + c] = ev[v];
@@ -371,6 +435,10 @@ __global__ void __launch_bounds__(256)
                     st_release_u32(p.flags + t, p.epoch);
                 }
             }
+        }
+        if (p.phase == PHASE_TUPLE) {  // only the tuples were wanted
+            __syncthreads();
+            continue;
         }
         if (s == 0) {
             if (c == 0)
@@ -392,7 +460,7 @@ __global__ void __launch_bounds__(256)
             float y1 = segF[(0 * S + s) * (TW + 1) + c];
 #pragma unroll
             for (int j = 0; j < LS; ++j) {
-                y1 *= a[j];
+                y1 *= causal(j);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) xv[v][j] = fmaf(y1, cv[v], xv[v][j]);
             }
@@ -411,7 +479,8 @@ __global__ void __launch_bounds__(256)
                         z[v] = fmaf(an, z[v] - yv, yv);
                         xv[v][j] = z[v];
                     } else {
-                        z[v] = fmaf(an, z[v], 1.f);
+                        const bool valid = !(colok && r0 + lo + j >= p.H);
+                        z[v] = fmaf(an, z[v], valid ? 1.f : 0.f);
                         xv[v][j] = yv + z[v] - 1.f;  // s_y = P + Q - 1
                     }
                 }
@@ -473,6 +542,43 @@ __global__ void __launch_bounds__(256)
         }
         __syncthreads();  // segF / segR / tuples are rewritten by the next item
     }
+}
+
+// Row-band exchange, second half: from the gathered rank tuples (in rank order) compute
+// the carries into rank `rank`:  c_{q+1} = A_q c_q + B_q (c_0 = 0, the image top);
+// e_{q-1} = Z0_q + S_q c_q + Q_q e_q (e_{P-1} = 0, the image bottom).  One thread per column.
+__global__ void k_rank_compose(const float* __restrict__ g, int P, int rank, int ntiles, int NV,
+                               float* __restrict__ ext) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ntiles * TW) return;
+    const int t = i / TW, c = i - t * TW;
+    const int NT = 2 * NV + 3;
+    const int64_t rstride = (int64_t)ntiles * NT * TW;  // one rank's tuples
+    const float* base = g + (int64_t)t * NT * TW + c;
+    for (int v = 0; v < NV; ++v) {
+        float cq[64];
+        float cv = 0.f;
+        for (int q = 0; q < P; ++q) {
+            cq[q] = cv;
+            const float* tq = base + q * rstride;
+            cv = fmaf(tq[0], cv, tq[(1 + v) * TW]);
+        }
+        float ev = 0.f;
+        for (int q = P - 1; q > rank; --q) {
+            const float* tq = base + q * rstride;
+            ev = fmaf(tq[(1 + NV) * TW], ev, fmaf(tq[(2 + 2 * NV) * TW], cq[q], tq[(2 + NV + v) * TW]));
+        }
+        ext[((int64_t)t * 2 * NV + v) * TW + c] = cq[rank];
+        ext[((int64_t)t * 2 * NV + NV + v) * TW + c] = ev;
+    }
+}
+
+cudaError_t launch_rank_compose(const float* gathered, int P, int rank, int ntiles, int NV, float* ext,
+                                cudaStream_t s) {
+    if (P > 64) return cudaErrorInvalidValue;
+    const int n = ntiles * TW;
+    k_rank_compose<<<(n + 127) / 128, 128, 0, s>>>(gathered, P, rank, ntiles, NV, ext);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -605,8 +711,12 @@ cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int 
     p.nitems = plan.ntiles * plan.nb;
     p.epoch = scr.epoch;
     p.kc = kc;
+    p.phase = scr.phase;
+    p.halo_below = scr.halo_below;
+    p.ext = scr.ext;
+    p.rank_tuples = scr.rank_tuples;
     CUtensorMap tx, td;
-    if (!make_tmap2(&td, d, g.pitch, g.H, plan.Ls)) return cudaErrorInvalidValue;
+    if (!make_tmap2(&td, d, g.pitch, g.H + (scr.halo_below ? 1 : 0), plan.Ls)) return cudaErrorInvalidValue;
     if (mode != MODE_SUPPORT) {
         if (!make_tmap3(&tx, x, g.pitch, g.H, Ct, plan.Ls)) return cudaErrorInvalidValue;
     } else {

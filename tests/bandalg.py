@@ -1,0 +1,58 @@
+"""Row-band algebra of one column pass in plain fp64 numpy (tests only).
+
+An independent restatement of the exchange the CUDA row-band mode performs
+(DESIGN.md "Multi-GPU"): each band of rows [lo, hi) of a column summarises its
+causal + anticausal recursive-filter pass (R4) as the 5-tuple
+    y[hi-1] = A c + B,            z[lo] = Z0 + S c + Q e
+in the unknown carries c = y[lo-1] (from above) and e = z[hi] (from below); the
+tuples are gathered in band order, the carries composed
+    c_{k+1} = A_k c_k + B_k (c_0 = 0),   e_{k-1} = Z0_k + S_k c_k + Q_k e_k (e_last = 0),
+and each band finishes with its exact carries.  Nothing here calls the oracle or
+the CUDA library.
+"""
+import numpy as np
+
+
+def band_parts(x, A, lo, hi, A_below):
+    """Per-band quantities for x[lo:hi] with coefficients A[lo:hi] and the link
+    coefficient A_below between row hi-1 and row hi (0 at the image bottom)."""
+    n = hi - lo
+    y0 = np.zeros(n)
+    y1 = np.zeros(n)
+    p0, p1 = 0.0, 1.0
+    for i in range(n):
+        a = A[lo + i]
+        p0 = a * p0 + (1 - a) * x[lo + i]
+        p1 = a * p1
+        y0[i], y1[i] = p0, p1
+    z0 = np.zeros(n)
+    S = np.zeros(n)
+    Q = np.zeros(n)
+    q0, qs, qq = 0.0, 0.0, 1.0
+    for i in range(n - 1, -1, -1):
+        an = A_below if i == n - 1 else A[lo + i + 1]
+        q0 = an * q0 + (1 - an) * y0[i]
+        qs = an * qs + (1 - an) * y1[i]
+        qq = an * qq
+        z0[i], S[i], Q[i] = q0, qs, qq
+    tup = np.array([y1[-1], y0[-1], z0[0], S[0], Q[0]])  # A, B, Z0, S, Q
+    return tup, (y0, y1, z0, S, Q)
+
+
+def compose(tuples):
+    """Carries (c_k, e_k) of every band from the gathered tuples (band order)."""
+    P = len(tuples)
+    c = np.zeros(P)
+    for k in range(P - 1):
+        A, B = tuples[k][0], tuples[k][1]
+        c[k + 1] = A * c[k] + B
+    e = np.zeros(P)
+    for k in range(P - 1, 0, -1):
+        Z0, S, Q = tuples[k][2], tuples[k][3], tuples[k][4]
+        e[k - 1] = Z0 + S * c[k] + Q * e[k]
+    return c, e
+
+
+def finish(parts, c, e):
+    y0, y1, z0, S, Q = parts
+    return z0 + S * c + Q * e
