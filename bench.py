@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--bands", action="store_true",
+                    help="row-band mode even on one rank (exercises the NCCL transport at N=1)")
     return ap.parse_args()
 
 
@@ -162,7 +164,8 @@ def main():
     import paper_1805_04590_b200 as dts
 
     rank, world, local = dist_env()
-    if world > 1:
+    launched = "WORLD_SIZE" in os.environ  # under torchrun (any N)
+    if world > 1 or (launched and args.bands):
         import torch.distributed as tdist
         torch.cuda.set_device(local)
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -181,17 +184,18 @@ def main():
         per = cfg.batch // world
         images = list(range(rank * per, (rank + 1) * per))
         inputs = [make_inputs(cfg.name, image=i) for i in images]
-    elif world > 1:
+    elif world > 1 or args.bands:
+        import torch.distributed as tdist
         r0, r1 = dts.band_rows(cfg.H, world, rank)
         a, b = dts.band_guide_rows(cfg.H, r0, r1)
         g, t, c = make_inputs(cfg.name, rows=(a, b))
         inputs = [(g, np.ascontiguousarray(t[r0 - a:r1 - a]), np.ascontiguousarray(c[r0 - a:r1 - a]))]
         band = (r0, r1)
-        import torch.distributed as tdist
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(dts.dts_comm_unique_id()), dtype=torch.uint8))
-        tdist.broadcast(uid, 0)
+        if world > 1:
+            tdist.broadcast(uid, 0)
         comm = dts.dts_comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
     else:
         inputs = [make_inputs(cfg.name)]
@@ -281,9 +285,8 @@ def main():
     if rank != 0:
         if comm:
             dts.dts_comm_destroy(comm)
-        if world > 1:
-            import torch.distributed as tdist
-            tdist.destroy_process_group()
+        import torch.distributed as tdist
+        tdist.destroy_process_group()
         return 0
 
     # ---- roofline of the dominant kernel ----
@@ -333,7 +336,7 @@ def main():
     print(json.dumps(line), flush=True)
     if comm:
         dts.dts_comm_destroy(comm)
-    if world > 1:
+    if world > 1 or (launched and args.bands):
         import torch.distributed as tdist
         tdist.destroy_process_group()
     return 0

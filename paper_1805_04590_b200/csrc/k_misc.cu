@@ -14,7 +14,7 @@ namespace dts {
 // memory with a conflict-free odd pixel stride, and the previous row stays
 // resident, so the guide is read from HBM once (plus 1/KROWS re-read of a row).
 constexpr int DERIV_STRIP = 256;
-constexpr int DERIV_ROWS = 16;
+constexpr int DERIV_ROWS = 32;
 
 template <int CT>  // CT = channel count (0: runtime C)
 __global__ void __launch_bounds__(DERIV_STRIP) k_guide_deriv(const float* __restrict__ guide, int Crt, float ratio2,
@@ -108,8 +108,84 @@ __global__ void __launch_bounds__(DERIV_STRIP) k_guide_deriv(const float* __rest
     }
 }
 
+// K1 for C % 4 == 0 (e.g. the 16-band satellite guide): one thread per pixel column,
+// walking DERIV_ROWS rows; each pixel's C channels arrive as C/4 float4 loads (a warp
+// covers one contiguous 32*C-float span), the left neighbour is the lane to the left
+// (an L1 hit), the previous row stays in registers, and the next row's loads are issued
+// before the current row's arithmetic.
+template <int Q>  // Q = C / 4
+__global__ void __launch_bounds__(256) k_guide_deriv_vec(const float* __restrict__ guide, float ratio2, Geometry g,
+                                                         float* __restrict__ dx, float* __restrict__ dy) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t rbeg = (int64_t)blockIdx.y * DERIV_ROWS;
+    const int64_t rend = min(rbeg + (int64_t)DERIV_ROWS, g.H);
+    if (c >= g.pitch) return;
+    const float inf = __int_as_float(0x7f800000);
+    if (c >= g.W) {
+        for (int64_t r = rbeg; r < rend; ++r) {
+            dx[r * g.pitch + c] = inf;
+            dy[r * g.pitch + c] = inf;
+        }
+        return;
+    }
+    const int64_t cl = c > 0 ? c - 1 : 0;
+    auto px = [&](int64_t r, int64_t col) { return reinterpret_cast<const float4*>(guide + (r * g.W + col) * (4 * Q)); };
+    float4 up[Q], cur[Q], lef[Q], ncur[Q], nlef[Q];
+    if (rbeg > 0) {
+        const float4* pu = px(rbeg - 1, c);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) up[q] = __ldg(pu + q);
+    }
+    {
+        const float4* pc = px(rbeg, c);
+        const float4* pl = px(rbeg, cl);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            cur[q] = __ldg(pc + q);
+            lef[q] = __ldg(pl + q);
+        }
+    }
+    for (int64_t r = rbeg; r < rend; ++r) {
+        if (r + 1 < rend) {  // next row in flight during this row's arithmetic
+            const float4* pc = px(r + 1, c);
+            const float4* pl = px(r + 1, cl);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                ncur[q] = __ldg(pc + q);
+                nlef[q] = __ldg(pl + q);
+            }
+        }
+        float sx = 0.f, sy = 0.f;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const float ax = cur[q].x - lef[q].x, ay = cur[q].y - lef[q].y, az = cur[q].z - lef[q].z,
+                        aw = cur[q].w - lef[q].w;
+            const float bx = cur[q].x - up[q].x, by = cur[q].y - up[q].y, bz = cur[q].z - up[q].z,
+                        bw = cur[q].w - up[q].w;
+            sx = fmaf(ax, ax, fmaf(ay, ay, fmaf(az, az, fmaf(aw, aw, sx))));
+            sy = fmaf(bx, bx, fmaf(by, by, fmaf(bz, bz, fmaf(bw, bw, sy))));
+        }
+        dx[r * g.pitch + c] = c > 0 ? sqrtf(fmaf(ratio2, sx, 1.f)) : inf;
+        dy[r * g.pitch + c] = r > 0 ? sqrtf(fmaf(ratio2, sy, 1.f)) : inf;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            up[q] = cur[q];
+            cur[q] = ncur[q];
+            lef[q] = nlef[q];
+        }
+    }
+}
+
 cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Geometry& g, float* dx, float* dy,
                                cudaStream_t s) {
+    if ((C == 4 || C == 8 || C == 16) && ((uintptr_t)guide % 16 == 0)) {
+        dim3 block(256);
+        dim3 grid((unsigned)((g.pitch + 255) / 256), (unsigned)((g.H + DERIV_ROWS - 1) / DERIV_ROWS));
+        if (C == 4) k_guide_deriv_vec<1><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy);
+        if (C == 8) k_guide_deriv_vec<2><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy);
+        if (C == 16) k_guide_deriv_vec<4><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy);
+        return cudaGetLastError();
+    }
     dim3 block(DERIV_STRIP);
     dim3 grid((unsigned)((g.pitch + DERIV_STRIP - 1) / DERIV_STRIP), (unsigned)((g.H + DERIV_ROWS - 1) / DERIV_ROWS));
     const size_t smem = 2 * (size_t)(DERIV_STRIP + 1) * (C | 1) * sizeof(float);
@@ -142,30 +218,63 @@ cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Ge
     return cudaGetLastError();
 }
 
-// K6: planar state from the HWC target, chat = c / S (R7).
+// K6: planar state from the HWC target, chat = c / S (R7).  One thread per 4
+// consecutive pixels of a row: float4 stores of Z, T, chat (and float4 loads of the target
+// and confidence when a row of them is 16-B aligned, i.e. W % 4 == 0 and C_t == 1).
+template <bool VEC>
 __global__ void __launch_bounds__(256) k_prologue(const float* __restrict__ target, const float* __restrict__ conf,
                                                   int Ct, Geometry g, const float* __restrict__ S, int support_mode,
                                                   float* __restrict__ Z, float* __restrict__ T,
                                                   float* __restrict__ chat) {
-    const int64_t r = blockIdx.y;
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= g.W) return;
-    const int64_t p = r * g.W + c;
-    const int64_t o = r * g.pitch + c;
-    for (int v = 0; v < Ct; ++v) {
-        const float t = __ldg(target + p * Ct + v);
-        Z[v * g.plane + o] = t;
-        T[v * g.plane + o] = t;
+    const int64_t per_row = g.pitch / 4;
+    const int64_t n = g.H * per_row;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / per_row;
+        const int64_t c4 = (i - r * per_row) * 4;
+        if (c4 >= g.W) continue;
+        const int64_t o = r * g.pitch + c4;
+        const int64_t p = r * g.W + c4;
+        float cv[4];
+        if constexpr (VEC) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(conf + p));
+            cv[0] = q.x; cv[1] = q.y; cv[2] = q.z; cv[3] = q.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cv[u] = (c4 + u < g.W) ? __ldg(conf + p + u) : 0.f;
+        }
+        const float4 sv = __ldg(reinterpret_cast<const float4*>(S + o));
+        const float ss[4] = {sv.x, sv.y, sv.z, sv.w};
+        float ch[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ch[u] = (c4 + u < g.W) ? (support_mode == 1 ? cv[u] : cv[u] / ss[u]) : 0.f;
+        *reinterpret_cast<float4*>(chat + o) = make_float4(ch[0], ch[1], ch[2], ch[3]);
+        for (int v = 0; v < Ct; ++v) {
+            float tv[4];
+            if constexpr (VEC) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(target + p));
+                tv[0] = q.x; tv[1] = q.y; tv[2] = q.z; tv[3] = q.w;
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) tv[u] = (c4 + u < g.W) ? __ldg(target + (p + u) * Ct + v) : 0.f;
+            }
+            const float4 t4 = make_float4(tv[0], tv[1], tv[2], tv[3]);
+            *reinterpret_cast<float4*>(Z + v * g.plane + o) = t4;
+            *reinterpret_cast<float4*>(T + v * g.plane + o) = t4;
+        }
     }
-    const float cv = __ldg(conf + p);
-    chat[o] = support_mode == 1 ? cv : cv / S[o];
 }
 
 cudaError_t launch_prologue(const float* target, const float* conf, int Ct, const Geometry& g, const float* S,
                             int support_mode, float* Z, float* T, float* chat, cudaStream_t s) {
-    dim3 block(256);
-    dim3 grid((unsigned)((g.W + 255) / 256), (unsigned)g.H);
-    k_prologue<<<grid, block, 0, s>>>(target, conf, Ct, g, S, support_mode, Z, T, chat);
+    const int64_t n = g.H * (g.pitch / 4);
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    const bool vec = Ct == 1 && g.W % 4 == 0 && ((uintptr_t)target % 16 == 0) && ((uintptr_t)conf % 16 == 0);
+    if (vec)
+        k_prologue<true><<<(unsigned)blocks, 256, 0, s>>>(target, conf, Ct, g, S, support_mode, Z, T, chat);
+    else
+        k_prologue<false><<<(unsigned)blocks, 256, 0, s>>>(target, conf, Ct, g, S, support_mode, Z, T, chat);
     return cudaGetLastError();
 }
 
