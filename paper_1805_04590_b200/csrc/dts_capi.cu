@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -110,6 +111,11 @@ struct dts_ctx {
     unsigned int* flags = nullptr;
     size_t tuple_cap = 0, flag_cap = 0;
     unsigned int epoch = 0;
+    // streaming column kernel (kind 2) scratch: its own tuples/carries and counters/flags
+    float* v_tuples = nullptr;
+    unsigned int* v_flags = nullptr;
+    size_t v_tuple_cap = 0, v_flag_cap = 0;
+    unsigned int v_epoch = 0;
     cudaStream_t last_stream = nullptr;
     int64_t launches = 0;
 };
@@ -118,11 +124,11 @@ namespace {
 
 enum Family {
     F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
-    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_COUNT
+    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
-                                     "rank_compose"};
+                                     "rank_compose", "row_update"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -237,6 +243,26 @@ cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* 
 
 dts_status ensure_col_scratch(dts_ctx* ctx, const ColPlan& cp, cudaStream_t s) {
     cudaError_t e;
+    if (cp.kind == 2) {
+        if (cp.tuple_floats > ctx->v_tuple_cap) {
+            if (ctx->v_tuples) cudaFreeAsync(ctx->v_tuples, s);
+            ctx->v_tuples = nullptr;
+            if ((e = cudaMallocAsync((void**)&ctx->v_tuples, cp.tuple_floats * sizeof(float), s)) != cudaSuccess)
+                return cuda_fail(e);
+            ctx->v_tuple_cap = cp.tuple_floats;
+        }
+        if (cp.flag_count > ctx->v_flag_cap) {
+            if (ctx->v_flags) cudaFreeAsync(ctx->v_flags, s);
+            ctx->v_flags = nullptr;
+            if ((e = cudaMallocAsync((void**)&ctx->v_flags, cp.flag_count * sizeof(unsigned int), s)) !=
+                    cudaSuccess ||
+                (e = cudaMemsetAsync(ctx->v_flags, 0, cp.flag_count * sizeof(unsigned int), s)) != cudaSuccess)
+                return cuda_fail(e);
+            ctx->v_flag_cap = cp.flag_count;
+            ctx->v_epoch = 0;
+        }
+        return DTS_OK;
+    }
     if (cp.kind != 0) return DTS_OK;
     if (cp.tuple_floats > ctx->tuple_cap) {
         if (ctx->tuples) cudaFreeAsync(ctx->tuples, s);
@@ -262,6 +288,15 @@ ColScratch next_scratch(dts_ctx* ctx);
 cudaError_t col_launch(dts_ctx* ctx, const ColPlan& plan, int Ct, int mode, float* x, const float* d, float kc,
                        const UpdateArgs* upd, float* support, cudaStream_t s) {
     if (plan.kind == 1) return launch_col_cluster(plan, ctx->g, Ct, mode, x, d, kc, upd, support, s);
+    if (plan.kind == 2) {
+        ColScratch sc = {};
+        sc.phase = PHASE_FULL;
+        sc.tuples = ctx->v_tuples;
+        sc.flags = ctx->v_flags;
+        sc.epoch = ++ctx->v_epoch;
+        if (sc.epoch == 0) sc.epoch = ++ctx->v_epoch;
+        return launch_col_stream(plan, ctx->g, Ct, mode, x, d, kc, upd, sc, s);
+    }
     return launch_col_pass(plan, ctx->g, Ct, mode, x, d, kc, upd, support, next_scratch(ctx), s);
 }
 
@@ -435,8 +470,11 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
         return DTS_E_ARG;
     }
     const size_t plane_x = (size_t)Hx * ctx->g.pitch * sizeof(float);
+    // d_y gets one extra row: row H of the band is the link to the rows below (the halo
+    // when there is one, else +inf: A = 0 at the image bottom, R4) -- the streaming
+    // column kernel reads it as the band-closing coefficient
     if ((e = cudaMallocAsync((void**)&ctx->dx_base, plane_x, s)) != cudaSuccess ||
-        (e = cudaMallocAsync((void**)&ctx->dy_base, plane_x, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->dy_base, plane_x + ctx->g.pitch * sizeof(float), s)) != cudaSuccess ||
         (e = cudaMallocAsync((void**)&ctx->S, plane, s)) != cudaSuccess ||
         (e = cudaMallocAsync((void**)&ctx->counters, 2 * sizeof(unsigned int), s)) != cudaSuccess) {
         st = cuda_fail(e);
@@ -464,6 +502,11 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
     st = run_launch(ctx, F_DERIV, px * (4.0 * C + 8.0), s, [&] {
         return launch_guide_deriv(gdev, C, ratio * ratio, gx, ctx->dx_base, ctx->dy_base, s);
     });
+    if (st == DTS_OK && !ctx->halo_below) {
+        const float inf = std::numeric_limits<float>::infinity();
+        if ((e = launch_fill(ctx->dy + H * ctx->g.pitch, ctx->g.pitch, inf, s)) != cudaSuccess) st = cuda_fail(e);
+        ++ctx->launches;
+    }
     if (st == DTS_OK)
         st = run_launch(ctx, F_SUPPORT_ROW, px * 8.0, s, [&] {
             return launch_row_pass(rp, ctx->g, 1, MODE_SUPPORT, nullptr, ctx->S, ctx->dx, ctx->ks, s);
@@ -561,12 +604,24 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
 
     RowPlan rp;
     ColPlan cpf, cpu;
-    if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess ||
-        (ctx->comm ? plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)
-                   : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess ||
-        (ctx->comm ? plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu)
-                   : plan_col(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu)) != cudaSuccess)
-        return DTS_E_SHAPE;
+    if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess) return DTS_E_SHAPE;
+    // column kernel: the cluster kernel (k_colc.cu) by default; DTS_COL=stream selects the
+    // TMEM-lagged decoupled kernel (k_colv.cu, experimental), DTS_COL=legacy forces the
+    // cluster / band-tuple kernels with the separate update kernel
+    const char* colsel = std::getenv("DTS_COL");
+    // streaming path: TMEM-lagged column kernel (FILTER) + the Eq. (3) step fused into the
+    // next iteration's first row pass (and one closing update kernel)
+    const bool stream_ok = !ctx->comm && colsel && std::strcmp(colsel, "stream") == 0 &&
+                           plan_col_stream(g, Ct, MODE_FILTER, ctx->num_sms, &cpf) == cudaSuccess;
+    if (stream_ok) cpu = cpf;
+    if (!stream_ok) {
+        cudaGetLastError();
+        if ((ctx->comm ? plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)
+                       : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess ||
+            (ctx->comm ? plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu)
+                       : plan_col(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu)) != cudaSuccess)
+            return DTS_E_SHAPE;
+    }
 
     const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),
                   ko = classify(out, ctx->device);
@@ -615,7 +670,39 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         if (st != DTS_OK) return st;
         const double row_bytes = px * (8.0 * Ct + 4);
         const double upd_bytes = px * (16.0 * Ct + 8);  // X, d, Z, T, chat in; Z out
-        for (int k = 0; k < iterations; ++k) {
+        if (stream_ok) {
+            UpdateArgs u;
+            u.Z = ctx->Z;
+            u.T = ctx->T;
+            u.chat = ctx->chat;
+            u.lam = lambda;
+            u.step = step;
+            u.out_hwc = nullptr;
+            for (int k = 0; k < iterations; ++k) {
+                for (int i = 0; i < ctx->N; ++i) {
+                    if (i == 0 && k > 0) {  // Eq. (3) step of iteration k-1 fused into this row pass
+                        st = run_launch(ctx, F_ROWUPD, px * (20.0 * Ct + 8), s, [&] {
+                            return launch_row_update(rp, g, Ct, ctx->X, ctx->X, ctx->dx, ctx->kc[i], u, s);
+                        });
+                    } else {
+                        const float* in = (i == 0) ? ctx->Z : ctx->X;
+                        st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
+                            return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
+                        });
+                    }
+                    if (st != DTS_OK) return st;
+                    st = run_launch(ctx, F_COL, row_bytes, s, [&] {
+                        return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
+                    });
+                    if (st != DTS_OK) return st;
+                }
+            }
+            st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
+                return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, o_d, ctx->num_sms, s);
+            });
+            if (st != DTS_OK) return st;
+        }
+        for (int k = 0; k < (stream_ok ? 0 : iterations); ++k) {
             for (int i = 0; i < ctx->N; ++i) {
                 const float* in = (i == 0) ? ctx->Z : ctx->X;
                 st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
@@ -696,6 +783,8 @@ void dts_destroy(dts_ctx* ctx) {
     if (ctx->counters) cudaFreeAsync(ctx->counters, s);
     if (ctx->tuples) cudaFreeAsync(ctx->tuples, s);
     if (ctx->flags) cudaFreeAsync(ctx->flags, s);
+    if (ctx->v_tuples) cudaFreeAsync(ctx->v_tuples, s);
+    if (ctx->v_flags) cudaFreeAsync(ctx->v_flags, s);
     delete ctx;
 }
 

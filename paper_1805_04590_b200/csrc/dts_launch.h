@@ -5,7 +5,7 @@
 
 namespace dts {
 
-enum PassMode : int { MODE_FILTER = 0, MODE_UPDATE = 1, MODE_SUPPORT = 2 };
+enum PassMode : int { MODE_FILTER = 0, MODE_UPDATE = 1, MODE_SUPPORT = 2, MODE_ROWUPD = 3 };
 // column-pass phases (row-band mode): FULL = single band set; TUPLE = emit the aggregate
 // 5-tuple of this rank's rows; APPLY = finish with external carries (after the exchange)
 enum ColPhase : int { PHASE_FULL = 0, PHASE_TUPLE = 1, PHASE_APPLY = 2 };
@@ -30,10 +30,16 @@ cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowP
 cudaError_t launch_row_pass(const RowPlan& plan, const Geometry& g, int Ct, int mode, const float* in, float* out,
                             const float* d, float kc, cudaStream_t s);
 
+// K2 fused with the previous iteration's Eq. (3) step (MODE_ROWUPD): Z <- Z - step [lam (Z -
+// zbar) + chat (Z - T)] written back, then the row filter of the new Z -> out.
+struct UpdateArgs;
+cudaError_t launch_row_update(const RowPlan& plan, const Geometry& g, int Ct, const float* zbar, float* out,
+                              const float* d, float kc, const UpdateArgs& u, cudaStream_t s);
+
 // K3/K4: recursive-filter column pass (decoupled band-tuple scan, cooperative
 // persistent grid), FILTER, UPDATE (fused solver step, Eq. 3) or SUPPORT mode.
 struct ColPlan {
-    int kind;  // 0: decoupled band-tuple kernel (k_col.cu), 1: cluster kernel (k_colc.cu)
+    int kind;  // 0: decoupled band-tuple kernel (k_col.cu), 1: cluster kernel (k_colc.cu), 2: k_colv.cu
     int TW, CB, HB, S, Ls, nb, ntiles, threads;
     dim3 grid;
     size_t smem;
@@ -66,6 +72,17 @@ cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int 
 cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
                                float kc, const UpdateArgs* upd, float* support, cudaStream_t s);
+
+// K3/K4 streaming path (k_colv.cu): decoupled band-tuple scan over 64-column tiles with
+// shared-memory-held items and a TMA producer warp; FILTER and UPDATE (fused Eq. 3).
+// Needs d with H + 1 rows (row H = +inf, or the halo link).  kind = 2; its scratch is
+// `tuple_floats` floats + `flag_count` zero-initialised words, owned by the caller.
+cudaError_t plan_col_stream(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
+cudaError_t launch_col_stream(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
+                              float kc, const UpdateArgs* upd, const ColScratch& scr, cudaStream_t s);
+
+// fill n floats with v
+cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);
 
 // K4b: Eq. (3) update as a streaming kernel (zbar in X); writes Z, or out_hwc when non-null.
 cudaError_t launch_update(const float* X, float* Z, const float* T, const float* chat, int Ct, const Geometry& g,

@@ -352,4 +352,15 @@ cudaError_t launch_check_inputs(const float* target, const float* conf, int Ct, 
     return cudaGetLastError();
 }
 
+__global__ void k_fill(float* p, int64_t n, float v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t blocks = (n + 255) / 256;
+    k_fill<<<(unsigned)(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(p, n, v);
+    return cudaGetLastError();
+}
+
 }  // namespace dts

@@ -25,6 +25,12 @@ struct RowParams {
     const float* in;
     float* out;
     const float* d;
+    // MODE_ROWUPD: Eq. (3) step applied on the fly, Z <- Z - step [lam (Z - in) + chat (Z - T)],
+    // and the new Z is the row filter's input (in = zbar of the previous iteration)
+    float* Z;
+    const float* T;
+    const float* chat;
+    float lam, step;
     int64_t plane, pitch, rowstride;
     int H, W, G, R, nbuf;
     float kc;
@@ -93,7 +99,7 @@ __device__ __forceinline__ Aff<NV> group_exclusive_scan(Aff<NV> v, int t, int G,
 template <int L, int CT, int MODE>
 __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
     static_assert(L % 4 == 0, "L must be a multiple of 4 (float4 smem reads)");
-    constexpr int NX = (MODE == MODE_SUPPORT) ? 0 : CT;  // input planes
+    constexpr int NX = (MODE == MODE_SUPPORT) ? 0 : CT;  // input planes (ROWUPD: zbar)
     constexpr int NSLOT = 1 + (MODE == MODE_SUPPORT ? 1 : CT);
     constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
 
@@ -143,10 +149,33 @@ __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
             bulk_wait_read0();  // stores issued from buffer b^1 have read their smem
             issue(nxt, b ^ 1);
         }
+        const int k0 = t * L;
+        const int64_t grow = (int64_t)grp * R + rs;  // this thread group's image row
+        // ROWUPD: state, target and chat of this chunk straight from global (in flight
+        // while the TMA row lands)
+        float zo[MODE == MODE_ROWUPD ? CT : 1][MODE == MODE_ROWUPD ? L : 1];
+        float tv[MODE == MODE_ROWUPD ? CT : 1][MODE == MODE_ROWUPD ? L : 1];
+        float ch[MODE == MODE_ROWUPD ? L : 1];
+        if constexpr (MODE == MODE_ROWUPD) {
+            const bool rok = grow < p.H;
+#pragma unroll
+            for (int j4 = 0; j4 < L; j4 += 4) {
+                const bool ok = rok && (k0 + j4 < p.W);
+                const int64_t o = grow * p.pitch + k0 + j4;
+                float4 cv = ok ? __ldg(reinterpret_cast<const float4*>(p.chat + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                ch[j4] = cv.x, ch[j4 + 1] = cv.y, ch[j4 + 2] = cv.z, ch[j4 + 3] = cv.w;
+#pragma unroll
+                for (int c = 0; c < CT; ++c) {
+                    float4 zv = ok ? *reinterpret_cast<const float4*>(p.Z + c * p.plane + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    float4 tt = ok ? __ldg(reinterpret_cast<const float4*>(p.T + c * p.plane + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    zo[c][j4] = zv.x, zo[c][j4 + 1] = zv.y, zo[c][j4 + 2] = zv.z, zo[c][j4 + 3] = zv.w;
+                    tv[c][j4] = tt.x, tv[c][j4 + 1] = tt.y, tv[c][j4 + 2] = tt.z, tv[c][j4 + 3] = tt.w;
+                }
+            }
+        }
         mbar_wait(&bar[b], (uint32_t)(dbl ? ((it >> 1) & 1) : (it & 1)));
 
         float* row = smem + b * bufFloats + (int64_t)rs * NSLOT * p.rowstride;
-        const int k0 = t * L;
 
         // ---- load chunk: coefficients A and samples x (masked beyond W) ----
         float A[L];
@@ -167,6 +196,29 @@ __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
                     float xx[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u) x[c][j4 + u] = (k0 + j4 + u < p.W) ? xx[u] : 0.f;
+                }
+            }
+        }
+        if constexpr (MODE == MODE_ROWUPD) {  // Eq. (3): x <- z - step [lam (z - zbar) + chat (z - t)]
+#pragma unroll
+            for (int c = 0; c < CT; ++c) {
+#pragma unroll
+                for (int j = 0; j < L; ++j) {
+                    const float g = fmaf(p.lam, zo[c][j] - x[c][j], ch[j] * (zo[c][j] - tv[c][j]));
+                    x[c][j] = (k0 + j < p.W) ? fmaf(-p.step, g, zo[c][j]) : 0.f;
+                }
+                if (grow < p.H) {
+#pragma unroll
+                    for (int j4 = 0; j4 < L; j4 += 4) {
+                        float* o = p.Z + c * p.plane + grow * p.pitch + k0 + j4;
+                        if (k0 + j4 + 3 < p.W) {
+                            *reinterpret_cast<float4*>(o) = make_float4(x[c][j4], x[c][j4 + 1], x[c][j4 + 2], x[c][j4 + 3]);
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                if (k0 + j4 + u < p.W) o[u] = x[c][j4 + u];
+                        }
+                    }
                 }
             }
         }
@@ -331,9 +383,38 @@ static cudaError_t launch_ct(const RowPlan& plan, const RowParams& p, int Ct, cu
     }
 }
 
+cudaError_t launch_row_update(const RowPlan& plan, const Geometry& g, int Ct, const float* zbar, float* out,
+                              const float* d, float kc, const UpdateArgs& u, cudaStream_t s) {
+    RowParams p = {};
+    p.in = zbar;
+    p.out = out;
+    p.d = d;
+    p.Z = u.Z;
+    p.T = u.T;
+    p.chat = u.chat;
+    p.lam = u.lam;
+    p.step = u.step;
+    p.plane = g.plane;
+    p.pitch = g.pitch;
+    p.rowstride = plan.rowstride;
+    p.H = (int)g.H;
+    p.W = (int)g.W;
+    p.G = plan.G;
+    p.R = plan.R;
+    p.nbuf = plan.nbuf;
+    p.kc = kc;
+    switch (plan.L) {
+        case 4: return launch_ct<4, MODE_ROWUPD>(plan, p, Ct, s);
+        case 12: return launch_ct<12, MODE_ROWUPD>(plan, p, Ct, s);
+        case 20: return launch_ct<20, MODE_ROWUPD>(plan, p, Ct, s);
+        case 36: return launch_ct<36, MODE_ROWUPD>(plan, p, Ct, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_row_pass(const RowPlan& plan, const Geometry& g, int Ct, int mode, const float* in, float* out,
                             const float* d, float kc, cudaStream_t s) {
-    RowParams p;
+    RowParams p = {};
     p.in = in;
     p.out = out;
     p.d = d;

@@ -214,16 +214,17 @@ def test_profile_counters():
     gd, td, cd = (torch.from_numpy(a).cuda() for a in (g, t, c))
     with dts.Solver(gd, 5.0, 0.2, 3) as s:
         n0 = dts.dts_launch_count(s.ctx)
-        assert n0 == 3  # deriv + support row + support col
+        assert n0 == 4  # deriv + bottom-link row fill + support row + support col
         dts.dts_profile_enable(s.ctx, True)
         s.solve(td, cd, 0.99, 4)
         st = dts.dts_profile_read(s.ctx)
         n1 = dts.dts_launch_count(s.ctx)
-    # 3 row passes + 3 column passes per iteration; the Eq. (3) step is either fused into
-    # the last column pass (col_update) or a separate streaming kernel (update)
-    assert st["row_pass"]["launches"] == 12
+    # 3 row passes + 3 column passes per iteration; the Eq. (3) step is fused into the
+    # next iteration's first row pass (row_update) + one closing update kernel, or fused
+    # into the last column pass (col_update), or a separate streaming kernel (update)
+    assert st["row_pass"]["launches"] + st["row_update"]["launches"] == 12
     assert st["col_pass"]["launches"] + st["col_update"]["launches"] == 12
-    assert st["update"]["launches"] + st["col_update"]["launches"] == 4
+    assert st["update"]["launches"] + st["col_update"]["launches"] + st["row_update"]["launches"] == 4
     assert st["prologue"]["launches"] == 1
     assert n1 == n0 + 1 + 4 * 6 + st["update"]["launches"]
     assert st["row_pass"]["total_ms"] > 0
@@ -257,5 +258,36 @@ def test_fallback_column_kernel_parity(H, W, Ct, monkeypatch):
     """The decoupled band-tuple column kernel (used when a column does not fit a
     cluster) forced for ordinary shapes: DTS_NO_CLUSTER=1."""
     monkeypatch.setenv("DTS_NO_CLUSTER", "1")
+    monkeypatch.setenv("DTS_COL", "legacy")
     g, t, c = random_problem(H, W, 3, Ct, seed=H + 3 * W)
     check(g, t, c, 6.0, 0.2, 3, 0.99, 5)
+
+
+@pytest.mark.parametrize("H,W,Ct", [(48, 64, 1), (700, 130, 1), (300, 90, 3), (2600, 35, 1)])
+def test_legacy_cluster_column_kernel_parity(H, W, Ct, monkeypatch):
+    """The cluster column kernel + streaming update kernel (DTS_COL=legacy)."""
+    monkeypatch.setenv("DTS_COL", "legacy")
+    g, t, c = random_problem(H, W, 3, Ct, seed=H + 5 * W)
+    check(g, t, c, 6.0, 0.2, 3, 0.99, 5)
+
+
+# streaming column kernel (k_colv.cu): band boundaries (HB = 128 rows for Ct = 1, 32..64
+# for Ct > 1), 64-column tiles with ragged / odd widths, many bands per tile
+@pytest.mark.parametrize("H,W,Ct", [(127, 64, 1), (128, 64, 1), (129, 64, 1), (256, 65, 1), (385, 127, 1),
+                                    (1000, 199, 1), (10000, 9, 1), (4000, 513, 1), (65, 33, 2), (129, 131, 3),
+                                    (64, 1, 1), (1, 200, 1)])
+def test_stream_column_kernel_parity(H, W, Ct, monkeypatch):
+    """The TMEM-lagged decoupled column kernel (DTS_COL=stream) + the Eq. (3) step fused
+    into the next iteration's first row pass."""
+    monkeypatch.setenv("DTS_COL", "stream")
+    g, t, c = random_problem(H, W, 3, Ct, seed=3 * H + W + Ct)
+    check(g, t, c, 9.0, 0.3, 3, 0.99, 4)
+
+
+def test_stream_matches_default(monkeypatch):
+    """Two independent column kernels agree to fp32 rounding on a C1-like problem."""
+    g, t, c = random_problem(1000, 700, 3, 1, seed=99)
+    a = gpu_solve(g, t, c, 16.0, 0.1, 3, 0.99, 10)
+    monkeypatch.setenv("DTS_COL", "stream")
+    b = gpu_solve(g, t, c, 16.0, 0.1, 3, 0.99, 10)
+    assert np.max(np.abs(a - b)) <= 1e-5 * target_range(t)
