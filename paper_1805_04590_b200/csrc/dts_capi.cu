@@ -243,7 +243,7 @@ cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* 
 
 dts_status ensure_col_scratch(dts_ctx* ctx, const ColPlan& cp, cudaStream_t s) {
     cudaError_t e;
-    if (cp.kind == 2) {
+    if (cp.kind == 2 || cp.kind == 3) {
         if (cp.tuple_floats > ctx->v_tuple_cap) {
             if (ctx->v_tuples) cudaFreeAsync(ctx->v_tuples, s);
             ctx->v_tuples = nullptr;
@@ -288,13 +288,14 @@ ColScratch next_scratch(dts_ctx* ctx);
 cudaError_t col_launch(dts_ctx* ctx, const ColPlan& plan, int Ct, int mode, float* x, const float* d, float kc,
                        const UpdateArgs* upd, float* support, cudaStream_t s) {
     if (plan.kind == 1) return launch_col_cluster(plan, ctx->g, Ct, mode, x, d, kc, upd, support, s);
-    if (plan.kind == 2) {
+    if (plan.kind == 2 || plan.kind == 3) {
         ColScratch sc = {};
         sc.phase = PHASE_FULL;
         sc.tuples = ctx->v_tuples;
         sc.flags = ctx->v_flags;
         sc.epoch = ++ctx->v_epoch;
         if (sc.epoch == 0) sc.epoch = ++ctx->v_epoch;
+        if (plan.kind == 3) return launch_col_2p(plan, ctx->g, Ct, x, d, kc, sc, s);
         return launch_col_stream(plan, ctx->g, Ct, mode, x, d, kc, upd, sc, s);
     }
     return launch_col_pass(plan, ctx->g, Ct, mode, x, d, kc, upd, support, next_scratch(ctx), s);
@@ -614,7 +615,10 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     const bool stream_ok = !ctx->comm && colsel && std::strcmp(colsel, "stream") == 0 &&
                            plan_col_stream(g, Ct, MODE_FILTER, ctx->num_sms, &cpf) == cudaSuccess;
     if (stream_ok) cpu = cpf;
-    if (!stream_ok) {
+    const bool twop_ok = !stream_ok && !ctx->comm && colsel && std::strcmp(colsel, "2p") == 0 &&
+                         plan_col_2p(g, Ct, MODE_FILTER, ctx->num_sms, &cpf) == cudaSuccess;
+    if (twop_ok) cpu = cpf;  // FILTER column passes + the streaming update kernel (K4b)
+    if (!stream_ok && !twop_ok) {
         cudaGetLastError();
         if ((ctx->comm ? plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)
                        : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess ||
@@ -729,8 +733,8 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                         return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
                                           s);
                     });
-                } else if (cpu.kind == 1) {
-                    // cluster column kernel + streaming update kernel (K4b)
+                } else if (cpu.kind == 1 || cpu.kind == 3) {
+                    // column kernel (FILTER) + streaming update kernel (K4b)
                     st = run_launch(ctx, F_COL, row_bytes, s, [&] {
                         return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
                                           s);

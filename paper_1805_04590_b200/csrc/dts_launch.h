@@ -39,7 +39,7 @@ cudaError_t launch_row_update(const RowPlan& plan, const Geometry& g, int Ct, co
 // K3/K4: recursive-filter column pass (decoupled band-tuple scan, cooperative
 // persistent grid), FILTER, UPDATE (fused solver step, Eq. 3) or SUPPORT mode.
 struct ColPlan {
-    int kind;  // 0: decoupled band-tuple kernel (k_col.cu), 1: cluster kernel (k_colc.cu), 2: k_colv.cu
+    int kind;  // 0: decoupled band-tuple kernel (k_col.cu), 1: cluster kernel (k_colc.cu), 2: k_colv.cu, 3: k_col2p.cu
     int TW, CB, HB, S, Ls, nb, ntiles, threads;
     dim3 grid;
     size_t smem;
@@ -80,6 +80,12 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
 cudaError_t plan_col_stream(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
 cudaError_t launch_col_stream(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
                               float kc, const UpdateArgs* upd, const ColScratch& scr, cudaStream_t s);
+
+// K3 two-phase path (k_col2p.cu): decoupled band-tuple scan with an L2 lag, high occupancy;
+// FILTER only.  kind = 3; scratch as for kind 2.
+cudaError_t plan_col_2p(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
+cudaError_t launch_col_2p(const ColPlan& plan, const Geometry& g, int Ct, float* x, const float* d, float kc,
+                          const ColScratch& scr, cudaStream_t s);
 
 // fill n floats with v
 cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);

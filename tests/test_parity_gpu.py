@@ -291,3 +291,12 @@ def test_stream_matches_default(monkeypatch):
     monkeypatch.setenv("DTS_COL", "stream")
     b = gpu_solve(g, t, c, 16.0, 0.1, 3, 0.99, 10)
     assert np.max(np.abs(a - b)) <= 1e-5 * target_range(t)
+
+
+@pytest.mark.parametrize("H,W,Ct", [(48, 64, 1), (129, 64, 1), (700, 130, 1), (1000, 199, 1), (300, 90, 3),
+                                    (61, 97, 2), (2600, 35, 1)])
+def test_two_phase_column_kernel_parity(H, W, Ct, monkeypatch):
+    """The two-phase L2-lag column kernel (k_col2p.cu, DTS_COL=2p)."""
+    monkeypatch.setenv("DTS_COL", "2p")
+    g, t, c = random_problem(H, W, 3, Ct, seed=5 * H + W + Ct)
+    check(g, t, c, 6.0, 0.2, 3, 0.99, 4)
