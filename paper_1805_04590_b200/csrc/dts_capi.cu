@@ -733,7 +733,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                         return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
                                           s);
                     });
-                } else if (cpu.kind == 1 || cpu.kind == 3) {
+                } else if ((cpu.kind == 1 && !std::getenv("DTS_FUSED_UPDATE")) || cpu.kind == 3) {
                     // column kernel (FILTER) + streaming update kernel (K4b)
                     st = run_launch(ctx, F_COL, row_bytes, s, [&] {
                         return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
