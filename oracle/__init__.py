@@ -13,8 +13,9 @@ Functions (each cites the passage its C routine follows; see dts_oracle.c):
   dtf(X, dx, dy, sigma_s, N)                    O4  X then Y passes
   support(dx, dy, sigma_s, mode)                O5  S = sum_j W_ij
   solve(guide, target, conf, ...)               O6  Eq. (3) gradient descent
+  confidence(guide, target, ..., sigma_c)       O7  Eq. (7) edge-aware variance confidence
 
-Parity status: O1, O3, O4, O5 and O6 are pinned by tests/test_oracle_pins.py
+Parity status: O1, O3, O4, O5, O6 and O7 are pinned by tests/test_oracle_pins.py
 (worked examples, dense triangular matrices, closed forms, brute force,
 reductions); the whole solve is NOT pinned against the paper's own outputs,
 which it never prints ("parity unpinned vs the paper").
@@ -66,6 +67,9 @@ def _load():
                                      _c_float_p, i32, _c_float_p, dbl, dbl, i32, i32,
                                      _c_double_p, _c_double_p]
     lib.dts_oracle_solve.restype = ctypes.c_int
+    lib.dts_oracle_confidence.argtypes = [_c_float_p, i64, i64, i32, dbl, dbl, i32, _c_float_p, dbl,
+                                          _c_double_p, _c_double_p]
+    lib.dts_oracle_confidence.restype = ctypes.c_int
     lib.dts_oracle_num_threads.argtypes = []
     lib.dts_oracle_num_threads.restype = ctypes.c_int
     lib.dts_oracle_set_threads.argtypes = [ctypes.c_int]
@@ -180,3 +184,21 @@ def solve(guide, target, confidence, sigma_s: float, sigma_r: float, N: int,
     if diagnostics:
         return res, diag[:iters]
     return res
+
+
+def confidence(guide, target, sigma_s: float, sigma_r: float, N: int, sigma_c: float):
+    """O7: Eq. (7) confidence c = exp(-V / (2 sigma_c^2)), V = DTF(t^2) - DTF(t)^2 clamped at 0.
+    Returns (c, V), each H x W float64."""
+    g = _f32(guide)
+    if g.ndim == 2:
+        g = g[:, :, None]
+    t = _f32(target)
+    H, W, Cg = g.shape
+    assert t.shape == (H, W)
+    c = np.empty((H, W), np.float64)
+    v = np.empty((H, W), np.float64)
+    st = _load().dts_oracle_confidence(_p(g, _c_float_p), H, W, Cg, sigma_s, sigma_r, N,
+                                       _p(t, _c_float_p), sigma_c, _p(c, _c_double_p), _p(v, _c_double_p))
+    if st:
+        raise ValueError(f"dts_oracle_confidence failed ({st})")
+    return c, v

@@ -339,3 +339,44 @@ done:
     free(Ax); free(Ay);
     return st;
 }
+
+/* ------------------------------------------------------------------------ */
+/* O7: confidence from the edge-aware variance (Eq. 7):
+ *     V_i = DT(z_i^2) - DT(z_i)^2,    c_i = exp(-V_i / (2 sigma_c^2))
+ * "the domain transform is treated as a local estimate of the mean in an edge-aware
+ * sense": DT is the O4 edge-aware mean DTF with the guide's coefficients, and
+ * z is the target (the confidence of the MC-CNN disparity target).  V is
+ * clamped at 0 (DTF is a convex combination, so V >= 0 up to rounding; reading R22).
+ * target: H x W fp32 (one channel); conf, var (optional): H x W doubles.         */
+int dts_oracle_confidence(const float* guide, int64_t H, int64_t W, int32_t Cg,
+                          double sigma_s, double sigma_r, int32_t N,
+                          const float* target, double sigma_c, double* conf, double* var) {
+    if (!guide || !target || !conf || H < 1 || W < 1 || Cg < 1 || N < 1) return ORACLE_E_ARG;
+    if (!(sigma_c > 0.0)) return ORACLE_E_ARG;
+    const int64_t HW = H * W;
+    double* dx = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* dy = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* X = (double*)malloc(sizeof(double) * (size_t)HW * 2);  /* [z ; z^2] planar */
+    int st = ORACLE_OK;
+    if (!dx || !dy || !X) { st = ORACLE_E_OOM; goto done; }
+    st = dts_oracle_distances(guide, H, W, Cg, sigma_s, sigma_r, dx, dy);        /* O1 */
+    if (st) goto done;
+    for (int64_t p = 0; p < HW; ++p) {
+        const double z = (double)target[p];
+        X[p] = z;
+        X[HW + p] = z * z;
+    }
+    st = dts_oracle_dtf(X, H, W, 2, dx, dy, sigma_s, N);                         /* O4 */
+    if (st) goto done;
+    for (int64_t p = 0; p < HW; ++p) {
+        double v = X[HW + p] - X[p] * X[p];                                      /* Eq. 7 */
+        if (v < 0.0) v = 0.0;
+        if (var) var[p] = v;
+        conf[p] = exp(-v / (2.0 * sigma_c * sigma_c));
+    }
+done:
+    free(dx);
+    free(dy);
+    free(X);
+    return st;
+}

@@ -345,3 +345,64 @@ def test_solve_thread_count_invariant():
     finally:
         oracle.set_threads(n0)
     np.testing.assert_array_equal(z8, z1)
+
+
+# ---------------------------------------------------------------- O7: Eq. (7) confidence
+def test_confidence_dense_operator():
+    """V = K t^2 - (K t)^2 with K built from the closed-form L/U products (tests/dense.py),
+    independent of the recurrences; c = exp(-V / 2 sigma_c^2)."""
+    g, t, _ = random_problem(5, 4, 3, 1, seed=21)
+    ss, sr, N, sc = 3.0, 0.4, 2, 0.7
+    dx, dy = oracle.distances(g, ss, sr)
+    K = dense.dtf_operator(dx, dy, oracle.sigmas(ss, N))
+    tv = t.astype(np.float64).ravel()
+    V = np.maximum(K @ (tv * tv) - (K @ tv) ** 2, 0.0).reshape(t.shape)
+    c, v = oracle.confidence(g, t, ss, sr, N, sc)
+    np.testing.assert_allclose(v, V, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(c, np.exp(-V / (2 * sc * sc)), rtol=0, atol=1e-13)
+    assert np.all(v >= 0) and np.all((c > 0) & (c <= 1))
+
+
+def test_confidence_edge_free_alternating_closed_form():
+    """Constant guide, N = 1, a row alternating {0, 2}: at interior pixels the one-pass kernel
+    h[k] = (1-a)/(1+a) a^|k| gives mean 1 + s r^(1/2) and mean of squares 2 + 2 s r^(1/2) with
+    r = ((1-a)/(1+a))^4, so V = 1 - ((1-a)/(1+a))^4 (SPEC's 'V -> 1 for wide windows' is a -> 1).
+    Choosing sigma_c^2 = V / 2 then gives c = e^-1 (Eq. 7 arithmetic)."""
+    W = 801
+    g = const_guide(1, W)
+    t = np.tile(np.array([0.0, 2.0], np.float32), W // 2 + 1)[:W][None, :]
+    ss = 9.0
+    a = math.exp(-math.sqrt(2.0) / ss)  # N = 1: sigma_1 = sigma_s, d = 1
+    Vexp = 1.0 - ((1 - a) / (1 + a)) ** 4
+    sc = math.sqrt(Vexp / 2)
+    c, v = oracle.confidence(g, t, ss, 0.3, 1, sc)
+    mid = slice(300, 501)
+    np.testing.assert_allclose(v[0, mid], Vexp, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(c[0, mid], math.exp(-1.0), rtol=0, atol=1e-12)
+
+
+def test_confidence_constant_target_and_range():
+    g, _, _ = random_problem(20, 30, 3, 1, seed=4)
+    t = np.full((20, 30), 3.25, np.float32)
+    c, v = oracle.confidence(g, t, 5.0, 0.2, 3, 0.5)
+    assert np.max(v) <= 1e-12 and np.max(np.abs(c - 1.0)) <= 1e-12
+    g, t, _ = random_problem(25, 33, 3, 1, seed=5)
+    c, v = oracle.confidence(g, t, 5.0, 0.2, 3, 0.5)
+    assert np.all(v >= 0) and np.all((c > 0) & (c <= 1))
+    c2, _ = oracle.confidence(g, t, 5.0, 0.2, 3, 1.0)  # larger sigma_c: never less confident
+    assert np.all(c2 >= c)
+
+
+def test_confidence_decoupled_regions_exact():
+    """A guide edge with tiny sigma_r underflows A to exactly 0: region A's variance is
+    bit-identical whatever the target in region B."""
+    H, W = 12, 20
+    g = np.zeros((H, W, 3), np.float32)
+    g[:, W // 2:] = 1.0
+    rng = np.random.default_rng(3)
+    t1 = rng.uniform(0, 1, (H, W)).astype(np.float32)
+    t2 = t1.copy()
+    t2[:, W // 2:] = rng.uniform(5, 9, (H, W - W // 2)).astype(np.float32)
+    _, v1 = oracle.confidence(g, t1, 6.0, 1e-3, 3, 0.5)
+    _, v2 = oracle.confidence(g, t2, 6.0, 1e-3, 3, 0.5)
+    assert np.array_equal(v1[:, :W // 2], v2[:, :W // 2])
