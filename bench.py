@@ -282,6 +282,28 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / e_steps,
                "check_max_abs_vs_device": float((host_out[0].to(dev) - outs[0]).abs().max().item())}
 
+    # ---- Eq. (7) confidence on the same guide/target (single image, N = 1) ----
+    extras = {}
+    if world == 1 and band is None and cfg.batch == 1 and cfg.Ct == 1:
+        g0, t0, _ = dev_in[0]
+        conf_out = torch.empty_like(t0)
+        var_out = torch.empty_like(t0)
+        ctx = make_ctx(g0)
+        sc = 0.5 * float(t0.max().item() - t0.min().item())  # sigma_c: half the target range (R22)
+        dts.dts_confidence(ctx, t0, sc, conf_out, var_out, stream=stream.cuda_stream)  # warm-up
+        reps = 3
+        c_ms = timed(lambda: dts.dts_confidence(ctx, t0, sc, conf_out, var_out, stream=stream.cuda_stream), reps)
+        dts.dts_destroy(ctx)
+        c_ms /= reps
+        px = t0.numel()
+        cbytes = px * (28.0 + 40.0 * cfg.N)  # t in, [t, t^2] out; N x (row + col, C_t = 2); X in, c + V out
+        # (on C4 the column passes run plane by plane: +4 B/pixel each, not counted as algorithmic)
+        peak_c, _ = measured_peaks()
+        extras["confidence"] = {"what": "dts_confidence (Eq. 7): DT(t^2) - DT(t)^2 -> c, same guide", "sigma_c": sc,
+                                "ms": c_ms, "mpix_per_s": px / 1e6 / (c_ms / 1e3),
+                                "gbs_algorithmic": cbytes / (c_ms / 1e3) / 1e9,
+                                "frac": cbytes / (c_ms / 1e3) / 1e9 / peak_c}
+
     if rank != 0:
         if comm:
             dts.dts_comm_destroy(comm)
@@ -332,7 +354,7 @@ def main():
             "roofline": roofline,
             "kernels": {k: {kk: v[kk] for kk in ("launches", "avg_ms", "bytes_per_launch", "gbs", "share_of_step")}
                         for k, v in fams.items()},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk, "extras": extras}
     print(json.dumps(line), flush=True)
     if comm:
         dts.dts_comm_destroy(comm)

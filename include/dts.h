@@ -114,6 +114,23 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t target_channe
                         const float* confidence, float lambda, int32_t iterations,
                         float* out, void* stream, const dts_solve_opts* opts);
 
+/* Confidence from the edge-aware variance, Eq. (7) of the paper:
+ *     V_i = DT(t_i^2) - DT(t_i)^2   (clamped at 0),     c_i = exp(-V_i / (2 sigma_c^2))
+ * where DT is the context's N-pass edge-aware mean (the same recursive filter and
+ * coefficients dts_solve uses) and t a one-channel target, e.g. the disparity
+ * whose confidence feeds dts_solve.  SURVEY 8(f) #1.
+ *   target     H x W fp32 (device or host pointer), finite.
+ *   sigma_c    variance scale, finite, > 0 (the paper gives no value; SPEC S:210 uses 16
+ *              disparity units as a default).
+ *   conf_out   H x W fp32, receives c in (0, 1]; must not overlap target.
+ *   var_out    optional (NULL allowed) H x W fp32, receives V >= 0.
+ * Stream-ordered like dts_solve; host pointers are staged (and the call synchronises).
+ * Errors: DTS_E_ARG (NULL / overlapping pointers, sigma_c <= 0 or not finite),
+ *         DTS_E_CUDA / DTS_E_OOM from the device.  Uses the context's solver buffers,
+ *         so it must not run concurrently with dts_solve on the same context. */
+dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, float* conf_out, float* var_out,
+                          void* stream);
+
 /* Buffers a test can read back (row-major H x W, fp32; stream-ordered then synchronised). */
 typedef enum { DTS_BUF_DX = 0, DTS_BUF_DY = 1, DTS_BUF_SUPPORT = 2 } dts_buffer;
 /* Copies the H x W buffer `which` into host memory `host_out` (H*W floats). */

@@ -17,7 +17,8 @@ import os
 
 import numpy as np
 
-__all__ = ["DTSError", "dts_create", "dts_solve", "dts_solve_ex", "dts_destroy", "dts_status_string",
+__all__ = ["DTSError", "dts_create", "dts_solve", "dts_solve_ex", "dts_confidence", "dts_destroy",
+           "dts_status_string",
            "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback", "dts_comm_destroy",
            "dts_create_band", "band_rows", "band_guide_rows",
            "dts_debug_read", "dts_profile_enable", "dts_profile_read", "dts_launch_count", "dts_version",
@@ -34,7 +35,7 @@ DTS_BUF_DX, DTS_BUF_DY, DTS_BUF_SUPPORT = 0, 1, 2
 ABI_FUNCTIONS = ["dts_create", "dts_solve", "dts_destroy", "dts_status_string", "dts_last_error_string",
                  "dts_solve_ex", "dts_debug_read", "dts_profile_enable", "dts_profile_read",
                  "dts_launch_count", "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback",
-                 "dts_comm_destroy", "dts_create_band", "dts_version"]
+                 "dts_comm_destroy", "dts_create_band", "dts_version", "dts_confidence"]
 
 
 class DTSError(RuntimeError):
@@ -75,6 +76,8 @@ def load_library():
     lib.dts_solve.restype = ctypes.c_int
     lib.dts_solve_ex.argtypes = [vp, vp, i32, vp, f32, i32, vp, vp, ctypes.POINTER(SolveOpts)]
     lib.dts_solve_ex.restype = ctypes.c_int
+    lib.dts_confidence.argtypes = [vp, vp, f32, vp, vp, vp]
+    lib.dts_confidence.restype = ctypes.c_int
     lib.dts_destroy.argtypes = [vp]
     lib.dts_destroy.restype = None
     lib.dts_status_string.argtypes = [ctypes.c_int]
@@ -179,6 +182,16 @@ def dts_solve(ctx: int, target, confidence, lam: float, iterations: int, out, st
                                   iterations, _ptr(out, "out"), _stream(stream, target, confidence, out))
     _check(st, "dts_solve")
     return out
+
+
+def dts_confidence(ctx: int, target, sigma_c: float, conf_out, var_out=None, stream=None):
+    """Eq. (7): conf_out = exp(-V / (2 sigma_c^2)), V = DT(t^2) - DT(t)^2 (>= 0) -> var_out.
+    target, conf_out, var_out: H x W float32 (device tensors or host arrays)."""
+    st = load_library().dts_confidence(ctx, _ptr(target, "target"), sigma_c, _ptr(conf_out, "conf_out"),
+                                       _ptr(var_out, "var_out") if var_out is not None else None,
+                                       _stream(stream, target, conf_out))
+    _check(st, "dts_confidence")
+    return conf_out
 
 
 def dts_destroy(ctx: int) -> None:
@@ -289,6 +302,15 @@ class Solver:
         if opts:
             return dts_solve_ex(self.ctx, target, confidence, lam, iterations, out, stream, **opts)
         return dts_solve(self.ctx, target, confidence, lam, iterations, out, stream)
+
+    def confidence(self, target, sigma_c: float, out=None, var_out=None, stream=None):
+        if out is None:
+            if isinstance(target, np.ndarray):
+                out = np.empty_like(target)
+            else:
+                import torch
+                out = torch.empty_like(target)
+        return dts_confidence(self.ctx, target, sigma_c, out, var_out, stream)
 
     def read(self, which: int) -> np.ndarray:
         return dts_debug_read(self.ctx, which, self.H, self.W)

@@ -124,11 +124,11 @@ namespace {
 
 enum Family {
     F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
-    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_COUNT
+    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
-                                     "rank_compose", "row_update"};
+                                     "rank_compose", "row_update", "confidence"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -767,6 +767,75 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     if (any_host) {
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e);
     }
+    return DTS_OK;
+}
+
+dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, float* conf_out, float* var_out,
+                          void* stream) {
+    if (!ctx || !target || !conf_out) return DTS_E_ARG;
+    if (!std::isfinite(sigma_c) || !(sigma_c > 0.f)) return DTS_E_ARG;
+    if (ctx->comm) return DTS_E_SHAPE;  // row-band contexts: not supported (yet)
+    const Geometry& g = ctx->g;
+    const size_t cb = (size_t)g.H * g.W * sizeof(float);
+    if (overlaps(conf_out, cb, target, cb) || (var_out && (overlaps(var_out, cb, target, cb) ||
+                                                           overlaps(var_out, cb, conf_out, cb))))
+        return DTS_E_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->last_stream = s;
+    RowPlan rp;
+    ColPlan cp, cp1;
+    if (plan_row_pass(g, 2, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess ||
+        plan_col(g, 2, MODE_FILTER, ctx->num_sms, &cp) != cudaSuccess)
+        return DTS_E_SHAPE;
+    // when two planes do not fit the cluster column kernel (tall images) but one does, the
+    // column passes run plane by plane on it
+    const bool per_plane = cp.kind != 1 && plan_col(g, 1, MODE_FILTER, ctx->num_sms, &cp1) == cudaSuccess &&
+                           cp1.kind == 1;
+    cudaGetLastError();
+    const PtrKind kt = classify(target, ctx->device), kc = classify(conf_out, ctx->device),
+                  kv = var_out ? classify(var_out, ctx->device) : PTR_DEVICE;
+    if (kt == PTR_BAD || kc == PTR_BAD || kv == PTR_BAD) return DTS_E_ARG;
+    const bool any_host = kt == PTR_HOST || kc == PTR_HOST || kv == PTR_HOST;
+    dts_status st;
+    cudaError_t e;
+    if (any_host && (st = ensure_staging(ctx, cb, s)) != DTS_OK) return st;
+    const float* t_d = target;
+    float* c_d = kc == PTR_HOST ? ctx->st_o : conf_out;
+    float* v_d = (var_out && kv == PTR_HOST) ? ctx->st_c : var_out;
+    if (kt == PTR_HOST) {
+        if ((e = cudaMemcpyAsync(ctx->st_t, target, cb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+            return cuda_fail(e);
+        t_d = ctx->st_t;
+    }
+    if ((st = ensure_solver_state(ctx, 2, s)) != DTS_OK) return st;
+    if ((st = ensure_col_scratch(ctx, cp, s)) != DTS_OK) return st;
+    const double px = (double)g.H * g.W;
+    // planes [t ; t^2] -> DTF (N passes of rows then columns) -> Eq. (7)
+    st = run_launch(ctx, F_CONF, px * 12.0, s, [&] { return launch_conf_prologue(t_d, g, ctx->X, s); });
+    for (int i = 0; i < ctx->N && st == DTS_OK; ++i) {
+        st = run_launch(ctx, F_ROW, px * 20.0, s, [&] {
+            return launch_row_pass(rp, g, 2, MODE_FILTER, ctx->X, ctx->X, ctx->dx, ctx->kc[i], s);
+        });
+        if (st == DTS_OK && !per_plane)
+            st = run_launch(ctx, F_COL, px * 20.0, s, [&] {
+                return col_launch(ctx, cp, 2, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
+            });
+        for (int v = 0; v < 2 && st == DTS_OK && per_plane; ++v)
+            st = run_launch(ctx, F_COL, px * 12.0, s, [&] {
+                return col_launch(ctx, cp1, 1, MODE_FILTER, ctx->X + v * g.plane, ctx->dy, ctx->kc[i], nullptr,
+                                  nullptr, s);
+            });
+    }
+    const float inv = 1.f / (2.f * sigma_c * sigma_c);
+    if (st == DTS_OK)
+        st = run_launch(ctx, F_CONF, px * (var_out ? 16.0 : 12.0), s,
+                        [&] { return launch_conf_epilogue(ctx->X, g, inv, c_d, v_d, s); });
+    if (st != DTS_OK) return st;
+    if (kc == PTR_HOST && (e = cudaMemcpyAsync(conf_out, c_d, cb, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cuda_fail(e);
+    if (var_out && kv == PTR_HOST && (e = cudaMemcpyAsync(var_out, v_d, cb, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cuda_fail(e);
+    if (any_host && (e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e);
     return DTS_OK;
 }
 

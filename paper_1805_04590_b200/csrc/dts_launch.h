@@ -87,6 +87,12 @@ cudaError_t plan_col_2p(const Geometry& g, int Ct, int mode, int num_sms, ColPla
 cudaError_t launch_col_2p(const ColPlan& plan, const Geometry& g, int Ct, float* x, const float* d, float kc,
                           const ColScratch& scr, cudaStream_t s);
 
+// Eq. (7) confidence: planar X0 = t, X1 = t^2 from a row-major H x W
+// target; and, after the DTF of both planes, V = max(0, X1 - X0^2), c = exp(-V / (2 sc^2)).
+cudaError_t launch_conf_prologue(const float* target, const Geometry& g, float* X, cudaStream_t s);
+cudaError_t launch_conf_epilogue(const float* X, const Geometry& g, float inv_2sc2, float* conf, float* var,
+                                 cudaStream_t s);
+
 // fill n floats with v
 cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);
 

@@ -363,4 +363,48 @@ cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Eq. (7) confidence: the two planes the DTF turns into local moments.  The
+// target is shifted by t[0] first: DT is row-stochastic, so V(t - k) = V(t) exactly, and
+// the shift keeps DT(t^2) - DT(t)^2 from cancelling catastrophically in fp32 when |t| is
+// large against its range (reading R22).  2-D grid: blockIdx.y walks rows, threads columns.
+__global__ void __launch_bounds__(256) k_conf_prologue(const float* __restrict__ t, Geometry g, float* __restrict__ X) {
+    const float k0 = __ldg(t);
+    for (int64_t r = blockIdx.y; r < g.H; r += gridDim.y) {
+        for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.W; c += (int64_t)gridDim.x * blockDim.x) {
+            const float v = __ldg(t + r * g.W + c) - k0;
+            X[r * g.pitch + c] = v;
+            X[g.plane + r * g.pitch + c] = v * v;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_conf_epilogue(const float* __restrict__ X, Geometry g, float inv_2sc2,
+                                                       float* __restrict__ conf, float* __restrict__ var) {
+    for (int64_t r = blockIdx.y; r < g.H; r += gridDim.y) {
+        for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.W; c += (int64_t)gridDim.x * blockDim.x) {
+            const float m1 = X[r * g.pitch + c], m2 = X[g.plane + r * g.pitch + c];
+            const float v = fmaxf(fmaf(-m1, m1, m2), 0.f);  // DT(t^2) - DT(t)^2, clamped (R22)
+            conf[r * g.W + c] = __expf(-v * inv_2sc2);
+            if (var) var[r * g.W + c] = v;
+        }
+    }
+}
+
+static dim3 conf_grid(const Geometry& g) {
+    const int64_t bx = (g.W + 255) / 256;
+    const int64_t by = g.H < 8192 ? g.H : 8192;
+    return dim3((unsigned)(bx < 64 ? bx : 64), (unsigned)by, 1);
+}
+
+cudaError_t launch_conf_prologue(const float* target, const Geometry& g, float* X, cudaStream_t s) {
+    k_conf_prologue<<<conf_grid(g), 256, 0, s>>>(target, g, X);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_conf_epilogue(const float* X, const Geometry& g, float inv_2sc2, float* conf, float* var,
+                                 cudaStream_t s) {
+    k_conf_epilogue<<<conf_grid(g), 256, 0, s>>>(X, g, inv_2sc2, conf, var);
+    return cudaGetLastError();
+}
+
 }  // namespace dts
