@@ -94,6 +94,7 @@ struct dts_ctx {
     float* dx = nullptr;
     float* dy = nullptr;
     float* S = nullptr;
+    float* Sy = nullptr;  // column support factor when the cluster kernel computes it (S then holds s_x)
     // solver state (allocated for ct_cap target channels)
     int ct_cap = 0;
     float* Z = nullptr;
@@ -517,10 +518,17 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
         if (comm)
             st = col_pass_banded(ctx, 1, MODE_SUPPORT, nullptr, ctx->ks, nullptr, ctx->S, F_SUPPORT_COL, px * 12.0,
                                  s);
-        else
+        else if (cp.kind == 1) {  // cluster kernel: s_y into its own plane (no read-modify-write of S)
+            if ((e = cudaMallocAsync((void**)&ctx->Sy, plane, s)) != cudaSuccess) st = cuda_fail(e);
+            if (st == DTS_OK)
+                st = run_launch(ctx, F_SUPPORT_COL, px * 8.0, s, [&] {
+                    return col_launch(ctx, cp, 1, MODE_SUPPORT, nullptr, ctx->dy, ctx->ks, nullptr, ctx->Sy, s);
+                });
+        } else {
             st = run_launch(ctx, F_SUPPORT_COL, px * 12.0, s, [&] {
                 return col_launch(ctx, cp, 1, MODE_SUPPORT, nullptr, ctx->dy, ctx->ks, nullptr, ctx->S, s);
             });
+        }
     }
     if (gstage) {
         cudaFreeAsync(gstage, s);
@@ -668,8 +676,8 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         if ((st = ensure_col_scratch(ctx, cpf, s)) != DTS_OK) return st;
         if ((st = ensure_col_scratch(ctx, cpu, s)) != DTS_OK) return st;
         const double px = (double)g.H * g.W;
-        st = run_launch(ctx, F_PROLOGUE, px * (12.0 * Ct + 12), s, [&] {
-            return launch_prologue(t_d, c_d, Ct, g, ctx->S, support_mode, ctx->Z, ctx->T, ctx->chat, s);
+        st = run_launch(ctx, F_PROLOGUE, px * (12.0 * Ct + 12 + (ctx->Sy ? 4.0 : 0.0)), s, [&] {
+            return launch_prologue(t_d, c_d, Ct, g, ctx->S, ctx->Sy, support_mode, ctx->Z, ctx->T, ctx->chat, s);
         });
         if (st != DTS_OK) return st;
         const double row_bytes = px * (8.0 * Ct + 4);
@@ -848,7 +856,7 @@ void dts_destroy(dts_ctx* ctx) {
     if (!ctx) return;
     cudaStream_t s = ctx->last_stream;
     free_solver_state(ctx, s);
-    for (float** p : {&ctx->dx_base, &ctx->dy_base, &ctx->S, &ctx->st_t, &ctx->st_c, &ctx->st_o, &ctx->rank_tup,
+    for (float** p : {&ctx->dx_base, &ctx->dy_base, &ctx->S, &ctx->Sy, &ctx->st_t, &ctx->st_c, &ctx->st_o, &ctx->rank_tup,
                       &ctx->gathered, &ctx->ext}) {
         if (*p) cudaFreeAsync(*p, s);
         *p = nullptr;
@@ -869,6 +877,14 @@ dts_status dts_debug_read(dts_ctx* ctx, dts_buffer which, float* host_out) {
     cudaError_t e = cudaMemcpy2DAsync(host_out, ctx->g.W * sizeof(float), src, ctx->g.pitch * sizeof(float),
                                       ctx->g.W * sizeof(float), ctx->g.H, cudaMemcpyDeviceToHost, ctx->last_stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->last_stream);
+    if (e == cudaSuccess && which == DTS_BUF_SUPPORT && ctx->Sy) {  // S = s_x * s_y
+        std::vector<float> sy((size_t)ctx->g.H * ctx->g.W);
+        e = cudaMemcpy2DAsync(sy.data(), ctx->g.W * sizeof(float), ctx->Sy, ctx->g.pitch * sizeof(float),
+                              ctx->g.W * sizeof(float), ctx->g.H, cudaMemcpyDeviceToHost, ctx->last_stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->last_stream);
+        if (e == cudaSuccess)
+            for (size_t i = 0; i < sy.size(); ++i) host_out[i] *= sy[i];
+    }
     return e == cudaSuccess ? DTS_OK : cuda_fail(e);
 }
 

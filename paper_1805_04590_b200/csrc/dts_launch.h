@@ -106,7 +106,9 @@ cudaError_t launch_rank_compose(const float* gathered, int P, int rank, int ntil
                                 cudaStream_t s);
 
 // K6: solve prologue -- planar Z = T = target, chat = c / S (or c when support_mode = 1).
+// Sy (nullable): the column support factor kept separately (S = s_x, chat = c / (S Sy))
 cudaError_t launch_prologue(const float* target, const float* conf, int Ct, const Geometry& g, const float* S,
+                            const float* Sy,
                             int support_mode, float* Z, float* T, float* chat, cudaStream_t s);
 
 // optional input checks: counts non-finite target/confidence values and confidences outside [0, 1]

@@ -31,7 +31,7 @@ constexpr int LS = 32;  // rows per warp segment (registers)
 struct Params {
     float* x;        // planar state (in; FILTER: out)
     const float* d;  // d_y
-    float* support;  // SUPPORT: S *= s_y
+    float* support;  // SUPPORT: receives s_y (the solve multiplies it into S in the prologue)
     UpdateArgs upd;
     int64_t plane, pitch;
     int H, W, HB, S, CB, ntiles;
@@ -340,14 +340,10 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
 #pragma unroll
                             for (int v = 0; v < NV; ++v) p.x[v * p.plane + o] = xv[v][j];
                         }
-                } else if constexpr (MODE == MODE_SUPPORT) {
-                    float sv[LS];  // all loads in flight before any store
+                } else if constexpr (MODE == MODE_SUPPORT) {  // the column factor s_y into its own plane
 #pragma unroll
                     for (int j = 0; j < LS; ++j)
-                        sv[j] = p.support[(int64_t)(r0 + lo + (j < nrow ? j : 0)) * p.pitch + col];
-#pragma unroll
-                    for (int j = 0; j < LS; ++j)
-                        if (j < nrow) p.support[(int64_t)(r0 + lo + j) * p.pitch + col] = sv[j] * xv[0][j];
+                        if (j < nrow) p.support[(int64_t)(r0 + lo + j) * p.pitch + col] = xv[0][j];
                 } else {  // MODE_UPDATE, Eq. (3) with zbar = xv
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {

@@ -223,7 +223,8 @@ cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Ge
 // and confidence when a row of them is 16-B aligned, i.e. W % 4 == 0 and C_t == 1).
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_prologue(const float* __restrict__ target, const float* __restrict__ conf,
-                                                  int Ct, Geometry g, const float* __restrict__ S, int support_mode,
+                                                  int Ct, Geometry g, const float* __restrict__ S,
+                                                  const float* __restrict__ Sy, int support_mode,
                                                   float* __restrict__ Z, float* __restrict__ T,
                                                   float* __restrict__ chat) {
     const int64_t per_row = g.pitch / 4;
@@ -242,7 +243,11 @@ __global__ void __launch_bounds__(256) k_prologue(const float* __restrict__ targ
 #pragma unroll
             for (int u = 0; u < 4; ++u) cv[u] = (c4 + u < g.W) ? __ldg(conf + p + u) : 0.f;
         }
-        const float4 sv = __ldg(reinterpret_cast<const float4*>(S + o));
+        float4 sv = __ldg(reinterpret_cast<const float4*>(S + o));
+        if (Sy) {  // support kept as its two separable factors: S = s_x s_y (R7)
+            const float4 sy = __ldg(reinterpret_cast<const float4*>(Sy + o));
+            sv = make_float4(sv.x * sy.x, sv.y * sy.y, sv.z * sy.z, sv.w * sy.w);
+        }
         const float ss[4] = {sv.x, sv.y, sv.z, sv.w};
         float ch[4];
 #pragma unroll
@@ -265,6 +270,7 @@ __global__ void __launch_bounds__(256) k_prologue(const float* __restrict__ targ
 }
 
 cudaError_t launch_prologue(const float* target, const float* conf, int Ct, const Geometry& g, const float* S,
+                            const float* Sy,
                             int support_mode, float* Z, float* T, float* chat, cudaStream_t s) {
     const int64_t n = g.H * (g.pitch / 4);
     int64_t blocks = (n + 255) / 256;
@@ -272,9 +278,9 @@ cudaError_t launch_prologue(const float* target, const float* conf, int Ct, cons
     if (blocks < 1) blocks = 1;
     const bool vec = Ct == 1 && g.W % 4 == 0 && ((uintptr_t)target % 16 == 0) && ((uintptr_t)conf % 16 == 0);
     if (vec)
-        k_prologue<true><<<(unsigned)blocks, 256, 0, s>>>(target, conf, Ct, g, S, support_mode, Z, T, chat);
+        k_prologue<true><<<(unsigned)blocks, 256, 0, s>>>(target, conf, Ct, g, S, Sy, support_mode, Z, T, chat);
     else
-        k_prologue<false><<<(unsigned)blocks, 256, 0, s>>>(target, conf, Ct, g, S, support_mode, Z, T, chat);
+        k_prologue<false><<<(unsigned)blocks, 256, 0, s>>>(target, conf, Ct, g, S, Sy, support_mode, Z, T, chat);
     return cudaGetLastError();
 }
 
