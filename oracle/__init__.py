@@ -14,8 +14,9 @@ Functions (each cites the passage its C routine follows; see dts_oracle.c):
   support(dx, dy, sigma_s, mode)                O5  S = sum_j W_ij
   solve(guide, target, conf, ...)               O6  Eq. (3) gradient descent
   confidence(guide, target, ..., sigma_c)       O7  Eq. (7) edge-aware variance confidence
+  solve_stereo(left, right, target, conf, ...)  O8  Eq. (10) stereo refinement, Charbonnier target
 
-Parity status: O1, O3, O4, O5, O6 and O7 are pinned by tests/test_oracle_pins.py
+Parity status: O1, O3, O4, O5, O6, O7 and O8 are pinned by tests/test_oracle_pins.py
 (worked examples, dense triangular matrices, closed forms, brute force,
 reductions); the whole solve is NOT pinned against the paper's own outputs,
 which it never prints ("parity unpinned vs the paper").
@@ -70,6 +71,9 @@ def _load():
     lib.dts_oracle_confidence.argtypes = [_c_float_p, i64, i64, i32, dbl, dbl, i32, _c_float_p, dbl,
                                           _c_double_p, _c_double_p]
     lib.dts_oracle_confidence.restype = ctypes.c_int
+    lib.dts_oracle_solve_stereo.argtypes = [_c_float_p, _c_float_p, i64, i64, i32, dbl, dbl, i32, _c_float_p,
+                                            _c_float_p, dbl, dbl, i32, dbl, dbl, i32, _c_double_p]
+    lib.dts_oracle_solve_stereo.restype = ctypes.c_int
     lib.dts_oracle_num_threads.argtypes = []
     lib.dts_oracle_num_threads.restype = ctypes.c_int
     lib.dts_oracle_set_threads.argtypes = [ctypes.c_int]
@@ -202,3 +206,26 @@ def confidence(guide, target, sigma_s: float, sigma_r: float, N: int, sigma_c: f
     if st:
         raise ValueError(f"dts_oracle_confidence failed ({st})")
     return c, v
+
+
+def solve_stereo(left, right, target, confidence, sigma_s: float, sigma_r: float, N: int, lam: float,
+                 iters: int, gamma: float, eps: float = 1e-3, step: float = 0.99, support_mode: int = 0):
+    """O8: Eq. (10) stereo refinement with the Charbonnier target term.  left (the guide) and
+    right: H x W x Cg; target, confidence: H x W.  Returns z (H x W float64)."""
+    g = _f32(left)
+    if g.ndim == 2:
+        g = g[:, :, None]
+    rr = _f32(right)
+    if rr.ndim == 2:
+        rr = rr[:, :, None]
+    t = _f32(target)
+    c = _f32(confidence)
+    H, W, Cg = g.shape
+    assert rr.shape == g.shape and t.shape == (H, W) and c.shape == (H, W)
+    out = np.empty((H, W), np.float64)
+    st = _load().dts_oracle_solve_stereo(_p(g, _c_float_p), _p(rr, _c_float_p), H, W, Cg, sigma_s, sigma_r, N,
+                                         _p(t, _c_float_p), _p(c, _c_float_p), lam, step, iters, gamma, eps,
+                                         support_mode, _p(out, _c_double_p))
+    if st:
+        raise ValueError(f"dts_oracle_solve_stereo failed ({st})")
+    return out

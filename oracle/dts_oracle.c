@@ -380,3 +380,79 @@ done:
     free(X);
     return st;
 }
+
+/* ------------------------------------------------------------------------ */
+/* O8: stereo refinement (Eq. 10): gradient descent on
+ *     lambda/2 sum (z - zbar)^2 + sum c rho(z - t) + 1/2 sum gamma ||I_L(i) - I_R(i - z_i)||^2
+ * with the Charbonnier rho(r) = sqrt(r^2 + eps^2) on the target term.  In the
+ * convention of Eq. (3) (reading R23):
+ *     g = lambda (z - zbar) + chat rho'(z - t) + gamma sum_k (I_L,k(x) - I_R,k(u)) dI_R,k/dx(u),
+ *     rho'(r) = r / sqrt(r^2 + eps^2),   u = x - z   (rectified pair: disparity along the row),
+ * I_L = the guide, I_R sampled by linear interpolation along the row; outside
+ * [0, W-1] the sample is clamped and its derivative is 0.  chat = c / S as in O6;
+ * z^0 = t; z <- z - step g.  guide / right: H x W x Cg fp32 HWC; target, conf: H x W.   */
+static void stereo_sample(const float* right, int64_t W, int32_t Cg, int64_t r, double u, int32_t k,
+                          double* val, double* slope) {
+    const float* row = right + (size_t)r * (size_t)W * (size_t)Cg;
+    if (W == 1) { *val = row[k]; *slope = 0.0; return; }
+    const int inside = (u >= 0.0 && u <= (double)(W - 1));
+    double uc = u < 0.0 ? 0.0 : (u > (double)(W - 1) ? (double)(W - 1) : u);
+    int64_t x0 = (int64_t)floor(uc);
+    if (x0 > W - 2) x0 = W - 2;
+    const double f = uc - (double)x0;
+    const double a = row[x0 * Cg + k], b = row[(x0 + 1) * Cg + k];
+    *val = (1.0 - f) * a + f * b;
+    *slope = inside ? (b - a) : 0.0;
+}
+
+int dts_oracle_solve_stereo(const float* guide, const float* right, int64_t H, int64_t W, int32_t Cg,
+                            double sigma_s, double sigma_r, int32_t N, const float* target,
+                            const float* confidence, double lambda, double step, int32_t iters,
+                            double gamma, double eps, int32_t support_mode, double* out) {
+    if (!guide || !right || !target || !confidence || !out) return ORACLE_E_ARG;
+    if (H < 1 || W < 1 || Cg < 1 || N < 1 || iters < 0 || !(eps > 0.0)) return ORACLE_E_ARG;
+    const int64_t HW = H * W;
+    double* dx = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* dy = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* S = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* Z = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* Zbar = (double*)malloc(sizeof(double) * (size_t)HW);
+    double *Ax = NULL, *Ay = NULL;
+    int st = ORACLE_OK;
+    if (!dx || !dy || !S || !Z || !Zbar) { st = ORACLE_E_OOM; goto done; }
+    st = dts_oracle_distances(guide, H, W, Cg, sigma_s, sigma_r, dx, dy);        /* O1 */
+    if (st) goto done;
+    st = dts_oracle_support(dx, dy, H, W, sigma_s, support_mode, S);            /* O5 */
+    if (st) goto done;
+    st = make_coefs(dx, dy, H, W, sigma_s, N, &Ax, &Ay);                        /* O2 */
+    if (st) goto done;
+    for (int64_t p = 0; p < HW; ++p) Z[p] = (double)target[p];
+    for (int32_t k = 0; k < iters; ++k) {
+        memcpy(Zbar, Z, sizeof(double) * (size_t)HW);
+        dtf_with_coefs(Zbar, H, W, 1, N, Ax, Ay);                               /* O4 */
+        int64_t p;
+#pragma omp parallel for schedule(static)
+        for (p = 0; p < HW; ++p) {
+            const int64_t r = p / W, x = p % W;
+            const double z = Z[p], res = z - (double)target[p];
+            const double rho1 = res / sqrt(res * res + eps * eps);              /* Charbonnier */
+            double gp = 0.0;
+            if (gamma != 0.0) {
+                const double u = (double)x - z;
+                for (int32_t ch = 0; ch < Cg; ++ch) {
+                    double v, sl;
+                    stereo_sample(right, W, Cg, r, u, ch, &v, &sl);
+                    gp += ((double)guide[(size_t)p * (size_t)Cg + (size_t)ch] - v) * sl;
+                }
+            }
+            const double chat = (double)confidence[p] / S[p];
+            Zbar[p] = z - step * (lambda * (z - Zbar[p]) + chat * rho1 + gamma * gp);  /* Eq. (10) step */
+        }
+        memcpy(Z, Zbar, sizeof(double) * (size_t)HW);
+    }
+    for (int64_t p = 0; p < HW; ++p) out[p] = Z[p];
+done:
+    free(dx); free(dy); free(S); free(Z); free(Zbar);
+    free(Ax); free(Ay);
+    return st;
+}

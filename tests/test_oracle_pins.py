@@ -13,7 +13,7 @@ import pytest
 
 import oracle
 from tests import dense
-from synth import make_inputs, random_problem
+from synth import make_inputs, random_problem, target_range
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
 SS = GOLD["sigma_s"]  # a = 1/2
@@ -406,3 +406,79 @@ def test_confidence_decoupled_regions_exact():
     _, v1 = oracle.confidence(g, t1, 6.0, 1e-3, 3, 0.5)
     _, v2 = oracle.confidence(g, t2, 6.0, 1e-3, 3, 0.5)
     assert np.array_equal(v1[:, :W // 2], v2[:, :W // 2])
+
+
+# ---------------------------------------------------------------- O8: Eq. (10) stereo
+def test_stereo_reduces_to_solve_for_large_eps():
+    """gamma = 0 and eps >> |z - t|: rho'(r) = r / sqrt(r^2 + eps^2) = r / eps (1 + O(r^2/eps^2)),
+    so with confidence c * eps the stereo iteration is the O6 iteration with c."""
+    g, t, c = random_problem(14, 17, 3, 1, seed=31)
+    eps = 1e7
+    ref = oracle.solve(g, t, c, 5.0, 0.2, 3, 0.99, 6)
+    got = oracle.solve_stereo(g, g, t, (c.astype(np.float64) * eps).astype(np.float32), 5.0, 0.2, 3, 0.99, 6,
+                              gamma=0.0, eps=eps)
+    assert np.max(np.abs(got - ref)) <= 1e-6 * target_range(t)
+
+
+def test_stereo_fixed_point_at_true_disparity():
+    """Right image = left image shifted by an integer disparity d*: at z = d* every in-range
+    residual I_L(x) - I_R(x - d*) is 0 and out-of-range samples have zero slope, so the
+    gradient vanishes and z = t = d* is a fixed point."""
+    rng = np.random.default_rng(8)
+    H, W, C, dstar = 9, 40, 3, 5
+    L = rng.uniform(0, 1, (H, W, C)).astype(np.float32)
+    R = np.empty_like(L)
+    R[:, :W - dstar] = L[:, dstar:]   # I_R(u) = I_L(u + d*)
+    R[:, W - dstar:] = L[:, -1:]
+    t = np.full((H, W), float(dstar), np.float32)
+    c = np.full((H, W), 0.5, np.float32)
+    # eps in the contractive regime (the paper's eps = 1e-3 makes rho' stiff at r = 0: curvature
+    # chat / eps > 2 / step, so rounding-level deviations grow until |r| ~ eps; DESIGN.md R23)
+    got = oracle.solve_stereo(L, R, t, c, 6.0, 0.3, 3, 0.99, 5, gamma=0.3, eps=1.0)
+    assert np.max(np.abs(got - dstar)) <= 1e-12
+
+
+def test_stereo_photometric_gradient_finite_difference():
+    """One step with lambda = 0 and c = 0 isolates the photometric gradient:
+    z1 = z0 - step gamma dE_p/dz; compare with a central finite difference of the brute-force
+    energy E_p(z) = 1/2 sum_k (I_L,k(x) - interp(I_R,k)(x - z))^2 at non-integer u."""
+    rng = np.random.default_rng(12)
+    H, W, C = 3, 30, 2
+    L = rng.uniform(0, 1, (H, W, C)).astype(np.float32)
+    R = rng.uniform(0, 1, (H, W, C)).astype(np.float32)
+    t = (rng.uniform(2.1, 2.9, (H, W))).astype(np.float32)  # u = x - z never integer, inside for x >= 3
+    c = np.zeros((H, W), np.float32)
+    gamma, step = 0.7, 0.5
+    z1 = oracle.solve_stereo(L, R, t, c, 4.0, 0.3, 1, 0.0, 1, gamma=gamma, step=step)
+    gnum = (t.astype(np.float64) - z1) / (step * gamma)
+
+    def energy(r, x, z):
+        u = x - z
+        out = 0.0
+        for k in range(C):
+            v = np.interp(u, np.arange(W), R[r, :, k].astype(np.float64))
+            out += 0.5 * (float(L[r, x, k]) - v) ** 2
+        return out
+
+    h = 1e-6
+    for r in range(H):
+        for x in range(3, W):
+            z = float(t[r, x])
+            fd = (energy(r, x, z + h) - energy(r, x, z - h)) / (2 * h)
+            assert abs(fd - gnum[r, x]) <= 1e-6, (r, x, fd, gnum[r, x])
+
+
+def test_stereo_charbonnier_stationarity():
+    """gamma = 0, many iterations: the iterate approaches the point where
+    lambda (z - K z) + chat rho'(z - t) = 0 (Eq. 4 with the Charbonnier target); K is the dense
+    operator of tests/dense.py and rho' the closed form."""
+    g, t, c = random_problem(6, 5, 3, 1, seed=6)
+    ss, sr, N, lam, eps = 3.0, 0.3, 2, 0.99, 0.5
+    z = oracle.solve_stereo(g, g, t, c, ss, sr, N, lam, 3000, gamma=0.0, eps=eps)
+    dx, dy = oracle.distances(g, ss, sr)
+    K = dense.dtf_operator(dx, dy, oracle.sigmas(ss, N))
+    S = oracle.support(dx, dy, ss)
+    zv = z.ravel()
+    r = zv - t.astype(np.float64).ravel()
+    res = lam * (zv - K @ zv) + (c.astype(np.float64).ravel() / S.ravel()) * r / np.sqrt(r * r + eps * eps)
+    assert np.max(np.abs(res)) <= 1e-6
