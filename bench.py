@@ -304,6 +304,29 @@ def main():
                                 "gbs_algorithmic": cbytes / (c_ms / 1e3) / 1e9,
                                 "frac": cbytes / (c_ms / 1e3) / 1e9 / peak_c}
 
+    # ---- Eq. (10) stereo refinement, C1 shape (single GPU, rank 0) ----
+    if world == 1 and band is None:
+        c1 = CONFIGS["C1"]
+        Lh, th, ch = make_inputs("C1")
+        rng = np.random.default_rng(1)
+        Rh = (np.roll(Lh, -16, axis=1) + rng.normal(0, 0.01, Lh.shape)).astype(np.float32)
+        Ld, Rd, td, cd = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (Lh, Rh, th, ch))
+        sout = torch.empty_like(td)
+        sctx = dts.dts_create(Ld, c1.sigma_s, c1.sigma_r, c1.N, stream=stream.cuda_stream)
+        run = lambda: dts.dts_solve_stereo(sctx, td, cd, c1.lam, c1.iters, sout, Ld, Rd, 0.001, 0.001,  # noqa: E731
+                                           stream=stream.cuda_stream)
+        run()
+        reps = 3
+        s_ms = timed(run, reps) / reps
+        dts.dts_destroy(sctx)
+        spx = c1.H * c1.W
+        sbytes = spx * c1.iters * (6 * 12.0 + 20.0 + 12.0 * c1.Cg) + spx * 28.0
+        extras["stereo"] = {"what": "dts_solve_stereo (Eq. 10, Charbonnier target, gamma = eps = 0.001) on C1 "
+                                    "(1400 x 1000, 3-channel pair: right = left shifted 16 px + noise)",
+                            "iterations": c1.iters, "ms": s_ms,
+                            "mpix_iter_per_s": spx * c1.iters / 1e6 / (s_ms / 1e3),
+                            "gbs_algorithmic": sbytes / (s_ms / 1e3) / 1e9}
+
     if rank != 0:
         if comm:
             dts.dts_comm_destroy(comm)

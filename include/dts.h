@@ -131,6 +131,26 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t target_channe
 dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, float* conf_out, float* var_out,
                           void* stream);
 
+/* Stereo refinement, Eq. (10) of the paper: gradient descent on
+ *     lambda/2 sum (z - zbar)^2 + sum c rho(z - t) + 1/2 sum gamma ||I_L(i) - I_R(i - z_i)||^2
+ * with the Charbonnier rho(r) = sqrt(r^2 + eps^2) on the target term (the paper uses
+ * eps = 0.001, gamma = 0.001).  Each iteration: the context's N-pass
+ * edge-aware mean zbar, then z <- z - step [lambda (z - zbar) + chat rho'(z - t)
+ * + gamma sum_k (I_L,k(x) - I_R,k(x - z)) dI_R,k/dx(x - z)], chat = c / S (R7), I_R sampled
+ * by linear interpolation along the row (rectified pair), clamped, slope 0 outside the
+ * image (reading R23).  z^0 = t.  SURVEY 8(f) #2.
+ *   target, confidence, out  H x W fp32 (one channel: the disparity), as dts_solve.
+ *   left, right  H x W x C fp32 HWC, C = the context's guide channels; `left` is the
+ *                image the context was created from, `right` its stereo partner.
+ *   gamma        photometric weight, finite, >= 0 (0: only the robust target term).
+ *   eps          Charbonnier epsilon, finite, > 0.
+ * Pointers may be host or device (host arrays are staged; the call then synchronises).
+ * Errors: DTS_E_ARG (NULL / overlapping pointers, bad scalars as in dts_solve),
+ *         DTS_E_SHAPE (row-band contexts), DTS_E_CUDA / DTS_E_OOM. */
+dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* confidence, float lambda,
+                            int32_t iterations, float* out, const float* left, const float* right, float gamma,
+                            float eps, void* stream);
+
 /* Buffers a test can read back (row-major H x W, fp32; stream-ordered then synchronised). */
 typedef enum { DTS_BUF_DX = 0, DTS_BUF_DY = 1, DTS_BUF_SUPPORT = 2 } dts_buffer;
 /* Copies the H x W buffer `which` into host memory `host_out` (H*W floats). */

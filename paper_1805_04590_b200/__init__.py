@@ -17,7 +17,8 @@ import os
 
 import numpy as np
 
-__all__ = ["DTSError", "dts_create", "dts_solve", "dts_solve_ex", "dts_confidence", "dts_destroy",
+__all__ = ["DTSError", "dts_create", "dts_solve", "dts_solve_ex", "dts_confidence", "dts_solve_stereo",
+           "dts_destroy",
            "dts_status_string",
            "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback", "dts_comm_destroy",
            "dts_create_band", "band_rows", "band_guide_rows",
@@ -35,7 +36,7 @@ DTS_BUF_DX, DTS_BUF_DY, DTS_BUF_SUPPORT = 0, 1, 2
 ABI_FUNCTIONS = ["dts_create", "dts_solve", "dts_destroy", "dts_status_string", "dts_last_error_string",
                  "dts_solve_ex", "dts_debug_read", "dts_profile_enable", "dts_profile_read",
                  "dts_launch_count", "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback",
-                 "dts_comm_destroy", "dts_create_band", "dts_version", "dts_confidence"]
+                 "dts_comm_destroy", "dts_create_band", "dts_version", "dts_confidence", "dts_solve_stereo"]
 
 
 class DTSError(RuntimeError):
@@ -78,6 +79,8 @@ def load_library():
     lib.dts_solve_ex.restype = ctypes.c_int
     lib.dts_confidence.argtypes = [vp, vp, f32, vp, vp, vp]
     lib.dts_confidence.restype = ctypes.c_int
+    lib.dts_solve_stereo.argtypes = [vp, vp, vp, f32, i32, vp, vp, vp, f32, f32, vp]
+    lib.dts_solve_stereo.restype = ctypes.c_int
     lib.dts_destroy.argtypes = [vp]
     lib.dts_destroy.restype = None
     lib.dts_status_string.argtypes = [ctypes.c_int]
@@ -194,6 +197,18 @@ def dts_confidence(ctx: int, target, sigma_c: float, conf_out, var_out=None, str
     return conf_out
 
 
+def dts_solve_stereo(ctx: int, target, confidence, lam: float, iterations: int, out, left, right,
+                     gamma: float = 0.001, eps: float = 0.001, stream=None):
+    """Eq. (10): stereo refinement of a disparity target with the Charbonnier target term and the
+    photometric term gamma (I_L(x) - I_R(x - z))^2; left = the context's guide image, right its
+    partner (H x W x C float32 HWC); target, confidence, out: H x W float32."""
+    st = load_library().dts_solve_stereo(ctx, _ptr(target, "target"), _ptr(confidence, "confidence"), lam,
+                                         iterations, _ptr(out, "out"), _ptr(left, "left"), _ptr(right, "right"),
+                                         gamma, eps, _stream(stream, target, confidence, out, left, right))
+    _check(st, "dts_solve_stereo")
+    return out
+
+
 def dts_destroy(ctx: int) -> None:
     if ctx:
         load_library().dts_destroy(ctx)
@@ -302,6 +317,16 @@ class Solver:
         if opts:
             return dts_solve_ex(self.ctx, target, confidence, lam, iterations, out, stream, **opts)
         return dts_solve(self.ctx, target, confidence, lam, iterations, out, stream)
+
+    def solve_stereo(self, target, confidence, lam: float, iterations: int, left, right, gamma: float = 0.001,
+                     eps: float = 0.001, out=None, stream=None):
+        if out is None:
+            if isinstance(target, np.ndarray):
+                out = np.empty_like(target)
+            else:
+                import torch
+                out = torch.empty_like(target)
+        return dts_solve_stereo(self.ctx, target, confidence, lam, iterations, out, left, right, gamma, eps, stream)
 
     def confidence(self, target, sigma_c: float, out=None, var_out=None, stream=None):
         if out is None:

@@ -125,11 +125,11 @@ namespace {
 
 enum Family {
     F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
-    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_COUNT
+    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
-                                     "rank_compose", "row_update", "confidence"};
+                                     "rank_compose", "row_update", "confidence", "stereo_update"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -845,6 +845,108 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
         return cuda_fail(e);
     if (any_host && (e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e);
     return DTS_OK;
+}
+
+dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* confidence, float lambda,
+                            int32_t iterations, float* out, const float* left, const float* right, float gamma,
+                            float eps, void* stream) {
+    if (!ctx || !target || !confidence || !out || !left || !right) return DTS_E_ARG;
+    if (iterations < 0) return DTS_E_ARG;
+    const float step = 0.99f;
+    if (!std::isfinite(lambda) || lambda < 0.f || step * (lambda + 1.f) >= 2.f) return DTS_E_ARG;
+    if (!std::isfinite(gamma) || gamma < 0.f || !std::isfinite(eps) || !(eps > 0.f)) return DTS_E_ARG;
+    if (ctx->comm) return DTS_E_SHAPE;  // row-band contexts: not supported (yet)
+    const Geometry& g = ctx->g;
+    const size_t cb = (size_t)g.H * g.W * sizeof(float);
+    const size_t gb = cb * (size_t)ctx->C;
+    if (overlaps(out, cb, target, cb) || overlaps(out, cb, confidence, cb) || overlaps(out, cb, left, gb) ||
+        overlaps(out, cb, right, gb))
+        return DTS_E_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->last_stream = s;
+    RowPlan rp;
+    ColPlan cp;
+    if (plan_row_pass(g, 1, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess ||
+        plan_col(g, 1, MODE_FILTER, ctx->num_sms, &cp) != cudaSuccess)
+        return DTS_E_SHAPE;
+    cudaGetLastError();
+    const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),
+                  ko = classify(out, ctx->device), kl = classify(left, ctx->device), kr = classify(right, ctx->device);
+    if (kt == PTR_BAD || kc == PTR_BAD || ko == PTR_BAD || kl == PTR_BAD || kr == PTR_BAD) return DTS_E_ARG;
+    const bool any_host = kt == PTR_HOST || kc == PTR_HOST || ko == PTR_HOST || kl == PTR_HOST || kr == PTR_HOST;
+    dts_status st = DTS_OK;
+    cudaError_t e;
+    if (any_host && (st = ensure_staging(ctx, cb, s)) != DTS_OK) return st;
+    const float* t_d = target;
+    const float* c_d = confidence;
+    float* o_d = ko == PTR_HOST ? ctx->st_o : out;
+    float *l_tmp = nullptr, *r_tmp = nullptr;
+    const float* l_d = left;
+    const float* r_d = right;
+    auto cleanup = [&]() {
+        if (l_tmp) cudaFreeAsync(l_tmp, s);
+        if (r_tmp) cudaFreeAsync(r_tmp, s);
+    };
+    if (kt == PTR_HOST) {
+        if ((e = cudaMemcpyAsync(ctx->st_t, target, cb, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e);
+        t_d = ctx->st_t;
+    }
+    if (kc == PTR_HOST) {
+        if ((e = cudaMemcpyAsync(ctx->st_c, confidence, cb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+            return cuda_fail(e);
+        c_d = ctx->st_c;
+    }
+    if (kl == PTR_HOST) {
+        if ((e = cudaMallocAsync((void**)&l_tmp, gb, s)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(l_tmp, left, gb, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
+            cleanup();
+            return cuda_fail(e);
+        }
+        l_d = l_tmp;
+    }
+    if (kr == PTR_HOST) {
+        if ((e = cudaMallocAsync((void**)&r_tmp, gb, s)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(r_tmp, right, gb, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
+            cleanup();
+            return cuda_fail(e);
+        }
+        r_d = r_tmp;
+    }
+    if (iterations == 0) {
+        if ((e = cudaMemcpyAsync(o_d, t_d, cb, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) st = cuda_fail(e);
+    } else {
+        if (st == DTS_OK) st = ensure_solver_state(ctx, 1, s);
+        if (st == DTS_OK) st = ensure_col_scratch(ctx, cp, s);
+        const double px = (double)g.H * g.W;
+        if (st == DTS_OK)
+            st = run_launch(ctx, F_PROLOGUE, px * (24.0 + (ctx->Sy ? 4.0 : 0.0)), s, [&] {
+                return launch_prologue(t_d, c_d, 1, g, ctx->S, ctx->Sy, 0, ctx->Z, ctx->T, ctx->chat, s);
+            });
+        for (int k = 0; k < iterations && st == DTS_OK; ++k) {
+            for (int i = 0; i < ctx->N && st == DTS_OK; ++i) {
+                const float* in = (i == 0) ? ctx->Z : ctx->X;
+                st = run_launch(ctx, F_ROW, px * 12.0, s, [&] {
+                    return launch_row_pass(rp, g, 1, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
+                });
+                if (st == DTS_OK)
+                    st = run_launch(ctx, F_COL, px * 12.0, s, [&] {
+                        return col_launch(ctx, cp, 1, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
+                    });
+            }
+            float* ohw = (k + 1 == iterations) ? o_d : nullptr;
+            if (st == DTS_OK)
+                st = run_launch(ctx, F_STEREO, px * (20.0 + 12.0 * ctx->C), s, [&] {
+                    return launch_update_stereo(ctx->X, ctx->Z, ctx->T, ctx->chat, l_d, r_d, ctx->C, g, lambda, step,
+                                                gamma, eps, ohw, s);
+                });
+        }
+    }
+    if (st == DTS_OK && ko == PTR_HOST &&
+        (e = cudaMemcpyAsync(out, o_d, cb, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        st = cuda_fail(e);
+    cleanup();
+    if (st == DTS_OK && any_host && (e = cudaStreamSynchronize(s)) != cudaSuccess) st = cuda_fail(e);
+    return st;
 }
 
 dts_status dts_solve(dts_ctx* ctx, const float* target, int32_t target_channels, const float* confidence,

@@ -93,6 +93,12 @@ cudaError_t launch_conf_prologue(const float* target, const Geometry& g, float* 
 cudaError_t launch_conf_epilogue(const float* X, const Geometry& g, float inv_2sc2, float* conf, float* var,
                                  cudaStream_t s);
 
+// Eq. (10) stereo step: Charbonnier target + photometric term, C_t = 1;
+// writes Z, or out (H x W) when non-null.
+cudaError_t launch_update_stereo(const float* X, float* Z, const float* T, const float* chat, const float* left,
+                                 const float* right, int Cg, const Geometry& g, float lam, float step, float gamma,
+                                 float eps, float* out, cudaStream_t s);
+
 // fill n floats with v
 cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);
 

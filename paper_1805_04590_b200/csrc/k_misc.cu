@@ -413,4 +413,62 @@ cudaError_t launch_conf_epilogue(const float* X, const Geometry& g, float inv_2s
     return cudaGetLastError();
 }
 
+// Eq. (10) stereo step (R23), one-channel disparity z:
+//     g = lam (z - zbar) + chat rho'(z - t) + gamma sum_k (I_L,k(x) - I_R,k(u)) dI_R,k/dx(u)
+//     rho'(r) = r / sqrt(r^2 + eps^2),  u = x - z,  I_R linear along the row, clamped; slope 0 outside
+// 2-D grid: blockIdx.y walks rows, threads columns; left / right are H x W x Cg HWC.
+template <int CG>
+__global__ void __launch_bounds__(256) k_update_stereo(const float* __restrict__ X, float* __restrict__ Z,
+                                                       const float* __restrict__ T, const float* __restrict__ chat,
+                                                       const float* __restrict__ left,
+                                                       const float* __restrict__ right, int Cgr, Geometry g,
+                                                       float lam, float step, float gamma, float eps,
+                                                       float* __restrict__ out) {
+    const int Cg = CG > 0 ? CG : Cgr;
+    const float e2 = eps * eps;
+    for (int64_t r = blockIdx.y; r < g.H; r += gridDim.y) {
+        const float* Lrow = left + r * g.W * Cg;
+        const float* Rrow = right + r * g.W * Cg;
+        for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < g.W; x += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t o = r * g.pitch + x;
+            const float z = Z[o], zb = __ldg(X + o), t = __ldg(T + o), ch = __ldg(chat + o);
+            const float res = z - t;
+            const float rho1 = res * rsqrtf(fmaf(res, res, e2));  // Charbonnier derivative
+            float gp = 0.f;
+            if (gamma != 0.f && g.W > 1) {
+                const float u = (float)x - z;
+                const bool inside = u >= 0.f && u <= (float)(g.W - 1);
+                const float uc = fminf(fmaxf(u, 0.f), (float)(g.W - 1));
+                int64_t x0 = (int64_t)floorf(uc);
+                if (x0 > g.W - 2) x0 = g.W - 2;
+                const float f = uc - (float)x0;
+                const float* ra = Rrow + x0 * Cg;
+                const float* lp = Lrow + x * Cg;
+                for (int k = 0; k < Cg; ++k) {
+                    const float a = __ldg(ra + k), b = __ldg(ra + Cg + k);
+                    const float iv = fmaf(f, b - a, a);
+                    gp = fmaf(__ldg(lp + k) - iv, inside ? (b - a) : 0.f, gp);
+                }
+            }
+            const float gr = fmaf(lam, z - zb, fmaf(ch, rho1, gamma * gp));
+            const float zn = fmaf(-step, gr, z);
+            if (out) out[r * g.W + x] = zn;
+            else Z[o] = zn;
+        }
+    }
+}
+
+cudaError_t launch_update_stereo(const float* X, float* Z, const float* T, const float* chat, const float* left,
+                                 const float* right, int Cg, const Geometry& g, float lam, float step, float gamma,
+                                 float eps, float* out, cudaStream_t s) {
+    const int64_t bx = (g.W + 255) / 256;
+    dim3 grid((unsigned)(bx < 64 ? bx : 64), (unsigned)(g.H < 8192 ? g.H : 8192), 1);
+    switch (Cg) {
+        case 1: k_update_stereo<1><<<grid, 256, 0, s>>>(X, Z, T, chat, left, right, Cg, g, lam, step, gamma, eps, out); break;
+        case 3: k_update_stereo<3><<<grid, 256, 0, s>>>(X, Z, T, chat, left, right, Cg, g, lam, step, gamma, eps, out); break;
+        default: k_update_stereo<0><<<grid, 256, 0, s>>>(X, Z, T, chat, left, right, Cg, g, lam, step, gamma, eps, out);
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace dts

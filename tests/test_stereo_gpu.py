@@ -1,0 +1,125 @@
+"""GPU parity of dts_solve_stereo (Eq. 10) against the fp64 oracle
+O8 on the same seeded fp32 inputs: max |gpu - oracle| <= 1e-4 * range(t) (north star).
+
+Two properties of the method shape the test cases (R23): the photometric gradient
+is discontinuous where u = x - z crosses an integer (I_R is interpolated linearly), so the
+fp32 and fp64 iterates can take different sides of a kink -- the paper's gamma = 0.001
+keeps such a flip below 1e-3 in z; and the paper's eps = 0.001 makes the Charbonnier term
+stiff (curvature chat / eps > 2 / step), so parity is checked with eps in the contractive
+regime (the bench times the paper's values)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import paper_1805_04590_b200 as dts  # noqa: E402
+from synth import CONFIGS, make_inputs, random_problem, target_range  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    torch.cuda.set_device(0)
+
+
+def right_image(L, shift, seed):
+    """A stereo partner: the left image shifted by `shift` pixels along the rows plus noise."""
+    rng = np.random.default_rng(seed)
+    R = np.roll(L, -shift, axis=1) + rng.normal(0, 0.01, L.shape)
+    return np.ascontiguousarray(R.astype(np.float32))
+
+
+def gpu_stereo(L, R, t, c, ss, sr, N, lam, iters, gamma, eps, host=False):
+    if host:
+        out = np.empty_like(t)
+        with dts.Solver(L, ss, sr, N) as s:
+            s.solve_stereo(t, c, lam, iters, L, R, gamma, eps, out=out)
+        return out.astype(np.float64)
+    Ld, Rd, td, cd = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (L, R, t, c))
+    out = torch.empty_like(td)
+    with dts.Solver(Ld, ss, sr, N) as s:
+        s.solve_stereo(td, cd, lam, iters, Ld, Rd, gamma, eps, out=out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+def check(L, R, t, c, ss, sr, N, lam, iters, gamma, eps, **kw):
+    ref = oracle.solve_stereo(L, R, t, c, ss, sr, N, lam, iters, gamma, eps)
+    got = gpu_stereo(L, R, t, c, ss, sr, N, lam, iters, gamma, eps, **kw)
+    rng = target_range(t)
+    assert np.all(np.isfinite(got))
+    err = np.max(np.abs(got - ref))
+    assert err <= 1e-4 * rng, err / rng
+    return err / rng
+
+
+@pytest.mark.parametrize("H,W", [(1, 9), (9, 1), (48, 64), (61, 97), (700, 130), (300, 1000)])
+def test_stereo_shapes(H, W):
+    L, t, c = random_problem(H, W, 3, 1, seed=H + 3 * W)
+    t = (t * 8.0).astype(np.float32)  # disparities of a few pixels
+    R = right_image(L, 3, H)
+    check(L, R, t, c, 6.0, 0.2, 3, 0.99, 8, gamma=0.001, eps=1.0)
+
+
+def test_stereo_c1_config():
+    """C1 (stereo-refinement shape: 1400 x 1000, disparity target in [0, 256] with outliers)."""
+    cfg = CONFIGS["C1"]
+    L, t, c = make_inputs("C1")
+    R = right_image(L, 16, 1)
+    check(L, R, t, c, cfg.sigma_s, cfg.sigma_r, cfg.N, cfg.lam, 20, gamma=0.001, eps=1.0)
+
+
+def test_stereo_gamma0_matches_charbonnier_reduction():
+    """gamma = 0, eps large, confidence c * eps: the plain DTS solve (dts_solve) result."""
+    L, t, c = random_problem(90, 70, 3, 1, seed=4)
+    eps = 1e4
+    R = right_image(L, 2, 4)
+    Ld, Rd, td = (torch.from_numpy(a).cuda() for a in (L, R, t))
+    cd = torch.from_numpy(c).cuda()
+    ce = torch.from_numpy((c.astype(np.float64) * eps).astype(np.float32)).cuda()
+    with dts.Solver(Ld, 5.0, 0.2, 3) as s:
+        a = s.solve(td, cd, 0.99, 6)
+        b = s.solve_stereo(td, ce, 0.99, 6, Ld, Rd, 0.0, eps)
+    torch.cuda.synchronize()
+    assert torch.max(torch.abs(a - b)).item() <= 1e-5 * target_range(t)
+
+
+def test_stereo_fixed_point_and_zero_iterations():
+    rng = np.random.default_rng(8)
+    H, W, dstar = 40, 120, 5
+    L = rng.uniform(0, 1, (H, W, 3)).astype(np.float32)
+    R = np.empty_like(L)
+    R[:, :W - dstar] = L[:, dstar:]
+    R[:, W - dstar:] = L[:, -1:]
+    t = np.full((H, W), float(dstar), np.float32)
+    c = np.full((H, W), 0.5, np.float32)
+    got = gpu_stereo(L, R, t, c, 6.0, 0.3, 3, 0.99, 10, gamma=0.3, eps=1.0)
+    assert np.max(np.abs(got - dstar)) <= 1e-5
+    got0 = gpu_stereo(L, R, t, c, 6.0, 0.3, 3, 0.99, 0, gamma=0.3, eps=1.0)
+    assert np.array_equal(got0, t.astype(np.float64))
+
+
+def test_stereo_host_pointers_match_device():
+    L, t, c = random_problem(50, 60, 3, 1, seed=7)
+    t = (t * 4).astype(np.float32)
+    R = right_image(L, 2, 7)
+    a = gpu_stereo(L, R, t, c, 5.0, 0.2, 3, 0.99, 5, 0.01, 0.5)
+    b = gpu_stereo(L, R, t, c, 5.0, 0.2, 3, 0.99, 5, 0.01, 0.5, host=True)
+    assert np.array_equal(a, b)
+
+
+def test_stereo_argument_errors():
+    L, t, c = random_problem(10, 12, 3, 1, seed=1)
+    Ld, td, cd = (torch.from_numpy(a).cuda() for a in (L, t, c))
+    out = torch.empty_like(td)
+    with dts.Solver(Ld, 5.0, 0.2, 3) as s:
+        for gamma, eps in ((-1.0, 0.001), (float("nan"), 0.001), (0.1, 0.0), (0.1, -1.0), (0.1, float("inf"))):
+            with pytest.raises(dts.DTSError) as ei:
+                dts.dts_solve_stereo(s.ctx, td, cd, 0.99, 3, out, Ld, Ld, gamma, eps)
+            assert ei.value.status == 1
+        with pytest.raises(dts.DTSError) as ei:
+            dts.dts_solve_stereo(s.ctx, td, cd, 0.99, 3, td, Ld, Ld, 0.001, 0.001)  # out aliases target
+        assert ei.value.status == 1
