@@ -15,8 +15,9 @@ Functions (each cites the passage its C routine follows; see dts_oracle.c):
   solve(guide, target, conf, ...)               O6  Eq. (3) gradient descent
   confidence(guide, target, ..., sigma_c)       O7  Eq. (7) edge-aware variance confidence
   solve_stereo(left, right, target, conf, ...)  O8  Eq. (10) stereo refinement, Charbonnier target
+  sr_prepare(low, factor)                       O9  depth-SR front end: bicubic target, bump confidence
 
-Parity status: O1, O3, O4, O5, O6, O7 and O8 are pinned by tests/test_oracle_pins.py
+Parity status: O1, O3, O4, O5, O6, O7, O8 and O9 are pinned by tests/test_oracle_pins.py
 (worked examples, dense triangular matrices, closed forms, brute force,
 reductions); the whole solve is NOT pinned against the paper's own outputs,
 which it never prints ("parity unpinned vs the paper").
@@ -74,6 +75,8 @@ def _load():
     lib.dts_oracle_solve_stereo.argtypes = [_c_float_p, _c_float_p, i64, i64, i32, dbl, dbl, i32, _c_float_p,
                                             _c_float_p, dbl, dbl, i32, dbl, dbl, i32, _c_double_p]
     lib.dts_oracle_solve_stereo.restype = ctypes.c_int
+    lib.dts_oracle_sr_prepare.argtypes = [_c_float_p, i64, i64, i32, _c_double_p, _c_double_p]
+    lib.dts_oracle_sr_prepare.restype = ctypes.c_int
     lib.dts_oracle_num_threads.argtypes = []
     lib.dts_oracle_num_threads.restype = ctypes.c_int
     lib.dts_oracle_set_threads.argtypes = [ctypes.c_int]
@@ -229,3 +232,16 @@ def solve_stereo(left, right, target, confidence, sigma_s: float, sigma_r: float
     if st:
         raise ValueError(f"dts_oracle_solve_stereo failed ({st})")
     return out
+
+
+def sr_prepare(low, factor: int):
+    """O9: (target, confidence), each (h f) x (w f) float64, from an h x w low-res depth map."""
+    lo = _f32(low)
+    h, w = lo.shape
+    H, W = h * factor, w * factor
+    t = np.empty((H, W), np.float64)
+    c = np.empty((H, W), np.float64)
+    st = _load().dts_oracle_sr_prepare(_p(lo, _c_float_p), h, w, int(factor), _p(t, _c_double_p), _p(c, _c_double_p))
+    if st:
+        raise ValueError(f"dts_oracle_sr_prepare failed ({st})")
+    return t, c

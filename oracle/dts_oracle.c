@@ -456,3 +456,56 @@ done:
     free(Ax); free(Ay);
     return st;
 }
+
+/* ------------------------------------------------------------------------ */
+/* O9: depth super-resolution front end (reading R24):
+ *   target = bicubic upsampling of the low-resolution depth by an integer factor f
+ *            ("simple bicubic interpolation"): Catmull-Rom kernel (a = -0.5),
+ *            separable, clamped borders, low-res sample k at high-res coordinate
+ *            k f + (f - 1) / 2, i.e. high-res pixel X reads low-res position
+ *            u = (X + 0.5) / f - 0.5;
+ *   confidence = Gaussian bump around the low-res sample centres (Barron & Poole):
+ *            c = exp(-dist^2 / (2 sigma_b^2)), dist = Euclidean distance (high-res pixels)
+ *            to the nearest sample centre, sigma_b = f / 4.
+ * low: h x w fp32; target, conf: (h f) x (w f) doubles.                               */
+static double catmull_rom(double t) {  /* Keys cubic, a = -0.5 */
+    t = fabs(t);
+    if (t < 1.0) return 1.5 * t * t * t - 2.5 * t * t + 1.0;
+    if (t < 2.0) return -0.5 * t * t * t + 2.5 * t * t - 4.0 * t + 2.0;
+    return 0.0;
+}
+
+int dts_oracle_sr_prepare(const float* low, int64_t h, int64_t w, int32_t f, double* target, double* conf) {
+    if (!low || !target || !conf || h < 1 || w < 1 || f < 1) return ORACLE_E_ARG;
+    const int64_t H = h * f, W = w * f;
+    const double sb = (double)f / 4.0;
+    for (int64_t Y = 0; Y < H; ++Y) {
+        const double v = ((double)Y + 0.5) / f - 0.5;
+        const int64_t j0 = (int64_t)floor(v);
+        for (int64_t X = 0; X < W; ++X) {
+            const double u = ((double)X + 0.5) / f - 0.5;
+            const int64_t i0 = (int64_t)floor(u);
+            double acc = 0.0;
+            for (int64_t dj = -1; dj <= 2; ++dj) {
+                int64_t j = j0 + dj;
+                const double wy = catmull_rom(v - (double)j);
+                j = j < 0 ? 0 : (j > h - 1 ? h - 1 : j);
+                for (int64_t di = -1; di <= 2; ++di) {
+                    int64_t i = i0 + di;
+                    const double wx = catmull_rom(u - (double)i);
+                    i = i < 0 ? 0 : (i > w - 1 ? w - 1 : i);
+                    acc += wy * wx * (double)low[j * w + i];
+                }
+            }
+            target[Y * W + X] = acc;
+            /* nearest sample centre: k f + (f - 1)/2 with k = clamp(round(u)) */
+            int64_t ku = (int64_t)floor(u + 0.5), kv = (int64_t)floor(v + 0.5);
+            ku = ku < 0 ? 0 : (ku > w - 1 ? w - 1 : ku);
+            kv = kv < 0 ? 0 : (kv > h - 1 ? h - 1 : kv);
+            const double ddx = (double)X - ((double)ku * f + (f - 1) / 2.0);
+            const double ddy = (double)Y - ((double)kv * f + (f - 1) / 2.0);
+            conf[Y * W + X] = exp(-(ddx * ddx + ddy * ddy) / (2.0 * sb * sb));
+        }
+    }
+    return ORACLE_OK;
+}

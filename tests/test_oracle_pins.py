@@ -482,3 +482,63 @@ def test_stereo_charbonnier_stationarity():
     r = zv - t.astype(np.float64).ravel()
     res = lam * (zv - K @ zv) + (c.astype(np.float64).ravel() / S.ravel()) * r / np.sqrt(r * r + eps * eps)
     assert np.max(np.abs(res)) <= 1e-6
+
+
+# ---------------------------------------------------------------- O9: SR front end
+def test_sr_factor_one_identity_and_constant():
+    rng = np.random.default_rng(2)
+    low = rng.uniform(0.5, 10, (7, 9)).astype(np.float32)
+    t, c = oracle.sr_prepare(low, 1)
+    assert np.array_equal(t, low.astype(np.float64)) and np.all(c == 1.0)
+    t, _ = oracle.sr_prepare(np.full((5, 6), 3.5, np.float32), 4)
+    np.testing.assert_allclose(t, 3.5, rtol=0, atol=1e-14)
+
+
+def test_sr_reproduces_quadratics_in_the_interior():
+    """The Catmull-Rom (Keys a = -0.5) kernel reproduces polynomials of degree <= 2; with the
+    centre alignment, high-res pixel X samples the low-res polynomial at u = (X + 0.5)/f - 0.5."""
+    h, w, f = 12, 14, 3
+    jj, ii = np.mgrid[0:h, 0:w].astype(np.float64)
+    poly = lambda v, u: 0.3 * u * u - 0.7 * u * v + 0.2 * v * v + 1.5 * u - 2.0 * v + 4.0  # noqa: E731
+    low = poly(jj, ii).astype(np.float32)
+    t, _ = oracle.sr_prepare(low, f)
+    YY, XX = np.mgrid[0:h * f, 0:w * f].astype(np.float64)
+    U, V = (XX + 0.5) / f - 0.5, (YY + 0.5) / f - 0.5
+    ref = poly(V, U)
+    inner = (U >= 1) & (U <= w - 2) & (V >= 1) & (V <= h - 2)  # all 4 taps inside
+    np.testing.assert_allclose(t[inner], ref[inner], rtol=0, atol=2e-5)  # fp32 inputs
+
+
+def test_sr_brute_force_2d_and_interpolation():
+    """Against an independent 2-D sum over all low-res pixels with the closed-form kernel
+    (indices clamped); odd f puts sample centres on pixels, where the value is the sample."""
+    rng = np.random.default_rng(5)
+    h, w, f = 5, 6, 3
+    low = rng.uniform(0, 1, (h, w)).astype(np.float32)
+    t, c = oracle.sr_prepare(low, f)
+
+    def k(x):
+        x = abs(x)
+        return 1.5 * x ** 3 - 2.5 * x ** 2 + 1 if x < 1 else (-0.5 * x ** 3 + 2.5 * x ** 2 - 4 * x + 2 if x < 2 else 0.0)
+
+    for Y in range(h * f):
+        for X in range(w * f):
+            u, v = (X + 0.5) / f - 0.5, (Y + 0.5) / f - 0.5
+            acc = 0.0
+            for j in range(int(np.floor(v)) - 1, int(np.floor(v)) + 3):
+                for i in range(int(np.floor(u)) - 1, int(np.floor(u)) + 3):
+                    acc += k(v - j) * k(u - i) * float(low[min(max(j, 0), h - 1), min(max(i, 0), w - 1)])
+            assert abs(acc - t[Y, X]) <= 1e-12
+    for j in range(h):
+        for i in range(w):
+            Y, X = j * f + (f - 1) // 2, i * f + (f - 1) // 2
+            assert abs(t[Y, X] - float(low[j, i])) <= 1e-12 and c[Y, X] == 1.0
+
+
+def test_sr_bump_confidence_closed_form():
+    """f = 4: sigma_b = 1; centres at 4k + 1.5, so pixel (1, 1) is at distance sqrt(0.5) from the
+    first centre -> c = exp(-0.25); c is periodic with period f away from the borders."""
+    _, c = oracle.sr_prepare(np.zeros((6, 6), np.float32), 4)
+    assert abs(c[1, 1] - np.exp(-0.25)) <= 1e-15
+    np.testing.assert_allclose(c[4:20, 4:20], np.tile(c[4:8, 4:8], (4, 4)), rtol=0, atol=1e-15)
+    assert np.all((c > 0) & (c <= 1))
