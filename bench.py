@@ -327,6 +327,16 @@ def main():
                             "mpix_iter_per_s": spx * c1.iters / 1e6 / (s_ms / 1e3),
                             "gbs_algorithmic": sbytes / (s_ms / 1e3) / 1e9}
 
+    # ---- depth-SR front end, C2 shape (86 x 64 -> 1376 x 1024, f = 16) ----
+    if world == 1 and band is None:
+        low = torch.rand(64, 86, device=dev) * 9.5 + 0.5
+        st_o, sc_o = torch.empty(1024, 1376, device=dev), torch.empty(1024, 1376, device=dev)
+        runp = lambda: dts.dts_sr_prepare(low, 16, st_o, sc_o, stream=stream.cuda_stream)  # noqa: E731
+        runp()
+        p_ms = timed(runp, 10) / 10
+        extras["sr_prepare"] = {"what": "dts_sr_prepare: bicubic x16 target + bump confidence, 86x64 -> 1376x1024",
+                                "ms": p_ms, "mpix_per_s": 1376 * 1024 / 1e6 / (p_ms / 1e3)}
+
     if rank != 0:
         if comm:
             dts.dts_comm_destroy(comm)

@@ -151,6 +151,22 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
                             int32_t iterations, float* out, const float* left, const float* right, float gamma,
                             float eps, void* stream);
 
+/* Depth super-resolution front end: from an h x w low-resolution
+ * depth map, the target and confidence of an (h f) x (w f) DTS solve (use them with a context
+ * built on the high-resolution colour guide):
+ *   target = bicubic upsampling ("simple bicubic interpolation"): Catmull-Rom kernel
+ *            (a = -0.5), separable, clamped borders, centre-aligned (low-res sample k at
+ *            high-res coordinate k f + (f - 1)/2);
+ *   conf   = Gaussian bump around the nearest low-res sample centre:
+ *            exp(-dist^2 / (2 sigma_b^2)), sigma_b = f / 4 (reading R24).
+ *   low            h x w fp32 (device or host); target_out, conf_out (h f) x (w f) fp32.
+ *   factor         integer >= 1 (f = 1 copies `low` and sets conf = 1).
+ * Context-free; stream-ordered (host pointers are staged and the call synchronises).
+ * Errors: DTS_E_ARG (NULL pointers, h, w or factor < 1, outputs overlapping `low` or each
+ *         other), DTS_E_CUDA / DTS_E_OOM. */
+dts_status dts_sr_prepare(const float* low, int64_t h, int64_t w, int32_t factor, float* target_out,
+                          float* conf_out, void* stream);
+
 /* Buffers a test can read back (row-major H x W, fp32; stream-ordered then synchronised). */
 typedef enum { DTS_BUF_DX = 0, DTS_BUF_DY = 1, DTS_BUF_SUPPORT = 2 } dts_buffer;
 /* Copies the H x W buffer `which` into host memory `host_out` (H*W floats). */

@@ -18,6 +18,7 @@ import os
 import numpy as np
 
 __all__ = ["DTSError", "dts_create", "dts_solve", "dts_solve_ex", "dts_confidence", "dts_solve_stereo",
+           "dts_sr_prepare",
            "dts_destroy",
            "dts_status_string",
            "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback", "dts_comm_destroy",
@@ -36,7 +37,8 @@ DTS_BUF_DX, DTS_BUF_DY, DTS_BUF_SUPPORT = 0, 1, 2
 ABI_FUNCTIONS = ["dts_create", "dts_solve", "dts_destroy", "dts_status_string", "dts_last_error_string",
                  "dts_solve_ex", "dts_debug_read", "dts_profile_enable", "dts_profile_read",
                  "dts_launch_count", "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback",
-                 "dts_comm_destroy", "dts_create_band", "dts_version", "dts_confidence", "dts_solve_stereo"]
+                 "dts_comm_destroy", "dts_create_band", "dts_version", "dts_confidence", "dts_solve_stereo",
+                 "dts_sr_prepare"]
 
 
 class DTSError(RuntimeError):
@@ -81,6 +83,8 @@ def load_library():
     lib.dts_confidence.restype = ctypes.c_int
     lib.dts_solve_stereo.argtypes = [vp, vp, vp, f32, i32, vp, vp, vp, f32, f32, vp]
     lib.dts_solve_stereo.restype = ctypes.c_int
+    lib.dts_sr_prepare.argtypes = [vp, i64, i64, i32, vp, vp, vp]
+    lib.dts_sr_prepare.restype = ctypes.c_int
     lib.dts_destroy.argtypes = [vp]
     lib.dts_destroy.restype = None
     lib.dts_status_string.argtypes = [ctypes.c_int]
@@ -207,6 +211,26 @@ def dts_solve_stereo(ctx: int, target, confidence, lam: float, iterations: int, 
                                          gamma, eps, _stream(stream, target, confidence, out, left, right))
     _check(st, "dts_solve_stereo")
     return out
+
+
+def dts_sr_prepare(low, factor: int, target_out=None, conf_out=None, stream=None):
+    """Depth-SR front end: bicubic x factor target and Gaussian-bump confidence from an
+    h x w low-res depth map.  Returns (target, conf), (h f) x (w f) float32 (numpy for numpy input,
+    torch on the input's device otherwise)."""
+    h, w = int(low.shape[0]), int(low.shape[1])
+    shape = (h * factor, w * factor)
+    if target_out is None or conf_out is None:
+        if isinstance(low, np.ndarray):
+            target_out = np.empty(shape, np.float32) if target_out is None else target_out
+            conf_out = np.empty(shape, np.float32) if conf_out is None else conf_out
+        else:
+            import torch
+            target_out = torch.empty(shape, dtype=torch.float32, device=low.device) if target_out is None else target_out
+            conf_out = torch.empty(shape, dtype=torch.float32, device=low.device) if conf_out is None else conf_out
+    st = load_library().dts_sr_prepare(_ptr(low, "low"), h, w, int(factor), _ptr(target_out, "target_out"),
+                                       _ptr(conf_out, "conf_out"), _stream(stream, low, target_out, conf_out))
+    _check(st, "dts_sr_prepare")
+    return target_out, conf_out
 
 
 def dts_destroy(ctx: int) -> None:

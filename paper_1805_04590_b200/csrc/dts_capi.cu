@@ -380,6 +380,51 @@ extern "C" {
 
 const char* dts_version(void) { return "dts-b200 0.1 (sm_100a)"; }
 
+dts_status dts_sr_prepare(const float* low, int64_t h, int64_t w, int32_t factor, float* target_out,
+                          float* conf_out, void* stream) {
+    if (!low || !target_out || !conf_out || h < 1 || w < 1 || factor < 1) return DTS_E_ARG;
+    const size_t lb = (size_t)h * (size_t)w * sizeof(float);
+    const size_t ob = lb * (size_t)factor * (size_t)factor;
+    if (overlaps(target_out, ob, low, lb) || overlaps(conf_out, ob, low, lb) || overlaps(target_out, ob, conf_out, ob))
+        return DTS_E_ARG;
+    int device = 0;
+    cudaError_t e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return cuda_fail(e);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const PtrKind kl = classify(low, device), kt = classify(target_out, device), kc = classify(conf_out, device);
+    if (kl == PTR_BAD || kt == PTR_BAD || kc == PTR_BAD) return DTS_E_ARG;
+    float *dl = nullptr, *dt = nullptr, *dc = nullptr;
+    const float* l_d = low;
+    float* t_d = target_out;
+    float* c_d = conf_out;
+    dts_status st = DTS_OK;
+    if (kl == PTR_HOST) {
+        if ((e = cudaMallocAsync((void**)&dl, lb, s)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(dl, low, lb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+            st = cuda_fail(e);
+        l_d = dl;
+    }
+    if (st == DTS_OK && kt == PTR_HOST) {
+        if ((e = cudaMallocAsync((void**)&dt, ob, s)) != cudaSuccess) st = cuda_fail(e);
+        t_d = dt;
+    }
+    if (st == DTS_OK && kc == PTR_HOST) {
+        if ((e = cudaMallocAsync((void**)&dc, ob, s)) != cudaSuccess) st = cuda_fail(e);
+        c_d = dc;
+    }
+    if (st == DTS_OK && (e = launch_sr_prepare(l_d, h, w, factor, t_d, c_d, s)) != cudaSuccess) st = cuda_fail(e);
+    if (st == DTS_OK && kt == PTR_HOST && (e = cudaMemcpyAsync(target_out, dt, ob, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        st = cuda_fail(e);
+    if (st == DTS_OK && kc == PTR_HOST && (e = cudaMemcpyAsync(conf_out, dc, ob, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        st = cuda_fail(e);
+    for (float* p : {dl, dt, dc})
+        if (p) cudaFreeAsync(p, s);
+    if (st == DTS_OK && (kl == PTR_HOST || kt == PTR_HOST || kc == PTR_HOST) &&
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+        st = cuda_fail(e);
+    return st;
+}
+
 const char* dts_status_string(dts_status s) {
     switch (s) {
         case DTS_OK: return "DTS_OK";

@@ -99,6 +99,10 @@ cudaError_t launch_update_stereo(const float* X, float* Z, const float* T, const
                                  const float* right, int Cg, const Geometry& g, float lam, float step, float gamma,
                                  float eps, float* out, cudaStream_t s);
 
+// Depth-SR front end: bicubic target and bump confidence, (h f) x (w f).
+cudaError_t launch_sr_prepare(const float* low, int64_t h, int64_t w, int f, float* target, float* conf,
+                              cudaStream_t s);
+
 // fill n floats with v
 cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);
 

@@ -471,4 +471,66 @@ cudaError_t launch_update_stereo(const float* X, float* Z, const float* T, const
     return cudaGetLastError();
 }
 
+// Depth-SR front end (reading R24): bicubic (Catmull-Rom, a = -0.5) upsampling of
+// the low-res depth by an integer factor f with clamped borders and centre alignment (high-res
+// X reads low-res u = (X + 0.5)/f - 0.5), and the Gaussian-bump confidence
+// exp(-dist^2 / (2 (f/4)^2)) around the nearest low-res sample centre.
+__device__ __forceinline__ float cr_weight(float t) {
+    t = fabsf(t);
+    if (t < 1.f) return fmaf(t * t, fmaf(1.5f, t, -2.5f), 1.f);
+    if (t < 2.f) return fmaf(t, fmaf(t, fmaf(-0.5f, t, 2.5f), -4.f), 2.f);
+    return 0.f;
+}
+
+__global__ void __launch_bounds__(256) k_sr_prepare(const float* __restrict__ low, int64_t h, int64_t w, int f,
+                                                    float* __restrict__ target, float* __restrict__ conf) {
+    const int64_t H = h * f, W = w * f;
+    const float inv = 1.f / (float)f, half = 0.5f * (float)(f - 1);
+    const float k2 = 8.f / ((float)f * (float)f);  // 1 / (2 sigma_b^2), sigma_b = f / 4
+    for (int64_t Y = blockIdx.y; Y < H; Y += gridDim.y) {
+        const float v = ((float)Y + 0.5f) * inv - 0.5f;
+        const int64_t j0 = (int64_t)floorf(v);
+        float wy[4];
+        int64_t jr[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const int64_t j = j0 - 1 + d;
+            wy[d] = cr_weight(v - (float)j);
+            jr[d] = (j < 0 ? 0 : (j > h - 1 ? h - 1 : j)) * w;
+        }
+        int64_t kv = (int64_t)floorf(v + 0.5f);
+        kv = kv < 0 ? 0 : (kv > h - 1 ? h - 1 : kv);
+        const float dy = (float)Y - ((float)kv * (float)f + half);
+        for (int64_t X = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; X < W; X += (int64_t)gridDim.x * blockDim.x) {
+            const float u = ((float)X + 0.5f) * inv - 0.5f;
+            const int64_t i0 = (int64_t)floorf(u);
+            float acc = 0.f;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                int64_t i = i0 - 1 + d;
+                const float wx = cr_weight(u - (float)i);
+                i = i < 0 ? 0 : (i > w - 1 ? w - 1 : i);
+                float col = 0.f;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) col = fmaf(wy[e], __ldg(low + jr[e] + i), col);
+                acc = fmaf(wx, col, acc);
+            }
+            int64_t ku = (int64_t)floorf(u + 0.5f);
+            ku = ku < 0 ? 0 : (ku > w - 1 ? w - 1 : ku);
+            const float dx = (float)X - ((float)ku * (float)f + half);
+            target[Y * W + X] = acc;
+            conf[Y * W + X] = __expf(-(dx * dx + dy * dy) * k2);
+        }
+    }
+}
+
+cudaError_t launch_sr_prepare(const float* low, int64_t h, int64_t w, int f, float* target, float* conf,
+                              cudaStream_t s) {
+    const int64_t H = h * f, W = w * f;
+    const int64_t bx = (W + 255) / 256;
+    dim3 grid((unsigned)(bx < 64 ? bx : 64), (unsigned)(H < 8192 ? H : 8192), 1);
+    k_sr_prepare<<<grid, 256, 0, s>>>(low, h, w, f, target, conf);
+    return cudaGetLastError();
+}
+
 }  // namespace dts
