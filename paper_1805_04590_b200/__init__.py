@@ -250,11 +250,11 @@ def dts_profile_enable(ctx: int, on: bool = True) -> None:
 
 def dts_profile_read(ctx: int):
     """{family: {"launches", "total_ms", "bytes_per_launch", "avg_ms"}}"""
-    arr = (KernelStat * 16)()
+    arr = (KernelStat * 32)()
     n = ctypes.c_int32(0)
-    _check(load_library().dts_profile_read(ctx, arr, 16, ctypes.byref(n)), "dts_profile_read")
+    _check(load_library().dts_profile_read(ctx, arr, 32, ctypes.byref(n)), "dts_profile_read")
     res = {}
-    for i in range(min(n.value, 16)):
+    for i in range(min(n.value, 32)):
         k = arr[i]
         res[k.name.decode()] = {"launches": int(k.launches), "total_ms": float(k.total_ms),
                                 "bytes_per_launch": float(k.bytes_per_launch),

@@ -125,11 +125,11 @@ namespace {
 
 enum Family {
     F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
-    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_COUNT
+    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_FILL, F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
-                                     "rank_compose", "row_update", "confidence", "stereo_update"};
+                                     "rank_compose", "row_update", "confidence", "stereo_update", "link_fill"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -551,8 +551,8 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
     });
     if (st == DTS_OK && !ctx->halo_below) {
         const float inf = std::numeric_limits<float>::infinity();
-        if ((e = launch_fill(ctx->dy + H * ctx->g.pitch, ctx->g.pitch, inf, s)) != cudaSuccess) st = cuda_fail(e);
-        ++ctx->launches;
+        st = run_launch(ctx, F_FILL, ctx->g.pitch * 4.0, s,
+                        [&] { return launch_fill(ctx->dy + H * ctx->g.pitch, ctx->g.pitch, inf, s); });
     }
     if (st == DTS_OK)
         st = run_launch(ctx, F_SUPPORT_ROW, px * 8.0, s, [&] {

@@ -1,13 +1,14 @@
 #!/bin/bash
 # Profiling recipe used for profiles/ (run under gpurun on one B200; see B200_PROFILING.md).
-# 1) plain run must exit 0; 2) launch list of one full timed step (144 launches);
-# 3) one `--set full` capture per kernel family (one launch each, after warm-up).
+# 1) the plain run must exit 0; 2) launch list of one full timed step (145 launches: guide
+# derivative, bottom-link fill, support row + column, prologue, 20 x [3 row, 3 column, update]);
+# 3) one `--set full` capture per kernel family (steady-state launches).
 set -u
 OUT=${OUT:-gpurun_out}
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
 $CMD > $OUT/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -s 144 -c 144 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
+    -s 145 -c 145 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
 for spec in "k_col_cluster 4" "k_row_pass 2" "k_update 1" "k_guide_deriv 1" "k_prologue 1"; do
   set -- $spec
   ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 \
