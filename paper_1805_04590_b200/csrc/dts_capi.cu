@@ -112,6 +112,12 @@ struct dts_ctx {
     unsigned int* flags = nullptr;
     size_t tuple_cap = 0, flag_cap = 0;
     unsigned int epoch = 0;
+    // CUDA graph of the last solve's launch sequence (cluster column path, device buffers)
+    cudaGraphExec_t graph_exec = nullptr;
+    std::vector<uintptr_t> graph_key;
+    std::vector<uintptr_t> graph_seen;  // key of the last eager solve: a repeat is captured
+    int64_t graph_launches = 0;
+    cudaStream_t cap_stream = nullptr;
     // streaming column kernel (kind 2) scratch: its own tuples/carries and counters/flags
     float* v_tuples = nullptr;
     unsigned int* v_flags = nullptr;
@@ -720,56 +726,86 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         if ((st = ensure_solver_state(ctx, Ct, s)) != DTS_OK) return st;
         if ((st = ensure_col_scratch(ctx, cpf, s)) != DTS_OK) return st;
         if ((st = ensure_col_scratch(ctx, cpu, s)) != DTS_OK) return st;
-        const double px = (double)g.H * g.W;
-        st = run_launch(ctx, F_PROLOGUE, px * (12.0 * Ct + 12 + (ctx->Sy ? 4.0 : 0.0)), s, [&] {
-            return launch_prologue(t_d, c_d, Ct, g, ctx->S, ctx->Sy, support_mode, ctx->Z, ctx->T, ctx->chat, s);
-        });
-        if (st != DTS_OK) return st;
-        const double row_bytes = px * (8.0 * Ct + 4);
-        const double upd_bytes = px * (16.0 * Ct + 8);  // X, d, Z, T, chat in; Z out
-        if (stream_ok) {
-            UpdateArgs u;
-            u.Z = ctx->Z;
-            u.T = ctx->T;
-            u.chat = ctx->chat;
-            u.lam = lambda;
-            u.step = step;
-            u.out_hwc = nullptr;
-            for (int k = 0; k < iterations; ++k) {
-                for (int i = 0; i < ctx->N; ++i) {
-                    if (i == 0 && k > 0) {  // Eq. (3) step of iteration k-1 fused into this row pass
-                        st = run_launch(ctx, F_ROWUPD, px * (20.0 * Ct + 8), s, [&] {
-                            return launch_row_update(rp, g, Ct, ctx->X, ctx->X, ctx->dx, ctx->kc[i], u, s);
-                        });
-                    } else {
-                        const float* in = (i == 0) ? ctx->Z : ctx->X;
-                        st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
-                            return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
-                        });
-                    }
-                    if (st != DTS_OK) return st;
-                    st = run_launch(ctx, F_COL, row_bytes, s, [&] {
-                        return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
-                    });
-                    if (st != DTS_OK) return st;
-                }
-            }
-            st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
-                return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, o_d, ctx->num_sms, s);
+        auto enqueue = [&](cudaStream_t s) -> dts_status {
+            dts_status st;
+            const double px = (double)g.H * g.W;
+            st = run_launch(ctx, F_PROLOGUE, px * (12.0 * Ct + 12 + (ctx->Sy ? 4.0 : 0.0)), s, [&] {
+                return launch_prologue(t_d, c_d, Ct, g, ctx->S, ctx->Sy, support_mode, ctx->Z, ctx->T, ctx->chat, s);
             });
             if (st != DTS_OK) return st;
-        }
-        for (int k = 0; k < (stream_ok ? 0 : iterations); ++k) {
-            for (int i = 0; i < ctx->N; ++i) {
-                const float* in = (i == 0) ? ctx->Z : ctx->X;
-                st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
-                    return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
+            const double row_bytes = px * (8.0 * Ct + 4);
+            const double upd_bytes = px * (16.0 * Ct + 8);  // X, d, Z, T, chat in; Z out
+            if (stream_ok) {
+                UpdateArgs u;
+                u.Z = ctx->Z;
+                u.T = ctx->T;
+                u.chat = ctx->chat;
+                u.lam = lambda;
+                u.step = step;
+                u.out_hwc = nullptr;
+                for (int k = 0; k < iterations; ++k) {
+                    for (int i = 0; i < ctx->N; ++i) {
+                        if (i == 0 && k > 0) {  // Eq. (3) step of iteration k-1 fused into this row pass
+                            st = run_launch(ctx, F_ROWUPD, px * (20.0 * Ct + 8), s, [&] {
+                                return launch_row_update(rp, g, Ct, ctx->X, ctx->X, ctx->dx, ctx->kc[i], u, s);
+                            });
+                        } else {
+                            const float* in = (i == 0) ? ctx->Z : ctx->X;
+                            st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
+                                return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
+                            });
+                        }
+                        if (st != DTS_OK) return st;
+                        st = run_launch(ctx, F_COL, row_bytes, s, [&] {
+                            return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
+                        });
+                        if (st != DTS_OK) return st;
+                    }
+                }
+                st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
+                    return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, o_d, ctx->num_sms, s);
                 });
                 if (st != DTS_OK) return st;
-                if (ctx->comm) {  // row-band mode: TUPLE -> all-gather -> compose -> APPLY
-                    if (i + 1 < ctx->N) {
-                        st = col_pass_banded(ctx, Ct, MODE_FILTER, ctx->X, ctx->kc[i], nullptr, nullptr, F_COL,
-                                             row_bytes, s);
+            }
+            for (int k = 0; k < (stream_ok ? 0 : iterations); ++k) {
+                for (int i = 0; i < ctx->N; ++i) {
+                    const float* in = (i == 0) ? ctx->Z : ctx->X;
+                    st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
+                        return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
+                    });
+                    if (st != DTS_OK) return st;
+                    if (ctx->comm) {  // row-band mode: TUPLE -> all-gather -> compose -> APPLY
+                        if (i + 1 < ctx->N) {
+                            st = col_pass_banded(ctx, Ct, MODE_FILTER, ctx->X, ctx->kc[i], nullptr, nullptr, F_COL,
+                                                 row_bytes, s);
+                        } else {
+                            UpdateArgs u;
+                            u.Z = ctx->Z;
+                            u.T = ctx->T;
+                            u.chat = ctx->chat;
+                            u.lam = lambda;
+                            u.step = step;
+                            u.out_hwc = (k + 1 == iterations) ? o_d : nullptr;
+                            st = col_pass_banded(ctx, Ct, MODE_UPDATE, ctx->X, ctx->kc[i], &u, nullptr, F_UPDATE,
+                                                 upd_bytes, s);
+                        }
+                    } else if (i + 1 < ctx->N) {
+                        st = run_launch(ctx, F_COL, row_bytes, s, [&] {
+                            return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
+                                              s);
+                        });
+                    } else if ((cpu.kind == 1 && !std::getenv("DTS_FUSED_UPDATE")) || cpu.kind == 3) {
+                        // column kernel (FILTER) + streaming update kernel (K4b)
+                        st = run_launch(ctx, F_COL, row_bytes, s, [&] {
+                            return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
+                                              s);
+                        });
+                        if (st != DTS_OK) return st;
+                        float* ohwc = (k + 1 == iterations) ? o_d : nullptr;
+                        st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
+                            return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, ohwc,
+                                                 ctx->num_sms, s);
+                        });
                     } else {
                         UpdateArgs u;
                         u.Z = ctx->Z;
@@ -778,40 +814,72 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                         u.lam = lambda;
                         u.step = step;
                         u.out_hwc = (k + 1 == iterations) ? o_d : nullptr;
-                        st = col_pass_banded(ctx, Ct, MODE_UPDATE, ctx->X, ctx->kc[i], &u, nullptr, F_UPDATE,
-                                             upd_bytes, s);
+                        st = run_launch(ctx, F_UPDATE, upd_bytes, s, [&] {
+                            return col_launch(ctx, cpu, Ct, MODE_UPDATE, ctx->X, ctx->dy, ctx->kc[i], &u, nullptr, s);
+                        });
                     }
-                } else if (i + 1 < ctx->N) {
-                    st = run_launch(ctx, F_COL, row_bytes, s, [&] {
-                        return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
-                                          s);
-                    });
-                } else if ((cpu.kind == 1 && !std::getenv("DTS_FUSED_UPDATE")) || cpu.kind == 3) {
-                    // column kernel (FILTER) + streaming update kernel (K4b)
-                    st = run_launch(ctx, F_COL, row_bytes, s, [&] {
-                        return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
-                                          s);
-                    });
                     if (st != DTS_OK) return st;
-                    float* ohwc = (k + 1 == iterations) ? o_d : nullptr;
-                    st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
-                        return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, ohwc,
-                                             ctx->num_sms, s);
-                    });
-                } else {
-                    UpdateArgs u;
-                    u.Z = ctx->Z;
-                    u.T = ctx->T;
-                    u.chat = ctx->chat;
-                    u.lam = lambda;
-                    u.step = step;
-                    u.out_hwc = (k + 1 == iterations) ? o_d : nullptr;
-                    st = run_launch(ctx, F_UPDATE, upd_bytes, s, [&] {
-                        return col_launch(ctx, cpu, Ct, MODE_UPDATE, ctx->X, ctx->dy, ctx->kc[i], &u, nullptr, s);
-                    });
                 }
-                if (st != DTS_OK) return st;
             }
+
+            return DTS_OK;
+        };
+        // Replay a captured graph of the whole launch sequence when the same solve is issued
+        // again (small images are launch-bound).  Only the cluster column path (its kernels
+        // carry no per-launch epochs), device buffers, and the profiler off.
+        bool prof_on;
+        {
+            Profiler& P = profiler();
+            std::lock_guard<std::mutex> lk(P.mu);
+            prof_on = P.on;
+        }
+        const bool use_graph = !any_host && !prof_on && !ctx->comm && cpf.kind == 1 && cpu.kind == 1 && !stream_ok &&
+                               !twop_ok && !std::getenv("DTS_NO_GRAPH");
+        std::vector<uintptr_t> key;
+        if (use_graph) {
+            uint32_t lb, sb;
+            std::memcpy(&lb, &lambda, 4);
+            std::memcpy(&sb, &step, 4);
+            key = {(uintptr_t)t_d, (uintptr_t)c_d, (uintptr_t)o_d, (uintptr_t)Ct, (uintptr_t)iterations, lb, sb,
+                   (uintptr_t)support_mode, (uintptr_t)ctx->X, (uintptr_t)ctx->Z, (uintptr_t)ctx->chat};
+        }
+        const bool replay = use_graph && ctx->graph_exec && ctx->graph_key == key;
+        const bool capture = use_graph && !replay && ctx->graph_seen == key;
+        if (!replay && !capture) {
+            if ((st = enqueue(s)) != DTS_OK) return st;
+            ctx->graph_seen = key;  // the next identical solve is captured
+        } else {
+            if (capture) {
+                if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+                ctx->graph_exec = nullptr;
+                // capture on a context-owned stream (the caller's may be the uncapturable legacy
+                // default stream); the graph is then launched on the caller's stream
+                if (!ctx->cap_stream &&
+                    (e = cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking)) != cudaSuccess)
+                    return cuda_fail(e);
+                cudaStream_t cs = ctx->cap_stream;
+                if ((e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return cuda_fail(e);
+                const int64_t l0 = ctx->launches;
+                st = enqueue(cs);
+                cudaGraph_t graph = nullptr;
+                e = cudaStreamEndCapture(cs, &graph);
+                if (st != DTS_OK) {
+                    if (graph) cudaGraphDestroy(graph);
+                    return st;
+                }
+                if (e != cudaSuccess) return cuda_fail(e);
+                e = cudaGraphInstantiate(&ctx->graph_exec, graph, 0);
+                cudaGraphDestroy(graph);
+                if (e != cudaSuccess) {
+                    ctx->graph_exec = nullptr;
+                    return cuda_fail(e);
+                }
+                ctx->graph_key = key;
+                ctx->graph_launches = ctx->launches - l0;
+                ctx->launches = l0;
+            }
+            if ((e = cudaGraphLaunch(ctx->graph_exec, s)) != cudaSuccess) return cuda_fail(e);
+            ctx->launches += ctx->graph_launches;
         }
     }
     if (ko == PTR_HOST) {
@@ -1013,6 +1081,11 @@ void dts_destroy(dts_ctx* ctx) {
     if (ctx->flags) cudaFreeAsync(ctx->flags, s);
     if (ctx->v_tuples) cudaFreeAsync(ctx->v_tuples, s);
     if (ctx->v_flags) cudaFreeAsync(ctx->v_flags, s);
+    if (ctx->graph_exec) {  // a replay may still be in flight on s
+        cudaStreamSynchronize(s);
+        cudaGraphExecDestroy(ctx->graph_exec);
+    }
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     delete ctx;
 }
 
