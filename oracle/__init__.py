@@ -16,8 +16,13 @@ Functions (each cites the passage its C routine follows; see dts_oracle.c):
   confidence(guide, target, ..., sigma_c)       O7  Eq. (7) edge-aware variance confidence
   solve_stereo(left, right, target, conf, ...)  O8  Eq. (10) stereo refinement, Charbonnier target
   sr_prepare(low, factor)                       O9  depth-SR front end: bicubic target, bump confidence
+  box_increments(guide, sigma_s, sigma_r)       O10a fixed-point DT increments (reading R25)
+  box_radius(radius_scale, sigma)               O10  R = floor(r * 2^16)
+  box_tables(guide, ..., N, radius_scale)       O10b box windows of every pass + support
+  box_dtf(X, guide, ..., N, radius_scale)       O10d 2-D box mean, X then Y per pass
+  solve_box(guide, target, conf, ...)           O10e Eq. (3) iteration with the box mean
 
-Parity status: O1, O3, O4, O5, O6, O7, O8 and O9 are pinned by tests/test_oracle_pins.py
+Parity status: O1, O3, O4, O5, O6, O7, O8, O9 and O10 are pinned by tests/test_oracle_pins.py
 (worked examples, dense triangular matrices, closed forms, brute force,
 reductions); the whole solve is NOT pinned against the paper's own outputs,
 which it never prints ("parity unpinned vs the paper").
@@ -77,6 +82,21 @@ def _load():
     lib.dts_oracle_solve_stereo.restype = ctypes.c_int
     lib.dts_oracle_sr_prepare.argtypes = [_c_float_p, i64, i64, i32, _c_double_p, _c_double_p]
     lib.dts_oracle_sr_prepare.restype = ctypes.c_int
+    c_i64_p = ctypes.POINTER(ctypes.c_int64)
+    c_i32_p = ctypes.POINTER(ctypes.c_int32)
+    flt = ctypes.c_float
+    lib.dts_oracle_box_increments.argtypes = [_c_float_p, i64, i64, i32, flt, flt, c_i64_p, c_i64_p]
+    lib.dts_oracle_box_increments.restype = ctypes.c_int
+    lib.dts_oracle_box_radius.argtypes = [dbl, dbl]
+    lib.dts_oracle_box_radius.restype = i64
+    lib.dts_oracle_box_tables.argtypes = [_c_float_p, i64, i64, i32, flt, flt, i32, dbl,
+                                          c_i32_p, c_i32_p, c_i32_p, c_i32_p, _c_double_p]
+    lib.dts_oracle_box_tables.restype = ctypes.c_int
+    lib.dts_oracle_box_dtf.argtypes = [_c_double_p, i64, i64, i32, _c_float_p, i32, flt, flt, i32, dbl]
+    lib.dts_oracle_box_dtf.restype = ctypes.c_int
+    lib.dts_oracle_solve_box.argtypes = [_c_float_p, i64, i64, i32, flt, flt, i32, dbl, _c_float_p, i32,
+                                         _c_float_p, dbl, dbl, i32, i32, _c_double_p]
+    lib.dts_oracle_solve_box.restype = ctypes.c_int
     lib.dts_oracle_num_threads.argtypes = []
     lib.dts_oracle_num_threads.restype = ctypes.c_int
     lib.dts_oracle_set_threads.argtypes = [ctypes.c_int]
@@ -245,3 +265,86 @@ def sr_prepare(low, factor: int):
     if st:
         raise ValueError(f"dts_oracle_sr_prepare failed ({st})")
     return t, c
+
+
+SQRT3 = float(np.sqrt(3.0))
+
+
+def _guide3(guide):
+    g = _f32(guide)
+    return g[:, :, None] if g.ndim == 2 else g
+
+
+def box_increments(guide, sigma_s: float, sigma_r: float):
+    """O10a: fixed-point DT increments (qx, qy), each H x W int64 (d in fp32, times 2^16,
+    rounded half-even, capped at 2^30; qx[:, 0] = qy[0, :] = 0).  Reading R25."""
+    g = _guide3(guide)
+    H, W, C = g.shape
+    qx = np.empty((H, W), np.int64)
+    qy = np.empty((H, W), np.int64)
+    c_i64_p = ctypes.POINTER(ctypes.c_int64)
+    st = _load().dts_oracle_box_increments(_p(g, _c_float_p), H, W, C, float(np.float32(sigma_s)),
+                                           float(np.float32(sigma_r)), _p(qx, c_i64_p), _p(qy, c_i64_p))
+    if st:
+        raise ValueError(f"dts_oracle_box_increments failed ({st})")
+    return qx, qy
+
+
+def box_radius(radius_scale: float, sigma: float) -> int:
+    """R = floor(radius_scale * sigma * 2^16) (fixed-point box radius, reading R25)."""
+    return int(_load().dts_oracle_box_radius(float(radius_scale), float(sigma)))
+
+
+def box_tables(guide, sigma_s: float, sigma_r: float, N: int, radius_scale: float = SQRT3):
+    """O10b: windows of every pass and the support.  Returns (lox, hix, loy, hiy, S):
+    lo/hi offsets N x H x W int32 (window of pixel i along the line = [i - lo, i + hi]),
+    S = |N^x| |N^y| at r = radius_scale * sigma_s, H x W float64.  sigma_s and sigma_r
+    are taken as float32 (the ABI's type)."""
+    g = _guide3(guide)
+    H, W, C = g.shape
+    lox, hix, loy, hiy = (np.empty((N, H, W), np.int32) for _ in range(4))
+    S = np.empty((H, W), np.float64)
+    c_i32_p = ctypes.POINTER(ctypes.c_int32)
+    st = _load().dts_oracle_box_tables(_p(g, _c_float_p), H, W, C, float(np.float32(sigma_s)),
+                                       float(np.float32(sigma_r)), N, float(radius_scale),
+                                       _p(lox, c_i32_p), _p(hix, c_i32_p), _p(loy, c_i32_p), _p(hiy, c_i32_p),
+                                       _p(S, _c_double_p))
+    if st:
+        raise ValueError(f"dts_oracle_box_tables failed ({st})")
+    return lox, hix, loy, hiy, S
+
+
+def box_dtf(X, guide, sigma_s: float, sigma_r: float, N: int, radius_scale: float = SQRT3):
+    """O10d: 2-D box mean of X (H x W, or Ct x H x W planar), float64 result."""
+    x = np.array(X, dtype=np.float64, copy=True, order="C")
+    planes = x[None] if x.ndim == 2 else x
+    g = _guide3(guide)
+    H, W, C = g.shape
+    assert planes.shape[1:] == (H, W)
+    st = _load().dts_oracle_box_dtf(_p(planes, _c_double_p), H, W, planes.shape[0], _p(g, _c_float_p), C,
+                                    float(np.float32(sigma_s)), float(np.float32(sigma_r)), N, float(radius_scale))
+    if st:
+        raise ValueError(f"dts_oracle_box_dtf failed ({st})")
+    return planes[0] if x.ndim == 2 else planes
+
+
+def solve_box(guide, target, confidence, sigma_s: float, sigma_r: float, N: int, lam: float, iters: int,
+              step: float = 0.99, support_mode: int = 0, radius_scale: float = SQRT3):
+    """O10e: the DTS iteration with the box mean and the box support.  Returns H x W x Ct
+    (H x W for a 2-D target) float64."""
+    g = _guide3(guide)
+    t = _f32(target)
+    squeeze = t.ndim == 2
+    if squeeze:
+        t = t[:, :, None]
+    c = _f32(confidence)
+    H, W, Cg = g.shape
+    assert t.shape[:2] == (H, W) and c.shape == (H, W)
+    Ct = t.shape[2]
+    out = np.empty((H, W, Ct), np.float64)
+    st = _load().dts_oracle_solve_box(_p(g, _c_float_p), H, W, Cg, float(np.float32(sigma_s)),
+                                      float(np.float32(sigma_r)), N, float(radius_scale), _p(t, _c_float_p), Ct,
+                                      _p(c, _c_float_p), lam, step, iters, support_mode, _p(out, _c_double_p))
+    if st:
+        raise ValueError(f"dts_oracle_solve_box failed ({st})")
+    return out[:, :, 0] if squeeze else out

@@ -18,6 +18,11 @@
  *   O4 dts_oracle_dtf         2-D edge-aware mean: rows then columns, per pass (Q6)
  *   O5 dts_oracle_support     S = sum_j W_ij by unnormalised two-sided sums (Q7)
  *   O6 dts_oracle_solve       gradient descent on Eq. (2) with the Eq. (3) gradient
+ *   O7 dts_oracle_confidence  Eq. (7) confidence from the edge-aware variance
+ *   O8 dts_oracle_solve_stereo Eq. (10) stereo refinement with the Charbonnier target term
+ *   O9 dts_oracle_sr_prepare  depth-SR front end
+ *   O10 dts_oracle_box_*      box (normalised-convolution) edge-aware mean, its support and
+ *                             the DTS iteration with it (reading R25)
  * Parallelism: OpenMP "parallel for" over independent rows / column ranges only;
  * each output element is produced by exactly one thread with the same
  * arithmetic, so results do not depend on the thread count.  Reductions for
@@ -508,4 +513,239 @@ int dts_oracle_sr_prepare(const float* low, int64_t h, int64_t w, int32_t f, dou
         }
     }
     return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O10: box (normalised-convolution) variant of the edge-aware mean.
+ * zbar_i = sum_j W_ij z_j with W_ij = delta{ DT(z_i) - DT(z_j) <= r },
+ * read (reading R25, with S:132-160) as the normalised box window on the domain-
+ * transform axis:  zbar_i = (1/|N_i|) sum_{j in N_i} z_j,  N_i = { j : |T_j - T_i| <= r },
+ * taken along rows (T from the row increments) then columns, N passes with
+ * r_i = radius_scale * sigma_i (O2 schedule; radius_scale = sqrt(3), makes the
+ * box's standard deviation sigma_i), and the support S_i = |N_i^x| * |N_i^y| at
+ * r = radius_scale * sigma_s.
+ *
+ * Window membership is an integer decision, so both implementations take it in the
+ * same precision (reading R25): the increment is evaluated in IEEE single precision in
+ * this fixed order (no fused multiply-add, correctly rounded sqrt)
+ *     k2 = (sigma_s / sigma_r)^2;  s = sum_k (I_k(c) - I_k(c-1))^2  (k = 0, 1, ...)
+ *     d  = sqrt(1 + k2 * s)
+ * and the DT coordinate is held in fixed point with 16 fractional bits,
+ *     q(c) = round_half_even(d * 2^16)  (capped at 2^30),  T(c) = sum_{c' <= c} q(c'),
+ * with the radius R = floor(r * 2^16) computed in double.  Then T is an exact
+ * integer and |T_j - T_i| <= R is decided exactly.                          */
+#define BOX_QMAX ((int64_t)1 << 30)
+
+static int64_t box_increment(const float* a, const float* b, int32_t C, float k2) {
+    float s = 0.0f;
+    for (int32_t k = 0; k < C; ++k) {
+        float diff = a[k] - b[k];
+        float sq = diff * diff;
+        s = s + sq;
+    }
+    float t = k2 * s;
+    float v = 1.0f + t;
+    float d = sqrtf(v);
+    float scaled = d * 65536.0f;
+    int64_t q = (int64_t)rintf(scaled);
+    return q > BOX_QMAX ? BOX_QMAX : q;
+}
+
+/* O10a: fixed-point increments.  qx[r][c] = q between (r, c-1) and (r, c) (qx[r][0] = 0),
+ * qy[r][c] = q between (r-1, c) and (r, c) (qy[0][c] = 0).  guide HWC fp32.     */
+int dts_oracle_box_increments(const float* guide, int64_t H, int64_t W, int32_t C, float sigma_s,
+                              float sigma_r, int64_t* qx, int64_t* qy) {
+    if (!guide || !qx || !qy || H < 1 || W < 1 || C < 1) return ORACLE_E_ARG;
+    if (!(sigma_s > 0.0f) || !(sigma_r > 0.0f)) return ORACLE_E_ARG;
+    const float ratio = sigma_s / sigma_r;
+    const float k2 = ratio * ratio;
+    for (int64_t r = 0; r < H; ++r)
+        for (int64_t c = 0; c < W; ++c) {
+            const float* px = guide + (r * W + c) * C;
+            qx[r * W + c] = c == 0 ? 0 : box_increment(px, px - C, C, k2);
+            qy[r * W + c] = r == 0 ? 0 : box_increment(px, px - W * C, C, k2);
+        }
+    return ORACLE_OK;
+}
+
+/* box radius in fixed point: R = floor(radius_scale * sigma * 2^16), in double */
+int64_t dts_oracle_box_radius(double radius_scale, double sigma) {
+    return (int64_t)floor(radius_scale * sigma * 65536.0);
+}
+
+/* O10b: window of every sample of a line of n samples spaced `stride` apart, from
+ * its increments q (q[0] unused): lo = smallest j <= i with T_i - T_j <= R, hi =
+ * largest j >= i with T_j - T_i <= R (T is increasing, so N_i = [lo, hi]).
+ * lo_off[i] = i - lo, hi_off[i] = hi - i (output spaced like the input).     */
+static void box_window_line(const int64_t* q, int64_t n, int64_t stride, int64_t R, int32_t* lo_off,
+                            int32_t* hi_off) {
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t dist = 0, j = i;
+        while (j > 0 && dist + q[j * stride] <= R) { dist += q[j * stride]; --j; }   /* T_i - T_{j-1} */
+        lo_off[i * stride] = (int32_t)(i - j);
+        dist = 0;
+        j = i;
+        while (j + 1 < n && dist + q[(j + 1) * stride] <= R) { dist += q[(j + 1) * stride]; ++j; }
+        hi_off[i * stride] = (int32_t)(j - i);
+    }
+}
+
+/* windows of all rows (from qx) and all columns (from qy) at radius R            */
+int dts_oracle_box_windows(const int64_t* qx, const int64_t* qy, int64_t H, int64_t W, int64_t R,
+                           int32_t* lox, int32_t* hix, int32_t* loy, int32_t* hiy) {
+    if (!qx || !qy || !lox || !hix || !loy || !hiy || H < 1 || W < 1 || R < 0) return ORACLE_E_ARG;
+    int64_t r, c;
+#pragma omp parallel for schedule(static)
+    for (r = 0; r < H; ++r) box_window_line(qx + r * W, W, 1, R, lox + r * W, hix + r * W);
+#pragma omp parallel for schedule(static)
+    for (c = 0; c < W; ++c) box_window_line(qy + c, H, W, R, loy + c, hiy + c);
+    return ORACLE_OK;
+}
+
+/* O10c: the box mean of one line: out_i = (1/(hi-lo+1)) sum_{j=lo}^{hi} x_j, fp64. */
+static void box_mean_line(const double* x, double* out, int64_t n, int64_t stride, const int32_t* lo_off,
+                          const int32_t* hi_off) {
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t lo = i - lo_off[i * stride], hi = i + hi_off[i * stride];
+        double sum = 0.0;
+        for (int64_t j = lo; j <= hi; ++j) sum += x[j * stride];
+        out[i * stride] = sum / (double)(hi - lo + 1);
+    }
+}
+
+typedef struct {
+    int32_t *lox, *hix, *loy, *hiy; /* N x H x W each */
+    double* S;                      /* H x W */
+} box_tables;
+
+static void box_tables_free(box_tables* b) {
+    free(b->lox); free(b->hix); free(b->loy); free(b->hiy); free(b->S);
+    memset(b, 0, sizeof(*b));
+}
+
+static int box_tables_make(const float* guide, int64_t H, int64_t W, int32_t Cg, float sigma_s, float sigma_r,
+                           int32_t N, double radius_scale, int32_t support_mode, box_tables* b) {
+    double sig[64];
+    memset(b, 0, sizeof(*b));
+    if (N < 1 || N > 64) return ORACLE_E_ARG;
+    const int64_t HW = H * W;
+    int64_t* qx = (int64_t*)malloc(sizeof(int64_t) * (size_t)HW);
+    int64_t* qy = (int64_t*)malloc(sizeof(int64_t) * (size_t)HW);
+    int32_t* t0 = (int32_t*)malloc(sizeof(int32_t) * (size_t)HW * 4);
+    b->lox = (int32_t*)malloc(sizeof(int32_t) * (size_t)HW * (size_t)N);
+    b->hix = (int32_t*)malloc(sizeof(int32_t) * (size_t)HW * (size_t)N);
+    b->loy = (int32_t*)malloc(sizeof(int32_t) * (size_t)HW * (size_t)N);
+    b->hiy = (int32_t*)malloc(sizeof(int32_t) * (size_t)HW * (size_t)N);
+    b->S = (double*)malloc(sizeof(double) * (size_t)HW);
+    int st = ORACLE_OK;
+    if (!qx || !qy || !t0 || !b->lox || !b->hix || !b->loy || !b->hiy || !b->S) { st = ORACLE_E_OOM; goto done; }
+    st = dts_oracle_box_increments(guide, H, W, Cg, sigma_s, sigma_r, qx, qy);          /* O10a */
+    if (st) goto done;
+    dts_oracle_sigmas((double)sigma_s, N, sig);                                         /* O2 */
+    for (int32_t i = 0; i < N; ++i) {                                                   /* O10b */
+        const int64_t off = (int64_t)i * HW;
+        st = dts_oracle_box_windows(qx, qy, H, W, dts_oracle_box_radius(radius_scale, sig[i]), b->lox + off,
+                                    b->hix + off, b->loy + off, b->hiy + off);
+        if (st) goto done;
+    }
+    /* support: |N^x| |N^y| at r = radius_scale * sigma_s */
+    st = dts_oracle_box_windows(qx, qy, H, W, dts_oracle_box_radius(radius_scale, (double)sigma_s), t0, t0 + HW,
+                                t0 + 2 * HW, t0 + 3 * HW);
+    if (st) goto done;
+    for (int64_t p = 0; p < HW; ++p)
+        b->S[p] = support_mode == 1 ? 1.0
+                                    : (double)(t0[p] + t0[HW + p] + 1) * (double)(t0[2 * HW + p] + t0[3 * HW + p] + 1);
+done:
+    free(qx); free(qy); free(t0);
+    if (st) box_tables_free(b);
+    return st;
+}
+
+/* O10d: 2-D box mean: for i = 1..N, rows with the pass-i row windows, then columns
+ * with the pass-i column windows (each pass reads the previous pass's output).   */
+static void box_dtf_with_tables(double* X, double* tmp, int64_t H, int64_t W, int32_t Ct, int32_t N,
+                                const box_tables* b) {
+    const int64_t HW = H * W;
+    for (int32_t i = 0; i < N; ++i) {
+        const int64_t off = (int64_t)i * HW;
+        for (int32_t ch = 0; ch < Ct; ++ch) {
+            double* P = X + (int64_t)ch * HW;
+            int64_t r, c;
+#pragma omp parallel for schedule(static)
+            for (r = 0; r < H; ++r) box_mean_line(P + r * W, tmp + r * W, W, 1, b->lox + off + r * W, b->hix + off + r * W);
+#pragma omp parallel for schedule(static)
+            for (c = 0; c < W; ++c) box_mean_line(tmp + c, P + c, H, W, b->loy + off + c, b->hiy + off + c);
+        }
+    }
+}
+
+/* Python-facing: box tables of a guide (windows of every pass, support). */
+int dts_oracle_box_tables(const float* guide, int64_t H, int64_t W, int32_t Cg, float sigma_s, float sigma_r,
+                          int32_t N, double radius_scale, int32_t* lox, int32_t* hix, int32_t* loy, int32_t* hiy,
+                          double* S) {
+    if (!guide || !lox || !hix || !loy || !hiy || !S || H < 1 || W < 1 || Cg < 1) return ORACLE_E_ARG;
+    box_tables b;
+    int st = box_tables_make(guide, H, W, Cg, sigma_s, sigma_r, N, radius_scale, 0, &b);
+    if (st) return st;
+    const size_t n = sizeof(int32_t) * (size_t)(H * W) * (size_t)N;
+    memcpy(lox, b.lox, n); memcpy(hix, b.hix, n); memcpy(loy, b.loy, n); memcpy(hiy, b.hiy, n);
+    memcpy(S, b.S, sizeof(double) * (size_t)(H * W));
+    box_tables_free(&b);
+    return ORACLE_OK;
+}
+
+/* Python-facing: the 2-D box mean of Ct planar channels (X in place) for a guide. */
+int dts_oracle_box_dtf(double* X, int64_t H, int64_t W, int32_t Ct, const float* guide, int32_t Cg, float sigma_s,
+                       float sigma_r, int32_t N, double radius_scale) {
+    if (!X || !guide || H < 1 || W < 1 || Ct < 1 || Cg < 1) return ORACLE_E_ARG;
+    box_tables b;
+    int st = box_tables_make(guide, H, W, Cg, sigma_s, sigma_r, N, radius_scale, 0, &b);
+    if (st) return st;
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)(H * W));
+    if (!tmp) { box_tables_free(&b); return ORACLE_E_OOM; }
+    box_dtf_with_tables(X, tmp, H, W, Ct, N, &b);
+    free(tmp);
+    box_tables_free(&b);
+    return ORACLE_OK;
+}
+
+/* O10e: the DTS iteration of O6 with the box mean (O10d) and the box support. */
+int dts_oracle_solve_box(const float* guide, int64_t H, int64_t W, int32_t Cg, float sigma_s, float sigma_r,
+                         int32_t N, double radius_scale, const float* target, int32_t Ct, const float* confidence,
+                         double lambda, double step, int32_t iters, int32_t support_mode, double* out) {
+    if (!guide || !target || !confidence || !out) return ORACLE_E_ARG;
+    if (H < 1 || W < 1 || Cg < 1 || Ct < 1 || N < 1 || iters < 0) return ORACLE_E_ARG;
+    const int64_t HW = H * W;
+    box_tables b;
+    int st = box_tables_make(guide, H, W, Cg, sigma_s, sigma_r, N, radius_scale, support_mode, &b);
+    if (st) return st;
+    double* chat = (double*)malloc(sizeof(double) * (size_t)HW);
+    double* Z = (double*)malloc(sizeof(double) * (size_t)HW * (size_t)Ct);
+    double* T = (double*)malloc(sizeof(double) * (size_t)HW * (size_t)Ct);
+    double* Zbar = (double*)malloc(sizeof(double) * (size_t)HW * (size_t)Ct);
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)HW);
+    if (!chat || !Z || !T || !Zbar || !tmp) { st = ORACLE_E_OOM; goto done; }
+    for (int64_t p = 0; p < HW; ++p) chat[p] = (double)confidence[p] / b.S[p];
+    for (int32_t ch = 0; ch < Ct; ++ch)
+        for (int64_t p = 0; p < HW; ++p) {
+            T[ch * HW + p] = (double)target[p * Ct + ch];
+            Z[ch * HW + p] = T[ch * HW + p];
+        }
+    for (int32_t k = 0; k < iters; ++k) {
+        memcpy(Zbar, Z, sizeof(double) * (size_t)HW * (size_t)Ct);
+        box_dtf_with_tables(Zbar, tmp, H, W, Ct, N, &b);                            /* O10d */
+        int64_t q;
+#pragma omp parallel for schedule(static)
+        for (q = 0; q < HW * Ct; ++q) {
+            int64_t p = q % HW;
+            double g = lambda * (Z[q] - Zbar[q]) + chat[p] * (Z[q] - T[q]);        /* Eq. (3) */
+            Z[q] = Z[q] - step * g;
+        }
+    }
+    for (int32_t ch = 0; ch < Ct; ++ch)
+        for (int64_t p = 0; p < HW; ++p) out[p * Ct + ch] = Z[ch * HW + p];
+done:
+    free(chat); free(Z); free(T); free(Zbar); free(tmp);
+    box_tables_free(&b);
+    return st;
 }

@@ -542,3 +542,177 @@ def test_sr_bump_confidence_closed_form():
     assert abs(c[1, 1] - np.exp(-0.25)) <= 1e-15
     np.testing.assert_allclose(c[4:20, 4:20], np.tile(c[4:8, 4:8], (4, 4)), rtol=0, atol=1e-15)
     assert np.all((c > 0) & (c <= 1))
+
+
+# ---------------------------------------------------------------------------------------
+# O10: box (normalised-convolution) variant (reading R25)
+
+BOX = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "box_spec_examples.json")))
+
+
+def _line_guide(n):
+    return np.zeros((1, n), np.float32)
+
+
+def test_box_spec_worked_examples():
+    for key in ("box_mean_constant_guide", "box_mean_radius_zero"):
+        ex = BOX[key]
+        x = np.array([ex["values"]], np.float64)
+        got = oracle.box_dtf(x, _line_guide(x.shape[1]), 1.0, 0.1, 1, radius_scale=ex["radius"])
+        np.testing.assert_allclose(got[0], ex["mean"], rtol=0, atol=1e-15)
+    for key in ("box_count_constant_guide", "box_count_radius_zero"):
+        ex = BOX[key]
+        lox, hix, _, _, S = oracle.box_tables(_line_guide(ex["length"]), 1.0, 0.1, 1, radius_scale=ex["radius"])
+        assert (lox[0, 0] + hix[0, 0] + 1).tolist() == ex["count"]
+        assert S[0].tolist() == ex["count"]  # H = 1: the column count is 1
+
+
+def test_box_increments_match_the_fp64_distance():
+    # q = round(d * 2^16) with d the O1 increment (pinned above), evaluated in fp32
+    rng = np.random.default_rng(5)
+    g = rng.random((13, 17, 3), dtype=np.float32)
+    for ss, sr in ((8.0, 0.1), (64.0, 0.2), (3.0, 2.0)):
+        qx, qy = oracle.box_increments(g, ss, sr)
+        dx, dy = oracle.distances(g, ss, sr)
+        for q, d in ((qx[:, 1:], dx[:, 1:]), (qy[1:], dy[1:])):
+            ref = d * 65536.0
+            assert np.all(np.abs(q - ref) <= 0.5 + 4e-7 * ref)
+        assert np.all(qx[:, 0] == 0) and np.all(qy[0] == 0)
+        assert np.all(qx[:, 1:] >= 65536) and np.all(qy[1:] >= 65536)  # d >= 1
+
+
+def _brute_windows(T, r):
+    """Real-valued window of every sample from the DT coordinate T (fp64): the set
+    {j : |T_j - T_i| <= r}, checked contiguous; returns (lo_off, hi_off, margin) where
+    margin is the distance of the nearest |T_j - T_i| to r (to skip rounding ties)."""
+    n = T.size
+    lo, hi, margin = np.zeros(n, int), np.zeros(n, int), np.full(n, np.inf)
+    for i in range(n):
+        dist = np.abs(T - T[i])
+        idx = np.nonzero(dist <= r)[0]
+        assert idx.size == idx[-1] - idx[0] + 1  # contiguous (T is increasing)
+        lo[i], hi[i] = i - idx[0], idx[-1] - i
+        margin[i] = np.min(np.abs(dist - r))
+    return lo, hi, margin
+
+
+def test_box_windows_brute_force():
+    rng = np.random.default_rng(7)
+    g = rng.random((9, 31, 3), dtype=np.float32)
+    ss, sr, N = 6.0, 0.6, 3
+    dx, dy = oracle.distances(g, ss, sr)
+    sig = oracle.sigmas(ss, N)
+    lox, hix, loy, hiy, S = oracle.box_tables(g, ss, sr, N)
+    checked = 0
+    for i in range(N):
+        r = np.sqrt(3.0) * sig[i]
+        for row in range(9):
+            T = np.concatenate([[0.0], np.cumsum(dx[row, 1:])])
+            lo, hi, m = _brute_windows(T, r)
+            ok = m > 1e-3
+            assert np.array_equal(lox[i, row][ok], lo[ok]) and np.array_equal(hix[i, row][ok], hi[ok])
+            checked += ok.sum()
+        for col in range(31):
+            T = np.concatenate([[0.0], np.cumsum(dy[1:, col])])
+            lo, hi, m = _brute_windows(T, r)
+            ok = m > 1e-3
+            assert np.array_equal(loy[i, :, col][ok], lo[ok]) and np.array_equal(hiy[i, :, col][ok], hi[ok])
+            checked += ok.sum()
+    assert checked > 0.95 * N * 2 * 9 * 31
+    # support: counts at r = sqrt(3) sigma_s, multiplied
+    r = np.sqrt(3.0) * ss
+    cx = np.array([[sum(_brute_windows(np.concatenate([[0.0], np.cumsum(dx[row, 1:])]), r)[k][c] for k in (0, 1)) + 1
+                    for c in range(31)] for row in range(9)])
+    cy = np.array([[sum(_brute_windows(np.concatenate([[0.0], np.cumsum(dy[1:, col])]), r)[k][row] for k in (0, 1)) + 1
+                    for col in range(31)] for row in range(9)])
+    np.testing.assert_array_equal(S, cx * cy)
+
+
+def _box_dense_operator(g, ss, sr, N, radius_scale=np.sqrt(3.0)):
+    """Dense matrix of the 2-D box mean built from real-valued brute-force windows:
+    K = prod_i (M_y,i M_x,i) (rows then columns per pass)."""
+    H, W = g.shape[:2]
+    dx, dy = oracle.distances(g, ss, sr)
+    sig = oracle.sigmas(ss, N)
+    K = np.eye(H * W)
+    margin = np.inf
+    for i in range(N):
+        r = radius_scale * sig[i]
+        Mx, My = np.zeros((H * W, H * W)), np.zeros((H * W, H * W))
+        for row in range(H):
+            lo, hi, m = _brute_windows(np.concatenate([[0.0], np.cumsum(dx[row, 1:])]), r)
+            margin = min(margin, m.min())
+            for c in range(W):
+                Mx[row * W + c, row * W + c - lo[c]: row * W + c + hi[c] + 1] = 1.0 / (lo[c] + hi[c] + 1)
+        for col in range(W):
+            lo, hi, m = _brute_windows(np.concatenate([[0.0], np.cumsum(dy[1:, col])]), r)
+            margin = min(margin, m.min())
+            for rr in range(H):
+                for j in range(rr - lo[rr], rr + hi[rr] + 1):
+                    My[rr * W + col, j * W + col] = 1.0 / (lo[rr] + hi[rr] + 1)
+        K = My @ Mx @ K
+    return K, margin
+
+
+@pytest.mark.parametrize("H,W,N", [(7, 9, 1), (6, 11, 3)])
+def test_box_dtf_equals_dense_operator(H, W, N):
+    rng = np.random.default_rng(H * 100 + W)
+    g = rng.random((H, W, 2), dtype=np.float32)
+    K, margin = _box_dense_operator(g, 4.0, 0.8, N)
+    assert margin > 1e-4  # no rounding tie on this instance
+    x = rng.standard_normal((2, H, W))
+    got = oracle.box_dtf(x, g, 4.0, 0.8, N)
+    for ch in range(2):
+        np.testing.assert_allclose(got[ch].ravel(), K @ x[ch].ravel(), rtol=0, atol=1e-13)
+    np.testing.assert_allclose(K.sum(axis=1), 1.0, atol=1e-13)  # normalised: row-stochastic
+
+
+def test_box_two_region_spec_example():
+    ex = BOX["two_region"]
+    H, W, s = ex["H"], ex["W"], ex["split"]
+    g = np.zeros((H, W, 3), np.float32)
+    g[:, s:] = 1.0
+    x = np.where(np.arange(W)[None, :] < s, ex["left"], ex["right"]) * np.ones((H, 1))
+    got = oracle.box_dtf(x, g, ex["sigma_s"], ex["sigma_r"], 1)
+    np.testing.assert_array_equal(got, x)  # no window crosses the edge: exact
+    _, _, _, _, S = oracle.box_tables(g, ex["sigma_s"], ex["sigma_r"], 1)
+    h = ex["half_width"]
+
+    def counts(n):
+        i = np.arange(n)
+        return np.minimum(i, h) + np.minimum(n - 1 - i, h) + 1
+
+    cx = np.concatenate([counts(s), counts(W - s)])
+    np.testing.assert_array_equal(S, counts(H)[:, None] * cx[None, :])
+
+
+def test_box_constant_values_any_guide():
+    rng = np.random.default_rng(11)
+    g = rng.random((12, 15, 3), dtype=np.float32)
+    got = oracle.box_dtf(np.full((12, 15), 0.375), g, 5.0, 0.3, 3)
+    np.testing.assert_allclose(got, 0.375, rtol=0, atol=1e-15)
+
+
+def test_box_solve_equals_dense_iteration():
+    rng = np.random.default_rng(13)
+    H, W, N = 6, 8, 2
+    g = rng.random((H, W, 3), dtype=np.float32)
+    t = rng.random((H, W), dtype=np.float32)
+    c = rng.uniform(0.1, 1.0, (H, W)).astype(np.float32)
+    lam, step, iters = 0.99, 0.99, 4
+    K, margin = _box_dense_operator(g, 3.0, 0.5, N)
+    assert margin > 1e-4
+    _, _, _, _, S = oracle.box_tables(g, 3.0, 0.5, N)
+    chat = c.astype(np.float64).ravel() / S.ravel()
+    z = t.astype(np.float64).ravel()
+    T = z.copy()
+    for _ in range(iters):
+        z = z - step * (lam * (z - K @ z) + chat * (z - T))  # Eq. (3)
+    got = oracle.solve_box(g, t, c, 3.0, 0.5, N, lam, iters, step=step)
+    np.testing.assert_allclose(got.ravel(), z, rtol=0, atol=1e-12)
+    # support mode 1: S = 1
+    z = T.copy()
+    for _ in range(iters):
+        z = z - step * (lam * (z - K @ z) + c.astype(np.float64).ravel() * (z - T))
+    got = oracle.solve_box(g, t, c, 3.0, 0.5, N, lam, iters, step=step, support_mode=1)
+    np.testing.assert_allclose(got.ravel(), z, rtol=0, atol=1e-12)
