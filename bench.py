@@ -304,6 +304,35 @@ def main():
                                 "gbs_algorithmic": cbytes / (c_ms / 1e3) / 1e9,
                                 "frac": cbytes / (c_ms / 1e3) / 1e9 / peak_c}
 
+    # ---- the box (normalised-convolution) variant on the same workload ----
+    if world == 1 and band is None and cfg.batch == 1:
+        g0, t0, c0 = dev_in[0]
+        bout = torch.empty_like(t0)
+
+        def box_step():
+            bctx = dts.dts_create_ex(g0, cfg.sigma_s, cfg.sigma_r, cfg.N, dts.DTS_FILTER_BOX, stream=stream.cuda_stream)
+            dts.dts_solve(bctx, t0, c0, cfg.lam, cfg.iters, bout, stream=stream.cuda_stream)
+            dts.dts_destroy(bctx)
+
+        box_step()
+        dts.dts_profile_enable(0, True)
+        b_ms = timed(box_step, 2) / 2
+        bstats = dts.dts_profile_read(0)
+        dts.dts_profile_enable(0, False)
+        peak_b, _ = measured_peaks()
+        bpx = t0.shape[0] * t0.shape[1]
+        extras["box"] = {"what": "dts_create_ex(DTS_FILTER_BOX) + dts_solve + dts_destroy: the box-window edge-aware "
+                                 "mean (reading R25), same guide / target / confidence / iterations",
+                         "ms_per_step": b_ms, "mpix_iter_per_s": bpx * cfg.iters / 1e6 / (b_ms / 1e3),
+                         "kernels": {}}
+        for name in ("box_windows", "box_row", "box_col", "update", "prologue"):
+            v = bstats.get(name)
+            if v and v["launches"]:
+                avg = v["total_ms"] / v["launches"]
+                gbs = v["bytes_per_launch"] / (avg / 1e3) / 1e9
+                extras["box"]["kernels"][name] = {"launches": v["launches"], "avg_ms": avg, "gbs": gbs,
+                                                  "frac": gbs / peak_b}
+
     # ---- Eq. (10) stereo refinement, C1 shape (single GPU, rank 0) ----
     if world == 1 and band is None:
         c1 = CONFIGS["C1"]

@@ -114,6 +114,38 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t target_channe
                         const float* confidence, float lambda, int32_t iterations,
                         float* out, void* stream, const dts_solve_opts* opts);
 
+/* ---- box (normalised-convolution) variant of the edge-aware mean ---------
+ * P:243-245 write the mean with the box indicator W_ij = delta{DT(z_i) - DT(z_j) <= r};
+ * reading R25 takes it as the normalised window on the guide's
+ * domain-transform axis, zbar_i = (1/|N_i|) sum_{j in N_i} z_j, N_i = {j : |T_j - T_i| <= r},
+ * N passes of rows then columns with r_i = radius_scale * sigma_i (R5 schedule), and the
+ * support S = |N^x| * |N^y| at r = radius_scale * sigma_s.  Window
+ * membership is exact integer arithmetic: d is evaluated in IEEE fp32 in a fixed order
+ * (k2 = (sigma_s/sigma_r)^2 in fp32, s = sum_k dI_k^2 in channel order, d = sqrt(1 + k2 s),
+ * no fused multiply-add) and T is held in fixed point, q = round_half_even(d * 2^16) capped
+ * at 2^30, R = floor(r * 2^16) (double). */
+typedef enum { DTS_FILTER_RF = 0, DTS_FILTER_BOX = 1 } dts_filter;
+typedef struct {
+    int32_t filter;      /* DTS_FILTER_RF (default, what dts_create builds) or DTS_FILTER_BOX  */
+    float radius_scale;  /* box: r_i = radius_scale * sigma_i; 0 selects sqrt(3), < 0 is
+                            DTS_E_ARG.  Ignored for DTS_FILTER_RF                               */
+} dts_create_opts;
+
+/* dts_create with options; opts == NULL (or filter == DTS_FILTER_RF) is exactly dts_create.
+ * A box context supports dts_solve / dts_solve_ex (same arguments and semantics, with the
+ * box mean and the box support in Eq. 3); dts_confidence and dts_solve_stereo return
+ * DTS_E_ARG for it.  Box limits: window half-width <= 65535 px, and the column tile needs
+ * min(floor(r_1), H - 1) <= ~800 rows (else DTS_E_SHAPE).  Memory: 2N window planes
+ * (4 B/px each) + the fixed-point increments (8 B/px) + S, plus a second state buffer
+ * per solve. */
+dts_status dts_create_ex(const float* guide, int64_t H, int64_t W, int32_t C, float sigma_s, float sigma_r,
+                         int32_t filter_passes, const dts_create_opts* opts, void* stream, dts_ctx** out_ctx);
+
+/* Box context only: copy the windows of pass `pass` (0-based) along `axis` (0: rows,
+ * 1: columns) to host_out (H x W uint32, row-major): lo | hi << 16, the window of pixel
+ * i along the line being [i - lo, i + hi].  Synchronises the context's last stream. */
+dts_status dts_debug_read_windows(dts_ctx* ctx, int32_t pass, int32_t axis, uint32_t* host_out);
+
 /* Confidence from the edge-aware variance, Eq. (7) of the paper:
  *     V_i = DT(t_i^2) - DT(t_i)^2   (clamped at 0),     c_i = exp(-V_i / (2 sigma_c^2))
  * where DT is the context's N-pass edge-aware mean (the same recursive filter and
@@ -169,7 +201,9 @@ dts_status dts_sr_prepare(const float* low, int64_t h, int64_t w, int32_t factor
 
 /* Buffers a test can read back (row-major H x W, fp32; stream-ordered then synchronised). */
 typedef enum { DTS_BUF_DX = 0, DTS_BUF_DY = 1, DTS_BUF_SUPPORT = 2 } dts_buffer;
-/* Copies the H x W buffer `which` into host memory `host_out` (H*W floats). */
+/* Copies the H x W buffer `which` into host memory `host_out` (H*W floats).  Box
+ * contexts: DX / DY hold the fixed-point increments q as uint32 bit patterns (view the
+ * floats as uint32), SUPPORT the window-count product. */
 dts_status dts_debug_read(dts_ctx* ctx, dts_buffer which, float* host_out);
 
 /* Per-kernel timing with CUDA events recorded on the launch stream around every

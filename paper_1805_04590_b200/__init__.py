@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 __all__ = ["DTSError", "dts_create", "dts_solve", "dts_solve_ex", "dts_confidence", "dts_solve_stereo",
-           "dts_sr_prepare",
+           "dts_sr_prepare", "dts_create_ex", "dts_debug_read_windows", "DTS_FILTER_RF", "DTS_FILTER_BOX",
            "dts_destroy",
            "dts_status_string",
            "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback", "dts_comm_destroy",
@@ -32,13 +32,14 @@ _LIB_PATH = os.path.join(_HERE, "libdts_b200.so")
 _lib = None
 
 DTS_BUF_DX, DTS_BUF_DY, DTS_BUF_SUPPORT = 0, 1, 2
+DTS_FILTER_RF, DTS_FILTER_BOX = 0, 1
 
 # every symbol declared in include/dts.h
 ABI_FUNCTIONS = ["dts_create", "dts_solve", "dts_destroy", "dts_status_string", "dts_last_error_string",
                  "dts_solve_ex", "dts_debug_read", "dts_profile_enable", "dts_profile_read",
                  "dts_launch_count", "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback",
                  "dts_comm_destroy", "dts_create_band", "dts_version", "dts_confidence", "dts_solve_stereo",
-                 "dts_sr_prepare"]
+                 "dts_sr_prepare", "dts_create_ex", "dts_debug_read_windows"]
 
 
 class DTSError(RuntimeError):
@@ -48,6 +49,11 @@ class DTSError(RuntimeError):
         if detail:
             msg += f" ({detail})"
         super().__init__(msg)
+
+
+class CreateOpts(ctypes.Structure):
+    """dts_create_opts (include/dts.h)."""
+    _fields_ = [("filter", ctypes.c_int32), ("radius_scale", ctypes.c_float)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -75,6 +81,11 @@ def load_library():
     vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
     lib.dts_create.argtypes = [vp, i64, i64, i32, f32, f32, i32, vp, ctypes.POINTER(vp)]
     lib.dts_create.restype = ctypes.c_int
+    lib.dts_create_ex.argtypes = [vp, i64, i64, i32, f32, f32, i32, ctypes.POINTER(CreateOpts), vp,
+                                  ctypes.POINTER(vp)]
+    lib.dts_create_ex.restype = ctypes.c_int
+    lib.dts_debug_read_windows.argtypes = [vp, i32, i32, vp]
+    lib.dts_debug_read_windows.restype = ctypes.c_int
     lib.dts_solve.argtypes = [vp, vp, i32, vp, f32, i32, vp, vp]
     lib.dts_solve.restype = ctypes.c_int
     lib.dts_solve_ex.argtypes = [vp, vp, i32, vp, f32, i32, vp, vp, ctypes.POINTER(SolveOpts)]
@@ -169,6 +180,30 @@ def dts_create(guide, sigma_s: float, sigma_r: float, filter_passes: int = 3, st
                                    _stream(stream, guide), ctypes.byref(ctx))
     _check(st, "dts_create")
     return ctx.value
+
+
+def dts_create_ex(guide, sigma_s: float, sigma_r: float, filter_passes: int = 3, filter: int = DTS_FILTER_RF,
+                  radius_scale: float = 0.0, stream=None) -> int:
+    """dts_create with options: filter = DTS_FILTER_BOX builds the box-variant context (reading
+    R25); radius_scale 0 selects sqrt(3)."""
+    if len(guide.shape) == 2:
+        H, W = guide.shape
+        C = 1
+    else:
+        H, W, C = guide.shape
+    opts = CreateOpts(int(filter), float(radius_scale))
+    ctx = ctypes.c_void_p()
+    st = load_library().dts_create_ex(_ptr(guide, "guide"), H, W, C, sigma_s, sigma_r, filter_passes,
+                                      ctypes.byref(opts), _stream(stream, guide), ctypes.byref(ctx))
+    _check(st, "dts_create_ex")
+    return ctx.value
+
+
+def dts_debug_read_windows(ctx: int, pass_index: int, axis: int, H: int, W: int) -> np.ndarray:
+    """Box context: packed windows (lo | hi << 16) of one pass along rows (axis 0) / columns (1)."""
+    out = np.empty((H, W), np.uint32)
+    _check(load_library().dts_debug_read_windows(ctx, pass_index, axis, out.ctypes.data), "dts_debug_read_windows")
+    return out
 
 
 def dts_solve_ex(ctx: int, target, confidence, lam: float, iterations: int, out, stream=None,
@@ -327,9 +362,14 @@ def dts_create_band(guide_with_halo, H_total: int, row0: int, rows: int, sigma_s
 class Solver:
     """Thin RAII wrapper: ``Solver(guide, sigma_s, sigma_r, N).solve(t, c, lam, iters)``."""
 
-    def __init__(self, guide, sigma_s: float, sigma_r: float, filter_passes: int = 3, stream=None):
+    def __init__(self, guide, sigma_s: float, sigma_r: float, filter_passes: int = 3, stream=None,
+                 filter: int = DTS_FILTER_RF, radius_scale: float = 0.0):
         self.H, self.W = int(guide.shape[0]), int(guide.shape[1])
-        self.ctx = dts_create(guide, sigma_s, sigma_r, filter_passes, stream)
+        self.filter = filter
+        if filter == DTS_FILTER_RF:
+            self.ctx = dts_create(guide, sigma_s, sigma_r, filter_passes, stream)
+        else:
+            self.ctx = dts_create_ex(guide, sigma_s, sigma_r, filter_passes, filter, radius_scale, stream)
 
     def solve(self, target, confidence, lam: float, iterations: int, out=None, stream=None, **opts):
         if out is None:
@@ -363,6 +403,9 @@ class Solver:
 
     def read(self, which: int) -> np.ndarray:
         return dts_debug_read(self.ctx, which, self.H, self.W)
+
+    def windows(self, pass_index: int, axis: int) -> np.ndarray:
+        return dts_debug_read_windows(self.ctx, pass_index, axis, self.H, self.W)
 
     def close(self):
         if self.ctx:

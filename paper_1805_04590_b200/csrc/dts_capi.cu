@@ -95,6 +95,12 @@ struct dts_ctx {
     float* dy = nullptr;
     float* S = nullptr;
     float* Sy = nullptr;  // column support factor when the cluster kernel computes it (S then holds s_x)
+    // box filter (dts_create_ex, DTS_FILTER_BOX): dx / dy hold the fixed-point increments q,
+    // win the packed windows (planes 2i: rows, 2i + 1: columns, pass i), S the window counts
+    int filter = DTS_FILTER_RF;
+    uint32_t* win = nullptr;
+    std::vector<BoxPlan> bplan;
+    float* X2 = nullptr;  // second state buffer (box passes are out of place)
     // solver state (allocated for ct_cap target channels)
     int ct_cap = 0;
     float* Z = nullptr;
@@ -131,11 +137,12 @@ namespace {
 
 enum Family {
     F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
-    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_FILL, F_COUNT
+    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_FILL, F_BOX_PREP, F_BOX_ROW, F_BOX_COL, F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
-                                     "rank_compose", "row_update", "confidence", "stereo_update", "link_fill"};
+                                     "rank_compose", "row_update", "confidence", "stereo_update", "link_fill",
+                                     "box_windows", "box_row", "box_col"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -206,7 +213,7 @@ dts_status run_launch(dts_ctx* ctx, int fam, double bytes, cudaStream_t s, F&& l
 }
 
 void free_solver_state(dts_ctx* ctx, cudaStream_t s) {
-    for (float** p : {&ctx->Z, &ctx->T, &ctx->X, &ctx->chat}) {
+    for (float** p : {&ctx->Z, &ctx->T, &ctx->X, &ctx->chat, &ctx->X2}) {
         if (*p) cudaFreeAsync(*p, s);
         *p = nullptr;
     }
@@ -222,6 +229,8 @@ dts_status ensure_solver_state(dts_ctx* ctx, int Ct, cudaStream_t s) {
     if ((e = cudaMallocAsync((void**)&ctx->T, plane * Ct, s)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaMallocAsync((void**)&ctx->X, plane * Ct, s)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaMallocAsync((void**)&ctx->chat, plane, s)) != cudaSuccess) return cuda_fail(e);
+    if (ctx->filter == DTS_FILTER_BOX && (e = cudaMallocAsync((void**)&ctx->X2, plane * Ct, s)) != cudaSuccess)
+        return cuda_fail(e);
     ctx->ct_cap = Ct;
     return DTS_OK;
 }
@@ -599,6 +608,141 @@ dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float
     return create_impl(guide, H, 0, H, W, C, sigma_s, sigma_r, filter_passes, nullptr, stream, out_ctx);
 }
 
+// Box-filter context (reading R25): fixed-point increments, windows of every pass and the
+// support, all computed once here.
+static dts_status create_box_impl(const float* guide, int64_t H, int64_t W, int32_t C, float sigma_s, float sigma_r,
+                                  int32_t filter_passes, double radius_scale, void* stream, dts_ctx** out_ctx) {
+    if (!out_ctx || !guide) return DTS_E_ARG;
+    *out_ctx = nullptr;
+    if (H < 1 || W < 1 || C < 1) return DTS_E_ARG;
+    if (!finite_pos(sigma_s) || !finite_pos(sigma_r)) return DTS_E_ARG;
+    if (!(radius_scale >= 0.0) || !std::isfinite(radius_scale)) return DTS_E_ARG;
+    if (filter_passes < 1 || filter_passes > 16) return DTS_E_ARG;
+    if (W > ((int64_t)1 << 24) || H > ((int64_t)1 << 30) || C > 4096) return DTS_E_SHAPE;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int device = 0;
+    cudaError_t e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return cuda_fail(e);
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    if (major < 10) {
+        g_last_error = "device is not sm_100-class";
+        return DTS_E_CUDA;
+    }
+    dts_ctx* ctx = new dts_ctx();
+    ctx->filter = DTS_FILTER_BOX;
+    ctx->device = device;
+    ctx->H_total = H;
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->g.H = H;
+    ctx->g.W = W;
+    ctx->g.pitch = (W + 31) / 32 * 32;
+    ctx->g.plane = H * ctx->g.pitch;
+    ctx->C = C;
+    ctx->sigma_s = sigma_s;
+    ctx->sigma_r = sigma_r;
+    ctx->N = filter_passes;
+    // radii in fixed point, R = floor(radius_scale * sigma * 2^16), sigma_i of R5 (the same
+    // double expressions as the oracle's O2 / O10)
+    std::vector<long long> R;
+    const double denom = std::sqrt(std::pow(4.0, (double)filter_passes) - 1.0);
+    for (int i = 1; i <= filter_passes; ++i) {
+        const double sig = (double)sigma_s * std::sqrt(3.0) * std::pow(2.0, (double)(filter_passes - i)) / denom;
+        R.push_back((long long)std::floor(radius_scale * sig * 65536.0));
+    }
+    R.push_back((long long)std::floor(radius_scale * (double)sigma_s * 65536.0));
+    for (long long r : R)
+        if ((r >> 16) > 65535) {  // window offsets are stored as 16-bit
+            delete ctx;
+            g_last_error = "box radius above 65535 pixels";
+            return DTS_E_SHAPE;
+        }
+    for (int i = 0; i < filter_passes; ++i) {
+        BoxPlan bp;
+        if (plan_box(ctx->g, R[i], ctx->num_sms, &bp) != cudaSuccess) {
+            cudaGetLastError();
+            delete ctx;
+            g_last_error = "box radius too large for the column tile";
+            return DTS_E_SHAPE;
+        }
+        ctx->bplan.push_back(bp);
+    }
+    const PtrKind gk = classify(guide, device);
+    if (gk == PTR_BAD) {
+        delete ctx;
+        return DTS_E_ARG;
+    }
+    const size_t plane = (size_t)ctx->g.plane * sizeof(float);
+    dts_status st = DTS_OK;
+    if ((e = cudaMallocAsync((void**)&ctx->dx_base, plane, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->dy_base, plane, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->S, plane, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->win, plane * 2 * filter_passes, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&ctx->counters, 2 * sizeof(unsigned int), s)) != cudaSuccess) {
+        st = cuda_fail(e);
+        dts_destroy(ctx);
+        return st;
+    }
+    ctx->dx = ctx->dx_base;
+    ctx->dy = ctx->dy_base;
+    const float* gdev = guide;
+    float* gstage = nullptr;
+    const size_t gbytes = (size_t)H * W * C * sizeof(float);
+    if (gk == PTR_HOST) {
+        if ((e = cudaMallocAsync((void**)&gstage, gbytes, s)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(gstage, guide, gbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
+            st = cuda_fail(e);
+            if (gstage) cudaFreeAsync(gstage, s);
+            dts_destroy(ctx);
+            return st;
+        }
+        gdev = gstage;
+    }
+    const float ratio = sigma_s / sigma_r;  // R25: k2 in fp32, as the oracle forms it
+    const float k2 = ratio * ratio;
+    uint32_t* qx = reinterpret_cast<uint32_t*>(ctx->dx);
+    uint32_t* qy = reinterpret_cast<uint32_t*>(ctx->dy);
+    const double px = (double)H * W;
+    st = run_launch(ctx, F_BOX_PREP, px * (4.0 * C + 8.0), s,
+                    [&] { return launch_box_increments(gdev, C, k2, ctx->g, qx, qy, s); });
+    if (st == DTS_OK)
+        st = run_launch(ctx, F_BOX_PREP, px * (8.0 + 8.0 * filter_passes + 4.0), s, [&] {
+            return launch_box_windows(qx, qy, ctx->g, R.data(), (int)R.size(), ctx->win, ctx->S, s);
+        });
+    if (gstage) {
+        cudaFreeAsync(gstage, s);
+        if (st == DTS_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess) st = cuda_fail(e);
+    }
+    if (st != DTS_OK) {
+        dts_destroy(ctx);
+        return st;
+    }
+    ctx->last_stream = s;
+    *out_ctx = ctx;
+    return DTS_OK;
+}
+
+dts_status dts_create_ex(const float* guide, int64_t H, int64_t W, int32_t C, float sigma_s, float sigma_r,
+                         int32_t filter_passes, const dts_create_opts* opts, void* stream, dts_ctx** out_ctx) {
+    const int filter = opts ? opts->filter : DTS_FILTER_RF;
+    if (filter == DTS_FILTER_RF)
+        return create_impl(guide, H, 0, H, W, C, sigma_s, sigma_r, filter_passes, nullptr, stream, out_ctx);
+    if (filter != DTS_FILTER_BOX) return DTS_E_ARG;
+    if (opts->radius_scale < 0.f) return DTS_E_ARG;
+    const double rs = (opts->radius_scale == 0.f) ? std::sqrt(3.0) : (double)opts->radius_scale;
+    return create_box_impl(guide, H, W, C, sigma_s, sigma_r, filter_passes, rs, stream, out_ctx);
+}
+
+dts_status dts_debug_read_windows(dts_ctx* ctx, int32_t pass, int32_t axis, uint32_t* host_out) {
+    if (!ctx || !host_out || ctx->filter != DTS_FILTER_BOX) return DTS_E_ARG;
+    if (pass < 0 || pass >= ctx->N || (axis != 0 && axis != 1)) return DTS_E_ARG;
+    const uint32_t* src = ctx->win + (size_t)(2 * pass + axis) * ctx->g.plane;
+    cudaError_t e = cudaMemcpy2DAsync(host_out, ctx->g.W * sizeof(uint32_t), src, ctx->g.pitch * sizeof(uint32_t),
+                                      ctx->g.W * sizeof(uint32_t), ctx->g.H, cudaMemcpyDeviceToHost, ctx->last_stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->last_stream);
+    return e == cudaSuccess ? DTS_OK : cuda_fail(e);
+}
+
 dts_status dts_create_band(const float* guide_with_halo, int64_t H_total, int64_t row0, int64_t rows, int64_t W,
                            int32_t C, float sigma_s, float sigma_r, int32_t filter_passes, dts_comm* comm,
                            void* stream, dts_ctx** out_ctx) {
@@ -662,13 +806,14 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->last_stream = s;
 
-    RowPlan rp;
-    ColPlan cpf, cpu;
-    if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess) return DTS_E_SHAPE;
+    const bool is_box = ctx->filter == DTS_FILTER_BOX;
+    RowPlan rp{};
+    ColPlan cpf{}, cpu{};
+    if (!is_box && plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess) return DTS_E_SHAPE;
     // column kernel: the cluster kernel (k_colc.cu) by default; DTS_COL=stream selects the
     // TMEM-lagged decoupled kernel (k_colv.cu, experimental), DTS_COL=legacy forces the
     // cluster / band-tuple kernels with the separate update kernel
-    const char* colsel = std::getenv("DTS_COL");
+    const char* colsel = is_box ? nullptr : std::getenv("DTS_COL");
     // streaming path: TMEM-lagged column kernel (FILTER) + the Eq. (3) step fused into the
     // next iteration's first row pass (and one closing update kernel)
     const bool stream_ok = !ctx->comm && colsel && std::strcmp(colsel, "stream") == 0 &&
@@ -677,7 +822,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     const bool twop_ok = !stream_ok && !ctx->comm && colsel && std::strcmp(colsel, "2p") == 0 &&
                          plan_col_2p(g, Ct, MODE_FILTER, ctx->num_sms, &cpf) == cudaSuccess;
     if (twop_ok) cpu = cpf;  // FILTER column passes + the streaming update kernel (K4b)
-    if (!stream_ok && !twop_ok) {
+    if (!is_box && !stream_ok && !twop_ok) {
         cudaGetLastError();
         if ((ctx->comm ? plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)
                        : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess ||
@@ -735,6 +880,29 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
             if (st != DTS_OK) return st;
             const double row_bytes = px * (8.0 * Ct + 4);
             const double upd_bytes = px * (16.0 * Ct + 8);  // X, d, Z, T, chat in; Z out
+            if (is_box) {  // R25: N x (box rows, box columns), ping-pong X2 <-> X, then Eq. (3)
+                for (int k = 0; k < iterations; ++k) {
+                    for (int i = 0; i < ctx->N; ++i) {
+                        const BoxPlan& bp = ctx->bplan[i];
+                        const uint32_t* wx = ctx->win + (size_t)(2 * i) * g.plane;
+                        const uint32_t* wy = ctx->win + (size_t)(2 * i + 1) * g.plane;
+                        const float* in = (i == 0) ? ctx->Z : ctx->X;
+                        st = run_launch(ctx, F_BOX_ROW, row_bytes, s,
+                                        [&] { return launch_box_row(bp, g, Ct, in, ctx->X2, wx, s); });
+                        if (st != DTS_OK) return st;
+                        st = run_launch(ctx, F_BOX_COL, row_bytes, s,
+                                        [&] { return launch_box_col(bp, g, Ct, ctx->X2, ctx->X, wy, s); });
+                        if (st != DTS_OK) return st;
+                    }
+                    float* ohwc = (k + 1 == iterations) ? o_d : nullptr;
+                    st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
+                        return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, ohwc,
+                                             ctx->num_sms, s);
+                    });
+                    if (st != DTS_OK) return st;
+                }
+                return DTS_OK;
+            }
             if (stream_ok) {
                 UpdateArgs u;
                 u.Z = ctx->Z;
@@ -833,7 +1001,8 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
             std::lock_guard<std::mutex> lk(P.mu);
             prof_on = P.on;
         }
-        const bool use_graph = !any_host && !prof_on && !ctx->comm && cpf.kind == 1 && cpu.kind == 1 && !stream_ok &&
+        const bool use_graph = !any_host && !prof_on && !ctx->comm && (is_box || (cpf.kind == 1 && cpu.kind == 1)) &&
+                               !stream_ok &&
                                !twop_ok && !std::getenv("DTS_NO_GRAPH");
         std::vector<uintptr_t> key;
         if (use_graph) {
@@ -893,6 +1062,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
 
 dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, float* conf_out, float* var_out,
                           void* stream) {
+    if (ctx && ctx->filter != DTS_FILTER_RF) return DTS_E_ARG;  // recursive-filter contexts only
     if (!ctx || !target || !conf_out) return DTS_E_ARG;
     if (!std::isfinite(sigma_c) || !(sigma_c > 0.f)) return DTS_E_ARG;
     if (ctx->comm) return DTS_E_SHAPE;  // row-band contexts: not supported (yet)
@@ -963,6 +1133,7 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
 dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* confidence, float lambda,
                             int32_t iterations, float* out, const float* left, const float* right, float gamma,
                             float eps, void* stream) {
+    if (ctx && ctx->filter != DTS_FILTER_RF) return DTS_E_ARG;  // recursive-filter contexts only
     if (!ctx || !target || !confidence || !out || !left || !right) return DTS_E_ARG;
     if (iterations < 0) return DTS_E_ARG;
     const float step = 0.99f;
@@ -1081,6 +1252,7 @@ void dts_destroy(dts_ctx* ctx) {
     if (ctx->flags) cudaFreeAsync(ctx->flags, s);
     if (ctx->v_tuples) cudaFreeAsync(ctx->v_tuples, s);
     if (ctx->v_flags) cudaFreeAsync(ctx->v_flags, s);
+    if (ctx->win) cudaFreeAsync(ctx->win, s);
     if (ctx->graph_exec) {  // a replay may still be in flight on s
         cudaStreamSynchronize(s);
         cudaGraphExecDestroy(ctx->graph_exec);

@@ -125,4 +125,26 @@ cudaError_t launch_prologue(const float* target, const float* conf, int Ct, cons
 cudaError_t launch_check_inputs(const float* target, const float* conf, int Ct, int64_t H, int64_t W,
                                 unsigned int* counters, cudaStream_t s);
 
+// Box (normalised-convolution) variant (k_box.cu, reading R25).
+// K_B1: fixed-point DT increments q (uint32) to the left / upper neighbour.
+cudaError_t launch_box_increments(const float* guide, int C, float k2, const Geometry& g, uint32_t* qx, uint32_t* qy,
+                                  cudaStream_t s);
+// K_B2: windows of nR - 1 passes (R[0..nR-2]) packed lo | hi << 16 into win planes 2i (rows)
+// and 2i + 1 (columns), and the support S = count_x * count_y at R[nR - 1].
+cudaError_t launch_box_windows(const uint32_t* qx, const uint32_t* qy, const Geometry& g, const long long* R, int nR,
+                               uint32_t* win, float* S, cudaStream_t s);
+struct BoxPlan {
+    int hx, hy;                                   // halo (max window half-width) per axis
+    int row_seg, row_nseg, row_lpad, row_threads, row_grid;
+    size_t row_smem;
+    int col_seg, col_nseg, col_ntc, col_lpad, col_grid;
+    size_t col_smem;
+};
+cudaError_t plan_box(const Geometry& g, long long R, int num_sms, BoxPlan* plan);
+// K_B3 / K_B4: one box pass along rows / columns, in -> out (out of place).
+cudaError_t launch_box_row(const BoxPlan& plan, const Geometry& g, int Ct, const float* in, float* out,
+                           const uint32_t* win, cudaStream_t s);
+cudaError_t launch_box_col(const BoxPlan& plan, const Geometry& g, int Ct, const float* in, float* out,
+                           const uint32_t* win, cudaStream_t s);
+
 }  // namespace dts

@@ -1,0 +1,397 @@
+// k_box.cu -- box (normalised-convolution) variant of the edge-aware mean.
+//
+// P:243-245 define the mean with the indicator W_ij = delta{DT(z_i) - DT(z_j) <= r}; reading
+// R25 takes it as the normalised box window on the guide's domain-transform axis,
+//     zbar_i = (1/|N_i|) sum_{j in N_i} z_j,   N_i = { j : |T_j - T_i| <= r },
+// N passes of rows then columns with r_i = radius_scale * sigma_i, and the support
+// S = |N^x| |N^y| at r = radius_scale * sigma_s.
+//
+// Window membership is an integer decision: the increment d is evaluated in IEEE fp32 in
+// the fixed order of R25 (no contraction, correctly rounded sqrt) and the DT axis is held
+// in fixed point, q = rn(d * 2^16) (capped at 2^30), R = floor(r * 2^16); then the windows
+// are exact integers.  They depend only on the guide, so dts_create computes them once:
+//   K_B1 k_box_increments  q between each pixel and its left / upper neighbour
+//   K_B2 k_box_windows     one outward walk per pixel and axis records the window edges of
+//                          every radius (the radii are nested); packs lo | hi << 16 per pass
+//                          and axis, and writes S = count_x * count_y
+// Per pass (every iteration):
+//   K_B3 k_box_row         a warp per row segment: the segment and its halo are staged in
+//                          shared memory, an fp32 exclusive prefix inside 32-element blocks
+//                          plus an fp64 prefix of the block totals give E(k) = sum_{j<k} x_j;
+//                          zbar = (E(hi + 1) - E(lo)) / (hi - lo + 1)
+//   K_B4 k_box_col         the same over a 32-column x (SEG + 2h)-row tile of a CTA (lane =
+//                          column, coalesced 128-B rows)
+// The halo makes the passes out of place (the solver ping-pongs two state buffers).
+// Algorithmic bytes per pixel and pass: 4 C_t read + 4 window + 4 C_t write.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "dts_launch.h"
+
+namespace dts {
+namespace box {
+
+constexpr uint32_t QMAX = 1u << 30;
+
+// R25: d = sqrt(1 + k2 * sum_k (I_k(p) - I_k(p'))^2) in fp32, this order, no FMA
+__device__ __forceinline__ uint32_t increment(const float* __restrict__ a, const float* __restrict__ b, int C,
+                                              float k2) {
+    float s = 0.0f;
+    for (int k = 0; k < C; ++k) {
+        const float diff = __fsub_rn(__ldg(a + k), __ldg(b + k));
+        s = __fadd_rn(s, __fmul_rn(diff, diff));
+    }
+    const float v = __fadd_rn(1.0f, __fmul_rn(k2, s));
+    const float d = __fsqrt_rn(v);
+    const long long q = __float2ll_rn(__fmul_rn(d, 65536.0f));
+    return q > (long long)QMAX ? QMAX : (uint32_t)q;
+}
+
+__global__ void __launch_bounds__(256) k_box_increments(const float* __restrict__ guide, int C, float k2, int64_t H,
+                                                        int64_t W, int64_t pitch, uint32_t* __restrict__ qx,
+                                                        uint32_t* __restrict__ qy) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = blockIdx.y;
+    if (c >= W || r >= H) return;
+    const float* p = guide + (r * W + c) * C;
+    qx[r * pitch + c] = c == 0 ? 0u : increment(p, p - C, C, k2);
+    qy[r * pitch + c] = r == 0 ? 0u : increment(p, p - W * C, C, k2);
+}
+
+constexpr int MAXR = 17;  // N <= 16 passes + the support radius
+struct Radii {
+    long long R[MAXR];  // R[0..N-1]: passes, R[N]: support
+    int n;
+    long long Rmax;
+};
+
+// walk from position i along a line (q at stride) in one direction; off[k] = number of
+// steps whose cumulative distance stays <= R[k]
+template <int DIR>
+__device__ __forceinline__ void walk(const uint32_t* __restrict__ q, int64_t stride, int64_t i, int64_t n,
+                                     const Radii& rd, int* off) {
+#pragma unroll 1
+    for (int k = 0; k < rd.n; ++k) off[k] = 0;
+    long long dist = 0;
+    int steps = 0;
+    int64_t j = i;
+#pragma unroll 1
+    while (DIR < 0 ? j > 0 : j + 1 < n) {
+        const long long nd = dist + (long long)__ldg(q + (DIR < 0 ? j : j + 1) * stride);
+        if (nd > rd.Rmax) break;
+        dist = nd;
+        ++steps;
+        j += DIR;
+#pragma unroll 1
+        for (int k = 0; k < rd.n; ++k)
+            if (dist <= rd.R[k]) off[k] = steps;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_box_windows(const uint32_t* __restrict__ qx, const uint32_t* __restrict__ qy,
+                                                     int64_t H, int64_t W, int64_t pitch, int64_t plane, Radii rd,
+                                                     uint32_t* __restrict__ win, float* __restrict__ S) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = blockIdx.y;
+    if (c >= W || r >= H) return;
+    int lo[MAXR], hi[MAXR];
+    const int np = rd.n - 1;
+    // rows
+    walk<-1>(qx + r * pitch, 1, c, W, rd, lo);
+    walk<+1>(qx + r * pitch, 1, c, W, rd, hi);
+#pragma unroll 1
+    for (int k = 0; k < np; ++k) win[(2 * k) * plane + r * pitch + c] = (uint32_t)lo[k] | ((uint32_t)hi[k] << 16);
+    const float cx = (float)(lo[np] + hi[np] + 1);
+    // columns
+    walk<-1>(qy + c, pitch, r, H, rd, lo);
+    walk<+1>(qy + c, pitch, r, H, rd, hi);
+#pragma unroll 1
+    for (int k = 0; k < np; ++k) win[(2 * k + 1) * plane + r * pitch + c] = (uint32_t)lo[k] | ((uint32_t)hi[k] << 16);
+    S[r * pitch + c] = cx * (float)(lo[np] + hi[np] + 1);
+}
+
+__device__ __forceinline__ float warp_incl_scan(float v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// window mean from the staged prefix: E(k) = Pb[k >> 5] + pe[k]
+template <int STRIDE>
+__device__ __forceinline__ float window_mean(const float* pe, const double* pb, int li, int hi1, int cnt) {
+    const double sum = (pb[(hi1 >> 5) * STRIDE] - pb[(li >> 5) * STRIDE]) +
+                       ((double)pe[hi1 * STRIDE] - (double)pe[li * STRIDE]);
+    return __fdiv_rn((float)sum, (float)cnt);
+}
+
+// shared memory of one warp of k_box_row: pe[lpad] floats + pb[lpad / 32] doubles, 16-B multiple
+__host__ __device__ constexpr size_t row_warp_bytes(int lpad) {
+    return ((size_t)lpad * 4 + (size_t)(lpad / 32) * 8 + 15) & ~(size_t)15;
+}
+
+struct RowArgs {
+    const float* in;
+    float* out;
+    const uint32_t* win;
+    int64_t H, W, pitch, plane;
+    int Ct, h, seg, nseg, lpad;  // lpad: staged elements per warp (multiple of 32) + 32
+};
+
+// K_B3: a warp per (row, segment, channel-loop).  Shared memory per warp: pe[lpad] floats
+// and pb[lpad / 32] doubles.
+__global__ void __launch_bounds__(256) k_box_row(RowArgs p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const size_t per_warp = row_warp_bytes(p.lpad);
+    float* pe = reinterpret_cast<float*>(smem_raw + per_warp * wid);
+    double* pb = reinterpret_cast<double*>(smem_raw + per_warp * wid + (size_t)p.lpad * 4);
+    const int64_t ntask = p.H * p.nseg;
+    for (int64_t task = (int64_t)blockIdx.x * nw + wid; task < ntask; task += (int64_t)gridDim.x * nw) {
+        const int64_t r = task / p.nseg;
+        const int64_t c0 = (task - r * p.nseg) * p.seg;
+        const int64_t c1 = c0 + p.seg < p.W ? c0 + p.seg : p.W;
+        const int64_t a = c0 - p.h > 0 ? c0 - p.h : 0;
+        const int64_t b = c1 + p.h < p.W ? c1 + p.h : p.W;
+        const int64_t a4 = a & ~(int64_t)3;  // 16-B aligned start (rows are 128-B aligned)
+        const int L = (int)(b - a4);
+        const int nblk = (L + 31) >> 5;
+        const uint32_t* wrow = p.win + r * p.pitch;
+        for (int ch = 0; ch < p.Ct; ++ch) {
+            const float* xr = p.in + ch * p.plane + r * p.pitch;
+            // stage [a4, a4 + 32 nblk) with zeros outside [a, b)
+            for (int e = lane * 4; e < nblk * 32; e += 128) {
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                const int64_t col = a4 + e;
+                if (col < b) v = __ldg(reinterpret_cast<const float4*>(xr + col));
+                if (col < a) v.x = 0.f;
+                if (col + 1 < a || col + 1 >= b) v.y = 0.f;
+                if (col + 2 < a || col + 2 >= b) v.z = 0.f;
+                if (col + 3 < a || col + 3 >= b) v.w = 0.f;
+                *reinterpret_cast<float4*>(pe + e) = v;
+            }
+            __syncwarp();
+            // exclusive prefix inside each 32-block (fp32) + block prefix (fp64)
+            double run = 0.0;
+            for (int j = 0; j < nblk; ++j) {
+                const float v = pe[j * 32 + lane];
+                const float inc = warp_incl_scan(v, lane);
+                pe[j * 32 + lane] = inc - v;
+                if (lane == 0) pb[j] = run;
+                run += (double)__shfl_sync(0xffffffffu, inc, 31);
+            }
+            pe[nblk * 32 + lane] = 0.f;
+            if (lane == 0) pb[nblk] = run;
+            __syncwarp();
+            float* orow = p.out + ch * p.plane + r * p.pitch;
+            for (int64_t k = c0 + lane; k < c1; k += 32) {
+                const uint32_t w = __ldg(wrow + k);
+                const int lo = (int)(w & 0xffffu), hi = (int)(w >> 16);
+                const int li = (int)(k - lo - a4), hi1 = (int)(k + hi + 1 - a4);
+                orow[k] = window_mean<1>(pe, pb, li, hi1, lo + hi + 1);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+struct ColArgs {
+    const float* in;
+    float* out;
+    const uint32_t* win;
+    int64_t H, W, pitch, plane;
+    int Ct, h, seg, nseg, ntc, lpad;  // lpad: staged rows (multiple of 32) + 32
+};
+
+// K_B4: a CTA per (32-column tile, row segment); lane = column.  Shared memory:
+// xs[lpad][32] floats (row-major, one 128-B row per image row) + pb[lpad/32][32] doubles.
+__global__ void __launch_bounds__(256) k_box_col(ColArgs p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* xs = reinterpret_cast<float*>(smem_raw);
+    double* pb = reinterpret_cast<double*>(smem_raw + (size_t)p.lpad * 128);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t ntask = (int64_t)p.ntc * p.nseg;
+    for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
+        const int64_t tc = task % p.ntc;  // consecutive CTAs take neighbouring column tiles
+        const int64_t r0 = (task / p.ntc) * p.seg;
+        const int64_t r1 = r0 + p.seg < p.H ? r0 + p.seg : p.H;
+        const int64_t c0 = tc * 32;
+        const int64_t a = r0 - p.h > 0 ? r0 - p.h : 0;
+        const int64_t b = r1 + p.h < p.H ? r1 + p.h : p.H;
+        const int L = (int)(b - a);
+        const int nblk = (L + 31) >> 5;
+        const uint32_t* wt = p.win + c0 + lane;
+        for (int ch = 0; ch < p.Ct; ++ch) {
+            const float* xt = p.in + ch * p.plane + c0;
+            // stage rows [a, a + 32 nblk + 32): 8 float4 per row, zeros past b
+            for (int e = threadIdx.x; e < (nblk + 1) * 32 * 8; e += blockDim.x) {
+                const int row = e >> 3, q4 = (e & 7) * 4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (a + row < b) v = __ldg(reinterpret_cast<const float4*>(xt + (a + row) * p.pitch + q4));
+                *reinterpret_cast<float4*>(xs + row * 32 + q4) = v;
+            }
+            __syncthreads();
+            // exclusive prefix of each 32-row block of every column (fp32), block totals
+            for (int j = wid; j < nblk; j += nw) {
+                float run = 0.f;
+                float* col = xs + j * 32 * 32 + lane;
+#pragma unroll 8
+                for (int k = 0; k < 32; ++k) {
+                    const float v = col[k * 32];
+                    col[k * 32] = run;
+                    run += v;
+                }
+                pb[j * 32 + lane] = (double)run;
+            }
+            __syncthreads();
+            if (wid == 0) {  // exclusive prefix of the block totals (fp64)
+                double run = 0.0;
+                for (int j = 0; j < nblk; ++j) {
+                    const double t = pb[j * 32 + lane];
+                    pb[j * 32 + lane] = run;
+                    run += t;
+                }
+                pb[nblk * 32 + lane] = run;  // row nblk*32 of xs is zero (staged)
+            }
+            __syncthreads();
+            float* ot = p.out + ch * p.plane + c0 + lane;
+            if (c0 + lane < p.W) {
+                for (int64_t k = r0 + wid; k < r1; k += nw) {
+                    const uint32_t w = __ldg(wt + k * p.pitch);
+                    const int lo = (int)(w & 0xffffu), hi = (int)(w >> 16);
+                    const int li = (int)(k - lo - a), hi1 = (int)(k + hi + 1 - a);
+                    ot[k * p.pitch] = window_mean<32>(xs + lane, pb + lane, li, hi1, lo + hi + 1);
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+
+static int occupancy(const void* fn, int threads, size_t smem) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+}  // namespace box
+
+cudaError_t launch_box_increments(const float* guide, int C, float k2, const Geometry& g, uint32_t* qx, uint32_t* qy,
+                                  cudaStream_t s) {
+    dim3 grid((unsigned)((g.W + 255) / 256), (unsigned)g.H);
+    box::k_box_increments<<<grid, 256, 0, s>>>(guide, C, k2, g.H, g.W, g.pitch, qx, qy);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_box_windows(const uint32_t* qx, const uint32_t* qy, const Geometry& g, const long long* R, int nR,
+                               uint32_t* win, float* S, cudaStream_t s) {
+    if (nR < 2 || nR > box::MAXR) return cudaErrorInvalidValue;
+    box::Radii rd = {};
+    rd.n = nR;
+    rd.Rmax = 0;
+    for (int k = 0; k < nR; ++k) {
+        rd.R[k] = R[k];
+        if (R[k] > rd.Rmax) rd.Rmax = R[k];
+    }
+    dim3 grid((unsigned)((g.W + 255) / 256), (unsigned)g.H);
+    box::k_box_windows<<<grid, 256, 0, s>>>(qx, qy, g.H, g.W, g.pitch, g.plane, rd, win, S);
+    return cudaGetLastError();
+}
+
+cudaError_t plan_box(const Geometry& g, long long R, int num_sms, BoxPlan* plan) {
+    const long long hmax = R >> 16;  // every step is >= 2^16 (d >= 1): no window is wider
+    plan->hx = (int)(hmax < g.W - 1 ? hmax : g.W - 1);
+    plan->hy = (int)(hmax < g.H - 1 ? hmax : g.H - 1);
+    // rows: a warp per segment of <= 2048 outputs plus the halo
+    plan->row_seg = (int)(g.W < 2048 ? g.W : 2048);
+    plan->row_nseg = (int)((g.W + plan->row_seg - 1) / plan->row_seg);
+    long long lrow = (long long)plan->row_seg + 2LL * plan->hx + 3;
+    if (lrow > g.W + 3) lrow = g.W + 3;
+    plan->row_lpad = (int)((lrow + 31) / 32 * 32 + 32);
+    const size_t pw = box::row_warp_bytes(plan->row_lpad);
+    if (pw > 200 * 1024) return cudaErrorInvalidValue;
+    int warps = (int)((110 * 1024) / pw);
+    warps = warps < 1 ? 1 : warps > 8 ? 8 : warps;
+    plan->row_threads = warps * 32;
+    plan->row_smem = pw * warps;
+    // the attribute is per function, shared by the plans of all passes: set it to the
+    // opt-in maximum once, so that no plan lowers another's limit
+    int optin = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+    if (e != cudaSuccess) return e;
+    if (plan->row_smem > (size_t)optin) return cudaErrorInvalidValue;
+    const void* frow = reinterpret_cast<const void*>(box::k_box_row);
+    if ((e = cudaFuncSetAttribute(frow, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess) return e;
+    const int orow = box::occupancy(frow, plan->row_threads, plan->row_smem);
+    if (orow < 1) return cudaErrorInvalidValue;
+    const long long rtasks = (g.H * plan->row_nseg + warps - 1) / warps;
+    plan->row_grid = (int)(rtasks < (long long)num_sms * orow ? rtasks : (long long)num_sms * orow);
+    // columns: a CTA per 32-column tile x segment, ~768 staged rows
+    long long seg = (736 - 2LL * plan->hy) / 32 * 32;
+    if (seg < 32) seg = 32;
+    if (seg > g.H) seg = g.H;
+    plan->col_seg = (int)seg;
+    plan->col_nseg = (int)((g.H + seg - 1) / seg);
+    plan->col_ntc = (int)((g.W + 31) / 32);
+    long long lcol = seg + 2LL * plan->hy;
+    if (lcol > g.H) lcol = g.H;
+    plan->col_lpad = (int)((lcol + 31) / 32 * 32 + 32);
+    plan->col_smem = (size_t)plan->col_lpad * 128 + (size_t)plan->col_lpad / 32 * 32 * 8;
+    if (plan->col_smem > (size_t)optin) return cudaErrorInvalidValue;
+    const void* fcol = reinterpret_cast<const void*>(box::k_box_col);
+    if ((e = cudaFuncSetAttribute(fcol, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess) return e;
+    const int ocol = box::occupancy(fcol, 256, plan->col_smem);
+    if (ocol < 1) return cudaErrorInvalidValue;
+    const long long ctasks = (long long)plan->col_ntc * plan->col_nseg;
+    plan->col_grid = (int)(ctasks < (long long)num_sms * ocol ? ctasks : (long long)num_sms * ocol);
+    return cudaSuccess;
+}
+
+cudaError_t launch_box_row(const BoxPlan& plan, const Geometry& g, int Ct, const float* in, float* out,
+                           const uint32_t* win, cudaStream_t s) {
+    box::RowArgs a;
+    a.in = in;
+    a.out = out;
+    a.win = win;
+    a.H = g.H;
+    a.W = g.W;
+    a.pitch = g.pitch;
+    a.plane = g.plane;
+    a.Ct = Ct;
+    a.h = plan.hx;
+    a.seg = plan.row_seg;
+    a.nseg = plan.row_nseg;
+    a.lpad = plan.row_lpad;
+    box::k_box_row<<<plan.row_grid, plan.row_threads, plan.row_smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_box_col(const BoxPlan& plan, const Geometry& g, int Ct, const float* in, float* out,
+                           const uint32_t* win, cudaStream_t s) {
+    box::ColArgs a;
+    a.in = in;
+    a.out = out;
+    a.win = win;
+    a.H = g.H;
+    a.W = g.W;
+    a.pitch = g.pitch;
+    a.plane = g.plane;
+    a.Ct = Ct;
+    a.h = plan.hy;
+    a.seg = plan.col_seg;
+    a.nseg = plan.col_nseg;
+    a.ntc = plan.col_ntc;
+    a.lpad = plan.col_lpad;
+    box::k_box_col<<<plan.col_grid, 256, plan.col_smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace dts
