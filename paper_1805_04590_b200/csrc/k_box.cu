@@ -119,12 +119,14 @@ __device__ __forceinline__ float warp_incl_scan(float v, int lane) {
     return v;
 }
 
-// window mean from the staged prefix: E(k) = Pb[k >> 5] + pe[k]
+// window mean from the staged prefix E(k) = Pb[k >> 5] + pe[k] (pe: exclusive prefix inside
+// the 32-block, so pe = 0 at a block start; Pb: fp64 exclusive prefix of the block totals):
+// the whole-block part of the sum in fp64, rounded once, the in-block parts in fp32
 template <int STRIDE>
 __device__ __forceinline__ float window_mean(const float* pe, const double* pb, int li, int hi1, int cnt) {
-    const double sum = (pb[(hi1 >> 5) * STRIDE] - pb[(li >> 5) * STRIDE]) +
-                       ((double)pe[hi1 * STRIDE] - (double)pe[li * STRIDE]);
-    return __fdiv_rn((float)sum, (float)cnt);
+    const float whole = (float)(pb[(hi1 >> 5) * STRIDE] - pb[(li >> 5) * STRIDE]);
+    const float sum = whole + (pe[hi1 * STRIDE] - pe[li * STRIDE]);
+    return __fdividef(sum, (float)cnt);  // branch-free (<= 2 ulp)
 }
 
 // shared memory of one warp of k_box_row: pe[lpad] floats + pb[lpad / 32] doubles, 16-B multiple
@@ -137,11 +139,22 @@ struct RowArgs {
     float* out;
     const uint32_t* win;
     int64_t H, W, pitch, plane;
-    int Ct, h, seg, nseg, lpad;  // lpad: staged elements per warp (multiple of 32) + 32
+    int Ct, h, seg, nseg, lpad;  // lpad: staged floats per warp (multiple of 128, >= 32 (nblk + 1))
 };
 
-// K_B3: a warp per (row, segment, channel-loop).  Shared memory per warp: pe[lpad] floats
-// and pb[lpad / 32] doubles.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+constexpr int WB = 8;  // window loads in flight per lane
+
+// K_B3: a warp per (row, segment); channels loop inside.  Shared memory per warp: pe[lpad]
+// floats and pb[lpad / 32] doubles.  Staged values at or beyond b (pad columns, stale
+// shared memory) are never inside a window and enter only prefixes no window reads.
 __global__ void __launch_bounds__(256) k_box_row(RowArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -149,6 +162,7 @@ __global__ void __launch_bounds__(256) k_box_row(RowArgs p) {
     float* pe = reinterpret_cast<float*>(smem_raw + per_warp * wid);
     double* pb = reinterpret_cast<double*>(smem_raw + per_warp * wid + (size_t)p.lpad * 4);
     const int64_t ntask = p.H * p.nseg;
+    const int sub = lane & 7;
     for (int64_t task = (int64_t)blockIdx.x * nw + wid; task < ntask; task += (int64_t)gridDim.x * nw) {
         const int64_t r = task / p.nseg;
         const int64_t c0 = (task - r * p.nseg) * p.seg;
@@ -157,40 +171,59 @@ __global__ void __launch_bounds__(256) k_box_row(RowArgs p) {
         const int64_t b = c1 + p.h < p.W ? c1 + p.h : p.W;
         const int64_t a4 = a & ~(int64_t)3;  // 16-B aligned start (rows are 128-B aligned)
         const int L = (int)(b - a4);
-        const int nblk = (L + 31) >> 5;
-        const uint32_t* wrow = p.win + r * p.pitch;
+        const int L4 = (L + 3) & ~3;         // staged floats (a4 + L4 <= pitch)
+        const int nchunk = ((L >> 5) + 1 + 3) >> 2;  // 128-float chunks covering blocks 0..nblk
+        const int n = (int)(c1 - c0), k0l = (int)(c0 - a4);  // outputs, local index of the first
+        const uint32_t* wrow = p.win + r * p.pitch + c0;
         for (int ch = 0; ch < p.Ct; ++ch) {
-            const float* xr = p.in + ch * p.plane + r * p.pitch;
-            // stage [a4, a4 + 32 nblk) with zeros outside [a, b)
-            for (int e = lane * 4; e < nblk * 32; e += 128) {
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                const int64_t col = a4 + e;
-                if (col < b) v = __ldg(reinterpret_cast<const float4*>(xr + col));
-                if (col < a) v.x = 0.f;
-                if (col + 1 < a || col + 1 >= b) v.y = 0.f;
-                if (col + 2 < a || col + 2 >= b) v.z = 0.f;
-                if (col + 3 < a || col + 3 >= b) v.w = 0.f;
-                *reinterpret_cast<float4*>(pe + e) = v;
-            }
+            const float* xr = p.in + ch * p.plane + r * p.pitch + a4;
+            for (int e = lane * 4; e < L4; e += 128) cp_async16(pe + e, xr + e);
+            uint32_t w[WB];  // first window batch in flight during the scan
+#pragma unroll
+            for (int u = 0; u < WB; ++u) w[u] = (lane + 32 * u < n) ? __ldg(wrow + lane + 32 * u) : 0u;
+            cp_async_wait_all();
             __syncwarp();
-            // exclusive prefix inside each 32-block (fp32) + block prefix (fp64)
+            // exclusive prefix inside 32-blocks: lane holds 4 consecutive floats, 8 lanes a
+            // block (segmented shuffle scan); block totals -> fp64 exclusive prefix
             double run = 0.0;
-            for (int j = 0; j < nblk; ++j) {
-                const float v = pe[j * 32 + lane];
-                const float inc = warp_incl_scan(v, lane);
-                pe[j * 32 + lane] = inc - v;
-                if (lane == 0) pb[j] = run;
-                run += (double)__shfl_sync(0xffffffffu, inc, 31);
+            for (int c = 0; c < nchunk; ++c) {
+                float4 v = *reinterpret_cast<const float4*>(pe + c * 128 + lane * 4);
+                const float s1 = v.x + v.y, s2 = s1 + v.z, t = s2 + v.w;
+                float inc = t;
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) {
+                    const float nb = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (sub >= o) inc += nb;
+                }
+                float ex = __shfl_up_sync(0xffffffffu, inc, 1);
+                if (sub == 0) ex = 0.f;
+                *reinterpret_cast<float4*>(pe + c * 128 + lane * 4) = make_float4(ex, ex + v.x, ex + s1, ex + s2);
+                const float t0 = __shfl_sync(0xffffffffu, inc, 7), t1 = __shfl_sync(0xffffffffu, inc, 15);
+                const float t2 = __shfl_sync(0xffffffffu, inc, 23), t3 = __shfl_sync(0xffffffffu, inc, 31);
+                const double p1 = run + (double)t0, p2 = p1 + (double)t1, p3 = p2 + (double)t2;
+                if (lane < 4) pb[c * 4 + lane] = lane == 0 ? run : lane == 1 ? p1 : lane == 2 ? p2 : p3;
+                run = p3 + (double)t3;
             }
-            pe[nblk * 32 + lane] = 0.f;
-            if (lane == 0) pb[nblk] = run;
             __syncwarp();
-            float* orow = p.out + ch * p.plane + r * p.pitch;
-            for (int64_t k = c0 + lane; k < c1; k += 32) {
-                const uint32_t w = __ldg(wrow + k);
-                const int lo = (int)(w & 0xffffu), hi = (int)(w >> 16);
-                const int li = (int)(k - lo - a4), hi1 = (int)(k + hi + 1 - a4);
-                orow[k] = window_mean<1>(pe, pb, li, hi1, lo + hi + 1);
+            float* orow = p.out + ch * p.plane + r * p.pitch + c0;
+            for (int j0 = lane; j0 < n; j0 += 32 * WB) {
+                uint32_t wn[WB];  // next batch
+#pragma unroll
+                for (int u = 0; u < WB; ++u) {
+                    const int j = j0 + 32 * WB + 32 * u;
+                    wn[u] = (j < n) ? __ldg(wrow + j) : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < WB; ++u) {
+                    const int j = j0 + 32 * u;
+                    if (j < n) {
+                        const int lo = (int)(w[u] & 0xffffu), hi = (int)(w[u] >> 16);
+                        const int kl = k0l + j;
+                        orow[j] = window_mean<1>(pe, pb, kl - lo, kl + hi + 1, lo + hi + 1);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < WB; ++u) w[u] = wn[u];
             }
             __syncwarp();
         }
@@ -222,26 +255,37 @@ __global__ void __launch_bounds__(256) k_box_col(ColArgs p) {
         const int64_t b = r1 + p.h < p.H ? r1 + p.h : p.H;
         const int L = (int)(b - a);
         const int nblk = (L + 31) >> 5;
-        const uint32_t* wt = p.win + c0 + lane;
+        const int n = (int)(r1 - r0), k0l = (int)(r0 - a);
+        const bool col_ok = c0 + lane < p.W;
+        const uint32_t* wt = p.win + r0 * p.pitch + c0 + lane;
         for (int ch = 0; ch < p.Ct; ++ch) {
-            const float* xt = p.in + ch * p.plane + c0;
-            // stage rows [a, a + 32 nblk + 32): 8 float4 per row, zeros past b
-            for (int e = threadIdx.x; e < (nblk + 1) * 32 * 8; e += blockDim.x) {
+            const float* xt = p.in + ch * p.plane + a * p.pitch + c0;
+            // stage rows [a, b) (8 x 16 B per row); rows L..32 nblk - 1 are never read by a
+            // window; row 32 nblk (block start: exclusive prefix 0) closes the last block
+            for (int e = threadIdx.x; e < L * 8; e += blockDim.x) {
                 const int row = e >> 3, q4 = (e & 7) * 4;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (a + row < b) v = __ldg(reinterpret_cast<const float4*>(xt + (a + row) * p.pitch + q4));
-                *reinterpret_cast<float4*>(xs + row * 32 + q4) = v;
+                cp_async16(xs + row * 32 + q4, xt + (int64_t)row * p.pitch + q4);
             }
+            if (threadIdx.x < 32) xs[nblk * 32 * 32 + threadIdx.x] = 0.f;  // pe at row 32 nblk
+            uint32_t w[WB];  // first window batch in flight during the scan
+#pragma unroll
+            for (int u = 0; u < WB; ++u) {
+                const int j = wid + nw * u;
+                w[u] = (col_ok && j < n) ? __ldg(wt + (int64_t)j * p.pitch) : 0u;
+            }
+            cp_async_wait_all();
             __syncthreads();
             // exclusive prefix of each 32-row block of every column (fp32), block totals
             for (int j = wid; j < nblk; j += nw) {
                 float run = 0.f;
                 float* col = xs + j * 32 * 32 + lane;
-#pragma unroll 8
+                float v[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) v[k] = col[k * 32];
+#pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    const float v = col[k * 32];
                     col[k * 32] = run;
-                    run += v;
+                    run += v[k];
                 }
                 pb[j * 32 + lane] = (double)run;
             }
@@ -253,16 +297,30 @@ __global__ void __launch_bounds__(256) k_box_col(ColArgs p) {
                     pb[j * 32 + lane] = run;
                     run += t;
                 }
-                pb[nblk * 32 + lane] = run;  // row nblk*32 of xs is zero (staged)
+                pb[nblk * 32 + lane] = run;
             }
             __syncthreads();
-            float* ot = p.out + ch * p.plane + c0 + lane;
-            if (c0 + lane < p.W) {
-                for (int64_t k = r0 + wid; k < r1; k += nw) {
-                    const uint32_t w = __ldg(wt + k * p.pitch);
-                    const int lo = (int)(w & 0xffffu), hi = (int)(w >> 16);
-                    const int li = (int)(k - lo - a), hi1 = (int)(k + hi + 1 - a);
-                    ot[k * p.pitch] = window_mean<32>(xs + lane, pb + lane, li, hi1, lo + hi + 1);
+            float* ot = p.out + ch * p.plane + r0 * p.pitch + c0 + lane;
+            if (col_ok) {
+                for (int j0 = wid; j0 < n; j0 += nw * WB) {
+                    uint32_t wn[WB];
+#pragma unroll
+                    for (int u = 0; u < WB; ++u) {
+                        const int j = j0 + nw * WB + nw * u;
+                        wn[u] = (j < n) ? __ldg(wt + (int64_t)j * p.pitch) : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < WB; ++u) {
+                        const int j = j0 + nw * u;
+                        if (j < n) {
+                            const int lo = (int)(w[u] & 0xffffu), hi = (int)(w[u] >> 16);
+                            const int kl = k0l + j;
+                            ot[(int64_t)j * p.pitch] =
+                                window_mean<32>(xs + lane, pb + lane, kl - lo, kl + hi + 1, lo + hi + 1);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < WB; ++u) w[u] = wn[u];
                 }
             }
             __syncthreads();
@@ -315,7 +373,7 @@ cudaError_t plan_box(const Geometry& g, long long R, int num_sms, BoxPlan* plan)
     plan->row_nseg = (int)((g.W + plan->row_seg - 1) / plan->row_seg);
     long long lrow = (long long)plan->row_seg + 2LL * plan->hx + 3;
     if (lrow > g.W + 3) lrow = g.W + 3;
-    plan->row_lpad = (int)((lrow + 31) / 32 * 32 + 32);
+    plan->row_lpad = (int)((((lrow >> 5) + 4) >> 2) * 128);  // 128-float chunks covering blocks 0..L/32
     const size_t pw = box::row_warp_bytes(plan->row_lpad);
     if (pw > 200 * 1024) return cudaErrorInvalidValue;
     int warps = (int)((110 * 1024) / pw);
