@@ -126,7 +126,16 @@ template <int STRIDE>
 __device__ __forceinline__ float window_mean(const float* pe, const double* pb, int li, int hi1, int cnt) {
     const float whole = (float)(pb[(hi1 >> 5) * STRIDE] - pb[(li >> 5) * STRIDE]);
     const float sum = whole + (pe[hi1 * STRIDE] - pe[li * STRIDE]);
-    return __fdividef(sum, (float)cnt);  // branch-free (<= 2 ulp)
+    float rc;  // 1 / cnt, <= 1 ulp (cnt >= 1)
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"((float)cnt));
+    return sum * rc;
+}
+
+// one output: decode the packed window of local index kl and form its mean
+template <int STRIDE>
+__device__ __forceinline__ float box_out(const float* pe, const double* pb, int kl, uint32_t w) {
+    const int lo = (int)(w & 0xffffu), hi = (int)(w >> 16);
+    return window_mean<STRIDE>(pe, pb, kl - lo, kl + hi + 1, lo + hi + 1);
 }
 
 // shared memory of one warp of k_box_row: pe[lpad] floats + pb[lpad / 32] doubles, 16-B multiple
@@ -205,22 +214,26 @@ __global__ void __launch_bounds__(256) k_box_row(RowArgs p) {
                 run = p3 + (double)t3;
             }
             __syncwarp();
-            float* orow = p.out + ch * p.plane + r * p.pitch + c0;
-            for (int j0 = lane; j0 < n; j0 += 32 * WB) {
+            float* orow = p.out + ch * p.plane + r * p.pitch + c0 + lane;
+            const uint32_t* wl = wrow + lane;
+            for (int j0 = 0; j0 < n; j0 += 32 * WB) {  // j0: warp-uniform batch start
                 uint32_t wn[WB];  // next batch
+                const int jn = j0 + 32 * WB;
+                if (jn + 32 * WB <= n) {
 #pragma unroll
-                for (int u = 0; u < WB; ++u) {
-                    const int j = j0 + 32 * WB + 32 * u;
-                    wn[u] = (j < n) ? __ldg(wrow + j) : 0u;
+                    for (int u = 0; u < WB; ++u) wn[u] = __ldg(wl + jn + 32 * u);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < WB; ++u) wn[u] = (jn + 32 * u + lane < n) ? __ldg(wl + jn + 32 * u) : 0u;
                 }
+                const int kb = k0l + j0 + lane;
+                if (j0 + 32 * WB <= n) {
 #pragma unroll
-                for (int u = 0; u < WB; ++u) {
-                    const int j = j0 + 32 * u;
-                    if (j < n) {
-                        const int lo = (int)(w[u] & 0xffffu), hi = (int)(w[u] >> 16);
-                        const int kl = k0l + j;
-                        orow[j] = window_mean<1>(pe, pb, kl - lo, kl + hi + 1, lo + hi + 1);
-                    }
+                    for (int u = 0; u < WB; ++u) orow[j0 + 32 * u] = box_out<1>(pe, pb, kb + 32 * u, w[u]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < WB; ++u)
+                        if (j0 + 32 * u + lane < n) orow[j0 + 32 * u] = box_out<1>(pe, pb, kb + 32 * u, w[u]);
                 }
 #pragma unroll
                 for (int u = 0; u < WB; ++u) w[u] = wn[u];
@@ -246,6 +259,8 @@ __global__ void __launch_bounds__(256) k_box_col(ColArgs p) {
     double* pb = reinterpret_cast<double*>(smem_raw + (size_t)p.lpad * 128);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int64_t ntask = (int64_t)p.ntc * p.nseg;
+    const int64_t pitch = p.pitch;
+    const int64_t wstep = (int64_t)nw * pitch;  // rows nw apart
     for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
         const int64_t tc = task % p.ntc;  // consecutive CTAs take neighbouring column tiles
         const int64_t r0 = (task / p.ntc) * p.seg;
@@ -257,7 +272,7 @@ __global__ void __launch_bounds__(256) k_box_col(ColArgs p) {
         const int nblk = (L + 31) >> 5;
         const int n = (int)(r1 - r0), k0l = (int)(r0 - a);
         const bool col_ok = c0 + lane < p.W;
-        const uint32_t* wt = p.win + r0 * p.pitch + c0 + lane;
+        const uint32_t* wt = p.win + r0 * pitch + c0 + lane;
         for (int ch = 0; ch < p.Ct; ++ch) {
             const float* xt = p.in + ch * p.plane + a * p.pitch + c0;
             // stage rows [a, b) (8 x 16 B per row); rows L..32 nblk - 1 are never read by a
@@ -268,11 +283,9 @@ __global__ void __launch_bounds__(256) k_box_col(ColArgs p) {
             }
             if (threadIdx.x < 32) xs[nblk * 32 * 32 + threadIdx.x] = 0.f;  // pe at row 32 nblk
             uint32_t w[WB];  // first window batch in flight during the scan
+            const uint32_t* wq = wt + (int64_t)wid * pitch;
 #pragma unroll
-            for (int u = 0; u < WB; ++u) {
-                const int j = wid + nw * u;
-                w[u] = (col_ok && j < n) ? __ldg(wt + (int64_t)j * p.pitch) : 0u;
-            }
+            for (int u = 0; u < WB; ++u) w[u] = (col_ok && wid + nw * u < n) ? __ldg(wq + u * wstep) : 0u;
             cp_async_wait_all();
             __syncthreads();
             // exclusive prefix of each 32-row block of every column (fp32), block totals
@@ -300,25 +313,29 @@ __global__ void __launch_bounds__(256) k_box_col(ColArgs p) {
                 pb[nblk * 32 + lane] = run;
             }
             __syncthreads();
-            float* ot = p.out + ch * p.plane + r0 * p.pitch + c0 + lane;
             if (col_ok) {
-                for (int j0 = wid; j0 < n; j0 += nw * WB) {
+                float* oq = p.out + ch * p.plane + (r0 + wid) * pitch + c0 + lane;
+                for (int j0 = 0; j0 < n; j0 += nw * WB) {  // warp rows j0 + wid + nw u
                     uint32_t wn[WB];
+                    wq += (int64_t)WB * wstep;
+                    const int jn = j0 + nw * WB + wid;
+                    if (jn + nw * (WB - 1) < n) {
 #pragma unroll
-                    for (int u = 0; u < WB; ++u) {
-                        const int j = j0 + nw * WB + nw * u;
-                        wn[u] = (j < n) ? __ldg(wt + (int64_t)j * p.pitch) : 0u;
-                    }
+                        for (int u = 0; u < WB; ++u) wn[u] = __ldg(wq + u * wstep);
+                    } else {
 #pragma unroll
-                    for (int u = 0; u < WB; ++u) {
-                        const int j = j0 + nw * u;
-                        if (j < n) {
-                            const int lo = (int)(w[u] & 0xffffu), hi = (int)(w[u] >> 16);
-                            const int kl = k0l + j;
-                            ot[(int64_t)j * p.pitch] =
-                                window_mean<32>(xs + lane, pb + lane, kl - lo, kl + hi + 1, lo + hi + 1);
-                        }
+                        for (int u = 0; u < WB; ++u) wn[u] = (jn + nw * u < n) ? __ldg(wq + u * wstep) : 0u;
                     }
+                    const int kb = k0l + j0 + wid;
+                    if (j0 + wid + nw * (WB - 1) < n) {
+#pragma unroll
+                        for (int u = 0; u < WB; ++u) oq[u * wstep] = box_out<32>(xs + lane, pb + lane, kb + nw * u, w[u]);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < WB; ++u)
+                            if (j0 + wid + nw * u < n) oq[u * wstep] = box_out<32>(xs + lane, pb + lane, kb + nw * u, w[u]);
+                    }
+                    oq += (int64_t)WB * wstep;
 #pragma unroll
                     for (int u = 0; u < WB; ++u) w[u] = wn[u];
                 }
