@@ -181,15 +181,31 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         mbar_wait(&bars[s], (uint32_t)(k & 1));
         float a[LS];
         float xv[NV][LS];
+        if (r0 + lo + LS <= p.H) {
+            // every row of the segment is in the image (warp-uniform): no per-row checks.
+            // Lanes past W read the row padding; their values stay in their own column
+            // (every step of the pass is per column) and are never stored.
+            const float* ldc = ld + lo * TW + c;
 #pragma unroll
-        for (int j = 0; j < LS; ++j) {
-            const int rr = lo + j;
-            const bool ok = colok && (r0 + rr) < p.H;
-            a[j] = ok ? coef_from_d(ld[rr * TW + c], p.kc) : 0.f;
+            for (int j = 0; j < LS; ++j) {
+                a[j] = coef_from_d(ldc[j * TW], p.kc);
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                if constexpr (HASX) xv[v][j] = ok ? lx[(v * HB + rr) * TW + c] : 0.f;
-                else xv[v][j] = 0.f;
+                for (int v = 0; v < NV; ++v) {
+                    if constexpr (HASX) xv[v][j] = lx[(v * HB + lo + j) * TW + c];
+                    else xv[v][j] = 0.f;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < LS; ++j) {
+                const int rr = lo + j;
+                const bool ok = colok && (r0 + rr) < p.H;
+                a[j] = ok ? coef_from_d(ld[rr * TW + c], p.kc) : 0.f;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    if constexpr (HASX) xv[v][j] = ok ? lx[(v * HB + rr) * TW + c] : 0.f;
+                    else xv[v][j] = 0.f;
+                }
             }
         }
         // coefficient linking this segment's last row to the next row: from the
@@ -332,18 +348,24 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         {
             const int nrow = min(LS, p.H - (r0 + lo));
             if (colok && nrow > 0) {
-                if constexpr (MODE == MODE_FILTER) {
+                if constexpr (MODE == MODE_FILTER || MODE == MODE_SUPPORT) {
+                    float* base = (MODE == MODE_FILTER ? p.x : p.support) + (int64_t)(r0 + lo) * p.pitch + col;
+                    const int64_t pitch = p.pitch;
+                    if (nrow == LS) {  // full segment: a running pointer, no per-row checks
 #pragma unroll
-                    for (int j = 0; j < LS; ++j)
-                        if (j < nrow) {
-                            const int64_t o = (int64_t)(r0 + lo + j) * p.pitch + col;
+                        for (int v = 0; v < NV; ++v) {
+                            float* q = base + v * p.plane;
 #pragma unroll
-                            for (int v = 0; v < NV; ++v) p.x[v * p.plane + o] = xv[v][j];
+                            for (int j = 0; j < LS; ++j, q += pitch) *q = xv[v][j];
                         }
-                } else if constexpr (MODE == MODE_SUPPORT) {  // the column factor s_y into its own plane
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < LS; ++j)
-                        if (j < nrow) p.support[(int64_t)(r0 + lo + j) * p.pitch + col] = xv[0][j];
+                        for (int j = 0; j < LS; ++j)
+                            if (j < nrow) {
+#pragma unroll
+                                for (int v = 0; v < NV; ++v) base[v * p.plane + (int64_t)j * pitch] = xv[v][j];
+                            }
+                    }
                 } else {  // MODE_UPDATE, Eq. (3) with zbar = xv
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
