@@ -223,6 +223,18 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         }
         __syncthreads();  // landing zone free
         if (threadIdx.x == 0 && tile + nclusters < p.ntiles) stage_in(tile + nclusters);
+        if constexpr (MODE == MODE_UPDATE) {  // the write-out's Z / T / chat lines -> L2 (lane = row)
+            const int r = r0 + lo + c;
+            if (r < p.H) {
+                const int64_t o = (int64_t)r * p.pitch + col0;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    prefetch_l2(p.upd.Z + v * p.plane + o);
+                    prefetch_l2(p.upd.T + v * p.plane + o);
+                }
+                prefetch_l2(p.upd.chat + o);
+            }
+        }
 
         // ---- 2. causal fold, segment scan, band total ----
         {
@@ -366,24 +378,33 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
                                 for (int v = 0; v < NV; ++v) base[v * p.plane + (int64_t)j * pitch] = xv[v][j];
                             }
                     }
-                } else {  // MODE_UPDATE, Eq. (3) with zbar = xv
+                } else {  // MODE_UPDATE, Eq. (3) with zbar = xv; Z / T / chat were prefetched
+                          // into L2 when the tile started; 16 rows of loads in flight at a time
+                    constexpr int UB = 16;
+                    const int64_t pitch = p.pitch;
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
-                        float zo[LS];  // all Z loads in flight before any store (a[] is dead here)
 #pragma unroll
-                        for (int j = 0; j < LS; ++j)
-                            zo[j] = p.upd.Z[v * p.plane + (int64_t)(r0 + lo + (j < nrow ? j : 0)) * p.pitch + col];
+                        for (int j0 = 0; j0 < LS; j0 += UB) {
+                            float zo[UB], tv[UB], ch[UB];
 #pragma unroll
-                        for (int j = 0; j < LS; ++j) {
-                            if (j < nrow) {
-                                const int64_t r = r0 + lo + j;
-                                const int64_t o = r * p.pitch + col;
-                                const float ch = __ldg(p.upd.chat + o);
-                                const float tv = __ldg(p.upd.T + v * p.plane + o);
-                                const float g = fmaf(p.upd.lam, zo[j] - xv[v][j], ch * (zo[j] - tv));
-                                const float zn = fmaf(-p.upd.step, g, zo[j]);
-                                if (p.upd.out_hwc) p.upd.out_hwc[(r * p.W + col) * CT + v] = zn;
-                                else p.upd.Z[v * p.plane + o] = zn;
+                            for (int u = 0; u < UB; ++u) {
+                                const int jj = (j0 + u < nrow) ? j0 + u : 0;
+                                const int64_t o = (int64_t)(r0 + lo + jj) * pitch + col;
+                                zo[u] = p.upd.Z[v * p.plane + o];
+                                tv[u] = __ldg(p.upd.T + v * p.plane + o);
+                                ch[u] = __ldg(p.upd.chat + o);
+                            }
+#pragma unroll
+                            for (int u = 0; u < UB; ++u) {
+                                const int j = j0 + u;
+                                if (j < nrow) {
+                                    const int64_t r = r0 + lo + j;
+                                    const float g = fmaf(p.upd.lam, zo[u] - xv[v][j], ch[u] * (zo[u] - tv[u]));
+                                    const float zn = fmaf(-p.upd.step, g, zo[u]);
+                                    if (p.upd.out_hwc) p.upd.out_hwc[(r * p.W + col) * CT + v] = zn;
+                                    else p.upd.Z[v * p.plane + r * pitch + col] = zn;
+                                }
                             }
                         }
                     }
