@@ -95,6 +95,7 @@ struct dts_ctx {
     float* dy = nullptr;
     float* S = nullptr;
     float* Sy = nullptr;  // column support factor when the cluster kernel computes it (S then holds s_x)
+    float* A1y = nullptr;  // pass-1 column coefficient a_1^{d_y} (rows 0..H), cluster FILTER passes (N <= 4)
     // box filter (dts_create_ex, DTS_FILTER_BOX): dx / dy hold the fixed-point increments q,
     // win the packed windows (planes 2i: rows, 2i + 1: columns, pass i), S the window counts
     int filter = DTS_FILTER_RF;
@@ -137,12 +138,13 @@ namespace {
 
 enum Family {
     F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
-    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_FILL, F_BOX_PREP, F_BOX_ROW, F_BOX_COL, F_COUNT
+    F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_FILL, F_BOX_PREP, F_BOX_ROW, F_BOX_COL, F_COEF,
+    F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
                                      "rank_compose", "row_update", "confidence", "stereo_update", "link_fill",
-                                     "box_windows", "box_row", "box_col"};
+                                     "box_windows", "box_row", "box_col", "col_coef"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -590,6 +592,15 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
             });
         }
     }
+    // the cluster column kernel reads a_1^{d_y} instead of d_y (one exp per pixel here instead
+    // of one per pixel and pass); later passes square it (R5: sigma halves per pass)
+    if (st == DTS_OK && !comm && filter_passes <= 4 && cp.kind == 1) {
+        const int64_t n = (H + 1) * ctx->g.pitch;  // row H: the bottom link (+inf -> 0)
+        if ((e = cudaMallocAsync((void**)&ctx->A1y, (size_t)n * sizeof(float), s)) != cudaSuccess) st = cuda_fail(e);
+        if (st == DTS_OK)
+            st = run_launch(ctx, F_COEF, (double)n * 8.0, s,
+                            [&] { return launch_coef(ctx->dy, ctx->A1y, n, ctx->kc[0], s); });
+    }
     if (gstage) {
         cudaFreeAsync(gstage, s);
         if (st == DTS_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess) st = cuda_fail(e);
@@ -880,6 +891,14 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
             if (st != DTS_OK) return st;
             const double row_bytes = px * (8.0 * Ct + 4);
             const double upd_bytes = px * (16.0 * Ct + 8);  // X, d, Z, T, chat in; Z out
+            // FILTER column pass i: the cluster kernel on A1 = a_1^{d_y} squared i times when
+            // the context holds it, else on d_y
+            auto col_filter = [&](int i) -> cudaError_t {
+                if (cpf.kind == 1 && ctx->A1y && i < 4)
+                    return launch_col_cluster(cpf, g, Ct, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr, nullptr,
+                                              s, i);
+                return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
+            };
             if (is_box) {  // R25: N x (box rows, box columns), ping-pong X2 <-> X, then Eq. (3)
                 for (int k = 0; k < iterations; ++k) {
                     for (int i = 0; i < ctx->N; ++i) {
@@ -958,16 +977,10 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                                                  upd_bytes, s);
                         }
                     } else if (i + 1 < ctx->N) {
-                        st = run_launch(ctx, F_COL, row_bytes, s, [&] {
-                            return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
-                                              s);
-                        });
+                        st = run_launch(ctx, F_COL, row_bytes, s, [&] { return col_filter(i); });
                     } else if ((cpu.kind == 1 && !std::getenv("DTS_FUSED_UPDATE")) || cpu.kind == 3) {
                         // column kernel (FILTER) + streaming update kernel (K4b)
-                        st = run_launch(ctx, F_COL, row_bytes, s, [&] {
-                            return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
-                                              s);
-                        });
+                        st = run_launch(ctx, F_COL, row_bytes, s, [&] { return col_filter(i); });
                         if (st != DTS_OK) return st;
                         float* ohwc = (k + 1 == iterations) ? o_d : nullptr;
                         st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
@@ -1242,8 +1255,8 @@ void dts_destroy(dts_ctx* ctx) {
     if (!ctx) return;
     cudaStream_t s = ctx->last_stream;
     free_solver_state(ctx, s);
-    for (float** p : {&ctx->dx_base, &ctx->dy_base, &ctx->S, &ctx->Sy, &ctx->st_t, &ctx->st_c, &ctx->st_o, &ctx->rank_tup,
-                      &ctx->gathered, &ctx->ext}) {
+    for (float** p : {&ctx->dx_base, &ctx->dy_base, &ctx->S, &ctx->Sy, &ctx->A1y, &ctx->st_t, &ctx->st_c, &ctx->st_o,
+                      &ctx->rank_tup, &ctx->gathered, &ctx->ext}) {
         if (*p) cudaFreeAsync(*p, s);
         *p = nullptr;
     }

@@ -16,6 +16,13 @@ __device__ __forceinline__ float coef_from_d(float d, float kc) {
     return y;
 }
 
+// pass coefficient from the stored pass-1 coefficient A1 = a_1^d: the R5 schedule halves
+// sigma from pass to pass, so a_i^d = A1^(2^(i-1)) (nsq = i - 1 squarings)
+__device__ __forceinline__ float coef_pow(float a1, int nsq) {
+    for (int k = 0; k < nsq; ++k) a1 *= a1;
+    return a1;
+}
+
 // ---- affine maps y_out = P * y_in + B[v] (one shared P, NV offsets) -------------------
 template <int NV>
 struct Aff {

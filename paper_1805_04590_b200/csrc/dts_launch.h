@@ -71,7 +71,8 @@ cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int 
 // Returns cudaErrorNotSupported when the shape does not fit (then use plan_col_pass).
 cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
-                               float kc, const UpdateArgs* upd, float* support, cudaStream_t s);
+                               float kc, const UpdateArgs* upd, float* support, cudaStream_t s,
+                               int nsq = -1);  // nsq >= 0: d holds A1 (see coef_pow)
 
 // K3/K4 streaming path (k_colv.cu): decoupled band-tuple scan over 64-column tiles with
 // shared-memory-held items and a TMA producer warp; FILTER and UPDATE (fused Eq. 3).
@@ -146,5 +147,8 @@ cudaError_t launch_box_row(const BoxPlan& plan, const Geometry& g, int Ct, const
                            const uint32_t* win, cudaStream_t s);
 cudaError_t launch_box_col(const BoxPlan& plan, const Geometry& g, int Ct, const float* in, float* out,
                            const uint32_t* win, cudaStream_t s);
+
+// A1 = a_1^d = 2^(-kc d) elementwise over n floats (the column kernel's pass-1 coefficient).
+cudaError_t launch_coef(const float* d, float* a1, int64_t n, float kc, cudaStream_t s);
 
 }  // namespace dts

@@ -36,6 +36,7 @@ struct Params {
     int64_t plane, pitch;
     int H, W, HB, S, CB, ntiles;
     float kc;
+    int nsq;  // < 0: d holds distances (a = 2^(-kc d)); >= 0: d holds A1, a = A1^(2^nsq)
 };
 
 struct Smem {
@@ -110,7 +111,7 @@ __device__ __forceinline__ void seg_scan(float* seg, int S, int cc, float* tot) 
 template <int NV>
 constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
 
-template <int CT, int MODE>
+template <int CT, int MODE, bool PRE>
 __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>(), 1)
     k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
     constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
@@ -138,6 +139,19 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
     const int nclusters = gridDim.x / CB;
     const int r0 = band * HB;
     const int lo = s * LS;
+    // PRE: d holds A1 = a_1^d and this pass's coefficient is A1^(2^nsq), nsq <= 3 (uniform)
+    const int nsq = p.nsq;
+    auto coef = [&](float v) {
+        if constexpr (PRE) {
+            float a1 = v;
+            if (nsq > 0) a1 *= a1;
+            if (nsq > 1) a1 *= a1;
+            if (nsq > 2) a1 *= a1;
+            return a1;
+        } else {
+            return coef_from_d(v, p.kc);
+        }
+    };
 
     const uint32_t xbytesC = (uint32_t)(band * (NV + 1) * TW * sizeof(float));
     const uint32_t xbytesA = (uint32_t)((CB - 1 - band) * (NV + 1) * TW * sizeof(float));
@@ -188,7 +202,7 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
             const float* ldc = ld + lo * TW + c;
 #pragma unroll
             for (int j = 0; j < LS; ++j) {
-                a[j] = coef_from_d(ldc[j * TW], p.kc);
+                a[j] = coef(ldc[j * TW]);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     if constexpr (HASX) xv[v][j] = lx[(v * HB + lo + j) * TW + c];
@@ -200,7 +214,7 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
             for (int j = 0; j < LS; ++j) {
                 const int rr = lo + j;
                 const bool ok = colok && (r0 + rr) < p.H;
-                a[j] = ok ? coef_from_d(ld[rr * TW + c], p.kc) : 0.f;
+                a[j] = ok ? coef(ld[rr * TW + c]) : 0.f;
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     if constexpr (HASX) xv[v][j] = ok ? lx[(v * HB + rr) * TW + c] : 0.f;
@@ -214,12 +228,12 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         float anext = 0.f;
         {
             const int rn = r0 + lo + LS;
-            if (s + 1 == S && colok && rn < p.H) anext = coef_from_d(__ldg(p.d + (int64_t)rn * p.pitch + col), p.kc);
+            if (s + 1 == S && colok && rn < p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
         }
         __syncthreads();
         if (s + 1 < S) {
             const int rn = r0 + lo + LS;
-            anext = (colok && rn < p.H) ? coef_from_d(ld[(lo + LS) * TW + c], p.kc) : 0.f;
+            anext = (colok && rn < p.H) ? coef(ld[(lo + LS) * TW + c]) : 0.f;
         }
         __syncthreads();  // landing zone free
         if (threadIdx.x == 0 && tile + nclusters < p.ntiles) stage_in(tile + nclusters);
@@ -444,12 +458,20 @@ static bool tmap(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int CT, int MODE>
+template <int CT, int MODE, bool PRE = false>
 static const void* kptr() {
-    return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE>);
+    return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE, PRE>);
 }
-static const void* colc_kernel(int Ct, int mode) {
+static const void* colc_kernel(int Ct, int mode, bool pre = false) {
     if (mode == MODE_SUPPORT) return kptr<1, MODE_SUPPORT>();
+    if (pre && mode == MODE_FILTER) {
+        switch (Ct) {
+            case 1: return kptr<1, MODE_FILTER, true>();
+            case 2: return kptr<2, MODE_FILTER, true>();
+            case 3: return kptr<3, MODE_FILTER, true>();
+        }
+        return nullptr;
+    }
     switch (Ct * 4 + mode) {
         case 4 + MODE_FILTER: return kptr<1, MODE_FILTER>();
         case 8 + MODE_FILTER: return kptr<2, MODE_FILTER>();
@@ -480,12 +502,19 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
         const int HB = S * colc::LS;
         const colc::Smem L = colc::layout(NV, HB, S);
         if (L.bytes > 227 * 1024) continue;
-        if (CB > 8) {
-            e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (e != cudaSuccess) return e;
+        // attributes are per function and shared by every plan: allow non-portable clusters and
+        // the opt-in shared memory maximum (so that no plan lowers another's limit); the
+        // A1-input variants of the FILTER kernel get the same
+        int optin = 0;
+        if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0)) != cudaSuccess) return e;
+        for (const void* f : {fn, mode == MODE_FILTER ? colc_kernel(Ct, mode, true) : fn}) {
+            cudaFuncAttributes fa2;
+            if ((e = cudaFuncGetAttributes(&fa2, f)) != cudaSuccess) return e;
+            if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess ||
+                (e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          optin - (int)fa2.sharedSizeBytes)) != cudaSuccess)
+                return e;
         }
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-        if (e != cudaSuccess) return e;
         // how many clusters can be resident at once
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)CB, 1, 1);
@@ -525,8 +554,9 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
 }
 
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
-                               float kc, const UpdateArgs* upd, float* support, cudaStream_t s) {
+                               float kc, const UpdateArgs* upd, float* support, cudaStream_t s, int nsq) {
     colc::Params p = {};
+    p.nsq = nsq;
     p.x = x;
     p.d = d;
     p.support = support;
@@ -547,7 +577,7 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     } else {
         tx = td;
     }
-    const void* fn = colc_kernel(Ct, mode);
+    const void* fn = colc_kernel(Ct, mode, nsq >= 0);
     if (!fn) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = plan.grid;

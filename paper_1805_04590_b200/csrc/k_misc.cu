@@ -533,4 +533,17 @@ cudaError_t launch_sr_prepare(const float* low, int64_t h, int64_t w, int f, flo
     return cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(256) k_coef(const float* __restrict__ d, float* __restrict__ a1, int64_t n, float kc) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a1[i] = coef_from_d(__ldg(d + i), kc);
+}
+
+cudaError_t launch_coef(const float* d, float* a1, int64_t n, float kc, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_coef<<<(unsigned)blocks, 256, 0, s>>>(d, a1, n, kc);
+    return cudaGetLastError();
+}
+
 }  // namespace dts

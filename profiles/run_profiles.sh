@@ -8,7 +8,7 @@ OUT=${OUT:-gpurun_out}
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
 $CMD > $OUT/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -s 145 -c 145 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
+    -s 146 -c 146 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
 for spec in "k_col_cluster 4" "k_row_pass 2" "k_update 1" "k_guide_deriv 1" "k_prologue 1"; do
   set -- $spec
   ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 \

@@ -214,7 +214,7 @@ def test_profile_counters():
     gd, td, cd = (torch.from_numpy(a).cuda() for a in (g, t, c))
     with dts.Solver(gd, 5.0, 0.2, 3) as s:
         n0 = dts.dts_launch_count(s.ctx)
-        assert n0 == 4  # deriv + bottom-link row fill + support row + support col
+        assert n0 == 5  # deriv + bottom-link row fill + support row + support col + column coefficient A1
         dts.dts_profile_enable(s.ctx, True)
         s.solve(td, cd, 0.99, 4)
         st = dts.dts_profile_read(s.ctx)
