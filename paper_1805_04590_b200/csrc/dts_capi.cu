@@ -353,6 +353,46 @@ dts_status ensure_band_buffers(dts_ctx* ctx, cudaStream_t s) {
 dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, const UpdateArgs* upd,
                            float* support, int fam, double bytes, cudaStream_t s) {
     const Geometry& g = ctx->g;
+    // cluster kernels when the band's columns fit a cluster: TUPLE (the rank 5-tuple, with the
+    // carry sensitivity as an extra channel) -> all-gather -> compose -> FILTER with the
+    // external carries (+ the streaming update kernel for the last pass of an iteration)
+    ColPlan pT, pF;
+    if (mode != MODE_SUPPORT && !std::getenv("DTS_BAND_LEGACY") &&
+        plan_col_cluster(g, Ct, MODE_TUPLE, ctx->num_sms, &pT) == cudaSuccess &&
+        plan_col_cluster(g, Ct, MODE_FILTER, ctx->num_sms, &pF) == cudaSuccess) {
+        dts_status st;
+        if ((st = ensure_band_buffers(ctx, s)) != DTS_OK) return st;
+        const size_t count = (size_t)pF.ntiles * (2 * Ct + 3) * 32;
+        const double px = (double)g.H * g.W;
+        st = run_launch(ctx, F_TUPLE, px * (4.0 * Ct + 4), s, [&] {
+            return launch_col_cluster(pT, g, Ct, MODE_TUPLE, x, ctx->dy, kc, nullptr, nullptr, s, -1, nullptr,
+                                      ctx->rank_tup);
+        });
+        if (st != DTS_OK) return st;
+        std::string err;
+        st = run_launch(ctx, F_EXCHANGE, (double)count * 4 * ctx->comm->nranks, s, [&] {
+            return comm_allgather(ctx->comm, ctx->rank_tup, ctx->gathered, count, s, &err) ? cudaSuccess
+                                                                                            : cudaErrorUnknown;
+        });
+        if (st != DTS_OK) {
+            g_last_error = err;
+            return DTS_E_NCCL;
+        }
+        st = run_launch(ctx, F_COMPOSE, 0.0, s, [&] {
+            return launch_rank_compose(ctx->gathered, ctx->comm->nranks, ctx->comm->rank, pF.ntiles, Ct, ctx->ext, s);
+        });
+        if (st != DTS_OK) return st;
+        st = run_launch(ctx, F_COL, px * (8.0 * Ct + 4), s, [&] {
+            return launch_col_cluster(pF, g, Ct, MODE_FILTER, x, ctx->dy, kc, nullptr, nullptr, s, -1, ctx->ext,
+                                      nullptr);
+        });
+        if (st != DTS_OK || mode != MODE_UPDATE) return st;
+        return run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
+            return launch_update(x, upd->Z, upd->T, upd->chat, Ct, g, upd->lam, upd->step, upd->out_hwc, ctx->num_sms,
+                                 s);
+        });
+    }
+    cudaGetLastError();
     ColPlan plan;
     if (plan_col_pass(g, Ct, mode, ctx->num_sms, &plan) != cudaSuccess) return DTS_E_SHAPE;
     dts_status st;

@@ -5,7 +5,8 @@
 
 namespace dts {
 
-enum PassMode : int { MODE_FILTER = 0, MODE_UPDATE = 1, MODE_SUPPORT = 2, MODE_ROWUPD = 3 };
+// MODE_TUPLE (cluster column kernel, row-band mode): only the rank band's 5-tuple per column
+enum PassMode : int { MODE_FILTER = 0, MODE_UPDATE = 1, MODE_SUPPORT = 2, MODE_ROWUPD = 3, MODE_TUPLE = 4 };
 // column-pass phases (row-band mode): FULL = single band set; TUPLE = emit the aggregate
 // 5-tuple of this rank's rows; APPLY = finish with external carries (after the exchange)
 enum ColPhase : int { PHASE_FULL = 0, PHASE_TUPLE = 1, PHASE_APPLY = 2 };
@@ -72,7 +73,9 @@ cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int 
 cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
                                float kc, const UpdateArgs* upd, float* support, cudaStream_t s,
-                               int nsq = -1);  // nsq >= 0: d holds A1 (see coef_pow)
+                               int nsq = -1,  // nsq >= 0: d holds A1 (see coef_pow)
+                               const float* ext = nullptr,    // APPLY: carries into the rank band [ntiles][2][Ct][32]
+                               float* rank_tuples = nullptr);  // TUPLE: [ntiles][2Ct+3][32]
 
 // K3/K4 streaming path (k_colv.cu): decoupled band-tuple scan over 64-column tiles with
 // shared-memory-held items and a TMA producer warp; FILTER and UPDATE (fused Eq. 3).

@@ -37,6 +37,10 @@ struct Params {
     int H, W, HB, S, CB, ntiles;
     float kc;
     int nsq;  // < 0: d holds distances (a = 2^(-kc d)); >= 0: d holds A1, a = A1^(2^nsq)
+    // row-band mode: APPLY carries into the rank band (causal c at the
+    // top, anticausal e at the bottom), [ntiles][2][CT][TW]; TUPLE output [ntiles][2CT+3][TW]
+    const float* ext;
+    float* rank_tuples;
 };
 
 struct Smem {
@@ -44,11 +48,12 @@ struct Smem {
     size_t bytes;
 };
 
-__host__ __device__ inline Smem layout(int NV, int HB, int S) {
+// NX planes of x staged per tile, NV channels carried (TUPLE: NX + 1, the carry sensitivity)
+__host__ __device__ inline Smem layout(int NX, int NV, int HB, int S) {
     Smem L;
     int o = 0;
     L.land_x = o;
-    o += NV * HB * TW;
+    o += NX * HB * TW;
     L.land_d = o;
     o += HB * TW;
     L.segF = o;
@@ -111,14 +116,22 @@ __device__ __forceinline__ void seg_scan(float* seg, int S, int cc, float* tot) 
 template <int NV>
 constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
 
-template <int CT, int MODE, bool PRE>
-__global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>(), 1)
+template <int CT, int MODE>
+__host__ __device__ constexpr int nchan() { return MODE == MODE_SUPPORT ? 1 : (MODE == MODE_TUPLE ? CT + 1 : CT); }
+
+// BAND (row-band mode, MODE_TUPLE or FILTER with external carries): rows past H are identity
+// maps and row H is the link to the next rank; the single-GPU instantiations keep the
+// plain code (a = 0 past H, no external carries)
+template <int CT, int MODE, bool PRE, bool BAND = (MODE == MODE_TUPLE)>
+__global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
     k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
-    constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
+    // TUPLE: channel CT is the carry sensitivity g (x = 0, carry-in 1 at the rank band's top)
+    constexpr int NV = nchan<CT, MODE>();
+    constexpr int NX = (MODE == MODE_SUPPORT) ? 0 : CT;  // x planes staged
     constexpr bool HASX = MODE != MODE_SUPPORT;
     extern __shared__ __align__(128) float smem[];
     const int HB = p.HB, S = p.S, CB = p.CB;
-    const Smem L = layout(NV, HB, S);
+    const Smem L = layout(NX, NV, HB, S);
     float* lx = smem + L.land_x;
     float* ld = smem + L.land_d;
     float* segF = smem + L.segF;
@@ -172,14 +185,12 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         const uint32_t box = (uint32_t)(LS * TW * sizeof(float));
         for (int q = 0; q < S; ++q) {
             const int rq = r0 + q * LS;
-            const uint32_t bytes = rq < p.H ? box * (1 + (HASX ? NV : 0)) : 0u;
+            const uint32_t bytes = rq < p.H ? box * (1 + NX) : 0u;
             mbar_arrive_expect_tx(&bars[q], bytes);
             if (bytes) {
                 tma_load_2d(ld + q * LS * TW, &tm_d, col0, rq, &bars[q]);
-                if constexpr (HASX) {
 #pragma unroll
-                    for (int v = 0; v < NV; ++v) tma_load_3d(lx + (v * HB + q * LS) * TW, &tm_x, col0, rq, v, &bars[q]);
-                }
+                for (int v = 0; v < NX; ++v) tma_load_3d(lx + (v * HB + q * LS) * TW, &tm_x, col0, rq, v, &bars[q]);
             }
         }
     };
@@ -205,19 +216,26 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
                 a[j] = coef(ldc[j * TW]);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
-                    if constexpr (HASX) xv[v][j] = lx[(v * HB + lo + j) * TW + c];
+                    if constexpr (HASX) xv[v][j] = v < NX ? lx[(v * HB + lo + j) * TW + c] : 0.f;
                     else xv[v][j] = 0.f;
                 }
             }
         } else {
+            // rows past H: row H carries the link coefficient to the rows below (d row H: the
+            // next rank's first row in row-band mode, +inf -> 0 at the image bottom); the rows
+            // after it are identity maps (a = 1, x = 0), so the causal map of the band stops at
+            // row H - 1 and the anticausal carry from below reaches row H unchanged
+            const float aH = (BAND && colok && r0 + lo <= p.H && p.H < r0 + lo + LS)
+                                 ? coef(__ldg(p.d + (int64_t)p.H * p.pitch + col)) : 0.f;
 #pragma unroll
             for (int j = 0; j < LS; ++j) {
                 const int rr = lo + j;
                 const bool ok = colok && (r0 + rr) < p.H;
-                a[j] = ok ? coef(ld[rr * TW + c]) : 0.f;
+                if constexpr (BAND) a[j] = ok ? coef(ld[rr * TW + c]) : (!colok ? 0.f : (r0 + rr == p.H ? aH : 1.f));
+                else a[j] = ok ? coef(ld[rr * TW + c]) : 0.f;
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
-                    if constexpr (HASX) xv[v][j] = ok ? lx[(v * HB + rr) * TW + c] : 0.f;
+                    if constexpr (HASX) xv[v][j] = (ok && v < NX) ? lx[(v * HB + rr) * TW + c] : 0.f;
                     else xv[v][j] = 0.f;
                 }
             }
@@ -225,15 +243,25 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         // coefficient linking this segment's last row to the next row: from the
         // landing zone (next segment; it landed before the barrier below) or, for the
         // band's last segment, straight from global (first row of the next band)
+        // (row H of d is the link below the band: the next rank's first row in row-band mode,
+        // +inf -- a = 0 -- at the image bottom)
         float anext = 0.f;
         {
             const int rn = r0 + lo + LS;
-            if (s + 1 == S && colok && rn < p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
+            if constexpr (BAND) {
+                if (colok) {
+                    if (rn > p.H) anext = 1.f;  // identity rows past the link (see the load above)
+                    else if (s + 1 == S || rn == p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
+                }
+            } else {
+                if ((s + 1 == S || rn == p.H) && colok && rn <= p.H)
+                    anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
+            }
         }
         __syncthreads();
         if (s + 1 < S) {
             const int rn = r0 + lo + LS;
-            anext = (colok && rn < p.H) ? coef(ld[(lo + LS) * TW + c]) : 0.f;
+            if (colok && rn < p.H) anext = coef(ld[(lo + LS) * TW + c]);
         }
         __syncthreads();  // landing zone free
         if (threadIdx.x == 0 && tile + nclusters < p.ntiles) stage_in(tile + nclusters);
@@ -281,9 +309,11 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         if (s == 0) {
             mbar_wait_cluster(xbarC, (uint32_t)(k & 1));
             if (c == 0) mbar_arrive_expect_tx(xbarC, xbytesC);  // re-arm for the next tile
-            float cin[NV];
+            float cin[NV];  // carry into the rank band's top: 0, the APPLY carry, or 1 for g (TUPLE)
 #pragma unroll
-            for (int v = 0; v < NV; ++v) cin[v] = 0.f;
+            for (int v = 0; v < NV; ++v)
+                cin[v] = (MODE == MODE_TUPLE) ? (v == CT ? 1.f : 0.f)
+                                              : (BAND ? p.ext[((int64_t)tile * 2 * NV + v) * TW + c] : 0.f);
             for (int q = 0; q < band; ++q) {
                 const float P = remC[(q * (NV + 1)) * TW + c];
 #pragma unroll
@@ -322,6 +352,19 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
             segR[(0 * S + s) * (TW + 1) + c] = Q;
 #pragma unroll
             for (int v = 0; v < NV; ++v) segR[((1 + v) * S + s) * (TW + 1) + c] = E[v];
+            if constexpr (MODE == MODE_TUPLE) {  // rank causal map c_out = A c + B: y at row H - 1
+                const int jl = p.H - 1 - (r0 + lo);  // of the x channels (c = 0) and of g (c = 1)
+                if (colok && jl >= 0 && jl < LS) {
+                    float* rt = p.rank_tuples + (int64_t)tile * (2 * CT + 3) * TW;
+#pragma unroll
+                    for (int j = 0; j < LS; ++j)
+                        if (j == jl) {
+                            rt[0 * TW + c] = xv[CT][j];
+#pragma unroll
+                            for (int v = 0; v < CT; ++v) rt[(1 + v) * TW + c] = xv[v][j];
+                        }
+                }
+            }
         }
         __syncthreads();
         for (int cc = s; cc < TW; cc += S) seg_scan<NV, true>(segR, S, cc, totA);
@@ -336,19 +379,30 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         if (s == 0) {
             mbar_wait_cluster(xbarA, (uint32_t)(k & 1));
             if (c == 0) mbar_arrive_expect_tx(xbarA, xbytesA);
-            float ein[NV];
+            float ein[NV];  // carry into the rank band's bottom: 0 or the APPLY carry
 #pragma unroll
-            for (int v = 0; v < NV; ++v) ein[v] = 0.f;
+            for (int v = 0; v < NV; ++v)
+                ein[v] = (MODE != MODE_TUPLE && BAND) ? p.ext[((int64_t)tile * 2 * NV + NV + v) * TW + c] : 0.f;
+            float Qbe = 1.f;
             for (int q = CB - 1; q > band; --q) {
                 const float Qb = remA[(q * (NV + 1)) * TW + c];
+                if constexpr (MODE == MODE_TUPLE) Qbe *= Qb;
 #pragma unroll
                 for (int v = 0; v < NV; ++v) ein[v] = fmaf(Qb, ein[v], remA[(q * (NV + 1) + 1 + v) * TW + c]);
             }
 #pragma unroll
             for (int v = 0; v < NV; ++v) carry[v * TW + c] = ein[v];
+            if (MODE == MODE_TUPLE && band == 0) {  // rank anticausal map: e_top = Z0 + S c + Q e
+                float* rt = p.rank_tuples + (int64_t)tile * (2 * CT + 3) * TW;
+                const float Qown = totA[0 * TW + c];
+                rt[(1 + CT) * TW + c] = Qbe * Qown;
+#pragma unroll
+                for (int v = 0; v < CT; ++v) rt[(2 + CT + v) * TW + c] = fmaf(Qown, ein[v], totA[(1 + v) * TW + c]);
+                rt[(2 + 2 * CT) * TW + c] = fmaf(Qown, ein[CT], totA[(1 + CT) * TW + c]);
+            }
         }
         __syncthreads();
-        {
+        if constexpr (MODE != MODE_TUPLE) {
             const float eQ = segR[(0 * S + s) * (TW + 1) + c];
             float z[NV];
 #pragma unroll
@@ -370,8 +424,8 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
             }
         }
 
-        // ---- 5. write-out straight from registers ----
-        {
+        // ---- 5. write-out straight from registers (TUPLE: nothing; the tuple is written) ----
+        if constexpr (MODE != MODE_TUPLE) {
             const int nrow = min(LS, p.H - (r0 + lo));
             if (colok && nrow > 0) {
                 if constexpr (MODE == MODE_FILTER || MODE == MODE_SUPPORT) {
@@ -458,17 +512,33 @@ static bool tmap(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int CT, int MODE, bool PRE = false>
+template <int CT, int MODE, bool PRE = false, bool BAND = (MODE == MODE_TUPLE)>
 static const void* kptr() {
-    return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE, PRE>);
+    return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE, PRE, BAND>);
 }
-static const void* colc_kernel(int Ct, int mode, bool pre = false) {
+static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = false) {
     if (mode == MODE_SUPPORT) return kptr<1, MODE_SUPPORT>();
+    if (band && mode == MODE_FILTER) {  // APPLY of the row-band exchange
+        switch (Ct) {
+            case 1: return kptr<1, MODE_FILTER, false, true>();
+            case 2: return kptr<2, MODE_FILTER, false, true>();
+            case 3: return kptr<3, MODE_FILTER, false, true>();
+        }
+        return nullptr;
+    }
     if (pre && mode == MODE_FILTER) {
         switch (Ct) {
             case 1: return kptr<1, MODE_FILTER, true>();
             case 2: return kptr<2, MODE_FILTER, true>();
             case 3: return kptr<3, MODE_FILTER, true>();
+        }
+        return nullptr;
+    }
+    if (mode == MODE_TUPLE) {
+        switch (Ct) {
+            case 1: return kptr<1, MODE_TUPLE>();
+            case 2: return kptr<2, MODE_TUPLE>();
+            case 3: return kptr<3, MODE_TUPLE>();
         }
         return nullptr;
     }
@@ -486,7 +556,8 @@ static const void* colc_kernel(int Ct, int mode, bool pre = false) {
 // Fast path if the column fits a cluster of <= 16 CTAs with register-resident segments.
 cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan) {
     (void)num_sms;
-    const int NV = (mode == MODE_SUPPORT) ? 1 : Ct;
+    const int NV = (mode == MODE_SUPPORT) ? 1 : (mode == MODE_TUPLE ? Ct + 1 : Ct);
+    const int NX = (mode == MODE_SUPPORT) ? 0 : Ct;
     const void* fn = colc_kernel(Ct, mode);
     if (!fn) return cudaErrorNotSupported;
     cudaFuncAttributes fa;
@@ -500,14 +571,15 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
         const int S = (int)((HBmin + rows_seg - 1) / rows_seg);
         if (S > Smax) continue;
         const int HB = S * colc::LS;
-        const colc::Smem L = colc::layout(NV, HB, S);
+        const colc::Smem L = colc::layout(NX, NV, HB, S);
         if (L.bytes > 227 * 1024) continue;
         // attributes are per function and shared by every plan: allow non-portable clusters and
         // the opt-in shared memory maximum (so that no plan lowers another's limit); the
         // A1-input variants of the FILTER kernel get the same
         int optin = 0;
         if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0)) != cudaSuccess) return e;
-        for (const void* f : {fn, mode == MODE_FILTER ? colc_kernel(Ct, mode, true) : fn}) {
+        for (const void* f : {fn, mode == MODE_FILTER ? colc_kernel(Ct, mode, true) : fn,
+                              mode == MODE_FILTER ? colc_kernel(Ct, mode, false, true) : fn}) {
             cudaFuncAttributes fa2;
             if ((e = cudaFuncGetAttributes(&fa2, f)) != cudaSuccess) return e;
             if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess ||
@@ -554,9 +626,12 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
 }
 
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
-                               float kc, const UpdateArgs* upd, float* support, cudaStream_t s, int nsq) {
+                               float kc, const UpdateArgs* upd, float* support, cudaStream_t s, int nsq,
+                               const float* ext, float* rank_tuples) {
     colc::Params p = {};
     p.nsq = nsq;
+    p.ext = ext;
+    p.rank_tuples = rank_tuples;
     p.x = x;
     p.d = d;
     p.support = support;
@@ -577,7 +652,7 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     } else {
         tx = td;
     }
-    const void* fn = colc_kernel(Ct, mode, nsq >= 0);
+    const void* fn = colc_kernel(Ct, mode, nsq >= 0, ext != nullptr);
     if (!fn) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = plan.grid;

@@ -70,7 +70,7 @@ def single(g, t, c, ss, sr, N, lam, iters):
 
 
 @pytest.mark.parametrize("P", [2, 3, 4])
-@pytest.mark.parametrize("H,W,Ct", [(60, 70, 1), (517, 130, 1), (301, 45, 3)])
+@pytest.mark.parametrize("H,W,Ct", [(60, 70, 1), (517, 130, 1), (301, 45, 3), (3000, 100, 1), (2100, 70, 3)])
 def test_bands_match_oracle_and_single(P, H, W, Ct):
     g, t, c = random_problem(H, W, 3, Ct, seed=P * 100 + H)
     args = (5.0, 0.2, 3, 0.99, 6)
@@ -118,3 +118,14 @@ def test_nccl_transport_single_rank():
         dts.dts_comm_destroy(comm)
     one = single(g, t, c, *args)
     assert np.max(np.abs(out.cpu().numpy() - one)) <= 1e-5 * target_range(t)
+
+
+def test_bands_legacy_kernel_matches(monkeypatch):
+    """The decoupled band-tuple kernel (DTS_BAND_LEGACY=1) and the cluster TUPLE / APPLY
+    kernels give the same banded solve (fp32 rounding)."""
+    g, t, c = random_problem(1500, 96, 3, 1, seed=11)
+    args = (9.0, 0.3, 3, 0.99, 4)
+    a = solve_bands(g, t, c, *args, P=2)
+    monkeypatch.setenv("DTS_BAND_LEGACY", "1")
+    b = solve_bands(g, t, c, *args, P=2)
+    assert np.max(np.abs(a - b)) <= 1e-5 * target_range(t)
