@@ -84,6 +84,9 @@ struct dts_ctx {
     float* gathered = nullptr;  // all ranks' tuples               [P][ntiles][2NV+3][32]
     float* ext = nullptr;       // carries into this rank's rows   [ntiles][2][NV][32]
     size_t band_cap = 0;
+    // edge fix-up scheme, per pass (nullptr: band too short, TUPLE/APPLY instead)
+    std::vector<float*> edge_gam, edge_theta;  // L x pitch each: Gamma (top rows), Theta (bottom rows)
+    std::vector<int> edge_L;
     int num_sms = 148;
     Geometry g{};
     int C = 0;
@@ -351,8 +354,53 @@ dts_status ensure_band_buffers(dts_ctx* ctx, cudaStream_t s) {
 // via NCCL, or the loopback transport), each rank composes the carries into its rows,
 // and the pass is finished with those carries (APPLY).
 dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, const UpdateArgs* upd,
-                           float* support, int fam, double bytes, cudaStream_t s) {
+                           float* support, int fam, double bytes, cudaStream_t s, int pass) {
     const Geometry& g = ctx->g;
+    // edge fix-up scheme (bands of >= 2L rows, profiles built at create): the zero-carry
+    // pass exports y at row H - 1 and z at row 0, one all-gather of those per-column values,
+    // then the corrections on the L rows at each edge
+    ColPlan pE;
+    if (mode != MODE_SUPPORT && pass >= 0 && pass < (int)ctx->edge_gam.size() && ctx->edge_gam[pass] &&
+        !std::getenv("DTS_BAND_TUPLE") && plan_col_cluster(g, Ct, MODE_FILTER, ctx->num_sms, &pE) == cudaSuccess) {
+        dts_status st;
+        cudaError_t e;
+        if ((st = ensure_band_buffers(ctx, s)) != DTS_OK) return st;
+        const int L = ctx->edge_L[pass];
+        const int NT = 2 * Ct + 1;
+        const size_t count = (size_t)pE.ntiles * NT * 32;
+        const double px = (double)g.H * g.W;
+        if ((e = cudaMemsetAsync(ctx->ext, 0, (size_t)pE.ntiles * 2 * Ct * 32 * sizeof(float), s)) != cudaSuccess)
+            return cuda_fail(e);
+        st = run_launch(ctx, F_COL, px * (8.0 * Ct + 4), s, [&] {
+            return launch_col_cluster(pE, g, Ct, MODE_FILTER, x, ctx->dy, kc, nullptr, nullptr, s, -1, ctx->ext,
+                                      nullptr, ctx->rank_tup);
+        });
+        if (st != DTS_OK) return st;
+        // Gamma_0 of this rank into slot 2Ct of its records
+        if ((e = cudaMemcpy2DAsync(ctx->rank_tup + 2 * Ct * 32, NT * 32 * sizeof(float), ctx->edge_gam[pass],
+                                   32 * sizeof(float), 32 * sizeof(float), pE.ntiles, cudaMemcpyDeviceToDevice, s)) !=
+            cudaSuccess)
+            return cuda_fail(e);
+        std::string err;
+        st = run_launch(ctx, F_EXCHANGE, (double)count * 4 * ctx->comm->nranks, s, [&] {
+            return comm_allgather(ctx->comm, ctx->rank_tup, ctx->gathered, count, s, &err) ? cudaSuccess
+                                                                                            : cudaErrorUnknown;
+        });
+        if (st != DTS_OK) {
+            g_last_error = err;
+            return DTS_E_NCCL;
+        }
+        st = run_launch(ctx, F_COMPOSE, (double)2 * L * g.W * (8.0 * Ct + 4), s, [&] {
+            return launch_edge_fix(x, Ct, g, L, ctx->edge_gam[pass], ctx->edge_theta[pass], ctx->gathered,
+                                   ctx->comm->nranks, ctx->comm->rank, s);
+        });
+        if (st != DTS_OK || mode != MODE_UPDATE) return st;
+        return run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
+            return launch_update(x, upd->Z, upd->T, upd->chat, Ct, g, upd->lam, upd->step, upd->out_hwc, ctx->num_sms,
+                                 s);
+        });
+    }
+    cudaGetLastError();
     // cluster kernels when the band's columns fit a cluster: TUPLE (the rank 5-tuple, with the
     // carry sensitivity as an extra channel) -> all-gather -> compose -> FILTER with the
     // external carries (+ the streaming update kernel for the last pass of an iteration)
@@ -619,7 +667,7 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
     if (st == DTS_OK) {
         if (comm)
             st = col_pass_banded(ctx, 1, MODE_SUPPORT, nullptr, ctx->ks, nullptr, ctx->S, F_SUPPORT_COL, px * 12.0,
-                                 s);
+                                 s, -1);
         else if (cp.kind == 1) {  // cluster kernel: s_y into its own plane (no read-modify-write of S)
             if ((e = cudaMallocAsync((void**)&ctx->Sy, plane, s)) != cudaSuccess) st = cuda_fail(e);
             if (st == DTS_OK)
@@ -629,6 +677,32 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
         } else {
             st = run_launch(ctx, F_SUPPORT_COL, px * 12.0, s, [&] {
                 return col_launch(ctx, cp, 1, MODE_SUPPORT, nullptr, ctx->dy, ctx->ks, nullptr, ctx->S, s);
+            });
+        }
+    }
+    // row-band contexts: edge profiles of every pass whose edge distance L (carry influence
+    // < 2^-26 after L rows, d >= 1 so a <= a_i = e^{-sqrt2/sigma_i}) fits twice in the band
+    if (st == DTS_OK && comm) {
+        ctx->edge_gam.assign(filter_passes, nullptr);
+        ctx->edge_theta.assign(filter_passes, nullptr);
+        ctx->edge_L.assign(filter_passes, 0);
+        for (int i = 1; i <= filter_passes && st == DTS_OK; ++i) {
+            const double sig = sigma_s * std::sqrt(3.0) * std::pow(2.0, filter_passes - i) / denom;
+            const double ai = std::exp(-sqrt2 / sig);
+            const int64_t L = ai > 0.0 ? (int64_t)std::ceil(std::log(std::ldexp(1.0, -26)) / std::log(ai)) : 1;
+            if (L < 1 || 2 * L + 1 > H || L > (1 << 20)) continue;
+            float *gam = nullptr, *th = nullptr;
+            const size_t b = (size_t)L * ctx->g.pitch * sizeof(float);
+            if ((e = cudaMallocAsync((void**)&gam, b, s)) != cudaSuccess ||
+                (e = cudaMallocAsync((void**)&th, b, s)) != cudaSuccess) {
+                st = cuda_fail(e);
+                break;
+            }
+            ctx->edge_gam[i - 1] = gam;
+            ctx->edge_theta[i - 1] = th;
+            ctx->edge_L[i - 1] = (int)L;
+            st = run_launch(ctx, F_COEF, (double)H * ctx->g.W * 8.0, s, [&] {
+                return launch_edge_profiles(ctx->dy, ctx->g, (int)L, ctx->kc[i - 1], gam, th, s);
             });
         }
     }
@@ -1004,7 +1078,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                     if (ctx->comm) {  // row-band mode: TUPLE -> all-gather -> compose -> APPLY
                         if (i + 1 < ctx->N) {
                             st = col_pass_banded(ctx, Ct, MODE_FILTER, ctx->X, ctx->kc[i], nullptr, nullptr, F_COL,
-                                                 row_bytes, s);
+                                                 row_bytes, s, i);
                         } else {
                             UpdateArgs u;
                             u.Z = ctx->Z;
@@ -1014,7 +1088,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                             u.step = step;
                             u.out_hwc = (k + 1 == iterations) ? o_d : nullptr;
                             st = col_pass_banded(ctx, Ct, MODE_UPDATE, ctx->X, ctx->kc[i], &u, nullptr, F_UPDATE,
-                                                 upd_bytes, s);
+                                                 upd_bytes, s, i);
                         }
                     } else if (i + 1 < ctx->N) {
                         st = run_launch(ctx, F_COL, row_bytes, s, [&] { return col_filter(i); });
@@ -1306,6 +1380,10 @@ void dts_destroy(dts_ctx* ctx) {
     if (ctx->v_tuples) cudaFreeAsync(ctx->v_tuples, s);
     if (ctx->v_flags) cudaFreeAsync(ctx->v_flags, s);
     if (ctx->win) cudaFreeAsync(ctx->win, s);
+    for (float* q : ctx->edge_gam)
+        if (q) cudaFreeAsync(q, s);
+    for (float* q : ctx->edge_theta)
+        if (q) cudaFreeAsync(q, s);
     if (ctx->graph_exec) {  // a replay may still be in flight on s
         cudaStreamSynchronize(s);
         cudaGraphExecDestroy(ctx->graph_exec);

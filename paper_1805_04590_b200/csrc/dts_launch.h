@@ -75,7 +75,8 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
                                float kc, const UpdateArgs* upd, float* support, cudaStream_t s,
                                int nsq = -1,  // nsq >= 0: d holds A1 (see coef_pow)
                                const float* ext = nullptr,    // APPLY: carries into the rank band [ntiles][2][Ct][32]
-                               float* rank_tuples = nullptr);  // TUPLE: [ntiles][2Ct+3][32]
+                               float* rank_tuples = nullptr,   // TUPLE: [ntiles][2Ct+3][32]
+                               float* edge = nullptr);         // edge scheme: [ntiles][2Ct+1][32]
 
 // K3/K4 streaming path (k_colv.cu): decoupled band-tuple scan over 64-column tiles with
 // shared-memory-held items and a TMA producer warp; FILTER and UPDATE (fused Eq. 3).
@@ -153,5 +154,12 @@ cudaError_t launch_box_col(const BoxPlan& plan, const Geometry& g, int Ct, const
 
 // A1 = a_1^d = 2^(-kc d) elementwise over n floats (the column kernel's pass-1 coefficient).
 cudaError_t launch_coef(const float* d, float* a1, int64_t n, float kc, cudaStream_t s);
+
+// Row-band edge fix-up scheme (k_colc.cu): create-time edge profiles of one pass, and the
+// elementwise corrections after the gathered edge records.
+cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float kc, float* gam, float* theta,
+                                 cudaStream_t s);
+cudaError_t launch_edge_fix(float* x, int Ct, const Geometry& g, int L, const float* gam, const float* theta,
+                            const float* gathered, int P, int rank, cudaStream_t s);
 
 }  // namespace dts

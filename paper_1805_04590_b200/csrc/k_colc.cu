@@ -41,6 +41,7 @@ struct Params {
     // top, anticausal e at the bottom), [ntiles][2][CT][TW]; TUPLE output [ntiles][2CT+3][TW]
     const float* ext;
     float* rank_tuples;
+    float* edge;  // BAND FILTER (edge fix-up scheme): [ntiles][2CT+1][TW]: y at row H-1, z at row 0
 };
 
 struct Smem {
@@ -352,6 +353,18 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
             segR[(0 * S + s) * (TW + 1) + c] = Q;
 #pragma unroll
             for (int v = 0; v < NV; ++v) segR[((1 + v) * S + s) * (TW + 1) + c] = E[v];
+            if constexpr (BAND && MODE == MODE_FILTER) {  // edge scheme: y at row H - 1 (c = 0)
+                const int jl = p.H - 1 - (r0 + lo);
+                if (p.edge && colok && jl >= 0 && jl < LS) {
+                    float* ed = p.edge + (int64_t)tile * (2 * CT + 1) * TW;
+#pragma unroll
+                    for (int j = 0; j < LS; ++j)
+                        if (j == jl) {
+#pragma unroll
+                            for (int v = 0; v < CT; ++v) ed[v * TW + c] = xv[v][j];
+                        }
+                }
+            }
             if constexpr (MODE == MODE_TUPLE) {  // rank causal map c_out = A c + B: y at row H - 1
                 const int jl = p.H - 1 - (r0 + lo);  // of the x channels (c = 0) and of g (c = 1)
                 if (colok && jl >= 0 && jl < LS) {
@@ -424,6 +437,13 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
             }
         }
 
+        if constexpr (BAND && MODE == MODE_FILTER) {  // edge scheme: z at row 0 (c = e = 0)
+            if (p.edge && colok && band == 0 && s == 0) {
+                float* ed = p.edge + (int64_t)tile * (2 * CT + 1) * TW;
+#pragma unroll
+                for (int v = 0; v < CT; ++v) ed[(CT + v) * TW + c] = xv[v][0];
+            }
+        }
         // ---- 5. write-out straight from registers (TUPLE: nothing; the tuple is written) ----
         if constexpr (MODE != MODE_TUPLE) {
             const int nrow = min(LS, p.H - (r0 + lo));
@@ -627,11 +647,12 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
 
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
                                float kc, const UpdateArgs* upd, float* support, cudaStream_t s, int nsq,
-                               const float* ext, float* rank_tuples) {
+                               const float* ext, float* rank_tuples, float* edge) {
     colc::Params p = {};
     p.nsq = nsq;
     p.ext = ext;
     p.rank_tuples = rank_tuples;
+    p.edge = edge;
     p.x = x;
     p.d = d;
     p.support = support;
@@ -669,6 +690,84 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     void* args[] = {&tx, &td, &p};
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// Row-band edge fix-up scheme.  A carry entering a band at its top
+// edge changes y by c G_k (G_k = prod_{j<=k} a_j) and z by c Gamma_k (Gamma = the anticausal
+// response of G); one entering at the bottom changes z by e Theta_k (Theta_k =
+// prod_{j=k+1..H} a_j).  Both decay at least like a_i^k; past L rows they are below fp32
+// resolution, so with bands of >= 2L rows the banded pass is the zero-carry pass plus
+// these two corrections on the L rows at each edge.
+
+// per column, sequential over the edge rows (create time): Gamma (top L rows), Theta
+// (bottom L rows, row H - L first); d has rows 0..H (row H: the link below the band)
+__global__ void k_edge_profiles(const float* __restrict__ d, int64_t H, int64_t W, int64_t pitch, int L, float kc,
+                                float* __restrict__ gam, float* __restrict__ theta) {
+    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= W) return;
+    float G = 1.f;
+    for (int k = 0; k < L; ++k) {  // G_k = prod_{j <= k} a_j (a_0: the link to the band above)
+        G *= coef_from_d(__ldg(d + (int64_t)k * pitch + col), kc);
+        gam[(int64_t)k * pitch + col] = G;
+    }
+    float dz = 0.f;  // anticausal response, zero at row L (below resolution)
+    for (int k = L - 1; k >= 0; --k) {
+        const float an = coef_from_d(__ldg(d + (int64_t)(k + 1) * pitch + col), kc);
+        const float g = gam[(int64_t)k * pitch + col];
+        dz = fmaf(an, dz - g, g);
+        gam[(int64_t)k * pitch + col] = dz;
+    }
+    float th = coef_from_d(__ldg(d + H * pitch + col), kc);  // a_H
+    for (int64_t k = H - 1; k >= H - L; --k) {
+        theta[(k - (H - L)) * pitch + col] = th;
+        th *= coef_from_d(__ldg(d + k * pitch + col), kc);
+    }
+}
+
+cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float kc, float* gam, float* theta,
+                                 cudaStream_t s) {
+    k_edge_profiles<<<(unsigned)((g.W + 127) / 128), 128, 0, s>>>(d, g.H, g.W, g.pitch, L, kc, gam, theta);
+    return cudaGetLastError();
+}
+
+// the corrections: x[v][k] += c_v Gamma_k (k < L), x[v][k] += e_v Theta_{k-H+L} (k >= H - L), with
+// c = y_last of the rank above and e = z_top0 + y_last(this rank) Gamma_0 of the rank below,
+// all from the gathered edge records [P][ntiles][2Ct+1][32] (slot 2Ct: Gamma_0)
+__global__ void k_edge_fix(float* __restrict__ x, int Ct, int64_t H, int64_t W, int64_t pitch, int64_t plane, int L,
+                           const float* __restrict__ gam, const float* __restrict__ theta,
+                           const float* __restrict__ gath, int P, int rank, int ntiles) {
+    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int kk = blockIdx.y;  // 0..2L-1: top rows, then bottom rows
+    if (col >= W) return;
+    const int NT = 2 * Ct + 1;
+    const int64_t t = col / colc::TW, cc = col - t * colc::TW;
+    const int64_t rstride = (int64_t)ntiles * NT * colc::TW;
+    const bool top = kk < L;
+    const int64_t row = top ? kk : H - L + (kk - L);
+    for (int v = 0; v < Ct; ++v) {
+        float carry = 0.f;
+        if (top) {
+            if (rank > 0) carry = gath[(rank - 1) * rstride + (t * NT + v) * colc::TW + cc];
+        } else if (rank + 1 < P) {
+            const float* nb = gath + (rank + 1) * rstride + t * NT * colc::TW;
+            const float ylast = gath[rank * rstride + (t * NT + v) * colc::TW + cc];
+            carry = fmaf(ylast, nb[(2 * Ct) * colc::TW + cc], nb[(Ct + v) * colc::TW + cc]);
+        }
+        if (carry != 0.f) {
+            const float prof = top ? gam[(int64_t)kk * pitch + col] : theta[(int64_t)(kk - L) * pitch + col];
+            float* q = x + v * plane + row * pitch + col;
+            *q = fmaf(carry, prof, *q);
+        }
+    }
+}
+
+cudaError_t launch_edge_fix(float* x, int Ct, const Geometry& g, int L, const float* gam, const float* theta,
+                            const float* gathered, int P, int rank, cudaStream_t s) {
+    const int ntiles = (int)((g.W + colc::TW - 1) / colc::TW);
+    dim3 grid((unsigned)((g.W + 127) / 128), (unsigned)(2 * L));
+    k_edge_fix<<<grid, 128, 0, s>>>(x, Ct, g.H, g.W, g.pitch, g.plane, L, gam, theta, gathered, P, rank, ntiles);
     return cudaGetLastError();
 }
 

@@ -129,3 +129,18 @@ def test_bands_legacy_kernel_matches(monkeypatch):
     monkeypatch.setenv("DTS_BAND_LEGACY", "1")
     b = solve_bands(g, t, c, *args, P=2)
     assert np.max(np.abs(a - b)) <= 1e-5 * target_range(t)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_bands_edge_scheme_matches_tuple_scheme(P, monkeypatch):
+    """Bands of >= 2L rows use the edge fix-up scheme (zero-carry pass + corrections on the L
+    rows at each edge); DTS_BAND_TUPLE=1 forces the exact TUPLE / APPLY composition.  The two
+    agree to fp32 rounding, and both match the oracle."""
+    g, t, c = random_problem(900, 80, 3, 1, seed=17 + P)
+    args = (5.0, 0.2, 3, 0.99, 5)
+    a = solve_bands(g, t, c, *args, P=P)
+    monkeypatch.setenv("DTS_BAND_TUPLE", "1")
+    b = solve_bands(g, t, c, *args, P=P)
+    rng = target_range(t)
+    assert np.max(np.abs(a - b)) <= 1e-5 * rng
+    assert np.max(np.abs(a - oracle.solve(g, t, c, *args))) <= 1e-4 * rng
