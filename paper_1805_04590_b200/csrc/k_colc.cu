@@ -37,11 +37,6 @@ struct Params {
     int H, W, HB, S, CB, ntiles;
     float kc;
     int nsq;  // < 0: d holds distances (a = 2^(-kc d)); >= 0: d holds A1, a = A1^(2^nsq)
-    // row-band mode: APPLY carries into the rank band (causal c at the
-    // top, anticausal e at the bottom), [ntiles][2][CT][TW]; TUPLE output [ntiles][2CT+3][TW]
-    const float* ext;
-    float* rank_tuples;
-    float* edge;  // BAND FILTER (edge fix-up scheme): [ntiles][2CT+1][TW]: y at row H-1, z at row 0
 };
 
 struct Smem {
@@ -49,12 +44,11 @@ struct Smem {
     size_t bytes;
 };
 
-// NX planes of x staged per tile, NV channels carried (TUPLE: NX + 1, the carry sensitivity)
-__host__ __device__ inline Smem layout(int NX, int NV, int HB, int S) {
+__host__ __device__ inline Smem layout(int NV, int HB, int S) {
     Smem L;
     int o = 0;
     L.land_x = o;
-    o += NX * HB * TW;
+    o += NV * HB * TW;
     L.land_d = o;
     o += HB * TW;
     L.segF = o;
@@ -117,22 +111,372 @@ __device__ __forceinline__ void seg_scan(float* seg, int S, int cc, float* tot) 
 template <int NV>
 constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
 
+template <int CT, int MODE, bool PRE>
+__global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>(), 1)
+    k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
+    constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
+    constexpr bool HASX = MODE != MODE_SUPPORT;
+    extern __shared__ __align__(128) float smem[];
+    const int HB = p.HB, S = p.S, CB = p.CB;
+    const Smem L = layout(NV, HB, S);
+    float* lx = smem + L.land_x;
+    float* ld = smem + L.land_d;
+    float* segF = smem + L.segF;
+    float* segR = smem + L.segR;
+    float* totC = smem + L.totC;
+    float* totA = smem + L.totA;
+    float* remC = smem + L.remC;
+    float* remA = smem + L.remA;
+    float* carry = smem + L.carry;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* xbarC = bars + S;      // causal totals from the bands above have landed
+    uint64_t* xbarA = bars + S + 1;  // anticausal totals from the bands below have landed
+
+    const int c = threadIdx.x & 31;
+    const int s = threadIdx.x >> 5;
+    const int band = (int)cluster_ctarank();
+    const int cluster = blockIdx.x / CB;
+    const int nclusters = gridDim.x / CB;
+    const int r0 = band * HB;
+    const int lo = s * LS;
+    // PRE: d holds A1 = a_1^d and this pass's coefficient is A1^(2^nsq), nsq <= 3 (uniform)
+    const int nsq = p.nsq;
+    auto coef = [&](float v) {
+        if constexpr (PRE) {
+            float a1 = v;
+            if (nsq > 0) a1 *= a1;
+            if (nsq > 1) a1 *= a1;
+            if (nsq > 2) a1 *= a1;
+            return a1;
+        } else {
+            return coef_from_d(v, p.kc);
+        }
+    };
+
+    const uint32_t xbytesC = (uint32_t)(band * (NV + 1) * TW * sizeof(float));
+    const uint32_t xbytesA = (uint32_t)((CB - 1 - band) * (NV + 1) * TW * sizeof(float));
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
+        mbar_init(xbarC, 1);
+        mbar_init(xbarA, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(xbarC, xbytesC);  // armed for the first tile
+        mbar_arrive_expect_tx(xbarA, xbytesA);
+        tma_prefetch_desc(&tm_d);
+        if (HASX) tma_prefetch_desc(&tm_x);
+    }
+    cluster_sync_all();  // every exchange barrier of the cluster is initialised and armed
+
+    auto stage_in = [&](int tile) {  // thread 0: TMA boxes of `tile` into the landing zone
+        const int col0 = tile * TW;
+        const uint32_t box = (uint32_t)(LS * TW * sizeof(float));
+        for (int q = 0; q < S; ++q) {
+            const int rq = r0 + q * LS;
+            const uint32_t bytes = rq < p.H ? box * (1 + (HASX ? NV : 0)) : 0u;
+            mbar_arrive_expect_tx(&bars[q], bytes);
+            if (bytes) {
+                tma_load_2d(ld + q * LS * TW, &tm_d, col0, rq, &bars[q]);
+                if constexpr (HASX) {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) tma_load_3d(lx + (v * HB + q * LS) * TW, &tm_x, col0, rq, v, &bars[q]);
+                }
+            }
+        }
+    };
+    if (threadIdx.x == 0 && cluster < p.ntiles) stage_in(cluster);
+
+    int k = 0;
+    for (int tile = cluster; tile < p.ntiles; tile += nclusters, ++k) {
+        const int col0 = tile * TW;
+        const int col = col0 + c;
+        const bool colok = col < p.W;
+
+        // ---- 1. landing zone -> registers; refill with the next tile ----
+        mbar_wait(&bars[s], (uint32_t)(k & 1));
+        float a[LS];
+        float xv[NV][LS];
+        if (r0 + lo + LS <= p.H) {
+            // every row of the segment is in the image (warp-uniform): no per-row checks.
+            // Lanes past W read the row padding; their values stay in their own column
+            // (every step of the pass is per column) and are never stored.
+            const float* ldc = ld + lo * TW + c;
+#pragma unroll
+            for (int j = 0; j < LS; ++j) {
+                a[j] = coef(ldc[j * TW]);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    if constexpr (HASX) xv[v][j] = lx[(v * HB + lo + j) * TW + c];
+                    else xv[v][j] = 0.f;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < LS; ++j) {
+                const int rr = lo + j;
+                const bool ok = colok && (r0 + rr) < p.H;
+                a[j] = ok ? coef(ld[rr * TW + c]) : 0.f;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    if constexpr (HASX) xv[v][j] = ok ? lx[(v * HB + rr) * TW + c] : 0.f;
+                    else xv[v][j] = 0.f;
+                }
+            }
+        }
+        // coefficient linking this segment's last row to the next row: from the
+        // landing zone (next segment; it landed before the barrier below) or, for the
+        // band's last segment, straight from global (first row of the next band)
+        float anext = 0.f;
+        {
+            const int rn = r0 + lo + LS;
+            if (s + 1 == S && colok && rn < p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
+        }
+        __syncthreads();
+        if (s + 1 < S) {
+            const int rn = r0 + lo + LS;
+            anext = (colok && rn < p.H) ? coef(ld[(lo + LS) * TW + c]) : 0.f;
+        }
+        __syncthreads();  // landing zone free
+        if (threadIdx.x == 0 && tile + nclusters < p.ntiles) stage_in(tile + nclusters);
+        if constexpr (MODE == MODE_UPDATE) {  // the write-out's Z / T / chat lines -> L2 (lane = row)
+            const int r = r0 + lo + c;
+            if (r < p.H) {
+                const int64_t o = (int64_t)r * p.pitch + col0;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    prefetch_l2(p.upd.Z + v * p.plane + o);
+                    prefetch_l2(p.upd.T + v * p.plane + o);
+                }
+                prefetch_l2(p.upd.chat + o);
+            }
+        }
+
+        // ---- 2. causal fold, segment scan, band total ----
+        {
+            Aff<NV> m = aff_identity<NV>();
+#pragma unroll
+            for (int j = 0; j < LS; ++j) {
+                m.P *= a[j];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    if constexpr (HASX) m.B[v] = fmaf(a[j], m.B[v] - xv[v][j], xv[v][j]);
+                    else m.B[v] = fmaf(a[j], m.B[v], 1.f);
+                }
+            }
+            segF[(0 * S + s) * (TW + 1) + c] = m.P;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) segF[((1 + v) * S + s) * (TW + 1) + c] = m.B[v];
+        }
+        __syncthreads();
+        for (int cc = s; cc < TW; cc += S) seg_scan<NV, false>(segF, S, cc, totC);
+        __syncthreads();
+
+        // ---- 3. push this band's causal total to every band below it (st.async into their
+        //         shared memory, completing on their exchange barrier); warp 0 waits for the
+        //         totals of the bands above and composes the causal carry ----
+        for (int q = band + 1 + s; q < CB; q += S) {
+#pragma unroll
+            for (int k2 = 0; k2 < NV + 1; ++k2)
+                st_async_f32(remC + (band * (NV + 1) + k2) * TW + c, totC[k2 * TW + c], xbarC, (uint32_t)q);
+        }
+        if (s == 0) {
+            mbar_wait_cluster(xbarC, (uint32_t)(k & 1));
+            if (c == 0) mbar_arrive_expect_tx(xbarC, xbytesC);  // re-arm for the next tile
+            float cin[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) cin[v] = 0.f;
+            for (int q = 0; q < band; ++q) {
+                const float P = remC[(q * (NV + 1)) * TW + c];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) cin[v] = fmaf(P, cin[v], remC[(q * (NV + 1) + 1 + v) * TW + c]);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) carry[v * TW + c] = cin[v];
+        }
+        __syncthreads();
+        {
+            const float eP = segF[(0 * S + s) * (TW + 1) + c];
+            float y[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) y[v] = fmaf(eP, carry[v * TW + c], segF[((1 + v) * S + s) * (TW + 1) + c]);
+            float Q = 1.f, E[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) E[v] = 0.f;
+#pragma unroll
+            for (int j = 0; j < LS; ++j) {
+                const float an = (j + 1 < LS) ? a[j + 1] : anext;
+                if constexpr (HASX) {
+                    const float qb = Q * (1.f - an);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        y[v] = fmaf(a[j], y[v] - xv[v][j], xv[v][j]);
+                        xv[v][j] = y[v];
+                        E[v] = fmaf(qb, y[v], E[v]);
+                    }
+                } else {
+                    y[0] = fmaf(a[j], y[0], 1.f);
+                    xv[0][j] = y[0];
+                    E[0] += Q;
+                }
+                Q *= an;
+            }
+            segR[(0 * S + s) * (TW + 1) + c] = Q;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) segR[((1 + v) * S + s) * (TW + 1) + c] = E[v];
+        }
+        __syncthreads();
+        for (int cc = s; cc < TW; cc += S) seg_scan<NV, true>(segR, S, cc, totA);
+        __syncthreads();
+
+        // ---- 4. anticausal totals flow upwards the same way ----
+        for (int q = band - 1 - s; q >= 0; q -= S) {
+#pragma unroll
+            for (int k2 = 0; k2 < NV + 1; ++k2)
+                st_async_f32(remA + (band * (NV + 1) + k2) * TW + c, totA[k2 * TW + c], xbarA, (uint32_t)q);
+        }
+        if (s == 0) {
+            mbar_wait_cluster(xbarA, (uint32_t)(k & 1));
+            if (c == 0) mbar_arrive_expect_tx(xbarA, xbytesA);
+            float ein[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) ein[v] = 0.f;
+            for (int q = CB - 1; q > band; --q) {
+                const float Qb = remA[(q * (NV + 1)) * TW + c];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) ein[v] = fmaf(Qb, ein[v], remA[(q * (NV + 1) + 1 + v) * TW + c]);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) carry[v * TW + c] = ein[v];
+        }
+        __syncthreads();
+        {
+            const float eQ = segR[(0 * S + s) * (TW + 1) + c];
+            float z[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) z[v] = fmaf(eQ, carry[v * TW + c], segR[((1 + v) * S + s) * (TW + 1) + c]);
+#pragma unroll
+            for (int j = LS - 1; j >= 0; --j) {
+                const float an = (j + 1 < LS) ? a[j + 1] : anext;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const float yv = xv[v][j];
+                    if constexpr (HASX) {
+                        z[v] = fmaf(an, z[v] - yv, yv);
+                        xv[v][j] = z[v];
+                    } else {
+                        z[v] = fmaf(an, z[v], 1.f);
+                        xv[v][j] = yv + z[v] - 1.f;  // s_y = P + Q - 1
+                    }
+                }
+            }
+        }
+
+        // ---- 5. write-out straight from registers ----
+        {
+            const int nrow = min(LS, p.H - (r0 + lo));
+            if (colok && nrow > 0) {
+                if constexpr (MODE == MODE_FILTER || MODE == MODE_SUPPORT) {
+                    float* base = (MODE == MODE_FILTER ? p.x : p.support) + (int64_t)(r0 + lo) * p.pitch + col;
+                    const int64_t pitch = p.pitch;
+                    if (nrow == LS) {  // full segment: a running pointer, no per-row checks
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) {
+                            float* q = base + v * p.plane;
+#pragma unroll
+                            for (int j = 0; j < LS; ++j, q += pitch) *q = xv[v][j];
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < LS; ++j)
+                            if (j < nrow) {
+#pragma unroll
+                                for (int v = 0; v < NV; ++v) base[v * p.plane + (int64_t)j * pitch] = xv[v][j];
+                            }
+                    }
+                } else {  // MODE_UPDATE, Eq. (3) with zbar = xv; Z / T / chat were prefetched
+                          // into L2 when the tile started; 16 rows of loads in flight at a time
+                    constexpr int UB = 16;
+                    const int64_t pitch = p.pitch;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+#pragma unroll
+                        for (int j0 = 0; j0 < LS; j0 += UB) {
+                            float zo[UB], tv[UB], ch[UB];
+#pragma unroll
+                            for (int u = 0; u < UB; ++u) {
+                                const int jj = (j0 + u < nrow) ? j0 + u : 0;
+                                const int64_t o = (int64_t)(r0 + lo + jj) * pitch + col;
+                                zo[u] = p.upd.Z[v * p.plane + o];
+                                tv[u] = __ldg(p.upd.T + v * p.plane + o);
+                                ch[u] = __ldg(p.upd.chat + o);
+                            }
+#pragma unroll
+                            for (int u = 0; u < UB; ++u) {
+                                const int j = j0 + u;
+                                if (j < nrow) {
+                                    const int64_t r = r0 + lo + j;
+                                    const float g = fmaf(p.upd.lam, zo[u] - xv[v][j], ch[u] * (zo[u] - tv[u]));
+                                    const float zn = fmaf(-p.upd.step, g, zo[u]);
+                                    if (p.upd.out_hwc) p.upd.out_hwc[(r * p.W + col) * CT + v] = zn;
+                                    else p.upd.Z[v * p.plane + r * pitch + col] = zn;
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();  // segF / segR / carry reused by the next tile
+    }
+    cluster_sync_all();  // no CTA leaves while another may still read its shared memory
+}
+
+
+// ---------------------------------------------------------------------------------------
+// Row-band variant.  A separate kernel so that the single-GPU
+// instantiations above keep their exact code: MODE_TUPLE emits the rank band's 5-tuple
+// (one extra channel, the carry sensitivity); BAND FILTER takes external carries and, for
+// the edge fix-up scheme, exports y at row H - 1 and z at row 0.
+struct BandParams : Params {
+    // APPLY carries into the rank band (causal c at the top, anticausal e at the bottom),
+    // [ntiles][2][CT][TW]; TUPLE output [ntiles][2CT+3][TW]; edge scheme [ntiles][2CT+1][TW]
+    const float* ext;
+    float* rank_tuples;
+    float* edge;
+};
+
+// NX planes of x staged per tile, NV channels carried (TUPLE: NX + 1)
+__host__ __device__ inline Smem layout_band(int NX, int NV, int HB, int S) {
+    Smem L = layout(NV, HB, S);
+    const int shrink = (NV - NX) * HB * TW;  // the carried-only channels are not staged
+    L.land_d -= shrink;
+    L.segF -= shrink;
+    L.segR -= shrink;
+    L.totC -= shrink;
+    L.totA -= shrink;
+    L.remC -= shrink;
+    L.remA -= shrink;
+    L.carry -= shrink;
+    L.bars -= shrink;
+    L.bytes -= (size_t)shrink * sizeof(float);
+    return L;
+}
+
 template <int CT, int MODE>
 __host__ __device__ constexpr int nchan() { return MODE == MODE_SUPPORT ? 1 : (MODE == MODE_TUPLE ? CT + 1 : CT); }
 
 // BAND (row-band mode, MODE_TUPLE or FILTER with external carries): rows past H are identity
 // maps and row H is the link to the next rank; the single-GPU instantiations keep the
 // plain code (a = 0 past H, no external carries)
-template <int CT, int MODE, bool PRE, bool BAND = (MODE == MODE_TUPLE)>
+template <int CT, int MODE, bool PRE, bool BAND>
 __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
-    k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
+    k_col_cluster_band(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const BandParams p) {
     // TUPLE: channel CT is the carry sensitivity g (x = 0, carry-in 1 at the rank band's top)
     constexpr int NV = nchan<CT, MODE>();
     constexpr int NX = (MODE == MODE_SUPPORT) ? 0 : CT;  // x planes staged
     constexpr bool HASX = MODE != MODE_SUPPORT;
     extern __shared__ __align__(128) float smem[];
     const int HB = p.HB, S = p.S, CB = p.CB;
-    const Smem L = layout(NX, NV, HB, S);
+    const Smem L = layout_band(NX, NV, HB, S);
     float* lx = smem + L.land_x;
     float* ld = smem + L.land_d;
     float* segF = smem + L.segF;
@@ -255,14 +599,17 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
                     else if (s + 1 == S || rn == p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
                 }
             } else {
-                if ((s + 1 == S || rn == p.H) && colok && rn <= p.H)
-                    anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
+                if (s + 1 == S && colok && rn < p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
             }
         }
         __syncthreads();
         if (s + 1 < S) {
             const int rn = r0 + lo + LS;
-            if (colok && rn < p.H) anext = coef(ld[(lo + LS) * TW + c]);
+            if constexpr (BAND) {
+                if (colok && rn < p.H) anext = coef(ld[(lo + LS) * TW + c]);
+            } else {
+                anext = (colok && rn < p.H) ? coef(ld[(lo + LS) * TW + c]) : 0.f;
+            }
         }
         __syncthreads();  // landing zone free
         if (threadIdx.x == 0 && tile + nclusters < p.ntiles) stage_in(tile + nclusters);
@@ -532,17 +879,21 @@ static bool tmap(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int CT, int MODE, bool PRE = false, bool BAND = (MODE == MODE_TUPLE)>
+template <int CT, int MODE, bool PRE = false>
 static const void* kptr() {
-    return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE, PRE, BAND>);
+    return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE, PRE>);
+}
+template <int CT, int MODE>
+static const void* kptr_band() {
+    return reinterpret_cast<const void*>(colc::k_col_cluster_band<CT, MODE, false, true>);
 }
 static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = false) {
     if (mode == MODE_SUPPORT) return kptr<1, MODE_SUPPORT>();
     if (band && mode == MODE_FILTER) {  // APPLY of the row-band exchange
         switch (Ct) {
-            case 1: return kptr<1, MODE_FILTER, false, true>();
-            case 2: return kptr<2, MODE_FILTER, false, true>();
-            case 3: return kptr<3, MODE_FILTER, false, true>();
+            case 1: return kptr_band<1, MODE_FILTER>();
+            case 2: return kptr_band<2, MODE_FILTER>();
+            case 3: return kptr_band<3, MODE_FILTER>();
         }
         return nullptr;
     }
@@ -556,9 +907,9 @@ static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = f
     }
     if (mode == MODE_TUPLE) {
         switch (Ct) {
-            case 1: return kptr<1, MODE_TUPLE>();
-            case 2: return kptr<2, MODE_TUPLE>();
-            case 3: return kptr<3, MODE_TUPLE>();
+            case 1: return kptr_band<1, MODE_TUPLE>();
+            case 2: return kptr_band<2, MODE_TUPLE>();
+            case 3: return kptr_band<3, MODE_TUPLE>();
         }
         return nullptr;
     }
@@ -591,7 +942,7 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
         const int S = (int)((HBmin + rows_seg - 1) / rows_seg);
         if (S > Smax) continue;
         const int HB = S * colc::LS;
-        const colc::Smem L = colc::layout(NX, NV, HB, S);
+        const colc::Smem L = mode == MODE_TUPLE ? colc::layout_band(NX, NV, HB, S) : colc::layout(NV, HB, S);
         if (L.bytes > 227 * 1024) continue;
         // attributes are per function and shared by every plan: allow non-portable clusters and
         // the opt-in shared memory maximum (so that no plan lowers another's limit); the
@@ -648,7 +999,7 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
                                float kc, const UpdateArgs* upd, float* support, cudaStream_t s, int nsq,
                                const float* ext, float* rank_tuples, float* edge) {
-    colc::Params p = {};
+    colc::BandParams p = {};
     p.nsq = nsq;
     p.ext = ext;
     p.rank_tuples = rank_tuples;

@@ -110,68 +110,67 @@ __global__ void __launch_bounds__(DERIV_STRIP) k_guide_deriv(const float* __rest
 
 // K1 for C % 4 == 0 (e.g. the 16-band satellite guide): one thread per pixel column,
 // walking DERIV_ROWS rows; each pixel's C channels arrive as C/4 float4 loads (a warp
-// covers one contiguous 32*C-float span), the left neighbour is the lane to the left
-// (an L1 hit), the previous row stays in registers, and the next row's loads are issued
-// before the current row's arithmetic.
+// covers one contiguous 32*C-float span), the previous row stays in registers, and the
+// next row's loads are issued before the current row's arithmetic.  Each warp covers 31
+// output columns: lane 0 loads the column before them (the left neighbour of lane 1,
+// handed over by a shuffle like every lane's) and writes nothing, so every lane keeps only
+// up / cur / next-row registers.
+constexpr int DERIV_VEC_COLS = 8 * 31;  // output columns per 256-thread block
 template <int Q>  // Q = C / 4
 __global__ void __launch_bounds__(256) k_guide_deriv_vec(const float* __restrict__ guide, float ratio2, Geometry g,
                                                          float* __restrict__ dx, float* __restrict__ dy) {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t c = (int64_t)blockIdx.x * DERIV_VEC_COLS + warp * 31 + lane - 1;  // lane 0: c0 - 1
     const int64_t rbeg = (int64_t)blockIdx.y * DERIV_ROWS;
     const int64_t rend = min(rbeg + (int64_t)DERIV_ROWS, g.H);
-    if (c >= g.pitch) return;
+    const bool writer = lane > 0 && c < g.pitch;
     const float inf = __int_as_float(0x7f800000);
-    if (c >= g.W) {
-        for (int64_t r = rbeg; r < rend; ++r) {
-            dx[r * g.pitch + c] = inf;
-            dy[r * g.pitch + c] = inf;
-        }
-        return;
+    if (c >= g.W || c < 0) {  // padding columns (writers) or the column before the image (lane 0)
+        if (writer)
+            for (int64_t r = rbeg; r < rend; ++r) {
+                dx[r * g.pitch + c] = inf;
+                dy[r * g.pitch + c] = inf;
+            }
+        // keep the warp's shuffles well-defined: fall through with a clamped column
     }
-    const int64_t cl = c > 0 ? c - 1 : 0;
-    auto px = [&](int64_t r, int64_t col) { return reinterpret_cast<const float4*>(guide + (r * g.W + col) * (4 * Q)); };
-    float4 up[Q], cur[Q], lef[Q], ncur[Q], nlef[Q];
+    const int64_t cc = c < 0 ? 0 : (c >= g.W ? g.W - 1 : c);
+    auto px = [&](int64_t r) { return reinterpret_cast<const float4*>(guide + (r * g.W + cc) * (4 * Q)); };
+    float4 up[Q], cur[Q], ncur[Q];
     if (rbeg > 0) {
-        const float4* pu = px(rbeg - 1, c);
+        const float4* pu = px(rbeg - 1);
 #pragma unroll
         for (int q = 0; q < Q; ++q) up[q] = __ldg(pu + q);
     }
     {
-        const float4* pc = px(rbeg, c);
-        const float4* pl = px(rbeg, cl);
+        const float4* pc = px(rbeg);
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            cur[q] = __ldg(pc + q);
-            lef[q] = __ldg(pl + q);
-        }
+        for (int q = 0; q < Q; ++q) cur[q] = __ldg(pc + q);
     }
     for (int64_t r = rbeg; r < rend; ++r) {
         if (r + 1 < rend) {  // next row in flight during this row's arithmetic
-            const float4* pc = px(r + 1, c);
-            const float4* pl = px(r + 1, cl);
+            const float4* pc = px(r + 1);
 #pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                ncur[q] = __ldg(pc + q);
-                nlef[q] = __ldg(pl + q);
-            }
+            for (int q = 0; q < Q; ++q) ncur[q] = __ldg(pc + q);
         }
         float sx = 0.f, sy = 0.f;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            const float ax = cur[q].x - lef[q].x, ay = cur[q].y - lef[q].y, az = cur[q].z - lef[q].z,
-                        aw = cur[q].w - lef[q].w;
+            const float lx = __shfl_up_sync(0xffffffffu, cur[q].x, 1), ly = __shfl_up_sync(0xffffffffu, cur[q].y, 1);
+            const float lz = __shfl_up_sync(0xffffffffu, cur[q].z, 1), lw = __shfl_up_sync(0xffffffffu, cur[q].w, 1);
+            const float ax = cur[q].x - lx, ay = cur[q].y - ly, az = cur[q].z - lz, aw = cur[q].w - lw;
             const float bx = cur[q].x - up[q].x, by = cur[q].y - up[q].y, bz = cur[q].z - up[q].z,
                         bw = cur[q].w - up[q].w;
             sx = fmaf(ax, ax, fmaf(ay, ay, fmaf(az, az, fmaf(aw, aw, sx))));
             sy = fmaf(bx, bx, fmaf(by, by, fmaf(bz, bz, fmaf(bw, bw, sy))));
         }
-        dx[r * g.pitch + c] = c > 0 ? sqrtf(fmaf(ratio2, sx, 1.f)) : inf;
-        dy[r * g.pitch + c] = r > 0 ? sqrtf(fmaf(ratio2, sy, 1.f)) : inf;
+        if (writer && c < g.W) {
+            dx[r * g.pitch + c] = c > 0 ? sqrtf(fmaf(ratio2, sx, 1.f)) : inf;
+            dy[r * g.pitch + c] = r > 0 ? sqrtf(fmaf(ratio2, sy, 1.f)) : inf;
+        }
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             up[q] = cur[q];
             cur[q] = ncur[q];
-            lef[q] = nlef[q];
         }
     }
 }
@@ -180,7 +179,8 @@ cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Ge
                                cudaStream_t s) {
     if ((C == 4 || C == 8 || C == 16) && ((uintptr_t)guide % 16 == 0)) {
         dim3 block(256);
-        dim3 grid((unsigned)((g.pitch + 255) / 256), (unsigned)((g.H + DERIV_ROWS - 1) / DERIV_ROWS));
+        dim3 grid((unsigned)((g.pitch + DERIV_VEC_COLS - 1) / DERIV_VEC_COLS),
+                  (unsigned)((g.H + DERIV_ROWS - 1) / DERIV_ROWS));
         if (C == 4) k_guide_deriv_vec<1><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy);
         if (C == 8) k_guide_deriv_vec<2><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy);
         if (C == 16) k_guide_deriv_vec<4><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy);
