@@ -147,7 +147,7 @@ enum Family {
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
                                      "rank_compose", "row_update", "confidence", "stereo_update", "link_fill",
-                                     "box_windows", "box_row", "box_col", "col_coef"};
+                                     "box_windows", "box_row", "box_col", "edge_profiles"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -651,13 +651,27 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
     Geometry gx = ctx->g;  // the guide rows including halos
     gx.H = Hx;
     gx.plane = Hx * gx.pitch;
-    st = run_launch(ctx, F_DERIV, px * (4.0 * C + 8.0), s, [&] {
-        return launch_guide_deriv(gdev, C, ratio * ratio, gx, ctx->dx_base, ctx->dy_base, s);
+    // the cluster column kernel reads a_1^{d_y} instead of d_y (one exp per pixel, written by
+    // the derivative kernel, instead of one per pixel and pass); later passes square it (R5:
+    // sigma halves per pass).  Rows 0..H: row H is the bottom link (+inf -> 0).
+    const bool with_a1 = !comm && filter_passes <= 4 && cp.kind == 1;
+    if (with_a1 && (e = cudaMallocAsync((void**)&ctx->A1y, (size_t)(H + 1) * ctx->g.pitch * sizeof(float), s)) !=
+                       cudaSuccess) {
+        st = cuda_fail(e);
+        if (gstage) cudaFreeAsync(gstage, s);
+        dts_destroy(ctx);
+        return st;
+    }
+    st = run_launch(ctx, F_DERIV, px * (4.0 * C + 8.0 + (with_a1 ? 4.0 : 0.0)), s, [&] {
+        return launch_guide_deriv(gdev, C, ratio * ratio, gx, ctx->dx_base, ctx->dy_base, s, ctx->A1y, ctx->kc[0]);
     });
     if (st == DTS_OK && !ctx->halo_below) {
         const float inf = std::numeric_limits<float>::infinity();
         st = run_launch(ctx, F_FILL, ctx->g.pitch * 4.0, s,
                         [&] { return launch_fill(ctx->dy + H * ctx->g.pitch, ctx->g.pitch, inf, s); });
+        if (st == DTS_OK && ctx->A1y)
+            st = run_launch(ctx, F_FILL, ctx->g.pitch * 4.0, s,
+                            [&] { return launch_fill(ctx->A1y + H * ctx->g.pitch, ctx->g.pitch, 0.f, s); });
     }
     if (st == DTS_OK)
         st = run_launch(ctx, F_SUPPORT_ROW, px * 8.0, s, [&] {
@@ -705,15 +719,6 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
                 return launch_edge_profiles(ctx->dy, ctx->g, (int)L, ctx->kc[i - 1], gam, th, s);
             });
         }
-    }
-    // the cluster column kernel reads a_1^{d_y} instead of d_y (one exp per pixel here instead
-    // of one per pixel and pass); later passes square it (R5: sigma halves per pass)
-    if (st == DTS_OK && !comm && filter_passes <= 4 && cp.kind == 1) {
-        const int64_t n = (H + 1) * ctx->g.pitch;  // row H: the bottom link (+inf -> 0)
-        if ((e = cudaMallocAsync((void**)&ctx->A1y, (size_t)n * sizeof(float), s)) != cudaSuccess) st = cuda_fail(e);
-        if (st == DTS_OK)
-            st = run_launch(ctx, F_COEF, (double)n * 8.0, s,
-                            [&] { return launch_coef(ctx->dy, ctx->A1y, n, ctx->kc[0], s); });
     }
     if (gstage) {
         cudaFreeAsync(gstage, s);

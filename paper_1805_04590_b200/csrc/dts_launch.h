@@ -18,8 +18,10 @@ struct Geometry {
 };
 
 // K1: domain distances from the HWC guide (Eqs. 8-9; R1, R2).
+// a1y (optional): also writes A1 = a_1^{d_y} = 2^(-kc0 d_y), the cluster column kernel's pass-1
+// coefficient (north star (1): the derivative kernel writes d and the coefficients a^d)
 cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Geometry& g, float* dx, float* dy,
-                               cudaStream_t s);
+                               cudaStream_t s, float* a1y = nullptr, float kc0 = 0.f);
 
 // K2: recursive-filter row pass (causal + anticausal, fused), FILTER or SUPPORT mode.
 struct RowPlan {
@@ -151,9 +153,6 @@ cudaError_t launch_box_row(const BoxPlan& plan, const Geometry& g, int Ct, const
                            const uint32_t* win, cudaStream_t s);
 cudaError_t launch_box_col(const BoxPlan& plan, const Geometry& g, int Ct, const float* in, float* out,
                            const uint32_t* win, cudaStream_t s);
-
-// A1 = a_1^d = 2^(-kc d) elementwise over n floats (the column kernel's pass-1 coefficient).
-cudaError_t launch_coef(const float* d, float* a1, int64_t n, float kc, cudaStream_t s);
 
 // Row-band edge fix-up scheme (k_colc.cu): create-time edge profiles of one pass, and the
 // elementwise corrections after the gathered edge records.

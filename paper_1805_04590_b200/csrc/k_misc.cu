@@ -19,7 +19,8 @@ constexpr int DERIV_ROWS = 32;
 template <int CT>  // CT = channel count (0: runtime C)
 __global__ void __launch_bounds__(DERIV_STRIP) k_guide_deriv(const float* __restrict__ guide, int Crt, float ratio2,
                                                              Geometry g, float* __restrict__ dx,
-                                                             float* __restrict__ dy) {
+                                                             float* __restrict__ dy, float* __restrict__ a1y,
+                                                             float kc0) {
     const int C = CT > 0 ? CT : Crt;
     const int CS = C | 1;  // odd pixel stride in shared memory -> conflict-free reads
     extern __shared__ float sm[];
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(DERIV_STRIP) k_guide_deriv(const float* __rest
             }
             dx[r * g.pitch + c] = ox;
             dy[r * g.pitch + c] = oy;
+            if (a1y) a1y[r * g.pitch + c] = coef_from_d(oy, kc0);  // pass-1 column coefficient
         }
         cur ^= 1;
         __syncthreads();
@@ -118,7 +120,8 @@ __global__ void __launch_bounds__(DERIV_STRIP) k_guide_deriv(const float* __rest
 constexpr int DERIV_VEC_COLS = 8 * 31;  // output columns per 256-thread block
 template <int Q>  // Q = C / 4
 __global__ void __launch_bounds__(256) k_guide_deriv_vec(const float* __restrict__ guide, float ratio2, Geometry g,
-                                                         float* __restrict__ dx, float* __restrict__ dy) {
+                                                         float* __restrict__ dx, float* __restrict__ dy,
+                                                         float* __restrict__ a1y, float kc0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t c = (int64_t)blockIdx.x * DERIV_VEC_COLS + warp * 31 + lane - 1;  // lane 0: c0 - 1
     const int64_t rbeg = (int64_t)blockIdx.y * DERIV_ROWS;
@@ -130,6 +133,7 @@ __global__ void __launch_bounds__(256) k_guide_deriv_vec(const float* __restrict
             for (int64_t r = rbeg; r < rend; ++r) {
                 dx[r * g.pitch + c] = inf;
                 dy[r * g.pitch + c] = inf;
+                if (a1y) a1y[r * g.pitch + c] = 0.f;
             }
         // keep the warp's shuffles well-defined: fall through with a clamped column
     }
@@ -165,7 +169,9 @@ __global__ void __launch_bounds__(256) k_guide_deriv_vec(const float* __restrict
         }
         if (writer && c < g.W) {
             dx[r * g.pitch + c] = c > 0 ? sqrtf(fmaf(ratio2, sx, 1.f)) : inf;
-            dy[r * g.pitch + c] = r > 0 ? sqrtf(fmaf(ratio2, sy, 1.f)) : inf;
+            const float oy = r > 0 ? sqrtf(fmaf(ratio2, sy, 1.f)) : inf;
+            dy[r * g.pitch + c] = oy;
+            if (a1y) a1y[r * g.pitch + c] = coef_from_d(oy, kc0);  // pass-1 column coefficient
         }
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -176,14 +182,14 @@ __global__ void __launch_bounds__(256) k_guide_deriv_vec(const float* __restrict
 }
 
 cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Geometry& g, float* dx, float* dy,
-                               cudaStream_t s) {
+                               cudaStream_t s, float* a1y, float kc0) {
     if ((C == 4 || C == 8 || C == 16) && ((uintptr_t)guide % 16 == 0)) {
         dim3 block(256);
         dim3 grid((unsigned)((g.pitch + DERIV_VEC_COLS - 1) / DERIV_VEC_COLS),
                   (unsigned)((g.H + DERIV_ROWS - 1) / DERIV_ROWS));
-        if (C == 4) k_guide_deriv_vec<1><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy);
-        if (C == 8) k_guide_deriv_vec<2><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy);
-        if (C == 16) k_guide_deriv_vec<4><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy);
+        if (C == 4) k_guide_deriv_vec<1><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy, a1y, kc0);
+        if (C == 8) k_guide_deriv_vec<2><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy, a1y, kc0);
+        if (C == 16) k_guide_deriv_vec<4><<<grid, block, 0, s>>>(guide, ratio2, g, dx, dy, a1y, kc0);
         return cudaGetLastError();
     }
     dim3 block(DERIV_STRIP);
@@ -198,7 +204,7 @@ cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Ge
             cudaFuncSetAttribute(k_guide_deriv<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
             cfg = true;                                                                               \
         }                                                                                             \
-        k_guide_deriv<K><<<grid, block, smem, s>>>(guide, C, ratio2, g, dx, dy);                       \
+        k_guide_deriv<K><<<grid, block, smem, s>>>(guide, C, ratio2, g, dx, dy, a1y, kc0);                       \
         break;                                                                                        \
     }
         DTS_DERIV_CASE(1)
@@ -211,7 +217,7 @@ cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Ge
                 cudaFuncSetAttribute(k_guide_deriv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
                 cfg = true;
             }
-            k_guide_deriv<0><<<grid, block, smem, s>>>(guide, C, ratio2, g, dx, dy);
+            k_guide_deriv<0><<<grid, block, smem, s>>>(guide, C, ratio2, g, dx, dy, a1y, kc0);
         }
 #undef DTS_DERIV_CASE
     }
@@ -530,19 +536,6 @@ cudaError_t launch_sr_prepare(const float* low, int64_t h, int64_t w, int f, flo
     const int64_t bx = (W + 255) / 256;
     dim3 grid((unsigned)(bx < 64 ? bx : 64), (unsigned)(H < 8192 ? H : 8192), 1);
     k_sr_prepare<<<grid, 256, 0, s>>>(low, h, w, f, target, conf);
-    return cudaGetLastError();
-}
-
-__global__ void __launch_bounds__(256) k_coef(const float* __restrict__ d, float* __restrict__ a1, int64_t n, float kc) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        a1[i] = coef_from_d(__ldg(d + i), kc);
-}
-
-cudaError_t launch_coef(const float* d, float* a1, int64_t n, float kc, cudaStream_t s) {
-    if (n <= 0) return cudaSuccess;
-    int64_t blocks = (n + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    k_coef<<<(unsigned)blocks, 256, 0, s>>>(d, a1, n, kc);
     return cudaGetLastError();
 }
 
