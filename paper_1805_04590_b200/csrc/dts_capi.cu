@@ -479,6 +479,58 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
     });
 }
 
+// Eager launch, or capture + replay of a CUDA graph: a solve whose key (pointers, sizes,
+// scalars) matches the previous eager one is captured on a context-owned stream (the
+// caller's may be the uncapturable legacy default stream) and launched as a graph; later
+// identical solves replay it.  The launch counter advances as for the eager sequence.
+template <typename F>
+dts_status run_cached(dts_ctx* ctx, bool use_graph, const std::vector<uintptr_t>& key, cudaStream_t s, F&& enqueue) {
+    cudaError_t e;
+    dts_status st;
+    const bool replay = use_graph && ctx->graph_exec && ctx->graph_key == key;
+    const bool capture = use_graph && !replay && ctx->graph_seen == key;
+    if (!replay && !capture) {
+        if ((st = enqueue(s)) != DTS_OK) return st;
+        ctx->graph_seen = use_graph ? key : std::vector<uintptr_t>();
+        return DTS_OK;
+    }
+    if (capture) {
+        if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+        ctx->graph_exec = nullptr;
+        if (!ctx->cap_stream && (e = cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e);
+        cudaStream_t cs = ctx->cap_stream;
+        if ((e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return cuda_fail(e);
+        const int64_t l0 = ctx->launches;
+        st = enqueue(cs);
+        cudaGraph_t graph = nullptr;
+        e = cudaStreamEndCapture(cs, &graph);
+        if (st != DTS_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (e != cudaSuccess) return cuda_fail(e);
+        e = cudaGraphInstantiate(&ctx->graph_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            ctx->graph_exec = nullptr;
+            return cuda_fail(e);
+        }
+        ctx->graph_key = key;
+        ctx->graph_launches = ctx->launches - l0;
+        ctx->launches = l0;
+    }
+    if ((e = cudaGraphLaunch(ctx->graph_exec, s)) != cudaSuccess) return cuda_fail(e);
+    ctx->launches += ctx->graph_launches;
+    return DTS_OK;
+}
+
+bool profiler_on() {
+    Profiler& P = profiler();
+    std::lock_guard<std::mutex> lk(P.mu);
+    return P.on;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1125,63 +1177,20 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
             return DTS_OK;
         };
         // Replay a captured graph of the whole launch sequence when the same solve is issued
-        // again (small images are launch-bound).  Only the cluster column path (its kernels
-        // carry no per-launch epochs), device buffers, and the profiler off.
-        bool prof_on;
-        {
-            Profiler& P = profiler();
-            std::lock_guard<std::mutex> lk(P.mu);
-            prof_on = P.on;
-        }
-        const bool use_graph = !any_host && !prof_on && !ctx->comm && (is_box || (cpf.kind == 1 && cpu.kind == 1)) &&
-                               !stream_ok &&
-                               !twop_ok && !std::getenv("DTS_NO_GRAPH");
+        // again (small images are launch-bound).  Only on the cluster column path or the box
+        // path (no per-launch epochs), with device buffers and the profiler off.
+        const bool use_graph = !any_host && !profiler_on() && !ctx->comm &&
+                               (is_box || (cpf.kind == 1 && cpu.kind == 1)) && !stream_ok && !twop_ok &&
+                               !std::getenv("DTS_NO_GRAPH");
         std::vector<uintptr_t> key;
         if (use_graph) {
             uint32_t lb, sb;
             std::memcpy(&lb, &lambda, 4);
             std::memcpy(&sb, &step, 4);
-            key = {(uintptr_t)t_d, (uintptr_t)c_d, (uintptr_t)o_d, (uintptr_t)Ct, (uintptr_t)iterations, lb, sb,
+            key = {1, (uintptr_t)t_d, (uintptr_t)c_d, (uintptr_t)o_d, (uintptr_t)Ct, (uintptr_t)iterations, lb, sb,
                    (uintptr_t)support_mode, (uintptr_t)ctx->X, (uintptr_t)ctx->Z, (uintptr_t)ctx->chat};
         }
-        const bool replay = use_graph && ctx->graph_exec && ctx->graph_key == key;
-        const bool capture = use_graph && !replay && ctx->graph_seen == key;
-        if (!replay && !capture) {
-            if ((st = enqueue(s)) != DTS_OK) return st;
-            ctx->graph_seen = key;  // the next identical solve is captured
-        } else {
-            if (capture) {
-                if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
-                ctx->graph_exec = nullptr;
-                // capture on a context-owned stream (the caller's may be the uncapturable legacy
-                // default stream); the graph is then launched on the caller's stream
-                if (!ctx->cap_stream &&
-                    (e = cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking)) != cudaSuccess)
-                    return cuda_fail(e);
-                cudaStream_t cs = ctx->cap_stream;
-                if ((e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return cuda_fail(e);
-                const int64_t l0 = ctx->launches;
-                st = enqueue(cs);
-                cudaGraph_t graph = nullptr;
-                e = cudaStreamEndCapture(cs, &graph);
-                if (st != DTS_OK) {
-                    if (graph) cudaGraphDestroy(graph);
-                    return st;
-                }
-                if (e != cudaSuccess) return cuda_fail(e);
-                e = cudaGraphInstantiate(&ctx->graph_exec, graph, 0);
-                cudaGraphDestroy(graph);
-                if (e != cudaSuccess) {
-                    ctx->graph_exec = nullptr;
-                    return cuda_fail(e);
-                }
-                ctx->graph_key = key;
-                ctx->graph_launches = ctx->launches - l0;
-                ctx->launches = l0;
-            }
-            if ((e = cudaGraphLaunch(ctx->graph_exec, s)) != cudaSuccess) return cuda_fail(e);
-            ctx->launches += ctx->graph_launches;
-        }
+        if ((st = run_cached(ctx, use_graph, key, s, enqueue)) != DTS_OK) return st;
     }
     if (ko == PTR_HOST) {
         if ((e = cudaMemcpyAsync(out, o_d, img, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return cuda_fail(e);
@@ -1334,27 +1343,46 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
         if (st == DTS_OK) st = ensure_solver_state(ctx, 1, s);
         if (st == DTS_OK) st = ensure_col_scratch(ctx, cp, s);
         const double px = (double)g.H * g.W;
-        if (st == DTS_OK)
-            st = run_launch(ctx, F_PROLOGUE, px * (24.0 + (ctx->Sy ? 4.0 : 0.0)), s, [&] {
+        auto enqueue = [&](cudaStream_t s) -> dts_status {
+            dts_status st = run_launch(ctx, F_PROLOGUE, px * (24.0 + (ctx->Sy ? 4.0 : 0.0)), s, [&] {
                 return launch_prologue(t_d, c_d, 1, g, ctx->S, ctx->Sy, 0, ctx->Z, ctx->T, ctx->chat, s);
             });
-        for (int k = 0; k < iterations && st == DTS_OK; ++k) {
-            for (int i = 0; i < ctx->N && st == DTS_OK; ++i) {
-                const float* in = (i == 0) ? ctx->Z : ctx->X;
-                st = run_launch(ctx, F_ROW, px * 12.0, s, [&] {
-                    return launch_row_pass(rp, g, 1, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
-                });
+            for (int k = 0; k < iterations && st == DTS_OK; ++k) {
+                for (int i = 0; i < ctx->N && st == DTS_OK; ++i) {
+                    const float* in = (i == 0) ? ctx->Z : ctx->X;
+                    st = run_launch(ctx, F_ROW, px * 12.0, s, [&] {
+                        return launch_row_pass(rp, g, 1, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
+                    });
+                    if (st == DTS_OK)
+                        st = run_launch(ctx, F_COL, px * 12.0, s, [&] {
+                            if (cp.kind == 1 && ctx->A1y && i < 4)  // pass-1 coefficient, squared per pass
+                                return launch_col_cluster(cp, g, 1, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr,
+                                                          nullptr, s, i);
+                            return col_launch(ctx, cp, 1, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
+                                              s);
+                        });
+                }
+                float* ohw = (k + 1 == iterations) ? o_d : nullptr;
                 if (st == DTS_OK)
-                    st = run_launch(ctx, F_COL, px * 12.0, s, [&] {
-                        return col_launch(ctx, cp, 1, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
+                    st = run_launch(ctx, F_STEREO, px * (20.0 + 12.0 * ctx->C), s, [&] {
+                        return launch_update_stereo(ctx->X, ctx->Z, ctx->T, ctx->chat, l_d, r_d, ctx->C, g, lambda,
+                                                    step, gamma, eps, ohw, s);
                     });
             }
-            float* ohw = (k + 1 == iterations) ? o_d : nullptr;
-            if (st == DTS_OK)
-                st = run_launch(ctx, F_STEREO, px * (20.0 + 12.0 * ctx->C), s, [&] {
-                    return launch_update_stereo(ctx->X, ctx->Z, ctx->T, ctx->chat, l_d, r_d, ctx->C, g, lambda, step,
-                                                gamma, eps, ohw, s);
-                });
+            return st;
+        };
+        if (st == DTS_OK) {
+            const bool use_graph = !any_host && !profiler_on() && cp.kind == 1 && !std::getenv("DTS_NO_GRAPH");
+            std::vector<uintptr_t> key;
+            if (use_graph) {
+                uint32_t lb, gb2, eb;
+                std::memcpy(&lb, &lambda, 4);
+                std::memcpy(&gb2, &gamma, 4);
+                std::memcpy(&eb, &eps, 4);
+                key = {2, (uintptr_t)t_d, (uintptr_t)c_d, (uintptr_t)o_d, (uintptr_t)l_d, (uintptr_t)r_d,
+                       (uintptr_t)iterations, lb, gb2, eb, (uintptr_t)ctx->X, (uintptr_t)ctx->Z, (uintptr_t)ctx->chat};
+            }
+            st = run_cached(ctx, use_graph, key, s, enqueue);
         }
     }
     if (st == DTS_OK && ko == PTR_HOST &&

@@ -123,3 +123,24 @@ def test_stereo_argument_errors():
         with pytest.raises(dts.DTSError) as ei:
             dts.dts_solve_stereo(s.ctx, td, cd, 0.99, 3, td, Ld, Ld, 0.001, 0.001)  # out aliases target
         assert ei.value.status == 1
+
+
+def test_stereo_repeated_solves_replay_a_graph():
+    """A repeated identical stereo solve is captured once and replayed as a CUDA graph:
+    bit-identical to the eager launches, the same launch count each time."""
+    L, t, c = random_problem(150, 230, 3, 1, seed=23)
+    t = (t * 6.0).astype(np.float32)
+    R = right_image(L, 3, 150)
+    Ld, Rd, td, cd = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (L, R, t, c))
+    outs, counts = [], []
+    with dts.Solver(Ld, 6.0, 0.2, 3) as s:
+        for _ in range(4):  # eager, capture + launch, replay, replay
+            o = torch.empty_like(td)
+            n0 = dts.dts_launch_count(s.ctx)
+            s.solve_stereo(td, cd, 0.99, 5, Ld, Rd, 0.001, 1.0, out=o)
+            counts.append(dts.dts_launch_count(s.ctx) - n0)
+            outs.append(o)
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    assert len(set(counts)) == 1 and counts[0] == 1 + 5 * 7
