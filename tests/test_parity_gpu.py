@@ -321,3 +321,40 @@ def test_repeated_solves_replay_a_graph():
     for o in outs[1:]:
         assert np.array_equal(o.cpu().numpy(), ref)
     assert len(set(counts)) == 1 and counts[0] == 1 + 5 * 7
+
+
+def test_concurrent_contexts_on_two_threads():
+    """Two host threads, each with its own context and stream, solving repeatedly (eager,
+    graph capture, replay) at the same time: every result equals the single-threaded one.
+    Covers the process-wide state (function attributes, profiler, plan caches)."""
+    import threading
+    probs = [random_problem(300, 410, 3, 1, seed=31), random_problem(520, 260, 3, 2, seed=32)]
+    refs = [gpu_solve(g, t, c, 7.0, 0.2, 3, 0.99, 6) for g, t, c in probs]
+    outs, errs = [[], []], []
+
+    def worker(k):
+        try:
+            torch.cuda.set_device(0)
+            g, t, c = probs[k]
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                gd, td, cd = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (g, t, c))
+                with dts.Solver(gd, 7.0, 0.2, 3, stream=stream.cuda_stream) as s:
+                    for _ in range(4):
+                        o = torch.empty_like(td)
+                        s.solve(td, cd, 0.99, 6, out=o, stream=stream.cuda_stream)
+                        stream.synchronize()
+                        outs[k].append(o.cpu().numpy().astype(np.float64))
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    ths = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join(timeout=120)
+    assert not errs, errs[0]
+    for k in range(2):
+        assert len(outs[k]) == 4
+        for o in outs[k]:
+            assert np.array_equal(o, refs[k])
