@@ -99,6 +99,7 @@ struct dts_ctx {
     float* S = nullptr;
     float* Sy = nullptr;  // column support factor when the cluster kernel computes it (S then holds s_x)
     float* A1y = nullptr;  // pass-1 column coefficient a_1^{d_y} (rows 0..H), cluster FILTER passes (N <= 4)
+    float* A1y_base = nullptr;  // allocation behind A1y (includes the halo rows, like dy_base)
     // box filter (dts_create_ex, DTS_FILTER_BOX): dx / dy hold the fixed-point increments q,
     // win the packed windows (planes 2i: rows, 2i + 1: columns, pass i), S the window counts
     int filter = DTS_FILTER_RF;
@@ -369,11 +370,10 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
         const int NT = 2 * Ct + 1;
         const size_t count = (size_t)pE.ntiles * NT * 32;
         const double px = (double)g.H * g.W;
-        if ((e = cudaMemsetAsync(ctx->ext, 0, (size_t)pE.ntiles * 2 * Ct * 32 * sizeof(float), s)) != cudaSuccess)
-            return cuda_fail(e);
+        const bool pre = ctx->A1y && pass < 4;  // pass-1 coefficient squared per pass
         st = run_launch(ctx, F_COL, px * (8.0 * Ct + 4), s, [&] {
-            return launch_col_cluster(pE, g, Ct, MODE_FILTER, x, ctx->dy, kc, nullptr, nullptr, s, -1, ctx->ext,
-                                      nullptr, ctx->rank_tup);
+            return launch_col_cluster(pE, g, Ct, MODE_FILTER, x, pre ? ctx->A1y : ctx->dy, kc, nullptr, nullptr, s,
+                                      pre ? pass : -1, nullptr, nullptr, ctx->rank_tup);  // zero carries
         });
         if (st != DTS_OK) return st;
         // Gamma_0 of this rank into slot 2Ct of its records
@@ -390,10 +390,11 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
             g_last_error = err;
             return DTS_E_NCCL;
         }
-        st = run_launch(ctx, F_COMPOSE, (double)2 * L * g.W * (8.0 * Ct + 4), s, [&] {
-            return launch_edge_fix(x, Ct, g, L, ctx->edge_gam[pass], ctx->edge_theta[pass], ctx->gathered,
-                                   ctx->comm->nranks, ctx->comm->rank, s);
-        });
+        if (ctx->comm->nranks > 1)  // a single rank has no edges to correct
+            st = run_launch(ctx, F_COMPOSE, (double)2 * L * g.W * (8.0 * Ct + 4), s, [&] {
+                return launch_edge_fix(x, Ct, g, L, ctx->edge_gam[pass], ctx->edge_theta[pass], ctx->gathered,
+                                       ctx->comm->nranks, ctx->comm->rank, s);
+            });
         if (st != DTS_OK || mode != MODE_UPDATE) return st;
         return run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
             return launch_update(x, upd->Z, upd->T, upd->chat, Ct, g, upd->lam, upd->step, upd->out_hwc, ctx->num_sms,
@@ -430,9 +431,10 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
             return launch_rank_compose(ctx->gathered, ctx->comm->nranks, ctx->comm->rank, pF.ntiles, Ct, ctx->ext, s);
         });
         if (st != DTS_OK) return st;
+        const bool pre = ctx->A1y && pass >= 0 && pass < 4;
         st = run_launch(ctx, F_COL, px * (8.0 * Ct + 4), s, [&] {
-            return launch_col_cluster(pF, g, Ct, MODE_FILTER, x, ctx->dy, kc, nullptr, nullptr, s, -1, ctx->ext,
-                                      nullptr);
+            return launch_col_cluster(pF, g, Ct, MODE_FILTER, x, pre ? ctx->A1y : ctx->dy, kc, nullptr, nullptr, s,
+                                      pre ? pass : -1, ctx->ext, nullptr);
         });
         if (st != DTS_OK || mode != MODE_UPDATE) return st;
         return run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
@@ -706,16 +708,18 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
     // the cluster column kernel reads a_1^{d_y} instead of d_y (one exp per pixel, written by
     // the derivative kernel, instead of one per pixel and pass); later passes square it (R5:
     // sigma halves per pass).  Rows 0..H: row H is the bottom link (+inf -> 0).
-    const bool with_a1 = !comm && filter_passes <= 4 && cp.kind == 1;
-    if (with_a1 && (e = cudaMallocAsync((void**)&ctx->A1y, (size_t)(H + 1) * ctx->g.pitch * sizeof(float), s)) !=
+    const bool with_a1 = filter_passes <= 4 && (comm || cp.kind == 1);
+    if (with_a1 && (e = cudaMallocAsync((void**)&ctx->A1y_base, (size_t)(Hx + 1) * ctx->g.pitch * sizeof(float), s)) !=
                        cudaSuccess) {
         st = cuda_fail(e);
         if (gstage) cudaFreeAsync(gstage, s);
         dts_destroy(ctx);
         return st;
     }
+    if (ctx->A1y_base) ctx->A1y = ctx->A1y_base + ctx->halo_above * ctx->g.pitch;
     st = run_launch(ctx, F_DERIV, px * (4.0 * C + 8.0 + (with_a1 ? 4.0 : 0.0)), s, [&] {
-        return launch_guide_deriv(gdev, C, ratio * ratio, gx, ctx->dx_base, ctx->dy_base, s, ctx->A1y, ctx->kc[0]);
+        return launch_guide_deriv(gdev, C, ratio * ratio, gx, ctx->dx_base, ctx->dy_base, s, ctx->A1y_base,
+                                  ctx->kc[0]);
     });
     if (st == DTS_OK && !ctx->halo_below) {
         const float inf = std::numeric_limits<float>::infinity();
@@ -1402,7 +1406,8 @@ void dts_destroy(dts_ctx* ctx) {
     if (!ctx) return;
     cudaStream_t s = ctx->last_stream;
     free_solver_state(ctx, s);
-    for (float** p : {&ctx->dx_base, &ctx->dy_base, &ctx->S, &ctx->Sy, &ctx->A1y, &ctx->st_t, &ctx->st_c, &ctx->st_o,
+    ctx->A1y = nullptr;
+    for (float** p : {&ctx->dx_base, &ctx->dy_base, &ctx->S, &ctx->Sy, &ctx->A1y_base, &ctx->st_t, &ctx->st_c, &ctx->st_o,
                       &ctx->rank_tup, &ctx->gathered, &ctx->ext}) {
         if (*p) cudaFreeAsync(*p, s);
         *p = nullptr;

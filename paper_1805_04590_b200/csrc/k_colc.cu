@@ -547,6 +547,14 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
         const int col = col0 + c;
         const bool colok = col < p.W;
 
+        // external carries of this tile (APPLY), loaded now so their latency hides behind the fold
+        float cx0[NV], ex0[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            cx0[v] = (MODE != MODE_TUPLE && s == 0 && p.ext) ? __ldg(p.ext + ((int64_t)tile * 2 * NV + v) * TW + c) : 0.f;
+            ex0[v] = (MODE != MODE_TUPLE && s == 0 && p.ext) ? __ldg(p.ext + ((int64_t)tile * 2 * NV + NV + v) * TW + c)
+                                                            : 0.f;
+        }
         // ---- 1. landing zone -> registers; refill with the next tile ----
         mbar_wait(&bars[s], (uint32_t)(k & 1));
         float a[LS];
@@ -660,8 +668,7 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
             float cin[NV];  // carry into the rank band's top: 0, the APPLY carry, or 1 for g (TUPLE)
 #pragma unroll
             for (int v = 0; v < NV; ++v)
-                cin[v] = (MODE == MODE_TUPLE) ? (v == CT ? 1.f : 0.f)
-                                              : (BAND ? p.ext[((int64_t)tile * 2 * NV + v) * TW + c] : 0.f);
+                cin[v] = (MODE == MODE_TUPLE) ? (v == CT ? 1.f : 0.f) : cx0[v];
             for (int q = 0; q < band; ++q) {
                 const float P = remC[(q * (NV + 1)) * TW + c];
 #pragma unroll
@@ -700,29 +707,28 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
             segR[(0 * S + s) * (TW + 1) + c] = Q;
 #pragma unroll
             for (int v = 0; v < NV; ++v) segR[((1 + v) * S + s) * (TW + 1) + c] = E[v];
-            if constexpr (BAND && MODE == MODE_FILTER) {  // edge scheme: y at row H - 1 (c = 0)
-                const int jl = p.H - 1 - (r0 + lo);
-                if (p.edge && colok && jl >= 0 && jl < LS) {
-                    float* ed = p.edge + (int64_t)tile * (2 * CT + 1) * TW;
+            // row-band outputs at row H - 1 (its warp only, warp-uniform): y of the x channels
+            // (c = 0) and, in TUPLE mode, of g (c = 1) -- the rank band's causal map c_out = A c + B
+            const int jl = p.H - 1 - (r0 + lo);
+            if ((MODE == MODE_TUPLE || p.edge) && jl >= 0 && jl < LS) {
+                float yl[NV];
 #pragma unroll
-                    for (int j = 0; j < LS; ++j)
-                        if (j == jl) {
+                for (int v = 0; v < NV; ++v) {
+                    yl[v] = xv[v][0];
 #pragma unroll
-                            for (int v = 0; v < CT; ++v) ed[v * TW + c] = xv[v][j];
-                        }
+                    for (int j = 1; j < LS; ++j) yl[v] = (j == jl) ? xv[v][j] : yl[v];
                 }
-            }
-            if constexpr (MODE == MODE_TUPLE) {  // rank causal map c_out = A c + B: y at row H - 1
-                const int jl = p.H - 1 - (r0 + lo);  // of the x channels (c = 0) and of g (c = 1)
-                if (colok && jl >= 0 && jl < LS) {
-                    float* rt = p.rank_tuples + (int64_t)tile * (2 * CT + 3) * TW;
+                if (colok) {
+                    if constexpr (MODE == MODE_TUPLE) {
+                        float* rt = p.rank_tuples + (int64_t)tile * (2 * CT + 3) * TW;
+                        rt[0 * TW + c] = yl[CT];
 #pragma unroll
-                    for (int j = 0; j < LS; ++j)
-                        if (j == jl) {
-                            rt[0 * TW + c] = xv[CT][j];
+                        for (int v = 0; v < CT; ++v) rt[(1 + v) * TW + c] = yl[v];
+                    } else {
+                        float* ed = p.edge + (int64_t)tile * (2 * CT + 1) * TW;
 #pragma unroll
-                            for (int v = 0; v < CT; ++v) rt[(1 + v) * TW + c] = xv[v][j];
-                        }
+                        for (int v = 0; v < CT; ++v) ed[v * TW + c] = yl[v];
+                    }
                 }
             }
         }
@@ -742,7 +748,7 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
             float ein[NV];  // carry into the rank band's bottom: 0 or the APPLY carry
 #pragma unroll
             for (int v = 0; v < NV; ++v)
-                ein[v] = (MODE != MODE_TUPLE && BAND) ? p.ext[((int64_t)tile * 2 * NV + NV + v) * TW + c] : 0.f;
+                ein[v] = (MODE != MODE_TUPLE) ? ex0[v] : 0.f;
             float Qbe = 1.f;
             for (int q = CB - 1; q > band; --q) {
                 const float Qb = remA[(q * (NV + 1)) * TW + c];
@@ -883,17 +889,20 @@ template <int CT, int MODE, bool PRE = false>
 static const void* kptr() {
     return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE, PRE>);
 }
-template <int CT, int MODE>
+template <int CT, int MODE, bool PRE = false>
 static const void* kptr_band() {
-    return reinterpret_cast<const void*>(colc::k_col_cluster_band<CT, MODE, false, true>);
+    return reinterpret_cast<const void*>(colc::k_col_cluster_band<CT, MODE, PRE, true>);
 }
 static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = false) {
     if (mode == MODE_SUPPORT) return kptr<1, MODE_SUPPORT>();
-    if (band && mode == MODE_FILTER) {  // APPLY of the row-band exchange
-        switch (Ct) {
-            case 1: return kptr_band<1, MODE_FILTER>();
-            case 2: return kptr_band<2, MODE_FILTER>();
-            case 3: return kptr_band<3, MODE_FILTER>();
+    if (band && mode == MODE_FILTER) {  // APPLY of the row-band exchange / the edge scheme's pass
+        switch (Ct * 2 + (pre ? 1 : 0)) {
+            case 2: return kptr_band<1, MODE_FILTER>();
+            case 3: return kptr_band<1, MODE_FILTER, true>();
+            case 4: return kptr_band<2, MODE_FILTER>();
+            case 5: return kptr_band<2, MODE_FILTER, true>();
+            case 6: return kptr_band<3, MODE_FILTER>();
+            case 7: return kptr_band<3, MODE_FILTER, true>();
         }
         return nullptr;
     }
@@ -950,7 +959,8 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
         int optin = 0;
         if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0)) != cudaSuccess) return e;
         for (const void* f : {fn, mode == MODE_FILTER ? colc_kernel(Ct, mode, true) : fn,
-                              mode == MODE_FILTER ? colc_kernel(Ct, mode, false, true) : fn}) {
+                              mode == MODE_FILTER ? colc_kernel(Ct, mode, false, true) : fn,
+                              mode == MODE_FILTER ? colc_kernel(Ct, mode, true, true) : fn}) {
             cudaFuncAttributes fa2;
             if ((e = cudaFuncGetAttributes(&fa2, f)) != cudaSuccess) return e;
             if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess ||
@@ -1024,7 +1034,7 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     } else {
         tx = td;
     }
-    const void* fn = colc_kernel(Ct, mode, nsq >= 0, ext != nullptr);
+    const void* fn = colc_kernel(Ct, mode, nsq >= 0, ext != nullptr || edge != nullptr);
     if (!fn) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = plan.grid;
