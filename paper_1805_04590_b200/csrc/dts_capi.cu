@@ -735,10 +735,67 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
         });
     if (st == DTS_OK) st = ensure_col_scratch(ctx, cp, s);
     if (st == DTS_OK) {
-        if (comm)
-            st = col_pass_banded(ctx, 1, MODE_SUPPORT, nullptr, ctx->ks, nullptr, ctx->S, F_SUPPORT_COL, px * 12.0,
-                                 s, -1);
-        else if (cp.kind == 1) {  // cluster kernel: s_y into its own plane (no read-modify-write of S)
+        if (comm) {
+            // edge scheme for the support: s = P + Q - 1 with independent
+            // causal P and anticausal Q; the zero-carry cluster pass gives s0 with P0(0) = 1 and
+            // Q0(H-1) = 1, so s0(H-1) is the P carry for the rank below and s0(0) the Q carry for
+            // the rank above; then s += c G_k (top rows) + e Theta_k (bottom rows)
+            const double as = std::exp(-sqrt2 / (double)sigma_s);
+            const int64_t Ls = as > 0.0 ? (int64_t)std::ceil(std::log(std::ldexp(1.0, -26)) / std::log(as)) : 1;
+            ColPlan cps;
+            bool edge = Ls >= 1 && 2 * Ls + 1 <= H && Ls <= (1 << 20) && !std::getenv("DTS_BAND_TUPLE") &&
+                        plan_col_cluster(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &cps) == cudaSuccess;
+            cudaGetLastError();
+            if (edge) {
+                float *G = nullptr, *Th = nullptr;
+                const size_t pb = (size_t)Ls * ctx->g.pitch * sizeof(float);
+                if ((e = cudaMallocAsync((void**)&ctx->Sy, plane, s)) != cudaSuccess ||
+                    (e = cudaMallocAsync((void**)&G, pb, s)) != cudaSuccess ||
+                    (e = cudaMallocAsync((void**)&Th, pb, s)) != cudaSuccess)
+                    st = cuda_fail(e);
+                if (st == DTS_OK) st = ensure_band_buffers(ctx, s);
+                if (st == DTS_OK)
+                    st = run_launch(ctx, F_SUPPORT_COL, px * 8.0, s, [&] {
+                        return launch_col_cluster(cps, ctx->g, 1, MODE_SUPPORT, nullptr, ctx->dy, ctx->ks, nullptr,
+                                                  ctx->Sy, s);
+                    });
+                const int NT = 3;
+                const size_t count = (size_t)cps.ntiles * NT * 32;
+                if (st == DTS_OK &&
+                    ((e = cudaMemsetAsync(ctx->rank_tup, 0, count * sizeof(float), s)) != cudaSuccess ||
+                     (e = cudaMemcpy2DAsync(ctx->rank_tup, NT * 32 * sizeof(float), ctx->Sy + (H - 1) * ctx->g.pitch,
+                                            32 * sizeof(float), 32 * sizeof(float), cps.ntiles,
+                                            cudaMemcpyDeviceToDevice, s)) != cudaSuccess ||
+                     (e = cudaMemcpy2DAsync(ctx->rank_tup + 32, NT * 32 * sizeof(float), ctx->Sy, 32 * sizeof(float),
+                                            32 * sizeof(float), cps.ntiles, cudaMemcpyDeviceToDevice, s)) !=
+                         cudaSuccess))
+                    st = cuda_fail(e);
+                std::string err;
+                if (st == DTS_OK)
+                    st = run_launch(ctx, F_EXCHANGE, (double)count * 4 * comm->nranks, s, [&] {
+                        return comm_allgather(comm, ctx->rank_tup, ctx->gathered, count, s, &err) ? cudaSuccess
+                                                                                                  : cudaErrorUnknown;
+                    });
+                if (st == DTS_E_CUDA && !err.empty()) {
+                    g_last_error = err;
+                    st = DTS_E_NCCL;
+                }
+                if (st == DTS_OK)
+                    st = run_launch(ctx, F_COEF, px * 8.0, s, [&] {
+                        return launch_edge_profiles(ctx->dy, ctx->g, (int)Ls, ctx->ks, G, Th, s, true);
+                    });
+                if (st == DTS_OK && comm->nranks > 1)
+                    st = run_launch(ctx, F_COMPOSE, (double)2 * Ls * W * 12.0, s, [&] {
+                        return launch_edge_fix(ctx->Sy, 1, ctx->g, (int)Ls, G, Th, ctx->gathered, comm->nranks,
+                                               comm->rank, s, false);
+                    });
+                if (G) cudaFreeAsync(G, s);
+                if (Th) cudaFreeAsync(Th, s);
+            } else {
+                st = col_pass_banded(ctx, 1, MODE_SUPPORT, nullptr, ctx->ks, nullptr, ctx->S, F_SUPPORT_COL,
+                                     px * 12.0, s, -1);
+            }
+        } else if (cp.kind == 1) {  // cluster kernel: s_y into its own plane (no read-modify-write of S)
             if ((e = cudaMallocAsync((void**)&ctx->Sy, plane, s)) != cudaSuccess) st = cuda_fail(e);
             if (st == DTS_OK)
                 st = run_launch(ctx, F_SUPPORT_COL, px * 8.0, s, [&] {

@@ -156,9 +156,12 @@ cudaError_t launch_box_col(const BoxPlan& plan, const Geometry& g, int Ct, const
 
 // Row-band edge fix-up scheme (k_colc.cu): create-time edge profiles of one pass, and the
 // elementwise corrections after the gathered edge records.
+// raw: keep the causal product profile G (the support's correction) instead of its
+// anticausal response Gamma; cross = false: the bottom carry has no causal-carry term
+// (the support's P and Q recurrences are independent)
 cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float kc, float* gam, float* theta,
-                                 cudaStream_t s);
+                                 cudaStream_t s, bool raw = false);
 cudaError_t launch_edge_fix(float* x, int Ct, const Geometry& g, int L, const float* gam, const float* theta,
-                            const float* gathered, int P, int rank, cudaStream_t s);
+                            const float* gathered, int P, int rank, cudaStream_t s, bool cross = true);
 
 }  // namespace dts

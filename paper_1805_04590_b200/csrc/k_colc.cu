@@ -1065,22 +1065,25 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
 // per column, sequential over the edge rows (create time): Gamma (top L rows), Theta
 // (bottom L rows, row H - L first); d has rows 0..H (row H: the link below the band)
 __global__ void k_edge_profiles(const float* __restrict__ d, int64_t H, int64_t W, int64_t pitch, int L, float kc,
-                                float* __restrict__ gam, float* __restrict__ theta) {
+                                float* __restrict__ gam, float* __restrict__ theta, bool raw) {
     const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (col >= W) return;
     float G = 1.f;
+#pragma unroll 8
     for (int k = 0; k < L; ++k) {  // G_k = prod_{j <= k} a_j (a_0: the link to the band above)
         G *= coef_from_d(__ldg(d + (int64_t)k * pitch + col), kc);
         gam[(int64_t)k * pitch + col] = G;
     }
-    float dz = 0.f;  // anticausal response, zero at row L (below resolution)
-    for (int k = L - 1; k >= 0; --k) {
+    float dz = 0.f;  // anticausal response, zero at row L (below resolution); raw: keep G itself
+#pragma unroll 8
+    for (int k = L - 1; k >= 0 && !raw; --k) {
         const float an = coef_from_d(__ldg(d + (int64_t)(k + 1) * pitch + col), kc);
         const float g = gam[(int64_t)k * pitch + col];
         dz = fmaf(an, dz - g, g);
         gam[(int64_t)k * pitch + col] = dz;
     }
     float th = coef_from_d(__ldg(d + H * pitch + col), kc);  // a_H
+#pragma unroll 8
     for (int64_t k = H - 1; k >= H - L; --k) {
         theta[(k - (H - L)) * pitch + col] = th;
         th *= coef_from_d(__ldg(d + k * pitch + col), kc);
@@ -1088,8 +1091,8 @@ __global__ void k_edge_profiles(const float* __restrict__ d, int64_t H, int64_t 
 }
 
 cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float kc, float* gam, float* theta,
-                                 cudaStream_t s) {
-    k_edge_profiles<<<(unsigned)((g.W + 127) / 128), 128, 0, s>>>(d, g.H, g.W, g.pitch, L, kc, gam, theta);
+                                 cudaStream_t s, bool raw) {
+    k_edge_profiles<<<(unsigned)((g.W + 127) / 128), 128, 0, s>>>(d, g.H, g.W, g.pitch, L, kc, gam, theta, raw);
     return cudaGetLastError();
 }
 
@@ -1098,7 +1101,7 @@ cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float
 // all from the gathered edge records [P][ntiles][2Ct+1][32] (slot 2Ct: Gamma_0)
 __global__ void k_edge_fix(float* __restrict__ x, int Ct, int64_t H, int64_t W, int64_t pitch, int64_t plane, int L,
                            const float* __restrict__ gam, const float* __restrict__ theta,
-                           const float* __restrict__ gath, int P, int rank, int ntiles) {
+                           const float* __restrict__ gath, int P, int rank, int ntiles, bool cross) {
     const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int kk = blockIdx.y;  // 0..2L-1: top rows, then bottom rows
     if (col >= W) return;
@@ -1114,7 +1117,8 @@ __global__ void k_edge_fix(float* __restrict__ x, int Ct, int64_t H, int64_t W, 
         } else if (rank + 1 < P) {
             const float* nb = gath + (rank + 1) * rstride + t * NT * colc::TW;
             const float ylast = gath[rank * rstride + (t * NT + v) * colc::TW + cc];
-            carry = fmaf(ylast, nb[(2 * Ct) * colc::TW + cc], nb[(Ct + v) * colc::TW + cc]);
+            carry = cross ? fmaf(ylast, nb[(2 * Ct) * colc::TW + cc], nb[(Ct + v) * colc::TW + cc])
+                          : nb[(Ct + v) * colc::TW + cc];
         }
         if (carry != 0.f) {
             const float prof = top ? gam[(int64_t)kk * pitch + col] : theta[(int64_t)(kk - L) * pitch + col];
@@ -1125,10 +1129,11 @@ __global__ void k_edge_fix(float* __restrict__ x, int Ct, int64_t H, int64_t W, 
 }
 
 cudaError_t launch_edge_fix(float* x, int Ct, const Geometry& g, int L, const float* gam, const float* theta,
-                            const float* gathered, int P, int rank, cudaStream_t s) {
+                            const float* gathered, int P, int rank, cudaStream_t s, bool cross) {
     const int ntiles = (int)((g.W + colc::TW - 1) / colc::TW);
     dim3 grid((unsigned)((g.W + 127) / 128), (unsigned)(2 * L));
-    k_edge_fix<<<grid, 128, 0, s>>>(x, Ct, g.H, g.W, g.pitch, g.plane, L, gam, theta, gathered, P, rank, ntiles);
+    k_edge_fix<<<grid, 128, 0, s>>>(x, Ct, g.H, g.W, g.pitch, g.plane, L, gam, theta, gathered, P, rank, ntiles,
+                                    cross);
     return cudaGetLastError();
 }
 
