@@ -56,3 +56,66 @@ def compose(tuples):
 def finish(parts, c, e):
     y0, y1, z0, S, Q = parts
     return z0 + S * c + Q * e
+
+
+# ---- edge fix-up scheme ("Edge fix-up scheme") ----------------------
+def zero_carry_pass(x, A, lo, hi, A_below):
+    """Causal + anticausal pass of rows [lo, hi) with zero carries: y[lo-1] = 0 enters
+    through A[lo], z[hi] = 0 enters through A_below.  Returns (y0, z0)."""
+    n = hi - lo
+    y = np.zeros(n)
+    p = 0.0
+    for i in range(n):
+        a = A[lo + i]
+        p = a * p + (1 - a) * x[lo + i]
+        y[i] = p
+    z = np.zeros(n)
+    q = 0.0
+    for i in range(n - 1, -1, -1):
+        an = A[lo + i + 1] if i + 1 < n else A_below
+        q = an * q + (1 - an) * y[i]
+        z[i] = q
+    return y, z
+
+
+def edge_profiles(A, lo, hi, A_below, L):
+    """Gamma (anticausal response of G_k = prod_{j<=k} A[lo+j]) on the top L rows and
+    Theta_k = prod_{j=k+1..hi} a_j (a_hi = A_below) on the bottom L rows."""
+    G = np.cumprod(A[lo:lo + L])
+    gam = np.zeros(L)
+    dz = 0.0
+    for k in range(L - 1, -1, -1):
+        an = A[lo + k + 1]
+        dz = an * (dz - G[k]) + G[k]
+        gam[k] = dz
+    theta = np.zeros(L)
+    th = A_below
+    for k in range(hi - 1, hi - L - 1, -1):
+        theta[k - (hi - L)] = th
+        th *= A[k]
+    return G, gam, theta
+
+
+def edge_scheme(x, A, cuts, L):
+    """The banded pass by the edge scheme: zero-carry pass per band, exchange of (y0 at the
+    band's last row, z0 at its first row, Gamma_0), corrections on the L edge rows."""
+    P = len(cuts) - 1
+    H = cuts[-1]
+    ys, zs, prof = [], [], []
+    for k in range(P):
+        lo, hi = cuts[k], cuts[k + 1]
+        below = A[hi] if hi < H else 0.0
+        y0, z0 = zero_carry_pass(x, A, lo, hi, below)
+        ys.append(y0)
+        zs.append(z0)
+        prof.append(edge_profiles(A, lo, hi, below, L))
+    out = []
+    for k in range(P):
+        z = zs[k].copy()
+        c = ys[k - 1][-1] if k > 0 else 0.0
+        e = zs[k + 1][0] + ys[k][-1] * prof[k + 1][1][0] if k + 1 < P else 0.0
+        _, gam, theta = prof[k]
+        z[:L] += c * gam
+        z[-L:] += e * theta
+        out.append(z)
+    return np.concatenate(out)

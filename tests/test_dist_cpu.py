@@ -121,3 +121,64 @@ def test_gloo_two_rank_exchange():
         assert p.exitcode == 0
     assert all(r[0] for r in res)
     assert max(r[1] for r in res) <= 1e-12
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+def test_edge_scheme_algebra(P):
+    """The edge fix-up scheme of the row-band column pass: with bands of >= 2L rows,
+    zero-carry passes + corrections c Gamma (top L rows) and e Theta (bottom L rows), with
+    c = y0 at the last row of the band above and e = z0 at the first row of the band below
+    + y0(this band's last row) Gamma_0(below), equal the full column pass to below 2^-26."""
+    rng = np.random.default_rng(P)
+    H = 480
+    amax = 0.7  # every coefficient <= a_i (d >= 1); L = 51 rows
+    A = rng.uniform(0.3, amax, H)
+    A[0] = 0.0
+    x = rng.normal(size=H)
+    ref = dense.pass1d(A) @ x
+    L = int(np.ceil(np.log(2.0 ** -26) / np.log(amax)))
+    assert 2 * L + 1 <= H // P
+    cuts = [k * H // P for k in range(P + 1)]
+    got = bandalg.edge_scheme(x, A, cuts, L)
+    assert np.max(np.abs(got - ref)) <= 2.0 ** -24 * np.max(np.abs(x))
+
+
+def test_edge_scheme_support_variant():
+    """The support's edge scheme: s = P + Q - 1 (P[k] = 1 + a_k P[k-1], Q[k] = 1 + a_{k+1} Q[k+1]),
+    zero-carry s0 per band, carries c = s0 at the last row of the band above (P carry) and
+    e = s0 at the first row of the band below (Q carry), corrections c G_k and e Theta_k."""
+    rng = np.random.default_rng(9)
+    H, P, amax = 360, 3, 0.85
+    a = rng.uniform(0.2, amax, H)
+    a[0] = 0.0
+    Pf, Qf = np.zeros(H), np.zeros(H)
+    for k in range(H):
+        Pf[k] = 1 + (a[k] * Pf[k - 1] if k > 0 else 0.0)
+    for k in range(H - 1, -1, -1):
+        Qf[k] = 1 + (a[k + 1] * Qf[k + 1] if k + 1 < H else 0.0)
+    ref = Pf + Qf - 1
+    L = int(np.ceil(np.log(2.0 ** -26) / np.log(amax)))
+    cuts = [k * H // P for k in range(P + 1)]
+    s0, prof = [], []
+    for k in range(P):
+        lo, hi = cuts[k], cuts[k + 1]
+        n = hi - lo
+        p0, q0 = np.zeros(n), np.zeros(n)
+        for i in range(n):
+            p0[i] = 1 + (a[lo + i] * p0[i - 1] if i > 0 else 0.0)
+        for i in range(n - 1, -1, -1):
+            q0[i] = 1 + (a[lo + i + 1] * q0[i + 1] if i + 1 < n else 0.0)
+        s0.append(p0 + q0 - 1)
+        below = a[hi] if hi < H else 0.0
+        G, _, theta = bandalg.edge_profiles(a, lo, hi, below, L)
+        prof.append((G, theta))
+    out = []
+    for k in range(P):
+        s = s0[k].copy()
+        c = s0[k - 1][-1] if k > 0 else 0.0
+        e = s0[k + 1][0] if k + 1 < P else 0.0
+        s[:L] += c * prof[k][0]
+        s[-L:] += e * prof[k][1]
+        out.append(s)
+    got = np.concatenate(out)
+    assert np.max(np.abs(got - ref)) <= 2.0 ** -22 * np.max(np.abs(ref))
