@@ -192,3 +192,24 @@ def test_box_c4_sampled_windows_and_constant_target():
         s.solve(tc, cd, cfg.lam, 2, out=out)
         torch.cuda.synchronize()
         assert float((out - 0.375).abs().max()) <= 1e-6
+
+
+def _random_box_cases(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        H = int(rng.choice([1, 5, 32, 33, 100, 257, 520, 1100]))
+        W = int(rng.choice([1, 7, 32, 33, 100, 255, 1030, 2100]))
+        out.append((H, W, int(rng.integers(1, 4)), float(rng.uniform(2.0, 60.0)), float(rng.uniform(0.05, 1.0)),
+                    int(rng.integers(1, 4)), int(rng.integers(1, 6)), float(rng.choice([0.0, 1.0, 2.5])),
+                    int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("H,W,Ct,ss,sr,N,iters,rs,seed", _random_box_cases(16, 77))
+def test_box_random_shapes_parity(H, W, Ct, ss, sr, N, iters, rs, seed):
+    """Seeded random sweep of the box variant: shapes across segment / tile boundaries,
+    halos wider than the image, radius scales, channels, passes, iterations."""
+    g, t, c = random_problem(H, W, 3, Ct, seed=seed % 100000)
+    check_tables(g, ss, sr, N, radius_scale=rs)
+    check_solve(g, t, c, ss, sr, N, 0.99, iters, radius_scale=rs)

@@ -358,3 +358,22 @@ def test_concurrent_contexts_on_two_threads():
         assert len(outs[k]) == 4
         for o in outs[k]:
             assert np.array_equal(o, refs[k])
+
+
+def _random_cases(n, seed):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for _ in range(n):
+        H = int(rng.choice([1, 2, 31, 33, 64, 65, 127, 200, 333, 641, 700]))
+        W = int(rng.choice([1, 3, 32, 33, 63, 96, 129, 257, 500, 700]))
+        cases.append((H, W, int(rng.integers(1, 4)), float(rng.uniform(2.0, 40.0)), float(rng.uniform(0.05, 1.0)),
+                      int(rng.integers(1, 5)), int(rng.integers(1, 9)), int(rng.integers(0, 1 << 30))))
+    return cases
+
+
+@pytest.mark.parametrize("H,W,Ct,ss,sr,N,iters,seed", _random_cases(24, 2026))
+def test_random_shapes_parity(H, W, Ct, ss, sr, N, iters, seed):
+    """Seeded random sweep of shapes (ragged tails, single rows / columns), target channels,
+    sigmas, pass counts and iteration counts through the default path, against the oracle."""
+    g, t, c = random_problem(H, W, 3, Ct, seed=seed % 100000)
+    check(g, t, c, ss, sr, N, 0.99, iters)
