@@ -62,8 +62,12 @@ typedef enum {
 /* dts_create -- domain-transform setup for one guide image.
  *   guide          H x W x C fp32, HWC; read once.  Colours are used as given (no
  *                  clamping, R16); only differences of adjacent pixels matter.
- *   H, W, C        >= 1.  This build supports W <= 18432 and H <= 12800 (C_t = 1;
- *                  H <= 6400 for C_t = 3) in one context; larger -> DTS_E_SHAPE.
+ *   H, W, C        >= 1.  W <= 18432 (the row kernel holds whole rows).  The column
+ *                  kernels keep a column tile's bands co-resident, which bounds H per
+ *                  context: on a 148-SM B200 at least 30000 rows for C_t = 1 and 6400 for
+ *                  C_t = 3 (cluster kernel up to 10240 rows, decoupled kernel beyond).  A
+ *                  larger H returns DTS_E_SHAPE (from dts_create, or from dts_solve for the
+ *                  C_t of that call); split such images into row bands (dts_create_band).
  *   sigma_s        spatial std-dev in pixels (sigma_x = sigma_y), > 0, finite.
  *   sigma_r        range std-dev in colour units, > 0, finite.
  *   filter_passes  N >= 1 recursive-filter passes per edge-aware mean (R5); N <= 16.

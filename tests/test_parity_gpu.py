@@ -377,3 +377,19 @@ def test_random_shapes_parity(H, W, Ct, ss, sr, N, iters, seed):
     sigmas, pass counts and iteration counts through the default path, against the oracle."""
     g, t, c = random_problem(H, W, 3, Ct, seed=seed % 100000)
     check(g, t, c, ss, sr, N, 0.99, iters)
+
+
+@pytest.mark.parametrize("H,W,Ct", [(25000, 33, 1), (16000, 40, 1), (6400, 20, 3)])
+def test_tall_images_parity(H, W, Ct):
+    """Columns longer than a cluster holds (10240 rows at C_t = 1): the decoupled column
+    kernel, near the per-context row limit stated in include/dts.h."""
+    g, t, c = random_problem(H, W, 3, Ct, seed=H)
+    check(g, t, c, 8.0, 0.2, 3, 0.99, 3)
+
+
+def test_too_tall_image_is_a_shape_error():
+    g, t, c = random_problem(60000, 8, 3, 1, seed=1)
+    with pytest.raises(dts.DTSError) as ei:
+        with dts.Solver(torch.from_numpy(g).cuda(), 8.0, 0.2, 3):
+            pass
+    assert "DTS_E_SHAPE" in str(ei.value)
