@@ -1311,10 +1311,16 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
         });
         if (st == DTS_OK && !per_plane)
             st = run_launch(ctx, F_COL, px * 20.0, s, [&] {
+                if (cp.kind == 1 && ctx->A1y && i < 4)  // pass-1 coefficient, squared per pass
+                    return launch_col_cluster(cp, g, 2, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr, nullptr,
+                                              s, i);
                 return col_launch(ctx, cp, 2, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
             });
         for (int v = 0; v < 2 && st == DTS_OK && per_plane; ++v)
             st = run_launch(ctx, F_COL, px * 12.0, s, [&] {
+                if (cp1.kind == 1 && ctx->A1y && i < 4)
+                    return launch_col_cluster(cp1, g, 1, MODE_FILTER, ctx->X + v * g.plane, ctx->A1y, ctx->kc[i],
+                                              nullptr, nullptr, s, i);
                 return col_launch(ctx, cp1, 1, MODE_FILTER, ctx->X + v * g.plane, ctx->dy, ctx->kc[i], nullptr,
                                   nullptr, s);
             });
