@@ -312,14 +312,23 @@ static const int kLs[] = {4, 12, 20, 36};
 
 cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowPlan* plan) {
     const int nslot = 1 + (mode == MODE_SUPPORT ? 1 : Ct);
+    // Narrow rows: the smallest segment length that fits >= 2 rows per CTA (G <= 128).  A
+    // row's scan is latency-bound; several rows per CTA keep more of them in flight (C1/C2:
+    // row pass 12.7 -> 10.5 us with L = 12 instead of 4); not with L > 12
+    // (C3, W = 3840: L = 36 gave 84.7 us against 51.6 at L = 12).  Wide rows: the smallest L with
+    // G <= 512 (one row per CTA, the segment loads coalesce either way).
     int L = 0, G = 0;
-    for (int cand : kLs) {
-        int64_t need = (g.W + cand - 1) / cand;
-        if (need <= 512) {
-            L = cand;
-            G = (int)need;
-            break;
+    for (int lim : {128, 512}) {
+        for (int cand : kLs) {
+            if (lim == 128 && cand > 12) break;  // long segments cost more than they save
+            int64_t need = (g.W + cand - 1) / cand;
+            if (need <= lim) {
+                L = cand;
+                G = (int)need;
+                break;
+            }
         }
+        if (G) break;
     }
     if (G == 0) return cudaErrorInvalidValue;  // W > 36 * 512
     if (G <= 32) {
