@@ -1131,6 +1131,14 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                                               s, i);
                 return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
             };
+            // last column pass of an iteration: FILTER + streaming update kernel (default), or
+            // the column kernel's UPDATE mode (Eq. (3) in its write-out; DTS_FUSED_UPDATE=1).
+            // Split wins everywhere measured: C4 0.331 + 0.302 ms against 0.91 fused; small
+            // Ct = 1 images under graph replay 0.750 against 0.882 ms per solve (640x480,
+            // tools/graph_time.py).  Only the per-launch-profiled bench favours fused there
+            // (one launch fewer per iteration).
+            const char* fu = std::getenv("DTS_FUSED_UPDATE");
+            const bool split_update = cpu.kind == 3 || (cpu.kind == 1 && !(fu && fu[0] == '1'));
             if (is_box) {  // R25: N x (box rows, box columns), ping-pong X2 <-> X, then Eq. (3)
                 for (int k = 0; k < iterations; ++k) {
                     for (int i = 0; i < ctx->N; ++i) {
@@ -1210,7 +1218,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                         }
                     } else if (i + 1 < ctx->N) {
                         st = run_launch(ctx, F_COL, row_bytes, s, [&] { return col_filter(i); });
-                    } else if ((cpu.kind == 1 && !std::getenv("DTS_FUSED_UPDATE")) || cpu.kind == 3) {
+                    } else if (split_update) {
                         // column kernel (FILTER) + streaming update kernel (K4b)
                         st = run_launch(ctx, F_COL, row_bytes, s, [&] { return col_filter(i); });
                         if (st != DTS_OK) return st;
