@@ -1194,12 +1194,31 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                 });
                 if (st != DTS_OK) return st;
             }
+            // Eq. (3) of iteration k-1 applied inside iteration k's first row pass (k_row.cu
+            // ROWUPD: Z, T, chat read coalesced while the row lands); one update kernel after
+            // the last iteration.  C4 0.467 ms against 0.189 + 0.302 separately, C1/C3 +8%/+5%
+            // per step.  DTS_ROWUPD=0: a separate update kernel every iteration.
+            const char* ru_env = std::getenv("DTS_ROWUPD");
+            const bool rowupd = split_update && !ctx->comm && !(ru_env && ru_env[0] == '0');
+            UpdateArgs ru;
+            ru.Z = ctx->Z;
+            ru.T = ctx->T;
+            ru.chat = ctx->chat;
+            ru.lam = lambda;
+            ru.step = step;
+            ru.out_hwc = nullptr;
             for (int k = 0; k < (stream_ok ? 0 : iterations); ++k) {
                 for (int i = 0; i < ctx->N; ++i) {
                     const float* in = (i == 0) ? ctx->Z : ctx->X;
-                    st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
-                        return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
-                    });
+                    if (rowupd && i == 0 && k > 0) {  // Eq. (3) of iteration k-1 in this row pass
+                        st = run_launch(ctx, F_ROWUPD, px * (20.0 * Ct + 8), s, [&] {
+                            return launch_row_update(rp, g, Ct, ctx->X, ctx->X, ctx->dx, ctx->kc[i], ru, s);
+                        });
+                    } else {
+                        st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
+                            return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
+                        });
+                    }
                     if (st != DTS_OK) return st;
                     if (ctx->comm) {  // row-band mode: TUPLE -> all-gather -> compose -> APPLY
                         if (i + 1 < ctx->N) {
@@ -1222,6 +1241,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                         // column kernel (FILTER) + streaming update kernel (K4b)
                         st = run_launch(ctx, F_COL, row_bytes, s, [&] { return col_filter(i); });
                         if (st != DTS_OK) return st;
+                        if (rowupd && k + 1 < iterations) continue;  // the next row pass applies Eq. (3)
                         float* ohwc = (k + 1 == iterations) ? o_d : nullptr;
                         st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
                             return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, ohwc,

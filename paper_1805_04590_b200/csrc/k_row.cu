@@ -135,6 +135,15 @@ __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
             for (int c = 0; c < NX; ++c)
                 bulk_g2s(buf + (q * NSLOT + 1 + c) * p.rowstride, p.in + c * p.plane + r * p.pitch, rowBytes,
                          &bar[b]);
+            if constexpr (MODE == MODE_ROWUPD) {  // Z, T, chat of that row group into L2
+                const uint32_t pb = (uint32_t)(p.W * sizeof(float) + 15) / 16 * 16;
+                bulk_prefetch_l2(p.chat + r * p.pitch, pb);
+#pragma unroll
+                for (int c = 0; c < CT; ++c) {
+                    bulk_prefetch_l2(p.Z + c * p.plane + r * p.pitch, pb);
+                    bulk_prefetch_l2(p.T + c * p.plane + r * p.pitch, pb);
+                }
+            }
         }
     };
 
@@ -151,31 +160,64 @@ __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
         }
         const int k0 = t * L;
         const int64_t grow = (int64_t)grp * R + rs;  // this thread group's image row
-        // ROWUPD: state, target and chat of this chunk straight from global (in flight
-        // while the TMA row lands)
-        float zo[MODE == MODE_ROWUPD ? CT : 1][MODE == MODE_ROWUPD ? L : 1];
-        float tv[MODE == MODE_ROWUPD ? CT : 1][MODE == MODE_ROWUPD ? L : 1];
-        float ch[MODE == MODE_ROWUPD ? L : 1];
+        // ROWUPD: state, target and chat of this row straight from global, coalesced (float4
+        // q = j G + t of the row), in flight while the TMA row lands
+        constexpr int NQ = (MODE == MODE_ROWUPD) ? L / 4 : 1;
+        constexpr int CU = (MODE == MODE_ROWUPD) ? CT : 1;
+        float4 zo[CU][NQ], tv[CU][NQ], ch[NQ];
         if constexpr (MODE == MODE_ROWUPD) {
             const bool rok = grow < p.H;
 #pragma unroll
-            for (int j4 = 0; j4 < L; j4 += 4) {
-                const bool ok = rok && (k0 + j4 < p.W);
-                const int64_t o = grow * p.pitch + k0 + j4;
-                float4 cv = ok ? __ldg(reinterpret_cast<const float4*>(p.chat + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
-                ch[j4] = cv.x, ch[j4 + 1] = cv.y, ch[j4 + 2] = cv.z, ch[j4 + 3] = cv.w;
+            for (int j = 0; j < NQ; ++j) {
+                const int k = 4 * (j * G + t);
+                const bool ok = rok && k < p.W;
+                const int64_t o = grow * p.pitch + k;
+                const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+                ch[j] = ok ? __ldg(reinterpret_cast<const float4*>(p.chat + o)) : zero;
 #pragma unroll
                 for (int c = 0; c < CT; ++c) {
-                    float4 zv = ok ? *reinterpret_cast<const float4*>(p.Z + c * p.plane + o) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    float4 tt = ok ? __ldg(reinterpret_cast<const float4*>(p.T + c * p.plane + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    zo[c][j4] = zv.x, zo[c][j4 + 1] = zv.y, zo[c][j4 + 2] = zv.z, zo[c][j4 + 3] = zv.w;
-                    tv[c][j4] = tt.x, tv[c][j4 + 1] = tt.y, tv[c][j4 + 2] = tt.z, tv[c][j4 + 3] = tt.w;
+                    zo[c][j] = ok ? *reinterpret_cast<const float4*>(p.Z + c * p.plane + o) : zero;
+                    tv[c][j] = ok ? __ldg(reinterpret_cast<const float4*>(p.T + c * p.plane + o)) : zero;
                 }
             }
         }
         mbar_wait(&bar[b], (uint32_t)(dbl ? ((it >> 1) & 1) : (it & 1)));
 
         float* row = smem + b * bufFloats + (int64_t)rs * NSLOT * p.rowstride;
+
+        if constexpr (MODE == MODE_ROWUPD) {  // Eq. (3): z <- z - step [lam (z - zbar) + chat (z - t)]
+#pragma unroll
+            for (int c = 0; c < CT; ++c) {
+#pragma unroll
+                for (int j = 0; j < NQ; ++j) {
+                    const int k = 4 * (j * G + t);
+                    if (k < p.W) {
+                        float* xs = row + (1 + c) * p.rowstride + k;  // zbar in, new z out (in place)
+                        const float4 zb = *reinterpret_cast<const float4*>(xs);
+                        const float zz[4] = {zo[c][j].x, zo[c][j].y, zo[c][j].z, zo[c][j].w};
+                        const float bb[4] = {zb.x, zb.y, zb.z, zb.w};
+                        const float tt[4] = {tv[c][j].x, tv[c][j].y, tv[c][j].z, tv[c][j].w};
+                        const float cc[4] = {ch[j].x, ch[j].y, ch[j].z, ch[j].w};
+                        float nz[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            nz[u] = fmaf(-p.step, fmaf(p.lam, zz[u] - bb[u], cc[u] * (zz[u] - tt[u])), zz[u]);
+                        *reinterpret_cast<float4*>(xs) = make_float4(nz[0], nz[1], nz[2], nz[3]);
+                        if (grow < p.H) {
+                            float* o = p.Z + c * p.plane + grow * p.pitch + k;
+                            if (k + 3 < p.W) {
+                                *reinterpret_cast<float4*>(o) = make_float4(nz[0], nz[1], nz[2], nz[3]);
+                            } else {
+#pragma unroll
+                                for (int u = 0; u < 4; ++u)
+                                    if (k + u < p.W) o[u] = nz[u];
+                            }
+                        }
+                    }
+                }
+            }
+            __syncthreads();  // the row's new z complete in shared memory
+        }
 
         // ---- load chunk: coefficients A and samples x (masked beyond W) ----
         float A[L];
@@ -196,29 +238,6 @@ __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
                     float xx[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u) x[c][j4 + u] = (k0 + j4 + u < p.W) ? xx[u] : 0.f;
-                }
-            }
-        }
-        if constexpr (MODE == MODE_ROWUPD) {  // Eq. (3): x <- z - step [lam (z - zbar) + chat (z - t)]
-#pragma unroll
-            for (int c = 0; c < CT; ++c) {
-#pragma unroll
-                for (int j = 0; j < L; ++j) {
-                    const float g = fmaf(p.lam, zo[c][j] - x[c][j], ch[j] * (zo[c][j] - tv[c][j]));
-                    x[c][j] = (k0 + j < p.W) ? fmaf(-p.step, g, zo[c][j]) : 0.f;
-                }
-                if (grow < p.H) {
-#pragma unroll
-                    for (int j4 = 0; j4 < L; j4 += 4) {
-                        float* o = p.Z + c * p.plane + grow * p.pitch + k0 + j4;
-                        if (k0 + j4 + 3 < p.W) {
-                            *reinterpret_cast<float4*>(o) = make_float4(x[c][j4], x[c][j4 + 1], x[c][j4 + 2], x[c][j4 + 3]);
-                        } else {
-#pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                if (k0 + j4 + u < p.W) o[u] = x[c][j4 + u];
-                        }
-                    }
                 }
             }
         }

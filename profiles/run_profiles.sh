@@ -1,17 +1,20 @@
 #!/bin/bash
 # Profiling recipe used for profiles/ (run under gpurun on one B200; see B200_PROFILING.md).
-# 1) the plain run must exit 0; 2) launch list of one full timed step (145 launches: guide
-# derivative, bottom-link fill, support row + column, prologue, 20 x [3 row, 3 column, update]);
-# 3) one `--set full` capture per kernel family (steady-state launches).
+# 1) the plain run must exit 0; 2) launch list of one full timed step (127 launches: guide
+# derivative, bottom-link fill, support row + column, A1 fill, prologue, 20 x [3 row, 3 column]
+# with iterations 2-20 taking the previous Eq. (3) step in their first row pass, and one
+# closing update); 3) one `--set full` capture per kernel family (steady-state launches;
+# k_row_pass launch 4 of a step is the first ROWUPD instance).
 set -u
 OUT=${OUT:-gpurun_out}
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
 $CMD > $OUT/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -s 146 -c 146 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
-for spec in "k_col_cluster 4" "k_row_pass 2" "k_update 1" "k_guide_deriv 1" "k_prologue 1"; do
+    -s 127 -c 127 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
+for spec in "k_col_cluster 4" "k_row_pass 2" "k_row_pass 4 row_update" "k_update 1" "k_guide_deriv 1" "k_prologue 1"; do
   set -- $spec
+  tag=${3:-$1}
   ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 \
-      -o $OUT/full_$1 $CMD > $OUT/ncu_full_$1.log 2>&1
+      -o $OUT/full_$tag $CMD > $OUT/ncu_full_$tag.log 2>&1
 done
 echo done

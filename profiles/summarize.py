@@ -26,7 +26,20 @@ BENCH_NAME = {"k_col_cluster": "col_pass", "k_row_pass": "row_pass", "k_update":
               "k_guide_deriv": "guide_deriv", "k_prologue": "prologue", "k_col_pass": "col_pass"}
 
 
+def row_mode(name):
+    """MODE template argument of a k_row_pass instance (mangled ILi<L>ELi<CT>ELi<MODE>E or
+    demangled k_row_pass<L, CT, MODE>)."""
+    m = re.search(r"k_row_pass(?:ILi\d+ELi\d+ELi(\d)E|<\s*\d+,\s*\d+,\s*(\d)\s*>)", name)
+    return int(m.group(1) or m.group(2)) if m else 0
+
+
 def family(name):
+    if "k_row_pass" in name:
+        mode = row_mode(name)
+        if mode == 3:
+            return "k_row_pass", "row_update (row pass + previous Eq. (3) step)"
+        if mode == 2:
+            return "k_row_pass", "row_pass (support, create)"
     for key, fam in FAMILY:
         if key in name:
             return key, fam
