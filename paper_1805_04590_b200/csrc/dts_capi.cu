@@ -1199,7 +1199,9 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
             // the last iteration.  C4 0.467 ms against 0.189 + 0.302 separately, C1/C3 +8%/+5%
             // per step.  DTS_ROWUPD=0: a separate update kernel every iteration.
             const char* ru_env = std::getenv("DTS_ROWUPD");
-            const bool rowupd = split_update && !ctx->comm && !(ru_env && ru_env[0] == '0');
+            // (row bands too: their row passes are rank-local; the band column pass of the
+            // last filter pass then runs in FILTER mode)
+            const bool rowupd = (split_update || ctx->comm) && !(ru_env && ru_env[0] == '0');
             UpdateArgs ru;
             ru.Z = ctx->Z;
             ru.T = ctx->T;
@@ -1221,7 +1223,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                     }
                     if (st != DTS_OK) return st;
                     if (ctx->comm) {  // row-band mode: TUPLE -> all-gather -> compose -> APPLY
-                        if (i + 1 < ctx->N) {
+                        if (i + 1 < ctx->N || (rowupd && k + 1 < iterations)) {
                             st = col_pass_banded(ctx, Ct, MODE_FILTER, ctx->X, ctx->kc[i], nullptr, nullptr, F_COL,
                                                  row_bytes, s, i);
                         } else {
