@@ -257,8 +257,14 @@ dts_status ensure_staging(dts_ctx* ctx, size_t bytes_per_image, cudaStream_t s) 
 
 // column-pass plan: cluster fast path when it fits, else the decoupled band-tuple kernel
 cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan) {
-    if (!std::getenv("DTS_NO_CLUSTER") && plan_col_cluster(g, Ct, mode, num_sms, plan) == cudaSuccess)
-        return cudaSuccess;
+    if (!std::getenv("DTS_NO_CLUSTER")) {
+        // C_t >= 2 FILTER: 16-row segments (20 warps per CTA) when the column fits a cluster
+        if (Ct >= 2 && mode == MODE_FILTER && !std::getenv("DTS_COL_LS32") &&
+            plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 16) == cudaSuccess)
+            return cudaSuccess;
+        cudaGetLastError();
+        if (plan_col_cluster(g, Ct, mode, num_sms, plan) == cudaSuccess) return cudaSuccess;
+    }
     cudaGetLastError();
     return plan_col_pass(g, Ct, mode, num_sms, plan);
 }

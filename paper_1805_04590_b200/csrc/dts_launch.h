@@ -73,6 +73,8 @@ cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int 
 // K3/K4 fast path: cluster-held column tiles, register-resident segments (k_colc.cu).
 // Returns cudaErrorNotSupported when the shape does not fit (then use plan_col_pass).
 cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
+// ls = 16: 16-row warp segments (FILTER, C_t >= 2, not for row bands); plan->Ls records it
+cudaError_t plan_col_cluster_ls(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int ls);
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
                                float kc, const UpdateArgs* upd, float* support, cudaStream_t s,
                                int nsq = -1,  // nsq >= 0: d holds A1 (see coef_pow)

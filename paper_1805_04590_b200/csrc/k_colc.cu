@@ -21,6 +21,11 @@
 #include "dts_device.cuh"
 #include "dts_launch.h"
 
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
+
 namespace dts {
 
 namespace colc {
@@ -111,8 +116,10 @@ __device__ __forceinline__ void seg_scan(float* seg, int S, int cc, float* tot) 
 template <int NV>
 constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
 
-template <int CT, int MODE, bool PRE>
-__global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>(), 1)
+// LSV: rows per warp segment; 16 for C_t >= 2 FILTER passes of images up to 16 x 320 rows
+// (half the registers per thread, so 20 warps fit where 32-row segments allow 11-14)
+template <int CT, int MODE, bool PRE, int LSV = LS>
+__global__ void __launch_bounds__(LSV == 16 ? 640 : max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>(), 1)
     k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
     constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
     constexpr bool HASX = MODE != MODE_SUPPORT;
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
     const int cluster = blockIdx.x / CB;
     const int nclusters = gridDim.x / CB;
     const int r0 = band * HB;
-    const int lo = s * LS;
+    const int lo = s * LSV;
     // PRE: d holds A1 = a_1^d and this pass's coefficient is A1^(2^nsq), nsq <= 3 (uniform)
     const int nsq = p.nsq;
     auto coef = [&](float v) {
@@ -169,16 +176,16 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
 
     auto stage_in = [&](int tile) {  // thread 0: TMA boxes of `tile` into the landing zone
         const int col0 = tile * TW;
-        const uint32_t box = (uint32_t)(LS * TW * sizeof(float));
+        const uint32_t box = (uint32_t)(LSV * TW * sizeof(float));
         for (int q = 0; q < S; ++q) {
-            const int rq = r0 + q * LS;
+            const int rq = r0 + q * LSV;
             const uint32_t bytes = rq < p.H ? box * (1 + (HASX ? NV : 0)) : 0u;
             mbar_arrive_expect_tx(&bars[q], bytes);
             if (bytes) {
-                tma_load_2d(ld + q * LS * TW, &tm_d, col0, rq, &bars[q]);
+                tma_load_2d(ld + q * LSV * TW, &tm_d, col0, rq, &bars[q]);
                 if constexpr (HASX) {
 #pragma unroll
-                    for (int v = 0; v < NV; ++v) tma_load_3d(lx + (v * HB + q * LS) * TW, &tm_x, col0, rq, v, &bars[q]);
+                    for (int v = 0; v < NV; ++v) tma_load_3d(lx + (v * HB + q * LSV) * TW, &tm_x, col0, rq, v, &bars[q]);
                 }
             }
         }
@@ -193,15 +200,15 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
 
         // ---- 1. landing zone -> registers; refill with the next tile ----
         mbar_wait(&bars[s], (uint32_t)(k & 1));
-        float a[LS];
-        float xv[NV][LS];
-        if (r0 + lo + LS <= p.H) {
+        float a[LSV];
+        float xv[NV][LSV];
+        if (r0 + lo + LSV <= p.H) {
             // every row of the segment is in the image (warp-uniform): no per-row checks.
             // Lanes past W read the row padding; their values stay in their own column
             // (every step of the pass is per column) and are never stored.
             const float* ldc = ld + lo * TW + c;
 #pragma unroll
-            for (int j = 0; j < LS; ++j) {
+            for (int j = 0; j < LSV; ++j) {
                 a[j] = coef(ldc[j * TW]);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
@@ -211,7 +218,7 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < LS; ++j) {
+            for (int j = 0; j < LSV; ++j) {
                 const int rr = lo + j;
                 const bool ok = colok && (r0 + rr) < p.H;
                 a[j] = ok ? coef(ld[rr * TW + c]) : 0.f;
@@ -227,13 +234,13 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         // band's last segment, straight from global (first row of the next band)
         float anext = 0.f;
         {
-            const int rn = r0 + lo + LS;
+            const int rn = r0 + lo + LSV;
             if (s + 1 == S && colok && rn < p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
         }
         __syncthreads();
         if (s + 1 < S) {
-            const int rn = r0 + lo + LS;
-            anext = (colok && rn < p.H) ? coef(ld[(lo + LS) * TW + c]) : 0.f;
+            const int rn = r0 + lo + LSV;
+            anext = (colok && rn < p.H) ? coef(ld[(lo + LSV) * TW + c]) : 0.f;
         }
         __syncthreads();  // landing zone free
         if (threadIdx.x == 0 && tile + nclusters < p.ntiles) stage_in(tile + nclusters);
@@ -254,7 +261,7 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
         {
             Aff<NV> m = aff_identity<NV>();
 #pragma unroll
-            for (int j = 0; j < LS; ++j) {
+            for (int j = 0; j < LSV; ++j) {
                 m.P *= a[j];
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
@@ -302,8 +309,8 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
 #pragma unroll
             for (int v = 0; v < NV; ++v) E[v] = 0.f;
 #pragma unroll
-            for (int j = 0; j < LS; ++j) {
-                const float an = (j + 1 < LS) ? a[j + 1] : anext;
+            for (int j = 0; j < LSV; ++j) {
+                const float an = (j + 1 < LSV) ? a[j + 1] : anext;
                 if constexpr (HASX) {
                     const float qb = Q * (1.f - an);
 #pragma unroll
@@ -354,8 +361,8 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
 #pragma unroll
             for (int v = 0; v < NV; ++v) z[v] = fmaf(eQ, carry[v * TW + c], segR[((1 + v) * S + s) * (TW + 1) + c]);
 #pragma unroll
-            for (int j = LS - 1; j >= 0; --j) {
-                const float an = (j + 1 < LS) ? a[j + 1] : anext;
+            for (int j = LSV - 1; j >= 0; --j) {
+                const float an = (j + 1 < LSV) ? a[j + 1] : anext;
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     const float yv = xv[v][j];
@@ -372,21 +379,21 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
 
         // ---- 5. write-out straight from registers ----
         {
-            const int nrow = min(LS, p.H - (r0 + lo));
+            const int nrow = min(LSV, p.H - (r0 + lo));
             if (colok && nrow > 0) {
                 if constexpr (MODE == MODE_FILTER || MODE == MODE_SUPPORT) {
                     float* base = (MODE == MODE_FILTER ? p.x : p.support) + (int64_t)(r0 + lo) * p.pitch + col;
                     const int64_t pitch = p.pitch;
-                    if (nrow == LS) {  // full segment: a running pointer, no per-row checks
+                    if (nrow == LSV) {  // full segment: a running pointer, no per-row checks
 #pragma unroll
                         for (int v = 0; v < NV; ++v) {
                             float* q = base + v * p.plane;
 #pragma unroll
-                            for (int j = 0; j < LS; ++j, q += pitch) *q = xv[v][j];
+                            for (int j = 0; j < LSV; ++j, q += pitch) *q = xv[v][j];
                         }
                     } else {
 #pragma unroll
-                        for (int j = 0; j < LS; ++j)
+                        for (int j = 0; j < LSV; ++j)
                             if (j < nrow) {
 #pragma unroll
                                 for (int v = 0; v < NV; ++v) base[v * p.plane + (int64_t)j * pitch] = xv[v][j];
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
 #pragma unroll
-                        for (int j0 = 0; j0 < LS; j0 += UB) {
+                        for (int j0 = 0; j0 < LSV; j0 += UB) {
                             float zo[UB], tv[UB], ch[UB];
 #pragma unroll
                             for (int u = 0; u < UB; ++u) {
@@ -873,12 +880,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     return fn;
 }
 
-static bool tmap(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int64_t planes, int rank) {
+static bool tmap(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int64_t planes, int rank,
+                 int box_rows = colc::LS) {
     auto enc = encoder();
     if (!enc) return false;
     cuuint64_t dims[3] = {(cuuint64_t)pitch, (cuuint64_t)H, (cuuint64_t)planes};
     cuuint64_t strides[2] = {(cuuint64_t)(pitch * sizeof(float)), (cuuint64_t)(pitch * H * sizeof(float))};
-    cuuint32_t box[3] = {(cuuint32_t)colc::TW, (cuuint32_t)colc::LS, 1};
+    cuuint32_t box[3] = {(cuuint32_t)colc::TW, (cuuint32_t)box_rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -893,7 +901,21 @@ template <int CT, int MODE, bool PRE = false>
 static const void* kptr_band() {
     return reinterpret_cast<const void*>(colc::k_col_cluster_band<CT, MODE, PRE, true>);
 }
-static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = false) {
+template <int CT, bool PRE>
+static const void* kptr16() {
+    return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE_FILTER, PRE, 16>);
+}
+static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = false, int ls = colc::LS) {
+    if (ls == 16) {  // FILTER, C_t >= 2, single context
+        if (mode != MODE_FILTER || band) return nullptr;
+        switch (Ct * 2 + (pre ? 1 : 0)) {
+            case 4: return kptr16<2, false>();
+            case 5: return kptr16<2, true>();
+            case 6: return kptr16<3, false>();
+            case 7: return kptr16<3, true>();
+        }
+        return nullptr;
+    }
     if (mode == MODE_SUPPORT) return kptr<1, MODE_SUPPORT>();
     if (band && mode == MODE_FILTER) {  // APPLY of the row-band exchange / the edge scheme's pass
         switch (Ct * 2 + (pre ? 1 : 0)) {
@@ -934,40 +956,48 @@ static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = f
 }
 
 // Fast path if the column fits a cluster of <= 16 CTAs with register-resident segments.
-cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan) {
-    (void)num_sms;
+// ls: rows per warp segment, 32 (every mode) or 16 (FILTER at C_t >= 2, single context).
+// Cluster size CB: its CTAs hold H / CB rows in <= 20 warps.  32-row segments: the smallest
+// such CB (fewest exchange participants; one-round images are latency-bound: C1 at CB 2,
+// 16 warps 14.4 us, at CB 9, 4 warps 20.8 us).  16-row segments: the fewest tile rounds
+// (ceil(tiles / resident clusters); residency depends on how CB packs into the GPCs), ties
+// to the larger CB (fewer warps per CTA): C3 CB 7 / 8 / 9 all give 15 clusters and 8 rounds,
+// 84 / 80 / 78 us; CB 10 11 clusters, 101 us; CB 14 9 rounds, 97 us.  Plans are cached per
+// device and shape (the occupancy queries cost host time on every solve).
+static cudaError_t plan_col_cluster_uncached(const Geometry& g, int Ct, int mode, ColPlan* plan, int ls, int fcb) {
     const int NV = (mode == MODE_SUPPORT) ? 1 : (mode == MODE_TUPLE ? Ct + 1 : Ct);
     const int NX = (mode == MODE_SUPPORT) ? 0 : Ct;
-    const void* fn = colc_kernel(Ct, mode);
+    const void* fn = colc_kernel(Ct, mode, false, false, ls);
     if (!fn) return cudaErrorNotSupported;
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, fn);
     if (e != cudaSuccess) return e;
     int Smax = fa.maxThreadsPerBlock / colc::TW;
     if (Smax > 20) Smax = 20;
-    const int64_t rows_seg = colc::LS;
-    for (int CB = 1; CB <= 16; ++CB) {
+    // attributes are per function and shared by every plan: allow non-portable clusters and
+    // the opt-in shared memory maximum (so that no plan lowers another's limit); the
+    // A1-input (and, at 32-row segments, row-band) variants of the FILTER kernel get the same
+    int optin = 0;
+    if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0)) != cudaSuccess) return e;
+    const bool f32 = mode == MODE_FILTER && ls == colc::LS;
+    for (const void* f : {fn, mode == MODE_FILTER ? colc_kernel(Ct, mode, true, false, ls) : fn,
+                          f32 ? colc_kernel(Ct, mode, false, true) : fn, f32 ? colc_kernel(Ct, mode, true, true) : fn}) {
+        cudaFuncAttributes fa2;
+        if ((e = cudaFuncGetAttributes(&fa2, f)) != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      optin - (int)fa2.sharedSizeBytes)) != cudaSuccess)
+            return e;
+    }
+    const int ntiles = (int)((g.W + colc::TW - 1) / colc::TW);
+    int64_t best_cost = -1;
+    for (int CB = fcb ? fcb : 1; CB <= (fcb ? fcb : 16); ++CB) {
         const int64_t HBmin = (g.H + CB - 1) / CB;
-        const int S = (int)((HBmin + rows_seg - 1) / rows_seg);
+        const int S = (int)((HBmin + ls - 1) / ls);
         if (S > Smax) continue;
-        const int HB = S * colc::LS;
+        const int HB = S * ls;
         const colc::Smem L = mode == MODE_TUPLE ? colc::layout_band(NX, NV, HB, S) : colc::layout(NV, HB, S);
         if (L.bytes > 227 * 1024) continue;
-        // attributes are per function and shared by every plan: allow non-portable clusters and
-        // the opt-in shared memory maximum (so that no plan lowers another's limit); the
-        // A1-input variants of the FILTER kernel get the same
-        int optin = 0;
-        if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0)) != cudaSuccess) return e;
-        for (const void* f : {fn, mode == MODE_FILTER ? colc_kernel(Ct, mode, true) : fn,
-                              mode == MODE_FILTER ? colc_kernel(Ct, mode, false, true) : fn,
-                              mode == MODE_FILTER ? colc_kernel(Ct, mode, true, true) : fn}) {
-            cudaFuncAttributes fa2;
-            if ((e = cudaFuncGetAttributes(&fa2, f)) != cudaSuccess) return e;
-            if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess ||
-                (e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          optin - (int)fa2.sharedSizeBytes)) != cudaSuccess)
-                return e;
-        }
         // how many clusters can be resident at once
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)CB, 1, 1);
@@ -986,14 +1016,19 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
             cudaGetLastError();
             continue;
         }
-        const int ntiles = (int)((g.W + colc::TW - 1) / colc::TW);
         if (nclusters > ntiles) nclusters = ntiles;
+        const int64_t cost = (ntiles + nclusters - 1) / nclusters;  // tile rounds
+        if (std::getenv("DTS_DEBUG"))
+            std::fprintf(stderr, "plan_col_cluster: Ct %d mode %d ls %d CB %d S %d clusters %d ntiles %d cost %lld\n", Ct,
+                         mode, ls, CB, S, nclusters, ntiles, (long long)cost);
+        if (best_cost >= 0 && (ls == colc::LS || cost > best_cost)) continue;
+        best_cost = cost;
         plan->kind = 1;
         plan->TW = colc::TW;
         plan->CB = CB;
         plan->HB = HB;
         plan->S = S;
-        plan->Ls = colc::LS;
+        plan->Ls = ls;
         plan->nb = CB;
         plan->ntiles = ntiles;
         plan->threads = colc::TW * S;
@@ -1001,9 +1036,45 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
         plan->smem = L.bytes;
         plan->tuple_floats = 0;
         plan->flag_count = 0;
-        return cudaSuccess;
+        if (ls == colc::LS) break;
     }
-    return cudaErrorNotSupported;
+    return best_cost >= 0 ? cudaSuccess : cudaErrorNotSupported;
+}
+
+cudaError_t plan_col_cluster_ls(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int ls) {
+    (void)num_sms;
+    const char* f = std::getenv("DTS_COL_CB");  // force a cluster size (experiments)
+    const int fcb = f ? atoi(f) : 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    struct Entry {
+        int dev, Ct, mode, ls, fcb;
+        int64_t H, W;
+        cudaError_t err;
+        ColPlan plan;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const Entry& en : cache)
+            if (en.dev == dev && en.Ct == Ct && en.mode == mode && en.ls == ls && en.fcb == fcb && en.H == g.H &&
+                en.W == g.W) {
+                if (en.err == cudaSuccess) *plan = en.plan;
+                return en.err;
+            }
+    }
+    ColPlan p{};
+    const cudaError_t e = plan_col_cluster_uncached(g, Ct, mode, &p, ls, fcb);
+    if (e != cudaSuccess) cudaGetLastError();
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() < 256) cache.push_back(Entry{dev, Ct, mode, ls, fcb, g.H, g.W, e, p});
+    if (e == cudaSuccess) *plan = p;
+    return e;
+}
+
+cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan) {
+    return plan_col_cluster_ls(g, Ct, mode, num_sms, plan, colc::LS);
 }
 
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
@@ -1028,13 +1099,13 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     p.ntiles = plan.ntiles;
     p.kc = kc;
     CUtensorMap tx, td;
-    if (!tmap(&td, d, g.pitch, g.H, 1, 2)) return cudaErrorInvalidValue;
+    if (!tmap(&td, d, g.pitch, g.H, 1, 2, plan.Ls)) return cudaErrorInvalidValue;
     if (mode != MODE_SUPPORT) {
-        if (!tmap(&tx, x, g.pitch, g.H, Ct, 3)) return cudaErrorInvalidValue;
+        if (!tmap(&tx, x, g.pitch, g.H, Ct, 3, plan.Ls)) return cudaErrorInvalidValue;
     } else {
         tx = td;
     }
-    const void* fn = colc_kernel(Ct, mode, nsq >= 0, ext != nullptr || edge != nullptr);
+    const void* fn = colc_kernel(Ct, mode, nsq >= 0, ext != nullptr || edge != nullptr, plan.Ls);
     if (!fn) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = plan.grid;
