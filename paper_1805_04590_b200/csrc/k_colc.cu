@@ -174,23 +174,23 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : max_threads<(MODE == MODE_SU
     }
     cluster_sync_all();  // every exchange barrier of the cluster is initialised and armed
 
-    auto stage_in = [&](int tile) {  // thread 0: TMA boxes of `tile` into the landing zone
+    // lane 0 of warp q: TMA boxes of segment q of `tile` into the landing zone (every warp
+    // issues its own segment's loads, so no warp carries the whole tile's issue)
+    auto stage_seg = [&](int tile, int q) {
         const int col0 = tile * TW;
         const uint32_t box = (uint32_t)(LSV * TW * sizeof(float));
-        for (int q = 0; q < S; ++q) {
-            const int rq = r0 + q * LSV;
-            const uint32_t bytes = rq < p.H ? box * (1 + (HASX ? NV : 0)) : 0u;
-            mbar_arrive_expect_tx(&bars[q], bytes);
-            if (bytes) {
-                tma_load_2d(ld + q * LSV * TW, &tm_d, col0, rq, &bars[q]);
-                if constexpr (HASX) {
+        const int rq = r0 + q * LSV;
+        const uint32_t bytes = rq < p.H ? box * (1 + (HASX ? NV : 0)) : 0u;
+        mbar_arrive_expect_tx(&bars[q], bytes);
+        if (bytes) {
+            tma_load_2d(ld + q * LSV * TW, &tm_d, col0, rq, &bars[q]);
+            if constexpr (HASX) {
 #pragma unroll
-                    for (int v = 0; v < NV; ++v) tma_load_3d(lx + (v * HB + q * LSV) * TW, &tm_x, col0, rq, v, &bars[q]);
-                }
+                for (int v = 0; v < NV; ++v) tma_load_3d(lx + (v * HB + q * LSV) * TW, &tm_x, col0, rq, v, &bars[q]);
             }
         }
     };
-    if (threadIdx.x == 0 && cluster < p.ntiles) stage_in(cluster);
+    if (c == 0 && cluster < p.ntiles) stage_seg(cluster, s);
 
     int k = 0;
     for (int tile = cluster; tile < p.ntiles; tile += nclusters, ++k) {
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : max_threads<(MODE == MODE_SU
             anext = (colok && rn < p.H) ? coef(ld[(lo + LSV) * TW + c]) : 0.f;
         }
         __syncthreads();  // landing zone free
-        if (threadIdx.x == 0 && tile + nclusters < p.ntiles) stage_in(tile + nclusters);
+        if (c == 0 && tile + nclusters < p.ntiles) stage_seg(tile + nclusters, s);
         if constexpr (MODE == MODE_UPDATE) {  // the write-out's Z / T / chat lines -> L2 (lane = row)
             const int r = r0 + lo + c;
             if (r < p.H) {
@@ -532,21 +532,19 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
     }
     cluster_sync_all();  // every exchange barrier of the cluster is initialised and armed
 
-    auto stage_in = [&](int tile) {  // thread 0: TMA boxes of `tile` into the landing zone
+    auto stage_seg = [&](int tile, int q) {  // lane 0 of warp q: segment q of `tile`
         const int col0 = tile * TW;
         const uint32_t box = (uint32_t)(LS * TW * sizeof(float));
-        for (int q = 0; q < S; ++q) {
-            const int rq = r0 + q * LS;
-            const uint32_t bytes = rq < p.H ? box * (1 + NX) : 0u;
-            mbar_arrive_expect_tx(&bars[q], bytes);
-            if (bytes) {
-                tma_load_2d(ld + q * LS * TW, &tm_d, col0, rq, &bars[q]);
+        const int rq = r0 + q * LS;
+        const uint32_t bytes = rq < p.H ? box * (1 + NX) : 0u;
+        mbar_arrive_expect_tx(&bars[q], bytes);
+        if (bytes) {
+            tma_load_2d(ld + q * LS * TW, &tm_d, col0, rq, &bars[q]);
 #pragma unroll
-                for (int v = 0; v < NX; ++v) tma_load_3d(lx + (v * HB + q * LS) * TW, &tm_x, col0, rq, v, &bars[q]);
-            }
+            for (int v = 0; v < NX; ++v) tma_load_3d(lx + (v * HB + q * LS) * TW, &tm_x, col0, rq, v, &bars[q]);
         }
     };
-    if (threadIdx.x == 0 && cluster < p.ntiles) stage_in(cluster);
+    if (c == 0 && cluster < p.ntiles) stage_seg(cluster, s);
 
     int k = 0;
     for (int tile = cluster; tile < p.ntiles; tile += nclusters, ++k) {
@@ -627,7 +625,7 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
             }
         }
         __syncthreads();  // landing zone free
-        if (threadIdx.x == 0 && tile + nclusters < p.ntiles) stage_in(tile + nclusters);
+        if (c == 0 && tile + nclusters < p.ntiles) stage_seg(tile + nclusters, s);
         if constexpr (MODE == MODE_UPDATE) {  // the write-out's Z / T / chat lines -> L2 (lane = row)
             const int r = r0 + lo + c;
             if (r < p.H) {
