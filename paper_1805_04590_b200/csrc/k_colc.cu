@@ -235,12 +235,12 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : max_threads<(MODE == MODE_SU
         float anext = 0.f;
         {
             const int rn = r0 + lo + LSV;
-            if (s + 1 == S && colok && rn < p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
-        }
-        __syncthreads();
-        if (s + 1 < S) {
-            const int rn = r0 + lo + LSV;
-            anext = (colok && rn < p.H) ? coef(ld[(lo + LSV) * TW + c]) : 0.f;
+            if (s + 1 == S) {
+                if (colok && rn < p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
+            } else {  // the next segment's first row: wait for its boxes too (no CTA barrier)
+                mbar_wait(&bars[s + 1], (uint32_t)(k & 1));
+                anext = (colok && rn < p.H) ? coef(ld[(lo + LSV) * TW + c]) : 0.f;
+            }
         }
         __syncthreads();  // landing zone free
         if (c == 0 && tile + nclusters < p.ntiles) stage_seg(tile + nclusters, s);
@@ -432,7 +432,8 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : max_threads<(MODE == MODE_SU
                 }
             }
         }
-        __syncthreads();  // segF / segR / carry reused by the next tile
+        // no barrier here: the next tile writes segF / segR / carry only after its
+        // landing-zone barrier, which every warp passes after finishing this tile
     }
     cluster_sync_all();  // no CTA leaves while another may still read its shared memory
 }
@@ -615,8 +616,8 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
                 if (s + 1 == S && colok && rn < p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
             }
         }
-        __syncthreads();
-        if (s + 1 < S) {
+        if (s + 1 < S) {  // the next segment's first row: wait for its boxes too (no CTA barrier)
+            mbar_wait(&bars[s + 1], (uint32_t)(k & 1));
             const int rn = r0 + lo + LS;
             if constexpr (BAND) {
                 if (colok && rn < p.H) anext = coef(ld[(lo + LS) * TW + c]);
@@ -857,7 +858,8 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
                 }
             }
         }
-        __syncthreads();  // segF / segR / carry reused by the next tile
+        // no barrier here: the next tile writes shared memory only after its landing-zone
+        // barrier, which every warp passes after finishing this tile
     }
     cluster_sync_all();  // no CTA leaves while another may still read its shared memory
 }
