@@ -395,3 +395,26 @@ def test_too_tall_image_is_a_shape_error():
         with dts.Solver(torch.from_numpy(g).cuda(), 8.0, 0.2, 3):
             pass
     assert "DTS_E_SHAPE" in str(ei.value)
+
+
+@pytest.mark.parametrize("H,W,Ct", [(1500, 330, 1), (9000, 200, 1), (2160, 390, 3), (700, 70, 2)])
+def test_repeat_solves_bit_identical(H, W, Ct, monkeypatch):
+    """Race stress for the cluster column kernels (per-warp TMA issue, no end-of-tile
+    barrier, link coefficient behind the next segment's mbarrier): their arithmetic order is
+    fixed, so a shared-memory hazard shows up as a run-to-run difference.  Shapes: several
+    CTAs per cluster with a ragged last segment, 15 CTAs per cluster, C_t = 3 and 2 on the
+    16-row-segment variant.  Ten eager solves each, outputs compared bit for bit."""
+    monkeypatch.setenv("DTS_NO_GRAPH", "1")
+    g, t, c = random_problem(H, W, 3, Ct, seed=H + W + Ct)
+    gd, td, cd = (torch.from_numpy(a).cuda() for a in (g, t, c))
+    outs = []
+    with dts.Solver(gd, 8.0, 0.1, 3) as s:
+        for _ in range(10):
+            o = torch.empty_like(td)
+            s.solve(td, cd, 0.99, 3, out=o)
+            outs.append(o)
+    torch.cuda.synchronize()
+    ref = outs[0].cpu().numpy()
+    assert np.isfinite(ref).all()
+    for o in outs[1:]:
+        assert np.array_equal(o.cpu().numpy(), ref)
