@@ -199,6 +199,14 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : max_threads<(MODE == MODE_SU
         const bool colok = col < p.W;
 
         // ---- 1. landing zone -> registers; refill with the next tile ----
+        // coefficient linking this segment's last row to the next row (the next segment's
+        // first row, or the next band's): straight from global -- L2-resident, as the TMA
+        // just brought it -- so no warp reads another warp's part of the landing zone
+        float anext = 0.f;
+        {
+            const int rn = r0 + lo + LSV;
+            if (colok && rn < p.H) anext = __ldg(p.d + (int64_t)rn * p.pitch + col);
+        }
         mbar_wait(&bars[s], (uint32_t)(k & 1));
         float a[LSV];
         float xv[NV][LSV];
@@ -232,17 +240,11 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : max_threads<(MODE == MODE_SU
         // coefficient linking this segment's last row to the next row: from the
         // landing zone (next segment; it landed before the barrier below) or, for the
         // band's last segment, straight from global (first row of the next band)
-        float anext = 0.f;
-        {
-            const int rn = r0 + lo + LSV;
-            if (s + 1 == S) {
-                if (colok && rn < p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
-            } else {  // the next segment's first row: wait for its boxes too (no CTA barrier)
-                mbar_wait(&bars[s + 1], (uint32_t)(k & 1));
-                anext = (colok && rn < p.H) ? coef(ld[(lo + LSV) * TW + c]) : 0.f;
-            }
-        }
-        __syncthreads();  // landing zone free
+        if (colok && r0 + lo + LSV < p.H) anext = coef(anext);
+        // this warp's segment is in registers: refill it with the next tile (only this warp
+        // reads it, so no CTA barrier; the next tile's shared-memory scratch writes are
+        // ordered by the fold barrier below, which every warp passes after this tile)
+        __syncwarp();
         if (c == 0 && tile + nclusters < p.ntiles) stage_seg(tile + nclusters, s);
         if constexpr (MODE == MODE_UPDATE) {  // the write-out's Z / T / chat lines -> L2 (lane = row)
             const int r = r0 + lo + c;
@@ -432,8 +434,9 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : max_threads<(MODE == MODE_SU
                 }
             }
         }
-        // no barrier here: the next tile writes segF / segR / carry only after its
-        // landing-zone barrier, which every warp passes after finishing this tile
+        // no barrier here: before the next tile's fold barrier a warp writes only its own
+        // segF slot and its own part of the landing zone, which no other warp reads after
+        // the anticausal carry barrier of this tile
     }
     cluster_sync_all();  // no CTA leaves while another may still read its shared memory
 }
@@ -562,6 +565,15 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
                                                             : 0.f;
         }
         // ---- 1. landing zone -> registers; refill with the next tile ----
+        // link coefficient of the segment's last row, raw from global (see the single-GPU
+        // kernel): the next segment's first row, the next band's, or row H (the link below
+        // the rank band); identity past it
+        float anext = 0.f;
+        {
+            const int rn = r0 + lo + LS;
+            const bool ld_ok = BAND ? (colok && rn <= p.H) : (colok && rn < p.H);
+            if (ld_ok) anext = __ldg(p.d + (int64_t)rn * p.pitch + col);
+        }
         mbar_wait(&bars[s], (uint32_t)(k & 1));
         float a[LS];
         float xv[NV][LS];
@@ -604,28 +616,15 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
         // band's last segment, straight from global (first row of the next band)
         // (row H of d is the link below the band: the next rank's first row in row-band mode,
         // +inf -- a = 0 -- at the image bottom)
-        float anext = 0.f;
         {
             const int rn = r0 + lo + LS;
             if constexpr (BAND) {
-                if (colok) {
-                    if (rn > p.H) anext = 1.f;  // identity rows past the link (see the load above)
-                    else if (s + 1 == S || rn == p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
-                }
+                if (colok) anext = rn > p.H ? 1.f : coef(anext);  // identity rows past the link
             } else {
-                if (s + 1 == S && colok && rn < p.H) anext = coef(__ldg(p.d + (int64_t)rn * p.pitch + col));
+                if (colok && rn < p.H) anext = coef(anext);
             }
         }
-        if (s + 1 < S) {  // the next segment's first row: wait for its boxes too (no CTA barrier)
-            mbar_wait(&bars[s + 1], (uint32_t)(k & 1));
-            const int rn = r0 + lo + LS;
-            if constexpr (BAND) {
-                if (colok && rn < p.H) anext = coef(ld[(lo + LS) * TW + c]);
-            } else {
-                anext = (colok && rn < p.H) ? coef(ld[(lo + LS) * TW + c]) : 0.f;
-            }
-        }
-        __syncthreads();  // landing zone free
+        __syncwarp();  // this warp's segment is in registers: refill it (only this warp reads it)
         if (c == 0 && tile + nclusters < p.ntiles) stage_seg(tile + nclusters, s);
         if constexpr (MODE == MODE_UPDATE) {  // the write-out's Z / T / chat lines -> L2 (lane = row)
             const int r = r0 + lo + c;
@@ -858,8 +857,8 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
                 }
             }
         }
-        // no barrier here: the next tile writes shared memory only after its landing-zone
-        // barrier, which every warp passes after finishing this tile
+        // no barrier here: before the next tile's fold barrier a warp writes only its own
+        // segF slot and its own part of the landing zone (as in the single-GPU kernel)
     }
     cluster_sync_all();  // no CTA leaves while another may still read its shared memory
 }
