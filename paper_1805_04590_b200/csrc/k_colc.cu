@@ -712,7 +712,19 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
             segR[(0 * S + s) * (TW + 1) + c] = Q;
 #pragma unroll
             for (int v = 0; v < NV; ++v) segR[((1 + v) * S + s) * (TW + 1) + c] = E[v];
-            // row-band outputs at row H - 1 (its warp only, warp-uniform): y of the x channels
+}
+        __syncthreads();
+        for (int cc = s; cc < TW; cc += S) seg_scan<NV, true>(segR, S, cc, totA);
+        __syncthreads();
+
+        // ---- 4. anticausal totals flow upwards the same way ----
+        for (int q = band - 1 - s; q >= 0; q -= S) {
+#pragma unroll
+            for (int k2 = 0; k2 < NV + 1; ++k2)
+                st_async_f32(remA + (band * (NV + 1) + k2) * TW + c, totA[k2 * TW + c], xbarA, (uint32_t)q);
+        }
+        {  // row-band outputs at row H - 1, off the critical path: while the exchange runs
+            // (its warp only, warp-uniform; xv still holds y): y of the x channels
             // (c = 0) and, in TUPLE mode, of g (c = 1) -- the rank band's causal map c_out = A c + B
             const int jl = p.H - 1 - (r0 + lo);
             if ((MODE == MODE_TUPLE || p.edge) && jl >= 0 && jl < LS) {
@@ -736,16 +748,6 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
                     }
                 }
             }
-        }
-        __syncthreads();
-        for (int cc = s; cc < TW; cc += S) seg_scan<NV, true>(segR, S, cc, totA);
-        __syncthreads();
-
-        // ---- 4. anticausal totals flow upwards the same way ----
-        for (int q = band - 1 - s; q >= 0; q -= S) {
-#pragma unroll
-            for (int k2 = 0; k2 < NV + 1; ++k2)
-                st_async_f32(remA + (band * (NV + 1) + k2) * TW + c, totA[k2 * TW + c], xbarA, (uint32_t)q);
         }
         if (s == 0) {
             mbar_wait_cluster(xbarA, (uint32_t)(k & 1));
