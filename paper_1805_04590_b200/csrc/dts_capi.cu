@@ -377,11 +377,30 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
         const size_t count = (size_t)pE.ntiles * NT * 32;
         const double px = (double)g.H * g.W;
         const bool pre = ctx->A1y && pass < 4;  // pass-1 coefficient squared per pass
+        // default: the single-context kernel (the link below the band cut: a_H taken as 0),
+        // whose output rows H - 1 and 0 are the exchanged y0(H - 1) and z0(0); the fix-up
+        // then carries z_H - y(H - 1) (reading R26).  DTS_BAND_EXPORT=1: the band kernel with
+        // the link, exporting those values itself (the bottom carry is z_H).
+        static const bool exporting = std::getenv("DTS_BAND_EXPORT") != nullptr;
         st = run_launch(ctx, F_COL, px * (8.0 * Ct + 4), s, [&] {
             return launch_col_cluster(pE, g, Ct, MODE_FILTER, x, pre ? ctx->A1y : ctx->dy, kc, nullptr, nullptr, s,
-                                      pre ? pass : -1, nullptr, nullptr, ctx->rank_tup);  // zero carries
+                                      pre ? pass : -1, nullptr, nullptr,
+                                      exporting ? ctx->rank_tup : nullptr);  // zero carries
         });
         if (st != DTS_OK) return st;
+        if (!exporting) {  // y0 at row H - 1 -> slots [0, Ct), z0 at row 0 -> slots [Ct, 2Ct)
+            for (int v = 0; v < Ct; ++v) {
+                const float* yrow = x + v * g.plane + (g.H - 1) * g.pitch;
+                const float* zrow = x + v * g.plane;
+                if ((e = cudaMemcpy2DAsync(ctx->rank_tup + v * 32, NT * 32 * sizeof(float), yrow, 32 * sizeof(float),
+                                           32 * sizeof(float), pE.ntiles, cudaMemcpyDeviceToDevice, s)) !=
+                        cudaSuccess ||
+                    (e = cudaMemcpy2DAsync(ctx->rank_tup + (Ct + v) * 32, NT * 32 * sizeof(float), zrow,
+                                           32 * sizeof(float), 32 * sizeof(float), pE.ntiles,
+                                           cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+                    return cuda_fail(e);
+            }
+        }
         // Gamma_0 of this rank into slot 2Ct of its records
         if ((e = cudaMemcpy2DAsync(ctx->rank_tup + 2 * Ct * 32, NT * 32 * sizeof(float), ctx->edge_gam[pass],
                                    32 * sizeof(float), 32 * sizeof(float), pE.ntiles, cudaMemcpyDeviceToDevice, s)) !=
@@ -399,7 +418,7 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
         if (ctx->comm->nranks > 1)  // a single rank has no edges to correct
             st = run_launch(ctx, F_COMPOSE, (double)2 * L * g.W * (8.0 * Ct + 4), s, [&] {
                 return launch_edge_fix(x, Ct, g, L, ctx->edge_gam[pass], ctx->edge_theta[pass], ctx->gathered,
-                                       ctx->comm->nranks, ctx->comm->rank, s);
+                                       ctx->comm->nranks, ctx->comm->rank, s, true, !exporting);
             });
         if (st != DTS_OK || mode != MODE_UPDATE) return st;
         return run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {

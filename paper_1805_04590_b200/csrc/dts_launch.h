@@ -160,10 +160,12 @@ cudaError_t launch_box_col(const BoxPlan& plan, const Geometry& g, int Ct, const
 // elementwise corrections after the gathered edge records.
 // raw: keep the causal product profile G (the support's correction) instead of its
 // anticausal response Gamma; cross = false: the bottom carry has no causal-carry term
-// (the support's P and Q recurrences are independent)
+// (the support's P and Q recurrences are independent); cut: the zero-carry pass cut the link
+// below the band (z(H-1) = y(H-1)), so the bottom carry is z_H - y(H-1)
 cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float kc, float* gam, float* theta,
                                  cudaStream_t s, bool raw = false);
 cudaError_t launch_edge_fix(float* x, int Ct, const Geometry& g, int L, const float* gam, const float* theta,
-                            const float* gathered, int P, int rank, cudaStream_t s, bool cross = true);
+                            const float* gathered, int P, int rank, cudaStream_t s, bool cross = true,
+                            bool cut = false);
 
 }  // namespace dts

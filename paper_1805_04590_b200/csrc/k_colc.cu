@@ -1173,7 +1173,7 @@ cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float
 // all from the gathered edge records [P][ntiles][2Ct+1][32] (slot 2Ct: Gamma_0)
 __global__ void k_edge_fix(float* __restrict__ x, int Ct, int64_t H, int64_t W, int64_t pitch, int64_t plane, int L,
                            const float* __restrict__ gam, const float* __restrict__ theta,
-                           const float* __restrict__ gath, int P, int rank, int ntiles, bool cross) {
+                           const float* __restrict__ gath, int P, int rank, int ntiles, bool cross, bool cut) {
     const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int kk = blockIdx.y;  // 0..2L-1: top rows, then bottom rows
     if (col >= W) return;
@@ -1191,6 +1191,9 @@ __global__ void k_edge_fix(float* __restrict__ x, int Ct, int64_t H, int64_t W, 
             const float ylast = gath[rank * rstride + (t * NT + v) * colc::TW + cc];
             carry = cross ? fmaf(ylast, nb[(2 * Ct) * colc::TW + cc], nb[(Ct + v) * colc::TW + cc])
                           : nb[(Ct + v) * colc::TW + cc];
+            // cut pass (the link below was taken as 0, so z(H-1) = y(H-1)): the missing part is
+            // a_H (z_H - y(H-1)), carried upwards by the same Theta
+            if (cut) carry -= ylast;
         }
         if (carry != 0.f) {
             const float prof = top ? gam[(int64_t)kk * pitch + col] : theta[(int64_t)(kk - L) * pitch + col];
@@ -1201,11 +1204,11 @@ __global__ void k_edge_fix(float* __restrict__ x, int Ct, int64_t H, int64_t W, 
 }
 
 cudaError_t launch_edge_fix(float* x, int Ct, const Geometry& g, int L, const float* gam, const float* theta,
-                            const float* gathered, int P, int rank, cudaStream_t s, bool cross) {
+                            const float* gathered, int P, int rank, cudaStream_t s, bool cross, bool cut) {
     const int ntiles = (int)((g.W + colc::TW - 1) / colc::TW);
     dim3 grid((unsigned)((g.W + 127) / 128), (unsigned)(2 * L));
     k_edge_fix<<<grid, 128, 0, s>>>(x, Ct, g.H, g.W, g.pitch, g.plane, L, gam, theta, gathered, P, rank, ntiles,
-                                    cross);
+                                    cross, cut);
     return cudaGetLastError();
 }
 

@@ -119,3 +119,30 @@ def edge_scheme(x, A, cuts, L):
         z[-L:] += e * theta
         out.append(z)
     return np.concatenate(out)
+
+
+def edge_scheme_cut(x, A, cuts, L, fix_carry=True):
+    """The edge scheme with the link below each band cut (a_hi taken as 0 in the zero-carry
+    pass, as the single-context column kernel does at its last row).  The cut pass's output
+    at the band's last row is y0 itself and at its first row z0, so the exchanged values are
+    read from the output; the bottom carry becomes z_hi - y0(hi - 1) on the same Theta."""
+    P = len(cuts) - 1
+    H = cuts[-1]
+    zs, prof = [], []
+    for k in range(P):
+        lo, hi = cuts[k], cuts[k + 1]
+        below = A[hi] if hi < H else 0.0
+        _, z0 = zero_carry_pass(x, A, lo, hi, 0.0)  # cut below
+        zs.append(z0)
+        prof.append(edge_profiles(A, lo, hi, below, L))
+    out = []
+    for k in range(P):
+        z = zs[k].copy()
+        ylast = zs[k][-1]  # = y0 at the last row (the cut makes z = y there)
+        c = zs[k - 1][-1] if k > 0 else 0.0
+        e = (zs[k + 1][0] + ylast * prof[k + 1][1][0]) - (ylast if fix_carry else 0.0) if k + 1 < P else 0.0
+        _, gam, theta = prof[k]
+        z[:L] += c * gam
+        z[-L:] += e * theta
+        out.append(z)
+    return np.concatenate(out)

@@ -143,6 +143,30 @@ def test_edge_scheme_algebra(P):
     assert np.max(np.abs(got - ref)) <= 2.0 ** -24 * np.max(np.abs(x))
 
 
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+def test_edge_scheme_cut_variant(P):
+    """The edge scheme run on the single-context column kernel: the zero-carry pass cuts the
+    link below the band (a_H = 0), so row H - 1 of its output is y0 and row 0 is z0; the
+    bottom correction is (z_H - y0(H - 1)) Theta_k with the uncut Theta.  Equals the full
+    column pass to below 2^-26, like the exported-value scheme."""
+    rng = np.random.default_rng(10 + P)
+    H = 480
+    amax = 0.7
+    A = rng.uniform(0.3, amax, H)
+    A[0] = 0.0
+    x = rng.normal(size=H)
+    ref = dense.pass1d(A) @ x
+    L = int(np.ceil(np.log(2.0 ** -26) / np.log(amax)))
+    cuts = [k * H // P for k in range(P + 1)]
+    got = bandalg.edge_scheme_cut(x, A, cuts, L)
+    assert np.max(np.abs(got - ref)) <= 2.0 ** -24 * np.max(np.abs(x))
+    # the changed bottom carry matters: with the exported-value scheme's carry the bands
+    # would not join
+    if P > 1:
+        bad = bandalg.edge_scheme_cut(x, A, cuts, L, fix_carry=False)
+        assert np.max(np.abs(bad - ref)) > 1e-3 * np.max(np.abs(x))
+
+
 def test_edge_scheme_support_variant():
     """The support's edge scheme: s = P + Q - 1 (P[k] = 1 + a_k P[k-1], Q[k] = 1 + a_{k+1} Q[k+1]),
     zero-carry s0 per band, carries c = s0 at the last row of the band above (P carry) and
