@@ -59,6 +59,73 @@ __global__ void __launch_bounds__(256) k_box_increments(const float* __restrict_
     qy[r * pitch + c] = r == 0 ? 0u : increment(p, p - W * C, C, k2);
 }
 
+// R25 quantisation of a channel sum s (the tail of increment() above)
+__device__ __forceinline__ uint32_t quantise(float s, float k2) {
+    const float v = __fadd_rn(1.0f, __fmul_rn(k2, s));
+    const float d = __fsqrt_rn(v);
+    const long long q = __float2ll_rn(__fmul_rn(d, 65536.0f));
+    return q > (long long)QMAX ? QMAX : (uint32_t)q;
+}
+
+// K_B1 for C = 4Q channels (16-B aligned guide): the layout of the guide-derivative kernel
+// (k_misc.cu k_guide_deriv_vec).  A thread walks 32 rows of one column; a pixel's channels
+// arrive as Q float4 loads, the row above stays in registers, the next row is in flight;
+// a warp covers 31 output columns and lane 0 loads the column before them, so every left
+// neighbour comes by shuffle.  The channel sums keep increment()'s order and rounding.
+constexpr int BI_ROWS = 32, BI_COLS = 8 * 31;
+template <int Q>
+__global__ void __launch_bounds__(256) k_box_increments_vec(const float* __restrict__ guide, float k2, int64_t H,
+                                                            int64_t W, int64_t pitch, uint32_t* __restrict__ qx,
+                                                            uint32_t* __restrict__ qy) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t c = (int64_t)blockIdx.x * BI_COLS + warp * 31 + lane - 1;  // lane 0: c0 - 1
+    const int64_t rbeg = (int64_t)blockIdx.y * BI_ROWS;
+    const int64_t rend = min(rbeg + (int64_t)BI_ROWS, H);
+    const bool writer = lane > 0 && c < W;
+    const int64_t cc = c < 0 ? 0 : (c >= W ? W - 1 : c);  // clamped: shuffles stay defined
+    auto px = [&](int64_t r) { return reinterpret_cast<const float4*>(guide + (r * W + cc) * (4 * Q)); };
+    float4 up[Q], cur[Q], ncur[Q];
+    if (rbeg > 0) {
+        const float4* pu = px(rbeg - 1);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) up[q] = __ldg(pu + q);
+    }
+    {
+        const float4* pc = px(rbeg);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) cur[q] = __ldg(pc + q);
+    }
+    for (int64_t r = rbeg; r < rend; ++r) {
+        if (r + 1 < rend) {
+            const float4* pc = px(r + 1);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) ncur[q] = __ldg(pc + q);
+        }
+        float sx = 0.0f, sy = 0.0f;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const float a[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
+            const float u[4] = {up[q].x, up[q].y, up[q].z, up[q].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {  // channel 4q + e, in order
+                const float l = __shfl_up_sync(0xffffffffu, a[e], 1);
+                const float dxv = __fsub_rn(a[e], l), dyv = __fsub_rn(a[e], u[e]);
+                sx = __fadd_rn(sx, __fmul_rn(dxv, dxv));
+                sy = __fadd_rn(sy, __fmul_rn(dyv, dyv));
+            }
+        }
+        if (writer) {
+            qx[r * pitch + c] = c == 0 ? 0u : quantise(sx, k2);
+            qy[r * pitch + c] = r == 0 ? 0u : quantise(sy, k2);
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            up[q] = cur[q];
+            cur[q] = ncur[q];
+        }
+    }
+}
+
 constexpr int MAXR = 17;  // N <= 16 passes + the support radius
 struct Radii {
     long long R[MAXR];  // R[0..N-1]: passes, R[N]: support
@@ -363,6 +430,14 @@ static int occupancy(const void* fn, int threads, size_t smem) {
 cudaError_t launch_box_increments(const float* guide, int C, float k2, const Geometry& g, uint32_t* qx, uint32_t* qy,
                                   cudaStream_t s) {
     dim3 grid((unsigned)((g.W + 255) / 256), (unsigned)g.H);
+    if ((C == 4 || C == 8 || C == 16) && (uintptr_t)guide % 16 == 0 && !std::getenv("DTS_BOX_SCALAR")) {
+        const dim3 gv((unsigned)((g.W + 1 + box::BI_COLS - 1) / box::BI_COLS),
+                      (unsigned)((g.H + box::BI_ROWS - 1) / box::BI_ROWS));
+        if (C == 4) box::k_box_increments_vec<1><<<gv, 256, 0, s>>>(guide, k2, g.H, g.W, g.pitch, qx, qy);
+        if (C == 8) box::k_box_increments_vec<2><<<gv, 256, 0, s>>>(guide, k2, g.H, g.W, g.pitch, qx, qy);
+        if (C == 16) box::k_box_increments_vec<4><<<gv, 256, 0, s>>>(guide, k2, g.H, g.W, g.pitch, qx, qy);
+        return cudaGetLastError();
+    }
     box::k_box_increments<<<grid, 256, 0, s>>>(guide, C, k2, g.H, g.W, g.pitch, qx, qy);
     return cudaGetLastError();
 }

@@ -74,7 +74,9 @@ def check_solve(g, t, c, ss, sr, N, lam, iters, radius_scale=0.0, **kw):
 @pytest.mark.parametrize("H,W,C,ss,sr,N", [
     (1, 1, 1, 8.0, 0.2, 3), (7, 5, 3, 4.0, 0.5, 1), (48, 64, 3, 8.0, 0.2, 3),
     (130, 300, 3, 16.0, 0.5, 3), (33, 70, 16, 64.0, 0.2, 3), (40, 2500, 2, 30.0, 1.0, 2),
-    (900, 45, 1, 50.0, 2.0, 4)])
+    (900, 45, 1, 50.0, 2.0, 4),
+    # float4 increments kernel (C = 4, 8, 16): several 248-column blocks and 32-row blocks
+    (70, 600, 4, 10.0, 0.3, 3), (65, 530, 8, 20.0, 0.3, 2), (40, 260, 16, 8.0, 0.1, 3)])
 def test_box_tables_bit_exact(H, W, C, ss, sr, N):
     g, _, _ = random_problem(H, W, C, 1, seed=H * 7 + W)
     check_tables(g, ss, sr, N)
