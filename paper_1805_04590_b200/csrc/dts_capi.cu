@@ -381,7 +381,7 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
         // whose output rows H - 1 and 0 are the exchanged y0(H - 1) and z0(0); the fix-up
         // then carries z_H - y(H - 1) (reading R26).  DTS_BAND_EXPORT=1: the band kernel with
         // the link, exporting those values itself (the bottom carry is z_H).
-        static const bool exporting = std::getenv("DTS_BAND_EXPORT") != nullptr;
+        const bool exporting = std::getenv("DTS_BAND_EXPORT") != nullptr;
         st = run_launch(ctx, F_COL, px * (8.0 * Ct + 4), s, [&] {
             return launch_col_cluster(pE, g, Ct, MODE_FILTER, x, pre ? ctx->A1y : ctx->dy, kc, nullptr, nullptr, s,
                                       pre ? pass : -1, nullptr, nullptr,

@@ -144,3 +144,19 @@ def test_bands_edge_scheme_matches_tuple_scheme(P, monkeypatch):
     rng = target_range(t)
     assert np.max(np.abs(a - b)) <= 1e-5 * rng
     assert np.max(np.abs(a - oracle.solve(g, t, c, *args))) <= 1e-4 * rng
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_bands_cut_edge_scheme_matches_exporting_kernel(P, monkeypatch):
+    """Reading R26: the edge scheme on the single-context kernel (link below each band cut,
+    edge values read from the output rows, bottom carry z_H - y(H-1)) against the band
+    kernel that keeps the link and exports the edge values (DTS_BAND_EXPORT=1).  Same
+    result to fp32 rounding, and both match the oracle."""
+    g, t, c = random_problem(1200, 90, 3, 1, seed=31 + P)
+    args = (5.0, 0.2, 3, 0.99, 4)
+    a = solve_bands(g, t, c, *args, P=P)
+    monkeypatch.setenv("DTS_BAND_EXPORT", "1")
+    b = solve_bands(g, t, c, *args, P=P)
+    rng = target_range(t)
+    assert np.max(np.abs(a - b)) <= 1e-5 * rng
+    assert np.max(np.abs(a - oracle.solve(g, t, c, *args))) <= 1e-4 * rng
