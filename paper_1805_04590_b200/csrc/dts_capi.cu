@@ -263,7 +263,21 @@ cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* 
             plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 16) == cudaSuccess)
             return cudaSuccess;
         cudaGetLastError();
-        if (plan_col_cluster(g, Ct, mode, num_sms, plan) == cudaSuccess) return cudaSuccess;
+        if (plan_col_cluster(g, Ct, mode, num_sms, plan) == cudaSuccess) {
+            // C_t = 1 FILTER with several tile rounds per launch (throughput-bound): 16 warps
+            // x 40-row segments (C4: 0.265 -> 0.249 ms).  One-round images are latency-bound
+            // and keep 32-row segments (C1: 12.6 us against 16.8 with 40-row ones).
+            const int clusters = (int)(plan->grid.x / plan->CB);
+            const int rounds = (plan->ntiles + clusters - 1) / clusters;
+            const char* f40 = std::getenv("DTS_COL_LS40");  // 0 / 1: force off / on
+            const bool want40 = f40 ? f40[0] == '1' : rounds >= 4;
+            ColPlan p40{};
+            if (Ct == 1 && mode == MODE_FILTER && want40 &&
+                plan_col_cluster_ls(g, Ct, mode, num_sms, &p40, 40) == cudaSuccess)
+                *plan = p40;
+            cudaGetLastError();
+            return cudaSuccess;
+        }
     }
     cudaGetLastError();
     return plan_col_pass(g, Ct, mode, num_sms, plan);
@@ -367,8 +381,12 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
     // pass exports y at row H - 1 and z at row 0, one all-gather of those per-column values,
     // then the corrections on the L rows at each edge
     ColPlan pE;
+    const bool exporting = std::getenv("DTS_BAND_EXPORT") != nullptr;
     if (mode != MODE_SUPPORT && pass >= 0 && pass < (int)ctx->edge_gam.size() && ctx->edge_gam[pass] &&
-        !std::getenv("DTS_BAND_TUPLE") && plan_col_cluster(g, Ct, MODE_FILTER, ctx->num_sms, &pE) == cudaSuccess) {
+        !std::getenv("DTS_BAND_TUPLE") &&
+        (exporting ? plan_col_cluster(g, Ct, MODE_FILTER, ctx->num_sms, &pE)
+                   : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &pE)) == cudaSuccess &&
+        pE.kind == 1) {
         dts_status st;
         cudaError_t e;
         if ((st = ensure_band_buffers(ctx, s)) != DTS_OK) return st;
@@ -381,7 +399,6 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
         // whose output rows H - 1 and 0 are the exchanged y0(H - 1) and z0(0); the fix-up
         // then carries z_H - y(H - 1) (reading R26).  DTS_BAND_EXPORT=1: the band kernel with
         // the link, exporting those values itself (the bottom carry is z_H).
-        const bool exporting = std::getenv("DTS_BAND_EXPORT") != nullptr;
         st = run_launch(ctx, F_COL, px * (8.0 * Ct + 4), s, [&] {
             return launch_col_cluster(pE, g, Ct, MODE_FILTER, x, pre ? ctx->A1y : ctx->dy, kc, nullptr, nullptr, s,
                                       pre ? pass : -1, nullptr, nullptr,

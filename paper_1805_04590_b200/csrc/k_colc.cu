@@ -119,7 +119,7 @@ constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
 // LSV: rows per warp segment; 16 for C_t >= 2 FILTER passes of images up to 16 x 320 rows
 // (half the registers per thread, so 20 warps fit where 32-row segments allow 11-14)
 template <int CT, int MODE, bool PRE, int LSV = LS>
-__global__ void __launch_bounds__(LSV == 16 ? 640 : max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>(), 1)
+__global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()), 1)
     k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
     constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
     constexpr bool HASX = MODE != MODE_SUPPORT;
@@ -907,6 +907,11 @@ static const void* kptr16() {
     return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE_FILTER, PRE, 16>);
 }
 static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = false, int ls = colc::LS) {
+    if (ls == 40) {  // experiment: 16 warps x 40-row segments, C_t = 1 FILTER
+        if (mode != MODE_FILTER || band || Ct != 1) return nullptr;
+        return pre ? reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, true, 40>)
+                   : reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, false, 40>);
+    }
     if (ls == 16) {  // FILTER, C_t >= 2, single context
         if (mode != MODE_FILTER || band) return nullptr;
         switch (Ct * 2 + (pre ? 1 : 0)) {

@@ -397,7 +397,7 @@ def test_too_tall_image_is_a_shape_error():
     assert "DTS_E_SHAPE" in str(ei.value)
 
 
-@pytest.mark.parametrize("H,W,Ct", [(1500, 330, 1), (9000, 200, 1), (2160, 390, 3), (700, 70, 2)])
+@pytest.mark.parametrize("H,W,Ct", [(1500, 330, 1), (9000, 200, 1), (2160, 390, 3), (700, 70, 2), (1300, 4100, 1)])
 def test_repeat_solves_bit_identical(H, W, Ct, monkeypatch):
     """Race stress for the cluster column kernels (per-warp TMA issue, no end-of-tile
     barrier, link coefficient behind the next segment's mbarrier): their arithmetic order is
@@ -418,3 +418,13 @@ def test_repeat_solves_bit_identical(H, W, Ct, monkeypatch):
     assert np.isfinite(ref).all()
     for o in outs[1:]:
         assert np.array_equal(o.cpu().numpy(), ref)
+
+
+def test_forty_row_segments_parity(monkeypatch):
+    """C_t = 1 images with several cluster tile rounds per column pass take the 16-warp x
+    40-row-segment instantiation of the cluster kernel (plan_col); a wide image reaches it.
+    Parity with the oracle, and again with the 32-row kernel forced (DTS_COL_LS40=0)."""
+    g, t, c = random_problem(1300, 4100, 3, 1, seed=77)
+    check(g, t, c, 6.0, 0.15, 3, 0.99, 3)
+    monkeypatch.setenv("DTS_COL_LS40", "0")
+    check(g, t, c, 6.0, 0.15, 3, 0.99, 3)
