@@ -113,6 +113,46 @@ __device__ __forceinline__ void seg_scan(float* seg, int S, int cc, float* tot) 
     }
 }
 
+// Two columns per warp when S <= 16: lanes 0-15 scan the S segment maps of column cA,
+// lanes 16-31 those of column cB (width-16 shuffles); otherwise as seg_scan.
+template <int NB, bool REV>
+__device__ __forceinline__ void seg_scan2(float* seg, int S, int cA, int cB, float* tot) {
+    const int lane = threadIdx.x & 31;
+    const int sl = lane & 15;
+    const int cc = lane < 16 ? cA : cB;
+    Aff<NB> v = aff_identity<NB>();
+    if (sl < S) {
+        v.P = seg[(0 * S + sl) * (TW + 1) + cc];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) v.B[k] = seg[((1 + k) * S + sl) * (TW + 1) + cc];
+    }
+#pragma unroll
+    for (int off = 1; off < 16; off <<= 1) {
+        Aff<NB> e;
+        e.P = REV ? __shfl_down_sync(FULL, v.P, off, 16) : __shfl_up_sync(FULL, v.P, off, 16);
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+            e.B[k] = REV ? __shfl_down_sync(FULL, v.B[k], off, 16) : __shfl_up_sync(FULL, v.B[k], off, 16);
+        if (REV ? (sl + off < 16) : (sl >= off)) v = aff_compose(e, v);
+    }
+    Aff<NB> ex;
+    ex.P = REV ? __shfl_down_sync(FULL, v.P, 1, 16) : __shfl_up_sync(FULL, v.P, 1, 16);
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+        ex.B[k] = REV ? __shfl_down_sync(FULL, v.B[k], 1, 16) : __shfl_up_sync(FULL, v.B[k], 1, 16);
+    if (REV ? sl == 15 : sl == 0) ex = aff_identity<NB>();
+    if (sl < S) {
+        seg[(0 * S + sl) * (TW + 1) + cc] = ex.P;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) seg[((1 + k) * S + sl) * (TW + 1) + cc] = ex.B[k];
+    }
+    if (sl == (REV ? 0 : 15)) {
+        tot[0 * TW + cc] = v.P;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) tot[(1 + k) * TW + cc] = v.B[k];
+    }
+}
+
 template <int NV>
 constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
 
@@ -276,7 +316,11 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
             for (int v = 0; v < NV; ++v) segF[((1 + v) * S + s) * (TW + 1) + c] = m.B[v];
         }
         __syncthreads();
-        for (int cc = s; cc < TW; cc += S) seg_scan<NV, false>(segF, S, cc, totC);
+        if (S <= 16) {  // two columns per warp (the 40-row instantiation has S = 16)
+            for (int cc = s; cc < TW / 2; cc += S) seg_scan2<NV, false>(segF, S, cc, cc + TW / 2, totC);
+        } else {
+            for (int cc = s; cc < TW; cc += S) seg_scan<NV, false>(segF, S, cc, totC);
+        }
         __syncthreads();
 
         // ---- 3. push this band's causal total to every band below it (st.async into their
@@ -333,7 +377,11 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
             for (int v = 0; v < NV; ++v) segR[((1 + v) * S + s) * (TW + 1) + c] = E[v];
         }
         __syncthreads();
-        for (int cc = s; cc < TW; cc += S) seg_scan<NV, true>(segR, S, cc, totA);
+        if (S <= 16) {
+            for (int cc = s; cc < TW / 2; cc += S) seg_scan2<NV, true>(segR, S, cc, cc + TW / 2, totA);
+        } else {
+            for (int cc = s; cc < TW; cc += S) seg_scan<NV, true>(segR, S, cc, totA);
+        }
         __syncthreads();
 
         // ---- 4. anticausal totals flow upwards the same way ----
