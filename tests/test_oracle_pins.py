@@ -716,3 +716,98 @@ def test_box_solve_equals_dense_iteration():
         z = z - step * (lam * (z - K @ z) + c.astype(np.float64).ravel() * (z - T))
     got = oracle.solve_box(g, t, c, 3.0, 0.5, N, lam, iters, step=step, support_mode=1)
     np.testing.assert_allclose(got.ravel(), z, rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------------------
+# Round 2: pins for the parts the round-1 review found unpinned (VERDICT r1 "What's weak" 1)
+
+def _dense_diag(K, chat, t, lam, step, iters):
+    """O6 diagnostics written out with the dense operator (reading R13):
+    per k, at Z^k: [max |g|, ||g||_2, lam/2 ||Z - zbar||^2 + 1/2 sum chat (Z - T)^2,
+    lam/2 Z.(Z - zbar) + 1/2 sum chat (Z - T)^2], g = lam (Z - zbar) + chat (Z - T)."""
+    z = t.copy()
+    rows, signs = [], []
+    for _ in range(iters):
+        zb = K @ z
+        gk = lam * (z - zb) + chat * (z - t)
+        data = 0.5 * float(np.sum(chat * (z - t) ** 2))
+        rows.append([float(np.max(np.abs(gk))), float(np.sqrt(np.sum(gk * gk))),
+                     0.5 * lam * float(np.sum((z - zb) ** 2)) + data,
+                     0.5 * lam * float(z @ (z - zb)) + data])
+        signs.append(float(np.max(gk)) < float(np.max(np.abs(gk))))  # the most negative g dominates
+        z = z - step * gk
+    return np.array(rows), signs
+
+
+def test_solve_diagnostics_equal_dense_values():
+    """The four O6 diagnostics against their definitions evaluated with the dense operator K
+    (tests/dense.py) and the brute-force support, over three iterations (k = 0 has Z = T, so the
+    data terms of F_hat and E_q are pinned from k = 1 on).  The target is run with both signs, so
+    on at least one iterate the most negative gradient outweighs the most positive one: a
+    ||g||_inf taken without |.| fails there; ||g||_2 without the square or the root fails."""
+    g, t, c = random_problem(5, 6, 3, 1, seed=6, conf_lo=0.2)
+    ss, sr, lam, step, iters = 3.0, 0.3, 0.9, 0.99, 3
+    dx, dy = oracle.distances(g, ss, sr)
+    K = dense.dtf_operator(dx, dy, oracle.sigmas(ss, 3))
+    chat = (c.astype(np.float64) / brute_support(dx, dy, ss)).ravel()
+    negative_dominant = 0
+    for sign in (1.0, -1.0):
+        ts = (sign * t).astype(np.float32)
+        want, signs = _dense_diag(K, chat, ts.astype(np.float64).ravel(), lam, step, iters)
+        negative_dominant += sum(signs)
+        _, diag = oracle.solve(g, ts, c, ss, sr, 3, lam, iters, step=step, diagnostics=True)
+        np.testing.assert_allclose(diag, want, rtol=1e-11, atol=1e-15)
+        assert np.all(want[1:, 2] != want[1:, 3])  # F_hat and E_q differ once Z != T
+    assert negative_dominant >= 1
+
+
+def test_solve_diagnostics_two_channels_and_support_off():
+    """Diagnostics sum over every channel (reading R14) and follow support_mode 1 (chat = c)."""
+    g, t, c = random_problem(4, 5, 3, 2, seed=12, conf_lo=0.3)
+    ss, sr, lam, step, iters = 2.5, 0.4, 0.99, 0.99, 2
+    dx, dy = oracle.distances(g, ss, sr)
+    K = dense.dtf_operator(dx, dy, oracle.sigmas(ss, 3))
+    KK = np.kron(np.eye(2), K)
+    for mode, S in ((0, brute_support(dx, dy, ss)), (1, np.ones(dx.shape))):
+        chat = np.tile((c.astype(np.float64) / S).ravel(), 2)
+        tt = np.concatenate([t[..., 0].astype(np.float64).ravel(), t[..., 1].astype(np.float64).ravel()])
+        want, _ = _dense_diag(KK, chat, tt, lam, step, iters)
+        _, diag = oracle.solve(g, t, c, ss, sr, 3, lam, iters, step=step, support_mode=mode, diagnostics=True)
+        np.testing.assert_allclose(diag, want, rtol=1e-11, atol=1e-15)
+
+
+def test_confidence_clamp_of_rounding_residues():
+    """Reading R22: V = DTF(z^2) - DTF(z)^2 is clamped at 0.  A constant target that is not a
+    dyadic fraction leaves rounding residues of either sign in the two filtered planes; the
+    clamp must turn every negative one into exactly 0, so with a tiny sigma_c the confidence
+    never exceeds 1 (without the clamp exp(-V / 2 sigma_c^2) > 1 wherever V < 0)."""
+    g, _, _ = random_problem(16, 21, 3, 1, seed=11)
+    t = np.full((16, 21), 0.1, np.float32)
+    z = float(t[0, 0])
+    K = dense.dtf_operator(*oracle.distances(g, 5.0, 0.2), oracle.sigmas(5.0, 3))
+    zz = np.full(t.size, z)
+    resid = (K @ (zz * zz)) - (K @ zz) ** 2  # rounding residues of the dense form
+    assert np.max(np.abs(resid)) < 1e-15
+    c, v = oracle.confidence(g, t, 5.0, 0.2, 3, 1e-9)
+    assert np.all(v >= 0.0) and np.all(v < 1e-15)
+    assert np.all(c <= 1.0)
+    assert np.sum(v == 0.0) >= 0.2 * v.size  # the clamped residues (about half of them)
+
+
+def test_box_radius_is_floored_on_a_tie():
+    """Reading R25: R = floor(r 2^16).  Constant guide: every increment is q = 2^16 exactly, so
+    T_j - T_i = 2^16 |j - i|.  With r = 2 - 2^-17 (N = 1, radius_scale 1: r = sigma_s), r 2^16 =
+    131071.5: floor keeps +-1 pixel (131072 > 131071), ceil or round would keep +-2."""
+    ss = 2.0 - 2.0 ** -17
+    assert oracle.box_radius(1.0, ss) == 131071
+    H, W = 6, 9
+    lox, hix, loy, hiy, S = oracle.box_tables(const_guide(H, W), ss, 0.2, 1, radius_scale=1.0)
+    i = np.arange(W)
+    np.testing.assert_array_equal(lox[0], np.broadcast_to(np.minimum(i, 1), (H, W)))
+    np.testing.assert_array_equal(hix[0], np.broadcast_to(np.minimum(W - 1 - i, 1), (H, W)))
+    j = np.arange(H)[:, None]
+    np.testing.assert_array_equal(loy[0], np.broadcast_to(np.minimum(j, 1), (H, W)))
+    np.testing.assert_array_equal(hiy[0], np.broadcast_to(np.minimum(H - 1 - j, 1), (H, W)))
+    cx = np.minimum(i, 1) + np.minimum(W - 1 - i, 1) + 1
+    cy = np.minimum(j, 1) + np.minimum(H - 1 - j, 1) + 1
+    np.testing.assert_array_equal(S, cy * cx[None, :])
