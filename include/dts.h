@@ -111,6 +111,13 @@ typedef struct {
     float step;          /* gradient step; <= 0 selects the paper's 0.99        */
     int32_t support_mode;/* 0: S = s_x * s_y (R7, default); 1: S = 1 (unweighted c)     */
     int32_t check_inputs;/* 1: verify finite target/confidence and c in [0,1] (syncs)   */
+    float* resid_inf_out;/* NULL, or `iterations` floats (device or host memory): entry k
+                            receives ||g_k||_inf, the max-norm of the Eq. (3) gradient
+                            g_k = lambda (z^k - zbar^k) + chat (z^k - t) at iterate k
+                            (reading R13), over all pixels and channels of this
+                            context (row-band contexts: of this rank's rows).  Computed on
+                            the device inside the update kernels (a max: deterministic).
+                            Must not overlap `out` or `target`.                            */
 } dts_solve_opts;
 
 /* dts_solve with options; opts == NULL is exactly dts_solve. */
@@ -261,6 +268,22 @@ void dts_comm_destroy(dts_comm* comm); /* NULL-safe; destroy after the contexts 
 dts_status dts_create_band(const float* guide_with_halo, int64_t H_total, int64_t row0, int64_t rows,
                            int64_t W, int32_t C, float sigma_s, float sigma_r, int32_t filter_passes,
                            dts_comm* comm, void* stream, dts_ctx** out_ctx);
+
+/* ---- test / experiment options (process-wide; the defaults are the product path) ----
+ * dts_set_option(name, value) selects among equivalent implementations so that tests can
+ * check each against the oracle; it never changes what is computed.  Names and values:
+ *   "col_kernel"   0 cluster column kernel when a column tile fits a cluster (default),
+ *                  1 the decoupled band-tuple kernel everywhere
+ *   "band_scheme"  row-band contexts (latched at dts_create_band): 0 edge fix-up where the
+ *                  bands allow it (default), 1 cluster TUPLE/APPLY, 2 decoupled kernel
+ *   "graphs"       1 replay repeated identical solves as CUDA graphs (default), 0 never
+ *   "persistent"   1 one persistent kernel per solve for L2-resident C_t = 1 images, 0 (default) off
+ *   "row_update"   1 Eq. (3) step fused into the next iteration's first row pass (default)
+ *   "col_rows"     0 auto (default), 32 or 40: rows per warp segment of the C_t = 1 column kernel
+ *   "col_cluster"  0 auto (default), 1..16: forced column-kernel cluster size
+ * Returns DTS_E_ARG for an unknown name or value.  dts_get_option returns -1 for unknown names. */
+dts_status dts_set_option(const char* name, int32_t value);
+int32_t dts_get_option(const char* name);
 
 /* Library version string. */
 const char* dts_version(void);

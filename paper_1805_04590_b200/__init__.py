@@ -23,7 +23,7 @@ __all__ = ["DTSError", "dts_create", "dts_solve", "dts_solve_ex", "dts_confidenc
            "dts_status_string",
            "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback", "dts_comm_destroy",
            "dts_create_band", "band_rows", "band_guide_rows",
-           "dts_debug_read", "dts_profile_enable", "dts_profile_read", "dts_launch_count", "dts_version",
+           "dts_debug_read", "dts_set_option", "dts_get_option", "options", "dts_profile_enable", "dts_profile_read", "dts_launch_count", "dts_version",
            "Solver", "lib_path", "load_library", "DTS_BUF_DX", "DTS_BUF_DY", "DTS_BUF_SUPPORT",
            "ABI_FUNCTIONS"]
 
@@ -39,7 +39,7 @@ ABI_FUNCTIONS = ["dts_create", "dts_solve", "dts_destroy", "dts_status_string", 
                  "dts_solve_ex", "dts_debug_read", "dts_profile_enable", "dts_profile_read",
                  "dts_launch_count", "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback",
                  "dts_comm_destroy", "dts_create_band", "dts_version", "dts_confidence", "dts_solve_stereo",
-                 "dts_sr_prepare", "dts_create_ex", "dts_debug_read_windows"]
+                 "dts_sr_prepare", "dts_create_ex", "dts_debug_read_windows", "dts_set_option", "dts_get_option"]
 
 
 class DTSError(RuntimeError):
@@ -57,7 +57,9 @@ class CreateOpts(ctypes.Structure):
 
 
 class SolveOpts(ctypes.Structure):
-    _fields_ = [("step", ctypes.c_float), ("support_mode", ctypes.c_int32), ("check_inputs", ctypes.c_int32)]
+    """dts_solve_opts (include/dts.h)."""
+    _fields_ = [("step", ctypes.c_float), ("support_mode", ctypes.c_int32), ("check_inputs", ctypes.c_int32),
+                ("resid_inf_out", ctypes.c_void_p)]
 
 
 class KernelStat(ctypes.Structure):
@@ -96,6 +98,10 @@ def load_library():
     lib.dts_solve_stereo.restype = ctypes.c_int
     lib.dts_sr_prepare.argtypes = [vp, i64, i64, i32, vp, vp, vp]
     lib.dts_sr_prepare.restype = ctypes.c_int
+    lib.dts_set_option.argtypes = [ctypes.c_char_p, i32]
+    lib.dts_set_option.restype = ctypes.c_int
+    lib.dts_get_option.argtypes = [ctypes.c_char_p]
+    lib.dts_get_option.restype = ctypes.c_int32
     lib.dts_destroy.argtypes = [vp]
     lib.dts_destroy.restype = None
     lib.dts_status_string.argtypes = [ctypes.c_int]
@@ -207,14 +213,44 @@ def dts_debug_read_windows(ctx: int, pass_index: int, axis: int, H: int, W: int)
 
 
 def dts_solve_ex(ctx: int, target, confidence, lam: float, iterations: int, out, stream=None,
-                 step: float = 0.0, support_mode: int = 0, check_inputs: bool = False):
+                 step: float = 0.0, support_mode: int = 0, check_inputs: bool = False, resid_inf_out=None):
+    """dts_solve with options; resid_inf_out: None or `iterations` float32 (device tensor or host
+    array) that receives ||g_k||_inf per iteration (K8)."""
     Ct = 1 if len(target.shape) == 2 else int(target.shape[2])
-    opts = SolveOpts(step, support_mode, 1 if check_inputs else 0)
+    opts = SolveOpts(step, support_mode, 1 if check_inputs else 0,
+                     _ptr(resid_inf_out, "resid_inf_out") if resid_inf_out is not None else None)
     st = load_library().dts_solve_ex(ctx, _ptr(target, "target"), Ct, _ptr(confidence, "confidence"), lam,
                                      iterations, _ptr(out, "out"), _stream(stream, target, confidence, out),
                                      ctypes.byref(opts))
     _check(st, "dts_solve_ex")
     return out
+
+
+def dts_set_option(name: str, value: int) -> None:
+    """Process-wide test / experiment option (include/dts.h); the defaults are the product path."""
+    _check(load_library().dts_set_option(name.encode(), int(value)), f"dts_set_option({name}={value})")
+
+
+def dts_get_option(name: str) -> int:
+    return int(load_library().dts_get_option(name.encode()))
+
+
+class options:
+    """``with options(persistent=0): ...`` sets library options and restores them on exit."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            self.old[k] = dts_get_option(k)
+            dts_set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            dts_set_option(k, v)
 
 
 def dts_solve(ctx: int, target, confidence, lam: float, iterations: int, out, stream=None):

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -65,6 +66,22 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 }
 
 std::once_flag g_pool_once;
+
+// Process-wide test / experiment options (dts_set_option; include/dts.h).  The defaults are
+// the product path; no environment variable changes what the library computes.
+struct Options {
+    std::atomic<int> col_kernel{0};   // 0: cluster kernel when the column fits, 1: decoupled kernel (k_col.cu)
+    std::atomic<int> band_scheme{0};  // 0: edge fix-up when bands are tall enough, 1: TUPLE/APPLY, 2: decoupled
+    std::atomic<int> graphs{1};       // replay repeated identical solves as CUDA graphs
+    std::atomic<int> persistent{0};   // one persistent kernel per solve for L2-resident C_t = 1 images
+    std::atomic<int> row_update{1};   // Eq. (3) step fused into the next iteration's first row pass
+    std::atomic<int> col_rows{0};     // column kernel rows per warp segment: 0 auto, 32 or 40 (C_t = 1)
+    std::atomic<int> col_cluster{0};  // column kernel cluster size: 0 auto, else forced (experiments)
+};
+Options& opts_g() {
+    static Options o;
+    return o;
+}
 
 }  // namespace
 
@@ -129,11 +146,20 @@ struct dts_ctx {
     std::vector<uintptr_t> graph_seen;  // key of the last eager solve: a repeat is captured
     int64_t graph_launches = 0;
     cudaStream_t cap_stream = nullptr;
-    // streaming column kernel (kind 2) scratch: its own tuples/carries and counters/flags
-    float* v_tuples = nullptr;
-    unsigned int* v_flags = nullptr;
-    size_t v_tuple_cap = 0, v_flag_cap = 0;
-    unsigned int v_epoch = 0;
+    // persistent L2-resident solve (k_persist.cu): segment maps, epoch flags, grid barrier
+    float* p_maps = nullptr;
+    unsigned int* p_flags = nullptr;  // zero-initialised; compared against epochs >= 1
+    unsigned long long* p_bar = nullptr;  // grid-barrier arrival counter (zero-initialised, monotonic)
+    unsigned long long p_bar_count = 0;   // its value after the last enqueued launch
+    size_t p_cap = 0;                 // segments the maps / flags hold
+    unsigned int p_epoch = 1;
+    // per-iteration ||g||_inf (dts_solve_opts.resid_inf_out), as float bits
+    unsigned int* resid = nullptr;
+    int resid_cap = 0;
+    // row-band mode: scheme decided once at create, identically on every rank (from the
+    // all-gathered band heights and carry-decay lengths)
+    int64_t band_H_max = 0;
+    int band_scheme = 0;  // 0 edge fix-up where the bands allow it, 1 cluster TUPLE/APPLY, 2 decoupled
     cudaStream_t last_stream = nullptr;
     int64_t launches = 0;
 };
@@ -143,12 +169,12 @@ namespace {
 enum Family {
     F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
     F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_FILL, F_BOX_PREP, F_BOX_ROW, F_BOX_COL, F_COEF,
-    F_COUNT
+    F_PERSIST, F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
                                      "rank_compose", "row_update", "confidence", "stereo_update", "link_fill",
-                                     "box_windows", "box_row", "box_col", "edge_profiles"};
+                                     "box_windows", "box_row", "box_col", "edge_profiles", "solve_persist"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -257,10 +283,9 @@ dts_status ensure_staging(dts_ctx* ctx, size_t bytes_per_image, cudaStream_t s) 
 
 // column-pass plan: cluster fast path when it fits, else the decoupled band-tuple kernel
 cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan) {
-    if (!std::getenv("DTS_NO_CLUSTER")) {
+    if (opts_g().col_kernel.load() == 0) {
         // C_t >= 2 FILTER: 16-row segments (20 warps per CTA) when the column fits a cluster
-        if (Ct >= 2 && mode == MODE_FILTER && !std::getenv("DTS_COL_LS32") &&
-            plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 16) == cudaSuccess)
+        if (Ct >= 2 && mode == MODE_FILTER && plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 16) == cudaSuccess)
             return cudaSuccess;
         cudaGetLastError();
         if (plan_col_cluster(g, Ct, mode, num_sms, plan) == cudaSuccess) {
@@ -269,8 +294,8 @@ cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* 
             // and keep 32-row segments (C1: 12.6 us against 16.8 with 40-row ones).
             const int clusters = (int)(plan->grid.x / plan->CB);
             const int rounds = (plan->ntiles + clusters - 1) / clusters;
-            const char* f40 = std::getenv("DTS_COL_LS40");  // 0 / 1: force off / on
-            const bool want40 = f40 ? f40[0] == '1' : rounds >= 4;
+            const int rows = opts_g().col_rows.load();
+            const bool want40 = rows ? rows == 40 : rounds >= 4;
             ColPlan p40{};
             if (Ct == 1 && mode == MODE_FILTER && want40 &&
                 plan_col_cluster_ls(g, Ct, mode, num_sms, &p40, 40) == cudaSuccess)
@@ -285,26 +310,6 @@ cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* 
 
 dts_status ensure_col_scratch(dts_ctx* ctx, const ColPlan& cp, cudaStream_t s) {
     cudaError_t e;
-    if (cp.kind == 2 || cp.kind == 3) {
-        if (cp.tuple_floats > ctx->v_tuple_cap) {
-            if (ctx->v_tuples) cudaFreeAsync(ctx->v_tuples, s);
-            ctx->v_tuples = nullptr;
-            if ((e = cudaMallocAsync((void**)&ctx->v_tuples, cp.tuple_floats * sizeof(float), s)) != cudaSuccess)
-                return cuda_fail(e);
-            ctx->v_tuple_cap = cp.tuple_floats;
-        }
-        if (cp.flag_count > ctx->v_flag_cap) {
-            if (ctx->v_flags) cudaFreeAsync(ctx->v_flags, s);
-            ctx->v_flags = nullptr;
-            if ((e = cudaMallocAsync((void**)&ctx->v_flags, cp.flag_count * sizeof(unsigned int), s)) !=
-                    cudaSuccess ||
-                (e = cudaMemsetAsync(ctx->v_flags, 0, cp.flag_count * sizeof(unsigned int), s)) != cudaSuccess)
-                return cuda_fail(e);
-            ctx->v_flag_cap = cp.flag_count;
-            ctx->v_epoch = 0;
-        }
-        return DTS_OK;
-    }
     if (cp.kind != 0) return DTS_OK;
     if (cp.tuple_floats > ctx->tuple_cap) {
         if (ctx->tuples) cudaFreeAsync(ctx->tuples, s);
@@ -330,16 +335,6 @@ ColScratch next_scratch(dts_ctx* ctx);
 cudaError_t col_launch(dts_ctx* ctx, const ColPlan& plan, int Ct, int mode, float* x, const float* d, float kc,
                        const UpdateArgs* upd, float* support, cudaStream_t s) {
     if (plan.kind == 1) return launch_col_cluster(plan, ctx->g, Ct, mode, x, d, kc, upd, support, s);
-    if (plan.kind == 2 || plan.kind == 3) {
-        ColScratch sc = {};
-        sc.phase = PHASE_FULL;
-        sc.tuples = ctx->v_tuples;
-        sc.flags = ctx->v_flags;
-        sc.epoch = ++ctx->v_epoch;
-        if (sc.epoch == 0) sc.epoch = ++ctx->v_epoch;
-        if (plan.kind == 3) return launch_col_2p(plan, ctx->g, Ct, x, d, kc, sc, s);
-        return launch_col_stream(plan, ctx->g, Ct, mode, x, d, kc, upd, sc, s);
-    }
     return launch_col_pass(plan, ctx->g, Ct, mode, x, d, kc, upd, support, next_scratch(ctx), s);
 }
 
@@ -370,23 +365,26 @@ dts_status ensure_band_buffers(dts_ctx* ctx, cudaStream_t s) {
     return DTS_OK;
 }
 
-// One column pass of a row-band context: every rank emits the
-// aggregate 5-tuple of its rows per column (TUPLE), the tuples are all-gathered (NVLink
-// via NCCL, or the loopback transport), each rank composes the carries into its rows,
-// and the pass is finished with those carries (APPLY).
+// One column pass of a row-band context.  Which scheme runs is
+// decided from state every rank shares (the band scheme latched at create from the
+// all-gathered band heights and decay lengths, and plans for the TALLEST band), so every
+// rank issues the same collective with the same count:
+//  - edge fix-up (pass with profiles): zero-carry cluster pass, one all-gather of the edge
+//    records, elementwise corrections on L rows at each edge;
+//  - cluster TUPLE -> all-gather -> compose -> cluster FILTER with the external carries;
+//  - the same on the decoupled kernel (k_col.cu) when the band's columns do not fit a cluster.
 dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, const UpdateArgs* upd,
                            float* support, int fam, double bytes, cudaStream_t s, int pass) {
     const Geometry& g = ctx->g;
-    // edge fix-up scheme (bands of >= 2L rows, profiles built at create): the zero-carry
-    // pass exports y at row H - 1 and z at row 0, one all-gather of those per-column values,
-    // then the corrections on the L rows at each edge
-    ColPlan pE;
-    const bool exporting = std::getenv("DTS_BAND_EXPORT") != nullptr;
-    if (mode != MODE_SUPPORT && pass >= 0 && pass < (int)ctx->edge_gam.size() && ctx->edge_gam[pass] &&
-        !std::getenv("DTS_BAND_TUPLE") &&
-        (exporting ? plan_col_cluster(g, Ct, MODE_FILTER, ctx->num_sms, &pE)
-                   : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &pE)) == cudaSuccess &&
-        pE.kind == 1) {
+    Geometry gmax = g;  // every rank plans for the tallest band: the same decision everywhere
+    gmax.H = ctx->band_H_max;
+    gmax.plane = gmax.H * gmax.pitch;
+    ColPlan pE, pT, pF;
+    const bool edge_ok = ctx->band_scheme == 0 && mode != MODE_SUPPORT && pass >= 0 &&
+                         pass < (int)ctx->edge_gam.size() && ctx->edge_gam[pass] &&
+                         plan_col(gmax, Ct, MODE_FILTER, ctx->num_sms, &pE) == cudaSuccess && pE.kind == 1;
+    cudaGetLastError();
+    if (edge_ok && plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &pE) == cudaSuccess && pE.kind == 1) {
         dts_status st;
         cudaError_t e;
         if ((st = ensure_band_buffers(ctx, s)) != DTS_OK) return st;
@@ -395,28 +393,23 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
         const size_t count = (size_t)pE.ntiles * NT * 32;
         const double px = (double)g.H * g.W;
         const bool pre = ctx->A1y && pass < 4;  // pass-1 coefficient squared per pass
-        // default: the single-context kernel (the link below the band cut: a_H taken as 0),
-        // whose output rows H - 1 and 0 are the exchanged y0(H - 1) and z0(0); the fix-up
-        // then carries z_H - y(H - 1) (reading R26).  DTS_BAND_EXPORT=1: the band kernel with
-        // the link, exporting those values itself (the bottom carry is z_H).
+        // the single-context kernel with the link below the band cut (a_H taken as 0): its
+        // output rows H - 1 and 0 are the exchanged y0(H - 1) and z0(0); the fix-up then
+        // carries z_H - y(H - 1) (reading R26)
         st = run_launch(ctx, F_COL, px * (8.0 * Ct + 4), s, [&] {
             return launch_col_cluster(pE, g, Ct, MODE_FILTER, x, pre ? ctx->A1y : ctx->dy, kc, nullptr, nullptr, s,
-                                      pre ? pass : -1, nullptr, nullptr,
-                                      exporting ? ctx->rank_tup : nullptr);  // zero carries
+                                      pre ? pass : -1);  // zero carries
         });
         if (st != DTS_OK) return st;
-        if (!exporting) {  // y0 at row H - 1 -> slots [0, Ct), z0 at row 0 -> slots [Ct, 2Ct)
-            for (int v = 0; v < Ct; ++v) {
-                const float* yrow = x + v * g.plane + (g.H - 1) * g.pitch;
-                const float* zrow = x + v * g.plane;
-                if ((e = cudaMemcpy2DAsync(ctx->rank_tup + v * 32, NT * 32 * sizeof(float), yrow, 32 * sizeof(float),
-                                           32 * sizeof(float), pE.ntiles, cudaMemcpyDeviceToDevice, s)) !=
-                        cudaSuccess ||
-                    (e = cudaMemcpy2DAsync(ctx->rank_tup + (Ct + v) * 32, NT * 32 * sizeof(float), zrow,
-                                           32 * sizeof(float), 32 * sizeof(float), pE.ntiles,
-                                           cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
-                    return cuda_fail(e);
-            }
+        for (int v = 0; v < Ct; ++v) {  // y0 at row H - 1 -> slots [0, Ct), z0 at row 0 -> slots [Ct, 2Ct)
+            const float* yrow = x + v * g.plane + (g.H - 1) * g.pitch;
+            const float* zrow = x + v * g.plane;
+            if ((e = cudaMemcpy2DAsync(ctx->rank_tup + v * 32, NT * 32 * sizeof(float), yrow, 32 * sizeof(float),
+                                       32 * sizeof(float), pE.ntiles, cudaMemcpyDeviceToDevice, s)) != cudaSuccess ||
+                (e = cudaMemcpy2DAsync(ctx->rank_tup + (Ct + v) * 32, NT * 32 * sizeof(float), zrow,
+                                       32 * sizeof(float), 32 * sizeof(float), pE.ntiles, cudaMemcpyDeviceToDevice,
+                                       s)) != cudaSuccess)
+                return cuda_fail(e);
         }
         // Gamma_0 of this rank into slot 2Ct of its records
         if ((e = cudaMemcpy2DAsync(ctx->rank_tup + 2 * Ct * 32, NT * 32 * sizeof(float), ctx->edge_gam[pass],
@@ -435,20 +428,21 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
         if (ctx->comm->nranks > 1)  // a single rank has no edges to correct
             st = run_launch(ctx, F_COMPOSE, (double)2 * L * g.W * (8.0 * Ct + 4), s, [&] {
                 return launch_edge_fix(x, Ct, g, L, ctx->edge_gam[pass], ctx->edge_theta[pass], ctx->gathered,
-                                       ctx->comm->nranks, ctx->comm->rank, s, true, !exporting);
+                                       ctx->comm->nranks, ctx->comm->rank, s, true, true);
             });
         if (st != DTS_OK || mode != MODE_UPDATE) return st;
         return run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
             return launch_update(x, upd->Z, upd->T, upd->chat, Ct, g, upd->lam, upd->step, upd->out_hwc, ctx->num_sms,
-                                 s);
+                                 s, upd->resid);
         });
     }
     cudaGetLastError();
-    // cluster kernels when the band's columns fit a cluster: TUPLE (the rank 5-tuple, with the
-    // carry sensitivity as an extra channel) -> all-gather -> compose -> FILTER with the
-    // external carries (+ the streaming update kernel for the last pass of an iteration)
-    ColPlan pT, pF;
-    if (mode != MODE_SUPPORT && !std::getenv("DTS_BAND_LEGACY") &&
+    // cluster kernels when the (tallest) band's columns fit a cluster: TUPLE (the rank 5-tuple,
+    // with the carry sensitivity as an extra channel) -> all-gather -> compose -> FILTER with
+    // the external carries (+ the streaming update kernel for the last pass of an iteration)
+    if (mode != MODE_SUPPORT && ctx->band_scheme != 2 &&
+        plan_col_cluster(gmax, Ct, MODE_TUPLE, ctx->num_sms, &pT) == cudaSuccess &&
+        plan_col_cluster(gmax, Ct, MODE_FILTER, ctx->num_sms, &pF) == cudaSuccess &&
         plan_col_cluster(g, Ct, MODE_TUPLE, ctx->num_sms, &pT) == cudaSuccess &&
         plan_col_cluster(g, Ct, MODE_FILTER, ctx->num_sms, &pF) == cudaSuccess) {
         dts_status st;
@@ -481,7 +475,7 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
         if (st != DTS_OK || mode != MODE_UPDATE) return st;
         return run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
             return launch_update(x, upd->Z, upd->T, upd->chat, Ct, g, upd->lam, upd->step, upd->out_hwc, ctx->num_sms,
-                                 s);
+                                 s, upd->resid);
         });
     }
     cudaGetLastError();
@@ -577,9 +571,45 @@ bool profiler_on() {
 
 }  // namespace
 
+namespace dts {
+int option_col_cluster() { return opts_g().col_cluster.load(); }
+}  // namespace dts
+
 extern "C" {
 
-const char* dts_version(void) { return "dts-b200 0.1 (sm_100a)"; }
+const char* dts_version(void) { return "dts-b200 0.2 (sm_100a)"; }
+
+dts_status dts_set_option(const char* name, int32_t value) {
+    if (!name) return DTS_E_ARG;
+    Options& o = opts_g();
+    const std::string n(name);
+    if (n == "col_kernel" && (value == 0 || value == 1)) o.col_kernel = value;
+    else if (n == "band_scheme" && value >= 0 && value <= 2) o.band_scheme = value;
+    else if (n == "graphs" && (value == 0 || value == 1)) o.graphs = value;
+    else if (n == "persistent" && (value == 0 || value == 1)) o.persistent = value;
+    else if (n == "row_update" && (value == 0 || value == 1)) o.row_update = value;
+    else if (n == "col_rows" && (value == 0 || value == 32 || value == 40)) o.col_rows = value;
+    else if (n == "col_cluster" && value >= 0 && value <= 16) o.col_cluster = value;
+    else return DTS_E_ARG;
+    return DTS_OK;
+}
+
+// debug hook (not in include/dts.h): phase timestamps of the persistent kernel
+void dts_debug_persist_timers(unsigned long long* device_buf) { dts::set_persist_timers(device_buf); }
+
+int32_t dts_get_option(const char* name) {
+    if (!name) return -1;
+    Options& o = opts_g();
+    const std::string n(name);
+    if (n == "col_kernel") return o.col_kernel;
+    if (n == "band_scheme") return o.band_scheme;
+    if (n == "graphs") return o.graphs;
+    if (n == "persistent") return o.persistent;
+    if (n == "row_update") return o.row_update;
+    if (n == "col_rows") return o.col_rows;
+    if (n == "col_cluster") return o.col_cluster;
+    return -1;
+}
 
 dts_status dts_sr_prepare(const float* low, int64_t h, int64_t w, int32_t factor, float* target_out,
                           float* conf_out, void* stream) {
@@ -641,6 +671,81 @@ const char* dts_status_string(dts_status s) {
 }
 
 const char* dts_last_error_string(void) { return g_last_error.c_str(); }
+
+// Row-band contexts: every rank measures how many rows a carry
+// entering its band edges keeps an influence >= 2^-26 of itself (per pass, and for the
+// support), from its own coefficients; the ranks all-gather (rows, lengths) and every rank
+// takes the same decisions from the same numbers: L_i = the largest length over ranks and
+// edges, the edge fix-up scheme for pass i iff the SHORTEST band holds 2 L_i + 1 rows.
+// Lengths: [0, N) the passes, N the support.  Returns the agreed lengths (0: no edge scheme).
+static dts_status band_agree(dts_ctx* ctx, cudaStream_t s, std::vector<int>* L_agreed) {
+    dts::Comm* comm = ctx->comm;
+    const int N = ctx->N, nl = N + 1, P = comm->nranks;
+    const int rec = 2 + 2 * nl;  // [rows, 0, (top, bottom) x nl] as 32-bit words
+    unsigned* dlen = nullptr;
+    float *send = nullptr, *recv = nullptr;
+    cudaError_t e;
+    dts_status st = DTS_OK;
+    std::vector<unsigned> host(rec, 0u), all((size_t)rec * P, 0u);
+    auto cleanup = [&]() {
+        for (void* q : {(void*)dlen, (void*)send, (void*)recv})
+            if (q) cudaFreeAsync(q, s);
+    };
+    if ((e = cudaMallocAsync((void**)&dlen, 2 * nl * sizeof(unsigned), s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&send, rec * sizeof(float), s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&recv, (size_t)rec * P * sizeof(float), s)) != cudaSuccess ||
+        (e = cudaMemsetAsync(dlen, 0, 2 * nl * sizeof(unsigned), s)) != cudaSuccess) {
+        cleanup();
+        return cuda_fail(e);
+    }
+    for (int i = 0; i < nl && st == DTS_OK; ++i) {
+        const float kc = i < N ? ctx->kc[i] : ctx->ks;  // coefficient 2^(-kc d), d >= 1
+        const int64_t worst = (int64_t)std::ceil(26.0 / (double)kc);
+        const int Lcap = (int)std::min<int64_t>(std::min<int64_t>(worst, ctx->g.H), 1 << 20);
+        st = run_launch(ctx, F_COEF, (double)ctx->g.W * Lcap * 8.0, s,
+                        [&] { return launch_edge_length(ctx->dy, ctx->g, Lcap, kc, dlen + 2 * i, s); });
+    }
+    if (st == DTS_OK &&
+        ((e = cudaMemcpyAsync(host.data() + 2, dlen, 2 * nl * sizeof(unsigned), cudaMemcpyDeviceToHost, s)) !=
+             cudaSuccess ||
+         (e = cudaStreamSynchronize(s)) != cudaSuccess))
+        st = cuda_fail(e);
+    host[0] = (unsigned)ctx->g.H;
+    if (st == DTS_OK && (e = cudaMemcpyAsync(send, host.data(), rec * sizeof(unsigned), cudaMemcpyHostToDevice, s)) !=
+                            cudaSuccess)
+        st = cuda_fail(e);
+    std::string err;
+    if (st == DTS_OK) {  // the words travel as opaque 32-bit values
+        st = run_launch(ctx, F_EXCHANGE, (double)rec * 4 * P, s, [&] {
+            return comm_allgather(comm, send, recv, (size_t)rec, s, &err) ? cudaSuccess : cudaErrorUnknown;
+        });
+        if (st != DTS_OK && !err.empty()) {
+            g_last_error = err;
+            st = DTS_E_NCCL;
+        }
+    }
+    if (st == DTS_OK &&
+        ((e = cudaMemcpyAsync(all.data(), recv, (size_t)rec * P * sizeof(unsigned), cudaMemcpyDeviceToHost, s)) !=
+             cudaSuccess ||
+         (e = cudaStreamSynchronize(s)) != cudaSuccess))
+        st = cuda_fail(e);
+    cleanup();
+    if (st != DTS_OK) return st;
+    int64_t hmin = INT64_MAX, hmax = 0;
+    for (int r = 0; r < P; ++r) {
+        hmin = std::min<int64_t>(hmin, all[(size_t)r * rec]);
+        hmax = std::max<int64_t>(hmax, all[(size_t)r * rec]);
+    }
+    ctx->band_H_max = hmax;
+    L_agreed->assign(nl, 0);
+    for (int i = 0; i < nl; ++i) {
+        int64_t L = 1;
+        for (int r = 0; r < P; ++r)
+            for (int edge = 0; edge < 2; ++edge) L = std::max<int64_t>(L, all[(size_t)r * rec + 2 + 2 * i + edge]);
+        (*L_agreed)[i] = (ctx->band_scheme == 0 && 2 * L + 1 <= hmin && L <= (1 << 20)) ? (int)L : 0;
+    }
+    return DTS_OK;
+}
 
 static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0, int64_t H, int64_t W, int32_t C,
                               float sigma_s, float sigma_r, int32_t filter_passes, dts::Comm* comm, void* stream,
@@ -776,16 +881,23 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
             return launch_row_pass(rp, ctx->g, 1, MODE_SUPPORT, nullptr, ctx->S, ctx->dx, ctx->ks, s);
         });
     if (st == DTS_OK) st = ensure_col_scratch(ctx, cp, s);
+    std::vector<int> band_L;  // agreed edge lengths (row-band contexts): passes, then the support
+    if (st == DTS_OK && comm) {
+        ctx->band_scheme = opts_g().band_scheme.load();  // latched: the same on every rank of a job
+        st = band_agree(ctx, s, &band_L);
+    }
     if (st == DTS_OK) {
         if (comm) {
             // edge scheme for the support: s = P + Q - 1 with independent
             // causal P and anticausal Q; the zero-carry cluster pass gives s0 with P0(0) = 1 and
             // Q0(H-1) = 1, so s0(H-1) is the P carry for the rank below and s0(0) the Q carry for
             // the rank above; then s += c G_k (top rows) + e Theta_k (bottom rows)
-            const double as = std::exp(-sqrt2 / (double)sigma_s);
-            const int64_t Ls = as > 0.0 ? (int64_t)std::ceil(std::log(std::ldexp(1.0, -26)) / std::log(as)) : 1;
+            const int64_t Ls = band_L[filter_passes];
+            Geometry gmax = ctx->g;  // decided for the tallest band: the same on every rank
+            gmax.H = ctx->band_H_max;
+            gmax.plane = gmax.H * gmax.pitch;
             ColPlan cps;
-            bool edge = Ls >= 1 && 2 * Ls + 1 <= H && Ls <= (1 << 20) && !std::getenv("DTS_BAND_TUPLE") &&
+            bool edge = Ls >= 1 && plan_col_cluster(gmax, 1, MODE_SUPPORT, ctx->num_sms, &cps) == cudaSuccess &&
                         plan_col_cluster(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &cps) == cudaSuccess;
             cudaGetLastError();
             if (edge) {
@@ -849,17 +961,15 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
             });
         }
     }
-    // row-band contexts: edge profiles of every pass whose edge distance L (carry influence
-    // < 2^-26 after L rows, d >= 1 so a <= a_i = e^{-sqrt2/sigma_i}) fits twice in the band
+    // row-band contexts: edge profiles of every pass whose agreed edge length L (carry
+    // influence < 2^-26 after L rows, measured on every rank) fits twice in the shortest band
     if (st == DTS_OK && comm) {
         ctx->edge_gam.assign(filter_passes, nullptr);
         ctx->edge_theta.assign(filter_passes, nullptr);
         ctx->edge_L.assign(filter_passes, 0);
         for (int i = 1; i <= filter_passes && st == DTS_OK; ++i) {
-            const double sig = sigma_s * std::sqrt(3.0) * std::pow(2.0, filter_passes - i) / denom;
-            const double ai = std::exp(-sqrt2 / sig);
-            const int64_t L = ai > 0.0 ? (int64_t)std::ceil(std::log(std::ldexp(1.0, -26)) / std::log(ai)) : 1;
-            if (L < 1 || 2 * L + 1 > H || L > (1 << 20)) continue;
+            const int64_t L = band_L[i - 1];
+            if (L < 1) continue;
             float *gam = nullptr, *th = nullptr;
             const size_t b = (size_t)L * ctx->g.pitch * sizeof(float);
             if ((e = cudaMallocAsync((void**)&gam, b, s)) != cudaSuccess ||
@@ -1081,6 +1191,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     if (iterations < 0) return DTS_E_ARG;
     const float step = (opts && opts->step > 0.f) ? opts->step : 0.99f;
     const int support_mode = opts ? opts->support_mode : 0;
+    float* resid_out = opts ? opts->resid_inf_out : nullptr;
     if (support_mode != 0 && support_mode != 1) return DTS_E_ARG;
     if (!std::isfinite(lambda) || lambda < 0.f || !std::isfinite(step)) return DTS_E_ARG;
     if (step * (lambda + 1.f) >= 2.f) return DTS_E_ARG;  // descent stability
@@ -1088,38 +1199,35 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     const size_t img = (size_t)g.H * g.W * Ct * sizeof(float);
     const size_t cb = (size_t)g.H * g.W * sizeof(float);
     if (overlaps(out, img, target, img) || overlaps(out, img, confidence, cb)) return DTS_E_ARG;
+    if (resid_out && (overlaps(resid_out, (size_t)iterations * 4, out, img) ||
+                      overlaps(resid_out, (size_t)iterations * 4, target, img)))
+        return DTS_E_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->last_stream = s;
 
     const bool is_box = ctx->filter == DTS_FILTER_BOX;
+    const bool want_resid = resid_out && iterations > 0;
     RowPlan rp{};
     ColPlan cpf{}, cpu{};
-    if (!is_box && plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess) return DTS_E_SHAPE;
-    // column kernel: the cluster kernel (k_colc.cu) by default; DTS_COL=stream selects the
-    // TMEM-lagged decoupled kernel (k_colv.cu, experimental), DTS_COL=legacy forces the
-    // cluster / band-tuple kernels with the separate update kernel
-    const char* colsel = is_box ? nullptr : std::getenv("DTS_COL");
-    // streaming path: TMEM-lagged column kernel (FILTER) + the Eq. (3) step fused into the
-    // next iteration's first row pass (and one closing update kernel)
-    const bool stream_ok = !ctx->comm && colsel && std::strcmp(colsel, "stream") == 0 &&
-                           plan_col_stream(g, Ct, MODE_FILTER, ctx->num_sms, &cpf) == cudaSuccess;
-    if (stream_ok) cpu = cpf;
-    const bool twop_ok = !stream_ok && !ctx->comm && colsel && std::strcmp(colsel, "2p") == 0 &&
-                         plan_col_2p(g, Ct, MODE_FILTER, ctx->num_sms, &cpf) == cudaSuccess;
-    if (twop_ok) cpu = cpf;  // FILTER column passes + the streaming update kernel (K4b)
-    if (!is_box && !stream_ok && !twop_ok) {
-        cudaGetLastError();
+    if (!is_box) {
+        if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess) return DTS_E_SHAPE;
         if ((ctx->comm ? plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)
-                       : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess ||
-            (ctx->comm ? plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu)
-                       : plan_col(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu)) != cudaSuccess)
+                       : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess)
             return DTS_E_SHAPE;
+        // the decoupled kernel (tall columns) applies Eq. (3) in its own write-out
+        if (cpf.kind != 1 && plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu) != cudaSuccess) return DTS_E_SHAPE;
+        cudaGetLastError();
     }
+    // one persistent kernel for L2-resident C_t = 1 images (k_persist.cu)
+    PersistPlan pp{};
+    const bool persist = !is_box && !ctx->comm && ctx->A1y && iterations > 0 && opts_g().persistent.load() &&
+                         plan_persist(g, Ct, ctx->N, ctx->num_sms, &pp) == cudaSuccess;
+    cudaGetLastError();
 
     const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),
-                  ko = classify(out, ctx->device);
-    if (kt == PTR_BAD || kc == PTR_BAD || ko == PTR_BAD) return DTS_E_ARG;
-    const bool any_host = kt == PTR_HOST || kc == PTR_HOST || ko == PTR_HOST;
+                  ko = classify(out, ctx->device), kr = want_resid ? classify(resid_out, ctx->device) : PTR_DEVICE;
+    if (kt == PTR_BAD || kc == PTR_BAD || ko == PTR_BAD || kr == PTR_BAD) return DTS_E_ARG;
+    const bool any_host = kt == PTR_HOST || kc == PTR_HOST || ko == PTR_HOST || kr == PTR_HOST;
     cudaError_t e;
     dts_status st;
     if (any_host && (st = ensure_staging(ctx, img, s)) != DTS_OK) return st;
@@ -1149,6 +1257,20 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         if (h[0]) return DTS_E_NONFINITE;
         if (h[1]) return DTS_E_RANGE;
     }
+    // K8: per-iteration ||g||_inf, folded in by the update kernels (atomicMax of float bits)
+    if (want_resid) {
+        if (ctx->resid_cap < iterations) {
+            if (ctx->resid) cudaFreeAsync(ctx->resid, s);
+            ctx->resid = nullptr;
+            ctx->resid_cap = 0;
+            if ((e = cudaMallocAsync((void**)&ctx->resid, (size_t)iterations * sizeof(unsigned), s)) != cudaSuccess)
+                return cuda_fail(e);
+            ctx->resid_cap = iterations;
+        }
+        if ((e = cudaMemsetAsync(ctx->resid, 0, (size_t)iterations * sizeof(unsigned), s)) != cudaSuccess)
+            return cuda_fail(e);
+    }
+    unsigned* resid = want_resid ? ctx->resid : nullptr;
 
     if (iterations == 0) {
         if ((e = cudaMemcpyAsync(o_d, t_d, img, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return cuda_fail(e);
@@ -1156,6 +1278,34 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         if ((st = ensure_solver_state(ctx, Ct, s)) != DTS_OK) return st;
         if ((st = ensure_col_scratch(ctx, cpf, s)) != DTS_OK) return st;
         if ((st = ensure_col_scratch(ctx, cpu, s)) != DTS_OK) return st;
+        if (persist) {
+            const size_t nseg = (size_t)pp.ntiles * pp.nseg;
+            if (ctx->p_cap < nseg) {
+                for (void* q : {(void*)ctx->p_maps, (void*)ctx->p_flags})
+                    if (q) cudaFreeAsync(q, s);
+                ctx->p_maps = nullptr;
+                ctx->p_flags = nullptr;
+                ctx->p_cap = 0;
+                if ((e = cudaMallocAsync((void**)&ctx->p_maps, nseg * 128 * sizeof(float), s)) != cudaSuccess ||
+                    (e = cudaMallocAsync((void**)&ctx->p_flags, nseg * 2 * sizeof(unsigned), s)) != cudaSuccess ||
+                    (e = cudaMemsetAsync(ctx->p_flags, 0, nseg * 2 * sizeof(unsigned), s)) != cudaSuccess)
+                    return cuda_fail(e);
+                ctx->p_cap = nseg;
+                ctx->p_epoch = 1;
+            }
+            if (!ctx->p_bar) {
+                if ((e = cudaMallocAsync((void**)&ctx->p_bar, sizeof(unsigned long long), s)) != cudaSuccess ||
+                    (e = cudaMemsetAsync(ctx->p_bar, 0, sizeof(unsigned long long), s)) != cudaSuccess)
+                    return cuda_fail(e);
+                ctx->p_bar_count = 0;
+            }
+            const uint64_t need = 2ull * ctx->N * (uint64_t)iterations + 2;
+            if ((uint64_t)ctx->p_epoch + need >= 0xF0000000ull) {  // epochs wrap: start the flags afresh
+                if ((e = cudaMemsetAsync(ctx->p_flags, 0, ctx->p_cap * 2 * sizeof(unsigned), s)) != cudaSuccess)
+                    return cuda_fail(e);
+                ctx->p_epoch = 1;
+            }
+        }
         auto enqueue = [&](cudaStream_t s) -> dts_status {
             dts_status st;
             const double px = (double)g.H * g.W;
@@ -1163,24 +1313,22 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                 return launch_prologue(t_d, c_d, Ct, g, ctx->S, ctx->Sy, support_mode, ctx->Z, ctx->T, ctx->chat, s);
             });
             if (st != DTS_OK) return st;
+            if (persist) {  // the whole iteration loop in one cooperative launch
+                const unsigned ep = ctx->p_epoch;
+                const unsigned long long base = ctx->p_bar_count;
+                st = run_launch(ctx, F_PERSIST, px * iterations * (2.0 * ctx->N + 1) * 12.0, s, [&] {
+                    return launch_persist(pp, g, ctx->N, iterations, ctx->kc.data(), lambda, step, ctx->X, ctx->Z,
+                                          ctx->T, ctx->chat, ctx->dx, ctx->A1y, o_d, resid, ctx->p_maps, ctx->p_flags,
+                                          ctx->p_bar, base, ep, s);
+                });
+                if (st == DTS_OK) {
+                    ctx->p_epoch += 2u * (unsigned)ctx->N * (unsigned)iterations + 2u;
+                    ctx->p_bar_count += persist_barriers(pp, ctx->N, iterations);
+                }
+                return st;
+            }
             const double row_bytes = px * (8.0 * Ct + 4);
             const double upd_bytes = px * (16.0 * Ct + 8);  // X, d, Z, T, chat in; Z out
-            // FILTER column pass i: the cluster kernel on A1 = a_1^{d_y} squared i times when
-            // the context holds it, else on d_y
-            auto col_filter = [&](int i) -> cudaError_t {
-                if (cpf.kind == 1 && ctx->A1y && i < 4)
-                    return launch_col_cluster(cpf, g, Ct, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr, nullptr,
-                                              s, i);
-                return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
-            };
-            // last column pass of an iteration: FILTER + streaming update kernel (default), or
-            // the column kernel's UPDATE mode (Eq. (3) in its write-out; DTS_FUSED_UPDATE=1).
-            // Split wins everywhere measured: C4 0.331 + 0.302 ms against 0.91 fused; small
-            // Ct = 1 images under graph replay 0.750 against 0.882 ms per solve (640x480,
-            // tools/graph_time.py).  Only the per-launch-profiled bench favours fused there
-            // (one launch fewer per iteration).
-            const char* fu = std::getenv("DTS_FUSED_UPDATE");
-            const bool split_update = cpu.kind == 3 || (cpu.kind == 1 && !(fu && fu[0] == '1'));
             if (is_box) {  // R25: N x (box rows, box columns), ping-pong X2 <-> X, then Eq. (3)
                 for (int k = 0; k < iterations; ++k) {
                     for (int i = 0; i < ctx->N; ++i) {
@@ -1198,52 +1346,27 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                     float* ohwc = (k + 1 == iterations) ? o_d : nullptr;
                     st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
                         return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, ohwc,
-                                             ctx->num_sms, s);
+                                             ctx->num_sms, s, resid ? resid + k : nullptr);
                     });
                     if (st != DTS_OK) return st;
                 }
                 return DTS_OK;
             }
-            if (stream_ok) {
-                UpdateArgs u;
-                u.Z = ctx->Z;
-                u.T = ctx->T;
-                u.chat = ctx->chat;
-                u.lam = lambda;
-                u.step = step;
-                u.out_hwc = nullptr;
-                for (int k = 0; k < iterations; ++k) {
-                    for (int i = 0; i < ctx->N; ++i) {
-                        if (i == 0 && k > 0) {  // Eq. (3) step of iteration k-1 fused into this row pass
-                            st = run_launch(ctx, F_ROWUPD, px * (20.0 * Ct + 8), s, [&] {
-                                return launch_row_update(rp, g, Ct, ctx->X, ctx->X, ctx->dx, ctx->kc[i], u, s);
-                            });
-                        } else {
-                            const float* in = (i == 0) ? ctx->Z : ctx->X;
-                            st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
-                                return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
-                            });
-                        }
-                        if (st != DTS_OK) return st;
-                        st = run_launch(ctx, F_COL, row_bytes, s, [&] {
-                            return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
-                        });
-                        if (st != DTS_OK) return st;
-                    }
-                }
-                st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
-                    return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, o_d, ctx->num_sms, s);
-                });
-                if (st != DTS_OK) return st;
-            }
-            // Eq. (3) of iteration k-1 applied inside iteration k's first row pass (k_row.cu
-            // ROWUPD: Z, T, chat read coalesced while the row lands); one update kernel after
-            // the last iteration.  C4 0.467 ms against 0.189 + 0.302 separately, C1/C3 +8%/+5%
-            // per step.  DTS_ROWUPD=0: a separate update kernel every iteration.
-            const char* ru_env = std::getenv("DTS_ROWUPD");
-            // (row bands too: their row passes are rank-local; the band column pass of the
-            // last filter pass then runs in FILTER mode)
-            const bool rowupd = (split_update || ctx->comm) && !(ru_env && ru_env[0] == '0');
+            // FILTER column pass i: the cluster kernel on A1 = a_1^{d_y} squared i times when
+            // the context holds it, else on d_y
+            auto col_filter = [&](int i) -> cudaError_t {
+                if (cpf.kind == 1 && ctx->A1y && i < 4)
+                    return launch_col_cluster(cpf, g, Ct, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr, nullptr,
+                                              s, i);
+                return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
+            };
+            // The last column pass of an iteration is a FILTER pass; Eq. (3) of iteration k-1 is
+            // applied inside iteration k's first row pass (k_row.cu ROWUPD: Z, T, chat read
+            // coalesced while the row lands) and one update kernel closes the solve.  The
+            // decoupled kernel (tall columns) applies Eq. (3) in its own write-out instead; with
+            // the residual requested the step runs as its own kernel every iteration.
+            const bool split_update = cpf.kind == 1 || ctx->comm || want_resid;
+            const bool rowupd = split_update && !want_resid && opts_g().row_update.load();
             UpdateArgs ru;
             ru.Z = ctx->Z;
             ru.T = ctx->T;
@@ -1251,7 +1374,8 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
             ru.lam = lambda;
             ru.step = step;
             ru.out_hwc = nullptr;
-            for (int k = 0; k < (stream_ok ? 0 : iterations); ++k) {
+            ru.resid = nullptr;
+            for (int k = 0; k < iterations; ++k) {
                 for (int i = 0; i < ctx->N; ++i) {
                     const float* in = (i == 0) ? ctx->Z : ctx->X;
                     if (rowupd && i == 0 && k > 0) {  // Eq. (3) of iteration k-1 in this row pass
@@ -1264,41 +1388,30 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                         });
                     }
                     if (st != DTS_OK) return st;
-                    if (ctx->comm) {  // row-band mode: TUPLE -> all-gather -> compose -> APPLY
-                        if (i + 1 < ctx->N || (rowupd && k + 1 < iterations)) {
+                    const bool last = i + 1 == ctx->N;
+                    float* ohwc = (k + 1 == iterations) ? o_d : nullptr;
+                    if (ctx->comm) {  // row-band mode: the exchange of DESIGN.md section 9
+                        if (!last || (rowupd && k + 1 < iterations)) {
                             st = col_pass_banded(ctx, Ct, MODE_FILTER, ctx->X, ctx->kc[i], nullptr, nullptr, F_COL,
                                                  row_bytes, s, i);
                         } else {
-                            UpdateArgs u;
-                            u.Z = ctx->Z;
-                            u.T = ctx->T;
-                            u.chat = ctx->chat;
-                            u.lam = lambda;
-                            u.step = step;
-                            u.out_hwc = (k + 1 == iterations) ? o_d : nullptr;
+                            UpdateArgs u = ru;
+                            u.out_hwc = ohwc;
+                            u.resid = resid ? resid + k : nullptr;
                             st = col_pass_banded(ctx, Ct, MODE_UPDATE, ctx->X, ctx->kc[i], &u, nullptr, F_UPDATE,
                                                  upd_bytes, s, i);
                         }
-                    } else if (i + 1 < ctx->N) {
-                        st = run_launch(ctx, F_COL, row_bytes, s, [&] { return col_filter(i); });
-                    } else if (split_update) {
-                        // column kernel (FILTER) + streaming update kernel (K4b)
+                    } else if (!last || split_update) {
                         st = run_launch(ctx, F_COL, row_bytes, s, [&] { return col_filter(i); });
                         if (st != DTS_OK) return st;
-                        if (rowupd && k + 1 < iterations) continue;  // the next row pass applies Eq. (3)
-                        float* ohwc = (k + 1 == iterations) ? o_d : nullptr;
+                        if (!last || (rowupd && k + 1 < iterations)) continue;  // the next row pass applies Eq. (3)
                         st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
                             return launch_update(ctx->X, ctx->Z, ctx->T, ctx->chat, Ct, g, lambda, step, ohwc,
-                                                 ctx->num_sms, s);
+                                                 ctx->num_sms, s, resid ? resid + k : nullptr);
                         });
-                    } else {
-                        UpdateArgs u;
-                        u.Z = ctx->Z;
-                        u.T = ctx->T;
-                        u.chat = ctx->chat;
-                        u.lam = lambda;
-                        u.step = step;
-                        u.out_hwc = (k + 1 == iterations) ? o_d : nullptr;
+                    } else {  // decoupled kernel: Eq. (3) in the column write-out
+                        UpdateArgs u = ru;
+                        u.out_hwc = ohwc;
                         st = run_launch(ctx, F_UPDATE, upd_bytes, s, [&] {
                             return col_launch(ctx, cpu, Ct, MODE_UPDATE, ctx->X, ctx->dy, ctx->kc[i], &u, nullptr, s);
                         });
@@ -1306,28 +1419,31 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                     if (st != DTS_OK) return st;
                 }
             }
-
             return DTS_OK;
         };
         // Replay a captured graph of the whole launch sequence when the same solve is issued
         // again (small images are launch-bound).  Only on the cluster column path or the box
         // path (no per-launch epochs), with device buffers and the profiler off.
-        const bool use_graph = !any_host && !profiler_on() && !ctx->comm &&
-                               (is_box || (cpf.kind == 1 && cpu.kind == 1)) && !stream_ok && !twop_ok &&
-                               !std::getenv("DTS_NO_GRAPH");
+        const bool use_graph = opts_g().graphs.load() && !persist && !any_host && !profiler_on() && !ctx->comm &&
+                               (is_box || cpf.kind == 1);
         std::vector<uintptr_t> key;
         if (use_graph) {
             uint32_t lb, sb;
             std::memcpy(&lb, &lambda, 4);
             std::memcpy(&sb, &step, 4);
             key = {1, (uintptr_t)t_d, (uintptr_t)c_d, (uintptr_t)o_d, (uintptr_t)Ct, (uintptr_t)iterations, lb, sb,
-                   (uintptr_t)support_mode, (uintptr_t)ctx->X, (uintptr_t)ctx->Z, (uintptr_t)ctx->chat};
+                   (uintptr_t)support_mode, (uintptr_t)ctx->X, (uintptr_t)ctx->Z, (uintptr_t)ctx->chat,
+                   (uintptr_t)resid};
         }
         if ((st = run_cached(ctx, use_graph, key, s, enqueue)) != DTS_OK) return st;
     }
     if (ko == PTR_HOST) {
         if ((e = cudaMemcpyAsync(out, o_d, img, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return cuda_fail(e);
     }
+    if (want_resid &&
+        (e = cudaMemcpyAsync(resid_out, ctx->resid, (size_t)iterations * sizeof(float), cudaMemcpyDefault, s)) !=
+            cudaSuccess)
+        return cuda_fail(e);
     if (any_host) {
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e);
     }
@@ -1511,7 +1627,7 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
             return st;
         };
         if (st == DTS_OK) {
-            const bool use_graph = !any_host && !profiler_on() && cp.kind == 1 && !std::getenv("DTS_NO_GRAPH");
+            const bool use_graph = opts_g().graphs.load() && !any_host && !profiler_on() && cp.kind == 1;
             std::vector<uintptr_t> key;
             if (use_graph) {
                 uint32_t lb, gb2, eb;
@@ -1550,8 +1666,10 @@ void dts_destroy(dts_ctx* ctx) {
     if (ctx->counters) cudaFreeAsync(ctx->counters, s);
     if (ctx->tuples) cudaFreeAsync(ctx->tuples, s);
     if (ctx->flags) cudaFreeAsync(ctx->flags, s);
-    if (ctx->v_tuples) cudaFreeAsync(ctx->v_tuples, s);
-    if (ctx->v_flags) cudaFreeAsync(ctx->v_flags, s);
+    if (ctx->p_maps) cudaFreeAsync(ctx->p_maps, s);
+    if (ctx->p_flags) cudaFreeAsync(ctx->p_flags, s);
+    if (ctx->p_bar) cudaFreeAsync(ctx->p_bar, s);
+    if (ctx->resid) cudaFreeAsync(ctx->resid, s);
     if (ctx->win) cudaFreeAsync(ctx->win, s);
     for (float* q : ctx->edge_gam)
         if (q) cudaFreeAsync(q, s);

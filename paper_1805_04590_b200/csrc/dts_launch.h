@@ -42,7 +42,7 @@ cudaError_t launch_row_update(const RowPlan& plan, const Geometry& g, int Ct, co
 // K3/K4: recursive-filter column pass (decoupled band-tuple scan, cooperative
 // persistent grid), FILTER, UPDATE (fused solver step, Eq. 3) or SUPPORT mode.
 struct ColPlan {
-    int kind;  // 0: decoupled band-tuple kernel (k_col.cu), 1: cluster kernel (k_colc.cu), 2: k_colv.cu, 3: k_col2p.cu
+    int kind;  // 0: decoupled band-tuple kernel (k_col.cu), 1: cluster kernel (k_colc.cu)
     int TW, CB, HB, S, Ls, nb, ntiles, threads;
     dim3 grid;
     size_t smem;
@@ -64,6 +64,7 @@ struct UpdateArgs {
     const float* chat;   // c / S
     float lam, step;
     float* out_hwc;      // when non-null: write the result here (H x W x Ct) instead of Z
+    unsigned* resid;     // when non-null (streaming update kernel only): ||g||_inf, atomicMax of float bits
 };
 cudaError_t plan_col_pass(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
 cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
@@ -82,20 +83,6 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
                                float* rank_tuples = nullptr,   // TUPLE: [ntiles][2Ct+3][32]
                                float* edge = nullptr);         // edge scheme: [ntiles][2Ct+1][32]
 
-// K3/K4 streaming path (k_colv.cu): decoupled band-tuple scan over 64-column tiles with
-// shared-memory-held items and a TMA producer warp; FILTER and UPDATE (fused Eq. 3).
-// Needs d with H + 1 rows (row H = +inf, or the halo link).  kind = 2; its scratch is
-// `tuple_floats` floats + `flag_count` zero-initialised words, owned by the caller.
-cudaError_t plan_col_stream(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
-cudaError_t launch_col_stream(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
-                              float kc, const UpdateArgs* upd, const ColScratch& scr, cudaStream_t s);
-
-// K3 two-phase path (k_col2p.cu): decoupled band-tuple scan with an L2 lag, high occupancy;
-// FILTER only.  kind = 3; scratch as for kind 2.
-cudaError_t plan_col_2p(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
-cudaError_t launch_col_2p(const ColPlan& plan, const Geometry& g, int Ct, float* x, const float* d, float kc,
-                          const ColScratch& scr, cudaStream_t s);
-
 // Eq. (7) confidence: planar X0 = t, X1 = t^2 from a row-major H x W
 // target; and, after the DTF of both planes, V = max(0, X1 - X0^2), c = exp(-V / (2 sc^2)).
 cudaError_t launch_conf_prologue(const float* target, const Geometry& g, float* X, cudaStream_t s);
@@ -112,12 +99,44 @@ cudaError_t launch_update_stereo(const float* X, float* Z, const float* T, const
 cudaError_t launch_sr_prepare(const float* low, int64_t h, int64_t w, int f, float* target, float* conf,
                               cudaStream_t s);
 
+// Persistent L2-resident solve (k_persist.cu): the whole iteration loop of a C_t = 1 solve in
+// one cooperative launch, for images whose columns fit one resident warp per 32-column x
+// LS-row segment and whose rows fit one warp (W <= 1536).  cudaErrorNotSupported otherwise.
+struct PersistPlan {
+    int L, LS, ntiles, nseg, grid, threads;  // nseg: bands (16 segments of LS rows) per 32-column tile
+    size_t smem;
+};
+cudaError_t plan_persist(const Geometry& g, int Ct, int N, int num_sms, PersistPlan* plan);
+// X, Z, T, chat, dx: the context planes; A1y: a_1^{d_y} rows 0..H; kc[i]: row exponents of pass
+// i; out: H x W row-major; resid (nullable): [iters] ||g_k||_inf as float bits, zeroed by the
+// caller; maps >= ntiles * nseg * 128 floats, flags >= ntiles * nseg * 2 words (zeroed once),
+// bar: the 64-bit barrier counter (zeroed once), bar_base its value at this launch; epoch0:
+// fresh base (flags compare against epoch0 + 2 phase + dir)
+cudaError_t launch_persist(const PersistPlan& plan, const Geometry& g, int N, int iters, const float* kc, float lam,
+                           float step, float* X, float* Z, const float* T, const float* chat, const float* dx,
+                           const float* A1y, float* out, unsigned* resid, float* maps, unsigned* flags,
+                           unsigned long long* bar, unsigned long long bar_base, unsigned epoch0, cudaStream_t s);
+// grid barriers one launch executes (the host advances its copy of the counter by this)
+inline unsigned long long persist_barriers(const PersistPlan& plan, int N, int iters) {
+    return 2ull * N * iters * (unsigned long long)plan.grid;
+}
+
+// dts_set_option("col_cluster") (experiments): forced column-kernel cluster size, 0 = auto
+int option_col_cluster();
+
+// debug: device buffer (4096 u64) receiving %globaltimer stamps of block 0 at every phase
+// boundary of the persistent kernel (nullptr: off)
+unsigned long long* persist_timers();
+void set_persist_timers(unsigned long long* t);
+
 // fill n floats with v
 cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);
 
 // K4b: Eq. (3) update as a streaming kernel (zbar in X); writes Z, or out_hwc when non-null.
+// resid (nullable): ||g||_inf of this step folded into *resid as float bits (atomicMax)
 cudaError_t launch_update(const float* X, float* Z, const float* T, const float* chat, int Ct, const Geometry& g,
-                          float lam, float step, float* out_hwc, int num_sms, cudaStream_t s);
+                          float lam, float step, float* out_hwc, int num_sms, cudaStream_t s,
+                          unsigned* resid = nullptr);
 
 // compose gathered rank tuples [P][ntiles][2NV+3][32] into this rank's carries
 // [ntiles][2][NV][32] (causal carry from the ranks above, anticausal from below)
@@ -164,6 +183,12 @@ cudaError_t launch_box_col(const BoxPlan& plan, const Geometry& g, int Ct, const
 // below the band (z(H-1) = y(H-1)), so the bottom carry is z_H - y(H-1)
 cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float kc, float* gam, float* theta,
                                  cudaStream_t s, bool raw = false);
+// decay lengths of a band's edge carries (top -> len[0], bottom -> len[1], atomicMax; zero them
+// first); d has rows 0..H (row H: the link below the band)
+cudaError_t launch_edge_length(const float* d, const Geometry& g, int Lcap, float kc, unsigned* len, cudaStream_t s);
+// set cudaFuncAttributeMaxDynamicSharedMemorySize of `fn` on the current device to at least
+// `bytes` (tracked per device and function, thread-safe)
+cudaError_t ensure_smem_attr(const void* fn, size_t bytes);
 cudaError_t launch_edge_fix(float* x, int Ct, const Geometry& g, int L, const float* gam, const float* theta,
                             const float* gathered, int P, int rank, cudaStream_t s, bool cross = true,
                             bool cut = false);

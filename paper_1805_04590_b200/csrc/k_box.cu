@@ -430,7 +430,7 @@ static int occupancy(const void* fn, int threads, size_t smem) {
 cudaError_t launch_box_increments(const float* guide, int C, float k2, const Geometry& g, uint32_t* qx, uint32_t* qy,
                                   cudaStream_t s) {
     dim3 grid((unsigned)((g.W + 255) / 256), (unsigned)g.H);
-    if ((C == 4 || C == 8 || C == 16) && (uintptr_t)guide % 16 == 0 && !std::getenv("DTS_BOX_SCALAR")) {
+    if ((C == 4 || C == 8 || C == 16) && (uintptr_t)guide % 16 == 0) {
         const dim3 gv((unsigned)((g.W + 1 + box::BI_COLS - 1) / box::BI_COLS),
                       (unsigned)((g.H + box::BI_ROWS - 1) / box::BI_ROWS));
         if (C == 4) box::k_box_increments_vec<1><<<gv, 256, 0, s>>>(guide, k2, g.H, g.W, g.pitch, qx, qy);
@@ -476,8 +476,9 @@ cudaError_t plan_box(const Geometry& g, long long R, int num_sms, BoxPlan* plan)
     plan->row_smem = pw * warps;
     // the attribute is per function, shared by the plans of all passes: set it to the
     // opt-in maximum once, so that no plan lowers another's limit
-    int optin = 0;
-    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+    int optin = 0, dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return e;
     if (plan->row_smem > (size_t)optin) return cudaErrorInvalidValue;
     const void* frow = reinterpret_cast<const void*>(box::k_box_row);

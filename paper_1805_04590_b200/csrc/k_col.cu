@@ -655,15 +655,10 @@ cudaError_t plan_col_pass(const Geometry& g, int Ct, int mode, int num_sms, ColP
     const int nb = (int)((g.H + HB - 1) / HB);
     const ColSmem L = col_smem_layout(NV, HB, S, nb);
     if (L.bytes > kSmemMax) return cudaErrorInvalidValue;
-    static size_t configured[64] = {0};
-    const int slot = (mode * 8 + Ct) & 63;
-    if (L.bytes > configured[slot]) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-        if (e != cudaSuccess) return e;
-        configured[slot] = L.bytes;
-    }
+    cudaError_t e = ensure_smem_attr(fn, L.bytes);
+    if (e != cudaSuccess) return e;
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TW * S, L.bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TW * S, L.bytes);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidValue;
     const int ntiles = (int)((g.W + TW - 1) / TW);

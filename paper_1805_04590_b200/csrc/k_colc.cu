@@ -1,8 +1,9 @@
-// k_colc.cu -- K3/K4 fast path: column pass with the column tile held by a
+// k_colc.cu -- K3 fast path: column pass with the column tile held by a
 // thread-block CLUSTER (sm_100a), persistent over tiles, TMA-prefetching the next tile.
 //
-// Same recurrence and modes as k_col.cu (R4-R7; UPDATE = Eq. (3),
-// P:185-189).  Layout of the work: a column tile is 32 columns x H rows; CTA
+// Same recurrence as k_col.cu (R4-R7), FILTER and SUPPORT modes (+ the
+// row-band TUPLE mode); the Eq. (3) step runs in the streaming update kernel or the next
+// iteration's first row pass (DESIGN.md section 12 records why the fused write-out lost).  Layout of the work: a column tile is 32 columns x H rows; CTA
 // b of a cluster of CB CTAs owns rows [b*HB, (b+1)*HB); inside the CTA, warp s owns
 // rows [s*LS, (s+1)*LS) and lane c owns column c, holding its LS samples and
 // coefficients in REGISTERS.  Per tile:
@@ -12,7 +13,7 @@
 //   distributed shared memory (DSMEM) after a cluster barrier -> exact causal apply
 //   with the anticausal map folded on the fly -> second DSMEM exchange -> exact
 //   anticausal apply -> stores straight from registers (one 128-B row segment per
-//   warp instruction) or the fused Eq. (3) update.
+//   warp instruction).
 // Each pixel is read from HBM once and written once per pass; the carries between
 // bands never leave the chip.
 #include <cuda.h>
@@ -286,18 +287,6 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
         // ordered by the fold barrier below, which every warp passes after this tile)
         __syncwarp();
         if (c == 0 && tile + nclusters < p.ntiles) stage_seg(tile + nclusters, s);
-        if constexpr (MODE == MODE_UPDATE) {  // the write-out's Z / T / chat lines -> L2 (lane = row)
-            const int r = r0 + lo + c;
-            if (r < p.H) {
-                const int64_t o = (int64_t)r * p.pitch + col0;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    prefetch_l2(p.upd.Z + v * p.plane + o);
-                    prefetch_l2(p.upd.T + v * p.plane + o);
-                }
-                prefetch_l2(p.upd.chat + o);
-            }
-        }
 
         // ---- 2. causal fold, segment scan, band total ----
         {
@@ -448,36 +437,6 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
 #pragma unroll
                                 for (int v = 0; v < NV; ++v) base[v * p.plane + (int64_t)j * pitch] = xv[v][j];
                             }
-                    }
-                } else {  // MODE_UPDATE, Eq. (3) with zbar = xv; Z / T / chat were prefetched
-                          // into L2 when the tile started; 16 rows of loads in flight at a time
-                    constexpr int UB = 16;
-                    const int64_t pitch = p.pitch;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) {
-#pragma unroll
-                        for (int j0 = 0; j0 < LSV; j0 += UB) {
-                            float zo[UB], tv[UB], ch[UB];
-#pragma unroll
-                            for (int u = 0; u < UB; ++u) {
-                                const int jj = (j0 + u < nrow) ? j0 + u : 0;
-                                const int64_t o = (int64_t)(r0 + lo + jj) * pitch + col;
-                                zo[u] = p.upd.Z[v * p.plane + o];
-                                tv[u] = __ldg(p.upd.T + v * p.plane + o);
-                                ch[u] = __ldg(p.upd.chat + o);
-                            }
-#pragma unroll
-                            for (int u = 0; u < UB; ++u) {
-                                const int j = j0 + u;
-                                if (j < nrow) {
-                                    const int64_t r = r0 + lo + j;
-                                    const float g = fmaf(p.upd.lam, zo[u] - xv[v][j], ch[u] * (zo[u] - tv[u]));
-                                    const float zn = fmaf(-p.upd.step, g, zo[u]);
-                                    if (p.upd.out_hwc) p.upd.out_hwc[(r * p.W + col) * CT + v] = zn;
-                                    else p.upd.Z[v * p.plane + r * pitch + col] = zn;
-                                }
-                            }
-                        }
                     }
                 }
             }
@@ -674,18 +633,6 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
         }
         __syncwarp();  // this warp's segment is in registers: refill it (only this warp reads it)
         if (c == 0 && tile + nclusters < p.ntiles) stage_seg(tile + nclusters, s);
-        if constexpr (MODE == MODE_UPDATE) {  // the write-out's Z / T / chat lines -> L2 (lane = row)
-            const int r = r0 + lo + c;
-            if (r < p.H) {
-                const int64_t o = (int64_t)r * p.pitch + col0;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    prefetch_l2(p.upd.Z + v * p.plane + o);
-                    prefetch_l2(p.upd.T + v * p.plane + o);
-                }
-                prefetch_l2(p.upd.chat + o);
-            }
-        }
 
         // ---- 2. causal fold, segment scan, band total ----
         {
@@ -874,36 +821,6 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
                                 for (int v = 0; v < NV; ++v) base[v * p.plane + (int64_t)j * pitch] = xv[v][j];
                             }
                     }
-                } else {  // MODE_UPDATE, Eq. (3) with zbar = xv; Z / T / chat were prefetched
-                          // into L2 when the tile started; 16 rows of loads in flight at a time
-                    constexpr int UB = 16;
-                    const int64_t pitch = p.pitch;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) {
-#pragma unroll
-                        for (int j0 = 0; j0 < LS; j0 += UB) {
-                            float zo[UB], tv[UB], ch[UB];
-#pragma unroll
-                            for (int u = 0; u < UB; ++u) {
-                                const int jj = (j0 + u < nrow) ? j0 + u : 0;
-                                const int64_t o = (int64_t)(r0 + lo + jj) * pitch + col;
-                                zo[u] = p.upd.Z[v * p.plane + o];
-                                tv[u] = __ldg(p.upd.T + v * p.plane + o);
-                                ch[u] = __ldg(p.upd.chat + o);
-                            }
-#pragma unroll
-                            for (int u = 0; u < UB; ++u) {
-                                const int j = j0 + u;
-                                if (j < nrow) {
-                                    const int64_t r = r0 + lo + j;
-                                    const float g = fmaf(p.upd.lam, zo[u] - xv[v][j], ch[u] * (zo[u] - tv[u]));
-                                    const float zn = fmaf(-p.upd.step, g, zo[u]);
-                                    if (p.upd.out_hwc) p.upd.out_hwc[(r * p.W + col) * CT + v] = zn;
-                                    else p.upd.Z[v * p.plane + r * pitch + col] = zn;
-                                }
-                            }
-                        }
-                    }
                 }
             }
         }
@@ -1002,9 +919,6 @@ static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = f
         case 4 + MODE_FILTER: return kptr<1, MODE_FILTER>();
         case 8 + MODE_FILTER: return kptr<2, MODE_FILTER>();
         case 12 + MODE_FILTER: return kptr<3, MODE_FILTER>();
-        case 4 + MODE_UPDATE: return kptr<1, MODE_UPDATE>();
-        case 8 + MODE_UPDATE: return kptr<2, MODE_UPDATE>();
-        case 12 + MODE_UPDATE: return kptr<3, MODE_UPDATE>();
     }
     return nullptr;
 }
@@ -1031,8 +945,10 @@ static cudaError_t plan_col_cluster_uncached(const Geometry& g, int Ct, int mode
     // attributes are per function and shared by every plan: allow non-portable clusters and
     // the opt-in shared memory maximum (so that no plan lowers another's limit); the
     // A1-input (and, at 32-row segments, row-band) variants of the FILTER kernel get the same
-    int optin = 0;
-    if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0)) != cudaSuccess) return e;
+    int optin = 0, dev = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess ||
+        (e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+        return e;
     const bool f32 = mode == MODE_FILTER && ls == colc::LS;
     for (const void* f : {fn, mode == MODE_FILTER ? colc_kernel(Ct, mode, true, false, ls) : fn,
                           f32 ? colc_kernel(Ct, mode, false, true) : fn, f32 ? colc_kernel(Ct, mode, true, true) : fn}) {
@@ -1072,9 +988,6 @@ static cudaError_t plan_col_cluster_uncached(const Geometry& g, int Ct, int mode
         }
         if (nclusters > ntiles) nclusters = ntiles;
         const int64_t cost = (ntiles + nclusters - 1) / nclusters;  // tile rounds
-        if (std::getenv("DTS_DEBUG"))
-            std::fprintf(stderr, "plan_col_cluster: Ct %d mode %d ls %d CB %d S %d clusters %d ntiles %d cost %lld\n", Ct,
-                         mode, ls, CB, S, nclusters, ntiles, (long long)cost);
         if (best_cost >= 0 && (ls == colc::LS || cost > best_cost)) continue;
         best_cost = cost;
         plan->kind = 1;
@@ -1097,8 +1010,7 @@ static cudaError_t plan_col_cluster_uncached(const Geometry& g, int Ct, int mode
 
 cudaError_t plan_col_cluster_ls(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int ls) {
     (void)num_sms;
-    const char* f = std::getenv("DTS_COL_CB");  // force a cluster size (experiments)
-    const int fcb = f ? atoi(f) : 0;
+    const int fcb = option_col_cluster();  // forced cluster size (experiments; 0 = auto)
     int dev = 0;
     cudaGetDevice(&dev);
     struct Entry {
@@ -1218,6 +1130,39 @@ __global__ void k_edge_profiles(const float* __restrict__ d, int64_t H, int64_t 
 cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float kc, float* gam, float* theta,
                                  cudaStream_t s, bool raw) {
     k_edge_profiles<<<(unsigned)((g.W + 127) / 128), 128, 0, s>>>(d, g.H, g.W, g.pitch, L, kc, gam, theta, raw);
+    return cudaGetLastError();
+}
+
+// How many rows a carry entering the band keeps an influence >= 2^-26 of itself, maximised
+// over the columns (folded into len[0] (top edge) and len[1] (bottom edge) with atomicMax):
+// top:    the influence on row k is G_k = prod_{j <= k} a_j (a_0: the link to the band above);
+//         rows 0..k-1 need the correction, where k is the first row with G_k < 2^-26;
+// bottom: the influence on row H-1-m is Theta = prod_{j = H-m..H} a_j (a_H: the link below).
+// The anticausal response Gamma of G is a convex combination of G_m, m >= k, so Gamma_k <= G_k.
+// Walks at most Lcap rows per column (d >= 1 bounds the true length by ceil(26 / kc)).
+__global__ void k_edge_length(const float* __restrict__ d, int64_t H, int64_t W, int64_t pitch, int Lcap, float kc,
+                              unsigned* __restrict__ len) {
+    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= W) return;
+    const float thr = 1.0f / 67108864.0f;  // 2^-26
+    float G = 1.f;
+    int k = 0;
+    for (; k < Lcap; ++k) {
+        G *= coef_from_d(__ldg(d + (int64_t)k * pitch + col), kc);
+        if (G < thr) break;
+    }
+    atomicMax(&len[0], (unsigned)k);
+    float Th = 1.f;
+    int m = 0;
+    for (; m < Lcap; ++m) {
+        Th *= coef_from_d(__ldg(d + (H - m) * pitch + col), kc);
+        if (Th < thr) break;
+    }
+    atomicMax(&len[1], (unsigned)m);
+}
+
+cudaError_t launch_edge_length(const float* d, const Geometry& g, int Lcap, float kc, unsigned* len, cudaStream_t s) {
+    k_edge_length<<<(unsigned)((g.W + 127) / 128), 128, 0, s>>>(d, g.H, g.W, g.pitch, Lcap, kc, len);
     return cudaGetLastError();
 }
 

@@ -2,6 +2,10 @@
 #include "dts_device.cuh"
 #include "dts_launch.h"
 
+#include <mutex>
+#include <utility>
+#include <vector>
+
 namespace dts {
 
 // K1: domain-transform increments between adjacent pixels (Eqs. 8-9 with
@@ -199,12 +203,9 @@ cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Ge
     switch (C) {
 #define DTS_DERIV_CASE(K)                                                                              \
     case K: {                                                                                         \
-        static bool cfg = false;                                                                      \
-        if (!cfg) {                                                                                   \
-            cudaFuncSetAttribute(k_guide_deriv<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
-            cfg = true;                                                                               \
-        }                                                                                             \
-        k_guide_deriv<K><<<grid, block, smem, s>>>(guide, C, ratio2, g, dx, dy, a1y, kc0);                       \
+        cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k_guide_deriv<K>), smem);      \
+        if (e != cudaSuccess) return e;                                                               \
+        k_guide_deriv<K><<<grid, block, smem, s>>>(guide, C, ratio2, g, dx, dy, a1y, kc0);            \
         break;                                                                                        \
     }
         DTS_DERIV_CASE(1)
@@ -212,11 +213,8 @@ cudaError_t launch_guide_deriv(const float* guide, int C, float ratio2, const Ge
         DTS_DERIV_CASE(4)
         DTS_DERIV_CASE(16)
         default: {
-            static bool cfg = false;
-            if (!cfg) {
-                cudaFuncSetAttribute(k_guide_deriv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-                cfg = true;
-            }
+            cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k_guide_deriv<0>), smem);
+            if (e != cudaSuccess) return e;
             k_guide_deriv<0><<<grid, block, smem, s>>>(guide, C, ratio2, g, dx, dy, a1y, kc0);
         }
 #undef DTS_DERIV_CASE
@@ -297,9 +295,10 @@ cudaError_t launch_prologue(const float* target, const float* conf, int Ct, cons
 __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X, float* __restrict__ Z,
                                                 const float* __restrict__ T, const float* __restrict__ chat,
                                                 int Ct, Geometry g, float lam, float step,
-                                                float* __restrict__ out_hwc) {
+                                                float* __restrict__ out_hwc, unsigned* __restrict__ resid) {
     const int64_t per_row = g.pitch / 4;
     const int64_t n = g.H * per_row;
+    float gmax = 0.f;  // ||g||_inf of this step (K8), when resid is requested
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = i / per_row;
         const int64_t c4 = (i - r * per_row) * 4;
@@ -316,6 +315,12 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X, flo
             zn.y = fmaf(-step, fmaf(lam, zo.y - zb.y, ch.y * (zo.y - tv.y)), zo.y);
             zn.z = fmaf(-step, fmaf(lam, zo.z - zb.z, ch.z * (zo.z - tv.z)), zo.z);
             zn.w = fmaf(-step, fmaf(lam, zo.w - zb.w, ch.w * (zo.w - tv.w)), zo.w);
+            if (resid) {
+                const float gg[4] = {fmaf(lam, zo.x - zb.x, ch.x * (zo.x - tv.x)), fmaf(lam, zo.y - zb.y, ch.y * (zo.y - tv.y)),
+                                     fmaf(lam, zo.z - zb.z, ch.z * (zo.z - tv.z)), fmaf(lam, zo.w - zb.w, ch.w * (zo.w - tv.w))};
+                for (int u = 0; u < 4; ++u)
+                    if (c4 + u < g.W) gmax = fmaxf(gmax, fabsf(gg[u]));
+            }
             if (out_hwc) {
                 const float zz[4] = {zn.x, zn.y, zn.z, zn.w};
                 for (int u = 0; u < 4; ++u)
@@ -325,16 +330,20 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X, flo
             }
         }
     }
+    if (resid) {  // max is order-independent: the result is deterministic
+        const unsigned m = __reduce_max_sync(FULL, __float_as_uint(gmax));
+        if ((threadIdx.x & 31) == 0 && m) atomicMax(resid, m);
+    }
 }
 
 cudaError_t launch_update(const float* X, float* Z, const float* T, const float* chat, int Ct, const Geometry& g,
-                          float lam, float step, float* out_hwc, int num_sms, cudaStream_t s) {
+                          float lam, float step, float* out_hwc, int num_sms, cudaStream_t s, unsigned* resid) {
     const int64_t n = g.H * (g.pitch / 4);
     int64_t blocks = (n + 255) / 256;
     const int64_t cap = (int64_t)num_sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    k_update<<<(unsigned)blocks, 256, 0, s>>>(X, Z, T, chat, Ct, g, lam, step, out_hwc);
+    k_update<<<(unsigned)blocks, 256, 0, s>>>(X, Z, T, chat, Ct, g, lam, step, out_hwc, resid);
     return cudaGetLastError();
 }
 
@@ -537,6 +546,30 @@ cudaError_t launch_sr_prepare(const float* low, int64_t h, int64_t w, int f, flo
     dim3 grid((unsigned)(bx < 64 ? bx : 64), (unsigned)(H < 8192 ? H : 8192), 1);
     k_sr_prepare<<<grid, 256, 0, s>>>(low, h, w, f, target, conf);
     return cudaGetLastError();
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per function AND per device: remember, per
+// (device, function), the largest value set so far, under a lock (one process may drive
+// several GPUs from several threads)
+cudaError_t ensure_smem_attr(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, const void*>, size_t>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& en : done)
+        if (en.first.first == dev && en.first.second == fn) {
+            if (en.second >= bytes) return cudaSuccess;
+            if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)) != cudaSuccess)
+                return e;
+            en.second = bytes;
+            return cudaSuccess;
+        }
+    if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)) != cudaSuccess)
+        return e;
+    done.push_back({{dev, fn}, bytes});
+    return cudaSuccess;
 }
 
 }  // namespace dts

@@ -389,13 +389,8 @@ cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowP
 
 template <int L, int CT, int MODE>
 static cudaError_t launch_t(const RowPlan& plan, const RowParams& p, cudaStream_t s) {
-    static size_t configured = 0;  // largest dynamic smem enabled so far for this instantiation
-    if (plan.smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_row_pass<L, CT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)plan.smem);
-        if (e != cudaSuccess) return e;
-        configured = plan.smem;
-    }
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k_row_pass<L, CT, MODE>), plan.smem);
+    if (e != cudaSuccess) return e;
     k_row_pass<L, CT, MODE><<<plan.grid, plan.threads, plan.smem, s>>>(p);
     return cudaGetLastError();
 }

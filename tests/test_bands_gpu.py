@@ -120,43 +120,41 @@ def test_nccl_transport_single_rank():
     assert np.max(np.abs(out.cpu().numpy() - one)) <= 1e-5 * target_range(t)
 
 
-def test_bands_legacy_kernel_matches(monkeypatch):
-    """The decoupled band-tuple kernel (DTS_BAND_LEGACY=1) and the cluster TUPLE / APPLY
+def test_bands_legacy_kernel_matches():
+    """The decoupled band-tuple kernel (option band_scheme = 2) and the cluster TUPLE / APPLY
     kernels give the same banded solve (fp32 rounding)."""
     g, t, c = random_problem(1500, 96, 3, 1, seed=11)
     args = (9.0, 0.3, 3, 0.99, 4)
-    a = solve_bands(g, t, c, *args, P=2)
-    monkeypatch.setenv("DTS_BAND_LEGACY", "1")
-    b = solve_bands(g, t, c, *args, P=2)
+    with dts.options(band_scheme=1):
+        a = solve_bands(g, t, c, *args, P=2)
+    with dts.options(band_scheme=2):
+        b = solve_bands(g, t, c, *args, P=2)
     assert np.max(np.abs(a - b)) <= 1e-5 * target_range(t)
 
 
 @pytest.mark.parametrize("P", [2, 3])
-def test_bands_edge_scheme_matches_tuple_scheme(P, monkeypatch):
+def test_bands_edge_scheme_matches_tuple_scheme(P):
     """Bands of >= 2L rows use the edge fix-up scheme (zero-carry pass + corrections on the L
-    rows at each edge); DTS_BAND_TUPLE=1 forces the exact TUPLE / APPLY composition.  The two
-    agree to fp32 rounding, and both match the oracle."""
+    rows at each edge); option band_scheme = 1 forces the exact TUPLE / APPLY composition.  The
+    two agree to fp32 rounding, and both match the oracle."""
     g, t, c = random_problem(900, 80, 3, 1, seed=17 + P)
     args = (5.0, 0.2, 3, 0.99, 5)
     a = solve_bands(g, t, c, *args, P=P)
-    monkeypatch.setenv("DTS_BAND_TUPLE", "1")
-    b = solve_bands(g, t, c, *args, P=P)
+    with dts.options(band_scheme=1):
+        b = solve_bands(g, t, c, *args, P=P)
     rng = target_range(t)
     assert np.max(np.abs(a - b)) <= 1e-5 * rng
     assert np.max(np.abs(a - oracle.solve(g, t, c, *args))) <= 1e-4 * rng
 
 
-@pytest.mark.parametrize("P", [2, 4])
-def test_bands_cut_edge_scheme_matches_exporting_kernel(P, monkeypatch):
-    """Reading R26: the edge scheme on the single-context kernel (link below each band cut,
-    edge values read from the output rows, bottom carry z_H - y(H-1)) against the band
-    kernel that keeps the link and exports the edge values (DTS_BAND_EXPORT=1).  Same
-    result to fp32 rounding, and both match the oracle."""
-    g, t, c = random_problem(1200, 90, 3, 1, seed=31 + P)
+def test_bands_straddling_the_edge_threshold():
+    """band heights that differ by one row around 2L + 1 must still run the same
+    scheme on every rank (H = 113 over 2 ranks: 56 and 57 rows; sigma_s = 5, N = 3)."""
+    g, t, c = random_problem(113, 70, 3, 1, seed=5)
     args = (5.0, 0.2, 3, 0.99, 4)
-    a = solve_bands(g, t, c, *args, P=P)
-    monkeypatch.setenv("DTS_BAND_EXPORT", "1")
-    b = solve_bands(g, t, c, *args, P=P)
     rng = target_range(t)
-    assert np.max(np.abs(a - b)) <= 1e-5 * rng
-    assert np.max(np.abs(a - oracle.solve(g, t, c, *args))) <= 1e-4 * rng
+    ref = oracle.solve(g, t, c, *args)
+    for scheme in (0, 1, 2):
+        with dts.options(band_scheme=scheme):
+            a = solve_bands(g, t, c, *args, P=2)
+        assert np.max(np.abs(a - ref)) <= 1e-4 * rng, scheme

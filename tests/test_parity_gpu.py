@@ -81,11 +81,15 @@ SHAPES = [(1, 1), (1, 7), (7, 1), (2, 2), (31, 33), (33, 31), (32, 32), (61, 97)
           (12000, 33)]
 
 
+@pytest.mark.parametrize("persistent", [1, 0])
 @pytest.mark.parametrize("H,W", SHAPES)
-def test_edge_shapes_parity(H, W):
+def test_edge_shapes_parity(H, W, persistent):
+    """Every shape on the default path (the persistent kernel where it applies) and on the
+    per-pass streaming kernels (option persistent = 0)."""
     g, t, c = random_problem(H, W, 3, 1, seed=7 * H + W)
     iters = 3 if H * W > 100000 else 6
-    check(g, t, c, 5.0, 0.2, 3, 0.99, iters)
+    with dts.options(persistent=persistent):
+        check(g, t, c, 5.0, 0.2, 3, 0.99, iters)
 
 
 @pytest.mark.parametrize("Ct", [2, 3, 4])
@@ -254,52 +258,21 @@ def test_c4_full_parity():
 
 
 @pytest.mark.parametrize("H,W,Ct", [(48, 64, 1), (33, 31, 1), (700, 130, 1), (300, 90, 3), (61, 97, 2)])
-def test_fallback_column_kernel_parity(H, W, Ct, monkeypatch):
-    """The decoupled band-tuple column kernel (used when a column does not fit a
-    cluster) forced for ordinary shapes: DTS_NO_CLUSTER=1."""
-    monkeypatch.setenv("DTS_NO_CLUSTER", "1")
-    monkeypatch.setenv("DTS_COL", "legacy")
+def test_fallback_column_kernel_parity(H, W, Ct):
+    """The decoupled band-tuple column kernel (used when a column does not fit a cluster)
+    forced for ordinary shapes (option col_kernel = 1), Eq. (3) in its write-out."""
     g, t, c = random_problem(H, W, 3, Ct, seed=H + 3 * W)
-    check(g, t, c, 6.0, 0.2, 3, 0.99, 5)
+    with dts.options(col_kernel=1, persistent=0):
+        check(g, t, c, 6.0, 0.2, 3, 0.99, 5)
 
 
 @pytest.mark.parametrize("H,W,Ct", [(48, 64, 1), (700, 130, 1), (300, 90, 3), (2600, 35, 1)])
-def test_legacy_cluster_column_kernel_parity(H, W, Ct, monkeypatch):
-    """The cluster column kernel + streaming update kernel (DTS_COL=legacy)."""
-    monkeypatch.setenv("DTS_COL", "legacy")
+def test_separate_update_kernel_parity(H, W, Ct):
+    """The cluster column kernel with the Eq. (3) step as its own streaming kernel every
+    iteration (option row_update = 0) instead of inside the next row pass."""
     g, t, c = random_problem(H, W, 3, Ct, seed=H + 5 * W)
-    check(g, t, c, 6.0, 0.2, 3, 0.99, 5)
-
-
-# streaming column kernel (k_colv.cu): band boundaries (HB = 128 rows for Ct = 1, 32..64
-# for Ct > 1), 64-column tiles with ragged / odd widths, many bands per tile
-@pytest.mark.parametrize("H,W,Ct", [(127, 64, 1), (128, 64, 1), (129, 64, 1), (256, 65, 1), (385, 127, 1),
-                                    (1000, 199, 1), (10000, 9, 1), (4000, 513, 1), (65, 33, 2), (129, 131, 3),
-                                    (64, 1, 1), (1, 200, 1)])
-def test_stream_column_kernel_parity(H, W, Ct, monkeypatch):
-    """The TMEM-lagged decoupled column kernel (DTS_COL=stream) + the Eq. (3) step fused
-    into the next iteration's first row pass."""
-    monkeypatch.setenv("DTS_COL", "stream")
-    g, t, c = random_problem(H, W, 3, Ct, seed=3 * H + W + Ct)
-    check(g, t, c, 9.0, 0.3, 3, 0.99, 4)
-
-
-def test_stream_matches_default(monkeypatch):
-    """Two independent column kernels agree to fp32 rounding on a C1-like problem."""
-    g, t, c = random_problem(1000, 700, 3, 1, seed=99)
-    a = gpu_solve(g, t, c, 16.0, 0.1, 3, 0.99, 10)
-    monkeypatch.setenv("DTS_COL", "stream")
-    b = gpu_solve(g, t, c, 16.0, 0.1, 3, 0.99, 10)
-    assert np.max(np.abs(a - b)) <= 1e-5 * target_range(t)
-
-
-@pytest.mark.parametrize("H,W,Ct", [(48, 64, 1), (129, 64, 1), (700, 130, 1), (1000, 199, 1), (300, 90, 3),
-                                    (61, 97, 2), (2600, 35, 1)])
-def test_two_phase_column_kernel_parity(H, W, Ct, monkeypatch):
-    """The two-phase L2-lag column kernel (k_col2p.cu, DTS_COL=2p)."""
-    monkeypatch.setenv("DTS_COL", "2p")
-    g, t, c = random_problem(H, W, 3, Ct, seed=5 * H + W + Ct)
-    check(g, t, c, 6.0, 0.2, 3, 0.99, 4)
+    with dts.options(row_update=0, persistent=0):
+        check(g, t, c, 6.0, 0.2, 3, 0.99, 5)
 
 
 def test_repeated_solves_replay_a_graph():
@@ -398,17 +371,16 @@ def test_too_tall_image_is_a_shape_error():
 
 
 @pytest.mark.parametrize("H,W,Ct", [(1500, 330, 1), (9000, 200, 1), (2160, 390, 3), (700, 70, 2), (1300, 4100, 1)])
-def test_repeat_solves_bit_identical(H, W, Ct, monkeypatch):
+def test_repeat_solves_bit_identical(H, W, Ct):
     """Race stress for the cluster column kernels (per-warp TMA issue, no end-of-tile
     barrier, link coefficient behind the next segment's mbarrier): their arithmetic order is
     fixed, so a shared-memory hazard shows up as a run-to-run difference.  Shapes: several
     CTAs per cluster with a ragged last segment, 15 CTAs per cluster, C_t = 3 and 2 on the
     16-row-segment variant.  Ten eager solves each, outputs compared bit for bit."""
-    monkeypatch.setenv("DTS_NO_GRAPH", "1")
     g, t, c = random_problem(H, W, 3, Ct, seed=H + W + Ct)
     gd, td, cd = (torch.from_numpy(a).cuda() for a in (g, t, c))
     outs = []
-    with dts.Solver(gd, 8.0, 0.1, 3) as s:
+    with dts.options(graphs=0), dts.Solver(gd, 8.0, 0.1, 3) as s:
         for _ in range(10):
             o = torch.empty_like(td)
             s.solve(td, cd, 0.99, 3, out=o)
@@ -420,11 +392,11 @@ def test_repeat_solves_bit_identical(H, W, Ct, monkeypatch):
         assert np.array_equal(o.cpu().numpy(), ref)
 
 
-def test_forty_row_segments_parity(monkeypatch):
+def test_forty_row_segments_parity():
     """C_t = 1 images with several cluster tile rounds per column pass take the 16-warp x
     40-row-segment instantiation of the cluster kernel (plan_col); a wide image reaches it.
-    Parity with the oracle, and again with the 32-row kernel forced (DTS_COL_LS40=0)."""
+    Parity with the oracle, and again with the 32-row kernel forced (option col_rows = 32)."""
     g, t, c = random_problem(1300, 4100, 3, 1, seed=77)
     check(g, t, c, 6.0, 0.15, 3, 0.99, 3)
-    monkeypatch.setenv("DTS_COL_LS40", "0")
-    check(g, t, c, 6.0, 0.15, 3, 0.99, 3)
+    with dts.options(col_rows=32):
+        check(g, t, c, 6.0, 0.15, 3, 0.99, 3)
