@@ -99,35 +99,29 @@ cudaError_t launch_update_stereo(const float* X, float* Z, const float* T, const
 cudaError_t launch_sr_prepare(const float* low, int64_t h, int64_t w, int f, float* target, float* conf,
                               cudaStream_t s);
 
-// Persistent L2-resident solve (k_persist.cu): the whole iteration loop of a C_t = 1 solve in
-// one cooperative launch, for images whose columns fit one resident warp per 32-column x
-// LS-row segment and whose rows fit one warp (W <= 1536).  cudaErrorNotSupported otherwise.
-struct PersistPlan {
-    int L, LS, ntiles, nseg, grid, threads;  // nseg: bands (16 segments of LS rows) per 32-column tile
+// SMEM-resident solve (k_resident.cu): the whole iteration loop of a C_t = 1 solve in one
+// cooperative launch, the image cut into TR x TC tiles (TH x TW, TW = 32 CG) held in the shared
+// memory of one CTA each; only the filter carries cross tiles (maps + epoch flags in L2).
+// cudaErrorNotSupported when the image does not fit.
+struct ResidentPlan {
+    int CG, TW, TH, THp, TC, TR, MAPN, grid, threads;
     size_t smem;
 };
-cudaError_t plan_persist(const Geometry& g, int Ct, int N, int num_sms, PersistPlan* plan);
-// X, Z, T, chat, dx: the context planes; A1y: a_1^{d_y} rows 0..H; kc[i]: row exponents of pass
-// i; out: H x W row-major; resid (nullable): [iters] ||g_k||_inf as float bits, zeroed by the
-// caller; maps >= ntiles * nseg * 128 floats, flags >= ntiles * nseg * 2 words (zeroed once),
-// bar: the 64-bit barrier counter (zeroed once), bar_base its value at this launch; epoch0:
-// fresh base (flags compare against epoch0 + 2 phase + dir)
-cudaError_t launch_persist(const PersistPlan& plan, const Geometry& g, int N, int iters, const float* kc, float lam,
-                           float step, float* X, float* Z, const float* T, const float* chat, const float* dx,
-                           const float* A1y, float* out, unsigned* resid, float* maps, unsigned* flags,
-                           unsigned long long* bar, unsigned long long bar_base, unsigned epoch0, cudaStream_t s);
-// grid barriers one launch executes (the host advances its copy of the counter by this)
-inline unsigned long long persist_barriers(const PersistPlan& plan, int N, int iters) {
-    return 2ull * N * iters * (unsigned long long)plan.grid;
-}
+cudaError_t plan_resident(const Geometry& g, int Ct, int N, int num_sms, ResidentPlan* plan);
+// Z0 (initial state), T, chat, dx: context planes; A1y: a_1^{d_y} rows 0..H; kc[i]: row exponent
+// of pass i; out: H x W row-major; resid (nullable): [iters] ||g_k||_inf as float bits, zeroed
+// by the caller; maps >= grid * 32 * MAPN floats (16-byte aligned), zeroed once; epoch0: fresh
+// base (records carry epoch0 + k N + i; the caller advances it by N iters + 1)
+cudaError_t launch_resident(const ResidentPlan& plan, const Geometry& g, int N, int iters, const float* kc, float lam,
+                            float step, const float* Z0, const float* T, const float* chat, const float* dx,
+                            const float* A1y, float* out, unsigned* resid, float* maps, unsigned epoch0,
+                            cudaStream_t s);
+
+// debug: 64 %globaltimer stamps of CTA `cta` of the resident kernel (nullptr: off)
+void set_resident_timers(unsigned long long* t, int cta);
 
 // dts_set_option("col_cluster") (experiments): forced column-kernel cluster size, 0 = auto
 int option_col_cluster();
-
-// debug: device buffer (4096 u64) receiving %globaltimer stamps of block 0 at every phase
-// boundary of the persistent kernel (nullptr: off)
-unsigned long long* persist_timers();
-void set_persist_timers(unsigned long long* t);
 
 // fill n floats with v
 cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);
