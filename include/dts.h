@@ -277,8 +277,6 @@ dts_status dts_create_band(const float* guide_with_halo, int64_t H_total, int64_
  *   "band_scheme"  row-band contexts (latched at dts_create_band): 0 edge fix-up where the
  *                  bands allow it (default), 1 cluster TUPLE/APPLY, 2 decoupled kernel
  *   "graphs"       1 replay repeated identical solves as CUDA graphs (default), 0 never
- *   "resident"     1 (default): a C_t = 1 solve whose image fits the GPU's shared memory runs as ONE
- *                  kernel with the image resident on chip; 0: per-pass kernels
  *   "row_update"   1 Eq. (3) step fused into the next iteration's first row pass (default)
  *   "col_rows"     0 auto (default), 32 or 40: rows per warp segment of the C_t = 1 column kernel
  *   "col_cluster"  0 auto (default), 1..16: forced column-kernel cluster size

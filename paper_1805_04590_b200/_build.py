@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdts_b200.so")
-SOURCES = ["k_misc.cu", "k_row.cu", "k_col.cu", "k_colc.cu", "k_resident.cu", "k_box.cu", "dts_comm.cu", "dts_capi.cu"]
+SOURCES = ["k_misc.cu", "k_row.cu", "k_col.cu", "k_colc.cu", "k_box.cu", "dts_comm.cu", "dts_capi.cu"]
 HEADERS = ["dts_device.cuh", "dts_launch.h", "dts_comm.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

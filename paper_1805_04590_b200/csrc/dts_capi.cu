@@ -73,7 +73,6 @@ struct Options {
     std::atomic<int> col_kernel{0};   // 0: cluster kernel when the column fits, 1: decoupled kernel (k_col.cu)
     std::atomic<int> band_scheme{0};  // 0: edge fix-up when bands are tall enough, 1: TUPLE/APPLY, 2: decoupled
     std::atomic<int> graphs{1};       // replay repeated identical solves as CUDA graphs
-    std::atomic<int> resident{0};     // one SMEM-resident kernel per solve for C_t = 1 images that fit
     std::atomic<int> row_update{1};   // Eq. (3) step fused into the next iteration's first row pass
     std::atomic<int> col_rows{0};     // column kernel rows per warp segment: 0 auto, 32 or 40 (C_t = 1)
     std::atomic<int> col_cluster{0};  // column kernel cluster size: 0 auto, else forced (experiments)
@@ -146,10 +145,6 @@ struct dts_ctx {
     std::vector<uintptr_t> graph_seen;  // key of the last eager solve: a repeat is captured
     int64_t graph_launches = 0;
     cudaStream_t cap_stream = nullptr;
-    // SMEM-resident solve (k_resident.cu): epoch-tagged tile map records in L2 (zero-initialised)
-    float* p_maps = nullptr;
-    size_t p_maps_cap = 0;
-    unsigned int p_epoch = 1;
     // per-iteration ||g||_inf (dts_solve_opts.resid_inf_out), as float bits
     unsigned int* resid = nullptr;
     int resid_cap = 0;
@@ -166,12 +161,12 @@ namespace {
 enum Family {
     F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
     F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_FILL, F_BOX_PREP, F_BOX_ROW, F_BOX_COL, F_COEF,
-    F_PERSIST, F_COUNT
+    F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
                                      "rank_compose", "row_update", "confidence", "stereo_update", "link_fill",
-                                     "box_windows", "box_row", "box_col", "edge_profiles", "solve_resident"};
+                                     "box_windows", "box_row", "box_col", "edge_profiles"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -583,16 +578,12 @@ dts_status dts_set_option(const char* name, int32_t value) {
     if (n == "col_kernel" && (value == 0 || value == 1)) o.col_kernel = value;
     else if (n == "band_scheme" && value >= 0 && value <= 2) o.band_scheme = value;
     else if (n == "graphs" && (value == 0 || value == 1)) o.graphs = value;
-    else if (n == "resident" && (value == 0 || value == 1)) o.resident = value;
     else if (n == "row_update" && (value == 0 || value == 1)) o.row_update = value;
     else if (n == "col_rows" && (value == 0 || value == 32 || value == 40)) o.col_rows = value;
     else if (n == "col_cluster" && value >= 0 && value <= 16) o.col_cluster = value;
     else return DTS_E_ARG;
     return DTS_OK;
 }
-
-// debug hook (not in include/dts.h): phase timeline of the SMEM-resident kernel
-void dts_debug_resident_timers(unsigned long long* device_buf, int32_t cta) { dts::set_resident_timers(device_buf, cta); }
 
 int32_t dts_get_option(const char* name) {
     if (!name) return -1;
@@ -601,7 +592,6 @@ int32_t dts_get_option(const char* name) {
     if (n == "col_kernel") return o.col_kernel;
     if (n == "band_scheme") return o.band_scheme;
     if (n == "graphs") return o.graphs;
-    if (n == "resident") return o.resident;
     if (n == "row_update") return o.row_update;
     if (n == "col_rows") return o.col_rows;
     if (n == "col_cluster") return o.col_cluster;
@@ -1215,12 +1205,6 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         if (cpf.kind != 1 && plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu) != cudaSuccess) return DTS_E_SHAPE;
         cudaGetLastError();
     }
-    // one SMEM-resident kernel for C_t = 1 images that fit the GPU's shared memory (k_resident.cu)
-    ResidentPlan pp{};
-    const bool resident = !is_box && !ctx->comm && ctx->A1y && iterations > 0 && opts_g().resident.load() &&
-                         plan_resident(g, Ct, ctx->N, ctx->num_sms, &pp) == cudaSuccess;
-    cudaGetLastError();
-
     const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),
                   ko = classify(out, ctx->device), kr = want_resid ? classify(resid_out, ctx->device) : PTR_DEVICE;
     if (kt == PTR_BAD || kc == PTR_BAD || ko == PTR_BAD || kr == PTR_BAD) return DTS_E_ARG;
@@ -1275,24 +1259,6 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         if ((st = ensure_solver_state(ctx, Ct, s)) != DTS_OK) return st;
         if ((st = ensure_col_scratch(ctx, cpf, s)) != DTS_OK) return st;
         if ((st = ensure_col_scratch(ctx, cpu, s)) != DTS_OK) return st;
-        if (resident) {
-            const size_t nmaps = (size_t)pp.grid * 32 * pp.MAPN;  // 16-byte records {P, epoch, B, epoch}
-            const uint64_t need = (uint64_t)ctx->N * (uint64_t)iterations + 2;
-            if (ctx->p_maps_cap < nmaps || (uint64_t)ctx->p_epoch + need >= 0xF0000000ull) {
-                if (ctx->p_maps_cap < nmaps) {
-                    if (ctx->p_maps) cudaFreeAsync(ctx->p_maps, s);
-                    ctx->p_maps = nullptr;
-                    ctx->p_maps_cap = 0;
-                    if ((e = cudaMallocAsync((void**)&ctx->p_maps, nmaps * sizeof(float), s)) != cudaSuccess)
-                        return cuda_fail(e);
-                    ctx->p_maps_cap = nmaps;
-                }
-                // fresh records (epochs restart) when first allocated or when the epochs would wrap
-                if ((e = cudaMemsetAsync(ctx->p_maps, 0, ctx->p_maps_cap * sizeof(float), s)) != cudaSuccess)
-                    return cuda_fail(e);
-                ctx->p_epoch = 1;
-            }
-        }
         auto enqueue = [&](cudaStream_t s) -> dts_status {
             dts_status st;
             const double px = (double)g.H * g.W;
@@ -1300,15 +1266,6 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                 return launch_prologue(t_d, c_d, Ct, g, ctx->S, ctx->Sy, support_mode, ctx->Z, ctx->T, ctx->chat, s);
             });
             if (st != DTS_OK) return st;
-            if (resident) {  // the whole iteration loop in one cooperative launch, image resident in SMEM
-                const unsigned ep = ctx->p_epoch;
-                st = run_launch(ctx, F_PERSIST, px * iterations * (2.0 * ctx->N + 1) * 12.0, s, [&] {
-                    return launch_resident(pp, g, ctx->N, iterations, ctx->kc.data(), lambda, step, ctx->Z, ctx->T,
-                                           ctx->chat, ctx->dx, ctx->A1y, o_d, resid, ctx->p_maps, ep, s);
-                });
-                if (st == DTS_OK) ctx->p_epoch += (unsigned)ctx->N * (unsigned)iterations + 1u;
-                return st;
-            }
             const double row_bytes = px * (8.0 * Ct + 4);
             const double upd_bytes = px * (16.0 * Ct + 8);  // X, d, Z, T, chat in; Z out
             if (is_box) {  // R25: N x (box rows, box columns), ping-pong X2 <-> X, then Eq. (3)
@@ -1406,7 +1363,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         // Replay a captured graph of the whole launch sequence when the same solve is issued
         // again (small images are launch-bound).  Only on the cluster column path or the box
         // path (no per-launch epochs), with device buffers and the profiler off.
-        const bool use_graph = opts_g().graphs.load() && !resident && !any_host && !profiler_on() && !ctx->comm &&
+        const bool use_graph = opts_g().graphs.load() && !any_host && !profiler_on() && !ctx->comm &&
                                (is_box || cpf.kind == 1);
         std::vector<uintptr_t> key;
         if (use_graph) {
@@ -1648,7 +1605,6 @@ void dts_destroy(dts_ctx* ctx) {
     if (ctx->counters) cudaFreeAsync(ctx->counters, s);
     if (ctx->tuples) cudaFreeAsync(ctx->tuples, s);
     if (ctx->flags) cudaFreeAsync(ctx->flags, s);
-    if (ctx->p_maps) cudaFreeAsync(ctx->p_maps, s);
     if (ctx->resid) cudaFreeAsync(ctx->resid, s);
     if (ctx->win) cudaFreeAsync(ctx->win, s);
     for (float* q : ctx->edge_gam)

@@ -23,6 +23,15 @@ __device__ __forceinline__ float coef_pow(float a1, int nsq) {
     return a1;
 }
 
+// ---- programmatic dependent launch (PDL) ----------------------------------------------
+// The hot-path kernels are launched with cudaLaunchAttributeProgrammaticStreamSerialization:
+// each lets its successor be scheduled as soon as all its CTAs run (pdl_trigger), and waits for
+// its predecessor's completion and memory flush before touching any data (pdl_wait), so the
+// successor's launch processing and CTA setup overlap the predecessor's tail.  Both are no-ops
+// for a launch without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- affine maps y_out = P * y_in + B[v] (one shared P, NV offsets) -------------------
 template <int NV>
 struct Aff {

@@ -5,6 +5,25 @@
 
 namespace dts {
 
+// launch `kern` on `s` with programmatic stream serialization (see pdl_trigger / pdl_wait)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 // MODE_TUPLE (cluster column kernel, row-band mode): only the rank band's 5-tuple per column
 enum PassMode : int { MODE_FILTER = 0, MODE_UPDATE = 1, MODE_SUPPORT = 2, MODE_ROWUPD = 3, MODE_TUPLE = 4 };
 // column-pass phases (row-band mode): FULL = single band set; TUPLE = emit the aggregate
@@ -98,27 +117,6 @@ cudaError_t launch_update_stereo(const float* X, float* Z, const float* T, const
 // Depth-SR front end: bicubic target and bump confidence, (h f) x (w f).
 cudaError_t launch_sr_prepare(const float* low, int64_t h, int64_t w, int f, float* target, float* conf,
                               cudaStream_t s);
-
-// SMEM-resident solve (k_resident.cu): the whole iteration loop of a C_t = 1 solve in one
-// cooperative launch, the image cut into TR x TC tiles (TH x TW, TW = 32 CG) held in the shared
-// memory of one CTA each; only the filter carries cross tiles (maps + epoch flags in L2).
-// cudaErrorNotSupported when the image does not fit.
-struct ResidentPlan {
-    int CG, TW, TH, THp, TC, TR, MAPN, grid, threads;
-    size_t smem;
-};
-cudaError_t plan_resident(const Geometry& g, int Ct, int N, int num_sms, ResidentPlan* plan);
-// Z0 (initial state), T, chat, dx: context planes; A1y: a_1^{d_y} rows 0..H; kc[i]: row exponent
-// of pass i; out: H x W row-major; resid (nullable): [iters] ||g_k||_inf as float bits, zeroed
-// by the caller; maps >= grid * 32 * MAPN floats (16-byte aligned), zeroed once; epoch0: fresh
-// base (records carry epoch0 + k N + i; the caller advances it by N iters + 1)
-cudaError_t launch_resident(const ResidentPlan& plan, const Geometry& g, int N, int iters, const float* kc, float lam,
-                            float step, const float* Z0, const float* T, const float* chat, const float* dx,
-                            const float* A1y, float* out, unsigned* resid, float* maps, unsigned epoch0,
-                            cudaStream_t s);
-
-// debug: 64 %globaltimer stamps of CTA `cta` of the resident kernel (nullptr: off)
-void set_resident_timers(unsigned long long* t, int cta);
 
 // dts_set_option("col_cluster") (experiments): forced column-kernel cluster size, 0 = auto
 int option_col_cluster();

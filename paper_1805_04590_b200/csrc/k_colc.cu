@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
         if (HASX) tma_prefetch_desc(&tm_x);
     }
     cluster_sync_all();  // every exchange barrier of the cluster is initialised and armed
+    pdl_trigger();
+    pdl_wait();  // the previous kernel's output (this pass's input X) is complete
 
     // lane 0 of warp q: TMA boxes of segment q of `tile` into the landing zone (every warp
     // issues its own segment's loads, so no warp carries the whole tile's issue)
@@ -542,6 +544,8 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
         if (HASX) tma_prefetch_desc(&tm_x);
     }
     cluster_sync_all();  // every exchange barrier of the cluster is initialised and armed
+    pdl_trigger();
+    pdl_wait();
 
     auto stage_seg = [&](int tile, int q) {  // lane 0 of warp q: segment q of `tile`
         const int col0 = tile * TW;
@@ -846,8 +850,44 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     return fn;
 }
 
+// Tensor maps are pure functions of their encode arguments; the column passes of a solve reuse
+// the same few (X and the coefficient plane), so they are encoded once and cached (the encode
+// is host work on every eager launch otherwise).
+struct TmapKey {
+    const void* base;
+    int64_t pitch, H, planes;
+    int rank, box_rows;
+    bool operator==(const TmapKey& o) const {
+        return base == o.base && pitch == o.pitch && H == o.H && planes == o.planes && rank == o.rank &&
+               box_rows == o.box_rows;
+    }
+};
+
+static bool tmap_encode(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int64_t planes, int rank,
+                        int box_rows);
+
 static bool tmap(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int64_t planes, int rank,
                  int box_rows = colc::LS) {
+    static std::mutex mu;
+    static std::vector<std::pair<TmapKey, CUtensorMap>> cache;  // most recent last, <= 64 entries
+    const TmapKey key{base, pitch, H, planes, rank, box_rows};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto it = cache.rbegin(); it != cache.rend(); ++it)
+            if (it->first == key) {
+                *m = it->second;
+                return true;
+            }
+    }
+    if (!tmap_encode(m, base, pitch, H, planes, rank, box_rows)) return false;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= 64) cache.erase(cache.begin());
+    cache.emplace_back(key, *m);
+    return true;
+}
+
+static bool tmap_encode(CUtensorMap* m, const void* base, int64_t pitch, int64_t H, int64_t planes, int rank,
+                        int box_rows) {
     auto enc = encoder();
     if (!enc) return false;
     cuuint64_t dims[3] = {(cuuint64_t)pitch, (cuuint64_t)H, (cuuint64_t)planes};
@@ -1078,13 +1118,15 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     cfg.blockDim = dim3((unsigned)plan.threads, 1, 1);
     cfg.dynamicSmemBytes = plan.smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = (unsigned)plan.CB;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (dts_device.cuh)
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     void* args[] = {&tx, &td, &p};
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return e;

@@ -231,6 +231,8 @@ __global__ void __launch_bounds__(256) k_prologue(const float* __restrict__ targ
                                                   const float* __restrict__ Sy, int support_mode,
                                                   float* __restrict__ Z, float* __restrict__ T,
                                                   float* __restrict__ chat) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t per_row = g.pitch / 4;
     const int64_t n = g.H * per_row;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -282,10 +284,10 @@ cudaError_t launch_prologue(const float* target, const float* conf, int Ct, cons
     if (blocks < 1) blocks = 1;
     const bool vec = Ct == 1 && g.W % 4 == 0 && ((uintptr_t)target % 16 == 0) && ((uintptr_t)conf % 16 == 0);
     if (vec)
-        k_prologue<true><<<(unsigned)blocks, 256, 0, s>>>(target, conf, Ct, g, S, Sy, support_mode, Z, T, chat);
-    else
-        k_prologue<false><<<(unsigned)blocks, 256, 0, s>>>(target, conf, Ct, g, S, Sy, support_mode, Z, T, chat);
-    return cudaGetLastError();
+        return launch_pdl(k_prologue<true>, dim3((unsigned)blocks), dim3(256), 0, s, target, conf, Ct, g, S, Sy,
+                          support_mode, Z, T, chat);
+    return launch_pdl(k_prologue<false>, dim3((unsigned)blocks), dim3(256), 0, s, target, conf, Ct, g, S, Sy,
+                      support_mode, Z, T, chat);
 }
 
 // K4b: the Eq. (3) step as a streaming kernel, used after the
@@ -296,6 +298,8 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X, flo
                                                 const float* __restrict__ T, const float* __restrict__ chat,
                                                 int Ct, Geometry g, float lam, float step,
                                                 float* __restrict__ out_hwc, unsigned* __restrict__ resid) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t per_row = g.pitch / 4;
     const int64_t n = g.H * per_row;
     float gmax = 0.f;  // ||g||_inf of this step (K8), when resid is requested
@@ -343,8 +347,8 @@ cudaError_t launch_update(const float* X, float* Z, const float* T, const float*
     const int64_t cap = (int64_t)num_sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    k_update<<<(unsigned)blocks, 256, 0, s>>>(X, Z, T, chat, Ct, g, lam, step, out_hwc, resid);
-    return cudaGetLastError();
+    return launch_pdl(k_update, dim3((unsigned)blocks), dim3(256), 0, s, X, Z, T, chat, Ct, g, lam, step, out_hwc,
+                      resid);
 }
 
 // opt-in input validation: counters[0] = non-finite target/confidence values,
@@ -439,6 +443,8 @@ __global__ void __launch_bounds__(256) k_update_stereo(const float* __restrict__
                                                        const float* __restrict__ right, int Cgr, Geometry g,
                                                        float lam, float step, float gamma, float eps,
                                                        float* __restrict__ out) {
+    pdl_trigger();
+    pdl_wait();
     const int Cg = CG > 0 ? CG : Cgr;
     const float e2 = eps * eps;
     for (int64_t r = blockIdx.y; r < g.H; r += gridDim.y) {
@@ -479,9 +485,15 @@ cudaError_t launch_update_stereo(const float* X, float* Z, const float* T, const
     const int64_t bx = (g.W + 255) / 256;
     dim3 grid((unsigned)(bx < 64 ? bx : 64), (unsigned)(g.H < 8192 ? g.H : 8192), 1);
     switch (Cg) {
-        case 1: k_update_stereo<1><<<grid, 256, 0, s>>>(X, Z, T, chat, left, right, Cg, g, lam, step, gamma, eps, out); break;
-        case 3: k_update_stereo<3><<<grid, 256, 0, s>>>(X, Z, T, chat, left, right, Cg, g, lam, step, gamma, eps, out); break;
-        default: k_update_stereo<0><<<grid, 256, 0, s>>>(X, Z, T, chat, left, right, Cg, g, lam, step, gamma, eps, out);
+        case 1:
+            return launch_pdl(k_update_stereo<1>, grid, dim3(256), 0, s, X, Z, T, chat, left, right, Cg, g, lam, step,
+                              gamma, eps, out);
+        case 3:
+            return launch_pdl(k_update_stereo<3>, grid, dim3(256), 0, s, X, Z, T, chat, left, right, Cg, g, lam, step,
+                              gamma, eps, out);
+        default:
+            return launch_pdl(k_update_stereo<0>, grid, dim3(256), 0, s, X, Z, T, chat, left, right, Cg, g, lam, step,
+                              gamma, eps, out);
     }
     return cudaGetLastError();
 }

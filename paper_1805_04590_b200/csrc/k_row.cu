@@ -119,6 +119,8 @@ __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
         mbar_init(&bar[1], 1);
         fence_mbar_init();
     }
+    pdl_trigger();
+    pdl_wait();  // the previous kernel's output (the row input, Z / T / chat) is complete
     __syncthreads();
 
     auto issue = [&](int grp, int b) {
@@ -391,8 +393,7 @@ template <int L, int CT, int MODE>
 static cudaError_t launch_t(const RowPlan& plan, const RowParams& p, cudaStream_t s) {
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k_row_pass<L, CT, MODE>), plan.smem);
     if (e != cudaSuccess) return e;
-    k_row_pass<L, CT, MODE><<<plan.grid, plan.threads, plan.smem, s>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(k_row_pass<L, CT, MODE>, dim3(plan.grid), dim3(plan.threads), plan.smem, s, p);
 }
 
 template <int L, int MODE>

@@ -81,15 +81,11 @@ SHAPES = [(1, 1), (1, 7), (7, 1), (2, 2), (31, 33), (33, 31), (32, 32), (61, 97)
           (12000, 33)]
 
 
-@pytest.mark.parametrize("resident", [1, 0])
 @pytest.mark.parametrize("H,W", SHAPES)
-def test_edge_shapes_parity(H, W, resident):
-    """Every shape on the default path (the SMEM-resident kernel where the image fits) and on
-    the per-pass streaming kernels (option resident = 0)."""
+def test_edge_shapes_parity(H, W):
     g, t, c = random_problem(H, W, 3, 1, seed=7 * H + W)
     iters = 3 if H * W > 100000 else 6
-    with dts.options(resident=resident):
-        check(g, t, c, 5.0, 0.2, 3, 0.99, iters)
+    check(g, t, c, 5.0, 0.2, 3, 0.99, iters)
 
 
 @pytest.mark.parametrize("Ct", [2, 3, 4])
@@ -262,7 +258,7 @@ def test_fallback_column_kernel_parity(H, W, Ct):
     """The decoupled band-tuple column kernel (used when a column does not fit a cluster)
     forced for ordinary shapes (option col_kernel = 1), Eq. (3) in its write-out."""
     g, t, c = random_problem(H, W, 3, Ct, seed=H + 3 * W)
-    with dts.options(col_kernel=1, resident=0):
+    with dts.options(col_kernel=1):
         check(g, t, c, 6.0, 0.2, 3, 0.99, 5)
 
 
@@ -271,7 +267,7 @@ def test_separate_update_kernel_parity(H, W, Ct):
     """The cluster column kernel with the Eq. (3) step as its own streaming kernel every
     iteration (option row_update = 0) instead of inside the next row pass."""
     g, t, c = random_problem(H, W, 3, Ct, seed=H + 5 * W)
-    with dts.options(row_update=0, resident=0):
+    with dts.options(row_update=0):
         check(g, t, c, 6.0, 0.2, 3, 0.99, 5)
 
 
