@@ -83,6 +83,9 @@ def measured_peaks():
 
 def spawn_ranks(args) -> int:
     """--gpus N > 1 outside torchrun: re-launch under torch.distributed.run, one rank per GPU."""
+    import torch
+    if torch.cuda.device_count() < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} GPU(s) visible")
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
@@ -412,6 +415,12 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return spawn_ranks(args)
 
+    # the JSON line is the only thing on stdout: libraries (NCCL prints its version at communicator
+    # init) write to stderr while this leg runs
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+
     import torch
     import paper_1805_04590_b200 as dts
 
@@ -610,7 +619,8 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(round(launches_per_step * args.steps)),
             "gpu_launches_per_step": launches_per_step, "clocks": clk, "split": split, "parity": parity,
             "profiled_ms_per_step": p_ms, "extras": extras}
-    print(json.dumps(line), flush=True)
+    sys.stdout.flush()
+    os.write(json_fd, (json.dumps(line) + "\n").encode())
     if comm:
         dts.dts_comm_destroy(comm)
     if tdist is not None:
