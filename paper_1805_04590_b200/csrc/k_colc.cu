@@ -291,17 +291,21 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
         if (c == 0 && tile + nclusters < p.ntiles) stage_seg(tile + nclusters, s);
 
         // ---- 2. causal fold, segment scan, band total ----
+        // Pin = a[1] ... a[LSV-1] serves both maps: the causal product is a[0] Pin, the
+        // anticausal one (the step at j uses a[j + 1]) Pin anext
+        float Pin = 1.f;
         {
             Aff<NV> m = aff_identity<NV>();
 #pragma unroll
             for (int j = 0; j < LSV; ++j) {
-                m.P *= a[j];
+                if (j > 0) Pin *= a[j];
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     if constexpr (HASX) m.B[v] = fmaf(a[j], m.B[v] - xv[v][j], xv[v][j]);
                     else m.B[v] = fmaf(a[j], m.B[v], 1.f);
                 }
             }
+            m.P = a[0] * Pin;
             segF[(0 * S + s) * (TW + 1) + c] = m.P;
 #pragma unroll
             for (int v = 0; v < NV; ++v) segF[((1 + v) * S + s) * (TW + 1) + c] = m.B[v];
@@ -345,23 +349,33 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
             float Q = 1.f, E[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) E[v] = 0.f;
+            if constexpr (HASX) {
+                // exact causal apply, then the anticausal map of the segment folded bottom-up
+                // (E = a_{j+1} (E - y_j) + y_j: two instructions per row and channel)
 #pragma unroll
-            for (int j = 0; j < LSV; ++j) {
-                const float an = (j + 1 < LSV) ? a[j + 1] : anext;
-                if constexpr (HASX) {
-                    const float qb = Q * (1.f - an);
+                for (int j = 0; j < LSV; ++j) {
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
                         y[v] = fmaf(a[j], y[v] - xv[v][j], xv[v][j]);
                         xv[v][j] = y[v];
-                        E[v] = fmaf(qb, y[v], E[v]);
                     }
-                } else {
+                }
+#pragma unroll
+                for (int j = LSV - 1; j >= 0; --j) {
+                    const float an = (j + 1 < LSV) ? a[j + 1] : anext;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) E[v] = fmaf(an, E[v] - xv[v][j], xv[v][j]);
+                }
+                Q = Pin * anext;
+            } else {
+#pragma unroll
+                for (int j = 0; j < LSV; ++j) {
+                    const float an = (j + 1 < LSV) ? a[j + 1] : anext;
                     y[0] = fmaf(a[j], y[0], 1.f);
                     xv[0][j] = y[0];
                     E[0] += Q;
+                    Q *= an;
                 }
-                Q *= an;
             }
             segR[(0 * S + s) * (TW + 1) + c] = Q;
 #pragma unroll
