@@ -293,11 +293,13 @@ cudaError_t launch_prologue(const float* target, const float* conf, int Ct, cons
 // K4b: the Eq. (3) step as a streaming kernel, used after the
 // cluster column kernel:  Z <- Z - step [lambda (Z - zbar) + chat (Z - T)], zbar = X;
 // on the last iteration the result goes to the HWC output instead of Z.
-// One thread per 4 consecutive pixels of a row (float4 loads of every plane).
+// One thread per 4 consecutive pixels of a row (float4 loads of every plane); the HWC output of
+// those 4 pixels is 4 CT consecutive floats, written as CT float4 stores when 16-byte aligned.
+template <int CT>
 __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X, float* __restrict__ Z,
                                                 const float* __restrict__ T, const float* __restrict__ chat,
-                                                int Ct, Geometry g, float lam, float step,
-                                                float* __restrict__ out_hwc, unsigned* __restrict__ resid) {
+                                                Geometry g, float lam, float step, float* __restrict__ out_hwc,
+                                                unsigned* __restrict__ resid) {
     pdl_trigger();
     pdl_wait();
     const int64_t per_row = g.pitch / 4;
@@ -308,29 +310,40 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X, flo
         const int64_t c4 = (i - r * per_row) * 4;
         if (c4 >= g.W) continue;
         const int64_t o = r * g.pitch + c4;
-        const float4 ch = __ldg(reinterpret_cast<const float4*>(chat + o));
-        for (int v = 0; v < Ct; ++v) {
+        const float4 ch4 = __ldg(reinterpret_cast<const float4*>(chat + o));
+        const float ch[4] = {ch4.x, ch4.y, ch4.z, ch4.w};
+        float zn[4][CT];  // [pixel][channel]
+#pragma unroll
+        for (int v = 0; v < CT; ++v) {
             const int64_t ov = v * g.plane + o;
-            const float4 zb = __ldg(reinterpret_cast<const float4*>(X + ov));
-            const float4 zo = *reinterpret_cast<const float4*>(Z + ov);
-            const float4 tv = __ldg(reinterpret_cast<const float4*>(T + ov));
-            float4 zn;
-            zn.x = fmaf(-step, fmaf(lam, zo.x - zb.x, ch.x * (zo.x - tv.x)), zo.x);
-            zn.y = fmaf(-step, fmaf(lam, zo.y - zb.y, ch.y * (zo.y - tv.y)), zo.y);
-            zn.z = fmaf(-step, fmaf(lam, zo.z - zb.z, ch.z * (zo.z - tv.z)), zo.z);
-            zn.w = fmaf(-step, fmaf(lam, zo.w - zb.w, ch.w * (zo.w - tv.w)), zo.w);
-            if (resid) {
-                const float gg[4] = {fmaf(lam, zo.x - zb.x, ch.x * (zo.x - tv.x)), fmaf(lam, zo.y - zb.y, ch.y * (zo.y - tv.y)),
-                                     fmaf(lam, zo.z - zb.z, ch.z * (zo.z - tv.z)), fmaf(lam, zo.w - zb.w, ch.w * (zo.w - tv.w))};
-                for (int u = 0; u < 4; ++u)
-                    if (c4 + u < g.W) gmax = fmaxf(gmax, fabsf(gg[u]));
+            const float4 zb4 = __ldg(reinterpret_cast<const float4*>(X + ov));
+            const float4 zo4 = *reinterpret_cast<const float4*>(Z + ov);
+            const float4 tv4 = __ldg(reinterpret_cast<const float4*>(T + ov));
+            const float zb[4] = {zb4.x, zb4.y, zb4.z, zb4.w};
+            const float zo[4] = {zo4.x, zo4.y, zo4.z, zo4.w};
+            const float tv[4] = {tv4.x, tv4.y, tv4.z, tv4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float gr = fmaf(lam, zo[u] - zb[u], ch[u] * (zo[u] - tv[u]));  // Eq. (3)
+                zn[u][v] = fmaf(-step, gr, zo[u]);
+                if (resid && c4 + u < g.W) gmax = fmaxf(gmax, fabsf(gr));
             }
-            if (out_hwc) {
-                const float zz[4] = {zn.x, zn.y, zn.z, zn.w};
-                for (int u = 0; u < 4; ++u)
-                    if (c4 + u < g.W) out_hwc[(r * g.W + c4 + u) * Ct + v] = zz[u];
+            if (!out_hwc) *reinterpret_cast<float4*>(Z + ov) = make_float4(zn[0][v], zn[1][v], zn[2][v], zn[3][v]);
+        }
+        if (out_hwc) {
+            float* dst = out_hwc + (r * g.W + c4) * CT;
+            if (c4 + 3 < g.W && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                const float* f = &zn[0][0];  // 4 CT consecutive values, pixel-major = HWC
+#pragma unroll
+                for (int q = 0; q < CT; ++q)
+                    reinterpret_cast<float4*>(dst)[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
             } else {
-                *reinterpret_cast<float4*>(Z + ov) = zn;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (c4 + u < g.W) {
+#pragma unroll
+                        for (int v = 0; v < CT; ++v) dst[u * CT + v] = zn[u][v];
+                    }
             }
         }
     }
@@ -347,8 +360,14 @@ cudaError_t launch_update(const float* X, float* Z, const float* T, const float*
     const int64_t cap = (int64_t)num_sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    return launch_pdl(k_update, dim3((unsigned)blocks), dim3(256), 0, s, X, Z, T, chat, Ct, g, lam, step, out_hwc,
-                      resid);
+    const dim3 grid((unsigned)blocks), block(256);
+    switch (Ct) {
+        case 1: return launch_pdl(k_update<1>, grid, block, 0, s, X, Z, T, chat, g, lam, step, out_hwc, resid);
+        case 2: return launch_pdl(k_update<2>, grid, block, 0, s, X, Z, T, chat, g, lam, step, out_hwc, resid);
+        case 3: return launch_pdl(k_update<3>, grid, block, 0, s, X, Z, T, chat, g, lam, step, out_hwc, resid);
+        case 4: return launch_pdl(k_update<4>, grid, block, 0, s, X, Z, T, chat, g, lam, step, out_hwc, resid);
+    }
+    return cudaErrorInvalidValue;
 }
 
 // opt-in input validation: counters[0] = non-finite target/confidence values,

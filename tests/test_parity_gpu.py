@@ -396,3 +396,26 @@ def test_forty_row_segments_parity():
     check(g, t, c, 6.0, 0.15, 3, 0.99, 3)
     with dts.options(col_rows=32):
         check(g, t, c, 6.0, 0.15, 3, 0.99, 3)
+
+
+def test_guide_beyond_2_31_elements():
+    """SURVEY 7 / 8(c) 64-bit indexing: a guide of more than 2^31 elements (10000 x 13500 x 16 =
+    2.16e9 floats, 8.6 GB); d_x and d_y of the last rows (element offsets past 2^31) against O1
+    evaluated on those rows (d_x of a row depends on that row only, d_y on it and the row above)."""
+    H, W, C = 10000, 13500, 16
+    assert H * W * C > 2 ** 31
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    g = torch.rand((H, W, C), device="cuda", generator=gen, dtype=torch.float32)
+    rows = [0, 1, H // 2, H - 2, H - 1]
+    with dts.Solver(g, 8.0, 0.2, 3) as s:
+        dx, dy = s.read(dts.DTS_BUF_DX), s.read(dts.DTS_BUF_DY)
+    for r in rows:
+        lo = max(r - 1, 0)
+        sl = g[lo:r + 1].cpu().numpy()
+        dx_r, dy_r = oracle.distances(sl, 8.0, 0.2)
+        for got, ref in ((dx[r], dx_r[r - lo]), (dy[r], dy_r[r - lo])):
+            inf = np.isinf(ref)  # the +inf sentinels: column 0 of d_x, row 0 of d_y
+            assert np.array_equal(np.isinf(got), inf)
+            np.testing.assert_allclose(got[~inf], ref[~inf], rtol=2e-6)
+    del g
+    torch.cuda.empty_cache()
