@@ -53,7 +53,10 @@ int main(int argc, char** argv) {
         fprintf(stderr, "dts_create: %s (%s)\n", dts_status_string(st), dts_last_error_string());
         return 4;
     }
-    dts_solve_opts opts = {0.99f, 0, 1}; /* step, support_mode, check_inputs */
+    float* resid = malloc(sizeof(float) * (size_t)(iters > 0 ? iters : 1));
+    if (!resid) return 3;
+    /* step, support_mode, check_inputs, resid_inf_out (per-iteration ||g||_inf, K8) */
+    dts_solve_opts opts = {0.99f, 0, 1, resid};
     st = dts_solve_ex(ctx, target, 1, conf, 0.99f, iters, out, NULL, &opts);
     dts_destroy(ctx);
     if (st != DTS_OK) {
@@ -64,12 +67,13 @@ int main(int argc, char** argv) {
     if (dts_create(guide, H, W, C, -1.0f, 0.2f, 3, NULL, &ctx) != DTS_E_ARG) return 6;
     const char* prefix = argv[5];
     if (dump(prefix, "guide", guide, n * (size_t)C) || dump(prefix, "target", target, n) ||
-        dump(prefix, "conf", conf, n) || dump(prefix, "out", out, n))
+        dump(prefix, "conf", conf, n) || dump(prefix, "out", out, n) || dump(prefix, "resid", resid, (size_t)iters))
         return 7;
     printf("c_solve: %s, %lldx%lld, %d iterations ok\n", dts_version(), (long long)H, (long long)W, iters);
     free(guide);
     free(target);
     free(conf);
     free(out);
+    free(resid);
     return 0;
 }

@@ -103,7 +103,7 @@ def main():
     tag = sys.argv[2]
     launches = os.path.join(src, "launches.csv")
     lines = [f"# ncu summary, {tag}", "",
-             "Workload: `python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu` (C4, 10000x10000, 16-band guide, "
+             "Workload: `python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-extras` (C4, 10000x10000, 16-band guide, "
              "20 iterations) on one B200, `--clock-control none`; commands in profiles/run_profiles.sh.", ""]
     traffic = {}
     if os.path.exists(launches):
@@ -147,6 +147,34 @@ def main():
         for h, (v, u) in met.items():
             lines.append(f"- {h}: {v} {u}")
         lines.append(f"- DRAM traffic per launch: {(rd + wr) / 1e9:.3f} GB")
+        lines.append("")
+    c1 = os.path.join(src, "c1_launches.csv")
+    if os.path.exists(c1):  # launch-gap breakdown of one eager C1 solve (tools/c1_once.py)
+        shutil.copy(c1, os.path.join(HERE, f"{tag}_c1_launches.csv"))
+        per = read_launches(c1)
+        durs = [to_ns(d, "gpu__time_duration.sum") for d in per.values()]
+        fam_t = defaultdict(float)
+        fam_n = defaultdict(int)
+        for (lid, name), d in per.items():
+            key, fam = family(name)
+            fam_t[fam] += to_ns(d, "gpu__time_duration.sum")
+            fam_n[fam] += 1
+        solve_ms = None
+        log = os.path.join(src, "c1_once.log")
+        if os.path.exists(log):
+            for ln in open(log):
+                if "c1_eager_solve_ms" in ln:
+                    solve_ms = json.loads(ln)["c1_eager_solve_ms"]
+        ksum = sum(durs) / 1e6
+        lines += ["## C1 eager solve: kernel time against the event-timed solve", "",
+                  f"{len(durs)} consecutive launches of the steady solve sequence (ncu, serialised, caches flushed "
+                  f"before each launch, so each duration is an upper bound for the L2-resident C1 planes): "
+                  f"{ksum:.3f} ms of kernel time.",
+                  f"The same solve timed with CUDA events without ncu (programmatic dependent launch): "
+                  f"{solve_ms:.3f} ms." if solve_ms else "", "",
+                  "| family | launches | total ms | avg us |", "|---|---|---|---|"]
+        for fam in sorted(fam_t, key=lambda f: -fam_t[f]):
+            lines.append(f"| {fam} | {fam_n[fam]} | {fam_t[fam] / 1e6:.3f} | {fam_t[fam] / fam_n[fam] / 1e3:.1f} |")
         lines.append("")
     with open(os.path.join(HERE, f"{tag}_summary.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")

@@ -40,5 +40,7 @@ def test_c_program_matches_oracle(tmp_path):
     t = np.fromfile(prefix + ".target", np.float32).reshape(H, W)
     c = np.fromfile(prefix + ".conf", np.float32).reshape(H, W)
     out = np.fromfile(prefix + ".out", np.float32).reshape(H, W).astype(np.float64)
-    ref = oracle.solve(g, t, c, 8.0, 0.2, 3, 0.99, iters)
+    ref, diag = oracle.solve(g, t, c, 8.0, 0.2, 3, 0.99, iters, diagnostics=True)
     assert np.max(np.abs(out - ref)) <= 1e-4 * target_range(t)
+    resid = np.fromfile(prefix + ".resid", np.float32).astype(np.float64)  # K8 through the C ABI
+    np.testing.assert_allclose(resid, diag[:, 0], rtol=0, atol=1e-4 * target_range(t))
