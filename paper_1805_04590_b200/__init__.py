@@ -226,6 +226,18 @@ def dts_solve_ex(ctx: int, target, confidence, lam: float, iterations: int, out,
     return out
 
 
+def debug_strips(ctx: int) -> dict:
+    """Row-strip plan of a context (tests / probes; not part of include/dts.h)."""
+    lib = load_library()
+    f = lib.dts_debug_strips
+    f.restype = ctypes.c_int32
+    f.argtypes = [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int32)] * 4
+    hs, cb, gr = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    L3 = (ctypes.c_int32 * 3)()
+    n = f(ctx, ctypes.byref(hs), L3, ctypes.byref(cb), ctypes.byref(gr))
+    return {"strips": n, "HS": hs.value, "L": list(L3), "CB": cb.value, "grid": gr.value}
+
+
 def dts_set_option(name: str, value: int) -> None:
     """Process-wide test / experiment option (include/dts.h); the defaults are the product path."""
     _check(load_library().dts_set_option(name.encode(), int(value)), f"dts_set_option({name}={value})")

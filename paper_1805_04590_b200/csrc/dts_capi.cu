@@ -76,6 +76,9 @@ struct Options {
     std::atomic<int> row_update{1};   // Eq. (3) step fused into the next iteration's first row pass
     std::atomic<int> col_rows{0};     // column kernel rows per warp segment: 0 auto, 32 or 40 (C_t = 1)
     std::atomic<int> col_cluster{0};  // column kernel cluster size: 0 auto, else forced (experiments)
+    std::atomic<int> strip_cluster{0};     // row strips: forced cluster size of the strip plan (0 = auto)
+    std::atomic<int> col_strips{1};   // tall single-context images: C_t = 1 column passes over row strips
+                                      // (0 off, 1 auto, n >= 2: exactly n strips when they fit)
 };
 Options& opts_g() {
     static Options o;
@@ -103,6 +106,13 @@ struct dts_ctx {
     // edge fix-up scheme, per pass (nullptr: band too short, TUPLE/APPLY instead)
     std::vector<float*> edge_gam, edge_theta;  // L x pitch each: Gamma (top rows), Theta (bottom rows)
     std::vector<int> edge_L;
+    // single-GPU row strips for the C_t = 1 FILTER column passes of tall images (DESIGN.md
+    // section 7): the cluster plan over strips, per pass the seam length and edge profiles
+    int vs_n = 0, vs_HS = 0;
+    ColPlan vs_plan{};
+    std::vector<int> vs_L;
+    std::vector<float*> vs_gam, vs_theta;  // [vs_n][L][pitch] each
+    float* vs_edge = nullptr;              // [vs_n][2][1][ntc * 32]: each strip's last / first output row
     int num_sms = 148;
     Geometry g{};
     int C = 0;
@@ -161,12 +171,12 @@ namespace {
 enum Family {
     F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
     F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_FILL, F_BOX_PREP, F_BOX_ROW, F_BOX_COL, F_COEF,
-    F_COUNT
+    F_SEAM, F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
                                      "rank_compose", "row_update", "confidence", "stereo_update", "link_fill",
-                                     "box_windows", "box_row", "box_col", "edge_profiles"};
+                                     "box_windows", "box_row", "box_col", "edge_profiles", "seam_fix"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -274,13 +284,14 @@ dts_status ensure_staging(dts_ctx* ctx, size_t bytes_per_image, cudaStream_t s) 
 }
 
 // column-pass plan: cluster fast path when it fits, else the decoupled band-tuple kernel
-cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan) {
+cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int force_cb = -1) {
     if (opts_g().col_kernel.load() == 0) {
         // C_t >= 2 FILTER: 16-row segments (20 warps per CTA) when the column fits a cluster
-        if (Ct >= 2 && mode == MODE_FILTER && plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 16) == cudaSuccess)
+        if (Ct >= 2 && mode == MODE_FILTER &&
+            plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 16, force_cb) == cudaSuccess)
             return cudaSuccess;
         cudaGetLastError();
-        if (plan_col_cluster(g, Ct, mode, num_sms, plan) == cudaSuccess) {
+        if (plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 32, force_cb) == cudaSuccess) {
             // C_t = 1 FILTER with several tile rounds per launch (throughput-bound): 16 warps
             // x 40-row segments (C4: 0.265 -> 0.249 ms).  One-round images are latency-bound
             // and keep 32-row segments (C1: 12.6 us against 16.8 with 40-row ones).
@@ -290,7 +301,7 @@ cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* 
             const bool want40 = rows ? rows == 40 : rounds >= 4;
             ColPlan p40{};
             if (Ct == 1 && mode == MODE_FILTER && want40 &&
-                plan_col_cluster_ls(g, Ct, mode, num_sms, &p40, 40) == cudaSuccess)
+                plan_col_cluster_ls(g, Ct, mode, num_sms, &p40, 40, force_cb) == cudaSuccess)
                 *plan = p40;
             cudaGetLastError();
             return cudaSuccess;
@@ -581,8 +592,20 @@ dts_status dts_set_option(const char* name, int32_t value) {
     else if (n == "row_update" && (value == 0 || value == 1)) o.row_update = value;
     else if (n == "col_rows" && (value == 0 || value == 32 || value == 40)) o.col_rows = value;
     else if (n == "col_cluster" && value >= 0 && value <= 16) o.col_cluster = value;
+    else if (n == "col_strips" && value >= 0 && value <= 64) o.col_strips = value;
+    else if (n == "strip_cluster" && value >= 0 && value <= 16) o.strip_cluster = value;
     else return DTS_E_ARG;
     return DTS_OK;
+}
+
+// debug hook (not in include/dts.h): the row-strip plan of a context (plan_strips)
+int32_t dts_debug_strips(const dts_ctx* ctx, int32_t* HS, int32_t* L3, int32_t* CB, int32_t* grid) {
+    if (!ctx) return -1;
+    if (HS) *HS = ctx->vs_HS;
+    for (int i = 0; i < 3 && L3; ++i) L3[i] = i < (int)ctx->vs_L.size() ? ctx->vs_L[i] : 0;
+    if (CB) *CB = ctx->vs_plan.CB;
+    if (grid) *grid = (int)ctx->vs_plan.grid.x;
+    return ctx->vs_n;
 }
 
 int32_t dts_get_option(const char* name) {
@@ -595,6 +618,8 @@ int32_t dts_get_option(const char* name) {
     if (n == "row_update") return o.row_update;
     if (n == "col_rows") return o.col_rows;
     if (n == "col_cluster") return o.col_cluster;
+    if (n == "col_strips") return o.col_strips;
+    if (n == "strip_cluster") return o.strip_cluster;
     return -1;
 }
 
@@ -658,6 +683,114 @@ const char* dts_status_string(dts_status s) {
 }
 
 const char* dts_last_error_string(void) { return g_last_error.c_str(); }
+
+// Tall single-context images: a column tile must sit on chip across its
+// cluster, and the clusters a tall column needs (16 CTAs for C4) pack only 7 per GPU (112 of
+// 148 SMs).  Cut the image into row strips whose columns fit smaller clusters, run the C_t = 1
+// FILTER passes over all strips in one launch (zero carry at each strip's top, link below cut)
+// and add the carries at the seams afterwards (k_seam_fix, reading R26).  Chosen at create when
+// the strips use >= 10% more SMs and every pass's measured carry-decay length L (k_edge_length:
+// influence below 2^-26 after L rows) fits twice in the shortest strip.
+static dts_status plan_strips(dts_ctx* ctx, cudaStream_t s) {
+    const Geometry& g = ctx->g;
+    ColPlan base{};
+    if (plan_col(g, 1, MODE_FILTER, ctx->num_sms, &base) != cudaSuccess || base.kind != 1) {
+        cudaGetLastError();
+        return DTS_OK;
+    }
+    // preference (measured on C4, unprofiled 20-iteration solves, tools/strips4.sh): the fewest
+    // strips whose plan covers >= 90% of the SMs and adds >= 10% over one strip (C4: 2 strips of
+    // 5000 rows on 15 clusters of 9, 30.58 ms against 31.18 unstripped; 4 strips x clusters of 4
+    // 30.84; 16 strips x 2 CTAs of 320 rows per SM 31.33 -- its column kernel is the fastest,
+    // 0.204 ms, but 15 seams cost more than that saves)
+    int best_n = 0;
+    ColPlan best{};
+    const int forced = opts_g().col_strips.load();
+    for (int n : {2, 4, 8, 16, 32}) {
+        if (forced >= 2 && n != forced) continue;
+        const int64_t HS = (g.H + n - 1) / n;
+        if (HS < 64 || (n - 1) * HS >= g.H) break;
+        Geometry gs = g;  // planned as n strips side by side: the launch has n times the tiles
+        gs.H = HS;
+        gs.W = g.W * n;
+        gs.pitch = (gs.W + 31) / 32 * 32;
+        gs.plane = HS * gs.pitch;
+        ColPlan ps{};
+        if (plan_col(gs, 1, MODE_FILTER, ctx->num_sms, &ps, opts_g().strip_cluster.load()) != cudaSuccess ||
+            ps.kind != 1) {
+            cudaGetLastError();
+            continue;
+        }
+        const bool wide = ps.grid.x * 10 >= (unsigned)ctx->num_sms * 9 && ps.grid.x * 10 >= base.grid.x * 11;
+        if (wide || forced >= 2) {
+            best_n = n;
+            best = ps;
+            best.HS = (int)HS;
+            break;
+        }
+    }
+    if (!best_n) return DTS_OK;
+    const int n = best_n, HS = best.HS;
+    const int64_t Hlast = g.H - (int64_t)(n - 1) * HS;
+    const int N = ctx->N;
+    cudaError_t e;
+    unsigned* dlen = nullptr;
+    if ((e = cudaMallocAsync((void**)&dlen, 2 * N * sizeof(unsigned), s)) != cudaSuccess ||
+        (e = cudaMemsetAsync(dlen, 0, 2 * N * sizeof(unsigned), s)) != cudaSuccess)
+        return cuda_fail(e);
+    dts_status st = DTS_OK;
+    for (int i = 0; i < N && st == DTS_OK; ++i) {
+        const int64_t worst = (int64_t)std::ceil(26.0 / (double)ctx->kc[i]);
+        const int Lcap = (int)std::min<int64_t>(std::min<int64_t>(worst, Hlast), 1 << 20);
+        for (int b = 0; b < n && st == DTS_OK; ++b) {
+            Geometry gs = g;
+            gs.H = std::min<int64_t>(HS, g.H - (int64_t)b * HS);
+            st = run_launch(ctx, F_COEF, (double)g.W * Lcap * 8.0, s, [&] {
+                return launch_edge_length(ctx->dy + (int64_t)b * HS * g.pitch, gs, Lcap, ctx->kc[i], dlen + 2 * i, s);
+            });
+        }
+    }
+    std::vector<unsigned> len(2 * N, 0);
+    if (st == DTS_OK && ((e = cudaMemcpyAsync(len.data(), dlen, 2 * N * sizeof(unsigned), cudaMemcpyDeviceToHost, s)) !=
+                             cudaSuccess ||
+                         (e = cudaStreamSynchronize(s)) != cudaSuccess))
+        st = cuda_fail(e);
+    cudaFreeAsync(dlen, s);
+    if (st != DTS_OK) return st;
+    std::vector<int> L(N);
+    for (int i = 0; i < N; ++i) {
+        L[i] = (int)std::max<unsigned>(1u, std::max(len[2 * i], len[2 * i + 1]));
+        if (2 * (int64_t)L[i] + 1 > Hlast) return DTS_OK;  // a seam correction would overlap: keep one strip
+    }
+    ctx->vs_gam.assign(N, nullptr);
+    ctx->vs_theta.assign(N, nullptr);
+    for (int i = 0; i < N && st == DTS_OK; ++i) {
+        const size_t bytes = (size_t)n * L[i] * g.pitch * sizeof(float);
+        if ((e = cudaMallocAsync((void**)&ctx->vs_gam[i], bytes, s)) != cudaSuccess ||
+            (e = cudaMallocAsync((void**)&ctx->vs_theta[i], bytes, s)) != cudaSuccess)
+            return cuda_fail(e);
+        for (int b = 0; b < n && st == DTS_OK; ++b) {
+            Geometry gs = g;
+            gs.H = std::min<int64_t>(HS, g.H - (int64_t)b * HS);
+            st = run_launch(ctx, F_COEF, (double)g.W * 2 * L[i] * 12.0, s, [&] {
+                return launch_edge_profiles(ctx->dy + (int64_t)b * HS * g.pitch, gs, L[i], ctx->kc[i],
+                                            ctx->vs_gam[i] + (size_t)b * L[i] * g.pitch,
+                                            ctx->vs_theta[i] + (size_t)b * L[i] * g.pitch, s);
+            });
+        }
+    }
+    if (st != DTS_OK) return st;
+    if ((e = cudaMallocAsync((void**)&ctx->vs_edge, (size_t)n * 2 * ((g.W + 31) / 32) * 32 * sizeof(float), s)) !=
+        cudaSuccess)
+        return cuda_fail(e);
+    ctx->vs_n = n;
+    ctx->vs_HS = HS;
+    ctx->vs_L = L;
+    ctx->vs_plan = best;
+    ctx->vs_plan.ntc = (int)((g.W + 31) / 32);
+    ctx->vs_plan.ntiles = ctx->vs_plan.ntc * n;
+    return DTS_OK;
+}
 
 // Row-band contexts: every rank measures how many rows a carry
 // entering its band edges keeps an influence >= 2^-26 of itself (per pass, and for the
@@ -972,6 +1105,7 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
             });
         }
     }
+    if (st == DTS_OK && !comm && ctx->A1y && opts_g().col_strips.load()) st = plan_strips(ctx, s);
     if (gstage) {
         cudaFreeAsync(gstage, s);
         if (st == DTS_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess) st = cuda_fail(e);
@@ -1293,11 +1427,23 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
             }
             // FILTER column pass i: the cluster kernel on A1 = a_1^{d_y} squared i times when
             // the context holds it, else on d_y
+            const bool strips = Ct == 1 && ctx->vs_n > 1 && cpf.kind == 1 && !ctx->comm && opts_g().col_strips.load();
             auto col_filter = [&](int i) -> cudaError_t {
+                if (strips)  // row strips (plan_strips); the seams are fixed by the launch that follows
+                    return launch_col_cluster(ctx->vs_plan, g, Ct, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr,
+                                              nullptr, s, i, nullptr, nullptr, nullptr, ctx->vs_edge);
                 if (cpf.kind == 1 && ctx->A1y && i < 4)
                     return launch_col_cluster(cpf, g, Ct, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr, nullptr,
                                               s, i);
                 return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
+            };
+            // the seam carries of strip column pass i (plan_strips): the fix-up kernel after it
+            auto seam_fix = [&](int i) -> dts_status {
+                if (!strips) return DTS_OK;
+                return run_launch(ctx, F_SEAM, px * 12.0 * (ctx->vs_n - 1) * 2 * ctx->vs_L[i] / (double)g.H, s, [&] {
+                    return launch_seam_fix(ctx->X, Ct, g, ctx->vs_HS, ctx->vs_n, ctx->vs_L[i], ctx->vs_gam[i],
+                                           ctx->vs_theta[i], ctx->vs_edge, s);
+                });
             };
             // The last column pass of an iteration is a FILTER pass; Eq. (3) of iteration k-1 is
             // applied inside iteration k's first row pass (k_row.cu ROWUPD: Z, T, chat read
@@ -1342,6 +1488,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                         }
                     } else if (!last || split_update) {
                         st = run_launch(ctx, F_COL, row_bytes, s, [&] { return col_filter(i); });
+                        if (st == DTS_OK) st = seam_fix(i);
                         if (st != DTS_OK) return st;
                         if (!last || (rowupd && k + 1 < iterations)) continue;  // the next row pass applies Eq. (3)
                         st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
@@ -1610,6 +1757,11 @@ void dts_destroy(dts_ctx* ctx) {
     for (float* q : ctx->edge_gam)
         if (q) cudaFreeAsync(q, s);
     for (float* q : ctx->edge_theta)
+        if (q) cudaFreeAsync(q, s);
+    for (float* q : ctx->vs_gam)
+        if (q) cudaFreeAsync(q, s);
+    if (ctx->vs_edge) cudaFreeAsync(ctx->vs_edge, s);
+    for (float* q : ctx->vs_theta)
         if (q) cudaFreeAsync(q, s);
     if (ctx->graph_exec) {  // a replay may still be in flight on s
         cudaStreamSynchronize(s);

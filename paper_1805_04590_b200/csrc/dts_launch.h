@@ -63,6 +63,7 @@ cudaError_t launch_row_update(const RowPlan& plan, const Geometry& g, int Ct, co
 struct ColPlan {
     int kind;  // 0: decoupled band-tuple kernel (k_col.cu), 1: cluster kernel (k_colc.cu)
     int TW, CB, HB, S, Ls, nb, ntiles, threads;
+    int HS = 0, ntc = 0;  // cluster kernel over row strips: strip height, column tiles per strip (0: one strip)
     dim3 grid;
     size_t smem;
     size_t tuple_floats, flag_count;  // scratch the launch needs (ColScratch)
@@ -94,13 +95,16 @@ cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int 
 // Returns cudaErrorNotSupported when the shape does not fit (then use plan_col_pass).
 cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
 // ls = 16: 16-row warp segments (FILTER, C_t >= 2, not for row bands); plan->Ls records it
-cudaError_t plan_col_cluster_ls(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int ls);
+// force_cb >= 0: cluster size (0 = auto) instead of the "col_cluster" option
+cudaError_t plan_col_cluster_ls(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int ls,
+                                int force_cb = -1);
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
                                float kc, const UpdateArgs* upd, float* support, cudaStream_t s,
                                int nsq = -1,  // nsq >= 0: d holds A1 (see coef_pow)
                                const float* ext = nullptr,    // APPLY: carries into the rank band [ntiles][2][Ct][32]
                                float* rank_tuples = nullptr,   // TUPLE: [ntiles][2Ct+3][32]
-                               float* edge = nullptr);         // edge scheme: [ntiles][2Ct+1][32]
+                               float* edge = nullptr,          // edge scheme: [ntiles][2Ct+1][32]
+                               float* sedge = nullptr);        // row strips: [strip][2][Ct][ntc*32] edge rows
 
 // Eq. (7) confidence: planar X0 = t, X1 = t^2 from a row-major H x W
 // target; and, after the DTF of both planes, V = max(0, X1 - X0^2), c = exp(-V / (2 sc^2)).
@@ -175,6 +179,10 @@ cudaError_t launch_box_col(const BoxPlan& plan, const Geometry& g, int Ct, const
 // below the band (z(H-1) = y(H-1)), so the bottom carry is z_H - y(H-1)
 cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float kc, float* gam, float* theta,
                                  cudaStream_t s, bool raw = false);
+// row-strip seam fix-up of a FILTER column pass run over nstrips strips of HS rows (zero carries
+// at each strip's top, link below cut); gam / theta: [nstrips][L][pitch] edge profiles
+cudaError_t launch_seam_fix(float* x, int Ct, const Geometry& g, int HS, int nstrips, int L, const float* gam,
+                            const float* theta, const float* sedge, cudaStream_t s);
 // decay lengths of a band's edge carries (top -> len[0], bottom -> len[1], atomicMax; zero them
 // first); d has rows 0..H (row H: the link below the band)
 cudaError_t launch_edge_length(const float* d, const Geometry& g, int Lcap, float kc, unsigned* len, cudaStream_t s);

@@ -38,9 +38,11 @@ struct Params {
     float* x;        // planar state (in; FILTER: out)
     const float* d;  // d_y
     float* support;  // SUPPORT: receives s_y (the solve multiplies it into S in the prologue)
+    float* sedge;    // row strips (nullable): [strip][2][CT][ntc * 32] outputs at each strip's last / first row
     UpdateArgs upd;
     int64_t plane, pitch;
     int H, W, HB, S, CB, ntiles;
+    int HS, ntc;  // row strips (single-GPU FILTER): strip height, column tiles per strip (HS = H: one strip)
     float kc;
     int nsq;  // < 0: d holds distances (a = 2^(-kc d)); >= 0: d holds A1, a = A1^(2^nsq)
 };
@@ -219,17 +221,21 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
 
     // lane 0 of warp q: TMA boxes of segment q of `tile` into the landing zone (every warp
     // issues its own segment's loads, so no warp carries the whole tile's issue)
+    // tile -> (row strip, column tile): a strip of HS rows is filtered with zero carries at its
+    // top and the link below it cut (the seam fix-up adds the carries)
     auto stage_seg = [&](int tile, int q) {
-        const int col0 = tile * TW;
+        const int col0 = (tile % p.ntc) * TW;
+        const int sb = (tile / p.ntc) * p.HS;
         const uint32_t box = (uint32_t)(LSV * TW * sizeof(float));
         const int rq = r0 + q * LSV;
-        const uint32_t bytes = rq < p.H ? box * (1 + (HASX ? NV : 0)) : 0u;
+        const uint32_t bytes = rq < min(p.HS, p.H - sb) ? box * (1 + (HASX ? NV : 0)) : 0u;
         mbar_arrive_expect_tx(&bars[q], bytes);
         if (bytes) {
-            tma_load_2d(ld + q * LSV * TW, &tm_d, col0, rq, &bars[q]);
+            tma_load_2d(ld + q * LSV * TW, &tm_d, col0, sb + rq, &bars[q]);
             if constexpr (HASX) {
 #pragma unroll
-                for (int v = 0; v < NV; ++v) tma_load_3d(lx + (v * HB + q * LSV) * TW, &tm_x, col0, rq, v, &bars[q]);
+                for (int v = 0; v < NV; ++v)
+                    tma_load_3d(lx + (v * HB + q * LSV) * TW, &tm_x, col0, sb + rq, v, &bars[q]);
             }
         }
     };
@@ -237,7 +243,9 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
 
     int k = 0;
     for (int tile = cluster; tile < p.ntiles; tile += nclusters, ++k) {
-        const int col0 = tile * TW;
+        const int col0 = (tile % p.ntc) * TW;
+        const int sb = (tile / p.ntc) * p.HS;  // first row of this tile's strip
+        const int Hs = min(p.HS, p.H - sb);    // rows of the strip
         const int col = col0 + c;
         const bool colok = col < p.W;
 
@@ -248,12 +256,12 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
         float anext = 0.f;
         {
             const int rn = r0 + lo + LSV;
-            if (colok && rn < p.H) anext = __ldg(p.d + (int64_t)rn * p.pitch + col);
+            if (colok && rn < Hs) anext = __ldg(p.d + (int64_t)(sb + rn) * p.pitch + col);
         }
         mbar_wait(&bars[s], (uint32_t)(k & 1));
         float a[LSV];
         float xv[NV][LSV];
-        if (r0 + lo + LSV <= p.H) {
+        if (r0 + lo + LSV <= Hs) {
             // every row of the segment is in the image (warp-uniform): no per-row checks.
             // Lanes past W read the row padding; their values stay in their own column
             // (every step of the pass is per column) and are never stored.
@@ -271,7 +279,7 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
 #pragma unroll
             for (int j = 0; j < LSV; ++j) {
                 const int rr = lo + j;
-                const bool ok = colok && (r0 + rr) < p.H;
+                const bool ok = colok && (r0 + rr) < Hs;
                 a[j] = ok ? coef(ld[rr * TW + c]) : 0.f;
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
         // coefficient linking this segment's last row to the next row: from the
         // landing zone (next segment; it landed before the barrier below) or, for the
         // band's last segment, straight from global (first row of the next band)
-        if (colok && r0 + lo + LSV < p.H) anext = coef(anext);
+        if (colok && r0 + lo + LSV < Hs) anext = coef(anext);
         // this warp's segment is in registers: refill it with the next tile (only this warp
         // reads it, so no CTA barrier; the next tile's shared-memory scratch writes are
         // ordered by the fold barrier below, which every warp passes after this tile)
@@ -434,10 +442,10 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
 
         // ---- 5. write-out straight from registers ----
         {
-            const int nrow = min(LSV, p.H - (r0 + lo));
+            const int nrow = min(LSV, Hs - (r0 + lo));
             if (colok && nrow > 0) {
                 if constexpr (MODE == MODE_FILTER || MODE == MODE_SUPPORT) {
-                    float* base = (MODE == MODE_FILTER ? p.x : p.support) + (int64_t)(r0 + lo) * p.pitch + col;
+                    float* base = (MODE == MODE_FILTER ? p.x : p.support) + (int64_t)(sb + r0 + lo) * p.pitch + col;
                     const int64_t pitch = p.pitch;
                     if (nrow == LSV) {  // full segment: a running pointer, no per-row checks
 #pragma unroll
@@ -454,6 +462,26 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
                                 for (int v = 0; v < NV; ++v) base[v * p.plane + (int64_t)j * pitch] = xv[v][j];
                             }
                     }
+                }
+            }
+            // row strips: the strip's last and first output rows, for the seam fix-up (which must
+            // read them before it corrects the rows around the seam)
+            if (MODE == MODE_FILTER && p.sedge) {
+                const int strip = tile / p.ntc;
+                const int64_t ew = (int64_t)p.ntc * TW, ec = (int64_t)(tile % p.ntc) * TW + c;
+                const int jl = Hs - 1 - (r0 + lo);
+                if (jl >= 0 && jl < LSV) {  // warp-uniform
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        float yl = xv[v][0];
+#pragma unroll
+                        for (int j = 1; j < LSV; ++j) yl = (j == jl) ? xv[v][j] : yl;
+                        p.sedge[((int64_t)(strip * 2 + 0) * NV + v) * ew + ec] = yl;
+                    }
+                }
+                if (r0 + lo == 0) {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) p.sedge[((int64_t)(strip * 2 + 1) * NV + v) * ew + ec] = xv[v][0];
                 }
             }
         }
@@ -1062,9 +1090,9 @@ static cudaError_t plan_col_cluster_uncached(const Geometry& g, int Ct, int mode
     return best_cost >= 0 ? cudaSuccess : cudaErrorNotSupported;
 }
 
-cudaError_t plan_col_cluster_ls(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int ls) {
+cudaError_t plan_col_cluster_ls(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int ls, int force_cb) {
     (void)num_sms;
-    const int fcb = option_col_cluster();  // forced cluster size (experiments; 0 = auto)
+    const int fcb = force_cb >= 0 ? force_cb : option_col_cluster();  // forced cluster size (0 = auto)
     int dev = 0;
     cudaGetDevice(&dev);
     struct Entry {
@@ -1099,8 +1127,9 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
 
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
                                float kc, const UpdateArgs* upd, float* support, cudaStream_t s, int nsq,
-                               const float* ext, float* rank_tuples, float* edge) {
+                               const float* ext, float* rank_tuples, float* edge, float* sedge) {
     colc::BandParams p = {};
+    p.sedge = sedge;
     p.nsq = nsq;
     p.ext = ext;
     p.rank_tuples = rank_tuples;
@@ -1117,6 +1146,8 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     p.S = plan.S;
     p.CB = plan.CB;
     p.ntiles = plan.ntiles;
+    p.HS = plan.HS > 0 ? plan.HS : (int)g.H;
+    p.ntc = plan.ntc > 0 ? plan.ntc : plan.ntiles;
     p.kc = kc;
     CUtensorMap tx, td;
     if (!tmap(&td, d, g.pitch, g.H, 1, 2, plan.Ls)) return cudaErrorInvalidValue;
@@ -1187,6 +1218,62 @@ cudaError_t launch_edge_profiles(const float* d, const Geometry& g, int L, float
                                  cudaStream_t s, bool raw) {
     k_edge_profiles<<<(unsigned)((g.W + 127) / 128), 128, 0, s>>>(d, g.H, g.W, g.pitch, L, kc, gam, theta, raw);
     return cudaGetLastError();
+}
+
+// Row-strip seam fix-up (single-GPU tall images).  Strip j starts at row
+// j HS; the FILTER pass ran every strip with a zero carry at its top and the link below it cut.
+// With y_last (strip j - 1's last output row) and z0 (strip j's first), both uncorrected, the
+// fix-up adds c Gamma_j on strip j's top L rows and e Theta_{j-1} on strip j - 1's bottom L rows,
+// c = y_last, e = z0 + y_last Gamma_j[0] - y_last (reading R26: the algebra of the row-band edge
+// scheme, on one GPU).  Seams touch disjoint rows (2L < HS).
+// The edge values come from the column kernel (sedge), so every corrected row is independent:
+// thread = (column, seam, 8 consecutive rows of the 2L-row window around the seam).
+__global__ void __launch_bounds__(128) k_seam_fix(float* __restrict__ x, int Ct, int64_t W, int64_t pitch,
+                                                  int64_t plane, int HS, int L, int ntc,
+                                                  const float* __restrict__ gam, const float* __restrict__ theta,
+                                                  const float* __restrict__ sedge) {
+    const int64_t col = (int64_t)blockIdx.x * 128 + threadIdx.x;
+    const int j = blockIdx.y + 1;  // seam between strips j - 1 and j
+    const int k0 = blockIdx.z * 8;
+    pdl_trigger();
+    pdl_wait();
+    if (col >= W) return;
+    const int64_t s0 = (int64_t)j * HS, ew = (int64_t)ntc * 32;
+    const float g0 = __ldg(gam + (int64_t)j * L * pitch + col);
+    for (int v = 0; v < Ct; ++v) {
+        const float yl = __ldg(sedge + ((int64_t)((j - 1) * 2 + 0) * Ct + v) * ew + col);  // y, last row of strip j-1
+        const float z0 = __ldg(sedge + ((int64_t)(j * 2 + 1) * Ct + v) * ew + col);        // z, first row of strip j
+        const float e = fmaf(yl, g0, z0) - yl;
+        float* X = x + v * plane + col;
+        // window row k: k < L is strip j's row k (+= y_last Gamma_j[k]); L <= k < 2L is strip j-1's
+        // row HS - 2L + k (+= e Theta_{j-1}[k - L]).  All eight rows are loaded before any is
+        // stored (the compiler cannot reorder X loads past X stores on its own).
+        float xv[8], pv[8], cv[8];
+        int64_t ro[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = k0 + u;
+            const bool top = k < L;
+            ro[u] = top ? (s0 + k) * pitch : (s0 - 2 * L + k) * pitch;
+            cv[u] = top ? yl : e;
+            if (k < 2 * L) {
+                xv[u] = X[ro[u]];
+                pv[u] = top ? __ldg(gam + ((int64_t)j * L + k) * pitch + col)
+                            : __ldg(theta + ((int64_t)(j - 1) * L + (k - L)) * pitch + col);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (k0 + u < 2 * L) X[ro[u]] = fmaf(cv[u], pv[u], xv[u]);
+    }
+}
+
+cudaError_t launch_seam_fix(float* x, int Ct, const Geometry& g, int HS, int nstrips, int L, const float* gam,
+                            const float* theta, const float* sedge, cudaStream_t s) {
+    if (nstrips < 2) return cudaSuccess;
+    const int ntc = (int)((g.W + 31) / 32);
+    return launch_pdl(k_seam_fix, dim3((unsigned)((g.W + 127) / 128), (unsigned)(nstrips - 1), (unsigned)((2 * L + 7) / 8)),
+                      dim3(128), 0, s, x, Ct, g.W, g.pitch, g.plane, HS, L, ntc, gam, theta, sedge);
 }
 
 // How many rows a carry entering the band keeps an influence >= 2^-26 of itself, maximised

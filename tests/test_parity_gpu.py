@@ -419,3 +419,50 @@ def test_guide_beyond_2_31_elements():
             np.testing.assert_allclose(got[~inf], ref[~inf], rtol=2e-6)
     del g
     torch.cuda.empty_cache()
+
+
+def _seam_fix_launches(g, t, c, ss, sr, N, lam, iters):
+    """Solve; also returns the number of row strips the context planned (0: none)."""
+    gd, td, cd = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (g, t, c))
+    out = torch.empty_like(td)
+    with dts.Solver(gd, ss, sr, N) as s:
+        s.solve(td, cd, lam, iters, out=out)
+        nst = dts.debug_strips(s.ctx)["strips"]
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64), nst
+
+
+@pytest.mark.parametrize("H,W,ss", [(3000, 4000, 6.0), (2900, 3000, 9.0), (1300, 4100, 4.0)])
+def test_row_strip_column_passes_parity(H, W, ss):
+    """Tall, wide single-context images run their C_t = 1 column passes over row strips with
+    small clusters (all 148 SMs) and a seam fix-up (plan_strips, reading R26 on one GPU): parity
+    with the oracle, and with the unstripped path (option col_strips = 0) to fp32 rounding."""
+    g, t, c = random_problem(H, W, 3, 1, seed=H + W)
+    ref = oracle.solve(g, t, c, ss, 0.2, 3, 0.99, 3)
+    got, nfix = _seam_fix_launches(g, t, c, ss, 0.2, 3, 0.99, 3)
+    rng = target_range(t)
+    assert np.max(np.abs(got - ref)) <= TOL * rng
+    with dts.options(col_strips=0):
+        plain, nfix0 = _seam_fix_launches(g, t, c, ss, 0.2, 3, 0.99, 3)
+    assert nfix0 == 0
+    assert np.max(np.abs(got - plain)) <= 1e-5 * rng
+    if H == 3000:
+        assert nfix > 1  # this shape takes row strips
+
+
+@pytest.mark.parametrize("opts", [{"row_update": 0}, {"graphs": 0}])
+def test_row_strips_with_separate_update_and_residual(opts):
+    """Row strips with the seam carries taken by the update kernel (row_update = 0) and by the
+    row update + closing update (default), with the residual output requested."""
+    g, t, c = random_problem(3000, 4000, 3, 1, seed=77)
+    ref, diag = oracle.solve(g, t, c, 6.0, 0.2, 3, 0.99, 4, diagnostics=True)
+    gd, td, cd = (torch.from_numpy(a).cuda() for a in (g, t, c))
+    out = torch.empty_like(td)
+    r = torch.zeros(4, device="cuda")
+    with dts.options(**opts), dts.Solver(gd, 6.0, 0.2, 3) as s:
+        s.solve(td, cd, 0.99, 4, out=out, resid_inf_out=r)
+        s.solve(td, cd, 0.99, 4, out=out)  # plain (row update) on the same context
+    torch.cuda.synchronize()
+    rng = target_range(t)
+    assert np.max(np.abs(out.cpu().numpy() - ref)) <= TOL * rng
+    np.testing.assert_allclose(r.cpu().numpy(), diag[:, 0], rtol=0, atol=TOL * rng)

@@ -34,3 +34,12 @@ for name in (sys.argv[1:] or ["C4", "C3"]):
                 res[k] = {"n": v["launches"], "avg_us": round(1e3 * v["avg_ms"], 2), "frac": round(gbs / PEAK, 4)}
         dts.dts_profile_enable(s.ctx, 0)
     print(json.dumps(res), flush=True)
+    import ctypes
+    lib = dts.load_library()
+    lib.dts_debug_strips.restype = ctypes.c_int32
+    lib.dts_debug_strips.argtypes = [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int32)] * 4
+    hs, cb, gr = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    L3 = (ctypes.c_int32 * 3)()
+    with dts.Solver(g, ss, sr, 3) as s2:
+        nst = lib.dts_debug_strips(s2.ctx, ctypes.byref(hs), L3, ctypes.byref(cb), ctypes.byref(gr))
+    print(json.dumps({"strips": nst, "HS": hs.value, "L": list(L3), "CB": cb.value, "grid": gr.value}), flush=True)
