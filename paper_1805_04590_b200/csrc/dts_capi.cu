@@ -698,6 +698,11 @@ static dts_status plan_strips(dts_ctx* ctx, cudaStream_t s) {
         cudaGetLastError();
         return DTS_OK;
     }
+    // only for columns that need big clusters (GPC packing wastes SMs) and several tile rounds per
+    // launch (throughput-bound): small images stay latency-bound and keep one strip
+    const int forced0 = opts_g().col_strips.load();
+    const int rounds = base.ntiles * base.CB / (int)base.grid.x;
+    if (forced0 < 2 && (base.CB < 8 || rounds < 4)) return DTS_OK;
     // preference (measured on C4, unprofiled 20-iteration solves, tools/strips4.sh): the fewest
     // strips whose plan covers >= 90% of the SMs and adds >= 10% over one strip (C4: 2 strips of
     // 5000 rows on 15 clusters of 9, 30.58 ms against 31.18 unstripped; 4 strips x clusters of 4

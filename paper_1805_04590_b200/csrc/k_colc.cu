@@ -161,7 +161,9 @@ constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
 
 // LSV: rows per warp segment; 16 for C_t >= 2 FILTER passes of images up to 16 x 320 rows
 // (half the registers per thread, so 20 warps fit where 32-row segments allow 11-14)
-template <int CT, int MODE, bool PRE, int LSV = LS>
+// STRIPS: the tiles cover row strips of p.HS rows (tile -> (strip, column tile)); a separate
+// instantiation so that the one-strip kernels keep their code
+template <int CT, int MODE, bool PRE, int LSV = LS, bool STRIPS = false>
 __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()), 1)
     k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
     constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
@@ -224,11 +226,11 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
     // tile -> (row strip, column tile): a strip of HS rows is filtered with zero carries at its
     // top and the link below it cut (the seam fix-up adds the carries)
     auto stage_seg = [&](int tile, int q) {
-        const int col0 = (tile % p.ntc) * TW;
-        const int sb = (tile / p.ntc) * p.HS;
+        const int col0 = (STRIPS ? tile % p.ntc : tile) * TW;
+        const int sb = STRIPS ? (tile / p.ntc) * p.HS : 0;
         const uint32_t box = (uint32_t)(LSV * TW * sizeof(float));
         const int rq = r0 + q * LSV;
-        const uint32_t bytes = rq < min(p.HS, p.H - sb) ? box * (1 + (HASX ? NV : 0)) : 0u;
+        const uint32_t bytes = rq < (STRIPS ? min(p.HS, p.H - sb) : p.H) ? box * (1 + (HASX ? NV : 0)) : 0u;
         mbar_arrive_expect_tx(&bars[q], bytes);
         if (bytes) {
             tma_load_2d(ld + q * LSV * TW, &tm_d, col0, sb + rq, &bars[q]);
@@ -243,9 +245,9 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
 
     int k = 0;
     for (int tile = cluster; tile < p.ntiles; tile += nclusters, ++k) {
-        const int col0 = (tile % p.ntc) * TW;
-        const int sb = (tile / p.ntc) * p.HS;  // first row of this tile's strip
-        const int Hs = min(p.HS, p.H - sb);    // rows of the strip
+        const int col0 = (STRIPS ? tile % p.ntc : tile) * TW;
+        const int sb = STRIPS ? (tile / p.ntc) * p.HS : 0;  // first row of this tile's strip
+        const int Hs = STRIPS ? min(p.HS, p.H - sb) : p.H;  // rows of the strip
         const int col = col0 + c;
         const bool colok = col < p.W;
 
@@ -466,7 +468,8 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
             }
             // row strips: the strip's last and first output rows, for the seam fix-up (which must
             // read them before it corrects the rows around the seam)
-            if (MODE == MODE_FILTER && p.sedge) {
+            if constexpr (STRIPS) {  // strips run the C_t = 1 FILTER passes only
+              if (p.sedge) {
                 const int strip = tile / p.ntc;
                 const int64_t ew = (int64_t)p.ntc * TW, ec = (int64_t)(tile % p.ntc) * TW + c;
                 const int jl = Hs - 1 - (r0 + lo);
@@ -483,6 +486,7 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
 #pragma unroll
                     for (int v = 0; v < NV; ++v) p.sedge[((int64_t)(strip * 2 + 1) * NV + v) * ew + ec] = xv[v][0];
                 }
+              }
             }
         }
         // no barrier here: before the next tile's fold barrier a warp writes only its own
@@ -953,8 +957,15 @@ template <int CT, bool PRE>
 static const void* kptr16() {
     return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE_FILTER, PRE, 16>);
 }
-static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = false, int ls = colc::LS) {
-    if (ls == 40) {  // experiment: 16 warps x 40-row segments, C_t = 1 FILTER
+static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = false, int ls = colc::LS,
+                               bool strips = false) {
+    if (strips) {  // row strips: C_t = 1 FILTER on the pass-1 coefficient (plan_strips)
+        if (mode != MODE_FILTER || band || Ct != 1 || !pre) return nullptr;
+        if (ls == 40) return reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, true, 40, true>);
+        if (ls == 32) return reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, true, 32, true>);
+        return nullptr;
+    }
+    if (ls == 40) {  // 16 warps x 40-row segments, C_t = 1 FILTER
         if (mode != MODE_FILTER || band || Ct != 1) return nullptr;
         return pre ? reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, true, 40>)
                    : reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, false, 40>);
@@ -1032,8 +1043,11 @@ static cudaError_t plan_col_cluster_uncached(const Geometry& g, int Ct, int mode
         (e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
         return e;
     const bool f32 = mode == MODE_FILTER && ls == colc::LS;
+    const bool strip = mode == MODE_FILTER && Ct == 1 && (ls == 32 || ls == 40);
     for (const void* f : {fn, mode == MODE_FILTER ? colc_kernel(Ct, mode, true, false, ls) : fn,
-                          f32 ? colc_kernel(Ct, mode, false, true) : fn, f32 ? colc_kernel(Ct, mode, true, true) : fn}) {
+                          f32 ? colc_kernel(Ct, mode, false, true) : fn, f32 ? colc_kernel(Ct, mode, true, true) : fn,
+                          strip ? colc_kernel(Ct, mode, true, false, ls, true) : fn}) {
+        if (!f) continue;
         cudaFuncAttributes fa2;
         if ((e = cudaFuncGetAttributes(&fa2, f)) != cudaSuccess) return e;
         if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess ||
@@ -1156,7 +1170,7 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     } else {
         tx = td;
     }
-    const void* fn = colc_kernel(Ct, mode, nsq >= 0, ext != nullptr || edge != nullptr, plan.Ls);
+    const void* fn = colc_kernel(Ct, mode, nsq >= 0, ext != nullptr || edge != nullptr, plan.Ls, plan.HS > 0);
     if (!fn) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = plan.grid;
