@@ -231,7 +231,8 @@ def dominant(table, solve_only=True):
 def extra_configs(dts, torch, dev, stream, timer, peak):
     """Every paper-shaped workload besides the headline (north star "Reporting"; VERDICT r1 item
     5): C1 stereo shape, C2 16x SR, C3 8 x 4K 3-channel.  Per
-    config: create + solve + destroy per step (profiler off), the dominant solve kernel's
+    config: create + solve + destroy per step (profiler off; C3: one batched context for its
+    images, and per-image contexts beside it), the dominant solve kernel's
     fraction of the HBM peak (profiled step) and parity of image 0 against the fp64 oracle."""
     import oracle
     from concurrent.futures import ThreadPoolExecutor
@@ -245,42 +246,63 @@ def extra_configs(dts, torch, dev, stream, timer, peak):
             host = [make_inputs(name)]
         devin = [tuple(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in x) for x in host]
         outs = [torch.empty_like(t) for _, t, _ in devin]
+        batched = cfg.batch > 1  # one context for all images (dts_create_batch)
+        if batched:
+            bin_ = tuple(torch.stack([x[j] for x in devin]) for j in range(3))
+            bout = torch.empty_like(bin_[1])
 
-        def step():
+        def step_per_image():
             for (g, t, c), o in zip(devin, outs):
                 ctx = dts.dts_create(g, cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
                 dts.dts_solve(ctx, t, c, cfg.lam, cfg.iters, o, stream=stream.cuda_stream)
                 dts.dts_destroy(ctx)
 
+        def step_batched():
+            ctx = dts.dts_create_batch(bin_[0], cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
+            dts.dts_solve(ctx, bin_[1], bin_[2], cfg.lam, cfg.iters, bout, stream=stream.cuda_stream)
+            dts.dts_destroy(ctx)
+
+        step = step_batched if batched else step_per_image
         step()
         steps = 3
         ms = timer(step, steps) / steps
-        # solve only, first (eager) solve of a fresh context and a repeat (graph replay)
-        g0, t0, c0 = devin[0]
-        ctx = dts.dts_create(g0, cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
-        first = timer(lambda: dts.dts_solve(ctx, t0, c0, cfg.lam, cfg.iters, outs[0], stream=stream.cuda_stream), 1)
-        dts.dts_solve(ctx, t0, c0, cfg.lam, cfg.iters, outs[0], stream=stream.cuda_stream)
-        rep = timer(lambda: dts.dts_solve(ctx, t0, c0, cfg.lam, cfg.iters, outs[0], stream=stream.cuda_stream), 3) / 3
+        ms_per_image_ctx = None
+        if batched:
+            step_per_image()
+            ms_per_image_ctx = timer(step_per_image, steps) / steps
+        # solve only, first (eager) solve of a fresh context and a repeat (graph replay): the
+        # batched context of every image, else image 0's
+        if batched:
+            ctx = dts.dts_create_batch(bin_[0], cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
+            g0, t0, c0, o0, px_solve = *bin_, bout, cfg.pixels
+        else:
+            (g0, t0, c0), o0, px_solve = devin[0], outs[0], cfg.H * cfg.W
+            ctx = dts.dts_create(g0, cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
+        first = timer(lambda: dts.dts_solve(ctx, t0, c0, cfg.lam, cfg.iters, o0, stream=stream.cuda_stream), 1)
+        dts.dts_solve(ctx, t0, c0, cfg.lam, cfg.iters, o0, stream=stream.cuda_stream)
+        rep = timer(lambda: dts.dts_solve(ctx, t0, c0, cfg.lam, cfg.iters, o0, stream=stream.cuda_stream), 3) / 3
         dts.dts_destroy(ctx)
         dts.dts_profile_enable(0, True)
         step()
         table = kernel_table(dts.dts_profile_read(0), 1, ms, peak)
         dts.dts_profile_enable(0, False)
         kname, k = dominant(table)
-        px_img = cfg.H * cfg.W
         t_or = time.perf_counter()
         ref = oracle.solve(host[0][0], host[0][1], host[0][2], cfg.sigma_s, cfg.sigma_r, cfg.N, cfg.lam, cfg.iters)
         t_or = time.perf_counter() - t_or
         step()  # outputs of a plain step for the parity check
         torch.cuda.synchronize()
-        err = float(np.max(np.abs(outs[0].cpu().numpy().astype(np.float64) - ref)))
+        got0 = (bout[0] if batched else outs[0]).cpu().numpy().astype(np.float64)
+        err = float(np.max(np.abs(got0 - ref)))
         rng = float(target_range(host[0][1]))
         res[name] = {"workload": workload_desc(cfg),
                      "mpix_iter_per_s": cfg.pixels * cfg.iters / 1e6 / (ms / 1e3), "ms_per_step": ms,
-                     "step": "dts_create + dts_solve + dts_destroy per image, all images",
+                     "step": ("dts_create_batch + dts_solve + dts_destroy, one context for all images" if batched
+                              else "dts_create + dts_solve + dts_destroy"),
+                     "solve_only": "all images (batched context)" if batched else "image 0",
                      "solve_only_first_ms": first, "solve_only_repeat_ms": rep,
-                     "solve_only_first_mpix_iter_per_s": px_img * cfg.iters / 1e6 / (first / 1e3),
-                     "solve_only_repeat_mpix_iter_per_s": px_img * cfg.iters / 1e6 / (rep / 1e3),
+                     "solve_only_first_mpix_iter_per_s": px_solve * cfg.iters / 1e6 / (first / 1e3),
+                     "solve_only_repeat_mpix_iter_per_s": px_solve * cfg.iters / 1e6 / (rep / 1e3),
                      "dominant_kernel": {"name": kname, "avg_ms": k["avg_ms"], "gbs": k["gbs"],
                                          "frac_of_peak": k["frac_of_peak"], "share_of_step": k["share_of_step"]},
                      "kernels": {kk: {"avg_ms": v["avg_ms"], "frac_of_peak": v["frac_of_peak"],
@@ -288,6 +310,10 @@ def extra_configs(dts, torch, dev, stream, timer, peak):
                      "parity": {"vs": "fp64 oracle (O6), image 0, full solve", "max_abs_err": err,
                                 "tol_abs": 1e-4 * rng, "max_abs_err_over_range": err / rng, "ok": err <= 1e-4 * rng,
                                 "oracle_seconds": t_or}}
+        if batched:
+            res[name]["per_image_contexts"] = {"ms_per_step": ms_per_image_ctx,
+                                               "mpix_iter_per_s": cfg.pixels * cfg.iters / 1e6 / (ms_per_image_ctx / 1e3)}
+            del bin_, bout
         del devin, outs
     return res
 

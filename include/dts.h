@@ -79,6 +79,24 @@ dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C,
                       float sigma_s, float sigma_r, int32_t filter_passes,
                       void* stream, dts_ctx** out_ctx);
 
+/* dts_create_batch -- one context for B independent images of the same size (the C3
+ * workload, "eight 4K images"; north star "independent images ... per rank").
+ *   guides         B x H x W x C fp32 (B HWC images back to back); read once.
+ *   B, H, W, C     B >= 1, B * H <= 2^30; otherwise as dts_create.
+ * The context is the B images stacked into one (B*H) x W image whose column recurrences
+ * are cut between consecutive images (d_y = +inf at each image's first row: the
+ * first-row rule R4 of every image), so every call on it -- dts_solve / dts_solve_ex with
+ * target and confidence B x H x W [x C_t], dts_confidence, dts_debug_read -- treats the
+ * images exactly as B separate contexts would (the recurrence restarts are exact: the cut
+ * coefficient is 0).  What batching buys: each column pass launches every image's column
+ * tiles at once (a per-C_t plan over image-high strips), every row pass all B*H rows.
+ * The per-context row limit above applies to the image height H (C_t <= 3 with the A1
+ * coefficient, N <= 4); other configurations fall back to the stacked-image plans and the
+ * (B*H)-row limits.  Errors: as dts_create; DTS_E_SHAPE when B * H > 2^30.          */
+dts_status dts_create_batch(const float* guides, int64_t B, int64_t H, int64_t W, int32_t C,
+                            float sigma_s, float sigma_r, int32_t filter_passes,
+                            void* stream, dts_ctx** out_ctx);
+
 /* dts_solve -- `iterations` gradient-descent steps of Eq. (3) with
  * step 0.99, starting from z^0 = t (R11).
  *   target            H x W x target_channels fp32, HWC.  Channels are solved

@@ -17,7 +17,7 @@ import os
 
 import numpy as np
 
-__all__ = ["DTSError", "dts_create", "dts_solve", "dts_solve_ex", "dts_confidence", "dts_solve_stereo",
+__all__ = ["DTSError", "dts_create", "dts_create_batch", "dts_solve", "dts_solve_ex", "dts_confidence", "dts_solve_stereo",
            "dts_sr_prepare", "dts_create_ex", "dts_debug_read_windows", "DTS_FILTER_RF", "DTS_FILTER_BOX",
            "dts_destroy",
            "dts_status_string",
@@ -39,7 +39,8 @@ ABI_FUNCTIONS = ["dts_create", "dts_solve", "dts_destroy", "dts_status_string", 
                  "dts_solve_ex", "dts_debug_read", "dts_profile_enable", "dts_profile_read",
                  "dts_launch_count", "dts_comm_unique_id", "dts_comm_init", "dts_comm_init_loopback",
                  "dts_comm_destroy", "dts_create_band", "dts_version", "dts_confidence", "dts_solve_stereo",
-                 "dts_sr_prepare", "dts_create_ex", "dts_debug_read_windows", "dts_set_option", "dts_get_option"]
+                 "dts_sr_prepare", "dts_create_ex", "dts_debug_read_windows", "dts_set_option", "dts_get_option",
+                 "dts_create_batch"]
 
 
 class DTSError(RuntimeError):
@@ -82,6 +83,8 @@ def load_library():
     lib = ctypes.CDLL(_LIB_PATH)
     vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
     lib.dts_create.argtypes = [vp, i64, i64, i32, f32, f32, i32, vp, ctypes.POINTER(vp)]
+    lib.dts_create_batch.argtypes = [vp, i64, i64, i64, i32, f32, f32, i32, vp, ctypes.POINTER(vp)]
+    lib.dts_create_batch.restype = ctypes.c_int
     lib.dts_create.restype = ctypes.c_int
     lib.dts_create_ex.argtypes = [vp, i64, i64, i32, f32, f32, i32, ctypes.POINTER(CreateOpts), vp,
                                   ctypes.POINTER(vp)]
@@ -188,6 +191,21 @@ def dts_create(guide, sigma_s: float, sigma_r: float, filter_passes: int = 3, st
     return ctx.value
 
 
+def dts_create_batch(guides, sigma_s: float, sigma_r: float, filter_passes: int = 3, stream=None) -> int:
+    """guides: B x H x W x C (or B x H x W) float32, the images back to back.  One context for
+    the B images; solve targets / confidences are B x H x W [x C_t] (include/dts.h)."""
+    if len(guides.shape) == 3:
+        B, H, W = guides.shape
+        C = 1
+    else:
+        B, H, W, C = guides.shape
+    ctx = ctypes.c_void_p()
+    st = load_library().dts_create_batch(_ptr(guides, "guides"), B, H, W, C, sigma_s, sigma_r, filter_passes,
+                                         _stream(stream, guides), ctypes.byref(ctx))
+    _check(st, "dts_create_batch")
+    return ctx.value
+
+
 def dts_create_ex(guide, sigma_s: float, sigma_r: float, filter_passes: int = 3, filter: int = DTS_FILTER_RF,
                   radius_scale: float = 0.0, stream=None) -> int:
     """dts_create with options: filter = DTS_FILTER_BOX builds the box-variant context (reading
@@ -216,7 +234,7 @@ def dts_solve_ex(ctx: int, target, confidence, lam: float, iterations: int, out,
                  step: float = 0.0, support_mode: int = 0, check_inputs: bool = False, resid_inf_out=None):
     """dts_solve with options; resid_inf_out: None or `iterations` float32 (device tensor or host
     array) that receives ||g_k||_inf per iteration (K8)."""
-    Ct = 1 if len(target.shape) == 2 else int(target.shape[2])
+    Ct = _target_channels(target, confidence)
     opts = SolveOpts(step, support_mode, 1 if check_inputs else 0,
                      _ptr(resid_inf_out, "resid_inf_out") if resid_inf_out is not None else None)
     st = load_library().dts_solve_ex(ctx, _ptr(target, "target"), Ct, _ptr(confidence, "confidence"), lam,
@@ -265,9 +283,20 @@ class options:
             dts_set_option(k, v)
 
 
+def _target_channels(target, confidence) -> int:
+    """C_t: the trailing target axis beyond the confidence's shape (H x W, or B x H x W for
+    batched contexts); a target shaped like the confidence has one channel."""
+    if len(target.shape) == len(confidence.shape):
+        return 1
+    if len(target.shape) != len(confidence.shape) + 1:
+        raise ValueError(f"target shape {tuple(target.shape)} does not extend confidence {tuple(confidence.shape)}")
+    return int(target.shape[-1])
+
+
 def dts_solve(ctx: int, target, confidence, lam: float, iterations: int, out, stream=None):
-    """target: H x W (x Ct) float32 HWC; confidence: H x W; out like target (written)."""
-    Ct = 1 if len(target.shape) == 2 else int(target.shape[2])
+    """target: H x W (x Ct) float32 HWC; confidence: H x W; out like target (written).  Batched
+    contexts (dts_create_batch): B x H x W (x Ct) and B x H x W."""
+    Ct = _target_channels(target, confidence)
     st = load_library().dts_solve(ctx, _ptr(target, "target"), Ct, _ptr(confidence, "confidence"), lam,
                                   iterations, _ptr(out, "out"), _stream(stream, target, confidence, out))
     _check(st, "dts_solve")
@@ -411,9 +440,17 @@ class Solver:
     """Thin RAII wrapper: ``Solver(guide, sigma_s, sigma_r, N).solve(t, c, lam, iters)``."""
 
     def __init__(self, guide, sigma_s: float, sigma_r: float, filter_passes: int = 3, stream=None,
-                 filter: int = DTS_FILTER_RF, radius_scale: float = 0.0):
-        self.H, self.W = int(guide.shape[0]), int(guide.shape[1])
+                 filter: int = DTS_FILTER_RF, radius_scale: float = 0.0, batched: bool = False):
+        """batched: guide is B x H x W [x C], one context for the B images (dts_create_batch)."""
         self.filter = filter
+        if batched:
+            if filter != DTS_FILTER_RF:
+                raise ValueError("batched contexts use the recursive filter")
+            # the stacked image (debug reads return B*H x W)
+            self.H, self.W = int(guide.shape[0]) * int(guide.shape[1]), int(guide.shape[2])
+            self.ctx = dts_create_batch(guide, sigma_s, sigma_r, filter_passes, stream)
+            return
+        self.H, self.W = int(guide.shape[0]), int(guide.shape[1])
         if filter == DTS_FILTER_RF:
             self.ctx = dts_create(guide, sigma_s, sigma_r, filter_passes, stream)
         else:

@@ -113,6 +113,12 @@ struct dts_ctx {
     std::vector<int> vs_L;
     std::vector<float*> vs_gam, vs_theta;  // [vs_n][L][pitch] each
     float* vs_edge = nullptr;              // [vs_n][2][1][ntc * 32]: each strip's last / first output row
+    // batched contexts (dts_create_batch): `batch` images of batch_H rows stacked vertically, the
+    // column recurrences cut between them (d_y = +inf, A1 = 0 at each image's first row); the
+    // FILTER column passes run every image's tiles in one launch (per-C_t strip plan, no seams)
+    int64_t batch = 1, batch_H = 0;
+    ColPlan bs_plan[5]{};
+    signed char bs_state[5] = {0, 0, 0, 0, 0};  // 0 not planned, 1 planned, -1 not available
     int num_sms = 148;
     Geometry g{};
     int C = 0;
@@ -874,12 +880,13 @@ static dts_status band_agree(dts_ctx* ctx, cudaStream_t s, std::vector<int>* L_a
 
 static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0, int64_t H, int64_t W, int32_t C,
                               float sigma_s, float sigma_r, int32_t filter_passes, dts::Comm* comm, void* stream,
-                              dts_ctx** out_ctx) {
+                              dts_ctx** out_ctx, int64_t batch = 1) {
     if (!out_ctx || !guide) return DTS_E_ARG;
     *out_ctx = nullptr;
     if (H < 1 || W < 1 || C < 1) return DTS_E_ARG;
     if (row0 < 0 || row0 + H > H_total) return DTS_E_ARG;
     if (!comm && (row0 != 0 || H != H_total)) return DTS_E_ARG;
+    if (batch < 1 || H % batch != 0 || (comm && batch != 1)) return DTS_E_ARG;
     if (!finite_pos(sigma_s) || !finite_pos(sigma_r)) return DTS_E_ARG;
     if (filter_passes < 1 || filter_passes > 16) return DTS_E_ARG;
     if (W > 18432 || H > (int64_t)1 << 30 || C > 4096) return DTS_E_SHAPE;
@@ -907,6 +914,8 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
     ctx->comm = comm;
     ctx->row0 = row0;
     ctx->H_total = H_total;
+    ctx->batch = batch;
+    ctx->batch_H = H / batch;
     ctx->halo_above = row0 > 0 ? 1 : 0;
     ctx->halo_below = row0 + H < H_total ? 1 : 0;
     const int64_t Hx = H + ctx->halo_above + ctx->halo_below;  // guide rows passed in
@@ -980,7 +989,7 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
     // the cluster column kernel reads a_1^{d_y} instead of d_y (one exp per pixel, written by
     // the derivative kernel, instead of one per pixel and pass); later passes square it (R5:
     // sigma halves per pass).  Rows 0..H: row H is the bottom link (+inf -> 0).
-    const bool with_a1 = filter_passes <= 4 && (comm || cp.kind == 1);
+    const bool with_a1 = filter_passes <= 4 && (comm || cp.kind == 1 || batch > 1);
     if (with_a1 && (e = cudaMallocAsync((void**)&ctx->A1y_base, (size_t)(Hx + 1) * ctx->g.pitch * sizeof(float), s)) !=
                        cudaSuccess) {
         st = cuda_fail(e);
@@ -1001,11 +1010,29 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
             st = run_launch(ctx, F_FILL, ctx->g.pitch * 4.0, s,
                             [&] { return launch_fill(ctx->A1y + H * ctx->g.pitch, ctx->g.pitch, 0.f, s); });
     }
+    // batched contexts: cut the column links between the stacked images (R4 at each image's
+    // first row: d_y = +inf, A = 0), so that every recurrence restarts there exactly
+    for (int64_t b = 1; b < batch && st == DTS_OK; ++b) {
+        const float inf = std::numeric_limits<float>::infinity();
+        const int64_t r = b * ctx->batch_H;
+        st = run_launch(ctx, F_FILL, ctx->g.pitch * 4.0, s,
+                        [&] { return launch_fill(ctx->dy + r * ctx->g.pitch, ctx->g.pitch, inf, s); });
+        if (st == DTS_OK && ctx->A1y)
+            st = run_launch(ctx, F_FILL, ctx->g.pitch * 4.0, s,
+                            [&] { return launch_fill(ctx->A1y + r * ctx->g.pitch, ctx->g.pitch, 0.f, s); });
+    }
     if (st == DTS_OK)
         st = run_launch(ctx, F_SUPPORT_ROW, px * 8.0, s, [&] {
             return launch_row_pass(rp, ctx->g, 1, MODE_SUPPORT, nullptr, ctx->S, ctx->dx, ctx->ks, s);
         });
     if (st == DTS_OK) st = ensure_col_scratch(ctx, cp, s);
+    Geometry gi = ctx->g;  // one image of a batched context
+    gi.H = ctx->batch_H;
+    gi.plane = gi.H * gi.pitch;
+    ColPlan cpi{};
+    const bool per_image_support = batch > 1 && cp.kind != 1 &&
+                                   plan_col(gi, 1, MODE_SUPPORT, ctx->num_sms, &cpi) == cudaSuccess && cpi.kind == 1;
+    cudaGetLastError();
     std::vector<int> band_L;  // agreed edge lengths (row-band contexts): passes, then the support
     if (st == DTS_OK && comm) {
         ctx->band_scheme = opts_g().band_scheme.load();  // latched: the same on every rank of a job
@@ -1074,6 +1101,17 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
                 st = col_pass_banded(ctx, 1, MODE_SUPPORT, nullptr, ctx->ks, nullptr, ctx->S, F_SUPPORT_COL,
                                      px * 12.0, s, -1);
             }
+        } else if (per_image_support) {
+            // batched context too tall for one cluster column: s_y image by image on the cluster
+            // kernel (each image's column ends at the cut below it)
+            if ((e = cudaMallocAsync((void**)&ctx->Sy, plane, s)) != cudaSuccess) st = cuda_fail(e);
+            for (int64_t b = 0; b < batch && st == DTS_OK; ++b) {
+                const int64_t off = b * ctx->batch_H * ctx->g.pitch;
+                st = run_launch(ctx, F_SUPPORT_COL, (double)gi.H * W * 8.0, s, [&] {
+                    return launch_col_cluster(cpi, gi, 1, MODE_SUPPORT, nullptr, ctx->dy + off, ctx->ks, nullptr,
+                                              ctx->Sy + off, s);
+                });
+            }
         } else if (cp.kind == 1) {  // cluster kernel: s_y into its own plane (no read-modify-write of S)
             if ((e = cudaMallocAsync((void**)&ctx->Sy, plane, s)) != cudaSuccess) st = cuda_fail(e);
             if (st == DTS_OK)
@@ -1110,7 +1148,7 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
             });
         }
     }
-    if (st == DTS_OK && !comm && ctx->A1y && opts_g().col_strips.load()) st = plan_strips(ctx, s);
+    if (st == DTS_OK && !comm && batch == 1 && ctx->A1y && opts_g().col_strips.load()) st = plan_strips(ctx, s);
     if (gstage) {
         cudaFreeAsync(gstage, s);
         if (st == DTS_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess) st = cuda_fail(e);
@@ -1127,6 +1165,41 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
 dts_status dts_create(const float* guide, int64_t H, int64_t W, int32_t C, float sigma_s, float sigma_r,
                       int32_t filter_passes, void* stream, dts_ctx** out_ctx) {
     return create_impl(guide, H, 0, H, W, C, sigma_s, sigma_r, filter_passes, nullptr, stream, out_ctx);
+}
+
+dts_status dts_create_batch(const float* guides, int64_t B, int64_t H, int64_t W, int32_t C, float sigma_s,
+                            float sigma_r, int32_t filter_passes, void* stream, dts_ctx** out_ctx) {
+    if (out_ctx) *out_ctx = nullptr;
+    if (B < 1 || H < 1 || B > ((int64_t)1 << 30) / H) return B < 1 || H < 1 ? DTS_E_ARG : DTS_E_SHAPE;
+    return create_impl(guides, B * H, 0, B * H, W, C, sigma_s, sigma_r, filter_passes, nullptr, stream, out_ctx, B);
+}
+
+// batched contexts: the FILTER column plan over the images as row strips (one launch holds every
+// image's column tiles; HS = image height; no seam fix-up, the links between images are cut)
+static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out) {
+    if (ctx->batch < 2 || !ctx->A1y || Ct < 1 || Ct > 4 || opts_g().col_kernel.load() != 0) return false;
+    if (ctx->bs_state[Ct] == 0) {
+        Geometry gs = ctx->g;  // planned as the images side by side
+        gs.H = ctx->batch_H;
+        gs.W = ctx->g.W * ctx->batch;
+        gs.pitch = (gs.W + 31) / 32 * 32;
+        gs.plane = gs.H * gs.pitch;
+        ColPlan ps{};
+        const bool ok = gs.W <= ((int64_t)1 << 31) / 2 &&
+                        plan_col(gs, Ct, MODE_FILTER, ctx->num_sms, &ps) == cudaSuccess && ps.kind == 1 &&
+                        colc_strips_supported(Ct, ps.Ls);
+        cudaGetLastError();
+        if (ok) {
+            ps.HS = (int)ctx->batch_H;
+            ps.ntc = (int)((ctx->g.W + 31) / 32);
+            ps.ntiles = ps.ntc * (int)ctx->batch;
+            ctx->bs_plan[Ct] = ps;
+        }
+        ctx->bs_state[Ct] = ok ? 1 : -1;
+    }
+    if (ctx->bs_state[Ct] != 1) return false;
+    *out = ctx->bs_plan[Ct];
+    return true;
 }
 
 // Box-filter context (reading R25): fixed-point increments, windows of every pass and the
@@ -1337,11 +1410,14 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     ColPlan cpf{}, cpu{};
     if (!is_box) {
         if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess) return DTS_E_SHAPE;
-        if ((ctx->comm ? plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)
-                       : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess)
-            return DTS_E_SHAPE;
-        // the decoupled kernel (tall columns) applies Eq. (3) in its own write-out
-        if (cpf.kind != 1 && plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu) != cudaSuccess) return DTS_E_SHAPE;
+        if (!batch_strip_plan(ctx, Ct, &cpf)) {  // batched contexts: every image's tiles in one launch
+            if ((ctx->comm ? plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)
+                           : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess)
+                return DTS_E_SHAPE;
+            // the decoupled kernel (tall columns) applies Eq. (3) in its own write-out
+            if (cpf.kind != 1 && plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu) != cudaSuccess)
+                return DTS_E_SHAPE;
+        }
         cudaGetLastError();
     }
     const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),

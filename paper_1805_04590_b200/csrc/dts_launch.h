@@ -94,6 +94,8 @@ cudaError_t launch_col_pass(const ColPlan& plan, const Geometry& g, int Ct, int 
 // K3/K4 fast path: cluster-held column tiles, register-resident segments (k_colc.cu).
 // Returns cudaErrorNotSupported when the shape does not fit (then use plan_col_pass).
 cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan);
+// a row-strip instantiation of the cluster FILTER kernel (A1 input) exists for (C_t, segment rows)
+bool colc_strips_supported(int Ct, int ls);
 // ls = 16: 16-row warp segments (FILTER, C_t >= 2, not for row bands); plan->Ls records it
 // force_cb >= 0: cluster size (0 = auto) instead of the "col_cluster" option
 cudaError_t plan_col_cluster_ls(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int ls,

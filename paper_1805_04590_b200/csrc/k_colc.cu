@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threa
             }
             // row strips: the strip's last and first output rows, for the seam fix-up (which must
             // read them before it corrects the rows around the seam)
-            if constexpr (STRIPS) {  // strips run the C_t = 1 FILTER passes only
+            if constexpr (STRIPS) {  // seam strips of one image (batched contexts pass no sedge)
               if (p.sedge) {
                 const int strip = tile / p.ntc;
                 const int64_t ew = (int64_t)p.ntc * TW, ec = (int64_t)(tile % p.ntc) * TW + c;
@@ -959,10 +959,12 @@ static const void* kptr16() {
 }
 static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = false, int ls = colc::LS,
                                bool strips = false) {
-    if (strips) {  // row strips: C_t = 1 FILTER on the pass-1 coefficient (plan_strips)
-        if (mode != MODE_FILTER || band || Ct != 1 || !pre) return nullptr;
-        if (ls == 40) return reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, true, 40, true>);
-        if (ls == 32) return reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, true, 32, true>);
+    if (strips) {  // row strips: FILTER on the pass-1 coefficient (plan_strips, batched contexts)
+        if (mode != MODE_FILTER || band || !pre) return nullptr;
+        if (Ct == 1 && ls == 40) return reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, true, 40, true>);
+        if (Ct == 1 && ls == 32) return reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, true, 32, true>);
+        if (Ct == 2 && ls == 16) return reinterpret_cast<const void*>(colc::k_col_cluster<2, MODE_FILTER, true, 16, true>);
+        if (Ct == 3 && ls == 16) return reinterpret_cast<const void*>(colc::k_col_cluster<3, MODE_FILTER, true, 16, true>);
         return nullptr;
     }
     if (ls == 40) {  // 16 warps x 40-row segments, C_t = 1 FILTER
@@ -1016,6 +1018,8 @@ static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = f
     return nullptr;
 }
 
+bool colc_strips_supported(int Ct, int ls) { return colc_kernel(Ct, MODE_FILTER, true, false, ls, true) != nullptr; }
+
 // Fast path if the column fits a cluster of <= 16 CTAs with register-resident segments.
 // ls: rows per warp segment, 32 (every mode) or 16 (FILTER at C_t >= 2, single context).
 // Cluster size CB: its CTAs hold H / CB rows in <= 20 warps.  32-row segments: the smallest
@@ -1043,7 +1047,7 @@ static cudaError_t plan_col_cluster_uncached(const Geometry& g, int Ct, int mode
         (e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
         return e;
     const bool f32 = mode == MODE_FILTER && ls == colc::LS;
-    const bool strip = mode == MODE_FILTER && Ct == 1 && (ls == 32 || ls == 40);
+    const bool strip = mode == MODE_FILTER && ((Ct == 1 && (ls == 32 || ls == 40)) || (Ct >= 2 && ls == 16));
     for (const void* f : {fn, mode == MODE_FILTER ? colc_kernel(Ct, mode, true, false, ls) : fn,
                           f32 ? colc_kernel(Ct, mode, false, true) : fn, f32 ? colc_kernel(Ct, mode, true, true) : fn,
                           strip ? colc_kernel(Ct, mode, true, false, ls, true) : fn}) {
