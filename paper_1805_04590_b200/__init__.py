@@ -244,6 +244,17 @@ def dts_solve_ex(ctx: int, target, confidence, lam: float, iterations: int, out,
     return out
 
 
+def debug_col_plan(ctx: int, Ct: int) -> dict:
+    """FILTER column plan dts_solve uses for C_t on this context (tests / probes)."""
+    f = load_library().dts_debug_col_plan
+    f.restype = ctypes.c_int32
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
+    v = (ctypes.c_int32 * 7)()
+    if f(ctx, Ct, v) != 0:
+        raise DTSError(2, "dts_debug_col_plan")
+    return dict(zip(("kind", "CB", "grid", "threads", "HS", "ntiles", "Ls"), list(v)))
+
+
 def debug_strips(ctx: int) -> dict:
     """Row-strip plan of a context (tests / probes; not part of include/dts.h)."""
     lib = load_library()

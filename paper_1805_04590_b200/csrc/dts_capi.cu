@@ -1186,7 +1186,9 @@ static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out) {
         gs.plane = gs.H * gs.pitch;
         ColPlan ps{};
         const bool ok = gs.W <= ((int64_t)1 << 31) / 2 &&
-                        plan_col(gs, Ct, MODE_FILTER, ctx->num_sms, &ps) == cudaSuccess && ps.kind == 1 &&
+                        plan_col(gs, Ct, MODE_FILTER, ctx->num_sms, &ps, opts_g().strip_cluster.load()) ==
+                            cudaSuccess &&
+                        ps.kind == 1 &&
                         colc_strips_supported(Ct, ps.Ls);
         cudaGetLastError();
         if (ok) {
@@ -1200,6 +1202,23 @@ static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out) {
     if (ctx->bs_state[Ct] != 1) return false;
     *out = ctx->bs_plan[Ct];
     return true;
+}
+
+// debug hook (not in include/dts.h): the FILTER column plan dts_solve uses for C_t on this
+// context -- out[0..6] = kind, CB, grid, threads, HS (0: one strip), ntiles, rows per segment
+int32_t dts_debug_col_plan(dts_ctx* ctx, int32_t Ct, int32_t* out) {
+    if (!ctx || !out || Ct < 1) return -1;
+    ColPlan p{};
+    if (!batch_strip_plan(ctx, Ct, &p) &&
+        (ctx->comm ? plan_col_pass(ctx->g, Ct, MODE_FILTER, ctx->num_sms, &p)
+                   : plan_col(ctx->g, Ct, MODE_FILTER, ctx->num_sms, &p)) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    if (p.kind == 1 && ctx->vs_n > 1 && Ct == 1) p = ctx->vs_plan;
+    const int32_t v[7] = {p.kind, p.CB, (int32_t)p.grid.x, p.threads, p.HS, p.ntiles, p.Ls};
+    for (int i = 0; i < 7; ++i) out[i] = v[i];
+    return 0;
 }
 
 // Box-filter context (reading R25): fixed-point increments, windows of every pass and the
