@@ -1204,6 +1204,29 @@ static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out) {
     return true;
 }
 
+// FILTER column pass i over the C_t planes at x, on plan cp (dts_solve's choice for C_t): row
+// strips + the seam fix-up for tall C_t = 1 images (plan_strips), the cluster kernel on A1
+// (image-high strips in batched contexts: cp.HS > 0), else the decoupled kernel on d_y.
+static dts_status col_filter_pass(dts_ctx* ctx, const ColPlan& cp, int Ct, int i, float* x, double bytes,
+                                  cudaStream_t s) {
+    const Geometry& g = ctx->g;
+    const bool strips = Ct == 1 && ctx->vs_n > 1 && cp.kind == 1 && !ctx->comm && opts_g().col_strips.load();
+    dts_status st = run_launch(ctx, F_COL, bytes, s, [&] {
+        if (strips)  // row strips (plan_strips); the seams are fixed by the launch that follows
+            return launch_col_cluster(ctx->vs_plan, g, 1, MODE_FILTER, x, ctx->A1y, ctx->kc[i], nullptr, nullptr, s, i,
+                                      nullptr, nullptr, nullptr, ctx->vs_edge);
+        if (cp.kind == 1 && ctx->A1y && i < 4)
+            return launch_col_cluster(cp, g, Ct, MODE_FILTER, x, ctx->A1y, ctx->kc[i], nullptr, nullptr, s, i);
+        return col_launch(ctx, cp, Ct, MODE_FILTER, x, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
+    });
+    if (st == DTS_OK && strips)
+        st = run_launch(ctx, F_SEAM, (double)g.W * 12.0 * (ctx->vs_n - 1) * 2 * ctx->vs_L[i], s, [&] {
+            return launch_seam_fix(x, 1, g, ctx->vs_HS, ctx->vs_n, ctx->vs_L[i], ctx->vs_gam[i], ctx->vs_theta[i],
+                                   ctx->vs_edge, s);
+        });
+    return st;
+}
+
 // debug hook (not in include/dts.h): the FILTER column plan dts_solve uses for C_t on this
 // context -- out[0..6] = kind, CB, grid, threads, HS (0: one strip), ntiles, rows per segment
 int32_t dts_debug_col_plan(dts_ctx* ctx, int32_t Ct, int32_t* out) {
@@ -1525,26 +1548,6 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                 }
                 return DTS_OK;
             }
-            // FILTER column pass i: the cluster kernel on A1 = a_1^{d_y} squared i times when
-            // the context holds it, else on d_y
-            const bool strips = Ct == 1 && ctx->vs_n > 1 && cpf.kind == 1 && !ctx->comm && opts_g().col_strips.load();
-            auto col_filter = [&](int i) -> cudaError_t {
-                if (strips)  // row strips (plan_strips); the seams are fixed by the launch that follows
-                    return launch_col_cluster(ctx->vs_plan, g, Ct, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr,
-                                              nullptr, s, i, nullptr, nullptr, nullptr, ctx->vs_edge);
-                if (cpf.kind == 1 && ctx->A1y && i < 4)
-                    return launch_col_cluster(cpf, g, Ct, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr, nullptr,
-                                              s, i);
-                return col_launch(ctx, cpf, Ct, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
-            };
-            // the seam carries of strip column pass i (plan_strips): the fix-up kernel after it
-            auto seam_fix = [&](int i) -> dts_status {
-                if (!strips) return DTS_OK;
-                return run_launch(ctx, F_SEAM, px * 12.0 * (ctx->vs_n - 1) * 2 * ctx->vs_L[i] / (double)g.H, s, [&] {
-                    return launch_seam_fix(ctx->X, Ct, g, ctx->vs_HS, ctx->vs_n, ctx->vs_L[i], ctx->vs_gam[i],
-                                           ctx->vs_theta[i], ctx->vs_edge, s);
-                });
-            };
             // The last column pass of an iteration is a FILTER pass; Eq. (3) of iteration k-1 is
             // applied inside iteration k's first row pass (k_row.cu ROWUPD: Z, T, chat read
             // coalesced while the row lands) and one update kernel closes the solve.  The
@@ -1587,8 +1590,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                                                  upd_bytes, s, i);
                         }
                     } else if (!last || split_update) {
-                        st = run_launch(ctx, F_COL, row_bytes, s, [&] { return col_filter(i); });
-                        if (st == DTS_OK) st = seam_fix(i);
+                        st = col_filter_pass(ctx, cpf, Ct, i, ctx->X, row_bytes, s);
                         if (st != DTS_OK) return st;
                         if (!last || (rowupd && k + 1 < iterations)) continue;  // the next row pass applies Eq. (3)
                         st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
@@ -1650,15 +1652,17 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->last_stream = s;
     RowPlan rp;
-    ColPlan cp, cp1;
-    if (plan_row_pass(g, 2, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess ||
-        plan_col(g, 2, MODE_FILTER, ctx->num_sms, &cp) != cudaSuccess)
-        return DTS_E_SHAPE;
+    ColPlan cp{}, cp1{};
+    if (plan_row_pass(g, 2, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess) return DTS_E_SHAPE;
+    const bool two = batch_strip_plan(ctx, 2, &cp) || plan_col(g, 2, MODE_FILTER, ctx->num_sms, &cp) == cudaSuccess;
     // when two planes do not fit the cluster column kernel (tall images) but one does, the
-    // column passes run plane by plane on it
-    const bool per_plane = cp.kind != 1 && plan_col(g, 1, MODE_FILTER, ctx->num_sms, &cp1) == cudaSuccess &&
+    // column passes run plane by plane on it (over row strips where dts_solve uses them)
+    const bool per_plane = !(two && cp.kind == 1) &&
+                           (batch_strip_plan(ctx, 1, &cp1) ||
+                            plan_col(g, 1, MODE_FILTER, ctx->num_sms, &cp1) == cudaSuccess) &&
                            cp1.kind == 1;
     cudaGetLastError();
+    if (!two && !per_plane) return DTS_E_SHAPE;
     const PtrKind kt = classify(target, ctx->device), kc = classify(conf_out, ctx->device),
                   kv = var_out ? classify(var_out, ctx->device) : PTR_DEVICE;
     if (kt == PTR_BAD || kc == PTR_BAD || kv == PTR_BAD) return DTS_E_ARG;
@@ -1675,7 +1679,7 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
         t_d = ctx->st_t;
     }
     if ((st = ensure_solver_state(ctx, 2, s)) != DTS_OK) return st;
-    if ((st = ensure_col_scratch(ctx, cp, s)) != DTS_OK) return st;
+    if (!per_plane && (st = ensure_col_scratch(ctx, cp, s)) != DTS_OK) return st;
     const double px = (double)g.H * g.W;
     // planes [t ; t^2] -> DTF (N passes of rows then columns) -> Eq. (7)
     st = run_launch(ctx, F_CONF, px * 12.0, s, [&] { return launch_conf_prologue(t_d, g, ctx->X, s); });
@@ -1683,21 +1687,9 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
         st = run_launch(ctx, F_ROW, px * 20.0, s, [&] {
             return launch_row_pass(rp, g, 2, MODE_FILTER, ctx->X, ctx->X, ctx->dx, ctx->kc[i], s);
         });
-        if (st == DTS_OK && !per_plane)
-            st = run_launch(ctx, F_COL, px * 20.0, s, [&] {
-                if (cp.kind == 1 && ctx->A1y && i < 4)  // pass-1 coefficient, squared per pass
-                    return launch_col_cluster(cp, g, 2, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr, nullptr,
-                                              s, i);
-                return col_launch(ctx, cp, 2, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
-            });
+        if (st == DTS_OK && !per_plane) st = col_filter_pass(ctx, cp, 2, i, ctx->X, px * 20.0, s);
         for (int v = 0; v < 2 && st == DTS_OK && per_plane; ++v)
-            st = run_launch(ctx, F_COL, px * 12.0, s, [&] {
-                if (cp1.kind == 1 && ctx->A1y && i < 4)
-                    return launch_col_cluster(cp1, g, 1, MODE_FILTER, ctx->X + v * g.plane, ctx->A1y, ctx->kc[i],
-                                              nullptr, nullptr, s, i);
-                return col_launch(ctx, cp1, 1, MODE_FILTER, ctx->X + v * g.plane, ctx->dy, ctx->kc[i], nullptr,
-                                  nullptr, s);
-            });
+            st = col_filter_pass(ctx, cp1, 1, i, ctx->X + v * g.plane, px * 12.0, s);
     }
     const float inv = 1.f / (2.f * sigma_c * sigma_c);
     if (st == DTS_OK)
@@ -1731,9 +1723,9 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->last_stream = s;
     RowPlan rp;
-    ColPlan cp;
+    ColPlan cp{};
     if (plan_row_pass(g, 1, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess ||
-        plan_col(g, 1, MODE_FILTER, ctx->num_sms, &cp) != cudaSuccess)
+        !(batch_strip_plan(ctx, 1, &cp) || plan_col(g, 1, MODE_FILTER, ctx->num_sms, &cp) == cudaSuccess))
         return DTS_E_SHAPE;
     cudaGetLastError();
     const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),
@@ -1794,14 +1786,7 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
                     st = run_launch(ctx, F_ROW, px * 12.0, s, [&] {
                         return launch_row_pass(rp, g, 1, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
                     });
-                    if (st == DTS_OK)
-                        st = run_launch(ctx, F_COL, px * 12.0, s, [&] {
-                            if (cp.kind == 1 && ctx->A1y && i < 4)  // pass-1 coefficient, squared per pass
-                                return launch_col_cluster(cp, g, 1, MODE_FILTER, ctx->X, ctx->A1y, ctx->kc[i], nullptr,
-                                                          nullptr, s, i);
-                            return col_launch(ctx, cp, 1, MODE_FILTER, ctx->X, ctx->dy, ctx->kc[i], nullptr, nullptr,
-                                              s);
-                        });
+                    if (st == DTS_OK) st = col_filter_pass(ctx, cp, 1, i, ctx->X, px * 12.0, s);
                 }
                 float* ohw = (k + 1 == iterations) ? o_d : nullptr;
                 if (st == DTS_OK)

@@ -102,3 +102,13 @@ def test_confidence_then_solve():
         out = s.solve(td, c, cfg.lam, cfg.iters)
     torch.cuda.synchronize()
     assert np.max(np.abs(out.cpu().numpy() - ref)) <= 1e-4 * target_range(t)
+
+
+def test_confidence_per_plane_over_row_strips():
+    """Too tall for the two-plane cluster column kernel (C_t = 2 holds <= 5120 rows): the passes
+    run plane by plane, over row strips with the seam fix-up (forced: col_strips = 2)."""
+    g, t, _ = random_problem(5400, 160, 3, 1, seed=5)
+    with dts.options(col_strips=2):
+        with dts.Solver(torch.from_numpy(g).cuda(), 6.0, 0.2, 3) as s:
+            assert dts.debug_strips(s.ctx)["strips"] == 2
+        check(g, t, 6.0, 0.2, 3, 0.3)

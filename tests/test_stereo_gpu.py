@@ -173,3 +173,16 @@ def test_stereo_paper_constants_iteration_counts(iters):
     L, t, c = make_inputs("C1")
     R = right_image(L, 16, 1)
     check(L, R, t, c, cfg.sigma_s, cfg.sigma_r, cfg.N, cfg.lam, iters, gamma=0.001, eps=0.001)
+
+
+def test_stereo_over_row_strips():
+    """A tall image whose column passes run over row strips (forced: col_strips = 2) with the
+    seam fix-up: stereo parity unchanged."""
+    L, _, c = random_problem(2600, 200, 3, 1, seed=41)
+    R = right_image(L, 2, 42)
+    t = np.random.default_rng(43).uniform(0, 8, (2600, 200)).astype(np.float32)
+    with dts.options(col_strips=2):
+        Ld = torch.from_numpy(L).cuda()
+        with dts.Solver(Ld, 6.0, 0.2, 3) as s:
+            assert dts.debug_strips(s.ctx)["strips"] == 2
+        check(L, R, t, c, 6.0, 0.2, 3, 0.99, 5, 0.001, 1.0)
