@@ -1,18 +1,20 @@
 #!/bin/bash
 # Profiling recipe used for profiles/ (run under gpurun on one B200; see B200_PROFILING.md).
-# 1) the plain run must exit 0; 2) launch list of one full timed C4 step (127 launches: guide
-# derivative, bottom-link fill, support row + column, A1 fill, prologue, 20 x [3 row, 3 column]
-# with iterations 2-20 taking the previous Eq. (3) step in their first row pass, and one
-# closing update); 3) one `--set full` capture per kernel family (steady-state launches;
-# k_row_pass launch 4 of a step is the first ROWUPD instance); 4) launch list of one eager C1
-# solve (302 launches) for the launch-gap breakdown (kernel time vs the event-timed solve).
+# 1) the plain run must exit 0; 2) launch list of one full timed C4 step (199 launches: guide
+# derivative, bottom-link fill, support row + column, A1 fill, the row-strip plan's edge
+# lengths and profiles (2 strips x 3 passes), prologue, 20 x [3 row, 3 column over the strips,
+# 3 seam fix-ups] with iterations 2-20 taking the previous Eq. (3) step in their first row
+# pass, and one closing update); 3) one `--set full` capture per kernel family (steady-state
+# launches; k_row_pass launch 5 of a step is the first ROWUPD instance); 4) launch list of one
+# eager C1 solve (302 launches) for the launch-gap breakdown (kernel time vs the event-timed
+# solve).
 set -u
 OUT=${OUT:-gpurun_out}
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-extras"
 $CMD > $OUT/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -s 127 -c 127 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
-for spec in "k_col_cluster 4" "k_row_pass 2" "k_row_pass 4 row_update" "k_update 1" "k_guide_deriv 1" "k_prologue 1"; do
+    -s 199 -c 199 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
+for spec in "k_col_cluster 4" "k_row_pass 2" "k_row_pass 4 row_update" "k_update 1" "k_guide_deriv 1" "k_prologue 1" "k_seam_fix 2"; do
   set -- $spec
   tag=${3:-$1}
   ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 \

@@ -21,9 +21,11 @@ from collections import defaultdict
 HERE = os.path.dirname(os.path.abspath(__file__))
 FAMILY = [("k_col_cluster", "col_pass (cluster)"), ("k_col_pass", "col_pass (band tuples)"),
           ("k_row_pass", "row_pass"), ("k_update", "update"), ("k_guide_deriv", "guide_deriv"),
-          ("k_prologue", "prologue"), ("k_rank_compose", "rank_compose")]
+          ("k_prologue", "prologue"), ("k_rank_compose", "rank_compose"), ("k_seam_fix", "seam_fix"),
+          ("k_edge_length", "edge_length (create)"), ("k_edge_profiles", "edge_profiles (create)")]
 BENCH_NAME = {"k_col_cluster": "col_pass", "k_row_pass": "row_pass", "k_update": "update",
-              "k_guide_deriv": "guide_deriv", "k_prologue": "prologue", "k_col_pass": "col_pass"}
+              "k_guide_deriv": "guide_deriv", "k_prologue": "prologue", "k_col_pass": "col_pass",
+              "k_seam_fix": "seam_fix"}
 
 
 def row_mode(name):
