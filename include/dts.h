@@ -296,7 +296,8 @@ dts_status dts_create_band(const float* guide_with_halo, int64_t H_total, int64_
  *                  bands allow it (default), 1 cluster TUPLE/APPLY, 2 decoupled kernel
  *   "graphs"       1 replay repeated identical solves as CUDA graphs (default), 0 never
  *   "row_update"   1 Eq. (3) step fused into the next iteration's first row pass (default)
- *   "col_rows"     0 auto (default), 32 or 40: rows per warp segment of the C_t = 1 column kernel
+ *   "col_rows"     0 auto (default); rows per warp segment of the cluster column kernel: 32 or
+ *                  40 (C_t = 1), 12 or 16 (C_t = 3)
  *   "col_cluster"  0 auto (default), 1..16: forced column-kernel cluster size
  * Returns DTS_E_ARG for an unknown name or value.  dts_get_option returns -1 for unknown names. */
 dts_status dts_set_option(const char* name, int32_t value);

@@ -74,7 +74,8 @@ struct Options {
     std::atomic<int> band_scheme{0};  // 0: edge fix-up when bands are tall enough, 1: TUPLE/APPLY, 2: decoupled
     std::atomic<int> graphs{1};       // replay repeated identical solves as CUDA graphs
     std::atomic<int> row_update{1};   // Eq. (3) step fused into the next iteration's first row pass
-    std::atomic<int> col_rows{0};     // column kernel rows per warp segment: 0 auto, 32 or 40 (C_t = 1)
+    std::atomic<int> col_rows{0};     // column kernel rows per warp segment: 0 auto; 32 or 40 (C_t = 1),
+                                      // 12 or 16 (C_t = 3)
     std::atomic<int> col_cluster{0};  // column kernel cluster size: 0 auto, else forced (experiments)
     std::atomic<int> strip_cluster{0};     // row strips: forced cluster size of the strip plan (0 = auto)
     std::atomic<int> col_strips{1};   // tall single-context images: C_t = 1 column passes over row strips
@@ -293,8 +294,23 @@ dts_status ensure_staging(dts_ctx* ctx, size_t bytes_per_image, cudaStream_t s) 
 cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int force_cb = -1) {
     if (opts_g().col_kernel.load() == 0) {
         // C_t >= 2 FILTER: 16-row segments (20 warps per CTA) when the column fits a cluster
-        if (Ct >= 2 && mode == MODE_FILTER &&
-            plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 16, force_cb) == cudaSuccess)
+        const int rows2 = opts_g().col_rows.load();
+        if (Ct >= 2 && mode == MODE_FILTER && rows2 != 12 &&
+            plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 16, force_cb) == cudaSuccess) {
+            // C_t = 3 with many tile rounds per launch (throughput-bound): 12-row segments, 20
+            // warps on a C3 band of 240 rows instead of 15 (batched C3, 64 rounds: 0.432 ms
+            // against 0.445; one C3 image, 8 rounds: 63.7 us against 61.0, so not there)
+            const int rounds = (plan->ntiles + (int)(plan->grid.x / plan->CB) - 1) / (int)(plan->grid.x / plan->CB);
+            ColPlan p12{};
+            if (Ct == 3 && (rows2 == 12 || (rows2 == 0 && rounds >= 16)) &&
+                plan_col_cluster_ls(g, Ct, mode, num_sms, &p12, 12, force_cb) == cudaSuccess && p12.CB == plan->CB)
+                *plan = p12;
+            cudaGetLastError();
+            return cudaSuccess;
+        }
+        cudaGetLastError();
+        if (Ct == 3 && mode == MODE_FILTER && rows2 == 12 &&
+            plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 12, force_cb) == cudaSuccess)
             return cudaSuccess;
         cudaGetLastError();
         if (plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 32, force_cb) == cudaSuccess) {
@@ -596,7 +612,8 @@ dts_status dts_set_option(const char* name, int32_t value) {
     else if (n == "band_scheme" && value >= 0 && value <= 2) o.band_scheme = value;
     else if (n == "graphs" && (value == 0 || value == 1)) o.graphs = value;
     else if (n == "row_update" && (value == 0 || value == 1)) o.row_update = value;
-    else if (n == "col_rows" && (value == 0 || value == 32 || value == 40)) o.col_rows = value;
+    else if (n == "col_rows" && (value == 0 || value == 12 || value == 16 || value == 32 || value == 40))
+        o.col_rows = value;
     else if (n == "col_cluster" && value >= 0 && value <= 16) o.col_cluster = value;
     else if (n == "col_strips" && value >= 0 && value <= 64) o.col_strips = value;
     else if (n == "strip_cluster" && value >= 0 && value <= 16) o.strip_cluster = value;

@@ -164,7 +164,7 @@ constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
 // STRIPS: the tiles cover row strips of p.HS rows (tile -> (strip, column tile)); a separate
 // instantiation so that the one-strip kernels keep their code
 template <int CT, int MODE, bool PRE, int LSV = LS, bool STRIPS = false>
-__global__ void __launch_bounds__(LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()), 1)
+__global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()), 1)
     k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
     constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
     constexpr bool HASX = MODE != MODE_SUPPORT;
@@ -953,9 +953,9 @@ template <int CT, int MODE, bool PRE = false>
 static const void* kptr_band() {
     return reinterpret_cast<const void*>(colc::k_col_cluster_band<CT, MODE, PRE, true>);
 }
-template <int CT, bool PRE>
+template <int CT, bool PRE, int LSV = 16>
 static const void* kptr16() {
-    return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE_FILTER, PRE, 16>);
+    return reinterpret_cast<const void*>(colc::k_col_cluster<CT, MODE_FILTER, PRE, LSV>);
 }
 static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = false, int ls = colc::LS,
                                bool strips = false) {
@@ -965,7 +965,12 @@ static const void* colc_kernel(int Ct, int mode, bool pre = false, bool band = f
         if (Ct == 1 && ls == 32) return reinterpret_cast<const void*>(colc::k_col_cluster<1, MODE_FILTER, true, 32, true>);
         if (Ct == 2 && ls == 16) return reinterpret_cast<const void*>(colc::k_col_cluster<2, MODE_FILTER, true, 16, true>);
         if (Ct == 3 && ls == 16) return reinterpret_cast<const void*>(colc::k_col_cluster<3, MODE_FILTER, true, 16, true>);
+        if (Ct == 3 && ls == 12) return reinterpret_cast<const void*>(colc::k_col_cluster<3, MODE_FILTER, true, 12, true>);
         return nullptr;
+    }
+    if (ls == 12) {  // C_t = 3 FILTER: 12-row segments, up to 24 warps per CTA
+        if (mode != MODE_FILTER || band || Ct != 3) return nullptr;
+        return pre ? kptr16<3, true, 12>() : kptr16<3, false, 12>();
     }
     if (ls == 40) {  // 16 warps x 40-row segments, C_t = 1 FILTER
         if (mode != MODE_FILTER || band || Ct != 1) return nullptr;
@@ -1038,7 +1043,7 @@ static cudaError_t plan_col_cluster_uncached(const Geometry& g, int Ct, int mode
     cudaError_t e = cudaFuncGetAttributes(&fa, fn);
     if (e != cudaSuccess) return e;
     int Smax = fa.maxThreadsPerBlock / colc::TW;
-    if (Smax > 20) Smax = 20;
+    if (Smax > (ls >= 16 ? 20 : 24)) Smax = ls >= 16 ? 20 : 24;
     // attributes are per function and shared by every plan: allow non-portable clusters and
     // the opt-in shared memory maximum (so that no plan lowers another's limit); the
     // A1-input (and, at 32-row segments, row-band) variants of the FILTER kernel get the same
@@ -1047,7 +1052,7 @@ static cudaError_t plan_col_cluster_uncached(const Geometry& g, int Ct, int mode
         (e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
         return e;
     const bool f32 = mode == MODE_FILTER && ls == colc::LS;
-    const bool strip = mode == MODE_FILTER && ((Ct == 1 && (ls == 32 || ls == 40)) || (Ct >= 2 && ls == 16));
+    const bool strip = mode == MODE_FILTER && ((Ct == 1 && (ls == 32 || ls == 40)) || (Ct >= 2 && ls <= 16));
     for (const void* f : {fn, mode == MODE_FILTER ? colc_kernel(Ct, mode, true, false, ls) : fn,
                           f32 ? colc_kernel(Ct, mode, false, true) : fn, f32 ? colc_kernel(Ct, mode, true, true) : fn,
                           strip ? colc_kernel(Ct, mode, true, false, ls, true) : fn}) {

@@ -143,3 +143,20 @@ def test_batch_argument_errors():
         assert ctx.value is None
     assert lib.dts_create_batch(g.data_ptr(), 1 << 20, 1 << 20, 8, 3, 8.0, 0.2, 3, None, ctypes.byref(ctx)) == \
         2  # DTS_E_SHAPE
+
+
+@pytest.mark.parametrize("rows", [12, 16])
+def test_three_channel_segment_lengths(rows):
+    """C_t = 3 column kernel at 12- and 16-row warp segments (option col_rows; the batched C3
+    plan takes 12): parity with the oracle, batched and single."""
+    B, H, W = 2, 700, 150
+    ps, g, t, c = problems(B, H, W, 3, 3, seed=rows)
+    with dts.options(col_rows=rows):
+        with dts.Solver(torch.from_numpy(g).cuda(), 10.0, 0.2, 3, batched=True) as s:
+            assert dts.debug_col_plan(s.ctx, 3)["Ls"] == rows
+        got = batch_solve(g, t, c, 10.0, 0.2, 3, 0.99, 3)
+        one = single_solve(*ps[0], 10.0, 0.2, 3, 0.99, 3)
+    for b, (gb, tb, cb) in enumerate(ps):
+        ref = oracle.solve(gb, tb, cb, 10.0, 0.2, 3, 0.99, 3)
+        assert float(np.max(np.abs(got[b] - ref))) <= TOL * target_range(tb)
+    assert float(np.max(np.abs(one - oracle.solve(*ps[0], 10.0, 0.2, 3, 0.99, 3)))) <= TOL * target_range(ps[0][1])
