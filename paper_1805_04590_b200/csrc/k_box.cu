@@ -156,6 +156,50 @@ __device__ __forceinline__ void walk(const uint32_t* __restrict__ q, int64_t str
     }
 }
 
+// the same walk with the radius count NR fixed at compile time: off[] stays in registers (the
+// generic walk keeps it in local memory, which is what bounded K_B2: 2.45 ms on C4)
+template <int NR, int DIR>
+__device__ __forceinline__ void walk_t(const uint32_t* __restrict__ q, int64_t stride, int64_t i, int64_t n,
+                                       const Radii& rd, int* off) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) off[k] = 0;
+    long long dist = 0;
+    int steps = 0;
+    int64_t j = i;
+#pragma unroll 1
+    while (DIR < 0 ? j > 0 : j + 1 < n) {
+        const long long nd = dist + (long long)__ldg(q + (DIR < 0 ? j : j + 1) * stride);
+        if (nd > rd.Rmax) break;
+        dist = nd;
+        ++steps;
+        j += DIR;
+#pragma unroll
+        for (int k = 0; k < NR; ++k)
+            if (dist <= rd.R[k]) off[k] = steps;
+    }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_box_windows_t(const uint32_t* __restrict__ qx, const uint32_t* __restrict__ qy,
+                                                       int64_t H, int64_t W, int64_t pitch, int64_t plane, Radii rd,
+                                                       uint32_t* __restrict__ win, float* __restrict__ S) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = blockIdx.y;
+    if (c >= W || r >= H) return;
+    int lo[NR], hi[NR];
+    constexpr int np = NR - 1;
+    walk_t<NR, -1>(qx + r * pitch, 1, c, W, rd, lo);
+    walk_t<NR, +1>(qx + r * pitch, 1, c, W, rd, hi);
+#pragma unroll
+    for (int k = 0; k < np; ++k) win[(2 * k) * plane + r * pitch + c] = (uint32_t)lo[k] | ((uint32_t)hi[k] << 16);
+    const float cx = (float)(lo[np] + hi[np] + 1);
+    walk_t<NR, -1>(qy + c, pitch, r, H, rd, lo);
+    walk_t<NR, +1>(qy + c, pitch, r, H, rd, hi);
+#pragma unroll
+    for (int k = 0; k < np; ++k) win[(2 * k + 1) * plane + r * pitch + c] = (uint32_t)lo[k] | ((uint32_t)hi[k] << 16);
+    S[r * pitch + c] = cx * (float)(lo[np] + hi[np] + 1);
+}
+
 __global__ void __launch_bounds__(256) k_box_windows(const uint32_t* __restrict__ qx, const uint32_t* __restrict__ qy,
                                                      int64_t H, int64_t W, int64_t pitch, int64_t plane, Radii rd,
                                                      uint32_t* __restrict__ win, float* __restrict__ S) {
@@ -453,7 +497,13 @@ cudaError_t launch_box_windows(const uint32_t* qx, const uint32_t* qy, const Geo
         if (R[k] > rd.Rmax) rd.Rmax = R[k];
     }
     dim3 grid((unsigned)((g.W + 255) / 256), (unsigned)g.H);
-    box::k_box_windows<<<grid, 256, 0, s>>>(qx, qy, g.H, g.W, g.pitch, g.plane, rd, win, S);
+    switch (nR) {  // N = 1..4 passes (+ the support radius): registers; otherwise the generic walk
+        case 2: box::k_box_windows_t<2><<<grid, 256, 0, s>>>(qx, qy, g.H, g.W, g.pitch, g.plane, rd, win, S); break;
+        case 3: box::k_box_windows_t<3><<<grid, 256, 0, s>>>(qx, qy, g.H, g.W, g.pitch, g.plane, rd, win, S); break;
+        case 4: box::k_box_windows_t<4><<<grid, 256, 0, s>>>(qx, qy, g.H, g.W, g.pitch, g.plane, rd, win, S); break;
+        case 5: box::k_box_windows_t<5><<<grid, 256, 0, s>>>(qx, qy, g.H, g.W, g.pitch, g.plane, rd, win, S); break;
+        default: box::k_box_windows<<<grid, 256, 0, s>>>(qx, qy, g.H, g.W, g.pitch, g.plane, rd, win, S);
+    }
     return cudaGetLastError();
 }
 
