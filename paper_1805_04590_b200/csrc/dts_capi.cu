@@ -78,6 +78,7 @@ struct Options {
                                       // 12 or 16 (C_t = 3)
     std::atomic<int> col_cluster{0};  // column kernel cluster size: 0 auto, else forced (experiments)
     std::atomic<int> strip_cluster{0};     // row strips: forced cluster size of the strip plan (0 = auto)
+    std::atomic<int> band_overlap{1};  // row bands, edge scheme: all-gather overlapped with the next row pass
     std::atomic<int> col_strips{1};   // tall single-context images: C_t = 1 column passes over row strips
                                       // (0 off, 1 auto, n >= 2: exactly n strips when they fit)
 };
@@ -162,6 +163,17 @@ struct dts_ctx {
     std::vector<uintptr_t> graph_seen;  // key of the last eager solve: a repeat is captured
     int64_t graph_launches = 0;
     cudaStream_t cap_stream = nullptr;
+    // row-band edge scheme, overlapped: a FILTER column pass followed by a
+    // row pass leaves its all-gather on comm_stream and its edge fix-up pending; the next row
+    // pass runs on the band's interior rows first, then waits for the exchange, fixes the L
+    // edge rows and filters them
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_cols = nullptr, ev_gath = nullptr;
+    struct {
+        bool on = false;
+        int pass = 0, L = 0, Ct = 0;
+        float* x = nullptr;
+    } pend;
     // per-iteration ||g||_inf (dts_solve_opts.resid_inf_out), as float bits
     unsigned int* resid = nullptr;
     int resid_cap = 0;
@@ -390,6 +402,21 @@ dts_status ensure_band_buffers(dts_ctx* ctx, cudaStream_t s) {
     return DTS_OK;
 }
 
+// the pending edge fix-up of an overlapped banded column pass: wait for its exchange, correct
+// the L rows at each band edge
+static dts_status finish_pending(dts_ctx* ctx, cudaStream_t s) {
+    if (!ctx->pend.on) return DTS_OK;
+    ctx->pend.on = false;
+    cudaError_t e = cudaStreamWaitEvent(s, ctx->ev_gath, 0);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const int L = ctx->pend.L, Ct = ctx->pend.Ct, pass = ctx->pend.pass;
+    float* x = ctx->pend.x;
+    return run_launch(ctx, F_COMPOSE, (double)2 * L * ctx->g.W * (8.0 * Ct + 4), s, [&] {
+        return launch_edge_fix(x, Ct, ctx->g, L, ctx->edge_gam[pass], ctx->edge_theta[pass], ctx->gathered,
+                               ctx->comm->nranks, ctx->comm->rank, s, true, true);
+    });
+}
+
 // One column pass of a row-band context.  Which scheme runs is
 // decided from state every rank shares (the band scheme latched at create from the
 // all-gathered band heights and decay lengths, and plans for the TALLEST band), so every
@@ -399,7 +426,7 @@ dts_status ensure_band_buffers(dts_ctx* ctx, cudaStream_t s) {
 //  - cluster TUPLE -> all-gather -> compose -> cluster FILTER with the external carries;
 //  - the same on the decoupled kernel (k_col.cu) when the band's columns do not fit a cluster.
 dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, const UpdateArgs* upd,
-                           float* support, int fam, double bytes, cudaStream_t s, int pass) {
+                           float* support, int fam, double bytes, cudaStream_t s, int pass, bool defer = false) {
     const Geometry& g = ctx->g;
     Geometry gmax = g;  // every rank plans for the tallest band: the same decision everywhere
     gmax.H = ctx->band_H_max;
@@ -442,13 +469,35 @@ dts_status col_pass_banded(dts_ctx* ctx, int Ct, int mode, float* x, float kc, c
             cudaSuccess)
             return cuda_fail(e);
         std::string err;
-        st = run_launch(ctx, F_EXCHANGE, (double)count * 4 * ctx->comm->nranks, s, [&] {
-            return comm_allgather(ctx->comm, ctx->rank_tup, ctx->gathered, count, s, &err) ? cudaSuccess
-                                                                                            : cudaErrorUnknown;
+        // overlapped: the exchange on the context's comm stream, the fix-up left pending for the
+        // next row pass (finish_pending)
+        const bool ovl = defer && mode == MODE_FILTER && ctx->comm->nranks > 1;
+        if (ovl) {
+            if ((!ctx->comm_stream &&
+                 (e = cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking)) != cudaSuccess) ||
+                (!ctx->ev_cols && (e = cudaEventCreateWithFlags(&ctx->ev_cols, cudaEventDisableTiming)) != cudaSuccess) ||
+                (!ctx->ev_gath && (e = cudaEventCreateWithFlags(&ctx->ev_gath, cudaEventDisableTiming)) != cudaSuccess) ||
+                (e = cudaEventRecord(ctx->ev_cols, s)) != cudaSuccess ||
+                (e = cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_cols, 0)) != cudaSuccess)
+                return cuda_fail(e);
+        }
+        cudaStream_t xs = ovl ? ctx->comm_stream : s;
+        st = run_launch(ctx, F_EXCHANGE, (double)count * 4 * ctx->comm->nranks, xs, [&] {
+            return comm_allgather(ctx->comm, ctx->rank_tup, ctx->gathered, count, xs, &err) ? cudaSuccess
+                                                                                             : cudaErrorUnknown;
         });
         if (st != DTS_OK) {
             g_last_error = err;
             return DTS_E_NCCL;
+        }
+        if (ovl) {
+            if ((e = cudaEventRecord(ctx->ev_gath, ctx->comm_stream)) != cudaSuccess) return cuda_fail(e);
+            ctx->pend.on = true;
+            ctx->pend.pass = pass;
+            ctx->pend.L = L;
+            ctx->pend.Ct = Ct;
+            ctx->pend.x = x;
+            return DTS_OK;
         }
         if (ctx->comm->nranks > 1)  // a single rank has no edges to correct
             st = run_launch(ctx, F_COMPOSE, (double)2 * L * g.W * (8.0 * Ct + 4), s, [&] {
@@ -617,6 +666,7 @@ dts_status dts_set_option(const char* name, int32_t value) {
     else if (n == "col_cluster" && value >= 0 && value <= 16) o.col_cluster = value;
     else if (n == "col_strips" && value >= 0 && value <= 64) o.col_strips = value;
     else if (n == "strip_cluster" && value >= 0 && value <= 16) o.strip_cluster = value;
+    else if (n == "band_overlap" && (value == 0 || value == 1)) o.band_overlap = value;
     else return DTS_E_ARG;
     return DTS_OK;
 }
@@ -643,6 +693,7 @@ int32_t dts_get_option(const char* name) {
     if (n == "col_cluster") return o.col_cluster;
     if (n == "col_strips") return o.col_strips;
     if (n == "strip_cluster") return o.strip_cluster;
+    if (n == "band_overlap") return o.band_overlap;
     return -1;
 }
 
@@ -1462,6 +1513,10 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         return DTS_E_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->last_stream = s;
+    if (ctx->pend.on) {  // a solve that failed mid-way left an exchange pending: order after it
+        ctx->pend.on = false;
+        cudaStreamWaitEvent(s, ctx->ev_gath, 0);
+    }
 
     const bool is_box = ctx->filter == DTS_FILTER_BOX;
     const bool want_resid = resid_out && iterations > 0;
@@ -1580,25 +1635,51 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
             ru.step = step;
             ru.out_hwc = nullptr;
             ru.resid = nullptr;
+            // row pass i over rows [r0, r0 + n) (the whole band, or part of it around a pending
+            // edge fix-up); upd: Eq. (3) of the previous iteration applied on the fly
+            auto row_rows = [&](int i, const float* in, bool upd, int64_t r0, int64_t n) -> dts_status {
+                if (n <= 0) return DTS_OK;
+                Geometry gs = g;  // rows r0.. of every plane (the plane stride stays)
+                gs.H = n;
+                RowPlan rps = rp;
+                if (n != g.H && plan_row_pass(gs, Ct, MODE_FILTER, ctx->num_sms, &rps) != cudaSuccess)
+                    return DTS_E_SHAPE;
+                const int64_t o = r0 * g.pitch;
+                if (upd) {
+                    UpdateArgs us = ru;
+                    us.Z = ru.Z + o;
+                    us.T = ru.T + o;
+                    us.chat = ru.chat + o;
+                    return run_launch(ctx, F_ROWUPD, (double)n * g.W * (20.0 * Ct + 8), s, [&] {
+                        return launch_row_update(rps, gs, Ct, ctx->X + o, ctx->X + o, ctx->dx + o, ctx->kc[i], us, s);
+                    });
+                }
+                return run_launch(ctx, F_ROW, (double)n * g.W * (8.0 * Ct + 4), s, [&] {
+                    return launch_row_pass(rps, gs, Ct, MODE_FILTER, in + o, ctx->X + o, ctx->dx + o, ctx->kc[i], s);
+                });
+            };
             for (int k = 0; k < iterations; ++k) {
                 for (int i = 0; i < ctx->N; ++i) {
                     const float* in = (i == 0) ? ctx->Z : ctx->X;
-                    if (rowupd && i == 0 && k > 0) {  // Eq. (3) of iteration k-1 in this row pass
-                        st = run_launch(ctx, F_ROWUPD, px * (20.0 * Ct + 8), s, [&] {
-                            return launch_row_update(rp, g, Ct, ctx->X, ctx->X, ctx->dx, ctx->kc[i], ru, s);
-                        });
+                    const bool upd = rowupd && i == 0 && k > 0;  // Eq. (3) of iteration k-1 in this row pass
+                    if (ctx->pend.on) {
+                        // overlapped band exchange: interior rows while the all-gather runs, then
+                        // the edge fix-up and the 2L edge rows
+                        const int64_t L = std::min<int64_t>(ctx->pend.L, g.H / 2);
+                        st = row_rows(i, in, upd, L, g.H - 2 * L);
+                        if (st == DTS_OK) st = finish_pending(ctx, s);
+                        if (st == DTS_OK) st = row_rows(i, in, upd, 0, L);
+                        if (st == DTS_OK) st = row_rows(i, in, upd, g.H - L, L);
                     } else {
-                        st = run_launch(ctx, F_ROW, row_bytes, s, [&] {
-                            return launch_row_pass(rp, g, Ct, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
-                        });
+                        st = row_rows(i, in, upd, 0, g.H);
                     }
                     if (st != DTS_OK) return st;
                     const bool last = i + 1 == ctx->N;
                     float* ohwc = (k + 1 == iterations) ? o_d : nullptr;
                     if (ctx->comm) {  // row-band mode: the exchange of DESIGN.md section 9
-                        if (!last || (rowupd && k + 1 < iterations)) {
+                        if (!last || (rowupd && k + 1 < iterations)) {  // a row pass follows: overlap
                             st = col_pass_banded(ctx, Ct, MODE_FILTER, ctx->X, ctx->kc[i], nullptr, nullptr, F_COL,
-                                                 row_bytes, s, i);
+                                                 row_bytes, s, i, opts_g().band_overlap.load() != 0);
                         } else {
                             UpdateArgs u = ru;
                             u.out_hwc = ohwc;
@@ -1870,6 +1951,12 @@ void dts_destroy(dts_ctx* ctx) {
         cudaGraphExecDestroy(ctx->graph_exec);
     }
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    if (ctx->comm_stream) {
+        cudaStreamSynchronize(ctx->comm_stream);
+        cudaStreamDestroy(ctx->comm_stream);
+    }
+    if (ctx->ev_cols) cudaEventDestroy(ctx->ev_cols);
+    if (ctx->ev_gath) cudaEventDestroy(ctx->ev_gath);
     delete ctx;
 }
 

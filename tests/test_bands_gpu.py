@@ -158,3 +158,18 @@ def test_bands_straddling_the_edge_threshold():
         with dts.options(band_scheme=scheme):
             a = solve_bands(g, t, c, *args, P=2)
         assert np.max(np.abs(a - ref)) <= 1e-4 * rng, scheme
+
+
+@pytest.mark.parametrize("Ct", [1, 3])
+def test_bands_overlapped_exchange_is_bit_identical(Ct):
+    """Edge scheme with the all-gather overlapped (default: the next row pass runs on the
+    band's interior rows while the exchange is in flight, then the edge fix-up and the 2L edge
+    rows) against the serial order (option band_overlap = 0): the same kernels on the same
+    rows, so the same bits; and parity with the oracle."""
+    g, t, c = random_problem(1200, 90, 3, Ct, seed=23 + Ct)
+    args = (6.0, 0.2, 3, 0.99, 5)
+    a = solve_bands(g, t, c, *args, P=3)
+    with dts.options(band_overlap=0):
+        b = solve_bands(g, t, c, *args, P=3)
+    np.testing.assert_array_equal(a, b)
+    assert np.max(np.abs(a - oracle.solve(g, t, c, *args))) <= 1e-4 * target_range(t)
