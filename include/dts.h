@@ -62,7 +62,11 @@ typedef enum {
 /* dts_create -- domain-transform setup for one guide image.
  *   guide          H x W x C fp32, HWC; read once.  Colours are used as given (no
  *                  clamping, R16); only differences of adjacent pixels matter.
- *   H, W, C        >= 1.  W <= 18432 (the row kernel holds whole rows).  The column
+ *   H, W, C        >= 1.  W <= 184320: the row kernel stages whole rows of every plane in
+ *                  shared memory (11520 columns at C_t = 4); wider rows run over up to 16
+ *                  vertical strips with a seam fix-up, which needs
+ *                  every pass's carry-decay length L (measured at create) to fit twice in a
+ *                  strip -- else DTS_E_SHAPE.  The column
  *                  kernels keep a column tile's bands co-resident, which bounds H per
  *                  context: on a 148-SM B200 at least 30000 rows for C_t = 1 and 6400 for
  *                  C_t = 3 (cluster kernel up to 10240 rows, decoupled kernel beyond).  A

@@ -119,6 +119,11 @@ struct dts_ctx {
     // column recurrences cut between them (d_y = +inf, A1 = 0 at each image's first row); the
     // FILTER column passes run every image's tiles in one launch (per-C_t strip plan, no seams)
     int64_t batch = 1, batch_H = 0;
+    // images wider than the row kernel's staging buffer (plan_row_strips): vertical strips,
+    // per pass (and the support, index N) the seam length and the per-row edge profiles
+    RowStrips hs{};
+    std::vector<int> hs_L;
+    std::vector<float*> hs_gam, hs_theta;  // [seam][H][L] each
     ColPlan bs_plan[5]{};
     signed char bs_state[5] = {0, 0, 0, 0, 0};  // 0 not planned, 1 planned, -1 not available
     int num_sms = 148;
@@ -190,12 +195,13 @@ namespace {
 enum Family {
     F_DERIV = 0, F_ROW, F_COL, F_UPDATE, F_SUPPORT_ROW, F_SUPPORT_COL, F_PROLOGUE, F_STEP,
     F_TUPLE, F_EXCHANGE, F_COMPOSE, F_ROWUPD, F_CONF, F_STEREO, F_FILL, F_BOX_PREP, F_BOX_ROW, F_BOX_COL, F_COEF,
-    F_SEAM, F_COUNT
+    F_SEAM, F_ROWSEAM, F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"guide_deriv", "row_pass", "col_pass", "col_update", "support_row",
                                      "support_col", "prologue", "update", "col_tuple", "exchange",
                                      "rank_compose", "row_update", "confidence", "stereo_update", "link_fill",
-                                     "box_windows", "box_row", "box_col", "edge_profiles", "seam_fix"};
+                                     "box_windows", "box_row", "box_col", "edge_profiles", "seam_fix",
+                                     "row_seam_fix"};
 
 // Process-wide kernel profiler (dts_profile_enable / dts_profile_read): contexts come
 // and go inside a timed step, the statistics outlive them.
@@ -758,6 +764,121 @@ const char* dts_status_string(dts_status s) {
 
 const char* dts_last_error_string(void) { return g_last_error.c_str(); }
 
+// Wide images: the row kernel stages whole rows of every plane in shared
+// memory, which holds 11520 columns at C_t = 4.  Wider images run their row passes over
+// vertical strips of at most that width with zero carries at the strip edges, and fix the
+// seams up with per-row edge profiles (reading R26 along x): planned here once, from d_x, with
+// each pass's (and the support's) measured carry-decay length L, which must fit twice in the
+// narrowest strip.
+constexpr int64_t kRowStripW = 11520;
+static dts_status plan_row_strips(dts_ctx* ctx, cudaStream_t s) {
+    const Geometry& g = ctx->g;
+    if (g.W <= kRowStripW) return DTS_OK;
+    const int n = (int)((g.W + kRowStripW - 1) / kRowStripW);
+    if (n > 16) {
+        g_last_error = "image too wide (more than 16 row strips)";
+        return DTS_E_SHAPE;
+    }
+    const int64_t WS = ((g.W + n - 1) / n + 31) / 32 * 32;
+    RowStrips st{};
+    st.n = n;
+    for (int b = 0; b < n; ++b) st.c[b] = (int)(b * WS);
+    st.c[n] = (int)g.W;
+    const int64_t minw = g.W - (int64_t)(n - 1) * WS;
+    const int N = ctx->N;
+    cudaError_t e;
+    unsigned* dlen = nullptr;
+    if ((e = cudaMallocAsync((void**)&dlen, 2 * (N + 1) * sizeof(unsigned), s)) != cudaSuccess ||
+        (e = cudaMemsetAsync(dlen, 0, 2 * (N + 1) * sizeof(unsigned), s)) != cudaSuccess)
+        return cuda_fail(e);
+    dts_status st2 = DTS_OK;
+    for (int i = 0; i <= N && st2 == DTS_OK; ++i) {
+        const float kc = i < N ? ctx->kc[i] : ctx->ks;
+        const int Lcap = (int)std::min<int64_t>(std::min<int64_t>((int64_t)std::ceil(26.0 / kc), minw), 1 << 20);
+        st2 = run_launch(ctx, F_COEF, (double)g.H * Lcap * 8.0, s,
+                         [&] { return launch_row_edge_length(ctx->dx, g, st, Lcap, kc, dlen + 2 * i, s); });
+    }
+    std::vector<unsigned> len(2 * (N + 1), 0);
+    if (st2 == DTS_OK &&
+        ((e = cudaMemcpyAsync(len.data(), dlen, len.size() * sizeof(unsigned), cudaMemcpyDeviceToHost, s)) !=
+             cudaSuccess ||
+         (e = cudaStreamSynchronize(s)) != cudaSuccess))
+        st2 = cuda_fail(e);
+    cudaFreeAsync(dlen, s);
+    if (st2 != DTS_OK) return st2;
+    std::vector<int> L(N + 1);
+    for (int i = 0; i <= N; ++i) {
+        L[i] = (int)std::max<unsigned>(1u, std::max(len[2 * i], len[2 * i + 1]));
+        if (2 * (int64_t)L[i] + 1 > minw) {
+            g_last_error = "image too wide for row strips at this sigma (a seam correction would overlap)";
+            return DTS_E_SHAPE;
+        }
+    }
+    ctx->hs_gam.assign(N + 1, nullptr);
+    ctx->hs_theta.assign(N + 1, nullptr);
+    for (int i = 0; i <= N && st2 == DTS_OK; ++i) {
+        const size_t bytes = (size_t)(n - 1) * g.H * L[i] * sizeof(float);
+        if ((e = cudaMallocAsync((void**)&ctx->hs_gam[i], bytes, s)) != cudaSuccess ||
+            (e = cudaMallocAsync((void**)&ctx->hs_theta[i], bytes, s)) != cudaSuccess)
+            return cuda_fail(e);
+        const float kc = i < N ? ctx->kc[i] : ctx->ks;
+        st2 = run_launch(ctx, F_COEF, (double)(n - 1) * g.H * L[i] * 12.0, s, [&] {
+            return launch_row_edge_profiles(ctx->dx, g, st, L[i], kc, ctx->hs_gam[i], ctx->hs_theta[i], i == N, s);
+        });
+    }
+    if (st2 != DTS_OK) return st2;
+    ctx->hs = st;
+    ctx->hs_L = L;
+    return DTS_OK;
+}
+
+// Row pass over rows [r0, r0 + n) of every plane (pass i, or the support when pass < 0; upd:
+// the ROWUPD variant with Eq. (3) applied on the fly): one launch when the row fits the
+// kernel's staging buffer, else one per row strip and the seam fix-up (plan_row_strips).
+static dts_status row_pass_x(dts_ctx* ctx, int Ct, int mode, int pass, const float* in, float* out,
+                             const UpdateArgs* upd, int64_t r0, int64_t n, int fam, double bytes, cudaStream_t s) {
+    if (n <= 0) return DTS_OK;
+    const Geometry& g = ctx->g;
+    Geometry gs = g;  // rows r0.. of every plane (the plane stride stays)
+    gs.H = n;
+    const int64_t o = r0 * g.pitch;
+    const float kc = pass >= 0 ? ctx->kc[pass] : ctx->ks;
+    const int pmode = mode == MODE_SUPPORT ? MODE_SUPPORT : MODE_FILTER;
+    auto launch = [&](const RowPlan& p, const Geometry& gg, int64_t c0) -> cudaError_t {
+        const int64_t oo = o + c0;
+        if (upd) {
+            UpdateArgs us = *upd;
+            us.Z += oo;
+            us.T += oo;
+            us.chat += oo;
+            return launch_row_update(p, gg, Ct, in + oo, out + oo, ctx->dx + oo, kc, us, s);
+        }
+        return launch_row_pass(p, gg, Ct, mode, in ? in + oo : nullptr, out + oo, ctx->dx + oo, kc, s);
+    };
+    RowPlan rp{};
+    if (plan_row_pass(gs, Ct, pmode, ctx->num_sms, &rp) == cudaSuccess)
+        return run_launch(ctx, fam, bytes, s, [&] { return launch(rp, gs, 0); });
+    cudaGetLastError();
+    const RowStrips& st = ctx->hs;
+    if (st.n < 2) return DTS_E_SHAPE;
+    for (int b = 0; b < st.n; ++b) {
+        Geometry gb = gs;
+        gb.W = st.c[b + 1] - st.c[b];
+        RowPlan pb{};
+        if (plan_row_pass(gb, Ct, pmode, ctx->num_sms, &pb, (gb.W + 3) / 4 * 4) != cudaSuccess) return DTS_E_SHAPE;
+        const dts_status r = run_launch(ctx, fam, bytes * (double)gb.W / (double)g.W, s,
+                                        [&] { return launch(pb, gb, st.c[b]); });
+        if (r != DTS_OK) return r;
+    }
+    const int li = pass >= 0 ? pass : ctx->N;
+    const int L = ctx->hs_L[li];
+    const int planes = mode == MODE_SUPPORT ? 1 : Ct;
+    return run_launch(ctx, F_ROWSEAM, (double)(st.n - 1) * n * 2 * L * 12.0 * planes, s, [&] {
+        return launch_row_seam_fix(out + o, planes, gs, st, L, ctx->hs_gam[li], ctx->hs_theta[li], g.H, r0,
+                                   mode == MODE_SUPPORT, s);
+    });
+}
+
 // Tall single-context images: a column tile must sit on chip across its
 // cluster, and the clusters a tall column needs (16 CTAs for C4) pack only 7 per GPU (112 of
 // 148 SMs).  Cut the image into row strips whose columns fit smaller clusters, run the C_t = 1
@@ -957,7 +1078,7 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
     if (batch < 1 || H % batch != 0 || (comm && batch != 1)) return DTS_E_ARG;
     if (!finite_pos(sigma_s) || !finite_pos(sigma_r)) return DTS_E_ARG;
     if (filter_passes < 1 || filter_passes > 16) return DTS_E_ARG;
-    if (W > 18432 || H > (int64_t)1 << 30 || C > 4096) return DTS_E_SHAPE;
+    if (W > 16 * kRowStripW || H > (int64_t)1 << 30 || C > 4096) return DTS_E_SHAPE;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
 
     int device = 0;
@@ -1008,12 +1129,15 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
     // plans (validate that this build supports the shape before allocating)
     RowPlan rp;
     ColPlan cp;
-    if (plan_row_pass(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &rp) != cudaSuccess ||
+    // rows wider than the row kernel stages run over row strips (plan_row_strips, below)
+    if ((plan_row_pass(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &rp) != cudaSuccess && W <= kRowStripW) ||
         (comm ? plan_col_pass(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &cp)
               : plan_col(ctx->g, 1, MODE_SUPPORT, ctx->num_sms, &cp)) != cudaSuccess) {
+        cudaGetLastError();
         delete ctx;
         return DTS_E_SHAPE;
     }
+    cudaGetLastError();
 
     const size_t plane = (size_t)ctx->g.plane * sizeof(float);
     dts_status st = DTS_OK;
@@ -1089,10 +1213,9 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
             st = run_launch(ctx, F_FILL, ctx->g.pitch * 4.0, s,
                             [&] { return launch_fill(ctx->A1y + r * ctx->g.pitch, ctx->g.pitch, 0.f, s); });
     }
+    if (st == DTS_OK) st = plan_row_strips(ctx, s);
     if (st == DTS_OK)
-        st = run_launch(ctx, F_SUPPORT_ROW, px * 8.0, s, [&] {
-            return launch_row_pass(rp, ctx->g, 1, MODE_SUPPORT, nullptr, ctx->S, ctx->dx, ctx->ks, s);
-        });
+        st = row_pass_x(ctx, 1, MODE_SUPPORT, -1, nullptr, ctx->S, nullptr, 0, H, F_SUPPORT_ROW, px * 8.0, s);
     if (st == DTS_OK) st = ensure_col_scratch(ctx, cp, s);
     Geometry gi = ctx->g;  // one image of a batched context
     gi.H = ctx->batch_H;
@@ -1523,7 +1646,8 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     RowPlan rp{};
     ColPlan cpf{}, cpu{};
     if (!is_box) {
-        if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess) return DTS_E_SHAPE;
+        if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess && ctx->hs.n < 2) return DTS_E_SHAPE;
+        cudaGetLastError();
         if (!batch_strip_plan(ctx, Ct, &cpf)) {  // batched contexts: every image's tiles in one launch
             if ((ctx->comm ? plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)
                            : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess)
@@ -1638,25 +1762,11 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
             // row pass i over rows [r0, r0 + n) (the whole band, or part of it around a pending
             // edge fix-up); upd: Eq. (3) of the previous iteration applied on the fly
             auto row_rows = [&](int i, const float* in, bool upd, int64_t r0, int64_t n) -> dts_status {
-                if (n <= 0) return DTS_OK;
-                Geometry gs = g;  // rows r0.. of every plane (the plane stride stays)
-                gs.H = n;
-                RowPlan rps = rp;
-                if (n != g.H && plan_row_pass(gs, Ct, MODE_FILTER, ctx->num_sms, &rps) != cudaSuccess)
-                    return DTS_E_SHAPE;
-                const int64_t o = r0 * g.pitch;
-                if (upd) {
-                    UpdateArgs us = ru;
-                    us.Z = ru.Z + o;
-                    us.T = ru.T + o;
-                    us.chat = ru.chat + o;
-                    return run_launch(ctx, F_ROWUPD, (double)n * g.W * (20.0 * Ct + 8), s, [&] {
-                        return launch_row_update(rps, gs, Ct, ctx->X + o, ctx->X + o, ctx->dx + o, ctx->kc[i], us, s);
-                    });
-                }
-                return run_launch(ctx, F_ROW, (double)n * g.W * (8.0 * Ct + 4), s, [&] {
-                    return launch_row_pass(rps, gs, Ct, MODE_FILTER, in + o, ctx->X + o, ctx->dx + o, ctx->kc[i], s);
-                });
+                if (upd)
+                    return row_pass_x(ctx, Ct, MODE_FILTER, i, ctx->X, ctx->X, &ru, r0, n, F_ROWUPD,
+                                      (double)n * g.W * (20.0 * Ct + 8), s);
+                return row_pass_x(ctx, Ct, MODE_FILTER, i, in, ctx->X, nullptr, r0, n, F_ROW,
+                                  (double)n * g.W * (8.0 * Ct + 4), s);
             };
             for (int k = 0; k < iterations; ++k) {
                 for (int i = 0; i < ctx->N; ++i) {
@@ -1751,7 +1861,8 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
     ctx->last_stream = s;
     RowPlan rp;
     ColPlan cp{}, cp1{};
-    if (plan_row_pass(g, 2, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess) return DTS_E_SHAPE;
+    if (plan_row_pass(g, 2, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess && ctx->hs.n < 2) return DTS_E_SHAPE;
+    cudaGetLastError();
     const bool two = batch_strip_plan(ctx, 2, &cp) || plan_col(g, 2, MODE_FILTER, ctx->num_sms, &cp) == cudaSuccess;
     // when two planes do not fit the cluster column kernel (tall images) but one does, the
     // column passes run plane by plane on it (over row strips where dts_solve uses them)
@@ -1782,9 +1893,7 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
     // planes [t ; t^2] -> DTF (N passes of rows then columns) -> Eq. (7)
     st = run_launch(ctx, F_CONF, px * 12.0, s, [&] { return launch_conf_prologue(t_d, g, ctx->X, s); });
     for (int i = 0; i < ctx->N && st == DTS_OK; ++i) {
-        st = run_launch(ctx, F_ROW, px * 20.0, s, [&] {
-            return launch_row_pass(rp, g, 2, MODE_FILTER, ctx->X, ctx->X, ctx->dx, ctx->kc[i], s);
-        });
+        st = row_pass_x(ctx, 2, MODE_FILTER, i, ctx->X, ctx->X, nullptr, 0, g.H, F_ROW, px * 20.0, s);
         if (st == DTS_OK && !per_plane) st = col_filter_pass(ctx, cp, 2, i, ctx->X, px * 20.0, s);
         for (int v = 0; v < 2 && st == DTS_OK && per_plane; ++v)
             st = col_filter_pass(ctx, cp1, 1, i, ctx->X + v * g.plane, px * 12.0, s);
@@ -1822,7 +1931,7 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
     ctx->last_stream = s;
     RowPlan rp;
     ColPlan cp{};
-    if (plan_row_pass(g, 1, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess ||
+    if ((plan_row_pass(g, 1, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess && ctx->hs.n < 2) ||
         !(batch_strip_plan(ctx, 1, &cp) || plan_col(g, 1, MODE_FILTER, ctx->num_sms, &cp) == cudaSuccess))
         return DTS_E_SHAPE;
     cudaGetLastError();
@@ -1881,9 +1990,7 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
             for (int k = 0; k < iterations && st == DTS_OK; ++k) {
                 for (int i = 0; i < ctx->N && st == DTS_OK; ++i) {
                     const float* in = (i == 0) ? ctx->Z : ctx->X;
-                    st = run_launch(ctx, F_ROW, px * 12.0, s, [&] {
-                        return launch_row_pass(rp, g, 1, MODE_FILTER, in, ctx->X, ctx->dx, ctx->kc[i], s);
-                    });
+                    st = row_pass_x(ctx, 1, MODE_FILTER, i, in, ctx->X, nullptr, 0, g.H, F_ROW, px * 12.0, s);
                     if (st == DTS_OK) st = col_filter_pass(ctx, cp, 1, i, ctx->X, px * 12.0, s);
                 }
                 float* ohw = (k + 1 == iterations) ? o_d : nullptr;
@@ -1945,6 +2052,10 @@ void dts_destroy(dts_ctx* ctx) {
         if (q) cudaFreeAsync(q, s);
     if (ctx->vs_edge) cudaFreeAsync(ctx->vs_edge, s);
     for (float* q : ctx->vs_theta)
+        if (q) cudaFreeAsync(q, s);
+    for (float* q : ctx->hs_gam)
+        if (q) cudaFreeAsync(q, s);
+    for (float* q : ctx->hs_theta)
         if (q) cudaFreeAsync(q, s);
     if (ctx->graph_exec) {  // a replay may still be in flight on s
         cudaStreamSynchronize(s);

@@ -47,8 +47,22 @@ struct RowPlan {
     int L, G, R, threads, grid, nbuf;
     size_t smem;
     int64_t rowstride;
+    int64_t rowlen = 0;  // floats staged per row (0 / the pitch; a row strip's padded width)
 };
-cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowPlan* plan);
+// rowlen > 0: rows of a vertical strip of that (padded) width inside rows of g.pitch
+cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowPlan* plan, int64_t rowlen = 0);
+// row strips of images wider than one CTA's staging buffer: strip b = columns [c[b], c[b+1])
+struct RowStrips {
+    int n;
+    int c[17];  // c[0] = 0, c[n] = W
+};
+cudaError_t launch_row_edge_length(const float* d, const Geometry& g, const RowStrips& st, int Lcap, float kc,
+                                   unsigned* len, cudaStream_t s);
+cudaError_t launch_row_edge_profiles(const float* d, const Geometry& g, const RowStrips& st, int L, float kc,
+                                     float* gam, float* theta, bool raw, cudaStream_t s);
+// x: row r0 of plane 0 (g.H rows from there); gam / theta: [seam][Hp][L]
+cudaError_t launch_row_seam_fix(float* x, int Ct, const Geometry& g, const RowStrips& st, int L, const float* gam,
+                                const float* theta, int64_t Hp, int64_t r0, bool raw, cudaStream_t s);
 cudaError_t launch_row_pass(const RowPlan& plan, const Geometry& g, int Ct, int mode, const float* in, float* out,
                             const float* d, float kc, cudaStream_t s);
 

@@ -32,6 +32,7 @@ struct RowParams {
     const float* chat;
     float lam, step;
     int64_t plane, pitch, rowstride;
+    int64_t rowlen;  // floats staged per row (the pitch; a row strip's padded width)
     int H, W, G, R, nbuf;
     float kc;
 };
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
     const int t = threadIdx.x - rs * G;
     const int64_t bufFloats = (int64_t)R * NSLOT * p.rowstride;
     float* scratch = smem + p.nbuf * bufFloats;  // cross-warp scan scratch (32 * (NV+1) floats)
-    const uint32_t rowBytes = (uint32_t)(p.pitch * sizeof(float));
+    const uint32_t rowBytes = (uint32_t)(p.rowlen * sizeof(float));
     const int ngroups = (p.H + R - 1) / R;
 
     if (threadIdx.x == 0) {
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
 
 static const int kLs[] = {4, 12, 20, 36};
 
-cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowPlan* plan) {
+cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowPlan* plan, int64_t rowlen) {
     const int nslot = 1 + (mode == MODE_SUPPORT ? 1 : Ct);
     // Narrow rows: the smallest segment length that fits >= 2 rows per CTA (G <= 128).  A
     // row's scan is latency-bound; several rows per CTA keep more of them in flight (C1/C2:
@@ -366,9 +367,11 @@ cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowP
     plan->G = G;
     plan->R = R;
     plan->threads = G * R;
-    int64_t rs = g.pitch > (int64_t)G * L ? g.pitch : (int64_t)G * L;
+    const int64_t rl = rowlen > 0 ? rowlen : g.pitch;
+    int64_t rs = rl > (int64_t)G * L ? rl : (int64_t)G * L;
     rs = (rs + 3) / 4 * 4;
     plan->rowstride = rs;
+    plan->rowlen = rl;
     plan->nbuf = 2;
     plan->smem = (size_t)2 * R * nslot * rs * sizeof(float) + 32 * 8 * sizeof(float);
     if (plan->smem > 227 * 1024) {  // very wide rows: one buffer (no prefetch overlap)
@@ -421,6 +424,7 @@ cudaError_t launch_row_update(const RowPlan& plan, const Geometry& g, int Ct, co
     p.plane = g.plane;
     p.pitch = g.pitch;
     p.rowstride = plan.rowstride;
+    p.rowlen = plan.rowlen;
     p.H = (int)g.H;
     p.W = (int)g.W;
     p.G = plan.G;
@@ -445,6 +449,7 @@ cudaError_t launch_row_pass(const RowPlan& plan, const Geometry& g, int Ct, int 
     p.plane = g.plane;
     p.pitch = g.pitch;
     p.rowstride = plan.rowstride;
+    p.rowlen = plan.rowlen;
     p.H = (int)g.H;
     p.W = (int)g.W;
     p.G = plan.G;
@@ -467,6 +472,124 @@ cudaError_t launch_row_pass(const RowPlan& plan, const Geometry& g, int Ct, int 
         case 36: return launch_ct<36, MODE_FILTER>(plan, p, Ct, s);
     }
     return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------------------
+// Row strips (images wider than one CTA's staging buffer holds).  The
+// row pass runs on vertical strips [c_b, c_{b+1}) with a zero carry at each strip's left edge
+// and the link to its right cut; the seams are fixed up afterwards with per-row edge profiles:
+// the row-strip algebra of the column passes (reading R26) along x.  Seam j (1 <= j < n) lies
+// between strips j - 1 and j at column c_j; profiles are [seam][row][L].
+
+// how many columns a carry entering a strip keeps an influence >= 2^-26 of itself (max over
+// rows, from the left edge of strip j and from the right edge of strip j - 1)
+__global__ void k_row_edge_length(const float* __restrict__ d, int64_t H, int64_t pitch, RowStrips st, int Lcap,
+                                  float kc, unsigned* __restrict__ len) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y + 1;
+    if (r >= H) return;
+    const float thr = 1.0f / 67108864.0f;  // 2^-26
+    const float* dr = d + r * pitch + st.c[j];
+    float G = 1.f;
+    int k = 0;
+    for (; k < Lcap; ++k) {
+        G *= coef_from_d(__ldg(dr + k), kc);
+        if (G < thr) break;
+    }
+    atomicMax(&len[0], (unsigned)k);
+    float Th = 1.f;
+    int m = 0;
+    for (; m < Lcap; ++m) {
+        Th *= coef_from_d(__ldg(dr - m), kc);
+        if (Th < thr) break;
+    }
+    atomicMax(&len[1], (unsigned)m);
+}
+
+// Gamma (the first L columns of strip j: G_k = prod_{m <= k} a_{c_j + m}, then its anticausal
+// response unless raw) and Theta (the last L columns of strip j - 1: the product of the links
+// from column k + 1 to c_j), thread per (row, seam)
+__global__ void k_row_edge_profiles(const float* __restrict__ d, int64_t H, int64_t pitch, RowStrips st, int L,
+                                    float kc, float* __restrict__ gam, float* __restrict__ theta, bool raw) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y + 1;
+    if (r >= H) return;
+    const float* dr = d + r * pitch + st.c[j];
+    float* gm = gam + ((int64_t)(j - 1) * H + r) * L;
+    float* th = theta + ((int64_t)(j - 1) * H + r) * L;
+    float G = 1.f;
+    for (int k = 0; k < L; ++k) {
+        G *= coef_from_d(__ldg(dr + k), kc);
+        gm[k] = G;
+    }
+    float dz = 0.f;
+    for (int k = L - 1; k >= 0 && !raw; --k) {
+        const float an = coef_from_d(__ldg(dr + k + 1), kc);
+        dz = fmaf(an, dz - gm[k], gm[k]);
+        gm[k] = dz;
+    }
+    float t = coef_from_d(__ldg(dr), kc);  // the link across the seam
+    for (int k = L - 1; k >= 0; --k) {     // theta[k]: column c_j - L + k
+        th[k] = t;
+        t *= coef_from_d(__ldg(dr - (L - k)), kc);
+    }
+}
+
+// block per (row, seam): every plane's y_last = x[c_j - 1] and z0 = x[c_j] are read before any
+// thread writes; then x[c_j + k] += y_last Gamma[k] and x[c_j - L + k] += e Theta[k], with
+// e = z0 + y_last Gamma[0] - y_last (raw, the support: c = s0[c_j - 1], e = s0[c_j])
+// x points at row r0 of plane 0; the profiles hold Hp rows
+__global__ void __launch_bounds__(128) k_row_seam_fix(float* __restrict__ x, int Ct, int64_t pitch, int64_t plane,
+                                                      RowStrips st, int L, const float* __restrict__ gam,
+                                                      const float* __restrict__ theta, int64_t Hp, int64_t r0,
+                                                      bool raw) {
+    const int64_t r = blockIdx.x;
+    const int j = blockIdx.y + 1;
+    pdl_trigger();
+    pdl_wait();
+    const int64_t cj = st.c[j];
+    const float* gm = gam + ((int64_t)(j - 1) * Hp + r0 + r) * L;
+    const float* th = theta + ((int64_t)(j - 1) * Hp + r0 + r) * L;
+    float yl[4], e[4];
+    const float g0 = __ldg(gm);
+    for (int v = 0; v < Ct && v < 4; ++v) {
+        const float* xr = x + v * plane + r * pitch;
+        yl[v] = xr[cj - 1];
+        const float z0 = xr[cj];
+        e[v] = raw ? z0 : fmaf(yl[v], g0, z0) - yl[v];
+    }
+    __syncthreads();
+    for (int v = 0; v < Ct && v < 4; ++v) {
+        float* xr = x + v * plane + r * pitch;
+        for (int k = threadIdx.x; k < 2 * L; k += blockDim.x) {
+            if (k < L) xr[cj + k] = fmaf(yl[v], __ldg(gm + k), xr[cj + k]);
+            else xr[cj - 2 * L + k] = fmaf(e[v], __ldg(th + (k - L)), xr[cj - 2 * L + k]);
+        }
+    }
+}
+
+cudaError_t launch_row_edge_length(const float* d, const Geometry& g, const RowStrips& st, int Lcap, float kc,
+                                   unsigned* len, cudaStream_t s) {
+    if (st.n < 2) return cudaSuccess;
+    k_row_edge_length<<<dim3((unsigned)((g.H + 127) / 128), (unsigned)(st.n - 1)), 128, 0, s>>>(d, g.H, g.pitch, st,
+                                                                                                 Lcap, kc, len);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_edge_profiles(const float* d, const Geometry& g, const RowStrips& st, int L, float kc,
+                                     float* gam, float* theta, bool raw, cudaStream_t s) {
+    if (st.n < 2) return cudaSuccess;
+    k_row_edge_profiles<<<dim3((unsigned)((g.H + 127) / 128), (unsigned)(st.n - 1)), 128, 0, s>>>(
+        d, g.H, g.pitch, st, L, kc, gam, theta, raw);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_seam_fix(float* x, int Ct, const Geometry& g, const RowStrips& st, int L, const float* gam,
+                                const float* theta, int64_t Hp, int64_t r0, bool raw, cudaStream_t s) {
+    if (st.n < 2 || g.H < 1) return cudaSuccess;
+    if (Ct > 4) return cudaErrorInvalidValue;
+    return launch_pdl(k_row_seam_fix, dim3((unsigned)g.H, (unsigned)(st.n - 1)), dim3(128), 0, s, x, Ct, g.pitch,
+                      g.plane, st, L, gam, theta, Hp, r0, raw);
 }
 
 }  // namespace dts
