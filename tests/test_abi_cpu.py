@@ -54,7 +54,8 @@ def test_create_rejects_bad_scalars_on_host(kw):
 
 
 def test_create_rejects_unsupported_width():
-    g = np.zeros((1, 20000, 1), np.float32)
+    """Wider than 16 row strips of 11520 columns (include/dts.h): rejected on the host."""
+    g = np.zeros((1, 184321, 1), np.float32)
     with pytest.raises(dts.DTSError) as ei:
         dts.dts_create(g, 8.0, 0.2, 3)
     assert ei.value.status == 2
