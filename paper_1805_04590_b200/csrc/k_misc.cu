@@ -410,44 +410,81 @@ cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s) {
 // Eq. (7) confidence: the two planes the DTF turns into local moments.  The
 // target is shifted by t[0] first: DT is row-stochastic, so V(t - k) = V(t) exactly, and
 // the shift keeps DT(t^2) - DT(t)^2 from cancelling catastrophically in fp32 when |t| is
-// large against its range (reading R22).  2-D grid: blockIdx.y walks rows, threads columns.
+// large against its range (reading R22).
+// Planes [t - t_0 ; (t - t_0)^2] and the epilogue, one thread per 4 consecutive pixels
+// of a row: float4 on the pitched planes, and on the H x W target / outputs when W % 4 == 0
+// (every row 16-B aligned); scalar otherwise
 __global__ void __launch_bounds__(256) k_conf_prologue(const float* __restrict__ t, Geometry g, float* __restrict__ X) {
     const float k0 = __ldg(t);
-    for (int64_t r = blockIdx.y; r < g.H; r += gridDim.y) {
-        for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.W; c += (int64_t)gridDim.x * blockDim.x) {
-            const float v = __ldg(t + r * g.W + c) - k0;
-            X[r * g.pitch + c] = v;
-            X[g.plane + r * g.pitch + c] = v * v;
+    const int64_t per_row = g.pitch / 4;
+    const int64_t n = g.H * per_row;
+    const bool vec = (g.W & 3) == 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / per_row;
+        const int64_t c = (i - r * per_row) * 4;
+        if (c >= g.W) continue;
+        float v[4];
+        if (vec) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(t + r * g.W + c));
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = c + u < g.W ? __ldg(t + r * g.W + c + u) : k0;
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] -= k0;
+        *reinterpret_cast<float4*>(X + r * g.pitch + c) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(X + g.plane + r * g.pitch + c) =
+            make_float4(v[0] * v[0], v[1] * v[1], v[2] * v[2], v[3] * v[3]);
     }
 }
 
 __global__ void __launch_bounds__(256) k_conf_epilogue(const float* __restrict__ X, Geometry g, float inv_2sc2,
                                                        float* __restrict__ conf, float* __restrict__ var) {
-    for (int64_t r = blockIdx.y; r < g.H; r += gridDim.y) {
-        for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.W; c += (int64_t)gridDim.x * blockDim.x) {
-            const float m1 = X[r * g.pitch + c], m2 = X[g.plane + r * g.pitch + c];
-            const float v = fmaxf(fmaf(-m1, m1, m2), 0.f);  // DT(t^2) - DT(t)^2, clamped (R22)
-            conf[r * g.W + c] = __expf(-v * inv_2sc2);
-            if (var) var[r * g.W + c] = v;
+    const int64_t per_row = g.pitch / 4;
+    const int64_t n = g.H * per_row;
+    const bool vec = (g.W & 3) == 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / per_row;
+        const int64_t c = (i - r * per_row) * 4;
+        if (c >= g.W) continue;
+        const float4 a = __ldg(reinterpret_cast<const float4*>(X + r * g.pitch + c));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(X + g.plane + r * g.pitch + c));
+        const float m1[4] = {a.x, a.y, a.z, a.w}, m2[4] = {b.x, b.y, b.z, b.w};
+        float v[4], e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            v[u] = fmaxf(fmaf(-m1[u], m1[u], m2[u]), 0.f);  // DT(t^2) - DT(t)^2, clamped (R22)
+            e[u] = __expf(-v[u] * inv_2sc2);
+        }
+        if (vec) {
+            *reinterpret_cast<float4*>(conf + r * g.W + c) = make_float4(e[0], e[1], e[2], e[3]);
+            if (var) *reinterpret_cast<float4*>(var + r * g.W + c) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c + u < g.W) {
+                    conf[r * g.W + c + u] = e[u];
+                    if (var) var[r * g.W + c + u] = v[u];
+                }
         }
     }
 }
 
-static dim3 conf_grid(const Geometry& g) {
-    const int64_t bx = (g.W + 255) / 256;
-    const int64_t by = g.H < 8192 ? g.H : 8192;
-    return dim3((unsigned)(bx < 64 ? bx : 64), (unsigned)by, 1);
+static unsigned conf_blocks(const Geometry& g) {
+    const int64_t n = g.H * (g.pitch / 4);
+    const int64_t b = (n + 255) / 256;
+    return (unsigned)(b < 148 * 16 ? b : 148 * 16);
 }
 
 cudaError_t launch_conf_prologue(const float* target, const Geometry& g, float* X, cudaStream_t s) {
-    k_conf_prologue<<<conf_grid(g), 256, 0, s>>>(target, g, X);
+    k_conf_prologue<<<conf_blocks(g), 256, 0, s>>>(target, g, X);
     return cudaGetLastError();
 }
 
 cudaError_t launch_conf_epilogue(const float* X, const Geometry& g, float inv_2sc2, float* conf, float* var,
                                  cudaStream_t s) {
-    k_conf_epilogue<<<conf_grid(g), 256, 0, s>>>(X, g, inv_2sc2, conf, var);
+    k_conf_epilogue<<<conf_blocks(g), 256, 0, s>>>(X, g, inv_2sc2, conf, var);
     return cudaGetLastError();
 }
 

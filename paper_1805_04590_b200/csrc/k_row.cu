@@ -247,6 +247,13 @@ __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
         // coefficient linking this chunk's last sample to the next chunk's first
         const int kn = k0 + L;
         const float Anext = (kn < p.W) ? coef_from_d(row[kn], p.kc) : 0.f;
+        // single buffer (rows too wide for two): every thread now holds its chunk in registers,
+        // so the buffer takes the next row group at once and this group's outputs leave by
+        // direct stores (C4 at C_t = 2, 120 KB per row: 445 -> 398 us)
+        if (!dbl) {
+            __syncthreads();
+            if (threadIdx.x == 0 && nxt < ngroups) issue(nxt, 0);
+        }
 
         // ---- causal: fold, scan, apply ----
         Aff<NV> m = aff_identity<NV>();
@@ -302,26 +309,29 @@ __global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
                 }
             }
 #pragma unroll
-            for (int j4 = 0; j4 < L; j4 += 4)
-                *reinterpret_cast<float4*>(orow + c * p.rowstride + k0 + j4) =
-                    make_float4(o[j4], o[j4 + 1], o[j4 + 2], o[j4 + 3]);
+            for (int j4 = 0; j4 < L; j4 += 4) {
+                const float4 v4 = make_float4(o[j4], o[j4 + 1], o[j4 + 2], o[j4 + 3]);
+                if (dbl)
+                    *reinterpret_cast<float4*>(orow + c * p.rowstride + k0 + j4) = v4;
+                else if (grow < p.H && k0 + j4 < p.rowlen)
+                    *reinterpret_cast<float4*>(p.out + c * p.plane + grow * p.pitch + k0 + j4) = v4;
+            }
         }
 
-        fence_proxy_async_smem();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            float* buf = smem + b * bufFloats;
-            for (int q = 0; q < R; ++q) {
-                const int64_t r = (int64_t)grp * R + q;
-                if (r >= p.H) break;
+        if (dbl) {  // the outputs leave through bulk stores from the buffer
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                float* buf = smem + b * bufFloats;
+                for (int q = 0; q < R; ++q) {
+                    const int64_t r = (int64_t)grp * R + q;
+                    if (r >= p.H) break;
 #pragma unroll
-                for (int c = 0; c < NV; ++c)
-                    bulk_s2g(p.out + c * p.plane + r * p.pitch, buf + (q * NSLOT + 1 + c) * p.rowstride, rowBytes);
-            }
-            bulk_commit();
-            if (!dbl && nxt < ngroups) {  // single buffer: refill once the stores have read it
-                bulk_wait_read0();
-                issue(nxt, 0);
+                    for (int c = 0; c < NV; ++c)
+                        bulk_s2g(p.out + c * p.plane + r * p.pitch, buf + (q * NSLOT + 1 + c) * p.rowstride,
+                                 rowBytes);
+                }
+                bulk_commit();
             }
         }
     }
