@@ -78,7 +78,8 @@ struct Options {
                                       // 12 or 16 (C_t = 3)
     std::atomic<int> col_cluster{0};  // column kernel cluster size: 0 auto, else forced (experiments)
     std::atomic<int> strip_cluster{0};     // row strips: forced cluster size of the strip plan (0 = auto)
-    std::atomic<int> band_overlap{1};  // row bands, edge scheme: all-gather overlapped with the next row pass
+    std::atomic<int> band_overlap{1};
+    std::atomic<int> row_two_ctas{1};  // C_t = 3 row passes of <= 3840 columns: two CTAs per SM  // row bands, edge scheme: all-gather overlapped with the next row pass
     std::atomic<int> col_strips{1};   // tall single-context images: C_t = 1 column passes over row strips
                                       // (0 off, 1 auto, n >= 2: exactly n strips when they fit)
 };
@@ -653,6 +654,7 @@ bool profiler_on() {
 
 namespace dts {
 int option_col_cluster() { return opts_g().col_cluster.load(); }
+int row_minb2() { return opts_g().row_two_ctas.load(); }
 }  // namespace dts
 
 extern "C" {
@@ -673,6 +675,7 @@ dts_status dts_set_option(const char* name, int32_t value) {
     else if (n == "col_strips" && value >= 0 && value <= 64) o.col_strips = value;
     else if (n == "strip_cluster" && value >= 0 && value <= 16) o.strip_cluster = value;
     else if (n == "band_overlap" && (value == 0 || value == 1)) o.band_overlap = value;
+    else if (n == "row_two_ctas" && (value == 0 || value == 1)) o.row_two_ctas = value;
     else return DTS_E_ARG;
     return DTS_OK;
 }
@@ -700,6 +703,7 @@ int32_t dts_get_option(const char* name) {
     if (n == "col_strips") return o.col_strips;
     if (n == "strip_cluster") return o.strip_cluster;
     if (n == "band_overlap") return o.band_overlap;
+    if (n == "row_two_ctas") return o.row_two_ctas;
     return -1;
 }
 
@@ -843,7 +847,7 @@ static dts_status row_pass_x(dts_ctx* ctx, int Ct, int mode, int pass, const flo
     gs.H = n;
     const int64_t o = r0 * g.pitch;
     const float kc = pass >= 0 ? ctx->kc[pass] : ctx->ks;
-    const int pmode = mode == MODE_SUPPORT ? MODE_SUPPORT : MODE_FILTER;
+    const int pmode = upd ? MODE_ROWUPD : (mode == MODE_SUPPORT ? MODE_SUPPORT : MODE_FILTER);
     auto launch = [&](const RowPlan& p, const Geometry& gg, int64_t c0) -> cudaError_t {
         const int64_t oo = o + c0;
         if (upd) {

@@ -48,6 +48,7 @@ struct RowPlan {
     size_t smem;
     int64_t rowstride;
     int64_t rowlen = 0;  // floats staged per row (0 / the pitch; a row strip's padded width)
+    int minb = 1;        // 2: the two-CTAs-per-SM instantiation (C_t = 3, <= 320 threads)
 };
 // rowlen > 0: rows of a vertical strip of that (padded) width inside rows of g.pitch
 cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowPlan* plan, int64_t rowlen = 0);
@@ -140,6 +141,8 @@ cudaError_t launch_sr_prepare(const float* low, int64_t h, int64_t w, int f, flo
 
 // dts_set_option("col_cluster") (experiments): forced column-kernel cluster size, 0 = auto
 int option_col_cluster();
+// dts_set_option("row_two_ctas"): C_t = 3 row passes as two CTAs per SM (k_row.cu)
+int row_minb2();
 
 // fill n floats with v
 cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);

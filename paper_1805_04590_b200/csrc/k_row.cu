@@ -97,8 +97,10 @@ __device__ __forceinline__ Aff<NV> group_exclusive_scan(Aff<NV> v, int t, int G,
     return aff_compose(pre, ex);
 }
 
-template <int L, int CT, int MODE>
-__global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
+// MINB = 2: two CTAs of <= 320 threads per SM (registers capped accordingly; C_t = 3 rows of
+// <= 3840 columns, single-buffered)
+template <int L, int CT, int MODE, int MINB = 1>
+__global__ void __launch_bounds__(MINB == 2 ? 320 : 512, MINB) k_row_pass(const RowParams p) {
     static_assert(L % 4 == 0, "L must be a multiple of 4 (float4 smem reads)");
     constexpr int NX = (MODE == MODE_SUPPORT) ? 0 : CT;  // input planes (ROWUPD: zbar)
     constexpr int NSLOT = 1 + (MODE == MODE_SUPPORT ? 1 : CT);
@@ -389,12 +391,22 @@ cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowP
         plan->smem = (size_t)R * nslot * rs * sizeof(float) + 32 * 8 * sizeof(float);
     }
     if (plan->smem > 227 * 1024) return cudaErrorInvalidValue;
+    plan->minb = 1;
+    if (Ct == 3 && L == 12 && mode == MODE_FILTER && plan->threads <= 320 && row_minb2()) {
+        // C_t = 3 rows of <= 3840 columns: two single-buffered CTAs per SM instead of one
+        // double-buffered one (registers capped at 96 per thread).  Batched C3 row pass 0.353
+        // -> 0.335 ms; not the fused row update (0.688 -> 0.827 ms), which plans as ROWUPD
+        plan->minb = 2;
+        plan->nbuf = 1;
+        plan->smem = (size_t)R * nslot * rs * sizeof(float) + 32 * 8 * sizeof(float);
+    }
     const int64_t ngroups = (g.H + R - 1) / R;
     int per_sm = 1;
     // occupancy limited by threads and smem
     int by_threads = 2048 / plan->threads;
     int by_smem = (int)((228 * 1024) / (plan->smem + 1024));
     per_sm = by_threads < by_smem ? by_threads : by_smem;
+    if (plan->minb == 2 && per_sm > 2) per_sm = 2;  // what the register cap allows
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)num_sms * per_sm;
     if (grid > ngroups) grid = ngroups;
@@ -404,6 +416,13 @@ cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowP
 
 template <int L, int CT, int MODE>
 static cudaError_t launch_t(const RowPlan& plan, const RowParams& p, cudaStream_t s) {
+    if constexpr (L == 12 && CT == 3 && MODE != MODE_SUPPORT) {
+        if (plan.minb == 2) {
+            cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k_row_pass<L, CT, MODE, 2>), plan.smem);
+            if (e != cudaSuccess) return e;
+            return launch_pdl(k_row_pass<L, CT, MODE, 2>, dim3(plan.grid), dim3(plan.threads), plan.smem, s, p);
+        }
+    }
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k_row_pass<L, CT, MODE>), plan.smem);
     if (e != cudaSuccess) return e;
     return launch_pdl(k_row_pass<L, CT, MODE>, dim3(plan.grid), dim3(plan.threads), plan.smem, s, p);
