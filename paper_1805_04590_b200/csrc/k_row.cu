@@ -99,8 +99,31 @@ __device__ __forceinline__ Aff<NV> group_exclusive_scan(Aff<NV> v, int t, int G,
 
 // MINB = 2: two CTAs of <= 320 threads per SM (registers capped accordingly; C_t = 3 rows of
 // <= 3840 columns, single-buffered)
-template <int L, int CT, int MODE, int MINB = 1>
-__global__ void __launch_bounds__(MINB == 2 ? 320 : 512, MINB) k_row_pass(const RowParams p) {
+// SB: single staging buffer, refilled with the next row group as soon as every thread holds its
+// chunk in registers; the outputs leave by direct float4 stores (rows too wide for two
+// buffers, and the two-CTAs-per-SM variant).  !SB: double buffer (or, for a single buffer,
+// refilled after the bulk stores have read it) and TMA bulk stores.
+template <int L, int CT, int MODE, bool SB>
+__device__ __forceinline__ void row_pass_body(const RowParams& p);
+
+template <int L, int CT, int MODE>
+__global__ void __launch_bounds__(512) k_row_pass(const RowParams p) {
+    row_pass_body<L, CT, MODE, false>(p);
+}
+
+template <int L, int CT, int MODE>
+__global__ void __launch_bounds__(512) k_row_pass_sb(const RowParams p) {
+    row_pass_body<L, CT, MODE, true>(p);
+}
+
+// two CTAs of <= 320 threads per SM (registers capped at 96): C_t = 3 rows of <= 3840 columns
+template <int L, int CT, int MODE>
+__global__ void __launch_bounds__(320, 2) k_row_pass2(const RowParams p) {
+    row_pass_body<L, CT, MODE, true>(p);
+}
+
+template <int L, int CT, int MODE, bool SB>
+__device__ __forceinline__ void row_pass_body(const RowParams& p) {
     static_assert(L % 4 == 0, "L must be a multiple of 4 (float4 smem reads)");
     constexpr int NX = (MODE == MODE_SUPPORT) ? 0 : CT;  // input planes (ROWUPD: zbar)
     constexpr int NSLOT = 1 + (MODE == MODE_SUPPORT ? 1 : CT);
@@ -155,7 +178,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 320 : 512, MINB) k_row_pass(const 
     int grp = blockIdx.x;
     if (grp < ngroups && threadIdx.x == 0) issue(grp, 0);
 
-    const bool dbl = p.nbuf == 2;
+    const bool dbl = !SB && p.nbuf == 2;
     for (int it = 0; grp < ngroups; grp += gridDim.x, ++it) {
         const int b = dbl ? (it & 1) : 0;
         const int nxt = grp + gridDim.x;
@@ -252,7 +275,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 320 : 512, MINB) k_row_pass(const 
         // single buffer (rows too wide for two): every thread now holds its chunk in registers,
         // so the buffer takes the next row group at once and this group's outputs leave by
         // direct stores (C4 at C_t = 2, 120 KB per row: 445 -> 398 us)
-        if (!dbl) {
+        if constexpr (SB) {
             __syncthreads();
             if (threadIdx.x == 0 && nxt < ngroups) issue(nxt, 0);
         }
@@ -313,14 +336,16 @@ __global__ void __launch_bounds__(MINB == 2 ? 320 : 512, MINB) k_row_pass(const 
 #pragma unroll
             for (int j4 = 0; j4 < L; j4 += 4) {
                 const float4 v4 = make_float4(o[j4], o[j4 + 1], o[j4 + 2], o[j4 + 3]);
-                if (dbl)
+                if constexpr (SB) {
+                    if (grow < p.H && k0 + j4 < p.rowlen)
+                        *reinterpret_cast<float4*>(p.out + c * p.plane + grow * p.pitch + k0 + j4) = v4;
+                } else {
                     *reinterpret_cast<float4*>(orow + c * p.rowstride + k0 + j4) = v4;
-                else if (grow < p.H && k0 + j4 < p.rowlen)
-                    *reinterpret_cast<float4*>(p.out + c * p.plane + grow * p.pitch + k0 + j4) = v4;
+                }
             }
         }
 
-        if (dbl) {  // the outputs leave through bulk stores from the buffer
+        if constexpr (!SB) {  // the outputs leave through bulk stores from the buffer
             fence_proxy_async_smem();
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -334,6 +359,10 @@ __global__ void __launch_bounds__(MINB == 2 ? 320 : 512, MINB) k_row_pass(const 
                                  rowBytes);
                 }
                 bulk_commit();
+                if (!dbl && nxt < ngroups) {  // single buffer: refill once the stores have read it
+                    bulk_wait_read0();
+                    issue(nxt, 0);
+                }
             }
         }
     }
@@ -418,10 +447,15 @@ template <int L, int CT, int MODE>
 static cudaError_t launch_t(const RowPlan& plan, const RowParams& p, cudaStream_t s) {
     if constexpr (L == 12 && CT == 3 && MODE != MODE_SUPPORT) {
         if (plan.minb == 2) {
-            cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k_row_pass<L, CT, MODE, 2>), plan.smem);
+            cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k_row_pass2<L, CT, MODE>), plan.smem);
             if (e != cudaSuccess) return e;
-            return launch_pdl(k_row_pass<L, CT, MODE, 2>, dim3(plan.grid), dim3(plan.threads), plan.smem, s, p);
+            return launch_pdl(k_row_pass2<L, CT, MODE>, dim3(plan.grid), dim3(plan.threads), plan.smem, s, p);
         }
+    }
+    if (plan.nbuf == 1) {  // one buffer: the early-refill variant
+        cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k_row_pass_sb<L, CT, MODE>), plan.smem);
+        if (e != cudaSuccess) return e;
+        return launch_pdl(k_row_pass_sb<L, CT, MODE>, dim3(plan.grid), dim3(plan.threads), plan.smem, s, p);
     }
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k_row_pass<L, CT, MODE>), plan.smem);
     if (e != cudaSuccess) return e;
