@@ -20,6 +20,18 @@ for spec in "k_col_cluster 4" "k_row_pass 2" "k_row_pass 4 row_update" "k_update
   ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 \
       -o $OUT/full_$tag $CMD > $OUT/ncu_full_$tag.log 2>&1
 done
+# 5) C3 (8 x 4K, C_t = 3) in one batched context, one iteration per solve (tools/c3_batch.py):
+#    the launch list of create + five solves, and one --set full capture each of a column pass
+#    (launch 10 of k_col_cluster: after the 8 per-image support passes and the first) and a row
+#    pass (launch 3 of k_row_pass: after the support pass and the first)
+C3_ITERS=1 python tools/c3_batch.py > $OUT/c3_once.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 80 --csv \
+    --log-file $OUT/c3_launches.csv env C3_ITERS=1 python tools/c3_batch.py > $OUT/ncu_c3.log 2>&1
+for spec in "k_col_cluster 9" "k_row_pass 2"; do
+  set -- $spec
+  ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 \
+      -o $OUT/full_c3_$1 env C3_ITERS=1 python tools/c3_batch.py > $OUT/ncu_full_c3_$1.log 2>&1
+done
 python tools/c1_once.py > $OUT/c1_once.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -s 307 -c 302 --csv --log-file $OUT/c1_launches.csv \
     python tools/c1_once.py > $OUT/ncu_c1.log 2>&1

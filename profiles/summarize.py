@@ -142,13 +142,33 @@ def main():
             {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(met.get("dram__bytes_read.sum", ("", "byte"))[1], 1)
         wr = float(met.get("dram__bytes_write.sum", ("0", ""))[0].replace(",", "")) * \
             {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(met.get("dram__bytes_write.sum", ("", "byte"))[1], 1)
-        traffic.setdefault("C4", {})[BENCH_NAME.get(key, key)] = {"dram_bytes_per_launch": rd + wr,
-                                                                  "source": os.path.basename(dst)}
+        cfg, base = ("C3", key[3:]) if key.startswith("c3_") else ("C4", key)
+        traffic.setdefault(cfg, {})[BENCH_NAME.get(base, base)] = {"dram_bytes_per_launch": rd + wr,
+                                                                   "source": os.path.basename(dst)}
         lines.append(f"### {key}  (`{os.path.basename(dst)}`)")
         lines.append("")
         for h, (v, u) in met.items():
             lines.append(f"- {h}: {v} {u}")
         lines.append(f"- DRAM traffic per launch: {(rd + wr) / 1e9:.3f} GB")
+        lines.append("")
+    c3 = os.path.join(src, "c3_launches.csv")
+    if os.path.exists(c3):  # C3 batched: create + five one-iteration solves (tools/c3_batch.py)
+        shutil.copy(c3, os.path.join(HERE, f"{tag}_c3_launches.csv"))
+        per = read_launches(c3)
+        fam_t = defaultdict(float)
+        fam_n = defaultdict(int)
+        fam_b = defaultdict(float)
+        for (lid, name), d in per.items():
+            key, fam = family(name)
+            fam_t[fam] += to_ns(d, "gpu__time_duration.sum")
+            fam_n[fam] += 1
+            fam_b[fam] += to_bytes(d, "dram__bytes_read.sum") + to_bytes(d, "dram__bytes_write.sum")
+        lines += ["## C3 (8 x 3840x2160, C_t = 3, one batched context): launch list", "",
+                  "`C3_ITERS=1 python tools/c3_batch.py` (create, then five one-iteration solves), ncu-serialised.", "",
+                  "| family | launches | total ms | avg us | DRAM bytes / launch |", "|---|---|---|---|---|"]
+        for fam in sorted(fam_t, key=lambda f: -fam_t[f]):
+            lines.append(f"| {fam} | {fam_n[fam]} | {fam_t[fam] / 1e6:.3f} | {fam_t[fam] / fam_n[fam] / 1e3:.1f} | "
+                         f"{fam_b[fam] / fam_n[fam] / 1e6:.1f} MB |")
         lines.append("")
     c1 = os.path.join(src, "c1_launches.csv")
     if os.path.exists(c1):  # launch-gap breakdown of one eager C1 solve (tools/c1_once.py)
