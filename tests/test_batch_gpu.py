@@ -160,3 +160,18 @@ def test_three_channel_segment_lengths(rows):
         ref = oracle.solve(gb, tb, cb, 10.0, 0.2, 3, 0.99, 3)
         assert float(np.max(np.abs(got[b] - ref))) <= TOL * target_range(tb)
     assert float(np.max(np.abs(one - oracle.solve(*ps[0], 10.0, 0.2, 3, 0.99, 3)))) <= TOL * target_range(ps[0][1])
+
+
+def test_batch_host_pointers_match_device():
+    """dts_create_batch / dts_solve with numpy (host) arrays: the library stages them; same
+    result as device tensors."""
+    B, H, W = 3, 50, 70
+    ps, g, t, c = problems(B, H, W, 3, 2, seed=31)
+    dev = batch_solve(g, t, c, 8.0, 0.2, 3, 0.99, 4)
+    ctx = dts.dts_create_batch(np.ascontiguousarray(g), 8.0, 0.2, 3)
+    try:
+        out = np.empty_like(t)
+        dts.dts_solve(ctx, np.ascontiguousarray(t), np.ascontiguousarray(c), 0.99, 4, out)
+    finally:
+        dts.dts_destroy(ctx)
+    np.testing.assert_array_equal(out.astype(np.float64), dev)
