@@ -8,9 +8,13 @@
 # launches; k_row_pass launch 5 of a step is the first ROWUPD instance); 4) launch list of one
 # eager C1 solve (302 launches) for the launch-gap breakdown (kernel time vs the event-timed
 # solve).
+# PART=c4 runs 1)-3), PART=extra runs 4)-5) (each part's outputs stay under gpurun's 64 MiB
+# copy-back limit); unset runs both.
 set -u
 OUT=${OUT:-gpurun_out}
+PART=${PART:-all}
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-extras"
+if [ "$PART" != extra ]; then
 $CMD > $OUT/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -s 199 -c 199 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
@@ -20,6 +24,8 @@ for spec in "k_col_cluster 4" "k_row_pass 2" "k_row_pass 4 row_update" "k_update
   ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 \
       -o $OUT/full_$tag $CMD > $OUT/ncu_full_$tag.log 2>&1
 done
+fi
+if [ "$PART" != c4 ]; then
 # 5) C3 (8 x 4K, C_t = 3) in one batched context, one iteration per solve (tools/c3_batch.py):
 #    the launch list of create + five solves, and one --set full capture each of a column pass
 #    (launch 10 of k_col_cluster: after the 8 per-image support passes and the first) and a row
@@ -35,4 +41,5 @@ done
 python tools/c1_once.py > $OUT/c1_once.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -s 307 -c 302 --csv --log-file $OUT/c1_launches.csv \
     python tools/c1_once.py > $OUT/ncu_c1.log 2>&1
+fi
 echo done
