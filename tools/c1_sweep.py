@@ -10,7 +10,8 @@ for name in ("C1", "C2"):
     g, t, c = make_inputs(name)
     gd, td, cd = (torch.from_numpy(a).cuda() for a in (g, t, c))
     o = torch.empty_like(td)
-    for cb in (0, 1, 2, 3, 4, 6):
+    dts.dts_set_option("col_rows", int(os.environ.get("COL_ROWS", "0")))
+    for cb in [int(x) for x in os.environ.get("CBS", "0 1 2 3 4 6").split()]:
         dts.dts_set_option("col_cluster", cb)
         with dts.Solver(gd, cfg.sigma_s, cfg.sigma_r, cfg.N) as s:
             ts = []
@@ -18,5 +19,7 @@ for name in ("C1", "C2"):
                 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
                 e0.record(); s.solve(td, cd, cfg.lam, cfg.iters, out=o); e1.record(); torch.cuda.synchronize()
                 ts.append(round(e0.elapsed_time(e1), 3))
-        print(json.dumps({"cfg": name, "col_cluster": cb, "ms": ts}), flush=True)
+        print(json.dumps({"cfg": name, "col_rows": dts.dts_get_option("col_rows"), "col_cluster": cb, "ms": ts}),
+              flush=True)
     dts.dts_set_option("col_cluster", 0)
+    dts.dts_set_option("col_rows", 0)
