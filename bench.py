@@ -320,8 +320,9 @@ def extra_configs(dts, torch, dev, stream, timer, peak):
 
 def sweeps(dts, torch, dev, stream, timer):
     """The paper's scaling claims on the C1 shape: run time nearly independent of sigma_s and
-    sigma_r and linear in the iteration count.  Solve time (eager first solve
-    of a fresh context, and a repeat) per setting."""
+    sigma_r and linear in the iteration count; and linear in the pixel count
+     over 0.35-100 Mpixel.  Solve time (eager first solve of a fresh context, and a repeat)
+    per setting."""
     cfg = CONFIGS["C1"]
     g, t, c = make_inputs("C1")
     gd, td, cd = (torch.from_numpy(a).to(dev) for a in (g, t, c))
@@ -356,6 +357,39 @@ def sweeps(dts, torch, dev, stream, timer):
     fit = A @ coef
     out["iterations"]["linear_fit_first"] = {"ms_at_0": float(coef[0]), "ms_per_iteration": float(coef[1]),
                                              "r2": float(1 - np.sum((y - fit) ** 2) / np.sum((y - y.mean()) ** 2))}
+    # run time against the pixel count ("linear in the number of pixels"): device-generated
+    # images from 0.35 to 100 Mpixel (3-channel guide, 20 iterations), the median of three eager
+    # solves (graph replay off) after a warm-up solve on the same context
+    del gd, td, cd, o
+    out["pixels"] = {"shape": "H x W random 3-channel guide with a step edge, 1-channel target, sigma_s = 16, "
+                            "sigma_r = 0.1, N = 3, 20 iterations, median of 3 eager solves"}
+    graphs0 = dts.dts_get_option("graphs")
+    dts.dts_set_option("graphs", 0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(5)
+    for H, W in ((500, 700), (1000, 1400), (2000, 2800), (4000, 5600), (7071, 10000), (10000, 10000)):
+        gq = torch.rand(H, W, 3, device=dev, generator=gen) * 0.05
+        gq[H // 3:, W // 3:, :] += 0.5
+        tq = torch.rand(H, W, device=dev, generator=gen)
+        cq = torch.rand(H, W, device=dev, generator=gen)
+        oq = torch.empty_like(tq)
+        ctx = dts.dts_create(gq, 16.0, 0.1, 3, stream=stream.cuda_stream)
+        dts.dts_solve(ctx, tq, cq, 0.99, 20, oq, stream=stream.cuda_stream)  # warm-up
+        ts = sorted(timer(lambda: dts.dts_solve(ctx, tq, cq, 0.99, 20, oq, stream=stream.cuda_stream), 1)
+                    for _ in range(3))
+        dts.dts_destroy(ctx)
+        out["pixels"][f"{H}x{W}"] = {"mpix": H * W / 1e6, "ms": ts[1], "ms_all": ts,
+                                     "mpix_iter_per_s": H * W * 20 / 1e6 / (ts[1] / 1e3)}
+        del gq, tq, cq, oq
+    dts.dts_set_option("graphs", graphs0)
+    sizes = [v for k, v in out["pixels"].items() if isinstance(v, dict)]
+    xp = np.array([v["mpix"] for v in sizes])
+    yp = np.array([v["ms"] for v in sizes])
+    A = np.stack([np.ones(len(xp)), xp], 1)
+    coef, *_ = np.linalg.lstsq(A, yp, rcond=None)
+    fit = A @ coef
+    out["pixels"]["linear_fit"] = {"ms_at_0": float(coef[0]), "ms_per_mpix": float(coef[1]),
+                                   "r2": float(1 - np.sum((yp - fit) ** 2) / np.sum((yp - yp.mean()) ** 2))}
     return out
 
 

@@ -301,6 +301,8 @@ dts_status dts_create_band(const float* guide_with_halo, int64_t H_total, int64_
  *   "band_overlap" row-band contexts, edge scheme: 1 (default) the all-gather of a column pass
  *                  runs on a context stream while the next row pass filters the band's
  *                  interior rows; 0 serial (same results, bit for bit)
+ *   "pdl"          programmatic dependent launch of the hot-path kernels: 1 (default) with the
+ *                  dependent launch triggered at the end of each kernel, 2 at the start, 0 off
  *   "graphs"       1 replay repeated identical solves as CUDA graphs (default), 0 never
  *   "row_update"   1 Eq. (3) step fused into the next iteration's first row pass (default)
  *   "col_rows"     0 auto (default); rows per warp segment of the cluster column kernel: 32 or

@@ -79,7 +79,9 @@ struct Options {
     std::atomic<int> col_cluster{0};  // column kernel cluster size: 0 auto, else forced (experiments)
     std::atomic<int> strip_cluster{0};     // row strips: forced cluster size of the strip plan (0 = auto)
     std::atomic<int> band_overlap{1};
-    std::atomic<int> row_two_ctas{1};  // C_t = 3 row passes of <= 3840 columns: two CTAs per SM  // row bands, edge scheme: all-gather overlapped with the next row pass
+    std::atomic<int> row_two_ctas{1};  // C_t = 3 row passes of <= 3840 columns: two CTAs per SM
+    std::atomic<int> pdl{1};           // programmatic dependent launch: 0 off, 1 on (trigger at kernel
+                                       // end; default), 2 on with the trigger at kernel start  // row bands, edge scheme: all-gather overlapped with the next row pass
     std::atomic<int> col_strips{1};   // tall single-context images: C_t = 1 column passes over row strips
                                       // (0 off, 1 auto, n >= 2: exactly n strips when they fit)
 };
@@ -655,6 +657,7 @@ bool profiler_on() {
 namespace dts {
 int option_col_cluster() { return opts_g().col_cluster.load(); }
 int row_minb2() { return opts_g().row_two_ctas.load(); }
+int option_pdl() { return opts_g().pdl.load(); }
 }  // namespace dts
 
 extern "C" {
@@ -676,6 +679,7 @@ dts_status dts_set_option(const char* name, int32_t value) {
     else if (n == "strip_cluster" && value >= 0 && value <= 16) o.strip_cluster = value;
     else if (n == "band_overlap" && (value == 0 || value == 1)) o.band_overlap = value;
     else if (n == "row_two_ctas" && (value == 0 || value == 1)) o.row_two_ctas = value;
+    else if (n == "pdl" && value >= 0 && value <= 2) o.pdl = value;
     else return DTS_E_ARG;
     return DTS_OK;
 }
@@ -704,6 +708,7 @@ int32_t dts_get_option(const char* name) {
     if (n == "strip_cluster") return o.strip_cluster;
     if (n == "band_overlap") return o.band_overlap;
     if (n == "row_two_ctas") return o.row_two_ctas;
+    if (n == "pdl") return o.pdl;
     return -1;
 }
 

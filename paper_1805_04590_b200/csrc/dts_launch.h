@@ -5,6 +5,8 @@
 
 namespace dts {
 
+// dts_set_option("pdl"): programmatic dependent launch on the hot-path kernels (default 1)
+int option_pdl();
 // launch `kern` on `s` with programmatic stream serialization (see pdl_trigger / pdl_wait)
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -18,7 +20,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = option_pdl() ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

@@ -45,6 +45,7 @@ struct Params {
     int HS, ntc;  // row strips (single-GPU FILTER): strip height, column tiles per strip (HS = H: one strip)
     float kc;
     int nsq;  // < 0: d holds distances (a = 2^(-kc d)); >= 0: d holds A1, a = A1^(2^nsq)
+    int pdl_early;  // trigger the dependent launch at the start (option pdl = 2) instead of the end
 };
 
 struct Smem {
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
         if (HASX) tma_prefetch_desc(&tm_x);
     }
     cluster_sync_all();  // every exchange barrier of the cluster is initialised and armed
-    pdl_trigger();
+    if (p.pdl_early) pdl_trigger();
     pdl_wait();  // the previous kernel's output (this pass's input X) is complete
 
     // lane 0 of warp q: TMA boxes of segment q of `tile` into the landing zone (every warp
@@ -493,6 +494,9 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
         // segF slot and its own part of the landing zone, which no other warp reads after
         // the anticausal carry barrier of this tile
     }
+    // the next kernel may launch once every CTA is here (triggering at the start lets its CTAs
+    // take SM resources while this persistent grid runs)
+    if (!p.pdl_early) pdl_trigger();
     cluster_sync_all();  // no CTA leaves while another may still read its shared memory
 }
 
@@ -590,7 +594,7 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
         if (HASX) tma_prefetch_desc(&tm_x);
     }
     cluster_sync_all();  // every exchange barrier of the cluster is initialised and armed
-    pdl_trigger();
+    if (p.pdl_early) pdl_trigger();
     pdl_wait();
 
     auto stage_seg = [&](int tile, int q) {  // lane 0 of warp q: segment q of `tile`
@@ -877,6 +881,9 @@ __global__ void __launch_bounds__(max_threads<nchan<CT, MODE>()>(), 1)
         // no barrier here: before the next tile's fold barrier a warp writes only its own
         // segF slot and its own part of the landing zone (as in the single-GPU kernel)
     }
+    // the next kernel may launch once every CTA is here (triggering at the start lets its CTAs
+    // take SM resources while this persistent grid runs)
+    if (!p.pdl_early) pdl_trigger();
     cluster_sync_all();  // no CTA leaves while another may still read its shared memory
 }
 
@@ -1172,6 +1179,9 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     p.HS = plan.HS > 0 ? plan.HS : (int)g.H;
     p.ntc = plan.ntc > 0 ? plan.ntc : plan.ntiles;
     p.kc = kc;
+    // PDL trigger at the end of the kernel (option pdl = 2: at the start, for experiments; a
+    // start trigger was never faster, and 20-30% slower on mid-size images)
+    p.pdl_early = option_pdl() == 2;
     CUtensorMap tx, td;
     if (!tmap(&td, d, g.pitch, g.H, 1, 2, plan.Ls)) return cudaErrorInvalidValue;
     if (mode != MODE_SUPPORT) {
@@ -1194,7 +1204,18 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (dts_device.cuh)
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    // PDL only when the grid has at most one CTA per SM: a grid of several CTAs per SM launched
+    // early lands its clusters on the SMs the previous kernel frees first, several to an SM,
+    // and keeps that imbalance for the whole persistent launch (7071 x 10000, 4 row strips of
+    // 405 CTAs: 27 ms per solve with PDL, 22.5 without)
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (nsm < 1) nsm = 1;
+    }
+    cfg.numAttrs = (option_pdl() && plan.grid.x <= (unsigned)nsm) ? 2 : 1;
     void* args[] = {&tx, &td, &p};
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return e;
@@ -1258,7 +1279,6 @@ __global__ void __launch_bounds__(128) k_seam_fix(float* __restrict__ x, int Ct,
     const int64_t col = (int64_t)blockIdx.x * 128 + threadIdx.x;
     const int j = blockIdx.y + 1;  // seam between strips j - 1 and j
     const int k0 = blockIdx.z * 8;
-    pdl_trigger();
     pdl_wait();
     if (col >= W) return;
     const int64_t s0 = (int64_t)j * HS, ew = (int64_t)ntc * 32;

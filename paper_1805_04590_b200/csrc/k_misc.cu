@@ -231,7 +231,6 @@ __global__ void __launch_bounds__(256) k_prologue(const float* __restrict__ targ
                                                   const float* __restrict__ Sy, int support_mode,
                                                   float* __restrict__ Z, float* __restrict__ T,
                                                   float* __restrict__ chat) {
-    pdl_trigger();
     pdl_wait();
     const int64_t per_row = g.pitch / 4;
     const int64_t n = g.H * per_row;
@@ -300,7 +299,6 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X, flo
                                                 const float* __restrict__ T, const float* __restrict__ chat,
                                                 Geometry g, float lam, float step, float* __restrict__ out_hwc,
                                                 unsigned* __restrict__ resid) {
-    pdl_trigger();
     pdl_wait();
     const int64_t per_row = g.pitch / 4;
     const int64_t n = g.H * per_row;
@@ -499,7 +497,6 @@ __global__ void __launch_bounds__(256) k_update_stereo(const float* __restrict__
                                                        const float* __restrict__ right, int Cgr, Geometry g,
                                                        float lam, float step, float gamma, float eps,
                                                        float* __restrict__ out) {
-    pdl_trigger();
     pdl_wait();
     const int Cg = CG > 0 ? CG : Cgr;
     const float e2 = eps * eps;

@@ -33,6 +33,7 @@ struct RowParams {
     float lam, step;
     int64_t plane, pitch, rowstride;
     int64_t rowlen;  // floats staged per row (the pitch; a row strip's padded width)
+    int pdl_early;   // trigger the dependent launch at the start (option pdl = 2) instead of the end
     int H, W, G, R, nbuf;
     float kc;
 };
@@ -145,7 +146,7 @@ __device__ __forceinline__ void row_pass_body(const RowParams& p) {
         mbar_init(&bar[1], 1);
         fence_mbar_init();
     }
-    pdl_trigger();
+    if (p.pdl_early) pdl_trigger();
     pdl_wait();  // the previous kernel's output (the row input, Z / T / chat) is complete
     __syncthreads();
 
@@ -366,6 +367,9 @@ __device__ __forceinline__ void row_pass_body(const RowParams& p) {
             }
         }
     }
+    // the next kernel may launch once every CTA is past its last row group (triggering at the
+    // start lets its CTAs take SM resources while this persistent grid runs)
+    if (!p.pdl_early) pdl_trigger();
     if (threadIdx.x == 0) bulk_wait0();
 }
 
@@ -443,6 +447,13 @@ cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowP
     return cudaSuccess;
 }
 
+// PDL trigger at the end of the kernel (option pdl = 2: at the start, for experiments)
+static int row_pdl_early(const RowPlan& plan, const Geometry& g) {
+    (void)plan;
+    (void)g;
+    return option_pdl() == 2;
+}
+
 template <int L, int CT, int MODE>
 static cudaError_t launch_t(const RowPlan& plan, const RowParams& p, cudaStream_t s) {
     if constexpr (L == 12 && CT == 3 && MODE != MODE_SUPPORT) {
@@ -494,6 +505,7 @@ cudaError_t launch_row_update(const RowPlan& plan, const Geometry& g, int Ct, co
     p.R = plan.R;
     p.nbuf = plan.nbuf;
     p.kc = kc;
+    p.pdl_early = row_pdl_early(plan, g);
     switch (plan.L) {
         case 4: return launch_ct<4, MODE_ROWUPD>(plan, p, Ct, s);
         case 12: return launch_ct<12, MODE_ROWUPD>(plan, p, Ct, s);
@@ -519,6 +531,7 @@ cudaError_t launch_row_pass(const RowPlan& plan, const Geometry& g, int Ct, int 
     p.R = plan.R;
     p.nbuf = plan.nbuf;
     p.kc = kc;
+    p.pdl_early = row_pdl_early(plan, g);
     if (mode == MODE_SUPPORT) {
         switch (plan.L) {
             case 4: return launch_t<4, 1, MODE_SUPPORT>(plan, p, s);
@@ -608,7 +621,6 @@ __global__ void __launch_bounds__(128) k_row_seam_fix(float* __restrict__ x, int
                                                       bool raw) {
     const int64_t r = blockIdx.x;
     const int j = blockIdx.y + 1;
-    pdl_trigger();
     pdl_wait();
     const int64_t cj = st.c[j];
     const float* gm = gam + ((int64_t)(j - 1) * Hp + r0 + r) * L;
