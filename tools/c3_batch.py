@@ -19,7 +19,7 @@ g, t, c = (torch.from_numpy(np.ascontiguousarray(np.stack([h[j] for h in host]))
 o = torch.empty_like(t)
 for cb in [int(a) for a in sys.argv[1:]] or [0]:
     with dts.options(strip_cluster=cb, col_rows=int(os.environ.get("COL_ROWS", "0")),
-                     row_two_ctas=int(os.environ.get("ROW_TWO", "1"))):
+                     row_two_ctas=int(os.environ.get("ROW_TWO", "1")), pdl=int(os.environ.get("PDL", "1"))):
       try:
         with dts.Solver(g, cfg.sigma_s, cfg.sigma_r, cfg.N, batched=True) as s:
             s.solve(t, c, cfg.lam, iters, out=o)
