@@ -80,6 +80,7 @@ struct Options {
     std::atomic<int> strip_cluster{0};     // row strips: forced cluster size of the strip plan (0 = auto)
     std::atomic<int> band_overlap{1};
     std::atomic<int> row_two_ctas{1};  // C_t = 3 row passes of <= 3840 columns: two CTAs per SM
+    std::atomic<int> row_seg{0};       // row kernel samples per thread: 0 auto, 4 / 12 / 20 / 36 forced
     std::atomic<int> pdl{1};           // programmatic dependent launch: 0 off, 1 on (trigger at kernel
                                        // end; default), 2 on with the trigger at kernel start  // row bands, edge scheme: all-gather overlapped with the next row pass
     std::atomic<int> col_strips{1};   // tall single-context images: C_t = 1 column passes over row strips
@@ -658,6 +659,7 @@ namespace dts {
 int option_col_cluster() { return opts_g().col_cluster.load(); }
 int row_minb2() { return opts_g().row_two_ctas.load(); }
 int option_pdl() { return opts_g().pdl.load(); }
+int option_row_seg() { return opts_g().row_seg.load(); }
 }  // namespace dts
 
 extern "C" {
@@ -680,6 +682,8 @@ dts_status dts_set_option(const char* name, int32_t value) {
     else if (n == "band_overlap" && (value == 0 || value == 1)) o.band_overlap = value;
     else if (n == "row_two_ctas" && (value == 0 || value == 1)) o.row_two_ctas = value;
     else if (n == "pdl" && value >= 0 && value <= 2) o.pdl = value;
+    else if (n == "row_seg" && (value == 0 || value == 4 || value == 12 || value == 20 || value == 36))
+        o.row_seg = value;
     else return DTS_E_ARG;
     return DTS_OK;
 }
@@ -709,6 +713,7 @@ int32_t dts_get_option(const char* name) {
     if (n == "band_overlap") return o.band_overlap;
     if (n == "row_two_ctas") return o.row_two_ctas;
     if (n == "pdl") return o.pdl;
+    if (n == "row_seg") return o.row_seg;
     return -1;
 }
 

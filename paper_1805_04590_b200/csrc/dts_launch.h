@@ -7,6 +7,8 @@ namespace dts {
 
 // dts_set_option("pdl"): programmatic dependent launch on the hot-path kernels (default 1)
 int option_pdl();
+// dts_set_option("row_seg"): forced row-kernel segment length (0 auto; 4, 12, 20, 36)
+int option_row_seg();
 // launch `kern` on `s` with programmatic stream serialization (see pdl_trigger / pdl_wait)
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -382,12 +382,21 @@ cudaError_t plan_row_pass(const Geometry& g, int Ct, int mode, int num_sms, RowP
     // Narrow rows: the smallest segment length that fits >= 2 rows per CTA (G <= 128).  A
     // row's scan is latency-bound; several rows per CTA keep more of them in flight (C1/C2:
     // row pass 12.7 -> 10.5 us with L = 12 instead of 4); not with L > 12
-    // (C3, W = 3840: L = 36 gave 84.7 us against 51.6 at L = 12).  Wide rows: the smallest L with
-    // G <= 512 (one row per CTA, the segment loads coalesce either way).
+    // (C3, W = 3840: L = 36 gave 84.7 us against 51.6 at L = 12).  Wide rows: the smallest L >= 12
+    // with G <= 512 (one row per CTA, the segment loads coalesce either way).
     int L = 0, G = 0;
+    const int forced = option_row_seg();  // experiments: a forced segment length
+    if (forced > 0 && (g.W + forced - 1) / forced <= 512) {
+        L = forced;
+        G = (int)((g.W + forced - 1) / forced);
+    }
     for (int lim : {128, 512}) {
+        if (G) break;
         for (int cand : kLs) {
             if (lim == 128 && cand > 12) break;  // long segments cost more than they save
+            // wide rows never take 4 samples per thread (512 threads per row at W = 2000: row pass
+            // 88 us against 54 at 12 samples, C_t = 1, H = 10000; 1920 x 1080 x 3: 25 -> 19 us)
+            if (lim == 512 && cand < 12) continue;
             int64_t need = (g.W + cand - 1) / cand;
             if (need <= lim) {
                 L = cand;
