@@ -96,6 +96,21 @@ Options& opts_g() {
 struct dts_comm {
     dts::Comm* c = nullptr;
 };
+struct dts_ctx;
+extern "C" {  // defined inside the extern "C" section below
+static bool strip_plan_n(dts_ctx* ctx, int n, int Ct, ColPlan* out);
+static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out);
+}
+
+// row strips of one image (single GPU; plan_strips / choose_col): n strips of HS rows, per pass
+// the measured seam length L and the edge profiles [n][L][pitch], the edge-row buffer
+// [n][2][3][ntc * 32] (each strip's last / first output row of up to three planes)
+struct StripSet {
+    int n = 0, HS = 0;
+    std::vector<int> L;
+    std::vector<float*> gam, theta;
+    float* edge = nullptr;
+};
 
 struct dts_ctx {
     int device = 0;
@@ -114,11 +129,8 @@ struct dts_ctx {
     std::vector<int> edge_L;
     // single-GPU row strips for the C_t = 1 FILTER column passes of tall images (DESIGN.md
     // section 7): the cluster plan over strips, per pass the seam length and edge profiles
-    int vs_n = 0, vs_HS = 0;
-    ColPlan vs_plan{};
-    std::vector<int> vs_L;
-    std::vector<float*> vs_gam, vs_theta;  // [vs_n][L][pitch] each
-    float* vs_edge = nullptr;              // [vs_n][2][1][ntc * 32]: each strip's last / first output row
+    std::vector<StripSet*> ssets;  // every strip set built so far (owned)
+    StripSet* vs_set = nullptr;    // the create-time C_t = 1 set (plan_strips), or null
     // batched contexts (dts_create_batch): `batch` images of batch_H rows stacked vertically, the
     // column recurrences cut between them (d_y = +inf, A1 = 0 at each image's first row); the
     // FILTER column passes run every image's tiles in one launch (per-C_t strip plan, no seams)
@@ -691,11 +703,14 @@ dts_status dts_set_option(const char* name, int32_t value) {
 // debug hook (not in include/dts.h): the row-strip plan of a context (plan_strips)
 int32_t dts_debug_strips(const dts_ctx* ctx, int32_t* HS, int32_t* L3, int32_t* CB, int32_t* grid) {
     if (!ctx) return -1;
-    if (HS) *HS = ctx->vs_HS;
-    for (int i = 0; i < 3 && L3; ++i) L3[i] = i < (int)ctx->vs_L.size() ? ctx->vs_L[i] : 0;
-    if (CB) *CB = ctx->vs_plan.CB;
-    if (grid) *grid = (int)ctx->vs_plan.grid.x;
-    return ctx->vs_n;
+    const StripSet* ss = ctx->vs_set;
+    ColPlan p{};
+    if (ss) strip_plan_n(const_cast<dts_ctx*>(ctx), ss->n, 1, &p);
+    if (HS) *HS = ss ? ss->HS : 0;
+    for (int i = 0; i < 3 && L3; ++i) L3[i] = ss && i < (int)ss->L.size() ? ss->L[i] : 0;
+    if (CB) *CB = ss ? p.CB : 0;
+    if (grid) *grid = ss ? (int)p.grid.x : 0;
+    return ss ? ss->n : 0;
 }
 
 int32_t dts_get_option(const char* name) {
@@ -895,56 +910,43 @@ static dts_status row_pass_x(dts_ctx* ctx, int Ct, int mode, int pass, const flo
 
 // Tall single-context images: a column tile must sit on chip across its
 // cluster, and the clusters a tall column needs (16 CTAs for C4) pack only 7 per GPU (112 of
-// 148 SMs).  Cut the image into row strips whose columns fit smaller clusters, run the C_t = 1
-// FILTER passes over all strips in one launch (zero carry at each strip's top, link below cut)
-// and add the carries at the seams afterwards (k_seam_fix, reading R26).  Chosen at create when
-// the strips use >= 10% more SMs and every pass's measured carry-decay length L (k_edge_length:
-// influence below 2^-26 after L rows) fits twice in the shortest strip.
-static dts_status plan_strips(dts_ctx* ctx, cudaStream_t s) {
+// 148 SMs); columns taller than 16 CTAs hold do not fit a cluster at all.  Cut the image into
+// row strips whose columns fit smaller clusters, run the FILTER passes over all strips in one
+// launch (zero carry at each strip's top, link below cut) and add the carries at the seams
+// afterwards (k_seam_fix, reading R26).  A strip set (n strips) holds every pass's measured
+// carry-decay length L (k_edge_length: influence below 2^-26 after L rows), which must fit
+// twice in the shortest strip, the edge profiles and the edge-row buffer; its per-C_t plans
+// are made on use.
+
+// the plan over n strips for C_t (a strip column must fit a cluster)
+static bool strip_plan_n(dts_ctx* ctx, int n, int Ct, ColPlan* out) {
     const Geometry& g = ctx->g;
-    ColPlan base{};
-    if (plan_col(g, 1, MODE_FILTER, ctx->num_sms, &base) != cudaSuccess || base.kind != 1) {
-        cudaGetLastError();
-        return DTS_OK;
-    }
-    // only for columns that need big clusters (GPC packing wastes SMs) and several tile rounds per
-    // launch (throughput-bound): small images stay latency-bound and keep one strip
-    const int forced0 = opts_g().col_strips.load();
-    const int rounds = base.ntiles * base.CB / (int)base.grid.x;
-    if (forced0 < 2 && (base.CB < 8 || rounds < 4)) return DTS_OK;
-    // preference (measured on C4, unprofiled 20-iteration solves, tools/strips4.sh): the fewest
-    // strips whose plan covers >= 90% of the SMs and adds >= 10% over one strip (C4: 2 strips of
-    // 5000 rows on 15 clusters of 9, 30.58 ms against 31.18 unstripped; 4 strips x clusters of 4
-    // 30.84; 16 strips x 2 CTAs of 320 rows per SM 31.33 -- its column kernel is the fastest,
-    // 0.204 ms, but 15 seams cost more than that saves)
-    int best_n = 0;
-    ColPlan best{};
-    const int forced = opts_g().col_strips.load();
-    for (int n : {2, 4, 8, 16, 32}) {
-        if (forced >= 2 && n != forced) continue;
-        const int64_t HS = (g.H + n - 1) / n;
-        if (HS < 64 || (n - 1) * HS >= g.H) break;
-        Geometry gs = g;  // planned as n strips side by side: the launch has n times the tiles
-        gs.H = HS;
-        gs.W = g.W * n;
-        gs.pitch = (gs.W + 31) / 32 * 32;
-        gs.plane = HS * gs.pitch;
-        ColPlan ps{};
-        if (plan_col(gs, 1, MODE_FILTER, ctx->num_sms, &ps, opts_g().strip_cluster.load()) != cudaSuccess ||
-            ps.kind != 1) {
-            cudaGetLastError();
-            continue;
-        }
-        const bool wide = ps.grid.x * 10 >= (unsigned)ctx->num_sms * 9 && ps.grid.x * 10 >= base.grid.x * 11;
-        if (wide || forced >= 2) {
-            best_n = n;
-            best = ps;
-            best.HS = (int)HS;
-            break;
-        }
-    }
-    if (!best_n) return DTS_OK;
-    const int n = best_n, HS = best.HS;
+    const int64_t HS = (g.H + n - 1) / n;
+    if (n < 2 || HS < 64 || (int64_t)(n - 1) * HS >= g.H) return false;
+    Geometry gs = g;  // planned as n strips side by side: the launch has n times the tiles
+    gs.H = HS;
+    gs.W = g.W * n;
+    gs.pitch = (gs.W + 31) / 32 * 32;
+    gs.plane = HS * gs.pitch;
+    ColPlan ps{};
+    const bool ok = gs.W <= ((int64_t)1 << 31) / 2 &&
+                    plan_col(gs, Ct, MODE_FILTER, ctx->num_sms, &ps, opts_g().strip_cluster.load()) == cudaSuccess &&
+                    ps.kind == 1 && colc_strips_supported(Ct, ps.Ls);
+    cudaGetLastError();
+    if (!ok) return false;
+    ps.HS = (int)HS;
+    ps.ntc = (int)((g.W + 31) / 32);
+    ps.ntiles = ps.ntc * n;
+    *out = ps;
+    return true;
+}
+
+// measure the seam lengths of n strips and build their profiles (syncs s once); *out stays
+// null when a seam correction would overlap the next (2L + 1 > the last strip)
+static dts_status build_strip_set(dts_ctx* ctx, int n, cudaStream_t s, StripSet** out) {
+    *out = nullptr;
+    const Geometry& g = ctx->g;
+    const int HS = (int)((g.H + n - 1) / n);
     const int64_t Hlast = g.H - (int64_t)(n - 1) * HS;
     const int N = ctx->N;
     cudaError_t e;
@@ -974,36 +976,82 @@ static dts_status plan_strips(dts_ctx* ctx, cudaStream_t s) {
     std::vector<int> L(N);
     for (int i = 0; i < N; ++i) {
         L[i] = (int)std::max<unsigned>(1u, std::max(len[2 * i], len[2 * i + 1]));
-        if (2 * (int64_t)L[i] + 1 > Hlast) return DTS_OK;  // a seam correction would overlap: keep one strip
+        if (2 * (int64_t)L[i] + 1 > Hlast) return DTS_OK;  // a seam correction would overlap
     }
-    ctx->vs_gam.assign(N, nullptr);
-    ctx->vs_theta.assign(N, nullptr);
+    StripSet* ss = new StripSet();
+    ss->n = n;
+    ss->HS = HS;
+    ss->L = L;
+    ctx->ssets.push_back(ss);  // owned by the context from here on (dts_destroy frees it)
+    ss->gam.assign(N, nullptr);
+    ss->theta.assign(N, nullptr);
     for (int i = 0; i < N && st == DTS_OK; ++i) {
         const size_t bytes = (size_t)n * L[i] * g.pitch * sizeof(float);
-        if ((e = cudaMallocAsync((void**)&ctx->vs_gam[i], bytes, s)) != cudaSuccess ||
-            (e = cudaMallocAsync((void**)&ctx->vs_theta[i], bytes, s)) != cudaSuccess)
+        if ((e = cudaMallocAsync((void**)&ss->gam[i], bytes, s)) != cudaSuccess ||
+            (e = cudaMallocAsync((void**)&ss->theta[i], bytes, s)) != cudaSuccess)
             return cuda_fail(e);
         for (int b = 0; b < n && st == DTS_OK; ++b) {
             Geometry gs = g;
             gs.H = std::min<int64_t>(HS, g.H - (int64_t)b * HS);
             st = run_launch(ctx, F_COEF, (double)g.W * 2 * L[i] * 12.0, s, [&] {
                 return launch_edge_profiles(ctx->dy + (int64_t)b * HS * g.pitch, gs, L[i], ctx->kc[i],
-                                            ctx->vs_gam[i] + (size_t)b * L[i] * g.pitch,
-                                            ctx->vs_theta[i] + (size_t)b * L[i] * g.pitch, s);
+                                            ss->gam[i] + (size_t)b * L[i] * g.pitch,
+                                            ss->theta[i] + (size_t)b * L[i] * g.pitch, s);
             });
         }
     }
     if (st != DTS_OK) return st;
-    if ((e = cudaMallocAsync((void**)&ctx->vs_edge, (size_t)n * 2 * ((g.W + 31) / 32) * 32 * sizeof(float), s)) !=
+    // edge rows of up to C_t = 3 planes (the cluster kernel's widest)
+    if ((e = cudaMallocAsync((void**)&ss->edge, (size_t)n * 2 * 3 * ((g.W + 31) / 32) * 32 * sizeof(float), s)) !=
         cudaSuccess)
         return cuda_fail(e);
-    ctx->vs_n = n;
-    ctx->vs_HS = HS;
-    ctx->vs_L = L;
-    ctx->vs_plan = best;
-    ctx->vs_plan.ntc = (int)((g.W + 31) / 32);
-    ctx->vs_plan.ntiles = ctx->vs_plan.ntc * n;
+    *out = ss;
     return DTS_OK;
+}
+
+static StripSet* find_strip_set(dts_ctx* ctx, int n) {
+    for (StripSet* ss : ctx->ssets)
+        if (ss->n == n) return ss;
+    return nullptr;
+}
+
+// create time, C_t = 1: strips for columns that fit a cluster but need big clusters (GPC
+// packing wastes SMs) and several tile rounds per launch (throughput-bound; small images stay
+// latency-bound and keep one strip).  Preference (measured on C4, unprofiled 20-iteration
+// solves, tools/strips4.sh): the fewest strips whose plan covers >= 90% of the SMs and adds
+// >= 10% over one strip (C4: 2 strips of 5000 rows on 15 clusters of 9, 30.58 ms against 31.18
+// unstripped; 4 strips x clusters of 4 30.84; 16 strips x 2 CTAs of 320 rows per SM 31.33 -- its
+// column kernel is the fastest, 0.204 ms, but 15 seams cost more than that saves).  Columns
+// too tall for one cluster get their strips per C_t at the first solve (choose_col).
+static dts_status plan_strips(dts_ctx* ctx, cudaStream_t s) {
+    const Geometry& g = ctx->g;
+    ColPlan base{};
+    if (plan_col(g, 1, MODE_FILTER, ctx->num_sms, &base) != cudaSuccess || base.kind != 1) {
+        cudaGetLastError();
+        return DTS_OK;
+    }
+    const int forced = opts_g().col_strips.load();
+    const int rounds = base.ntiles * base.CB / (int)base.grid.x;
+    if (forced < 2 && (base.CB < 8 || rounds < 4)) return DTS_OK;
+    int best_n = 0;
+    for (int n : {2, 4, 8, 16, 32}) {
+        if (forced >= 2 && n != forced) continue;
+        ColPlan ps{};
+        if (!strip_plan_n(ctx, n, 1, &ps)) {
+            if ((g.H + n - 1) / n < 64) break;
+            continue;
+        }
+        const bool wide = ps.grid.x * 10 >= (unsigned)ctx->num_sms * 9 && ps.grid.x * 10 >= base.grid.x * 11;
+        if (wide || forced >= 2) {
+            best_n = n;
+            break;
+        }
+    }
+    if (!best_n) return DTS_OK;
+    StripSet* ss = nullptr;
+    dts_status st = build_strip_set(ctx, best_n, s, &ss);
+    if (st == DTS_OK && ss) ctx->vs_set = ss;
+    return st;
 }
 
 // Row-band contexts: every rank measures how many rows a carry
@@ -1195,7 +1243,7 @@ static dts_status create_impl(const float* guide, int64_t H_total, int64_t row0,
     // the cluster column kernel reads a_1^{d_y} instead of d_y (one exp per pixel, written by
     // the derivative kernel, instead of one per pixel and pass); later passes square it (R5:
     // sigma halves per pass).  Rows 0..H: row H is the bottom link (+inf -> 0).
-    const bool with_a1 = filter_passes <= 4 && (comm || cp.kind == 1 || batch > 1);
+    const bool with_a1 = filter_passes <= 4;  // every cluster column pass reads it (full height or strips)
     if (with_a1 && (e = cudaMallocAsync((void**)&ctx->A1y_base, (size_t)(Hx + 1) * ctx->g.pitch * sizeof(float), s)) !=
                        cudaSuccess) {
         st = cuda_fail(e);
@@ -1409,25 +1457,62 @@ static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out) {
     return true;
 }
 
-// FILTER column pass i over the C_t planes at x, on plan cp (dts_solve's choice for C_t): row
-// strips + the seam fix-up for tall C_t = 1 images (plan_strips), the cluster kernel on A1
-// (image-high strips in batched contexts: cp.HS > 0), else the decoupled kernel on d_y.
-static dts_status col_filter_pass(dts_ctx* ctx, const ColPlan& cp, int Ct, int i, float* x, double bytes,
-                                  cudaStream_t s) {
+// The FILTER column plan of a solve / confidence / stereo call for C_t: the batched strips, the
+// create-time C_t = 1 strips, one cluster over the full height, or -- when no cluster holds
+// the full height -- the fewest row strips whose columns fit one (a strip set built on first
+// use: one stream sync), else the decoupled kernel.  *ss: the strip set whose seams need the
+// fix-up (null for none).
+static dts_status choose_col(dts_ctx* ctx, int Ct, cudaStream_t s, ColPlan* cp, StripSet** ss) {
+    *ss = nullptr;
+    if (batch_strip_plan(ctx, Ct, cp)) return DTS_OK;
+    const bool strips_ok = !ctx->comm && ctx->batch == 1 && ctx->A1y && opts_g().col_strips.load() != 0 &&
+                           opts_g().col_kernel.load() == 0;
+    if (Ct == 1 && ctx->vs_set && strips_ok && strip_plan_n(ctx, ctx->vs_set->n, 1, cp)) {
+        *ss = ctx->vs_set;
+        return DTS_OK;
+    }
+    const cudaError_t e = ctx->comm ? plan_col_pass(ctx->g, Ct, MODE_FILTER, ctx->num_sms, cp)
+                                    : plan_col(ctx->g, Ct, MODE_FILTER, ctx->num_sms, cp);
+    cudaGetLastError();
+    if (e == cudaSuccess && cp->kind == 1) return DTS_OK;
+    if (strips_ok && Ct <= 3) {
+        for (int n = 2; n <= 64; n *= 2) {
+            ColPlan ps{};
+            if (!strip_plan_n(ctx, n, Ct, &ps)) {
+                if ((ctx->g.H + n - 1) / n < 64) break;
+                continue;
+            }
+            StripSet* set = find_strip_set(ctx, n);
+            if (!set) {
+                const dts_status st = build_strip_set(ctx, n, s, &set);
+                if (st != DTS_OK) return st;
+                if (!set) break;  // the seam lengths do not fit: shorter strips would not either
+            }
+            *cp = ps;
+            *ss = set;
+            return DTS_OK;
+        }
+    }
+    return e == cudaSuccess ? DTS_OK : DTS_E_SHAPE;
+}
+
+// FILTER column pass i over the C_t planes at x, on plan cp (choose_col): over row strips (ss)
+// + the seam fix-up, the cluster kernel on A1 (image-high strips in batched contexts: cp.HS >
+// 0), else the decoupled kernel on d_y.
+static dts_status col_filter_pass(dts_ctx* ctx, const ColPlan& cp, const StripSet* ss, int Ct, int i, float* x,
+                                  double bytes, cudaStream_t s) {
     const Geometry& g = ctx->g;
-    const bool strips = Ct == 1 && ctx->vs_n > 1 && cp.kind == 1 && !ctx->comm && opts_g().col_strips.load();
     dts_status st = run_launch(ctx, F_COL, bytes, s, [&] {
-        if (strips)  // row strips (plan_strips); the seams are fixed by the launch that follows
-            return launch_col_cluster(ctx->vs_plan, g, 1, MODE_FILTER, x, ctx->A1y, ctx->kc[i], nullptr, nullptr, s, i,
-                                      nullptr, nullptr, nullptr, ctx->vs_edge);
+        if (ss)  // row strips; the seams are fixed by the launch that follows
+            return launch_col_cluster(cp, g, Ct, MODE_FILTER, x, ctx->A1y, ctx->kc[i], nullptr, nullptr, s, i,
+                                      nullptr, nullptr, nullptr, ss->edge);
         if (cp.kind == 1 && ctx->A1y && i < 4)
             return launch_col_cluster(cp, g, Ct, MODE_FILTER, x, ctx->A1y, ctx->kc[i], nullptr, nullptr, s, i);
         return col_launch(ctx, cp, Ct, MODE_FILTER, x, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
     });
-    if (st == DTS_OK && strips)
-        st = run_launch(ctx, F_SEAM, (double)g.W * 12.0 * (ctx->vs_n - 1) * 2 * ctx->vs_L[i], s, [&] {
-            return launch_seam_fix(x, 1, g, ctx->vs_HS, ctx->vs_n, ctx->vs_L[i], ctx->vs_gam[i], ctx->vs_theta[i],
-                                   ctx->vs_edge, s);
+    if (st == DTS_OK && ss)
+        st = run_launch(ctx, F_SEAM, (double)g.W * 12.0 * Ct * (ss->n - 1) * 2 * ss->L[i], s, [&] {
+            return launch_seam_fix(x, Ct, g, ss->HS, ss->n, ss->L[i], ss->gam[i], ss->theta[i], ss->edge, s);
         });
     return st;
 }
@@ -1437,13 +1522,8 @@ static dts_status col_filter_pass(dts_ctx* ctx, const ColPlan& cp, int Ct, int i
 int32_t dts_debug_col_plan(dts_ctx* ctx, int32_t Ct, int32_t* out) {
     if (!ctx || !out || Ct < 1) return -1;
     ColPlan p{};
-    if (!batch_strip_plan(ctx, Ct, &p) &&
-        (ctx->comm ? plan_col_pass(ctx->g, Ct, MODE_FILTER, ctx->num_sms, &p)
-                   : plan_col(ctx->g, Ct, MODE_FILTER, ctx->num_sms, &p)) != cudaSuccess) {
-        cudaGetLastError();
-        return -1;
-    }
-    if (p.kind == 1 && ctx->vs_n > 1 && Ct == 1) p = ctx->vs_plan;
+    StripSet* ss = nullptr;
+    if (choose_col(ctx, Ct, ctx->last_stream, &p, &ss) != DTS_OK) return -1;
     const int32_t v[7] = {p.kind, p.CB, (int32_t)p.grid.x, p.threads, p.HS, p.ntiles, p.Ls};
     for (int i = 0; i < 7; ++i) out[i] = v[i];
     return 0;
@@ -1659,17 +1739,25 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
     const bool want_resid = resid_out && iterations > 0;
     RowPlan rp{};
     ColPlan cpf{}, cpu{};
+    StripSet* ssf = nullptr;  // row strips of the FILTER column passes (choose_col)
+    int halves = 1;           // C_t = 4 without a cluster plan: two C_t = 2 halves
     if (!is_box) {
         if (plan_row_pass(g, Ct, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess && ctx->hs.n < 2) return DTS_E_SHAPE;
         cudaGetLastError();
-        if (!batch_strip_plan(ctx, Ct, &cpf)) {  // batched contexts: every image's tiles in one launch
-            if ((ctx->comm ? plan_col_pass(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)
-                           : plan_col(g, Ct, MODE_FILTER, ctx->num_sms, &cpf)) != cudaSuccess)
-                return DTS_E_SHAPE;
-            // the decoupled kernel (tall columns) applies Eq. (3) in its own write-out
-            if (cpf.kind != 1 && plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu) != cudaSuccess)
-                return DTS_E_SHAPE;
+        dts_status cs = choose_col(ctx, Ct, s, &cpf, &ssf);
+        if (cs != DTS_OK) return cs;
+        if (Ct == 4 && cpf.kind != 1 && !ctx->comm) {  // the cluster kernel has no C_t = 4 instance
+            ColPlan c2{};
+            StripSet* s2 = nullptr;
+            if (choose_col(ctx, 2, s, &c2, &s2) == DTS_OK && c2.kind == 1) {
+                cpf = c2;
+                ssf = s2;
+                halves = 2;
+            }
         }
+        // the decoupled kernel (tall columns) applies Eq. (3) in its own write-out
+        if (cpf.kind != 1 && plan_col_pass(g, Ct, MODE_UPDATE, ctx->num_sms, &cpu) != cudaSuccess)
+            return DTS_E_SHAPE;
         cudaGetLastError();
     }
     const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),
@@ -1812,7 +1900,9 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
                                                  upd_bytes, s, i);
                         }
                     } else if (!last || split_update) {
-                        st = col_filter_pass(ctx, cpf, Ct, i, ctx->X, row_bytes, s);
+                        for (int h = 0; h < halves && st == DTS_OK; ++h)
+                            st = col_filter_pass(ctx, cpf, ssf, Ct / halves, i, ctx->X + h * (Ct / halves) * g.plane,
+                                                 row_bytes / halves, s);
                         if (st != DTS_OK) return st;
                         if (!last || (rowupd && k + 1 < iterations)) continue;  // the next row pass applies Eq. (3)
                         st = run_launch(ctx, F_STEP, px * (16.0 * Ct + 4), s, [&] {
@@ -1877,13 +1967,11 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
     ColPlan cp{}, cp1{};
     if (plan_row_pass(g, 2, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess && ctx->hs.n < 2) return DTS_E_SHAPE;
     cudaGetLastError();
-    const bool two = batch_strip_plan(ctx, 2, &cp) || plan_col(g, 2, MODE_FILTER, ctx->num_sms, &cp) == cudaSuccess;
+    StripSet *ss2 = nullptr, *ss1 = nullptr;
+    const bool two = choose_col(ctx, 2, s, &cp, &ss2) == DTS_OK;
     // when two planes do not fit the cluster column kernel (tall images) but one does, the
     // column passes run plane by plane on it (over row strips where dts_solve uses them)
-    const bool per_plane = !(two && cp.kind == 1) &&
-                           (batch_strip_plan(ctx, 1, &cp1) ||
-                            plan_col(g, 1, MODE_FILTER, ctx->num_sms, &cp1) == cudaSuccess) &&
-                           cp1.kind == 1;
+    const bool per_plane = !(two && cp.kind == 1) && choose_col(ctx, 1, s, &cp1, &ss1) == DTS_OK && cp1.kind == 1;
     cudaGetLastError();
     if (!two && !per_plane) return DTS_E_SHAPE;
     const PtrKind kt = classify(target, ctx->device), kc = classify(conf_out, ctx->device),
@@ -1908,9 +1996,9 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
     st = run_launch(ctx, F_CONF, px * 12.0, s, [&] { return launch_conf_prologue(t_d, g, ctx->X, s); });
     for (int i = 0; i < ctx->N && st == DTS_OK; ++i) {
         st = row_pass_x(ctx, 2, MODE_FILTER, i, ctx->X, ctx->X, nullptr, 0, g.H, F_ROW, px * 20.0, s);
-        if (st == DTS_OK && !per_plane) st = col_filter_pass(ctx, cp, 2, i, ctx->X, px * 20.0, s);
+        if (st == DTS_OK && !per_plane) st = col_filter_pass(ctx, cp, ss2, 2, i, ctx->X, px * 20.0, s);
         for (int v = 0; v < 2 && st == DTS_OK && per_plane; ++v)
-            st = col_filter_pass(ctx, cp1, 1, i, ctx->X + v * g.plane, px * 12.0, s);
+            st = col_filter_pass(ctx, cp1, ss1, 1, i, ctx->X + v * g.plane, px * 12.0, s);
     }
     const float inv = 1.f / (2.f * sigma_c * sigma_c);
     if (st == DTS_OK)
@@ -1945,9 +2033,9 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
     ctx->last_stream = s;
     RowPlan rp;
     ColPlan cp{};
-    if ((plan_row_pass(g, 1, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess && ctx->hs.n < 2) ||
-        !(batch_strip_plan(ctx, 1, &cp) || plan_col(g, 1, MODE_FILTER, ctx->num_sms, &cp) == cudaSuccess))
-        return DTS_E_SHAPE;
+    StripSet* ss1 = nullptr;
+    if (plan_row_pass(g, 1, MODE_FILTER, ctx->num_sms, &rp) != cudaSuccess && ctx->hs.n < 2) return DTS_E_SHAPE;
+    if (choose_col(ctx, 1, s, &cp, &ss1) != DTS_OK) return DTS_E_SHAPE;
     cudaGetLastError();
     const PtrKind kt = classify(target, ctx->device), kc = classify(confidence, ctx->device),
                   ko = classify(out, ctx->device), kl = classify(left, ctx->device), kr = classify(right, ctx->device);
@@ -2005,7 +2093,7 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
                 for (int i = 0; i < ctx->N && st == DTS_OK; ++i) {
                     const float* in = (i == 0) ? ctx->Z : ctx->X;
                     st = row_pass_x(ctx, 1, MODE_FILTER, i, in, ctx->X, nullptr, 0, g.H, F_ROW, px * 12.0, s);
-                    if (st == DTS_OK) st = col_filter_pass(ctx, cp, 1, i, ctx->X, px * 12.0, s);
+                    if (st == DTS_OK) st = col_filter_pass(ctx, cp, ss1, 1, i, ctx->X, px * 12.0, s);
                 }
                 float* ohw = (k + 1 == iterations) ? o_d : nullptr;
                 if (st == DTS_OK)
@@ -2062,11 +2150,14 @@ void dts_destroy(dts_ctx* ctx) {
         if (q) cudaFreeAsync(q, s);
     for (float* q : ctx->edge_theta)
         if (q) cudaFreeAsync(q, s);
-    for (float* q : ctx->vs_gam)
-        if (q) cudaFreeAsync(q, s);
-    if (ctx->vs_edge) cudaFreeAsync(ctx->vs_edge, s);
-    for (float* q : ctx->vs_theta)
-        if (q) cudaFreeAsync(q, s);
+    for (StripSet* ss : ctx->ssets) {
+        for (float* q : ss->gam)
+            if (q) cudaFreeAsync(q, s);
+        for (float* q : ss->theta)
+            if (q) cudaFreeAsync(q, s);
+        if (ss->edge) cudaFreeAsync(ss->edge, s);
+        delete ss;
+    }
     for (float* q : ctx->hs_gam)
         if (q) cudaFreeAsync(q, s);
     for (float* q : ctx->hs_theta)

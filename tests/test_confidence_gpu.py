@@ -112,3 +112,8 @@ def test_confidence_per_plane_over_row_strips():
         with dts.Solver(torch.from_numpy(g).cuda(), 6.0, 0.2, 3) as s:
             assert dts.debug_strips(s.ctx)["strips"] == 2
         check(g, t, 6.0, 0.2, 3, 0.3)
+
+
+def test_confidence_taller_than_a_cluster():
+    g, t, _ = random_problem(11000, 40, 3, 1, seed=8)
+    check(g, t, 6.0, 0.2, 3, 0.3)

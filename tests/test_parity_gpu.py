@@ -466,3 +466,24 @@ def test_row_strips_with_separate_update_and_residual(opts):
     rng = target_range(t)
     assert np.max(np.abs(out.cpu().numpy() - ref)) <= TOL * rng
     np.testing.assert_allclose(r.cpu().numpy(), diag[:, 0], rtol=0, atol=TOL * rng)
+
+
+@pytest.mark.parametrize("H,W,Ct,strips", [(12000, 64, 1, True), (6000, 48, 3, True), (8000, 40, 2, True),
+                                            (5400, 36, 4, False), (300, 200, 4, False)])
+def test_columns_taller_than_a_cluster_run_over_strips(H, W, Ct, strips):
+    """Columns no cluster holds (C_t = 1 above 10240 rows, C_t = 2 above 7168, C_t = 3 above 5632)
+    run over row strips chosen at the first solve, with the seam fix-up, instead of the decoupled
+    kernel;
+    C_t = 4 (no cluster instance) runs as two C_t = 2 halves.  Parity with the oracle."""
+    g, t, c = random_problem(H, W, 3, Ct, seed=H + W + Ct)
+    args = (6.0, 0.2, 3, 0.99, 3)
+    gd, td, cd = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (g, t, c))
+    with dts.Solver(gd, 6.0, 0.2, 3) as s:
+        plan = dts.debug_col_plan(s.ctx, Ct if Ct < 4 else 2)
+        out = torch.empty_like(td)
+        s.solve(td, cd, 0.99, 3, out=out)
+    torch.cuda.synchronize()
+    assert plan["kind"] == 1
+    assert (plan["HS"] > 0) == strips
+    ref = oracle.solve(g, t, c, *args)
+    assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - ref)) <= TOL * target_range(t)
