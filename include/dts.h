@@ -66,12 +66,15 @@ typedef enum {
  *                  shared memory (11520 columns at C_t = 4); wider rows run over up to 16
  *                  vertical strips with a seam fix-up, which needs
  *                  every pass's carry-decay length L (measured at create) to fit twice in a
- *                  strip -- else DTS_E_SHAPE.  The column
- *                  kernels keep a column tile's bands co-resident, which bounds H per
- *                  context: on a 148-SM B200 at least 30000 rows for C_t = 1 and 6400 for
- *                  C_t = 3 (cluster kernel up to 10240 rows, decoupled kernel beyond).  A
- *                  larger H returns DTS_E_SHAPE (from dts_create, or from dts_solve for the
- *                  C_t of that call); split such images into row bands (dts_create_band).
+ *                  strip -- else DTS_E_SHAPE.  Columns taller than one thread-block
+ *                  cluster holds (10240 rows at C_t = 1, 7168 at 2, 5632 at 3) run over row
+ *                  strips with a seam fix-up (the first dts_solve that needs them measures
+ *                  the strips' seam lengths: one sync of its stream), else -- a seam length
+ *                  longer than half a strip, N > 4 -- over the decoupled kernel, which
+ *                  bounds H per context: on a 148-SM B200 at least 30000 rows for C_t = 1
+ *                  and 6400 for C_t = 3.  A larger H returns DTS_E_SHAPE (from dts_create,
+ *                  or from dts_solve for the C_t of that call); split such images into row
+ *                  bands (dts_create_band).
  *   sigma_s        spatial std-dev in pixels (sigma_x = sigma_y), > 0, finite.
  *   sigma_r        range std-dev in colour units, > 0, finite.
  *   filter_passes  N >= 1 recursive-filter passes per edge-aware mean (R5); N <= 16.
