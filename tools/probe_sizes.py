@@ -23,9 +23,11 @@ for sz in sizes:
     t = torch.rand(H, W, Ct, device="cuda", generator=gen) if Ct > 1 else torch.rand(H, W, device="cuda", generator=gen)
     c = torch.rand(H, W, device="cuda", generator=gen)
     o = torch.empty_like(t)
-    with dts.Solver(g, 16.0, 0.1, 3) as s:
+    NP = int(os.environ.get("NPASS", "3"))
+    SS = float(os.environ.get("SIGMA_S", "16"))
+    with dts.Solver(g, SS, 0.1, NP) as s:
         s.solve(t, c, 0.99, 20, out=o)
-    with dts.options(graphs=0, row_seg=int(os.environ.get("ROW_SEG", "0"))), dts.Solver(g, 16.0, 0.1, 3) as s:
+    with dts.options(graphs=0, row_seg=int(os.environ.get("ROW_SEG", "0"))), dts.Solver(g, SS, 0.1, NP) as s:
         s.solve(t, c, 0.99, 20, out=o)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
