@@ -1969,9 +1969,11 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
     cudaGetLastError();
     StripSet *ss2 = nullptr, *ss1 = nullptr;
     const bool two = choose_col(ctx, 2, s, &cp, &ss2) == DTS_OK;
-    // when two planes do not fit the cluster column kernel (tall images) but one does, the
-    // column passes run plane by plane on it (over row strips where dts_solve uses them)
-    const bool per_plane = !(two && cp.kind == 1) && choose_col(ctx, 1, s, &cp1, &ss1) == DTS_OK && cp1.kind == 1;
+    // when two planes do not fit the cluster column kernel (tall images) but one does, or one
+    // plane's plan covers >= 10% more SMs (C4: C_t = 1 strips on 135 SMs against C_t = 2 strips
+    // on 112: 2.9 against 3.3 ms per call), the column passes run plane by plane
+    const bool one = choose_col(ctx, 1, s, &cp1, &ss1) == DTS_OK && cp1.kind == 1;
+    const bool per_plane = one && (!(two && cp.kind == 1) || cp1.grid.x * 10 >= cp.grid.x * 11);
     cudaGetLastError();
     if (!two && !per_plane) return DTS_E_SHAPE;
     const PtrKind kt = classify(target, ctx->device), kc = classify(conf_out, ctx->device),
