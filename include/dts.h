@@ -304,6 +304,9 @@ dts_status dts_create_band(const float* guide_with_halo, int64_t H_total, int64_
  *   "band_overlap" row-band contexts, edge scheme: 1 (default) the all-gather of a column pass
  *                  runs on a context stream while the next row pass filters the band's
  *                  interior rows; 0 serial (same results, bit for bit)
+ *   "col_split"    C_t >= 2 column passes: 0 (default) plane by plane when the columns need
+ *                  row strips, 1 always plane by plane, 2 never
+ *   "row_seg"      row-kernel samples per thread: 0 auto (default), 4, 12, 20, 36
  *   "pdl"          programmatic dependent launch of the hot-path kernels: 1 (default) with the
  *                  dependent launch triggered at the end of each kernel, 2 at the start, 0 off
  *   "graphs"       1 replay repeated identical solves as CUDA graphs (default), 0 never
