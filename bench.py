@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the NEXT rows, the other configs and the sweeps")
     ap.add_argument("--bands", action="store_true",
                     help="row-band mode even on one rank (exercises the NCCL transport at N=1)")
+    ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
+                    help="library option (dts_set_option) for experiments; recorded in config.options")
     return ap.parse_args()
 
 
@@ -484,6 +486,11 @@ def main():
     import torch
     import paper_1805_04590_b200 as dts
 
+    opts = {}
+    for o in args.option:
+        k, v = o.split("=")
+        dts.dts_set_option(k, int(v))
+        opts[k] = int(v)
     rank, world, local = dist_env()
     if world != args.gpus:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)", file=sys.stderr)
@@ -673,7 +680,8 @@ def main():
                        "parallelism": (f"image split x{world}" if cfg.batch > 1 else
                                        (f"row bands x{world} (NCCL all-gather of column-pass edge records)"
                                         if band is not None else "single GPU")),
-                       "profiler": "off in the timed region; kernels / roofline from a second, profiled pass"},
+                       "profiler": "off in the timed region; kernels / roofline from a second, profiled pass",
+                       **({"options": opts} if opts else {})},
             "roofline": roofline,
             "kernels": table,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(round(launches_per_step * args.steps)),
