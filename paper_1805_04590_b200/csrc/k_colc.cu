@@ -22,6 +22,7 @@
 #include "dts_device.cuh"
 #include "dts_launch.h"
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -1251,12 +1252,16 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     // early lands its clusters on the SMs the previous kernel frees first, several to an SM,
     // and keeps that imbalance for the whole persistent launch (7071 x 10000, 4 row strips of
     // 405 CTAs: 27 ms per solve with PDL, 22.5 without)
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (nsm < 1) nsm = 1;
+    static std::atomic<int> nsm_dev[64];  // SM count per device (0: not queried yet)
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64) {
+        nsm = nsm_dev[dev].load(std::memory_order_relaxed);
+        if (nsm < 1) {
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            if (nsm < 1) nsm = 1;
+            nsm_dev[dev].store(nsm, std::memory_order_relaxed);
+        }
     }
     cfg.numAttrs = (option_pdl() && plan.grid.x <= (unsigned)nsm) ? 2 : 1;
     void* args[] = {&tx, &td, &p};
