@@ -317,13 +317,8 @@ dts_status dts_create_band(const float* guide_with_halo, int64_t H_total, int64_
  *   "col_strips"   tall single images: row strips for the C_t = 1 column passes, 0 off,
  *                  1 auto (default), n >= 2 exactly n strips when they fit
  *   "strip_cluster" 0 auto (default), 1..16: forced cluster size of a row-strip plan
- *   "col_halo"     row strips: 0 seam strips + the seam fix-up kernel (default), 1 halo strips
- *                  (each strip's window reaches the measured carry-decay length into its
- *                  neighbours; out of place, no fix-up)
- *   "batch_strips" batched contexts with col_halo = 1: halo strips per image, 0 whole images,
- *                  1 auto (default), n >= 2 forced
- *   "col_oop"      column passes out of place into a second state buffer: 0 only halo strips,
- *                  1 also seam strips (default), 2 every cluster-kernel pass
+ *   "col_oop"      column passes out of place into a second state buffer: 0 never, 1 the
+ *                  passes over row strips (default), 2 every cluster-kernel pass
  *   "row_two_ctas" C_t = 3 row passes of <= 3840 columns: 1 two CTAs per SM (default), 0 one
  * Returns DTS_E_ARG for an unknown name or value.  dts_get_option returns -1 for unknown names. */
 dts_status dts_set_option(const char* name, int32_t value);

@@ -87,12 +87,8 @@ struct Options {
                                        // end; default), 2 on with the trigger at kernel start  // row bands, edge scheme: all-gather overlapped with the next row pass
     std::atomic<int> col_strips{1};   // tall single-context images: C_t = 1 column passes over row strips
                                       // (0 off, 1 auto, n >= 2: exactly n strips when they fit)
-    std::atomic<int> col_halo{0};     // row strips: 1 halo strips (overlapping windows, no fix-up),
-                                      // 0 seam strips + the seam fix-up kernel
-    std::atomic<int> batch_strips{1}; // batched contexts: halo strips per image (1 auto, n >= 2 forced,
-                                      // 0: whole images)
-    std::atomic<int> col_oop{1};      // column passes out of place (col_oop): 0 only halo strips, 1 + seam
-                                      // strips, 2 every cluster-kernel pass
+    std::atomic<int> col_oop{1};      // column passes out of place (col_oop): 0 never, 1 row-strip passes,
+                                      // 2 every cluster-kernel pass
 };
 Options& opts_g() {
     static Options o;
@@ -105,11 +101,9 @@ struct dts_comm {
     dts::Comm* c = nullptr;
 };
 struct dts_ctx;
-struct StripSet;
 extern "C" {  // defined inside the extern "C" section below
 static bool strip_plan_n(dts_ctx* ctx, int n, int Ct, ColPlan* out);
-static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out, StripSet** ss, cudaStream_t s);
-static bool halo_plan(dts_ctx* ctx, const StripSet* ss, int Ct, ColPlan* out, int force_cb = -1);
+static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out);
 }
 
 // row strips of one image (single GPU; plan_strips / choose_col): n strips of HS rows, per pass
@@ -120,12 +114,6 @@ struct StripSet {
     std::vector<int> L;
     std::vector<float*> gam, theta;
     float* edge = nullptr;
-    // halo strips (no seam fix-up): n strips in each of nimg images of Hi rows, every strip's
-    // window reaching Lt[i] rows above and Lb[i] rows below it in pass i (k_halo_length)
-    bool halo = false;
-    int nimg = 1;
-    int64_t Hi = 0;
-    std::vector<int> Lt, Lb;
 };
 
 struct dts_ctx {
@@ -157,11 +145,6 @@ struct dts_ctx {
     std::vector<int> hs_L;
     std::vector<float*> hs_gam, hs_theta;  // [seam][H][L] each
     ColPlan bs_plan[5]{};
-    StripSet* bs_set[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // halo strips of bs_plan (or null)
-    // columns too tall for a cluster, per C_t: the halo strip set and its plan (choose_col)
-    ColPlan tall_plan[5]{};
-    StripSet* tall_set[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    signed char tall_state[5] = {0, 0, 0, 0, 0};
     signed char bs_state[5] = {0, 0, 0, 0, 0};  // 0 not planned, 1 planned, -1 not available
     int num_sms = 148;
     Geometry g{};
@@ -182,7 +165,7 @@ struct dts_ctx {
     uint32_t* win = nullptr;
     std::vector<BoxPlan> bplan;
     float* X2 = nullptr;  // second state buffer (box passes are out of place)
-    float* Xh = nullptr;  // output of out-of-place column passes (col_oop, ensure_halo_buf), xh_cap planes
+    float* Xh = nullptr;  // output planes of out-of-place column passes (col_oop, ensure_xh), xh_cap planes
     int xh_cap = 0;
     // solver state (allocated for ct_cap target channels)
     int ct_cap = 0;
@@ -715,8 +698,6 @@ dts_status dts_set_option(const char* name, int32_t value) {
     else if (n == "col_cluster" && value >= 0 && value <= 16) o.col_cluster = value;
     else if (n == "col_strips" && value >= 0 && value <= 64) o.col_strips = value;
     else if (n == "strip_cluster" && value >= 0 && value <= 16) o.strip_cluster = value;
-    else if (n == "col_halo" && (value == 0 || value == 1)) o.col_halo = value;
-    else if (n == "batch_strips" && value >= 0 && value <= 64) o.batch_strips = value;
     else if (n == "col_oop" && value >= 0 && value <= 2) o.col_oop = value;
     else if (n == "band_overlap" && (value == 0 || value == 1)) o.band_overlap = value;
     else if (n == "row_two_ctas" && (value == 0 || value == 1)) o.row_two_ctas = value;
@@ -733,13 +714,9 @@ int32_t dts_debug_strips(const dts_ctx* ctx, int32_t* HS, int32_t* L3, int32_t* 
     if (!ctx) return -1;
     const StripSet* ss = ctx->vs_set;
     ColPlan p{};
-    if (ss && ss->halo) halo_plan(const_cast<dts_ctx*>(ctx), ss, 1, &p);
-    else if (ss) strip_plan_n(const_cast<dts_ctx*>(ctx), ss->n, 1, &p);
+    if (ss) strip_plan_n(const_cast<dts_ctx*>(ctx), ss->n, 1, &p);
     if (HS) *HS = ss ? ss->HS : 0;
-    // seam strips: the seam lengths; halo strips: Lt + Lb (rows read beyond each strip)
-    for (int i = 0; i < 3 && L3; ++i)
-        L3[i] = !ss ? 0 : ss->halo ? (i < (int)ss->Lt.size() ? ss->Lt[i] + ss->Lb[i] : 0)
-                                   : (i < (int)ss->L.size() ? ss->L[i] : 0);
+    for (int i = 0; i < 3 && L3; ++i) L3[i] = ss && i < (int)ss->L.size() ? ss->L[i] : 0;
     if (CB) *CB = ss ? p.CB : 0;
     if (grid) *grid = ss ? (int)p.grid.x : 0;
     return ss ? ss->n : 0;
@@ -757,8 +734,6 @@ int32_t dts_get_option(const char* name) {
     if (n == "col_cluster") return o.col_cluster;
     if (n == "col_strips") return o.col_strips;
     if (n == "strip_cluster") return o.strip_cluster;
-    if (n == "col_halo") return o.col_halo;
-    if (n == "batch_strips") return o.batch_strips;
     if (n == "col_oop") return o.col_oop;
     if (n == "band_overlap") return o.band_overlap;
     if (n == "row_two_ctas") return o.row_two_ctas;
@@ -1047,187 +1022,8 @@ static dts_status build_strip_set(dts_ctx* ctx, int n, cudaStream_t s, StripSet*
 
 static StripSet* find_strip_set(dts_ctx* ctx, int n) {
     for (StripSet* ss : ctx->ssets)
-        if (ss->n == n && !ss->halo) return ss;
+        if (ss->n == n) return ss;
     return nullptr;
-}
-
-// ---- halo strips (reading R26) ----
-// A strip's column pass runs over a window reaching Lt rows above and Lb rows below the strip
-// (clipped to its image), starting the recurrence afresh at the window's top (y = x) and
-// bottom (z = y); after Lt rows the causal value has forgotten that start to 2^-26 of the
-// input's range, and the same holds upwards for the anticausal one, so every stored row equals
-// the full-column pass to that accuracy.  Only the strip's own rows are written.  Against seam
-// strips this reads Lt + Lb extra rows per strip and pass, and needs no fix-up kernel.
-
-// the plan of a halo strip set for C_t: the windows (at most HS + max_i(Lt_i + Lb_i) rows)
-// planned side by side; force_cb: cluster size (-1: option strip_cluster)
-static bool halo_plan(dts_ctx* ctx, const StripSet* ss, int Ct, ColPlan* out, int force_cb) {
-    const Geometry& g = ctx->g;
-    int Lw = 0;
-    for (size_t i = 0; i < ss->Lt.size(); ++i) Lw = std::max(Lw, ss->Lt[i] + ss->Lb[i]);
-    const int64_t nt = (int64_t)ss->n * ss->nimg;
-    Geometry gs = g;
-    gs.H = std::min<int64_t>(ss->HS + Lw, ss->Hi);
-    gs.W = g.W * nt;
-    gs.pitch = (gs.W + 31) / 32 * 32;
-    gs.plane = gs.H * gs.pitch;
-    ColPlan ps{};
-    const int fcb = force_cb >= 0 ? force_cb : opts_g().strip_cluster.load();
-    const bool ok = gs.W <= ((int64_t)1 << 31) / 2 &&
-                    plan_col(gs, Ct, MODE_FILTER, ctx->num_sms, &ps, fcb) == cudaSuccess && ps.kind == 1 &&
-                    colc_strips_supported(Ct, ps.Ls);
-    cudaGetLastError();
-    if (!ok) return false;
-    ps.HS = ss->HS;
-    ps.ntc = (int)((g.W + 31) / 32);
-    ps.ntiles = ps.ntc * (int)nt;
-    ps.Hi = (int)ss->Hi;
-    ps.nsi = ss->n;
-    *out = ps;
-    return true;
-}
-
-// halo lengths of candidate strip counts ns[c] (strips per image; nimg images of Hi rows),
-// every pass, in one launch (syncs s once): (*out)[c] = {Lt_0..Lt_{N-1}, Lb_0..Lb_{N-1}}, empty
-// when a carry does not decay within the rows walked
-static dts_status measure_halos(dts_ctx* ctx, int64_t Hi, int nimg, const std::vector<int>& ns, cudaStream_t s,
-                                std::vector<std::vector<int>>* out) {
-    const Geometry& g = ctx->g;
-    const int N = ctx->N;
-    out->assign(ns.size(), std::vector<int>());
-    if (N < 1 || N > 4 || ns.empty()) return DTS_OK;
-    std::vector<int4> seams;
-    for (size_t c = 0; c < ns.size(); ++c) {
-        const int64_t HS = (Hi + ns[c] - 1) / ns[c];
-        for (int64_t b = 0; b < nimg; ++b)
-            for (int64_t q = 1; q < ns[c] && q * HS < Hi; ++q)
-                seams.push_back(make_int4((int)(b * Hi + q * HS), (int)(b * Hi), (int)(b * Hi + Hi), (int)c));
-    }
-    if (seams.empty()) return DTS_OK;
-    double worst = 1;
-    for (int i = 0; i < N; ++i) worst = std::max(worst, std::ceil(26.0 / (double)ctx->kc[i]) + 1);
-    const int Lcap = (int)std::min<double>(worst, (double)Hi);
-    const size_t nlen = ns.size() * N * 2;
-    int4* dseam = nullptr;
-    unsigned* dlen = nullptr;
-    cudaError_t e;
-    if ((e = cudaMallocAsync((void**)&dseam, seams.size() * sizeof(int4), s)) != cudaSuccess ||
-        (e = cudaMallocAsync((void**)&dlen, nlen * sizeof(unsigned), s)) != cudaSuccess ||
-        (e = cudaMemsetAsync(dlen, 0, nlen * sizeof(unsigned), s)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(dseam, seams.data(), seams.size() * sizeof(int4), cudaMemcpyHostToDevice, s)) !=
-            cudaSuccess)
-        return cuda_fail(e);
-    std::vector<unsigned> len(nlen, 0);
-    dts_status st = run_launch(ctx, F_COEF, (double)seams.size() * g.W * N * Lcap * 8.0, s, [&] {
-        return launch_halo_length(ctx->dy, dseam, (int)seams.size(), g, N, ctx->kc.data(), Lcap, dlen, s);
-    });
-    if (st == DTS_OK &&
-        ((e = cudaMemcpyAsync(len.data(), dlen, nlen * sizeof(unsigned), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
-         (e = cudaStreamSynchronize(s)) != cudaSuccess))
-        st = cuda_fail(e);
-    cudaFreeAsync(dseam, s);
-    cudaFreeAsync(dlen, s);
-    if (st != DTS_OK) return st;
-    for (size_t c = 0; c < ns.size(); ++c) {
-        std::vector<int> L(2 * N);
-        bool ok = true;
-        for (int i = 0; i < N; ++i) {
-            L[i] = (int)len[(c * N + i) * 2];
-            L[N + i] = (int)len[(c * N + i) * 2 + 1];
-            ok = ok && L[i] <= Lcap && L[N + i] <= Lcap;
-        }
-        if (ok) (*out)[c] = L;
-    }
-    return DTS_OK;
-}
-
-static StripSet* find_halo_set(dts_ctx* ctx, int n, int nimg) {
-    for (StripSet* ss : ctx->ssets)
-        if (ss->halo && ss->n == n && ss->nimg == nimg) return ss;
-    return nullptr;
-}
-
-// modelled time of a column plan (arbitrary units) for strip-count selection: the busiest SM's
-// rows (tile rounds x window rows per CTA x CTAs per SM) at the per-SM rate, or the whole
-// pass's bytes at the HBM rate, whichever is longer (DESIGN.md section 7 has the measurements
-// the constants come from)
-static double col_plan_cost(const dts_ctx* ctx, const ColPlan& p, int64_t win_rows, int64_t store_rows_total,
-                            int64_t read_rows_total, int Ct) {
-    const int clusters = std::max(1, (int)p.grid.x / p.CB);
-    const int64_t rounds = (p.ntiles + clusters - 1) / clusters;
-    const int cps = std::max(1, (int)((p.grid.x + ctx->num_sms - 1) / ctx->num_sms));
-    const double rows_cta = (double)std::min<int64_t>(p.HB, (win_rows + p.CB - 1) / p.CB);
-    const double bytes_px_r = 4.0 * (Ct + 1), bytes_px_w = 4.0 * Ct;
-    // per-SM rate measured at about 46 GB/s with one CTA per SM, ~20% more with two
-    const double sm_rate = 46e3 * (cps >= 2 ? 1.2 : 1.0);  // bytes per us
-    const double t_sm = (double)rounds * cps * rows_cta * 32.0 * (bytes_px_r + bytes_px_w) / sm_rate;
-    const double t_hbm = ((double)read_rows_total * bytes_px_r + (double)store_rows_total * bytes_px_w) *
-                         (double)p.ntc * 32.0 / 6.2e6;
-    return std::max(t_sm, t_hbm);
-}
-
-// Halo strips for C_t over nimg images of Hi rows: measure the candidates' halo lengths (one
-// launch + sync), plan each, and keep the cheapest by col_plan_cost against `base` (the plan
-// without strips, nullable).  forced >= 2: only that strip count.  *out: the set (built and
-// owned by the context) or null when no strips are better.
-static dts_status choose_halo(dts_ctx* ctx, int Ct, int nimg, int64_t Hi, const ColPlan* base, int forced,
-                              cudaStream_t s, StripSet** out, ColPlan* plan_out) {
-    *out = nullptr;
-    std::vector<int> ns;
-    for (int n : {2, 3, 4, 6, 8, 9, 12, 16, 17, 18, 24, 32})
-        if ((forced < 2 || n == forced) && (Hi + n - 1) / n >= 32 && !((n - 1) * ((Hi + n - 1) / n) >= Hi)) ns.push_back(n);
-    if (forced >= 2 && ns.empty() && (Hi + forced - 1) / forced >= 32 && (forced - 1) * ((Hi + forced - 1) / forced) < Hi)
-        ns.push_back(forced);
-    if (ns.empty()) return DTS_OK;
-    std::vector<std::vector<int>> L;
-    const dts_status st = measure_halos(ctx, Hi, nimg, ns, s, &L);
-    if (st != DTS_OK) return st;
-    const int N = ctx->N;
-    double best = -1;
-    if (base && forced < 2) {
-        ColPlan b = *base;
-        if (b.ntc == 0) b.ntc = b.ntiles;
-        best = col_plan_cost(ctx, b, Hi * nimg / std::max<int64_t>(1, b.ntiles / b.ntc), Hi * nimg, Hi * nimg, Ct);
-    }
-    int bi = -1;
-    ColPlan bp{};
-    for (size_t c = 0; c < ns.size(); ++c) {
-        if (L[c].empty()) continue;
-        StripSet tmp;
-        tmp.halo = true;
-        tmp.n = ns[c];
-        tmp.nimg = nimg;
-        tmp.Hi = Hi;
-        tmp.HS = (int)((Hi + ns[c] - 1) / ns[c]);
-        tmp.Lt.assign(L[c].begin(), L[c].begin() + N);
-        tmp.Lb.assign(L[c].begin() + N, L[c].end());
-        ColPlan p{};
-        if (!halo_plan(ctx, &tmp, Ct, &p)) continue;
-        // rows read per pass: every strip's window; pass 0 has the longest halos
-        const int64_t reads = (Hi + (int64_t)(ns[c] - 1) * (tmp.Lt[0] + tmp.Lb[0])) * nimg;
-        const double cost = col_plan_cost(ctx, p, tmp.HS + tmp.Lt[0] + tmp.Lb[0], Hi * nimg, reads, Ct);
-        if (best < 0 || cost < best * 0.99) {
-            best = cost;
-            bi = (int)c;
-            bp = p;
-        }
-    }
-    if (bi < 0) return DTS_OK;
-    StripSet* ss = find_halo_set(ctx, ns[bi], nimg);
-    if (!ss) {
-        ss = new StripSet();
-        ss->halo = true;
-        ss->n = ns[bi];
-        ss->nimg = nimg;
-        ss->Hi = Hi;
-        ss->HS = (int)((Hi + ns[bi] - 1) / ns[bi]);
-        ss->Lt.assign(L[bi].begin(), L[bi].begin() + N);
-        ss->Lb.assign(L[bi].begin() + N, L[bi].end());
-        ctx->ssets.push_back(ss);
-    }
-    *out = ss;
-    if (plan_out) *plan_out = bp;
-    return DTS_OK;
 }
 
 // create time, C_t = 1: strips for columns that fit a cluster but need big clusters (GPC
@@ -1248,12 +1044,6 @@ static dts_status plan_strips(dts_ctx* ctx, cudaStream_t s) {
     const int forced = opts_g().col_strips.load();
     const int rounds = base.ntiles * base.CB / (int)base.grid.x;
     if (forced < 2 && (base.CB < 8 || rounds < 4)) return DTS_OK;
-    if (opts_g().col_halo.load()) {
-        StripSet* ss = nullptr;
-        const dts_status st = choose_halo(ctx, 1, 1, g.H, &base, forced, s, &ss, nullptr);
-        if (st == DTS_OK && ss) ctx->vs_set = ss;
-        return st;
-    }
     int best_n = 0;
     for (int n : {2, 4, 8, 16, 32}) {
         if (forced >= 2 && n != forced) continue;
@@ -1650,8 +1440,7 @@ dts_status dts_create_batch(const float* guides, int64_t B, int64_t H, int64_t W
 
 // batched contexts: the FILTER column plan over the images as row strips (one launch holds every
 // image's column tiles; HS = image height; no seam fix-up, the links between images are cut)
-static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out, StripSet** ss, cudaStream_t s) {
-    *ss = nullptr;
+static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out) {
     if (ctx->batch < 2 || !ctx->A1y || Ct < 1 || Ct > 4 || opts_g().col_kernel.load() != 0) return false;
     if (ctx->bs_state[Ct] == 0) {
         Geometry gs = ctx->g;  // planned as the images side by side
@@ -1670,26 +1459,12 @@ static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out, StripSet** ss, 
             ps.HS = (int)ctx->batch_H;
             ps.ntc = (int)((ctx->g.W + 31) / 32);
             ps.ntiles = ps.ntc * (int)ctx->batch;
-            ps.Hi = (int)ctx->batch_H;
-            ps.nsi = 1;
             ctx->bs_plan[Ct] = ps;
-            // halo strips inside every image when the model prefers them (option batch_strips)
-            const int bsn = opts_g().batch_strips.load();
-            if (bsn != 0 && opts_g().col_halo.load() && Ct <= 3) {
-                StripSet* set = nullptr;
-                ColPlan hp{};
-                if (choose_halo(ctx, Ct, (int)ctx->batch, ctx->batch_H, &ps, bsn, s, &set, &hp) == DTS_OK && set) {
-                    ctx->bs_plan[Ct] = hp;
-                    ctx->bs_set[Ct] = set;
-                }
-                cudaGetLastError();
-            }
         }
         ctx->bs_state[Ct] = ok ? 1 : -1;
     }
     if (ctx->bs_state[Ct] != 1) return false;
     *out = ctx->bs_plan[Ct];
-    *ss = ctx->bs_set[Ct];
     return true;
 }
 
@@ -1700,11 +1475,10 @@ static bool batch_strip_plan(dts_ctx* ctx, int Ct, ColPlan* out, StripSet** ss, 
 // fix-up (null for none).
 static dts_status choose_col(dts_ctx* ctx, int Ct, cudaStream_t s, ColPlan* cp, StripSet** ss) {
     *ss = nullptr;
-    if (batch_strip_plan(ctx, Ct, cp, ss, s)) return DTS_OK;
+    if (batch_strip_plan(ctx, Ct, cp)) return DTS_OK;
     const bool strips_ok = !ctx->comm && ctx->batch == 1 && ctx->A1y && opts_g().col_strips.load() != 0 &&
                            opts_g().col_kernel.load() == 0;
-    if (Ct == 1 && ctx->vs_set && strips_ok &&
-        (ctx->vs_set->halo ? halo_plan(ctx, ctx->vs_set, 1, cp) : strip_plan_n(ctx, ctx->vs_set->n, 1, cp))) {
+    if (Ct == 1 && ctx->vs_set && strips_ok && strip_plan_n(ctx, ctx->vs_set->n, 1, cp)) {
         *ss = ctx->vs_set;
         return DTS_OK;
     }
@@ -1712,25 +1486,7 @@ static dts_status choose_col(dts_ctx* ctx, int Ct, cudaStream_t s, ColPlan* cp, 
                                     : plan_col(ctx->g, Ct, MODE_FILTER, ctx->num_sms, cp);
     cudaGetLastError();
     if (e == cudaSuccess && cp->kind == 1) return DTS_OK;
-    if (strips_ok && Ct <= 3 && opts_g().col_halo.load()) {
-        // halo strips, chosen per C_t at the first call that needs them (one stream sync)
-        if (ctx->tall_state[Ct] == 0) {
-            StripSet* set = nullptr;
-            ColPlan hp{};
-            const int forced = opts_g().col_strips.load();
-            const dts_status st = choose_halo(ctx, Ct, 1, ctx->g.H, nullptr, forced, s, &set, &hp);
-            if (st != DTS_OK) return st;
-            ctx->tall_state[Ct] = set ? 1 : -1;
-            ctx->tall_set[Ct] = set;
-            ctx->tall_plan[Ct] = hp;
-        }
-        if (ctx->tall_state[Ct] == 1) {
-            *cp = ctx->tall_plan[Ct];
-            *ss = ctx->tall_set[Ct];
-            return DTS_OK;
-        }
-    }
-    if (strips_ok && Ct <= 3 && !opts_g().col_halo.load()) {
+    if (strips_ok && Ct <= 3) {
         for (int n = 2; n <= 64; n *= 2) {
             ColPlan ps{};
             if (!strip_plan_n(ctx, n, Ct, &ps)) {
@@ -1752,23 +1508,22 @@ static dts_status choose_col(dts_ctx* ctx, int Ct, cudaStream_t s, ColPlan* cp, 
 }
 
 // Whether a FILTER column pass writes its output to the same planes of ctx->Xh instead of over
-// its input in ctx->X.  Halo strips read rows of their neighbours' strips, so their pass cannot
-// run in place; option col_oop 1 (default) also moves seam-strip passes out of place (the next
-// row pass then reads Xh and writes X: the fused row update runs 458 against 481 us on C4 when
-// its z-bar input and its output are different planes), 2 every cluster-kernel pass.
+// its input in ctx->X (option col_oop; the next row pass then reads Xh and writes X).  Default 1:
+// the passes over row strips, where the fused row update that follows the last one reads its
+// z-bar input and writes its output in different buffers (C4: 466-468 against 476-481 us);
+// 2: every cluster-kernel pass (no further gain on C4, C3 1.7% slower).
 static bool col_oop(const dts_ctx* ctx, const ColPlan& cp, const StripSet* ss) {
-    if (ss && ss->halo) return true;
     const int o = opts_g().col_oop.load();
     return (o >= 1 && ss) || (o == 2 && cp.kind == 1 && ctx->A1y && ctx->N <= 4);
 }
 
-// where a FILTER column pass on (cp, ss) leaves the planes it read from ctx->X (x must lie there)
+// where a FILTER column pass on (cp, ss) leaves the planes it read from ctx->X
 static inline float* col_out(dts_ctx* ctx, const ColPlan& cp, const StripSet* ss) {
     return col_oop(ctx, cp, ss) ? ctx->Xh : ctx->X;
 }
 
 // the output planes of out-of-place column passes (ctx->Xh, as many planes as ctx->X)
-static dts_status ensure_halo_buf(dts_ctx* ctx, const ColPlan& cp, const StripSet* ss, cudaStream_t s) {
+static dts_status ensure_xh(dts_ctx* ctx, const ColPlan& cp, const StripSet* ss, cudaStream_t s) {
     if (!col_oop(ctx, cp, ss) || (ctx->Xh && ctx->xh_cap >= ctx->ct_cap)) return DTS_OK;
     if (ctx->Xh) cudaFreeAsync(ctx->Xh, s);
     ctx->Xh = nullptr;
@@ -1779,8 +1534,8 @@ static dts_status ensure_halo_buf(dts_ctx* ctx, const ColPlan& cp, const StripSe
     return DTS_OK;
 }
 
-// FILTER column pass i over the C_t planes at x, on plan cp (choose_col): over halo strips, over
-// seam strips (ss) + the seam fix-up, the cluster kernel on A1 (image-high strips in batched
+// FILTER column pass i over the C_t planes at x (x lies in ctx->X), on plan cp (choose_col): over
+// row strips (ss) + the seam fix-up, the cluster kernel on A1 (image-high strips in batched
 // contexts: cp.HS > 0), else the decoupled kernel on d_y.  The output lands at
 // col_out(ctx, cp, ss) + (x - ctx->X).
 static dts_status col_filter_pass(dts_ctx* ctx, const ColPlan& cp, const StripSet* ss, int Ct, int i, float* x,
@@ -1788,18 +1543,15 @@ static dts_status col_filter_pass(dts_ctx* ctx, const ColPlan& cp, const StripSe
     const Geometry& g = ctx->g;
     float* xo = col_out(ctx, cp, ss) + (x - ctx->X);
     dts_status st = run_launch(ctx, F_COL, bytes, s, [&] {
-        if (ss && ss->halo)  // halo strips: overlapping windows, nothing to fix up
-            return launch_col_cluster(cp, g, Ct, MODE_FILTER, x, ctx->A1y, ctx->kc[i], nullptr, nullptr, s, i,
-                                      nullptr, nullptr, nullptr, nullptr, ss->Lt[i], ss->Lb[i], xo);
         if (ss)  // row strips; the seams are fixed by the launch that follows
             return launch_col_cluster(cp, g, Ct, MODE_FILTER, x, ctx->A1y, ctx->kc[i], nullptr, nullptr, s, i,
-                                      nullptr, nullptr, nullptr, ss->edge, 0, 0, xo);
+                                      nullptr, nullptr, nullptr, ss->edge, xo);
         if (cp.kind == 1 && ctx->A1y && i < 4)
             return launch_col_cluster(cp, g, Ct, MODE_FILTER, x, ctx->A1y, ctx->kc[i], nullptr, nullptr, s, i,
-                                      nullptr, nullptr, nullptr, nullptr, 0, 0, xo);
+                                      nullptr, nullptr, nullptr, nullptr, xo);
         return col_launch(ctx, cp, Ct, MODE_FILTER, x, ctx->dy, ctx->kc[i], nullptr, nullptr, s);
     });
-    if (st == DTS_OK && ss && !ss->halo)
+    if (st == DTS_OK && ss)
         st = run_launch(ctx, F_SEAM, (double)g.W * 12.0 * Ct * (ss->n - 1) * 2 * ss->L[i], s, [&] {
             return launch_seam_fix(xo, Ct, g, ss->HS, ss->n, ss->L[i], ss->gam[i], ss->theta[i], ss->edge, s);
         });
@@ -2049,7 +1801,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         // against 25.3), while columns one cluster holds stay joint (2160 x 3840 x 3: 8.0 against
         // 10.1 plane by plane).  Option col_split: 1 always plane by plane, 2 never.
         const int split = opts_g().col_split.load();
-        if (Ct >= 2 && !ctx->comm && split != 2 && (split == 1 || (ssf && ctx->batch == 1) || cpf.kind != 1)) {
+        if (Ct >= 2 && !ctx->comm && split != 2 && (split == 1 || ssf || cpf.kind != 1)) {
             ColPlan c1{};
             StripSet* s1 = nullptr;
             if (choose_col(ctx, 1, s, &c1, &s1) == DTS_OK && c1.kind == 1) {
@@ -2117,7 +1869,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
         if ((st = ensure_solver_state(ctx, Ct, s)) != DTS_OK) return st;
         if ((st = ensure_col_scratch(ctx, cpf, s)) != DTS_OK) return st;
         if ((st = ensure_col_scratch(ctx, cpu, s)) != DTS_OK) return st;
-        if ((st = ensure_halo_buf(ctx, cpf, ssf, s)) != DTS_OK) return st;
+        if ((st = ensure_xh(ctx, cpf, ssf, s)) != DTS_OK) return st;
         auto enqueue = [&](cudaStream_t s) -> dts_status {
             dts_status st;
             const double px = (double)g.H * g.W;
@@ -2301,7 +2053,7 @@ dts_status dts_confidence(dts_ctx* ctx, const float* target, float sigma_c, floa
     if (!per_plane && (st = ensure_col_scratch(ctx, cp, s)) != DTS_OK) return st;
     const double px = (double)g.H * g.W;
     // planes [t ; t^2] -> DTF (N passes of rows then columns) -> Eq. (7)
-    if ((st = (per_plane ? ensure_halo_buf(ctx, cp1, ss1, s) : ensure_halo_buf(ctx, cp, ss2, s))) != DTS_OK) return st;
+    if ((st = (per_plane ? ensure_xh(ctx, cp1, ss1, s) : ensure_xh(ctx, cp, ss2, s))) != DTS_OK) return st;
     st = run_launch(ctx, F_CONF, px * 12.0, s, [&] { return launch_conf_prologue(t_d, g, ctx->X, s); });
     float* xc = ctx->X;  // the planes the last column pass wrote (col_out)
     for (int i = 0; i < ctx->N && st == DTS_OK; ++i) {
@@ -2395,7 +2147,7 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
     } else {
         if (st == DTS_OK) st = ensure_solver_state(ctx, 1, s);
         if (st == DTS_OK) st = ensure_col_scratch(ctx, cp, s);
-        if (st == DTS_OK) st = ensure_halo_buf(ctx, cp, ss1, s);
+        if (st == DTS_OK) st = ensure_xh(ctx, cp, ss1, s);
         const double px = (double)g.H * g.W;
         auto enqueue = [&](cudaStream_t s) -> dts_status {
             dts_status st = run_launch(ctx, F_PROLOGUE, px * (24.0 + (ctx->Sy ? 4.0 : 0.0)), s, [&] {

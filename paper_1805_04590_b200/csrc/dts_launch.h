@@ -83,7 +83,6 @@ struct ColPlan {
     int kind;  // 0: decoupled band-tuple kernel (k_col.cu), 1: cluster kernel (k_colc.cu)
     int TW, CB, HB, S, Ls, nb, ntiles, threads;
     int HS = 0, ntc = 0;  // cluster kernel over row strips: strip height, column tiles per strip (0: one strip)
-    int Hi = 0, nsi = 0;  // strips of stacked images: image height, strips per image (0: one image of H rows)
     dim3 grid;
     size_t smem;
     size_t tuple_floats, flag_count;  // scratch the launch needs (ColScratch)
@@ -126,8 +125,7 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
                                const float* ext = nullptr,    // APPLY: carries into the rank band [ntiles][2][Ct][32]
                                float* rank_tuples = nullptr,   // TUPLE: [ntiles][2Ct+3][32]
                                float* edge = nullptr,          // edge scheme: [ntiles][2Ct+1][32]
-                               float* sedge = nullptr,         // seam strips: [strip][2][Ct][ntc * 32]
-                               int halo_t = 0, int halo_b = 0,  // halo strips: rows above / below each strip
+                               float* sedge = nullptr,         // row strips: [strip][2][Ct][ntc * 32]
                                float* x_out = nullptr);  // FILTER output planes (null: in place over x)        // row strips: [strip][2][Ct][ntc*32] edge rows
 
 // Eq. (7) confidence: planar X0 = t, X1 = t^2 from a row-major H x W
@@ -211,10 +209,6 @@ cudaError_t launch_seam_fix(float* x, int Ct, const Geometry& g, int HS, int nst
                             const float* theta, const float* sedge, cudaStream_t s);
 // decay lengths of a band's edge carries (top -> len[0], bottom -> len[1], atomicMax; zero them
 // first); d has rows 0..H (row H: the link below the band)
-// halo strips: per pass i < N and seam-list candidate w the rows above (len[(wN + i)2]) and
-// below (+1) the listed seams {row, image top, image end, w} a carry needs to decay below 2^-26
-cudaError_t launch_halo_length(const float* d, const int4* seams, int nseams, const Geometry& g, int N,
-                               const float* kc, int Lcap, unsigned* len, cudaStream_t s);
 cudaError_t launch_edge_length(const float* d, const Geometry& g, int Lcap, float kc, unsigned* len, cudaStream_t s);
 // set cudaFuncAttributeMaxDynamicSharedMemorySize of `fn` on the current device to at least
 // `bytes` (tracked per device and function, thread-safe)

@@ -44,11 +44,6 @@ struct Params {
     int64_t plane, pitch;
     int H, W, HB, S, CB, ntiles;
     int HS, ntc;  // row strips (single-GPU FILTER): strip height, column tiles per strip (HS = H: one strip)
-    // strips of several images (batched contexts): image height Hi, nsi strips per image; strip
-    // j = (image j / nsi, strip j % nsi of it).  Halo strips (halo = 1): each strip's window reaches
-    // Lt rows above and Lb rows below it (clipped to its image), the window's top link is cut, and
-    // only the strip's own rows are stored (reading R26)
-    int Hi, nsi, Lt, Lb, halo;
     float kc;
     int nsq;  // < 0: d holds distances (a = 2^(-kc d)); >= 0: d holds A1, a = A1^(2^nsq)
     int pdl_early;  // trigger the dependent launch at the start (option pdl = 2) instead of the end
@@ -232,39 +227,12 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
     // issues its own segment's loads, so no warp carries the whole tile's issue)
     // tile -> (row strip, column tile): a strip of HS rows is filtered with zero carries at its
     // top and the link below it cut (the seam fix-up adds the carries)
-    // a tile's row window: first row wb, hw rows, the stored rows [y0, y1) of it (window-relative)
-    struct Win {
-        int wb, hw, y0, y1;
-        bool cut;  // halo strip whose window top is not its image's top: the link into it is cut
-    };
-    auto window = [&](int tile) {
-        Win w;
-        if constexpr (STRIPS) {
-            const int strip = tile / p.ntc;
-            const int img = strip / p.nsi, q = strip - img * p.nsi;
-            const int it = img * p.Hi, ib = min(it + p.Hi, p.H);
-            const int s0 = it + q * p.HS, s1 = min(s0 + p.HS, ib);
-            w.wb = max(it, s0 - p.Lt);
-            w.hw = min(ib, s1 + p.Lb) - w.wb;
-            w.y0 = s0 - w.wb;
-            w.y1 = s1 - w.wb;
-            w.cut = p.halo && w.wb > it;
-        } else {
-            w.wb = 0;
-            w.hw = p.H;
-            w.y0 = 0;
-            w.y1 = p.H;
-            w.cut = false;
-        }
-        return w;
-    };
     auto stage_seg = [&](int tile, int q) {
         const int col0 = (STRIPS ? tile % p.ntc : tile) * TW;
-        const Win w = window(tile);
-        const int sb = w.wb;
+        const int sb = STRIPS ? (tile / p.ntc) * p.HS : 0;
         const uint32_t box = (uint32_t)(LSV * TW * sizeof(float));
         const int rq = r0 + q * LSV;
-        const uint32_t bytes = rq < w.hw ? box * (1 + (HASX ? NV : 0)) : 0u;
+        const uint32_t bytes = rq < (STRIPS ? min(p.HS, p.H - sb) : p.H) ? box * (1 + (HASX ? NV : 0)) : 0u;
         mbar_arrive_expect_tx(&bars[q], bytes);
         if (bytes) {
             tma_load_2d(ld + q * LSV * TW, &tm_d, col0, sb + rq, &bars[q]);
@@ -280,9 +248,8 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
     int k = 0;
     for (int tile = cluster; tile < p.ntiles; tile += nclusters, ++k) {
         const int col0 = (STRIPS ? tile % p.ntc : tile) * TW;
-        const Win w = window(tile);
-        const int sb = w.wb;  // first row of this tile's window
-        const int Hs = w.hw;  // rows of the window
+        const int sb = STRIPS ? (tile / p.ntc) * p.HS : 0;  // first row of this tile's strip
+        const int Hs = STRIPS ? min(p.HS, p.H - sb) : p.H;  // rows of the strip
         const int col = col0 + c;
         const bool colok = col < p.W;
 
@@ -325,8 +292,6 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
                 }
             }
         }
-        // halo strip: the window's first row starts the recurrence (y = x), as at an image top
-        if (STRIPS && w.cut && r0 + lo == 0) a[0] = 0.f;
         // coefficient linking this segment's last row to the next row: from the
         // landing zone (next segment; it landed before the barrier below) or, for the
         // band's last segment, straight from global (first row of the next band)
@@ -481,14 +446,12 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
 
         // ---- 5. write-out straight from registers ----
         {
-            // stored rows of this segment: [j0, nrow) (halo rows of the window are not stored)
-            const int j0 = STRIPS ? max(0, w.y0 - (r0 + lo)) : 0;
-            const int nrow = min(LSV, (STRIPS ? w.y1 : Hs) - (r0 + lo));
-            if (colok && nrow > j0) {
+            const int nrow = min(LSV, Hs - (r0 + lo));
+            if (colok && nrow > 0) {
                 if constexpr (MODE == MODE_FILTER || MODE == MODE_SUPPORT) {
                     float* base = (MODE == MODE_FILTER ? p.x : p.support) + (int64_t)(sb + r0 + lo) * p.pitch + col;
                     const int64_t pitch = p.pitch;
-                    if (nrow == LSV && j0 == 0) {  // full segment: a running pointer, no per-row checks
+                    if (nrow == LSV) {  // full segment: a running pointer, no per-row checks
 #pragma unroll
                         for (int v = 0; v < NV; ++v) {
                             float* q = base + v * p.plane;
@@ -498,7 +461,7 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
                     } else {
 #pragma unroll
                         for (int j = 0; j < LSV; ++j)
-                            if (j >= j0 && j < nrow) {
+                            if (j < nrow) {
 #pragma unroll
                                 for (int v = 0; v < NV; ++v) base[v * p.plane + (int64_t)j * pitch] = xv[v][j];
                             }
@@ -1195,13 +1158,9 @@ cudaError_t plan_col_cluster(const Geometry& g, int Ct, int mode, int num_sms, C
 
 cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, int mode, float* x, const float* d,
                                float kc, const UpdateArgs* upd, float* support, cudaStream_t s, int nsq,
-                               const float* ext, float* rank_tuples, float* edge, float* sedge, int halo_t,
-                               int halo_b, float* x_out) {
+                               const float* ext, float* rank_tuples, float* edge, float* sedge, float* x_out) {
     colc::BandParams p = {};
     p.sedge = sedge;
-    p.Lt = halo_t;
-    p.Lb = halo_b;
-    p.halo = halo_t > 0 || halo_b > 0;
     p.nsq = nsq;
     p.ext = ext;
     p.rank_tuples = rank_tuples;
@@ -1220,8 +1179,6 @@ cudaError_t launch_col_cluster(const ColPlan& plan, const Geometry& g, int Ct, i
     p.ntiles = plan.ntiles;
     p.HS = plan.HS > 0 ? plan.HS : (int)g.H;
     p.ntc = plan.ntc > 0 ? plan.ntc : plan.ntiles;
-    p.Hi = plan.Hi > 0 ? plan.Hi : (int)g.H;
-    p.nsi = plan.nsi > 0 ? plan.nsi : plan.ntiles / p.ntc;
     p.kc = kc;
     // PDL trigger at the end of the kernel (option pdl = 2: at the start, for experiments; a
     // start trigger was never faster, and 20-30% slower on mid-size images)
@@ -1397,65 +1354,6 @@ __global__ void k_edge_length(const float* __restrict__ d, int64_t H, int64_t W,
 
 cudaError_t launch_edge_length(const float* d, const Geometry& g, int Lcap, float kc, unsigned* len, cudaStream_t s) {
     k_edge_length<<<(unsigned)((g.W + 127) / 128), 128, 0, s>>>(d, g.H, g.W, g.pitch, Lcap, kc, len);
-    return cudaGetLastError();
-}
-
-struct HaloKc {
-    float kc[4];
-};
-// Halo strips (reading R26): how many rows of the strip above a seam the
-// causal recurrence needs before the seam, and how many rows below it the anticausal one needs,
-// for a carry's influence to fall below 2^-26.  One thread per (column, seam, pass): the causal
-// influence of a wrong value at row s - m on row s is prod_{k = s-m+1..s} a_k, the anticausal
-// one of a wrong value at row s + m - 1 on row s - 1 is prod_{k = s..s+m-1} a_k; the first m
-// whose product is below 2^-26 is the halo (Lcap + 1: not reached within Lcap rows).  Seam q of
-// the list: row seam[q].x (its image spans rows [seam[q].y, seam[q].z)), lengths into
-// len[(seam[q].w * N + i) * 2 + {0: above, 1: below}], maximised over columns and seams (w: the
-// candidate strip count the seam belongs to).
-__global__ void k_halo_length(const float* __restrict__ d, const int4* __restrict__ seam, int64_t W, int64_t pitch,
-                              int N, int Lcap, HaloKc kc, unsigned* __restrict__ len) {
-    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (col >= W) return;
-    const int4 sq = seam[blockIdx.y];
-    const int i = blockIdx.z;
-    const int64_t sr = sq.x, it = sq.y, ib = sq.z;
-    const float thr = 1.0f / 67108864.0f;  // 2^-26
-    unsigned up = (unsigned)Lcap + 1, dn = (unsigned)Lcap + 1;
-    float P = 1.f;
-    for (int m = 0; m < Lcap; ++m) {
-        if (sr - m < it) {  // the image top (a = 0 there): nothing comes from above it
-            up = (unsigned)m;
-            break;
-        }
-        P *= coef_from_d(__ldg(d + (sr - m) * pitch + col), kc.kc[i]);
-        if (P < thr) {
-            up = (unsigned)m + 1;
-            break;
-        }
-    }
-    P = 1.f;
-    for (int m = 0; m < Lcap; ++m) {
-        if (sr + m >= ib) {  // the image ends: the recurrence restarts there, nothing to carry
-            dn = (unsigned)m;
-            break;
-        }
-        P *= coef_from_d(__ldg(d + (sr + m) * pitch + col), kc.kc[i]);
-        if (P < thr) {
-            dn = (unsigned)m + 1;
-            break;
-        }
-    }
-    atomicMax(&len[((int64_t)sq.w * N + i) * 2], up);
-    atomicMax(&len[((int64_t)sq.w * N + i) * 2 + 1], dn);
-}
-
-cudaError_t launch_halo_length(const float* d, const int4* seams, int nseams, const Geometry& g, int N,
-                               const float* kc, int Lcap, unsigned* len, cudaStream_t s) {
-    if (nseams < 1 || N < 1 || N > 4) return cudaErrorInvalidValue;
-    HaloKc k{};
-    for (int i = 0; i < N; ++i) k.kc[i] = kc[i];
-    dim3 grid((unsigned)((g.W + 127) / 128), (unsigned)nseams, (unsigned)N);
-    k_halo_length<<<grid, 128, 0, s>>>(d, seams, g.W, g.pitch, N, Lcap, k, len);
     return cudaGetLastError();
 }
 

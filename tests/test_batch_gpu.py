@@ -176,15 +176,3 @@ def test_batch_host_pointers_match_device():
         dts.dts_destroy(ctx)
     np.testing.assert_array_equal(out.astype(np.float64), dev)
 
-
-@pytest.mark.parametrize("Ct,n", [(1, 3), (3, 2)])
-def test_batch_halo_substrips_against_oracle(Ct, n):
-    """Batched contexts with every image cut into n halo strips (options col_halo = 1,
-    batch_strips = n): the windows are clipped to their image, so each image still equals the
-    oracle on that image alone."""
-    ps, g, t, c = problems(3, 900, 200, 3, Ct, seed=300 + Ct)
-    with dts.options(col_halo=1, batch_strips=n):
-        got = batch_solve(g, t, c, 5.0, 0.2, 3, 0.99, 3)
-    for b, (gb, tb, cb) in enumerate(ps):
-        ref = oracle.solve(gb, tb, cb, 5.0, 0.2, 3, 0.99, 3)
-        assert np.max(np.abs(got[b] - ref)) <= TOL * target_range(tb)
