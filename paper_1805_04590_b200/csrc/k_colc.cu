@@ -158,6 +158,72 @@ __device__ __forceinline__ void seg_scan2(float* seg, int S, int cA, int cB, flo
     }
 }
 
+// Grouped segment scan: GR lane groups per column, 32 / GR columns per warp, so GR warps cover
+// the 32 columns of a tile.  Lane = (column cl = lane % (32 / GR), group g = lane / (32 / GR));
+// group g owns m = ceil(S / GR) consecutive segments: it folds them serially (loads first, all
+// independent), the GR group totals of a column are scanned with log2(GR) shuffle steps, and
+// each group writes its segments' exclusive prefixes while re-folding them.  GR = 4 at NB = 3:
+// ~125 warp instructions for 8 columns against ~140 per column for the one-column-per-warp
+// shuffle scan (seg_scan).  REV scans from the last segment.  Same results as seg_scan up to the
+// association order of the compositions.
+template <int NB, bool REV, int GR>
+__device__ __forceinline__ void seg_scan_grp(float* seg, int S, int w, float* tot) {
+    constexpr int CW = 32 / GR;  // columns per warp
+    const int lane = threadIdx.x & 31;
+    const int cl = lane % CW, g = lane / CW;
+    const int cc = w * CW + cl;
+    const int m = (S + GR - 1) / GR;
+    const int lo = min(S, g * m), hi = min(S, lo + m);
+    constexpr int MMAX = (24 + GR - 1) / GR;  // S <= 24
+    // local fold (upstream first: ascending, or descending for REV)
+    Aff<NB> v = aff_identity<NB>();
+#pragma unroll
+    for (int q = 0; q < MMAX; ++q) {
+        const int sg = REV ? hi - 1 - q : lo + q;
+        if (q < hi - lo) {
+            Aff<NB> e;
+            e.P = seg[(0 * S + sg) * (TW + 1) + cc];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) e.B[k] = seg[((1 + k) * S + sg) * (TW + 1) + cc];
+            v = aff_compose(v, e);
+        }
+    }
+    // inclusive scan over the GR groups of a column (upstream groups: lower g, or higher for REV)
+#pragma unroll
+    for (int off = CW; off < 32; off <<= 1) {
+        Aff<NB> e;
+        e.P = REV ? __shfl_down_sync(FULL, v.P, off) : __shfl_up_sync(FULL, v.P, off);
+#pragma unroll
+        for (int k = 0; k < NB; ++k) e.B[k] = REV ? __shfl_down_sync(FULL, v.B[k], off) : __shfl_up_sync(FULL, v.B[k], off);
+        if (REV ? (lane + off < 32) : (lane >= off)) v = aff_compose(e, v);
+    }
+    if (g == (REV ? 0 : GR - 1)) {
+        tot[0 * TW + cc] = v.P;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) tot[(1 + k) * TW + cc] = v.B[k];
+    }
+    Aff<NB> run;
+    run.P = REV ? __shfl_down_sync(FULL, v.P, CW) : __shfl_up_sync(FULL, v.P, CW);
+#pragma unroll
+    for (int k = 0; k < NB; ++k) run.B[k] = REV ? __shfl_down_sync(FULL, v.B[k], CW) : __shfl_up_sync(FULL, v.B[k], CW);
+    if (g == (REV ? GR - 1 : 0)) run = aff_identity<NB>();
+    // exclusive prefixes of the group's segments
+#pragma unroll
+    for (int q = 0; q < MMAX; ++q) {
+        const int sg = REV ? hi - 1 - q : lo + q;
+        if (q < hi - lo) {
+            Aff<NB> e;
+            e.P = seg[(0 * S + sg) * (TW + 1) + cc];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) e.B[k] = seg[((1 + k) * S + sg) * (TW + 1) + cc];
+            seg[(0 * S + sg) * (TW + 1) + cc] = run.P;
+#pragma unroll
+            for (int k = 0; k < NB; ++k) seg[((1 + k) * S + sg) * (TW + 1) + cc] = run.B[k];
+            run = aff_compose(run, e);
+        }
+    }
+}
+
 template <int NV>
 constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
 
@@ -170,6 +236,12 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
     k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
     constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
     constexpr bool HASX = MODE != MODE_SUPPORT;
+    // grouped segment scans (seg_scan_grp) in the one-channel throughput instantiations (row
+    // strips, 40-row segments: many tile rounds per launch; C4 column pass 218-220 -> 214 us, the
+    // step 32.10 -> 31.72 ms); one-round (latency-bound) images keep the per-column shuffle scans
+    // (C1: 12.8 against 13.2 us), and so do the C_t = 3 instantiations, which are register-bound
+    // (batched C3 with grouped scans: 460 against 432 us, the 12-row kernel spilling 16 B)
+    constexpr bool GSCAN = NV == 1 && (STRIPS || LSV == 40);
     extern __shared__ __align__(128) float smem[];
     const int HB = p.HB, S = p.S, CB = p.CB;
     const Smem L = layout(NV, HB, S);
@@ -323,7 +395,9 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
             for (int v = 0; v < NV; ++v) segF[((1 + v) * S + s) * (TW + 1) + c] = m.B[v];
         }
         __syncthreads();
-        if (S <= 16) {  // two columns per warp (the 40-row instantiation has S = 16)
+        if (GSCAN && S <= 24) {  // grouped scans: 8 warps of 4 columns
+            for (int w8 = s; w8 < 8; w8 += S) seg_scan_grp<NV, false, 8>(segF, S, w8, totC);
+        } else if (S <= 16) {  // two columns per warp (the 40-row instantiation has S = 16)
             for (int cc = s; cc < TW / 2; cc += S) seg_scan2<NV, false>(segF, S, cc, cc + TW / 2, totC);
         } else {
             for (int cc = s; cc < TW; cc += S) seg_scan<NV, false>(segF, S, cc, totC);
@@ -394,7 +468,9 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
             for (int v = 0; v < NV; ++v) segR[((1 + v) * S + s) * (TW + 1) + c] = E[v];
         }
         __syncthreads();
-        if (S <= 16) {
+        if (GSCAN && S <= 24) {
+            for (int w8 = s; w8 < 8; w8 += S) seg_scan_grp<NV, true, 8>(segR, S, w8, totA);
+        } else if (S <= 16) {
             for (int cc = s; cc < TW / 2; cc += S) seg_scan2<NV, true>(segR, S, cc, cc + TW / 2, totA);
         } else {
             for (int cc = s; cc < TW; cc += S) seg_scan<NV, true>(segR, S, cc, totA);
