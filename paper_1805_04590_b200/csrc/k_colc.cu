@@ -232,7 +232,7 @@ constexpr int max_threads() { return NV == 1 ? 640 : (NV == 2 ? 448 : 352); }
 // STRIPS: the tiles cover row strips of p.HS rows (tile -> (strip, column tile)); a separate
 // instantiation so that the one-strip kernels keep their code
 template <int CT, int MODE, bool PRE, int LSV = LS, bool STRIPS = false>
-__global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()), 1)
+__global__ void __launch_bounds__(LSV == 12 ? 640 : LSV == 16 ? 640 : (LSV == 40 ? 512 : max_threads<(MODE == MODE_SUPPORT ? 1 : CT)>()), 1)
     k_col_cluster(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_d, const Params p) {
     constexpr int NV = (MODE == MODE_SUPPORT) ? 1 : CT;
     constexpr bool HASX = MODE != MODE_SUPPORT;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(LSV == 12 ? 768 : LSV == 16 ? 640 : (LSV == 40
     // step 32.10 -> 31.72 ms); one-round (latency-bound) images keep the per-column shuffle scans
     // (C1: 12.8 against 13.2 us), and so do the C_t = 3 instantiations, which are register-bound
     // (batched C3 with grouped scans: 460 against 432 us, the 12-row kernel spilling 16 B)
-    constexpr bool GSCAN = NV == 1 && (STRIPS || LSV == 40);
+    constexpr bool GSCAN = (NV == 1 && (STRIPS || LSV == 40)) || LSV == 12;
     extern __shared__ __align__(128) float smem[];
     const int HB = p.HB, S = p.S, CB = p.CB;
     const Smem L = layout(NV, HB, S);
