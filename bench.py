@@ -514,6 +514,8 @@ def main():
         per = cfg.batch // world
         images = list(range(rank * per, (rank + 1) * per))
         inputs = [make_inputs(cfg.name, image=i) for i in images]
+        if per > 1:  # one batched context for this rank's images (dts_create_batch)
+            inputs = [tuple(np.ascontiguousarray(np.stack([x[j] for x in inputs])) for j in range(3))]
     elif world > 1 or args.bands:
         r0, r1 = dts.band_rows(cfg.H, world, rank)
         a, b = dts.band_guide_rows(cfg.H, r0, r1)
@@ -528,7 +530,9 @@ def main():
         comm = dts.dts_comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
     else:
         inputs = [make_inputs(cfg.name)]
-    pixels_rank = sum(t.shape[0] * t.shape[1] for _, t, _ in inputs)
+    batched = cfg.batch > 1 and cfg.batch // world > 1
+    pixels_rank = (cfg.batch // world) * cfg.H * cfg.W if cfg.batch > 1 else sum(t.shape[0] * t.shape[1]
+                                                                                for _, t, _ in inputs)
 
     stream = torch.cuda.Stream(device=dev)
     timer = Timer(torch, stream, dev, world)
@@ -536,6 +540,8 @@ def main():
     outs = [torch.empty_like(t) for _, t, _ in dev_in]
 
     def make_ctx(g):
+        if batched:
+            return dts.dts_create_batch(g, cfg.sigma_s, cfg.sigma_r, cfg.N, stream=stream.cuda_stream)
         if band is not None:
             return dts.dts_create_band(g, cfg.H, band[0], band[1] - band[0], cfg.sigma_s, cfg.sigma_r, cfg.N,
                                        comm=comm, stream=stream.cuda_stream)
@@ -673,7 +679,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "pixels": cfg.pixels, "iterations": cfg.iters,
-                       "step": "dts_create + dts_solve + dts_destroy (guide derivative, support, prologue, "
+                       "step": ("dts_create_batch (one context for this rank's images) + dts_solve + dts_destroy"
+                                if batched else "dts_create + dts_solve + dts_destroy") +
+                               " (guide derivative, support, prologue, "
                                f"{cfg.iters} x (3 row + 3 column pass kernels), closing update)",
                        "l2": "inputs larger than L2 (6.4 GB guide, 0.4 GB per state plane): no flush needed"
                              if cfg.name == "C4" else "L2 not flushed between steps",
