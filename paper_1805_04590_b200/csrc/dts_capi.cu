@@ -1990,7 +1990,7 @@ dts_status dts_solve_ex(dts_ctx* ctx, const float* target, int32_t Ct, const flo
             std::memcpy(&lb, &lambda, 4);
             std::memcpy(&sb, &step, 4);
             key = {1, (uintptr_t)t_d, (uintptr_t)c_d, (uintptr_t)o_d, (uintptr_t)Ct, (uintptr_t)iterations, lb, sb,
-                   (uintptr_t)support_mode, (uintptr_t)ctx->X, (uintptr_t)ctx->Z, (uintptr_t)ctx->chat,
+                   (uintptr_t)support_mode, (uintptr_t)ctx->X, (uintptr_t)ctx->Xh, (uintptr_t)ctx->Z, (uintptr_t)ctx->chat,
                    (uintptr_t)resid};
         }
         if ((st = run_cached(ctx, use_graph, key, s, enqueue)) != DTS_OK) return st;
@@ -2179,7 +2179,8 @@ dts_status dts_solve_stereo(dts_ctx* ctx, const float* target, const float* conf
                 std::memcpy(&gb2, &gamma, 4);
                 std::memcpy(&eb, &eps, 4);
                 key = {2, (uintptr_t)t_d, (uintptr_t)c_d, (uintptr_t)o_d, (uintptr_t)l_d, (uintptr_t)r_d,
-                       (uintptr_t)iterations, lb, gb2, eb, (uintptr_t)ctx->X, (uintptr_t)ctx->Z, (uintptr_t)ctx->chat};
+                       (uintptr_t)iterations, lb, gb2, eb, (uintptr_t)ctx->X, (uintptr_t)ctx->Xh, (uintptr_t)ctx->Z,
+                       (uintptr_t)ctx->chat};
             }
             st = run_cached(ctx, use_graph, key, s, enqueue);
         }
