@@ -18,7 +18,8 @@ second, profiled pass gives the per-kernel table and the roofline of the dominan
 target and confidence and D2H of the output happen inside the timed region.
 --gpus N > 1 without torchrun re-launches this script under torch.distributed.run with N
 ranks (one per GPU): C4 is split into row bands (NCCL exchange of column-pass carries), C3 by
-image; rank 0 checks the gathered banded output against a single-context solve (untimed).
+image (each rank's images in one dts_create_batch context); rank 0 checks the gathered banded
+output against a single-context solve (untimed).
 --impl reference times the fp64 CPU oracle (oracle/) on a bounded row-band sample of the same
 workload; that and the cpu_baseline / parity legs are the only places this script executes
 oracle/.
