@@ -69,3 +69,21 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(dts.DTSError) as ei:
         dts.dts_create(g, 8.0, 0.2, 3)
     assert ei.value.status == 5  # DTS_E_CUDA: fails loudly, nothing computed on the CPU
+
+
+def test_every_documented_option_round_trips():
+    """Each option include/dts.h documents is accepted at its current (default) value, read back
+    by dts_get_option, and an out-of-range value is rejected with DTS_E_ARG (no GPU needed)."""
+    import re
+    hdr = open(os.path.join(ROOT, "include", "dts.h")).read()
+    block = hdr[hdr.index("test / experiment options"):hdr.index("dts_status dts_set_option")]
+    names = re.findall(r'^ \*   "([a-z_0-9]+)"', block, flags=re.M)
+    assert {"col_oop", "col_strips", "strip_cluster", "pdl", "graphs"} <= set(names)
+    lib = dts.load_library()
+    for n in names:
+        v = dts.dts_get_option(n)
+        assert v >= 0, n
+        dts.dts_set_option(n, v)
+        assert dts.dts_get_option(n) == v
+        assert lib.dts_set_option(n.encode(), 1000) != 0, n
+    assert dts.dts_get_option("no_such_option") == -1
