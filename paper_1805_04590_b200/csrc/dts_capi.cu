@@ -334,25 +334,21 @@ dts_status ensure_staging(dts_ctx* ctx, size_t bytes_per_image, cudaStream_t s) 
 // column-pass plan: cluster fast path when it fits, else the decoupled band-tuple kernel
 cudaError_t plan_col(const Geometry& g, int Ct, int mode, int num_sms, ColPlan* plan, int force_cb = -1) {
     if (opts_g().col_kernel.load() == 0) {
-        // C_t >= 2 FILTER: 16-row segments (20 warps per CTA) when the column fits a cluster
+        // C_t >= 2 FILTER: 12-row (C_t = 3) or 16-row segments (20 warps per CTA) when the column
+        // fits a cluster
         const int rows2 = opts_g().col_rows.load();
+        // C_t = 3: 12-row segments (up to 20 warps, grouped segment scans, 96 registers) wherever
+        // they plan: batched C3 0.373 against 0.445 ms (16-row), one 4K image 56.0 against 60.3
+        // us, one 1080p image 19.0 against 23.0 us
+        if (Ct == 3 && mode == MODE_FILTER && rows2 != 16 &&
+            plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 12, force_cb) == cudaSuccess)
+            return cudaSuccess;
+        cudaGetLastError();
         if (Ct >= 2 && mode == MODE_FILTER && rows2 != 12 &&
             plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 16, force_cb) == cudaSuccess) {
-            // C_t = 3 with many tile rounds per launch (throughput-bound): 12-row segments, 20
-            // warps on a C3 band of 240 rows instead of 15 (batched C3, 64 rounds: 0.432 ms
-            // against 0.445; one C3 image, 8 rounds: 63.7 us against 61.0, so not there)
-            const int rounds = (plan->ntiles + (int)(plan->grid.x / plan->CB) - 1) / (int)(plan->grid.x / plan->CB);
-            ColPlan p12{};
-            if (Ct == 3 && (rows2 == 12 || (rows2 == 0 && rounds >= 16)) &&
-                plan_col_cluster_ls(g, Ct, mode, num_sms, &p12, 12, force_cb) == cudaSuccess && p12.CB == plan->CB)
-                *plan = p12;
             cudaGetLastError();
             return cudaSuccess;
         }
-        cudaGetLastError();
-        if (Ct == 3 && mode == MODE_FILTER && rows2 == 12 &&
-            plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 12, force_cb) == cudaSuccess)
-            return cudaSuccess;
         cudaGetLastError();
         if (plan_col_cluster_ls(g, Ct, mode, num_sms, plan, 32, force_cb) == cudaSuccess) {
             // C_t = 1 FILTER with several tile rounds per launch (throughput-bound): 16 warps

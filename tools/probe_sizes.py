@@ -28,7 +28,8 @@ for sz in sizes:
     with dts.Solver(g, SS, 0.1, NP) as s:
         s.solve(t, c, 0.99, 20, out=o)
     with dts.options(graphs=0, row_seg=int(os.environ.get("ROW_SEG", "0")),
-                     col_split=int(os.environ.get("COL_SPLIT", "0"))), dts.Solver(g, SS, 0.1, NP) as s:
+                     col_split=int(os.environ.get("COL_SPLIT", "0")),
+                     col_rows=int(os.environ.get("COL_ROWS", "0"))), dts.Solver(g, SS, 0.1, NP) as s:
         s.solve(t, c, 0.99, 20, out=o)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
