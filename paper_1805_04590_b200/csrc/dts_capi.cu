@@ -167,6 +167,7 @@ struct dts_ctx {
     float* X2 = nullptr;  // second state buffer (box passes are out of place)
     float* Xh = nullptr;  // output planes of out-of-place column passes (col_oop, ensure_xh), xh_cap planes
     int xh_cap = 0;
+    bool xh_failed = false;  // Xh could not be allocated: the column passes run in place
     // solver state (allocated for ct_cap target channels)
     int ct_cap = 0;
     float* Z = nullptr;
@@ -1509,6 +1510,7 @@ static dts_status choose_col(dts_ctx* ctx, int Ct, cudaStream_t s, ColPlan* cp, 
 // z-bar input and writes its output in different buffers (C4: 466-468 against 476-481 us);
 // 2: every cluster-kernel pass (no further gain on C4, C3 1.7% slower).
 static bool col_oop(const dts_ctx* ctx, const ColPlan& cp, const StripSet* ss) {
+    if (ctx->xh_failed) return false;
     const int o = opts_g().col_oop.load();
     return (o >= 1 && ss) || (o == 2 && cp.kind == 1 && ctx->A1y && ctx->N <= 4);
 }
@@ -1523,9 +1525,13 @@ static dts_status ensure_xh(dts_ctx* ctx, const ColPlan& cp, const StripSet* ss,
     if (!col_oop(ctx, cp, ss) || (ctx->Xh && ctx->xh_cap >= ctx->ct_cap)) return DTS_OK;
     if (ctx->Xh) cudaFreeAsync(ctx->Xh, s);
     ctx->Xh = nullptr;
-    cudaError_t e;
-    if ((e = cudaMallocAsync((void**)&ctx->Xh, (size_t)ctx->g.plane * sizeof(float) * ctx->ct_cap, s)) != cudaSuccess)
-        return cuda_fail(e);
+    if (cudaMallocAsync((void**)&ctx->Xh, (size_t)ctx->g.plane * sizeof(float) * ctx->ct_cap, s) != cudaSuccess) {
+        // an optimisation only: without the memory the passes run in place (same results)
+        cudaGetLastError();
+        ctx->Xh = nullptr;
+        ctx->xh_failed = true;
+        return DTS_OK;
+    }
     ctx->xh_cap = ctx->ct_cap;
     return DTS_OK;
 }
